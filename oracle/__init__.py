@@ -1,0 +1,177 @@
+"""CPU oracle for the SMILE bi-level MoE layer -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and
+``--impl reference``) may import this package.  The product package
+``paper_2212_05191_b200`` never imports it; the two share no code.
+
+This module is argument marshalling around ``oracle/smile_oracle.c`` (plain C, fp64): it
+compiles the C file with gcc on first use and calls it through ctypes with numpy arrays.
+Every function of the arithmetic, and the passage of PAPER.md it follows, is documented
+in the C file.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "smile_oracle.c")
+_LIB = os.path.join(_HERE, "libsmile_oracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (-O2, no fast-math: IEEE semantics are part of the
+    contract, e.g. the strict '>' argmax and the fp64 softmax)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-fno-fast-math",
+                               "-ffp-contract=off", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("n", C.c_int32), ("m", C.c_int32), ("e", C.c_int32), ("flat", C.c_int32),
+                ("T", C.c_int64), ("cf", C.c_double), ("alpha", C.c_double), ("beta", C.c_double)]
+
+
+_P = C.c_void_p
+
+
+class _Route(C.Structure):
+    _fields_ = [(k, _P) for k in ("dest1", "dest2", "slot1", "keep1", "keep", "p", "q", "gate",
+                                   "counts1", "A1", "A2", "S1", "S2", "loss",
+                                   "jin", "slot2", "keep2", "counts2")]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        _lib.oracle_capacity.restype = C.c_int64
+        _lib.oracle_capacity.argtypes = [C.c_int64, C.c_int64, C.c_double]
+        _lib.oracle_sizes.argtypes = [C.POINTER(_Cfg)] + [C.POINTER(C.c_int64)] * 4
+        _lib.oracle_logits.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]
+        _lib.oracle_route.restype = C.c_int
+        _lib.oracle_route.argtypes = [C.POINTER(_Cfg), _P, C.POINTER(_Route)]
+        _lib.oracle_ffn_row.argtypes = [C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]
+        _lib.oracle_out_rows.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32, _P, C.POINTER(_Route),
+                                         _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]
+    return _lib
+
+
+@dataclass
+class Config:
+    """n groups x m ranks, e experts per rank, T tokens per rank (see smile_oracle.c)."""
+    n: int
+    m: int
+    e: int = 1
+    T: int = 8
+    cf: float = 2.0
+    flat: bool = False
+    alpha: float = 0.005
+    beta: float = 0.005
+
+    @property
+    def G(self) -> int:
+        return self.n * self.m
+
+    def _c(self) -> _Cfg:
+        return _Cfg(self.n, self.m, self.e, int(self.flat), self.T, self.cf, self.alpha, self.beta)
+
+    def sizes(self):
+        """(K1, K2, C1, C2) of the configuration."""
+        v = [C.c_int64() for _ in range(4)]
+        lib().oracle_sizes(C.byref(self._c()), *[C.byref(x) for x in v])
+        return tuple(int(x.value) for x in v)
+
+    @property
+    def logit_width(self) -> int:
+        K1, K2, _, _ = self.sizes()
+        return K1 if self.flat else K1 + K2
+
+
+def capacity(T: int, dests: int, cf: float) -> int:
+    return int(lib().oracle_capacity(T, dests, cf))
+
+
+def _ptr(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def logits(x: np.ndarray, W: np.ndarray) -> np.ndarray:
+    """Eq. (1) logits, fp32 of an fp64 accumulation.  x [rows, d], W [K, d]."""
+    x = np.ascontiguousarray(x, np.float32)
+    W = np.ascontiguousarray(W, np.float32)
+    out = np.empty((x.shape[0], W.shape[0]), np.float32)
+    lib().oracle_logits(x.shape[0], x.shape[1], W.shape[0], _ptr(x), _ptr(W), _ptr(out))
+    return out
+
+
+class Route:
+    """All outputs of oracle_route (numpy arrays, shapes as in smile_oracle.c)."""
+
+    def __init__(self, cfg: Config):
+        K1, K2, C1, C2 = cfg.sizes()
+        G, T, n = cfg.G, cfg.T, cfg.n
+        self.cfg, self.K1, self.K2, self.C1, self.C2 = cfg, K1, K2, C1, C2
+        z = lambda shape, dt: np.zeros(shape, dt)
+        self.dest1, self.dest2, self.slot1 = z((G, T), np.int32), z((G, T), np.int32), z((G, T), np.int32)
+        self.keep1, self.keep = z((G, T), np.uint8), z((G, T), np.uint8)
+        self.p, self.q, self.gate = z((G, T), np.float32), z((G, T), np.float32), z((G, T), np.float32)
+        self.counts1 = z((G, K1), np.int32)
+        self.A1, self.A2 = z((G, K1), np.int64), z((G, K2), np.int64)
+        self.S1, self.S2 = z((G, K1), np.float64), z((G, K2), np.float64)
+        self.loss = z((G,), np.float64)
+        nc = max(n * C1, 1)
+        self.jin, self.slot2 = z((G, nc), np.int32), z((G, nc), np.int32)
+        self.keep2 = z((G, nc), np.uint8)
+        self.counts2 = z((G, K2), np.int32)
+        self._s = _Route(*[self.__dict__[k].ctypes.data_as(C.c_void_p) for k, _ in _Route._fields_])
+
+
+def route(cfg: Config, lg: np.ndarray) -> Route:
+    """Run the bi-level (or flat) routing of every rank.  lg [G, T, logit_width] fp32."""
+    lg = np.ascontiguousarray(lg, np.float32)
+    assert lg.shape == (cfg.G, cfg.T, cfg.logit_width), lg.shape
+    r = Route(cfg)
+    rc = lib().oracle_route(C.byref(cfg._c()), _ptr(lg), C.byref(r._s))
+    if rc == 3:
+        raise ValueError("non-finite logits")
+    if rc != 0:
+        raise ValueError(f"invalid configuration ({rc})")
+    return r
+
+
+def ffn_row(x, W1, b1, W2, b2) -> np.ndarray:
+    """One expert, one token: W2^T GELU(W1^T x + b1) + b2 in fp64.  W1 [d, d_ff]."""
+    f = lambda a: np.ascontiguousarray(a, np.float32)
+    x, W1, b1, W2, b2 = map(f, (x, W1, b1, W2, b2))
+    y = np.empty(W1.shape[0], np.float64)
+    lib().oracle_ffn_row(W1.shape[0], W1.shape[1], _ptr(x), _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2), _ptr(y))
+    return y
+
+
+def out_rows(cfg: Config, r: Route, x: np.ndarray, W1=None, b1=None, W2=None, b2=None,
+             rows=None, identity: bool = False) -> np.ndarray:
+    """Eq. (3) layer output (fp64) for the global token rows g = rank*T + t.
+    x [G, T, d]; W1 [G*e, d, d_ff], b1 [G*e, d_ff], W2 [G*e, d_ff, d], b2 [G*e, d]."""
+    x = np.ascontiguousarray(x, np.float32)
+    d = x.shape[-1]
+    if identity:
+        W1 = b1 = W2 = b2 = np.zeros(1, np.float32)
+        d_ff = 0
+    else:
+        W1, b1, W2, b2 = (np.ascontiguousarray(a, np.float32) for a in (W1, b1, W2, b2))
+        d_ff = W1.shape[-1]
+    rows = np.arange(cfg.G * cfg.T, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
+    out = np.empty((rows.shape[0], d), np.float64)
+    lib().oracle_out_rows(C.byref(cfg._c()), d, d_ff, _ptr(x), C.byref(r._s), _ptr(W1), _ptr(b1),
+                          _ptr(W2), _ptr(b2), int(identity), rows.shape[0], _ptr(rows), _ptr(out))
+    return out

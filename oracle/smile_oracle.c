@@ -1,0 +1,292 @@
+/*
+ * smile_oracle.c -- CPU ORACLE for the SMILE bi-level MoE layer (arXiv 2212.05191).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load this library.  The product path
+ * (paper_2212_05191_b200/) never links, imports or executes anything under oracle/;
+ * the two share no code, headers or constants.
+ *
+ * Plain, slow, obviously-correct C99.  Every rank of the emulated cluster is simulated
+ * in one process, in the paper's order, with no threads, no blocking and no fusion.
+ * Floating point is fp64 unless the paper fixes otherwise; routing decisions are taken
+ * on the caller-supplied fp32 logits (reading R3).
+ *
+ * Citations: "P:Lx" = /root/reference/PAPER.md line x (not read at run time);
+ * "R<k>" = the reading of an ambiguous passage listed in DESIGN.md section "Readings".
+ *
+ *   Eq. (1)  P:L38-42    router logits r = W_r x, softmax probabilities            (R1)
+ *   Eq. (3)  P:L113-117  bi-level top-1 output h_out = p_i q_j E_ij(h_in)
+ *   Eq. (4)  P:L123-130  additive LB loss  a*n*sum f_i P_i + b*m*sum f_j Q_j
+ *   §3.2.1   P:L107      token routed first to a node (inter router), then to a GPU
+ *   §3.2.3   P:L148      inter / intra process groups, four sequential All2Alls
+ *   §4.2     P:L207      capacity factor 2.0; alpha=0.01 (Switch), alpha=beta=0.005
+ *   §4.1     P:L162      expert = FFN with GELU (dropout omitted, R21)
+ *
+ * Parity status per function:
+ *   oracle_capacity, oracle_logits, oracle_route, oracle_ffn_row, oracle_out_rows :
+ *   pinned by tests/test_oracle_*.py (closed forms, brute force, invariants and
+ *   independent library cross-checks).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* Layer configuration shared by every oracle entry point. */
+typedef struct {
+    int32_t n;        /* groups ("nodes") */
+    int32_t m;        /* ranks ("GPUs") per group */
+    int32_t e;        /* experts per rank (paper: 1; R19) */
+    int32_t flat;     /* 0 = SMILE bi-level, 1 = flat Switch baseline */
+    int64_t T;        /* tokens per rank */
+    double cf;        /* capacity factor */
+    double alpha;     /* inter LB coefficient (flat: the Switch alpha) */
+    double beta;      /* intra LB coefficient (ignored when flat) */
+} oracle_cfg;
+
+/* Outputs of oracle_route.  All arrays are caller-allocated; shapes in comments.
+ * G = n*m ranks, K1 = flat ? G*e : n, K2 = flat ? 1 : m*e, C1/C2 from oracle_sizes. */
+typedef struct {
+    /* per source rank r, token t: [G*T] */
+    int32_t *dest1;   /* i: first argmax over the level-1 logits (flat: expert E) */
+    int32_t *dest2;   /* j: first argmax over the level-2 logits (flat: 0) */
+    int32_t *slot1;   /* # earlier tokens of rank r with the same dest1 */
+    uint8_t *keep1;   /* slot1 < C1 */
+    uint8_t *keep;    /* kept at every level (keep1 && keep2 of its received slot) */
+    float   *p;       /* top-1 inter probability (fp32 of the fp64 value) */
+    float   *q;       /* top-1 intra probability (1 when flat) */
+    float   *gate;    /* fp32(p*q) */
+    /* per source rank: */
+    int32_t *counts1; /* [G*K1] kept tokens sent to each level-1 destination */
+    int64_t *A1;      /* [G*K1] argmax counts before capacity (f_i * T) */
+    int64_t *A2;      /* [G*K2] */
+    double  *S1;      /* [G*K1] sum over tokens of softmax_k (P_k * T) */
+    double  *S2;      /* [G*K2] */
+    double  *loss;    /* [G] Eq. (4) per rank */
+    /* per intermediate rank u, received slot (s, c): [G*n*C1] (bi-level only) */
+    int32_t *jin;     /* level-2 destination j carried with the token, -1 = empty slot */
+    int32_t *slot2;   /* running count per j in received order (s asc, then c asc) */
+    uint8_t *keep2;   /* slot2 < C2 */
+    int32_t *counts2; /* [G*K2] kept tokens per j at the intermediate */
+} oracle_route_out;
+
+/* R5: capacity = ceil(cf*T/dests) per (sending rank, destination); a level with a
+ * single destination has no capacity (R20), i.e. every token fits. */
+int64_t oracle_capacity(int64_t T, int64_t dests, double cf) {
+    if (T <= 0) return 0;
+    if (dests <= 1) return T;
+    return (int64_t)ceil(cf * (double)T / (double)dests);
+}
+
+/* Level sizes, derived from the configuration only. */
+void oracle_sizes(const oracle_cfg *c, int64_t *K1, int64_t *K2, int64_t *C1, int64_t *C2) {
+    int64_t G = (int64_t)c->n * c->m;
+    int64_t k1 = c->flat ? G * c->e : c->n;
+    int64_t k2 = c->flat ? 1 : (int64_t)c->m * c->e;
+    int64_t c1 = oracle_capacity(c->T, k1, c->cf);
+    /* R7: level-2 capacity is based on the original T; with one level-2 destination
+     * the level is an identity and holds everything a rank can receive (n*C1). */
+    int64_t c2 = k2 > 1 ? oracle_capacity(c->T, k2, c->cf) : (int64_t)c->n * c1;
+    if (c->flat) c2 = 0;
+    *K1 = k1; *K2 = k2; *C1 = c1; *C2 = c2;
+}
+
+/* Eq. (1): r = W x.  Logit[row][k] = fp32( sum_c x[row][c] * W[k][c] ) accumulated in fp64. */
+void oracle_logits(int64_t rows, int32_t d, int32_t K, const float *x, const float *W, float *out) {
+    for (int64_t r = 0; r < rows; ++r)
+        for (int32_t k = 0; k < K; ++k) {
+            double acc = 0.0;
+            for (int32_t c = 0; c < d; ++c) acc += (double)x[r * d + c] * (double)W[(int64_t)k * d + c];
+            out[r * K + k] = (float)acc;
+        }
+}
+
+/* R2: first index of the maximum, scanning ascending and replacing only on strict '>'
+ * (the plain IEEE compare, so -0.0 and +0.0 tie, R28). */
+static int32_t first_argmax(const float *v, int64_t K) {
+    int32_t best = 0;
+    for (int64_t k = 1; k < K; ++k)
+        if (v[k] > v[best]) best = (int32_t)k;
+    return best;
+}
+
+/* Eq. (1) (R1, R4): softmax of v with the maximum at index imax.  Writes every entry
+ * (fp64) to prob[] and returns the top-1 entry 1 / sum_k exp(v_k - v_imax). */
+static double softmax_top1(const float *v, int64_t K, int32_t imax, double *prob) {
+    double s = 0.0;
+    for (int64_t k = 0; k < K; ++k) s += exp((double)v[k] - (double)v[imax]);
+    for (int64_t k = 0; k < K; ++k) prob[k] = exp((double)v[k] - (double)v[imax]) / s;
+    return 1.0 / s;
+}
+
+/*
+ * Bi-level (and flat) routing with capacity, over all G ranks.
+ * logits: [G*T, K1+K2] fp32 (flat: [G*T, K1]); column k < K1 is the inter router W_p
+ * (flat: W_r), column K1+k the intra router W_q (shared across nodes R11).
+ * Returns 0 on success, 1 on invalid configuration, 3 on non-finite logits (R27).
+ */
+int oracle_route(const oracle_cfg *c, const float *logits, oracle_route_out *o) {
+    if (c->n < 1 || c->m < 1 || c->e < 1 || c->T < 0 || !(c->cf > 0.0)) return 1;
+    const int64_t G = (int64_t)c->n * c->m, T = c->T;
+    int64_t K1, K2, C1, C2;
+    oracle_sizes(c, &K1, &K2, &C1, &C2);
+    const int64_t KW = c->flat ? K1 : K1 + K2;        /* logits row width */
+
+    for (int64_t i = 0; i < G * T * KW; ++i)
+        if (!isfinite(logits[i])) return 3;
+
+    double *prob = (double *)malloc(sizeof(double) * (size_t)(K1 + K2));
+    int64_t *cnt1 = (int64_t *)calloc((size_t)K1, sizeof(int64_t));
+    memset(o->counts1, 0, sizeof(int32_t) * (size_t)(G * K1));
+    memset(o->A1, 0, sizeof(int64_t) * (size_t)(G * K1));
+    memset(o->A2, 0, sizeof(int64_t) * (size_t)(G * K2));
+    memset(o->S1, 0, sizeof(double) * (size_t)(G * K1));
+    memset(o->S2, 0, sizeof(double) * (size_t)(G * K2));
+
+    /* Step 1 (Eq. 3): the source gate, token by token in ascending order. */
+    for (int64_t r = 0; r < G; ++r) {
+        memset(cnt1, 0, sizeof(int64_t) * (size_t)K1);
+        for (int64_t t = 0; t < T; ++t) {
+            const int64_t g = r * T + t;
+            const float *L = logits + g * KW;
+            int32_t i = first_argmax(L, K1);
+            double p = softmax_top1(L, K1, i, prob);
+            for (int64_t k = 0; k < K1; ++k) o->S1[r * K1 + k] += prob[k];
+            int32_t j = 0;
+            double q = 1.0;
+            if (!c->flat) {
+                j = first_argmax(L + K1, K2);
+                q = softmax_top1(L + K1, K2, j, prob);
+                for (int64_t k = 0; k < K2; ++k) o->S2[r * K2 + k] += prob[k];
+            } else {
+                o->S2[r * K2 + 0] += 1.0;
+            }
+            o->A1[r * K1 + i] += 1;                 /* R13: f counts the argmax before capacity */
+            o->A2[r * K2 + j] += 1;
+            o->dest1[g] = i;
+            o->dest2[g] = j;
+            o->p[g] = (float)p;
+            o->q[g] = (float)q;
+            o->gate[g] = (float)((double)o->p[g] * (double)o->q[g]);   /* R24 */
+            o->slot1[g] = (int32_t)cnt1[i]++;        /* R8: earliest token index wins */
+            o->keep1[g] = (uint8_t)(o->slot1[g] < C1);
+            o->keep[g] = o->keep1[g];
+        }
+        for (int64_t k = 0; k < K1; ++k)
+            o->counts1[r * K1 + k] = (int32_t)(cnt1[k] < C1 ? cnt1[k] : C1);
+    }
+
+    /* Step 2: at each intermediate u = (i, l), walk the received
+     * slots in received order -- source node s ascending, then source slot c -- and
+     * apply the intra gate's capacity (R6, R8).  The first hop of (s, l) lands on
+     * (i, l) (R10). */
+    if (!c->flat) {
+        const int64_t n = c->n, m = c->m;
+        int64_t *cnt2 = (int64_t *)calloc((size_t)K2, sizeof(int64_t));
+        int64_t *src_of = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n * (C1 > 0 ? C1 : 1)));
+        for (int64_t u = 0; u < G; ++u) {
+            const int64_t i = u / m, l = u % m;
+            memset(cnt2, 0, sizeof(int64_t) * (size_t)K2);
+            /* inbox[u][s][slot1] = token (s*m+l, t) with dest1 == i and keep1 */
+            for (int64_t x = 0; x < n * C1; ++x) {
+                o->jin[u * n * C1 + x] = -1;
+                o->slot2[u * n * C1 + x] = -1;
+                o->keep2[u * n * C1 + x] = 0;
+                src_of[x] = -1;
+            }
+            for (int64_t s = 0; s < n; ++s) {
+                const int64_t r = s * m + l;
+                for (int64_t t = 0; t < T; ++t) {
+                    const int64_t g = r * T + t;
+                    if (o->dest1[g] == i && o->keep1[g]) {
+                        o->jin[u * n * C1 + s * C1 + o->slot1[g]] = o->dest2[g];
+                        src_of[s * C1 + o->slot1[g]] = g;
+                    }
+                }
+            }
+            for (int64_t s = 0; s < n; ++s)
+                for (int64_t cc = 0; cc < C1; ++cc) {
+                    const int64_t x = u * n * C1 + s * C1 + cc;
+                    const int32_t j = o->jin[x];
+                    if (j < 0) continue;
+                    o->slot2[x] = (int32_t)cnt2[j]++;
+                    o->keep2[x] = (uint8_t)(o->slot2[x] < C2);
+                    o->keep[src_of[s * C1 + cc]] = o->keep2[x];
+                }
+            for (int64_t k = 0; k < K2; ++k)
+                o->counts2[u * K2 + k] = (int32_t)(cnt2[k] < C2 ? cnt2[k] : C2);
+        }
+        free(cnt2);
+        free(src_of);
+    }
+
+    /* Step 4: Eq. (4) per rank, in fp64 (R14: rank-local batch for both terms;
+     * flat: the one-hop Switch loss alpha*N*sum f P). */
+    for (int64_t r = 0; r < G; ++r) {
+        double l1 = 0.0, l2 = 0.0;
+        if (T > 0) {
+            for (int64_t k = 0; k < K1; ++k)
+                l1 += ((double)o->A1[r * K1 + k] / (double)T) * (o->S1[r * K1 + k] / (double)T);
+            for (int64_t k = 0; k < K2; ++k)
+                l2 += ((double)o->A2[r * K2 + k] / (double)T) * (o->S2[r * K2 + k] / (double)T);
+        }
+        o->loss[r] = c->alpha * (double)K1 * l1 + (c->flat ? 0.0 : c->beta * (double)K2 * l2);
+    }
+    free(prob);
+    free(cnt1);
+    return 0;
+}
+
+/* GELU(z) = z * Phi(z) = 0.5 z (1 + erf(z / sqrt 2)), the exact form (R21). */
+static double gelu(double z) { return 0.5 * z * (1.0 + erf(z / sqrt(2.0))); }
+
+/* Expert E(x) = W2^T GELU(W1^T x + b1) + b2, fp64.
+ * W1 [d, d_ff], b1 [d_ff], W2 [d_ff, d], b2 [d] of ONE expert. */
+void oracle_ffn_row(int32_t d, int32_t d_ff, const float *x, const float *W1, const float *b1,
+                    const float *W2, const float *b2, double *y) {
+    double *h = (double *)malloc(sizeof(double) * (size_t)d_ff);
+    for (int32_t f = 0; f < d_ff; ++f) {
+        double a = (double)b1[f];
+        for (int32_t k = 0; k < d; ++k) a += (double)x[k] * (double)W1[(int64_t)k * d_ff + f];
+        h[f] = gelu(a);
+    }
+    for (int32_t cc = 0; cc < d; ++cc) {
+        double a = (double)b2[cc];
+        for (int32_t f = 0; f < d_ff; ++f) a += h[f] * (double)W2[(int64_t)f * d + cc];
+        y[cc] = a;
+    }
+    free(h);
+}
+
+/*
+ * Eq. (3): OUT[r][t] = p_i q_j E_ij(x) for tokens kept at every level, 0 otherwise
+ * (R9: dropped tokens contribute nothing; the residual is the caller's).  Evaluated for
+ * the listed global token rows (g = r*T + t) only, so full-size layers can be sampled.
+ * Expert of a bi-level token = global expert i*K2 + j (= rank (i, j/e), local j%e);
+ * of a flat token = E.  Weights are indexed by global expert: W1 [G*e, d, d_ff] ...
+ * identity != 0 replaces E by the identity map (the "identity expert" pin).
+ */
+void oracle_out_rows(const oracle_cfg *c, int32_t d, int32_t d_ff, const float *x,
+                     const oracle_route_out *o, const float *W1, const float *b1,
+                     const float *W2, const float *b2, int32_t identity,
+                     int64_t nrows, const int64_t *rows, double *out) {
+    int64_t K1, K2, C1, C2;
+    oracle_sizes(c, &K1, &K2, &C1, &C2);
+    for (int64_t a = 0; a < nrows; ++a) {
+        const int64_t g = rows[a];
+        double *y = out + a * d;
+        if (!o->keep[g]) {
+            for (int32_t cc = 0; cc < d; ++cc) y[cc] = 0.0;
+            continue;
+        }
+        const int64_t ex = c->flat ? o->dest1[g] : (int64_t)o->dest1[g] * K2 + o->dest2[g];
+        if (identity) {
+            for (int32_t cc = 0; cc < d; ++cc) y[cc] = (double)x[g * d + cc];
+        } else {
+            oracle_ffn_row(d, d_ff, x + g * d, W1 + ex * (int64_t)d * d_ff, b1 + ex * (int64_t)d_ff,
+                           W2 + ex * (int64_t)d_ff * d, b2 + ex * (int64_t)d, y);
+        }
+        const double gt = (double)o->gate[g];
+        for (int32_t cc = 0; cc < d; ++cc) y[cc] *= gt;
+    }
+}
