@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""Benchmark of the SMILE bi-level MoE layer (and the flat Switch layer beside it).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--mode both|bilevel|flat]
+                    [--config c2|c1|c4|c5] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): one MoE layer forward, G = 8 ranks as a 2x4
+hierarchy (n = 2 groups x m = 4 ranks), 1 expert per rank, T = 16384 tokens per rank,
+d = 768, d_ff = 3072, bf16, capacity factor 2.0, fused router (a1) on synthetic
+N(0,1) tokens with random-init weights.  The job always runs the 8-rank problem:
+N processes each drive V = 8/N ranks (N = 1 emulates all 8 ranks on one B200, the
+exchanges becoming device copies; N = 8 is one rank per GPU with NCCL all-to-alls on
+the split inter/intra communicators), so total work is fixed: "scaling": "strong".
+
+A step = one pass of the whole hot path over one batch.  value =
+G*T / (max over ranks of the device time of the step), inputs resident in HBM; L2 is
+flushed (a 256 MiB write) before every timed step, outside its events.  e2e = the same
+metric through smile_forward_host with pinned host buffers (H2D of x and D2H of the
+output and loss inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # tag: n, m, e, T (per rank), d, d_ff, cf, dtype
+    "c1": dict(n=2, m=4, e=1, T=1024, d=64, d_ff=256, cf=1.0, dtype="fp32"),
+    "c2": dict(n=2, m=4, e=1, T=16384, d=768, d_ff=3072, cf=2.0, dtype="bf16"),
+    "c4": dict(n=2, m=4, e=8, T=65536, d=1024, d_ff=4096, cf=2.0, dtype="bf16"),
+    "c5": dict(n=2, m=4, e=16, T=8192, d=1600, d_ff=6400, cf=2.0, dtype="bf16"),
+}
+METRIC = "MoE-layer tokens/sec (bi-level vs flat All2All) at 1/2/4/8 B200; kernel HBM GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="both", choices=["both", "bilevel", "flat"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--ffn", default="auto", choices=["auto", "simt", "tcgen05"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay each step as a CUDA graph")
+    return ap.parse_args()
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi samples of SM clock and throttle reasons during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- reference arm
+def cpu_oracle_sample(cfgd, mode, seconds_budget=12.0, ffn_rows=64, ranks=None):
+    """Time the CPU oracle (as it stands, single thread) on a bounded sample of the
+    workload: routing of all tokens of `ranks` ranks plus the expert FFN of `ffn_rows`
+    kept tokens, extrapolated to tokens/s of the whole layer."""
+    import numpy as np
+    import oracle
+    import synth
+    n, m, e, T, d, d_ff, cf = (cfgd[k] for k in ("n", "m", "e", "T", "d", "d_ff", "cf"))
+    flat = mode == "flat"
+    G = n * m
+    cfg = oracle.Config(n, m, e, T, cf, flat=flat, alpha=0.01 if flat else 0.005)
+    KW = cfg.logit_width
+    x = synth.tokens(G, T, d, seed=0, dtype=cfgd["dtype"])
+    W = synth.router_weights(KW, d, seed=0)
+    W1, b1, W2, b2 = synth.expert_weights(G * e, d, d_ff, seed=0, dtype=cfgd["dtype"], bias=False)
+    t0 = time.perf_counter()
+    lg = oracle.logits(x.reshape(-1, d), W).reshape(G, T, KW)
+    r = oracle.route(cfg, lg)
+    t_route = time.perf_counter() - t0
+    kept = np.flatnonzero(r.keep.reshape(-1))
+    rows = kept[:: max(1, kept.size // ffn_rows)][:ffn_rows]
+    t1 = time.perf_counter()
+    oracle.out_rows(cfg, r, x, W1, b1, W2, b2, rows=rows)
+    t_ffn = time.perf_counter() - t1
+    t_total = t_route + t_ffn * kept.size / max(1, rows.size)
+    return {"value": G * T / t_total, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+            "sample": f"router logits + routing of all {G}x{T} tokens ({t_route:.2f} s) + expert FFN of "
+                      f"{rows.size} of {kept.size} kept tokens ({t_ffn:.2f} s), FFN extrapolated linearly"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    import oracle
+    import synth
+    cfgd = CONFIGS[args.config]
+    n, m, e, T, d, d_ff, cf = (cfgd[k] for k in ("n", "m", "e", "T", "d", "d_ff", "cf"))
+    G = n * m
+    cfg = oracle.Config(n, m, e, T, cf, alpha=0.005)
+    KW = cfg.logit_width
+    x = synth.tokens(G, T, d, seed=0, dtype=cfgd["dtype"])
+    W = synth.router_weights(KW, d, seed=0)
+    W1, b1, W2, b2 = synth.expert_weights(G * e, d, d_ff, seed=0, dtype=cfgd["dtype"], bias=False)
+    # one step = the oracle on a bounded sample: all ranks' logits + routing of rank 0's
+    # batch is not separable (level 2 needs every source), so a step routes the whole
+    # layer once per `route_every` steps and evaluates FFN rows for the rest.
+    ffn_rows = 4
+    lg = oracle.logits(x.reshape(-1, d), W).reshape(G, T, KW)
+    times = []
+    rsel = None
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if it == 0 or it % 10 == 0:
+            r = oracle.route(cfg, lg)
+            kept = np.flatnonzero(r.keep.reshape(-1))
+            t_route = time.perf_counter() - t0
+        rsel = kept[(it * 997) % kept.size: (it * 997) % kept.size + ffn_rows]
+        t1 = time.perf_counter()
+        oracle.out_rows(cfg, r, x, W1, b1, W2, b2, rows=rsel)
+        t_ffn = time.perf_counter() - t1
+        est = t_route + t_ffn * kept.size / max(1, rsel.size)
+        if it >= args.warmup:
+            times.append(est)
+    t = statistics.mean(times)
+    value = G * T / t
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.config}: one SMILE layer fwd, {G} ranks 2x4, T={T}/rank, d={d}, "
+                                   f"d_ff={d_ff}, cf={cf}", "l2": "n/a (CPU)"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                             "sample": f"per step: routing of all {G}x{T} tokens (re-run every 10 steps) + "
+                                       f"expert FFN of {ffn_rows} kept tokens, FFN extrapolated to all kept"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+PHASES_BI = ["gate1", "dispatch1", "a2a_inter", "gate2", "dispatch2", "a2a_intra", "ffn", "a2a_intra_rev",
+             "combine2", "a2a_inter_rev", "combine1", "aux"]
+PHASES_FLAT = ["gate1", "dispatch1", "a2a_world", "ffn", "a2a_world_rev", "combine1", "aux"]
+
+
+class Addr:
+    def __init__(self, a):
+        self.a = a
+
+    def data_ptr(self):
+        return self.a
+
+
+def make_layer(cfgd, mode, nprocs, proc, dev, ffn, nccl_id):
+    from paper_2212_05191_b200 import SmileLayer
+    L = SmileLayer(cfgd["n"], cfgd["m"], cfgd["e"], cfgd["d"], cfgd["d_ff"], cfgd["T"], cfgd["cf"], cfgd["dtype"],
+                   mode, nprocs=nprocs, proc=proc, device=dev, ffn_impl=ffn, nccl_id=nccl_id)
+    L.alloc_workspace()
+    return L
+
+
+def step(L, inp, ev=None):
+    """One forward through the C-ABI steps (the sequence of smile_forward), with an event
+    recorded after each phase when `ev` is given."""
+    import torch
+    w = L._view
+    A = lambda p: Addr(p)
+    rec = (lambda i: ev[i].record()) if ev is not None else (lambda i: None)
+    rec(0)
+    L.gate_inter(inp["x"], w.route, w.stats, A(w.counts1), w_router=inp["w_router"])
+    rec(1)
+    L.dispatch(1, inp["x"], A(w.send1), route=w.route, send_meta=A(w.meta1) if not L.flat else None)
+    rec(2)
+    if not L.flat:
+        L.all2all_inter(0, A(w.send1), A(w.recv1), A(w.meta1), A(w.rmeta1), A(w.counts1))
+        rec(3)
+        L.gate_intra(A(w.rmeta1), A(w.slot2), A(w.counts2))
+        rec(4)
+        L.dispatch(2, A(w.recv1), A(w.send2), recv_meta=A(w.rmeta1), slot2=A(w.slot2))
+        rec(5)
+        L.all2all_intra(0, A(w.send2), A(w.recv2), A(w.counts2), A(w.rcounts), A(w.counts2))
+        rec(6)
+        L.expert_ffn(A(w.recv2), A(w.rcounts), inp["W1t"], inp["b1"], inp["W2t"], inp["b2"], A(w.H), A(w.Y))
+        rec(7)
+        L.all2all_intra(1, A(w.Y), A(w.ret2), fwd_counts=A(w.counts2))
+        rec(8)
+        L.combine(2, A(w.ret2), A(w.ret1), recv_meta=A(w.rmeta1), slot2=A(w.slot2))
+        rec(9)
+        L.all2all_inter(1, A(w.ret1), A(w.back1), fwd_counts=A(w.counts1))
+        rec(10)
+        L.combine(1, A(w.back1), inp["out"], route=w.route)
+        rec(11)
+        L.aux_loss(w.stats, inp["loss"], 0.005, 0.005)
+        rec(12)
+    else:
+        L.all2all(0, 0, A(w.send1), A(w.recv1), A(w.counts1), A(w.rcounts), A(w.counts1))
+        rec(3)
+        L.expert_ffn(A(w.recv1), A(w.rcounts), inp["W1t"], inp["b1"], inp["W2t"], inp["b2"], A(w.H), A(w.Y))
+        rec(4)
+        L.all2all(0, 1, A(w.Y), A(w.back1), fwd_counts=A(w.counts1))
+        rec(5)
+        L.combine(1, A(w.back1), inp["out"], route=w.route)
+        rec(6)
+        L.aux_loss(w.stats, inp["loss"], 0.01, 0.0)
+        rec(7)
+
+
+def launches_per_step(L, nprocs):
+    """Kernels of libsmile launched per step (NCCL kernels not counted)."""
+    V1 = nprocs > 1 and L.V == 1
+    if not L.flat:
+        # gate+scan, dispatch1, [copy], rank2+scan2, dispatch2, [copy], ffn x2, [copy], combine2, [copy], combine1, aux
+        return 2 + 1 + 2 + 1 + 2 + 1 + 1 + 1 + (0 if V1 else 4)
+    return 2 + 1 + 2 + 1 + 1 + (0 if V1 else 2)
+
+
+def run_ours(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfgd = CONFIGS[args.config]
+    G = cfgd["n"] * cfgd["m"]
+    if G % world:
+        raise SystemExit(f"{world} processes do not divide {G} ranks")
+    from paper_2212_05191_b200 import smile as smb
+    nccl_id = None
+    if world > 1:
+        buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(smb.unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        nccl_id = bytes(buf.cpu().numpy().tobytes())
+
+    modes = ["bilevel", "flat"] if args.mode == "both" else [args.mode]
+    V = G // world
+    T, d, d_ff, e = cfgd["T"], cfgd["d"], cfgd["d_ff"], cfgd["e"]
+    tdt = torch.bfloat16 if cfgd["dtype"] == "bf16" else torch.float32
+    gen = torch.Generator(device=dev)
+    results = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for mode in modes:
+        # the two layers are measured one after the other; the second gets its own id
+        if mode != modes[0] and world > 1:
+            buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if rank == 0:
+                buf.copy_(torch.frombuffer(bytearray(smb.unique_id()), dtype=torch.uint8))
+            dist.broadcast(buf, 0)
+            nccl_id = bytes(buf.cpu().numpy().tobytes())
+        L = make_layer(cfgd, mode, world, rank, local, args.ffn, nccl_id)
+        KW = L.KW
+        gen.manual_seed(1000 + rank)
+        x = torch.randn(V, T, d, generator=gen, device=dev, dtype=torch.float32).to(tdt)
+        gen.manual_seed(7)                                     # tied router: same on every rank
+        bw = 1.0 / math.sqrt(d)
+        w_router = (torch.rand(KW, d, generator=gen, device=dev) * 2 - 1) * bw
+        gen.manual_seed(2000 + rank)
+        W1t = ((torch.rand(V * e, d_ff, d, generator=gen, device=dev) * 2 - 1) / math.sqrt(d)).to(tdt)
+        W2t = ((torch.rand(V * e, d, d_ff, generator=gen, device=dev) * 2 - 1) / math.sqrt(d_ff)).to(tdt)
+        b1 = torch.zeros(V * e, d_ff, device=dev)
+        b2 = torch.zeros(V * e, d, device=dev)
+        out = torch.empty_like(x)
+        loss = torch.empty(V, dtype=torch.float64, device=dev)
+        inp = dict(x=x, w_router=w_router, W1t=W1t, W2t=W2t, b1=b1, b2=b2, out=out, loss=loss)
+        phases = PHASES_BI if mode == "bilevel" else PHASES_FLAT
+        nph = len(phases)
+        for _ in range(args.warmup):
+            step(L, inp)
+        torch.cuda.synchronize()
+        err = L.get_error()
+        if err:
+            raise SystemExit(f"device error {err} in {mode}")
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nph + 1)] for _ in range(args.steps)]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk = ClockSampler(local) if rank == 0 else None
+        if clk:
+            clk.start()
+        for k in range(args.steps):
+            flush.zero_()                       # L2 flush outside the step's events
+            step(L, inp, evs[k])
+        torch.cuda.synchronize()
+        clocks = clk.stop() if clk else None
+        if dist:
+            dist.barrier()
+        ph = [[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(nph)] for k in range(args.steps)]
+        step_ms = [sum(p) for p in ph]
+        tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        ms = tot.item() / args.steps
+        phase_ms = {phases[i]: statistics.mean(p[i] for p in ph) for i in range(nph)}
+        # algorithmic work of the dominant kernel (expert FFN): 4 * rows * d * d_ff flops
+        w = L.view()
+        rows = int(w["rcounts"].sum().item())
+        kept = rows
+        ffn_ms = phase_ms["ffn"]
+        ffn_tc = cfgd["dtype"] == "bf16" and args.ffn != "simt" and smb.TCGEN05_DEFAULT
+        res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms, clocks=clocks,
+                   tokens=G * T, launches=launches_per_step(L, world))
+        # e2e through smile_forward_host (pinned host x, D2H out + loss)
+        if not args.no_e2e:
+            hx = x.cpu().pin_memory()
+            ho = torch.empty_like(hx).pin_memory()
+            hl = torch.empty(V, dtype=torch.float64).pin_memory()
+            xd = torch.empty_like(x)
+            for _ in range(2):
+                L.forward_host(xd, hx, W1t, b1, W2t, b2, out, loss, ho, hl, w_router=w_router)
+            if dist:
+                dist.barrier()
+            e2e_steps = max(3, min(args.steps, 20))
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for _ in range(e2e_steps):
+                L.forward_host(xd, hx, W1t, b1, W2t, b2, out, loss, ho, hl, w_router=w_router)
+            t1.record()
+            torch.cuda.synchronize()
+            et = torch.tensor([t0.elapsed_time(t1) / e2e_steps], dtype=torch.float64, device=dev)
+            if dist:
+                dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            res["e2e"] = {"value": G * T / (et.item() / 1e3), "unit": "tokens/s",
+                          "h2d_bytes_per_step": x.numel() * x.element_size(),
+                          "d2h_bytes_per_step": out.numel() * out.element_size() + loss.numel() * 8,
+                          "ms_per_step": et.item(), "steps": e2e_steps}
+        results[mode] = res
+        del evs
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    main = results[modes[0]]
+    ms = main["ms"]
+    flops = 4.0 * main["rows"] * d * d_ff
+    timed_s = ms * args.steps / 1e3
+    bf16_peak = peaks.get("bf16_tflops_sustained" if timed_s > 1.0 else "bf16_tflops")
+    ffn_is_tensor = main["ffn_tc"]
+    traffic = load_json(os.path.join(ROOT, "profiles", "traffic.json")) or {}
+    achieved = flops / (main["ffn_ms"] / 1e3) / 1e12
+    if cfgd["dtype"] == "bf16" and ffn_is_tensor:
+        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
+                "frac": achieved / bf16_peak if bf16_peak else None,
+                "peak_source": "MEASURED_PEAKS.json " + ("bf16_tflops_sustained" if timed_s > 1.0 else "bf16_tflops")}
+    else:
+        # SIMT FFMA: 148 SMs x 128 lanes x 2 flop x sm clock
+        clk = (main["clocks"] or {}).get("sm_mhz") or 1965.0
+        alu_peak = 148 * 128 * 2 * clk * 1e6 / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
+                "frac": achieved / alu_peak, "peak_source": f"148 SM x 128 FP32 lanes x 2 x {clk:.0f} MHz"}
+    roof["kernel"] = "smile_expert_ffn (2 grouped GEMM launches)"
+    roof["traffic"] = traffic.get(f"{args.config}_{modes[0]}_ffn")
+    roof["algorithmic_flops_per_step"] = flops
+    line = {
+        "metric": METRIC, "value": main["tokens"] / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if cfgd["dtype"] == "bf16" else "f32",
+        "data": "synthetic (N(0,1) tokens, U(+-1/sqrt(fan_in)) random-init router and experts)",
+        "config": {"workload": f"{args.config}: one {modes[0]} MoE layer fwd, {G} ranks as 2x4 (n x m), "
+                               f"e={e}/rank, T={T}/rank, d={d}, d_ff={d_ff}, cf={cfgd['cf']}, fused router; "
+                               f"{V} ranks per GPU", "ranks_per_gpu": V, "mode": modes[0],
+                   "l2": "flushed (256 MiB write) before every timed step, outside its events"},
+        "phase_ms": main["phase_ms"], "kept_tokens": main["kept"],
+        "roofline": roof, "gpu_launches": main["launches"] * args.steps,
+        "clocks": main["clocks"],
+    }
+    if "e2e" in main:
+        line["e2e"] = main["e2e"]
+    if "flat" in results and modes[0] != "flat":
+        f = results["flat"]
+        line["flat"] = {"value": f["tokens"] / (f["ms"] / 1e3), "ms_per_step": f["ms"], "phase_ms": f["phase_ms"],
+                        "e2e": f.get("e2e"), "kept_tokens": f["kept"]}
+        line["bilevel_over_flat"] = line["value"] / line["flat"]["value"]
+    if not args.no_cpu and world == 1:           # rank 0 at N = 1 only
+        line["cpu_baseline"] = cpu_oracle_sample(cfgd, modes[0])
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,268 @@
+/*
+ * smile.h -- C ABI of libsmile: the B200 (sm_100a) hot path of SMILE, the bi-level
+ * Switch-style MoE layer of arXiv 2212.05191 ("SMILE: Scaling Mixture-of-Experts with
+ * Efficient Bi-level Routing"), next to the flat single-All2All Switch baseline.
+ *
+ * Citations "P:Lx" are lines of the paper's text; "R<k>" are the readings of
+ * ambiguous passages listed in DESIGN.md.
+ *
+ * ---------------------------------------------------------------------------------
+ * Model.  G = n*m ranks form n groups ("nodes") of m ranks ("GPUs"); rank r = s*m + l
+ * is local index l of group s (R10).  Each rank holds e experts and T
+ * tokens.  Level 1 routes a token to a group (K1 = n destinations, the inter router W_p),
+ * level 2 to an expert of that group (K2 = m*e destinations, the intra router W_q); the
+ * token of source (s, l) travels first to the intermediate (i, l) and then to the expert
+ * rank (i, j/e) (Eq. 3).  FLAT mode is the one-hop Switch layer with
+ * K1 = G*e experts and no level 2.
+ *
+ * Ranks per process.  A process drives V = G / nprocs consecutive ranks on ONE device
+ * ("resident ranks", r = proc*V + v).  nprocs == 1 emulates the whole G-rank layer on
+ * one GPU (the exchanges become device copies); nprocs == G is one rank per GPU with the
+ * exchanges as NCCL all-to-alls on the split inter / intra communicators.
+ * Every per-rank array below has a leading dimension V.
+ *
+ * ---------------------------------------------------------------------------------
+ * Conventions (all calls).
+ *  - Ownership: the caller owns every buffer and the stream; the library owns only the
+ *    context (its NCCL communicators, a sticky device error flag and small scratch sized
+ *    at smile_create).  Nothing is allocated after smile_create.
+ *  - Pointers: every buffer argument is a DEVICE pointer on the context's device unless
+ *    its name starts with host_.  Rows are row-major, 16-byte aligned (d*b % 16 == 0).
+ *  - Asynchrony: calls enqueue work on `stream` and return; there is no host sync on the
+ *    hot path (smile_get_error and smile_forward_host excepted), so a sequence of calls
+ *    is CUDA-graph capturable.
+ *  - Errors: synchronous validation returns a status and launches nothing
+ *    (SMILE_EINVAL bad value, SMILE_ESHAPE layout mismatch, SMILE_ENOTSUP unsupported
+ *    combination).  Errors found on the device (non-finite logits, R27; an index out of
+ *    range) set a sticky flag that smile_get_error returns.
+ *  - T == 0 is a legal no-op for gate, dispatch, exchange, ffn and combine;
+ *    smile_aux_loss returns SMILE_EINVAL for T == 0 (the loss divides by T).
+ *  - Order: the calls of one layer must follow the sequence of smile_forward below; any
+ *    other order is undefined behaviour.  A context is not thread-safe.
+ * ---------------------------------------------------------------------------------
+ */
+#ifndef SMILE_H
+#define SMILE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMILE_VERSION 100
+
+typedef enum {
+    SMILE_OK = 0,
+    SMILE_EINVAL = 1,      /* invalid argument value (n, m, e < 1, cf <= 0, T < 0, ...) */
+    SMILE_ESHAPE = 2,      /* layout / size mismatch */
+    SMILE_ENONFINITE = 3,  /* device: a router logit was NaN or Inf (R27) */
+    SMILE_ECUDA = 4,       /* a CUDA runtime call failed */
+    SMILE_ENCCL = 5,       /* an NCCL call failed */
+    SMILE_ENOTSUP = 6,     /* valid but unsupported combination */
+    SMILE_EINDEX = 7       /* device: routing index out of range (corrupt route input) */
+} smile_status;
+
+typedef enum { SMILE_FP32 = 0, SMILE_BF16 = 1 } smile_dtype;
+typedef enum { SMILE_BILEVEL = 0, SMILE_FLAT = 1 } smile_mode;
+
+/* Expert-FFN implementation.  AUTO picks tcgen05 for bf16 and SIMT FFMA for fp32. */
+typedef enum { SMILE_FFN_AUTO = 0, SMILE_FFN_SIMT = 1, SMILE_FFN_TCGEN05 = 2 } smile_ffn_impl;
+
+typedef struct {
+    int32_t n, m, e;        /* groups, ranks per group, experts per rank */
+    int32_t mode;           /* smile_mode */
+    int32_t dtype;          /* smile_dtype of x, the exchanged rows and the expert weights */
+    int32_t d, d_ff;        /* hidden and FFN sizes */
+    int64_t T;              /* tokens per rank (static) */
+    double cf;              /* capacity factor */
+    int32_t nprocs;         /* processes of the job, each driving G/nprocs ranks */
+    int32_t proc;           /* this process, 0 <= proc < nprocs */
+    int32_t device;         /* CUDA device ordinal of this process */
+    int32_t ffn_impl;       /* smile_ffn_impl */
+} smile_shape;
+
+/* Sizes derived from a shape (R5, R7, R20):
+ *   K1 = BILEVEL ? n : G*e;   K2 = BILEVEL ? m*e : 1;
+ *   C1 = K1 > 1 ? ceil(cf*T/K1) : T;   C2 = BILEVEL ? (K2 > 1 ? ceil(cf*T/K2) : n*C1) : 0.
+ * S = segments per local expert at the FFN (BILEVEL: m source ranks; FLAT: G);
+ * Cseg = rows per segment (BILEVEL: C2; FLAT: C1). */
+typedef struct {
+    int32_t G, V, rank0;    /* ranks, ranks resident in this process, first resident rank */
+    int32_t K1, K2, KW;     /* destinations per level; KW = logits row width (K1 + K2, FLAT: K1) */
+    int64_t C1, C2;
+    int32_t S;
+    int64_t Cseg;
+    size_t ws_bytes;        /* size of the workspace smile_forward needs (smile_forward_ws) */
+} smile_sizes;
+
+typedef struct smile_ctx_s *smile_ctx;
+
+/* ---------------- context ---------------- */
+
+int          smile_version(void);
+const char  *smile_strerror(smile_status s);
+/* Pure host function, usable without a GPU: fills *out from *shape or returns
+ * SMILE_EINVAL (n, m, e, d, d_ff < 1, T < 0, cf <= 0, nprocs not dividing G, ...). */
+smile_status smile_plan(const smile_shape *shape, smile_sizes *out);
+/* Pure host: the group of global rank r at `level` (1 = inter {(i, l)}, 2 = intra
+ * {(s, g)}, 0 = world), written in position order to members[] (room for G ints); the
+ * member count is returned through *count.  P:L148, R10. */
+smile_status smile_group(const smile_shape *shape, int32_t level, int32_t r, int32_t *members,
+                         int32_t *count);
+/* 128-byte NCCL unique id, to be broadcast by the caller (e.g. torch.distributed) from
+ * process 0 before smile_create when nprocs > 1. */
+smile_status smile_get_unique_id(uint8_t out[128]);
+/* Creates the context on shape->device.  nprocs > 1: initialises an NCCL world
+ * communicator from `nccl_id` (collective: every process must call it) and, when
+ * V == 1, splits it into the inter (color l, key s) and intra (color s, key l)
+ * communicators.  nprocs == 1: nccl_id may be NULL. */
+smile_status smile_create(smile_ctx *ctx, const smile_shape *shape, const uint8_t *nccl_id);
+smile_status smile_destroy(smile_ctx ctx);
+smile_status smile_query(smile_ctx ctx, smile_sizes *out);
+/* Synchronises `stream`, then returns and clears the sticky device error flag. */
+smile_status smile_get_error(smile_ctx ctx, void *stream);
+
+/* ---------------- the steps of the layer ---------------- */
+
+/* Per-token routing decisions [V, T] (SoA). */
+typedef struct {
+    int32_t *dest1;   /* i: level-1 destination, first argmax of logits[0, K1) (R2, R3) */
+    int32_t *dest2;   /* j: level-2 destination, first argmax of logits[K1, K1+K2) (FLAT: 0) */
+    int32_t *slot1;   /* after smile_gate_inter: rank within its block; after
+                         smile_dispatch(level 1): # earlier tokens of the rank with the same
+                         dest1 -- kept iff slot1 < C1 */
+    float *p;         /* top-1 inter probability 1/sum_k exp(r_k - r_i) (Eq. 1, R4) */
+    float *q;         /* top-1 intra probability (FLAT: 1) */
+    float *gate;      /* fp32(p*q) (Eq. 3, R24) */
+} smile_route;
+
+/* Load-balancing statistics per resident rank (R13): argmax counts before
+ * capacity and sums of all softmax entries over the rank's T tokens. */
+typedef struct {
+    int32_t *hist1;   /* [V, K1] */
+    int32_t *hist2;   /* [V, K2] */
+    double *psum1;    /* [V, K1] */
+    double *psum2;    /* [V, K2] */
+} smile_stats;
+
+/* a1-a3: level-1 gate at the source.  x [V, T, d] (dtype) with w_router [KW, d] fp32
+ * (fused router, rows 0..K1-1 = W_p, then W_q) when logits == NULL, else the
+ * caller-supplied fp32 logits [V, T, KW].  logits_out (optional, fused mode only)
+ * receives the computed fp32 logits.  Writes route, stats, counts1 [V, K1] =
+ * min(hist1, C1).  Scratch for the capacity scan lives in the context. */
+smile_status smile_gate_inter(smile_ctx ctx, const void *x, const float *w_router,
+                              const float *logits, float *logits_out, const smile_route *route,
+                              const smile_stats *stats, int32_t *counts1, void *stream);
+
+/* a4 (level 1) / a7 (level 2): permute token rows into per-destination send buffers.
+ * level 1: rows_in = x [V, T, d]; finalises route->slot1; send_rows [V, K1, C1, d];
+ *   send_meta [V, K1, C1] = j of the token in that slot, -1 for empty slots (BILEVEL),
+ *   unused (may be NULL) in FLAT.
+ * level 2 (BILEVEL only): rows_in = recv1 [V, n, C1, d]; recv_meta [V, n, C1] from the
+ *   inter exchange; slot2 [V, n, C1] as written by smile_gate_intra (finalised here:
+ *   running count per j in received order, R8); send_rows [V, K2, C2, d] (= [V, m, e,
+ *   C2, d]).  Padding rows are never written. */
+smile_status smile_dispatch(smile_ctx ctx, int32_t level, const void *rows_in,
+                            const smile_route *route, const int32_t *recv_meta, int32_t *slot2,
+                            void *send_rows, int32_t *send_meta, void *stream);
+
+/* a6: level-2 gate at the intermediate rank (i, l): ranks the valid received slots of
+ * recv_meta [V, n, C1] per j in received order (source node ascending, then slot,
+ * R8) into slot2 [V, n, C1] (block-local until smile_dispatch level 2) and writes
+ * counts2 [V, K2] = min(#received per j, C2). */
+smile_status smile_gate_intra(smile_ctx ctx, const int32_t *recv_meta, int32_t *slot2,
+                              int32_t *counts2, void *stream);
+
+/* a5/a12 (inter), a8/a10 (intra), flat world exchange (a15): the capacity-padded
+ * equal-split All2All of one level.  Chunk p of send (rows
+ * [V, P, rows_per_peer, d] and ints [V, P, ints_per_peer]) goes to the p-th member of
+ * the rank's group, which receives it as chunk pos(sender).  level: 1 = inter
+ * (rows_per_peer = C1, ints = C1 meta), 2 = intra (e*C2 rows, e counts), 0 = world
+ * (FLAT: e*C1 rows, e counts).  reverse != 0 is the return trip of the same level
+ * (rows only, send_ints/recv_ints ignored); `fwd_counts` is the forward trip's
+ * per-chunk valid-row counts (level 1: counts1 [V, n]; level 2: counts2 [V, K2];
+ * world: counts1 [V, K1]) used by the device-copy path to move only valid rows;
+ * NCCL moves whole padded chunks (R25). */
+smile_status smile_all2all(smile_ctx ctx, int32_t level, int32_t reverse, const void *send_rows,
+                           void *recv_rows, const int32_t *send_ints, int32_t *recv_ints,
+                           const int32_t *fwd_counts, void *stream);
+smile_status smile_all2all_inter(smile_ctx ctx, int32_t reverse, const void *send_rows,
+                                 void *recv_rows, const int32_t *send_meta, int32_t *recv_meta,
+                                 const int32_t *fwd_counts, void *stream);
+smile_status smile_all2all_intra(smile_ctx ctx, int32_t reverse, const void *send_rows,
+                                 void *recv_rows, const int32_t *send_cnt, int32_t *recv_cnt,
+                                 const int32_t *fwd_counts, void *stream);
+
+/* a9: expert FFN Y = GELU(X W1 + b1) W2 + b2 (exact erf GELU, R21) for every resident
+ * expert over its S segments: X, Y [V, S, e, Cseg, d], counts [V, S, e] valid rows per
+ * segment; W1t [V*e, d_ff, d] and W2t [V*e, d, d_ff] (K-major transposes, dtype);
+ * b1 [V*e, d_ff], b2 [V*e, d] fp32; H_ws [V, S, e, Cseg, d_ff] (dtype).  bf16: tcgen05
+ * MMA with fp32 accumulation in TMEM, H rounded to bf16; fp32: SIMT FFMA. */
+smile_status smile_expert_ffn(smile_ctx ctx, const void *X, const int32_t *counts,
+                              const void *W1t, const float *b1, const void *W2t, const float *b2,
+                              void *H_ws, void *Y, void *stream);
+
+/* a11 (level 2) / a13 (level 1): un-permute and combine.
+ * level 2: ret1[s, c] = keep2 ? ret_rows[j, slot2] : 0 for every valid received slot
+ *   (recv_meta >= 0); ret_rows [V, K2, C2, d], out = ret1 [V, n, C1, d].
+ * level 1: out[t] = slot1 < C1 ? dtype(gate[t] * ret_rows[dest1, slot1]) : 0;
+ *   ret_rows [V, K1, C1, d], out [V, T, d].  The residual is the caller's. */
+smile_status smile_combine(smile_ctx ctx, int32_t level, const void *ret_rows,
+                           const smile_route *route, const int32_t *recv_meta,
+                           const int32_t *slot2, void *out, void *stream);
+
+/* a14: Eq. (4) per resident rank in fp64: loss[v] = alpha*K1*sum_i (hist1_i/T)(psum1_i/T)
+ * + beta*K2*sum_j (hist2_j/T)(psum2_j/T) (FLAT: first term only, the Switch loss). */
+smile_status smile_aux_loss(smile_ctx ctx, const smile_stats *stats, double alpha, double beta,
+                            double *loss, void *stream);
+
+/* ---------------- whole layer ---------------- */
+
+/* Caller-owned buffers of one layer; shapes as in the step calls. */
+typedef struct {
+    const void *x;            /* [V, T, d] */
+    const float *logits;      /* [V, T, KW] or NULL for the fused router */
+    const float *w_router;    /* [KW, d] (fused router) */
+    const void *W1t; const float *b1; const void *W2t; const float *b2;
+    void *out;                /* [V, T, d] */
+    double *loss;             /* [V] */
+    double alpha, beta;
+    void *ws;                 /* smile_sizes.ws_bytes bytes, 256-byte aligned */
+} smile_layer_io;
+
+/* Device pointers into the workspace of smile_forward, for inspection. */
+typedef struct {
+    smile_route route; smile_stats stats;
+    int32_t *counts1;                       /* [V, K1] */
+    void *send1; int32_t *meta1;            /* [V, K1, C1, d], [V, K1, C1] */
+    void *recv1; int32_t *rmeta1;           /* [V, n, C1, d], [V, n, C1] (BILEVEL) */
+    int32_t *slot2, *counts2;               /* [V, n, C1], [V, K2] */
+    void *send2; void *recv2;               /* [V, K2, C2, d] (BILEVEL) */
+    int32_t *rcounts;                       /* [V, S, e] valid rows per FFN segment */
+    void *ffn_in; void *H; void *Y;         /* [V, S, e, Cseg, d|d_ff] */
+    void *ret2; void *ret1; void *back1;    /* return-path buffers */
+} smile_ws_view;
+
+smile_status smile_forward_ws(smile_ctx ctx, void *ws, smile_ws_view *view);
+
+/* The whole forward of the layer on `stream`, in the paper's order (§3.2.3: four
+ * sequential All2Alls): gate_inter, dispatch(1), all2all_inter, gate_intra, dispatch(2),
+ * all2all_intra, expert_ffn, all2all_intra(rev), combine(2), all2all_inter(rev),
+ * combine(1), aux_loss.  FLAT: gate, dispatch(1), all2all(world), ffn,
+ * all2all(world, rev), combine(1), aux_loss. */
+smile_status smile_forward(smile_ctx ctx, const smile_layer_io *io, void *stream);
+
+/* End to end from HOST memory: copies host_x [V, T, d] (and host_logits when non-NULL)
+ * to io->x / io->logits, runs smile_forward, copies io->out to host_out and io->loss to
+ * host_loss, all on `stream`; synchronises `stream` before returning.  Host buffers
+ * should be pinned for asynchronous copies. */
+smile_status smile_forward_host(smile_ctx ctx, const smile_layer_io *io, const void *host_x,
+                                const float *host_logits, void *host_out, double *host_loss,
+                                void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMILE_H */

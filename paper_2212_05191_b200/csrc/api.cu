@@ -1,0 +1,568 @@
+// api.cu -- the C ABI of libsmile (include/smile.h): validation, context, NCCL
+// process groups, the exchange of each level, and the whole-layer sequence.
+#include "smile_internal.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include <algorithm>
+#include <vector>
+
+namespace smile {
+bool ffn_simt_supported(int nseg, int d, int d_ff);
+}
+
+using namespace smile;
+
+#define CUDA_TRY(x)                                   \
+    do {                                              \
+        if ((x) != cudaSuccess) return SMILE_ECUDA;   \
+    } while (0)
+#define NCCL_TRY(x)                                   \
+    do {                                              \
+        if ((x) != ncclSuccess) return SMILE_ENCCL;   \
+    } while (0)
+
+static inline cudaStream_t S(void *p) { return reinterpret_cast<cudaStream_t>(p); }
+
+extern "C" int smile_version(void) { return SMILE_VERSION; }
+
+extern "C" const char *smile_strerror(smile_status s) {
+    switch (s) {
+        case SMILE_OK: return "ok";
+        case SMILE_EINVAL: return "invalid argument";
+        case SMILE_ESHAPE: return "shape or layout mismatch";
+        case SMILE_ENONFINITE: return "non-finite router logit";
+        case SMILE_ECUDA: return "CUDA error";
+        case SMILE_ENCCL: return "NCCL error";
+        case SMILE_ENOTSUP: return "unsupported configuration";
+        case SMILE_EINDEX: return "routing index out of range";
+    }
+    return "unknown status";
+}
+
+// R5, R20: capacity ceil(cf*T/dests); one destination = no capacity.
+static int64_t capacity(int64_t T, int64_t dests, double cf) {
+    if (T <= 0) return 0;
+    if (dests <= 1) return T;
+    return (int64_t)ceil(cf * (double)T / (double)dests);
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Workspace carve-up for smile_forward (also gives ws_bytes).
+struct WsLayout {
+    size_t off[32];
+    size_t total;
+};
+
+static void ws_layout(const smile_shape *s, const smile_sizes *z, WsLayout *L, smile_ws_view *view,
+                      char *base) {
+    const int64_t V = z->V, T = s->T;
+    const int64_t eb = s->dtype == SMILE_BF16 ? 2 : 4;
+    const int64_t rb = (int64_t)s->d * eb;
+    const bool bi = s->mode == SMILE_BILEVEL;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes ? bytes : 1); return base ? base + r : nullptr; };
+    smile_ws_view w;
+    memset(&w, 0, sizeof(w));
+    w.route.dest1 = (int32_t *)take(V * T * 4);
+    w.route.dest2 = (int32_t *)take(V * T * 4);
+    w.route.slot1 = (int32_t *)take(V * T * 4);
+    w.route.p = (float *)take(V * T * 4);
+    w.route.q = (float *)take(V * T * 4);
+    w.route.gate = (float *)take(V * T * 4);
+    w.stats.hist1 = (int32_t *)take(V * z->K1 * 4);
+    w.stats.hist2 = (int32_t *)take(V * z->K2 * 4);
+    w.stats.psum1 = (double *)take(V * z->K1 * 8);
+    w.stats.psum2 = (double *)take(V * z->K2 * 8);
+    w.counts1 = (int32_t *)take(V * z->K1 * 4);
+    w.send1 = take(V * z->K1 * z->C1 * rb);
+    w.meta1 = (int32_t *)take(V * z->K1 * z->C1 * 4);
+    w.recv1 = take(V * z->K1 * z->C1 * rb);      // BILEVEL: [V, n, C1, d]; FLAT: [V, G, e, C, d]
+    w.rmeta1 = (int32_t *)take(bi ? V * z->K1 * z->C1 * 4 : 0);
+    if (bi) {
+        w.slot2 = (int32_t *)take(V * z->K1 * z->C1 * 4);
+        w.counts2 = (int32_t *)take(V * z->K2 * 4);
+        w.send2 = take(V * z->K2 * z->C2 * rb);
+        w.recv2 = take(V * z->K2 * z->C2 * rb);
+    }
+    w.rcounts = (int32_t *)take(V * z->S * s->e * 4);
+    w.ffn_in = bi ? w.recv2 : w.recv1;
+    const int64_t ffn_rows = V * z->S * s->e * z->Cseg;
+    w.H = take(ffn_rows * s->d_ff * eb);
+    w.Y = take(ffn_rows * rb);
+    if (bi) {
+        w.ret2 = take(V * z->K2 * z->C2 * rb);
+        w.ret1 = take(V * z->K1 * z->C1 * rb);
+    }
+    w.back1 = take(V * z->K1 * z->C1 * rb);
+    if (L) L->total = o;
+    if (view) *view = w;
+}
+
+extern "C" smile_status smile_plan(const smile_shape *s, smile_sizes *out) {
+    if (!s || !out) return SMILE_EINVAL;
+    if (s->n < 1 || s->m < 1 || s->e < 1 || s->d < 1 || s->d_ff < 1 || s->T < 0 || !(s->cf > 0.0))
+        return SMILE_EINVAL;
+    if (s->mode != SMILE_BILEVEL && s->mode != SMILE_FLAT) return SMILE_EINVAL;
+    if (s->dtype != SMILE_FP32 && s->dtype != SMILE_BF16) return SMILE_EINVAL;
+    const int G = s->n * s->m;
+    if (s->nprocs < 1 || G % s->nprocs != 0 || s->proc < 0 || s->proc >= s->nprocs) return SMILE_EINVAL;
+    if (s->T > (int64_t)1 << 30) return SMILE_ENOTSUP;
+    const int eb = s->dtype == SMILE_BF16 ? 2 : 4;
+    if ((s->d * eb) % 16 != 0 || (s->d_ff * eb) % 16 != 0) return SMILE_ESHAPE;
+    smile_sizes z;
+    memset(&z, 0, sizeof(z));
+    z.G = G;
+    z.V = G / s->nprocs;
+    z.rank0 = s->proc * z.V;
+    const bool bi = s->mode == SMILE_BILEVEL;
+    z.K1 = bi ? s->n : G * s->e;
+    z.K2 = bi ? s->m * s->e : 1;
+    z.KW = bi ? z.K1 + z.K2 : z.K1;
+    z.C1 = capacity(s->T, z.K1, s->cf);
+    z.C2 = bi ? (z.K2 > 1 ? capacity(s->T, z.K2, s->cf) : (int64_t)s->n * z.C1) : 0;
+    z.S = bi ? s->m : G;
+    z.Cseg = bi ? z.C2 : z.C1;
+    if (z.KW > 512 || z.K2 > 256) return SMILE_ENOTSUP;   // gate smem tile / level-2 rank limits
+    WsLayout L;
+    ws_layout(s, &z, &L, nullptr, nullptr);
+    z.ws_bytes = L.total;
+    *out = z;
+    return SMILE_OK;
+}
+
+// Group of global rank r (R10): level 1 = inter {(i, l)}_i positioned by node,
+// level 2 = intra {(s, g)}_g positioned by local index, level 0 = world.
+static void group_of(int n, int m, int level, int r, std::vector<int> &mem, int *mypos) {
+    const int s = r / m, l = r % m;
+    mem.clear();
+    if (level == 1) {
+        for (int i = 0; i < n; ++i) mem.push_back(i * m + l);
+        *mypos = s;
+    } else if (level == 2) {
+        for (int g = 0; g < m; ++g) mem.push_back(s * m + g);
+        *mypos = l;
+    } else {
+        for (int q = 0; q < n * m; ++q) mem.push_back(q);
+        *mypos = r;
+    }
+}
+
+extern "C" smile_status smile_group(const smile_shape *shape, int32_t level, int32_t r, int32_t *members,
+                                    int32_t *count) {
+    if (!shape || !members || !count || shape->n < 1 || shape->m < 1) return SMILE_EINVAL;
+    if (level < 0 || level > 2 || r < 0 || r >= shape->n * shape->m) return SMILE_EINVAL;
+    std::vector<int> mem;
+    int pos = 0;
+    group_of(shape->n, shape->m, level, r, mem, &pos);
+    for (size_t i = 0; i < mem.size(); ++i) members[i] = mem[i];
+    *count = (int32_t)mem.size();
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_get_unique_id(uint8_t out[128]) {
+    if (!out) return SMILE_EINVAL;
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "nccl unique id size");
+    memcpy(out, &id, 128);
+    return SMILE_OK;
+}
+
+static smile_status build_level(smile_ctx c, int level, int P, int nsub, int64_t Csub, int ipp) {
+    Level &L = c->lv[level];
+    const int V = c->sz.V;
+    L.P = P; L.nsub = nsub; L.Csub = Csub; L.ints_per_peer = ipp;
+    std::vector<int32_t> mloc(V * P), mglob(V * P), pos(V);
+    std::vector<int> mem;
+    L.any_remote = 0;
+    for (int v = 0; v < V; ++v) {
+        int mp = 0;
+        group_of(c->shape.n, c->shape.m, level, c->sz.rank0 + v, mem, &mp);
+        pos[v] = mp;
+        for (int p = 0; p < P; ++p) {
+            mglob[v * P + p] = mem[p];
+            const int ql = mem[p] - c->sz.rank0;
+            mloc[v * P + p] = (ql >= 0 && ql < V) ? ql : -1;
+            if (mloc[v * P + p] < 0) L.any_remote = 1;
+        }
+    }
+    L.h_member = (int32_t *)malloc(sizeof(int32_t) * V * P);
+    L.h_mypos = (int32_t *)malloc(sizeof(int32_t) * V);
+    memcpy(L.h_member, mglob.data(), sizeof(int32_t) * V * P);
+    memcpy(L.h_mypos, pos.data(), sizeof(int32_t) * V);
+    CUDA_TRY(cudaMalloc(&L.d_member_local, sizeof(int32_t) * V * P));
+    CUDA_TRY(cudaMalloc(&L.d_mypos, sizeof(int32_t) * V));
+    CUDA_TRY(cudaMemcpy(L.d_member_local, mloc.data(), sizeof(int32_t) * V * P, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(L.d_mypos, pos.data(), sizeof(int32_t) * V, cudaMemcpyHostToDevice));
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, const uint8_t *nccl_id) {
+    if (!out || !shape) return SMILE_EINVAL;
+    smile_sizes z;
+    smile_status st = smile_plan(shape, &z);
+    if (st != SMILE_OK) return st;
+    if (shape->nprocs > 1 && !nccl_id) return SMILE_EINVAL;
+    CUDA_TRY(cudaSetDevice(shape->device));
+    smile_ctx c = new smile_ctx_s();
+    c->shape = *shape;
+    c->sz = z;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, shape->device);
+    const int V = z.V;
+    c->TB1 = gate_tokens_per_block(z.KW);
+    c->nblk1 = (int)((shape->T + c->TB1 - 1) / c->TB1);
+    const int64_t items2 = (int64_t)shape->n * z.C1;
+    c->nblk2 = shape->mode == SMILE_BILEVEL ? (int)((items2 + kRank2Items - 1) / kRank2Items) : 0;
+    const size_t nb1 = (size_t)V * (c->nblk1 > 0 ? c->nblk1 : 1);
+    const size_t nb2 = (size_t)V * (c->nblk2 > 0 ? c->nblk2 : 1);
+    CUDA_TRY(cudaMalloc(&c->d_err, sizeof(int)));
+    CUDA_TRY(cudaMemset(c->d_err, 0, sizeof(int)));
+    CUDA_TRY(cudaMalloc(&c->blk_hist1, nb1 * z.K1 * 4));
+    CUDA_TRY(cudaMalloc(&c->blk_off1, nb1 * z.K1 * 4));
+    CUDA_TRY(cudaMalloc(&c->blk_hist2a, nb1 * z.K2 * 4));
+    CUDA_TRY(cudaMalloc(&c->blk_psum, nb1 * (z.K1 + z.K2) * 8));
+    CUDA_TRY(cudaMalloc(&c->blk_hist2, nb2 * z.K2 * 4));
+    CUDA_TRY(cudaMalloc(&c->blk_off2, nb2 * z.K2 * 4));
+    const int n = shape->n, m = shape->m, e = shape->e, G = z.G;
+    if (shape->mode == SMILE_BILEVEL) {
+        st = build_level(c, 1, n, 1, z.C1, (int)z.C1);
+        if (st == SMILE_OK) st = build_level(c, 2, m, e, z.C2, e);
+    } else {
+        st = build_level(c, 0, G, e, z.C1, e);
+    }
+    if (st != SMILE_OK) { smile_destroy(c); return st; }
+    if (shape->nprocs > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, sizeof(id));
+        if (ncclCommInitRank(&c->world, shape->nprocs, id, shape->proc) != ncclSuccess) {
+            smile_destroy(c);
+            return SMILE_ENCCL;
+        }
+        c->lv[0].comm = c->world;
+        if (V == 1) {
+            // one inter-node and one intra-node process group per process.
+            const int r = z.rank0, s = r / m, l = r % m;
+            if (ncclCommSplit(c->world, l, s, &c->inter, nullptr) != ncclSuccess ||
+                ncclCommSplit(c->world, s, l, &c->intra, nullptr) != ncclSuccess) {
+                smile_destroy(c);
+                return SMILE_ENCCL;
+            }
+            c->lv[1].comm = c->inter;
+            c->lv[2].comm = c->intra;
+        }
+    }
+    *out = c;
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_destroy(smile_ctx c) {
+    if (!c) return SMILE_EINVAL;
+    cudaSetDevice(c->shape.device);
+    if (c->inter) ncclCommDestroy(c->inter);
+    if (c->intra) ncclCommDestroy(c->intra);
+    if (c->world) ncclCommDestroy(c->world);
+    cudaFree(c->d_err);
+    cudaFree(c->blk_hist1); cudaFree(c->blk_off1); cudaFree(c->blk_hist2a); cudaFree(c->blk_psum);
+    cudaFree(c->blk_hist2); cudaFree(c->blk_off2);
+    for (auto &L : c->lv) {
+        cudaFree(L.d_member_local); cudaFree(L.d_mypos);
+        free(L.h_member); free(L.h_mypos);
+    }
+    delete c;
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_query(smile_ctx c, smile_sizes *out) {
+    if (!c || !out) return SMILE_EINVAL;
+    *out = c->sz;
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_get_error(smile_ctx c, void *stream) {
+    if (!c) return SMILE_EINVAL;
+    cudaSetDevice(c->shape.device);
+    CUDA_TRY(cudaStreamSynchronize(S(stream)));
+    int h = 0;
+    CUDA_TRY(cudaMemcpy(&h, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemset(c->d_err, 0, sizeof(int)));
+    return (smile_status)h;
+}
+
+static smile_status post_launch() {
+    return cudaGetLastError() == cudaSuccess ? SMILE_OK : SMILE_ECUDA;
+}
+
+extern "C" smile_status smile_gate_inter(smile_ctx c, const void *x, const float *w_router, const float *logits,
+                                         float *logits_out, const smile_route *route, const smile_stats *stats,
+                                         int32_t *counts1, void *stream) {
+    if (!c || !route || !stats || !counts1) return SMILE_EINVAL;
+    if (!logits && (!x || !w_router)) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c->shape.device);
+    GateArgs a;
+    a.x = x; a.w = w_router; a.logits = logits; a.logits_out = logits_out;
+    a.route = *route;
+    a.blk_hist1 = c->blk_hist1; a.blk_hist2a = c->blk_hist2a; a.blk_psum = c->blk_psum;
+    a.err = c->d_err; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
+    a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1;
+    a.flat = c->shape.mode == SMILE_FLAT; a.bf16 = c->shape.dtype == SMILE_BF16;
+    launch_gate1(a, S(stream));
+    Scan1Args s;
+    s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
+    s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
+    s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T;
+    launch_scan1(s, S(stream));
+    return post_launch();
+}
+
+extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *rows_in, const smile_route *route,
+                                       const int32_t *recv_meta, int32_t *slot2, void *send_rows, int32_t *send_meta,
+                                       void *stream) {
+    if (!c || !rows_in || !send_rows) return SMILE_EINVAL;
+    const int64_t rb = (int64_t)c->shape.d * (c->shape.dtype == SMILE_BF16 ? 2 : 4);
+    const bool bi = c->shape.mode == SMILE_BILEVEL;
+    cudaSetDevice(c->shape.device);
+    if (level == 1) {
+        if (!route || (bi && !send_meta)) return SMILE_EINVAL;
+        if (c->shape.T == 0) return SMILE_OK;
+        Dispatch1Args a;
+        a.x = rows_in; a.route = *route; a.blk_off1 = c->blk_off1; a.blk_hist1 = c->blk_hist1;
+        a.send = send_rows; a.meta = bi ? send_meta : nullptr;
+        a.V = c->sz.V; a.T = c->shape.T; a.rowbytes = rb; a.K1 = c->sz.K1; a.C1 = c->sz.C1;
+        a.TB = c->TB1; a.nblk = c->nblk1;
+        launch_dispatch1(a, S(stream));
+        return post_launch();
+    }
+    if (level == 2) {
+        if (!bi) return SMILE_EINVAL;
+        if (!recv_meta || !slot2) return SMILE_EINVAL;
+        if (c->shape.T == 0) return SMILE_OK;
+        Dispatch2Args a;
+        a.recv1 = rows_in; a.recv_meta = recv_meta; a.slot2 = slot2; a.blk_off2 = c->blk_off2;
+        a.send2 = send_rows; a.V = c->sz.V; a.items = (int64_t)c->shape.n * c->sz.C1; a.rowbytes = rb;
+        a.K2 = c->sz.K2; a.C2 = c->sz.C2; a.nblk = c->nblk2;
+        launch_dispatch2(a, S(stream));
+        return post_launch();
+    }
+    return SMILE_EINVAL;
+}
+
+extern "C" smile_status smile_gate_intra(smile_ctx c, const int32_t *recv_meta, int32_t *slot2, int32_t *counts2,
+                                         void *stream) {
+    if (!c || !recv_meta || !slot2 || !counts2) return SMILE_EINVAL;
+    if (c->shape.mode != SMILE_BILEVEL) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c->shape.device);
+    Rank2Args a;
+    a.recv_meta = recv_meta; a.slot2 = slot2; a.blk_hist2 = c->blk_hist2; a.blk_off2 = c->blk_off2;
+    a.counts2 = counts2; a.err = c->d_err; a.V = c->sz.V; a.items = (int64_t)c->shape.n * c->sz.C1;
+    a.K2 = c->sz.K2; a.nblk = c->nblk2; a.C2 = c->sz.C2;
+    launch_rank2(a, S(stream));
+    return post_launch();
+}
+
+// One level's equal-split All2All.  Pairs of ranks resident on this
+// device are a device copy; V == 1 uses ncclAlltoAll on the level's split communicator;
+// several resident ranks per process plus remote peers use grouped ncclSend/ncclRecv
+// on the world communicator, posted in (source rank, destination rank) order on both
+// sides so NCCL matches them.
+extern "C" smile_status smile_all2all(smile_ctx c, int32_t level, int32_t reverse, const void *send_rows,
+                                      void *recv_rows, const int32_t *send_ints, int32_t *recv_ints,
+                                      const int32_t *fwd_counts, void *stream) {
+    if (!c || !send_rows || !recv_rows || level < 0 || level > 2) return SMILE_EINVAL;
+    const bool bi = c->shape.mode == SMILE_BILEVEL;
+    if (bi == (level == 0)) return SMILE_EINVAL;
+    const Level &L = c->lv[level];
+    const bool with_ints = !reverse && send_ints && recv_ints;
+    if (!reverse && (!send_ints || !recv_ints)) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c->shape.device);
+    cudaStream_t st = S(stream);
+    const int64_t rb = (int64_t)c->shape.d * (c->shape.dtype == SMILE_BF16 ? 2 : 4);
+    const size_t chunk = (size_t)L.nsub * L.Csub * rb;
+    const int V = c->sz.V, P = L.P;
+    const bool nccl_alltoall = c->shape.nprocs > 1 && V == 1 && L.comm;
+    if (!nccl_alltoall) {
+        CopyXArgs a;
+        a.send = (const char *)send_rows; a.recv = (char *)recv_rows;
+        a.sint = with_ints ? send_ints : nullptr; a.rint = with_ints ? recv_ints : nullptr;
+        a.cnt = fwd_counts; a.member_local = L.d_member_local; a.mypos = L.d_mypos;
+        a.V = V; a.P = P; a.nsub = L.nsub; a.Csub = L.Csub; a.rowbytes = rb; a.ipp = L.ints_per_peer;
+        a.rev = reverse ? 1 : 0;
+        launch_exchange_copy(a, st);
+        if (cudaGetLastError() != cudaSuccess) return SMILE_ECUDA;
+    }
+    if (c->shape.nprocs == 1) return SMILE_OK;
+    if (nccl_alltoall) {
+        NCCL_TRY(ncclGroupStart());
+        NCCL_TRY(ncclAlltoAll(send_rows, recv_rows, chunk, ncclUint8, L.comm, st));
+        if (with_ints) NCCL_TRY(ncclAlltoAll(send_ints, recv_ints, L.ints_per_peer, ncclInt32, L.comm, st));
+        NCCL_TRY(ncclGroupEnd());
+        return SMILE_OK;
+    }
+    if (!L.any_remote) return SMILE_OK;
+    // mixed: remote pairs over the world communicator
+    struct Op { int src, dst, v, p; };
+    std::vector<Op> sends, recvs;
+    for (int v = 0; v < V; ++v)
+        for (int p = 0; p < P; ++p) {
+            const int q = L.h_member[v * P + p];
+            const int ql = q - c->sz.rank0;
+            if (ql >= 0 && ql < V) continue;
+            sends.push_back({c->sz.rank0 + v, q, v, p});
+            // q sends its chunk at position pos(v) to v; v receives it at chunk p (= pos(q))
+            recvs.push_back({q, c->sz.rank0 + v, v, p});
+        }
+    auto by_pair = [](const Op &a, const Op &b) { return a.src != b.src ? a.src < b.src : a.dst < b.dst; };
+    std::sort(sends.begin(), sends.end(), by_pair);
+    std::sort(recvs.begin(), recvs.end(), by_pair);
+    const int ipp = L.ints_per_peer;
+    NCCL_TRY(ncclGroupStart());
+    for (const Op &o : sends) {
+        const int peer = o.dst / V;
+        const size_t ci = (size_t)o.v * P + o.p;
+        NCCL_TRY(ncclSend((const char *)send_rows + ci * chunk, chunk, ncclUint8, peer, c->world, st));
+        if (with_ints) NCCL_TRY(ncclSend(send_ints + ci * ipp, ipp, ncclInt32, peer, c->world, st));
+    }
+    for (const Op &o : recvs) {
+        const int peer = o.src / V;
+        const size_t ci = (size_t)o.v * P + o.p;
+        NCCL_TRY(ncclRecv((char *)recv_rows + ci * chunk, chunk, ncclUint8, peer, c->world, st));
+        if (with_ints) NCCL_TRY(ncclRecv(recv_ints + ci * ipp, ipp, ncclInt32, peer, c->world, st));
+    }
+    NCCL_TRY(ncclGroupEnd());
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_all2all_inter(smile_ctx c, int32_t reverse, const void *send_rows, void *recv_rows,
+                                            const int32_t *send_meta, int32_t *recv_meta, const int32_t *fwd_counts,
+                                            void *stream) {
+    return smile_all2all(c, 1, reverse, send_rows, recv_rows, send_meta, recv_meta, fwd_counts, stream);
+}
+
+extern "C" smile_status smile_all2all_intra(smile_ctx c, int32_t reverse, const void *send_rows, void *recv_rows,
+                                            const int32_t *send_cnt, int32_t *recv_cnt, const int32_t *fwd_counts,
+                                            void *stream) {
+    return smile_all2all(c, 2, reverse, send_rows, recv_rows, send_cnt, recv_cnt, fwd_counts, stream);
+}
+
+extern "C" smile_status smile_expert_ffn(smile_ctx c, const void *X, const int32_t *counts, const void *W1t,
+                                         const float *b1, const void *W2t, const float *b2, void *H_ws, void *Y,
+                                         void *stream) {
+    if (!c || !X || !counts || !W1t || !b1 || !W2t || !b2 || !H_ws || !Y) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c->shape.device);
+    FfnArgs f;
+    f.X = X; f.counts = counts; f.W1t = W1t; f.b1 = b1; f.W2t = W2t; f.b2 = b2; f.H = H_ws; f.Y = Y;
+    f.V = c->sz.V; f.S = c->sz.S; f.e = c->shape.e; f.Cseg = c->sz.Cseg; f.d = c->shape.d; f.d_ff = c->shape.d_ff;
+    f.bf16 = c->shape.dtype == SMILE_BF16; f.num_sms = c->num_sms;
+    int impl = c->shape.ffn_impl;
+    if (impl == SMILE_FFN_AUTO) impl = SMILE_FFN_SIMT;   // TODO(tcgen05): bf16 -> SMILE_FFN_TCGEN05
+    if (impl == SMILE_FFN_TCGEN05) {
+        if (!f.bf16) return SMILE_ENOTSUP;
+        cudaError_t e = launch_ffn_tcgen05(f, S(stream));
+        if (e == cudaErrorNotSupported) return SMILE_ENOTSUP;
+        return e == cudaSuccess ? post_launch() : SMILE_ECUDA;
+    }
+    if (!ffn_simt_supported(f.V * f.S * f.e, f.d, f.d_ff)) return SMILE_ENOTSUP;
+    launch_ffn_simt(f, S(stream));
+    return post_launch();
+}
+
+extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *ret_rows, const smile_route *route,
+                                      const int32_t *recv_meta, const int32_t *slot2, void *out, void *stream) {
+    if (!c || !ret_rows || !out) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c->shape.device);
+    const bool bf = c->shape.dtype == SMILE_BF16;
+    if (level == 1) {
+        if (!route) return SMILE_EINVAL;
+        Combine1Args a;
+        a.back1 = ret_rows; a.route = *route; a.out = out; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
+        a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = bf;
+        launch_combine1(a, S(stream));
+        return post_launch();
+    }
+    if (level == 2) {
+        if (c->shape.mode != SMILE_BILEVEL || !recv_meta || !slot2) return SMILE_EINVAL;
+        Combine2Args a;
+        a.ret2 = ret_rows; a.recv_meta = recv_meta; a.slot2 = slot2; a.ret1 = out; a.V = c->sz.V;
+        a.items = (int64_t)c->shape.n * c->sz.C1; a.rowbytes = (int64_t)c->shape.d * (bf ? 2 : 4);
+        a.K2 = c->sz.K2; a.C2 = c->sz.C2;
+        launch_combine2(a, S(stream));
+        return post_launch();
+    }
+    return SMILE_EINVAL;
+}
+
+extern "C" smile_status smile_aux_loss(smile_ctx c, const smile_stats *stats, double alpha, double beta,
+                                       double *loss, void *stream) {
+    if (!c || !stats || !loss) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_EINVAL;
+    cudaSetDevice(c->shape.device);
+    launch_aux(*stats, alpha, beta, loss, c->sz.V, c->sz.K1, c->sz.K2, c->shape.T,
+               c->shape.mode == SMILE_FLAT, S(stream));
+    return post_launch();
+}
+
+extern "C" smile_status smile_forward_ws(smile_ctx c, void *ws, smile_ws_view *view) {
+    if (!c || !ws || !view) return SMILE_EINVAL;
+    if (((uintptr_t)ws & 255) != 0) return SMILE_ESHAPE;
+    ws_layout(&c->shape, &c->sz, nullptr, view, (char *)ws);
+    return SMILE_OK;
+}
+
+#define STEP(x)                            \
+    do {                                   \
+        smile_status _s = (x);             \
+        if (_s != SMILE_OK) return _s;     \
+    } while (0)
+
+extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, void *stream) {
+    if (!c || !io || !io->x || !io->out || !io->loss || !io->ws) return SMILE_EINVAL;
+    if (!io->logits && !io->w_router) return SMILE_EINVAL;
+    smile_ws_view w;
+    STEP(smile_forward_ws(c, io->ws, &w));
+    if (c->shape.T == 0) return SMILE_OK;
+    STEP(smile_gate_inter(c, io->x, io->w_router, io->logits, nullptr, &w.route, &w.stats, w.counts1, stream));
+    STEP(smile_dispatch(c, 1, io->x, &w.route, nullptr, nullptr, w.send1, w.meta1, stream));
+    if (c->shape.mode == SMILE_BILEVEL) {
+        // the paper's "four sequential All2All operations"
+        STEP(smile_all2all_inter(c, 0, w.send1, w.recv1, w.meta1, w.rmeta1, w.counts1, stream));
+        STEP(smile_gate_intra(c, w.rmeta1, w.slot2, w.counts2, stream));
+        STEP(smile_dispatch(c, 2, w.recv1, nullptr, w.rmeta1, w.slot2, w.send2, nullptr, stream));
+        STEP(smile_all2all_intra(c, 0, w.send2, w.recv2, w.counts2, w.rcounts, w.counts2, stream));
+        STEP(smile_expert_ffn(c, w.recv2, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.H, w.Y, stream));
+        STEP(smile_all2all_intra(c, 1, w.Y, w.ret2, nullptr, nullptr, w.counts2, stream));
+        STEP(smile_combine(c, 2, w.ret2, nullptr, w.rmeta1, w.slot2, w.ret1, stream));
+        STEP(smile_all2all_inter(c, 1, w.ret1, w.back1, nullptr, nullptr, w.counts1, stream));
+    } else {
+        STEP(smile_all2all(c, 0, 0, w.send1, w.recv1, w.counts1, w.rcounts, w.counts1, stream));
+        STEP(smile_expert_ffn(c, w.recv1, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.H, w.Y, stream));
+        STEP(smile_all2all(c, 0, 1, w.Y, w.back1, nullptr, nullptr, w.counts1, stream));
+    }
+    STEP(smile_combine(c, 1, w.back1, &w.route, nullptr, nullptr, io->out, stream));
+    STEP(smile_aux_loss(c, &w.stats, io->alpha, io->beta, io->loss, stream));
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_forward_host(smile_ctx c, const smile_layer_io *io, const void *host_x,
+                                           const float *host_logits, void *host_out, double *host_loss, void *stream) {
+    if (!c || !io || !host_x || !host_out || !host_loss) return SMILE_EINVAL;
+    if (host_logits && !io->logits) return SMILE_EINVAL;
+    cudaSetDevice(c->shape.device);
+    cudaStream_t st = S(stream);
+    const size_t xb = (size_t)c->sz.V * c->shape.T * c->shape.d * (c->shape.dtype == SMILE_BF16 ? 2 : 4);
+    CUDA_TRY(cudaMemcpyAsync((void *)io->x, host_x, xb, cudaMemcpyHostToDevice, st));
+    if (host_logits)
+        CUDA_TRY(cudaMemcpyAsync((void *)io->logits, host_logits, (size_t)c->sz.V * c->shape.T * c->sz.KW * 4,
+                                 cudaMemcpyHostToDevice, st));
+    STEP(smile_forward(c, io, stream));
+    CUDA_TRY(cudaMemcpyAsync(host_out, io->out, xb, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(host_loss, io->loss, (size_t)c->sz.V * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return SMILE_OK;
+}

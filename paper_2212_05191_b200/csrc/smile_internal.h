@@ -1,0 +1,122 @@
+// smile_internal.h -- private declarations shared by the libsmile translation units.
+// Product code: never includes anything under oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <nccl.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "../../include/smile.h"
+
+namespace smile {
+
+constexpr int kWarp = 32;
+
+// Tokens per block of the level-1 gate (sized so the logits tile stays <= 32 KB of smem).
+inline int gate_tokens_per_block(int KW) {
+    if (KW <= 32) return 256;
+    if (KW <= 64) return 128;
+    if (KW <= 128) return 64;
+    return 32;
+}
+constexpr int kRank2Items = 256;     // received slots per block of the level-2 gate
+
+// Exchange topology of one level for the resident ranks (host-built at smile_create).
+struct Level {
+    int P = 1;                 // group size (peers incl. self)
+    int nsub = 1;              // sub-chunks per peer chunk (e experts, or 1)
+    int64_t Csub = 0;          // rows per sub-chunk
+    int ints_per_peer = 0;     // side ints per peer chunk (meta or counts)
+    int32_t *d_member_local = nullptr;  // [V, P] local index of member p, -1 if remote
+    int32_t *d_mypos = nullptr;         // [V]   position of resident rank v in its group
+    int32_t *h_member = nullptr;        // [V, P] global rank of member p (host)
+    int32_t *h_mypos = nullptr;         // [V]
+    int any_remote = 0;
+    ncclComm_t comm = nullptr;          // split comm when V == 1 (inter/intra) or world
+};
+
+}  // namespace smile
+
+struct smile_ctx_s {
+    smile_shape shape;
+    smile_sizes sz;
+    int TB1 = 256;             // gate tokens per block
+    int nblk1 = 0;             // gate blocks per rank
+    int nblk2 = 0;             // level-2 ranking blocks per rank
+    int *d_err = nullptr;      // sticky device error flag (smile_status)
+    int32_t *blk_hist1 = nullptr, *blk_off1 = nullptr, *blk_hist2a = nullptr;
+    double *blk_psum = nullptr;
+    int32_t *blk_hist2 = nullptr, *blk_off2 = nullptr;
+    ncclComm_t world = nullptr, inter = nullptr, intra = nullptr;
+    smile::Level lv[3];        // 0 world, 1 inter, 2 intra
+    int num_sms = 148;
+};
+
+namespace smile {
+
+// ---- launchers implemented in the .cu files (all asynchronous on `st`) ----
+struct GateArgs {
+    const void *x; const float *w; const float *logits; float *logits_out;
+    smile_route route; int32_t *blk_hist1, *blk_hist2a; double *blk_psum;
+    int *err; int V; int64_t T; int d; int K1, K2, KW; int TB, nblk; int flat; int bf16;
+};
+void launch_gate1(const GateArgs &a, cudaStream_t st);
+
+struct Scan1Args {
+    const int32_t *blk_hist1, *blk_hist2a; const double *blk_psum; int32_t *blk_off1;
+    smile_stats stats; int32_t *counts1; int V, nblk, K1, K2, KW; int64_t C1; int flat; int64_t T;
+};
+void launch_scan1(const Scan1Args &a, cudaStream_t st);
+
+struct Rank2Args {
+    const int32_t *recv_meta; int32_t *slot2; int32_t *blk_hist2; int32_t *blk_off2;
+    int32_t *counts2; int *err; int V; int64_t items; int K2; int nblk; int64_t C2;
+};
+void launch_rank2(const Rank2Args &a, cudaStream_t st);
+
+struct Dispatch1Args {
+    const void *x; smile_route route; const int32_t *blk_off1; const int32_t *blk_hist1;
+    void *send; int32_t *meta; int V; int64_t T; int64_t rowbytes; int K1; int64_t C1; int TB, nblk;
+};
+void launch_dispatch1(const Dispatch1Args &a, cudaStream_t st);
+
+struct Dispatch2Args {
+    const void *recv1; const int32_t *recv_meta; int32_t *slot2; const int32_t *blk_off2;
+    void *send2; int V; int64_t items; int64_t rowbytes; int K2; int64_t C2; int nblk;
+};
+void launch_dispatch2(const Dispatch2Args &a, cudaStream_t st);
+
+struct Combine2Args {
+    const void *ret2; const int32_t *recv_meta; const int32_t *slot2; void *ret1;
+    int V; int64_t items; int64_t rowbytes; int K2; int64_t C2;
+};
+void launch_combine2(const Combine2Args &a, cudaStream_t st);
+
+struct Combine1Args {
+    const void *back1; smile_route route; void *out; int V; int64_t T; int d; int K1; int64_t C1;
+    int bf16;
+};
+void launch_combine1(const Combine1Args &a, cudaStream_t st);
+
+void launch_aux(const smile_stats &s, double alpha, double beta, double *loss, int V, int K1,
+                int K2, int64_t T, int flat, cudaStream_t st);
+
+struct CopyXArgs {
+    const char *send; char *recv; const int32_t *sint; int32_t *rint; const int32_t *cnt;
+    const int32_t *member_local; const int32_t *mypos; int V, P, nsub; int64_t Csub;
+    int64_t rowbytes; int ipp; int rev;
+};
+void launch_exchange_copy(const CopyXArgs &a, cudaStream_t st);
+
+struct FfnArgs {
+    const void *X; const int32_t *counts; const void *W1t; const float *b1; const void *W2t;
+    const float *b2; void *H; void *Y; int V, S, e; int64_t Cseg; int d, d_ff; int bf16;
+    int num_sms;
+};
+void launch_ffn_simt(const FfnArgs &a, cudaStream_t st);
+// Returns cudaErrorNotSupported when the shape cannot run on the tcgen05 path.
+cudaError_t launch_ffn_tcgen05(const FfnArgs &a, cudaStream_t st);
+
+}  // namespace smile

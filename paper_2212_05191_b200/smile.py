@@ -1,0 +1,266 @@
+"""ctypes binding of libsmile (include/smile.h).  Argument marshalling only.
+
+PyTorch supplies device memory, streams and (for bootstrap) torch.distributed; every
+step of the layer runs in libsmile's kernels.  Names follow the C ABI: gate_inter,
+dispatch, all2all_inter / all2all_intra / all2all, gate_intra, expert_ffn, combine,
+aux_loss, forward, forward_host.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsmile.so")
+_lib = None
+
+BILEVEL, FLAT = 0, 1
+FP32, BF16 = 0, 1
+FFN_AUTO, FFN_SIMT, FFN_TCGEN05 = 0, 1, 2
+TCGEN05_DEFAULT = False   # AUTO resolves bf16 to the tcgen05 FFN (api.cu smile_expert_ffn)
+_STATUS = {0: "ok", 1: "invalid argument", 2: "shape or layout mismatch", 3: "non-finite router logit",
+           4: "CUDA error", 5: "NCCL error", 6: "unsupported configuration", 7: "routing index out of range"}
+
+
+class SmileError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: {_STATUS.get(code, code)} ({code})")
+        self.code = code
+
+
+class Shape(C.Structure):
+    _fields_ = [("n", C.c_int32), ("m", C.c_int32), ("e", C.c_int32), ("mode", C.c_int32),
+                ("dtype", C.c_int32), ("d", C.c_int32), ("d_ff", C.c_int32), ("T", C.c_int64),
+                ("cf", C.c_double), ("nprocs", C.c_int32), ("proc", C.c_int32), ("device", C.c_int32),
+                ("ffn_impl", C.c_int32)]
+
+
+class Sizes(C.Structure):
+    _fields_ = [("G", C.c_int32), ("V", C.c_int32), ("rank0", C.c_int32), ("K1", C.c_int32),
+                ("K2", C.c_int32), ("KW", C.c_int32), ("C1", C.c_int64), ("C2", C.c_int64),
+                ("S", C.c_int32), ("Cseg", C.c_int64), ("ws_bytes", C.c_size_t)]
+
+
+_P = C.c_void_p
+
+
+class Route(C.Structure):
+    _fields_ = [(k, _P) for k in ("dest1", "dest2", "slot1", "p", "q", "gate")]
+
+
+class Stats(C.Structure):
+    _fields_ = [(k, _P) for k in ("hist1", "hist2", "psum1", "psum2")]
+
+
+class LayerIO(C.Structure):
+    _fields_ = [("x", _P), ("logits", _P), ("w_router", _P), ("W1t", _P), ("b1", _P), ("W2t", _P),
+                ("b2", _P), ("out", _P), ("loss", _P), ("alpha", C.c_double), ("beta", C.c_double),
+                ("ws", _P)]
+
+
+class WsView(C.Structure):
+    _fields_ = [("route", Route), ("stats", Stats)] + [(k, _P) for k in (
+        "counts1", "send1", "meta1", "recv1", "rmeta1", "slot2", "counts2", "send2", "recv2", "rcounts",
+        "ffn_in", "H", "Y", "ret2", "ret1", "back1")]
+
+
+def lib():
+    """Load the in-tree libsmile.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2212_05191_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.smile_version.restype = C.c_int
+        L.smile_strerror.restype = C.c_char_p
+        for name in ("smile_plan", "smile_group", "smile_get_unique_id", "smile_create", "smile_destroy",
+                     "smile_query", "smile_get_error", "smile_gate_inter", "smile_dispatch", "smile_gate_intra",
+                     "smile_all2all", "smile_all2all_inter", "smile_all2all_intra", "smile_expert_ffn",
+                     "smile_combine", "smile_aux_loss", "smile_forward_ws", "smile_forward", "smile_forward_host"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise SmileError(rc, what)
+
+
+def _shape(n, m, e, d, d_ff, T, cf, dtype, mode, nprocs=1, proc=0, device=0, ffn_impl=FFN_AUTO) -> Shape:
+    dt = {"fp32": FP32, "bf16": BF16}[dtype] if isinstance(dtype, str) else dtype
+    md = {"bilevel": BILEVEL, "flat": FLAT}[mode] if isinstance(mode, str) else mode
+    fi = {"auto": FFN_AUTO, "simt": FFN_SIMT, "tcgen05": FFN_TCGEN05}[ffn_impl] if isinstance(ffn_impl, str) else ffn_impl
+    return Shape(n, m, e, md, dt, d, d_ff, T, cf, nprocs, proc, device, fi)
+
+
+def plan(**kw) -> Sizes:
+    """Host-only size plan (no GPU needed): smile_plan."""
+    z = Sizes()
+    _check(lib().smile_plan(C.byref(_shape(**kw)), C.byref(z)), "smile_plan")
+    return z
+
+
+def group(n: int, m: int, level: int, r: int) -> list[int]:
+    """Host-only: members of rank r's group at level (1 inter, 2 intra, 0 world)."""
+    sh = _shape(n, m, 1, 8, 8, 1, 1.0, "fp32", "bilevel")
+    buf = (C.c_int32 * (n * m))()
+    cnt = C.c_int32()
+    _check(lib().smile_group(C.byref(sh), level, r, buf, C.byref(cnt)), "smile_group")
+    return list(buf[: cnt.value])
+
+
+def unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().smile_get_unique_id(buf), "smile_get_unique_id")
+    return bytes(buf)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+class SmileLayer:
+    """One SMILE (or flat Switch) layer: G = n*m ranks, V = G/nprocs of them resident here.
+
+    Buffers are torch tensors owned by the caller / this object; calls are asynchronous on
+    the current torch stream."""
+
+    def __init__(self, n, m, e, d, d_ff, T, cf=2.0, dtype="bf16", mode="bilevel", nprocs=1, proc=0,
+                 device=None, ffn_impl="auto", nccl_id: bytes | None = None):
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.shape = _shape(n, m, e, d, d_ff, T, cf, dtype, mode, nprocs, proc, self.device.index, ffn_impl)
+        self.n, self.m, self.e, self.d, self.d_ff, self.T, self.cf = n, m, e, d, d_ff, T, cf
+        self.dtype = torch.bfloat16 if self.shape.dtype == BF16 else torch.float32
+        self.flat = self.shape.mode == FLAT
+        self._ctx = C.c_void_p()
+        idbuf = None if nccl_id is None else (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        _check(lib().smile_create(C.byref(self._ctx), C.byref(self.shape), idbuf), "smile_create")
+        self.sizes = Sizes()
+        _check(lib().smile_query(self._ctx, C.byref(self.sizes)), "smile_query")
+        z = self.sizes
+        self.G, self.V, self.K1, self.K2, self.KW = z.G, z.V, z.K1, z.K2, z.KW
+        self.C1, self.C2, self.S, self.Cseg = z.C1, z.C2, z.S, z.Cseg
+        self.ws = None
+
+    def close(self):
+        if self._ctx:
+            lib().smile_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- workspace ------------------------------------------------------------------
+    def alloc_workspace(self):
+        self.ws = torch.empty(self.sizes.ws_bytes + 256, dtype=torch.uint8, device=self.device)
+        off = (-self.ws.data_ptr()) % 256
+        self.ws = self.ws[off: off + self.sizes.ws_bytes]
+        self._view = WsView()
+        _check(lib().smile_forward_ws(self._ctx, _ptr(self.ws), C.byref(self._view)), "smile_forward_ws")
+        return self.ws
+
+    def _slice(self, addr, shape, dtype):
+        nel = 1
+        for s in shape:
+            nel *= s
+        nbytes = nel * torch.empty((), dtype=dtype).element_size()
+        off = addr - self.ws.data_ptr()
+        return self.ws[off: off + nbytes].view(dtype).view(shape)
+
+    def view(self) -> dict:
+        """Workspace buffers of the last forward as tensors (for inspection / tests)."""
+        w, V, T = self._view, self.V, self.T
+        i32, f32, f64, dt = torch.int32, torch.float32, torch.float64, self.dtype
+        out = {k: self._slice(getattr(w.route, k), (V, T), i32 if k in ("dest1", "dest2", "slot1") else f32)
+               for k in ("dest1", "dest2", "slot1", "p", "q", "gate")}
+        out["hist1"] = self._slice(w.stats.hist1, (V, self.K1), i32)
+        out["hist2"] = self._slice(w.stats.hist2, (V, self.K2), i32)
+        out["psum1"] = self._slice(w.stats.psum1, (V, self.K1), f64)
+        out["psum2"] = self._slice(w.stats.psum2, (V, self.K2), f64)
+        out["counts1"] = self._slice(w.counts1, (V, self.K1), i32)
+        out["rcounts"] = self._slice(w.rcounts, (V, self.S, self.e), i32)
+        if not self.flat:
+            out["rmeta1"] = self._slice(w.rmeta1, (V, self.n * self.C1), i32)
+            out["slot2"] = self._slice(w.slot2, (V, self.n * self.C1), i32)
+            out["counts2"] = self._slice(w.counts2, (V, self.K2), i32)
+        return out
+
+    # ---- the steps (C ABI) ------------------------------------------------------------
+    def route_struct(self):
+        return self._view.route
+
+    def forward(self, x, W1t, b1, W2t, b2, out, loss, logits=None, w_router=None, alpha=0.005, beta=0.005,
+                stream=None):
+        if self.ws is None:
+            self.alloc_workspace()
+        io = LayerIO(_ptr(x), _ptr(logits), _ptr(w_router), _ptr(W1t), _ptr(b1), _ptr(W2t), _ptr(b2), _ptr(out),
+                     _ptr(loss), alpha, beta, _ptr(self.ws))
+        _check(lib().smile_forward(self._ctx, C.byref(io), _stream(stream)), "smile_forward")
+
+    def forward_host(self, x_dev, host_x, W1t, b1, W2t, b2, out, loss, host_out, host_loss, logits=None,
+                     host_logits=None, w_router=None, alpha=0.005, beta=0.005, stream=None):
+        if self.ws is None:
+            self.alloc_workspace()
+        io = LayerIO(_ptr(x_dev), _ptr(logits), _ptr(w_router), _ptr(W1t), _ptr(b1), _ptr(W2t), _ptr(b2),
+                     _ptr(out), _ptr(loss), alpha, beta, _ptr(self.ws))
+        _check(lib().smile_forward_host(self._ctx, C.byref(io), _ptr(host_x), _ptr(host_logits), _ptr(host_out),
+                                        _ptr(host_loss), _stream(stream)), "smile_forward_host")
+
+    def get_error(self, stream=None) -> int:
+        return lib().smile_get_error(self._ctx, _stream(stream))
+
+    # individual steps, same names as the C ABI ------------------------------------------
+    def gate_inter(self, x, route, stats, counts1, w_router=None, logits=None, logits_out=None, stream=None):
+        _check(lib().smile_gate_inter(self._ctx, _ptr(x), _ptr(w_router), _ptr(logits), _ptr(logits_out),
+                                      C.byref(route), C.byref(stats), _ptr(counts1), _stream(stream)),
+               "smile_gate_inter")
+
+    def dispatch(self, level, rows_in, send_rows, route=None, recv_meta=None, slot2=None, send_meta=None,
+                 stream=None):
+        _check(lib().smile_dispatch(self._ctx, level, _ptr(rows_in), None if route is None else C.byref(route),
+                                    _ptr(recv_meta), _ptr(slot2), _ptr(send_rows), _ptr(send_meta),
+                                    _stream(stream)), "smile_dispatch")
+
+    def gate_intra(self, recv_meta, slot2, counts2, stream=None):
+        _check(lib().smile_gate_intra(self._ctx, _ptr(recv_meta), _ptr(slot2), _ptr(counts2), _stream(stream)),
+               "smile_gate_intra")
+
+    def all2all(self, level, reverse, send_rows, recv_rows, send_ints=None, recv_ints=None, fwd_counts=None,
+                stream=None):
+        _check(lib().smile_all2all(self._ctx, level, int(reverse), _ptr(send_rows), _ptr(recv_rows),
+                                   _ptr(send_ints), _ptr(recv_ints), _ptr(fwd_counts), _stream(stream)),
+               "smile_all2all")
+
+    def all2all_inter(self, reverse, send_rows, recv_rows, send_meta=None, recv_meta=None, fwd_counts=None,
+                      stream=None):
+        _check(lib().smile_all2all_inter(self._ctx, int(reverse), _ptr(send_rows), _ptr(recv_rows), _ptr(send_meta),
+                                         _ptr(recv_meta), _ptr(fwd_counts), _stream(stream)), "smile_all2all_inter")
+
+    def all2all_intra(self, reverse, send_rows, recv_rows, send_cnt=None, recv_cnt=None, fwd_counts=None,
+                      stream=None):
+        _check(lib().smile_all2all_intra(self._ctx, int(reverse), _ptr(send_rows), _ptr(recv_rows), _ptr(send_cnt),
+                                         _ptr(recv_cnt), _ptr(fwd_counts), _stream(stream)), "smile_all2all_intra")
+
+    def expert_ffn(self, X, counts, W1t, b1, W2t, b2, H, Y, stream=None):
+        _check(lib().smile_expert_ffn(self._ctx, _ptr(X), _ptr(counts), _ptr(W1t), _ptr(b1), _ptr(W2t), _ptr(b2),
+                                      _ptr(H), _ptr(Y), _stream(stream)), "smile_expert_ffn")
+
+    def combine(self, level, ret_rows, out, route=None, recv_meta=None, slot2=None, stream=None):
+        _check(lib().smile_combine(self._ctx, level, _ptr(ret_rows), None if route is None else C.byref(route),
+                                   _ptr(recv_meta), _ptr(slot2), _ptr(out), _stream(stream)), "smile_combine")
+
+    def aux_loss(self, stats, loss, alpha=0.005, beta=0.005, stream=None):
+        _check(lib().smile_aux_loss(self._ctx, C.byref(stats), C.c_double(alpha), C.c_double(beta), _ptr(loss),
+                                    _stream(stream)), "smile_aux_loss")
