@@ -70,7 +70,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs = list(ex.map(compile_one, srcs))
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-L", lib, "-l:libnccl.so.2",
-                                                            "-Xlinker", f"-rpath={lib}", "-lcuda"]
+                                                            "-Xlinker", f"-rpath={lib}"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

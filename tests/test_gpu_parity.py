@@ -191,3 +191,33 @@ def test_skewed_drops_full_size_sampled():
     rs = np.random.default_rng(1)
     rows = np.unique(np.concatenate([rs.integers(0, 8 * 16384, 48), dropped[:16]]))
     run_and_check(case, rows=rows)
+
+
+# ---- tcgen05 / TMEM / TMA expert FFN (bf16 product path) -------------------------------
+
+@pytest.mark.parametrize("n,m,e,T,d,d_ff,cf,mode", [
+    (2, 4, 1, 1000, 64, 128, 1.0, "bilevel"),     # BN 64 / 128, one K block
+    (2, 2, 2, 700, 256, 512, 1.25, "flat"),
+    (2, 4, 1, 2048, 768, 3072, 2.0, "bilevel"),   # C2 layer shape, reduced T
+    (2, 2, 1, 600, 1600, 6400, 2.0, "bilevel"),   # C5 widths: BN 160 for d = 1600
+    (2, 4, 8, 512, 1024, 4096, 2.0, "bilevel"),   # C4 widths, 64 experts
+])
+def test_tcgen05_ffn(n, m, e, T, d, d_ff, cf, mode):
+    run_and_check(Case(n, m, e, T, d, d_ff, cf, dtype="bf16", mode=mode, dist="skewed", seed=9, ffn_impl="tcgen05"))
+
+
+def test_tcgen05_c2_full_size_sampled():
+    case = Case(2, 4, 1, 16384, 768, 3072, 2.0, dtype="bf16", dist="balanced", seed=2, ffn_impl="tcgen05")
+    rs = np.random.default_rng(2)
+    rows = np.unique(np.concatenate([rs.integers(0, 8 * 16384, 96), [0, 8 * 16384 - 1]]))
+    run_and_check(case, rows=rows)
+
+
+def test_tcgen05_matches_simt():
+    """Same inputs through both FFN paths: identical routing, outputs within bf16 rounding."""
+    a = Case(2, 4, 1, 1500, 256, 1024, 1.25, dtype="bf16", dist="balanced", seed=10, ffn_impl="tcgen05")
+    b = Case(2, 4, 1, 1500, 256, 1024, 1.25, dtype="bf16", dist="balanced", seed=10, ffn_impl="simt")
+    _, oa, la, _ = a.run_gpu()
+    _, ob, lb, _ = b.run_gpu()
+    assert torch.equal(la, lb)
+    assert_close_scaled(oa.float().cpu().numpy(), ob.float().cpu().numpy(), 1e-2, "tcgen05 vs simt")
