@@ -244,17 +244,16 @@ static double gelu(double z) { return 0.5 * z * (1.0 + erf(z / sqrt(2.0))); }
  * W1 [d, d_ff], b1 [d_ff], W2 [d_ff, d], b2 [d] of ONE expert. */
 void oracle_ffn_row(int32_t d, int32_t d_ff, const float *x, const float *W1, const float *b1,
                     const float *W2, const float *b2, double *y) {
+    /* a_f = b1_f + sum_k x_k W1[k][f] and y_c = b2_c + sum_f h_f W2[f][c], each sum taken
+     * in ascending k (resp. f) order; the loops run row-wise over W1 / W2. */
     double *h = (double *)malloc(sizeof(double) * (size_t)d_ff);
-    for (int32_t f = 0; f < d_ff; ++f) {
-        double a = (double)b1[f];
-        for (int32_t k = 0; k < d; ++k) a += (double)x[k] * (double)W1[(int64_t)k * d_ff + f];
-        h[f] = gelu(a);
-    }
-    for (int32_t cc = 0; cc < d; ++cc) {
-        double a = (double)b2[cc];
-        for (int32_t f = 0; f < d_ff; ++f) a += h[f] * (double)W2[(int64_t)f * d + cc];
-        y[cc] = a;
-    }
+    for (int32_t f = 0; f < d_ff; ++f) h[f] = (double)b1[f];
+    for (int32_t k = 0; k < d; ++k)
+        for (int32_t f = 0; f < d_ff; ++f) h[f] += (double)x[k] * (double)W1[(int64_t)k * d_ff + f];
+    for (int32_t f = 0; f < d_ff; ++f) h[f] = gelu(h[f]);
+    for (int32_t cc = 0; cc < d; ++cc) y[cc] = (double)b2[cc];
+    for (int32_t f = 0; f < d_ff; ++f)
+        for (int32_t cc = 0; cc < d; ++cc) y[cc] += h[f] * (double)W2[(int64_t)f * d + cc];
     free(h);
 }
 

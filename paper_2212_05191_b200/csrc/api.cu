@@ -460,7 +460,7 @@ extern "C" smile_status smile_expert_ffn(smile_ctx c, const void *X, const int32
     f.V = c->sz.V; f.S = c->sz.S; f.e = c->shape.e; f.Cseg = c->sz.Cseg; f.d = c->shape.d; f.d_ff = c->shape.d_ff;
     f.bf16 = c->shape.dtype == SMILE_BF16; f.num_sms = c->num_sms;
     int impl = c->shape.ffn_impl;
-    if (impl == SMILE_FFN_AUTO) impl = SMILE_FFN_SIMT;   // TODO(tcgen05): bf16 -> SMILE_FFN_TCGEN05
+    if (impl == SMILE_FFN_AUTO) impl = f.bf16 ? SMILE_FFN_TCGEN05 : SMILE_FFN_SIMT;
     if (impl == SMILE_FFN_TCGEN05) {
         if (!f.bf16) return SMILE_ENOTSUP;
         cudaError_t e = launch_ffn_tcgen05(f, S(stream));

@@ -19,7 +19,7 @@ _lib = None
 BILEVEL, FLAT = 0, 1
 FP32, BF16 = 0, 1
 FFN_AUTO, FFN_SIMT, FFN_TCGEN05 = 0, 1, 2
-TCGEN05_DEFAULT = False   # AUTO resolves bf16 to the tcgen05 FFN (api.cu smile_expert_ffn)
+TCGEN05_DEFAULT = True    # AUTO resolves bf16 to the tcgen05 FFN (api.cu smile_expert_ffn)
 _STATUS = {0: "ok", 1: "invalid argument", 2: "shape or layout mismatch", 3: "non-finite router logit",
            4: "CUDA error", 5: "NCCL error", 6: "unsupported configuration", 7: "routing index out of range"}
 
