@@ -111,6 +111,22 @@ smile_status smile_plan(const smile_shape *shape, smile_sizes *out);
  * member count is returned through *count.  P:L148, R10. */
 smile_status smile_group(const smile_shape *shape, int32_t level, int32_t r, int32_t *members,
                          int32_t *count);
+/* Pure host: the point-to-point schedule smile_all2all posts for the pairs of `level`
+ * whose two ranks live in different processes, for process shape->proc.  ops[] receives
+ * every send (ordered by source rank, then destination rank) followed by every receive
+ * (same order), so two processes list their common transfers in the same order, which is
+ * how NCCL matches them inside one ncclGroupStart/End.  `chunk` indexes the caller's
+ * [V, P] chunk array (send side: the chunk sent; receive side: where it lands).  Pairs
+ * inside this process are device copies and are not listed.  count = #ops written
+ * (SMILE_ESHAPE when more than `cap`). */
+typedef struct {
+    int32_t kind;        /* 0 = send, 1 = receive */
+    int32_t peer_proc;   /* the other process */
+    int32_t src, dst;    /* global ranks of the transfer */
+    int32_t chunk;       /* v * P + p in this process's send / receive buffer */
+} smile_xop;
+smile_status smile_exchange_plan(const smile_shape *shape, int32_t level, smile_xop *ops, int32_t cap,
+                                 int32_t *count);
 /* 128-byte NCCL unique id, to be broadcast by the caller (e.g. torch.distributed) from
  * process 0 before smile_create when nprocs > 1. */
 smile_status smile_get_unique_id(uint8_t out[128]);

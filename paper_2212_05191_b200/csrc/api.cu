@@ -162,6 +162,45 @@ extern "C" smile_status smile_group(const smile_shape *shape, int32_t level, int
     return SMILE_OK;
 }
 
+// Remote transfers of one level for process shape->proc (see smile.h).
+static void exchange_ops(const smile_shape *sh, int level, std::vector<smile_xop> &out) {
+    const int G = sh->n * sh->m, V = G / sh->nprocs, rank0 = sh->proc * V;
+    std::vector<int> mem;
+    std::vector<smile_xop> sends, recvs;
+    for (int v = 0; v < V; ++v) {
+        int mp = 0;
+        group_of(sh->n, sh->m, level, rank0 + v, mem, &mp);
+        const int P = (int)mem.size();
+        for (int p = 0; p < P; ++p) {
+            const int q = mem[p];
+            if (q / V == sh->proc) continue;                     // same process: device copy
+            // chunk p of rank v goes to member q, which files it under our position mp;
+            // q's chunk at position mp comes back into our chunk p (the level is an involution)
+            sends.push_back({0, q / V, rank0 + v, q, v * P + p});
+            recvs.push_back({1, q / V, q, rank0 + v, v * P + p});
+        }
+    }
+    auto by_pair = [](const smile_xop &a, const smile_xop &b) { return a.src != b.src ? a.src < b.src : a.dst < b.dst; };
+    std::sort(sends.begin(), sends.end(), by_pair);
+    std::sort(recvs.begin(), recvs.end(), by_pair);
+    out = sends;
+    out.insert(out.end(), recvs.begin(), recvs.end());
+}
+
+extern "C" smile_status smile_exchange_plan(const smile_shape *shape, int32_t level, smile_xop *ops, int32_t cap,
+                                            int32_t *count) {
+    if (!shape || !count || level < 0 || level > 2) return SMILE_EINVAL;
+    smile_sizes z;
+    smile_status st = smile_plan(shape, &z);
+    if (st != SMILE_OK) return st;
+    std::vector<smile_xop> v;
+    exchange_ops(shape, level, v);
+    *count = (int32_t)v.size();
+    if ((int32_t)v.size() > cap || (!ops && !v.empty())) return SMILE_ESHAPE;
+    for (size_t i = 0; i < v.size(); ++i) ops[i] = v[i];
+    return SMILE_OK;
+}
+
 extern "C" smile_status smile_get_unique_id(uint8_t out[128]) {
     if (!out) return SMILE_EINVAL;
     ncclUniqueId id;
@@ -404,34 +443,20 @@ extern "C" smile_status smile_all2all(smile_ctx c, int32_t level, int32_t revers
         return SMILE_OK;
     }
     if (!L.any_remote) return SMILE_OK;
-    // mixed: remote pairs over the world communicator
-    struct Op { int src, dst, v, p; };
-    std::vector<Op> sends, recvs;
-    for (int v = 0; v < V; ++v)
-        for (int p = 0; p < P; ++p) {
-            const int q = L.h_member[v * P + p];
-            const int ql = q - c->sz.rank0;
-            if (ql >= 0 && ql < V) continue;
-            sends.push_back({c->sz.rank0 + v, q, v, p});
-            // q sends its chunk at position pos(v) to v; v receives it at chunk p (= pos(q))
-            recvs.push_back({q, c->sz.rank0 + v, v, p});
-        }
-    auto by_pair = [](const Op &a, const Op &b) { return a.src != b.src ? a.src < b.src : a.dst < b.dst; };
-    std::sort(sends.begin(), sends.end(), by_pair);
-    std::sort(recvs.begin(), recvs.end(), by_pair);
+    // mixed: remote pairs over the world communicator, in smile_exchange_plan order
+    std::vector<smile_xop> ops;
+    exchange_ops(&c->shape, level, ops);
     const int ipp = L.ints_per_peer;
     NCCL_TRY(ncclGroupStart());
-    for (const Op &o : sends) {
-        const int peer = o.dst / V;
-        const size_t ci = (size_t)o.v * P + o.p;
-        NCCL_TRY(ncclSend((const char *)send_rows + ci * chunk, chunk, ncclUint8, peer, c->world, st));
-        if (with_ints) NCCL_TRY(ncclSend(send_ints + ci * ipp, ipp, ncclInt32, peer, c->world, st));
-    }
-    for (const Op &o : recvs) {
-        const int peer = o.src / V;
-        const size_t ci = (size_t)o.v * P + o.p;
-        NCCL_TRY(ncclRecv((char *)recv_rows + ci * chunk, chunk, ncclUint8, peer, c->world, st));
-        if (with_ints) NCCL_TRY(ncclRecv(recv_ints + ci * ipp, ipp, ncclInt32, peer, c->world, st));
+    for (const smile_xop &o : ops) {
+        if (o.kind == 0) {
+            NCCL_TRY(ncclSend((const char *)send_rows + (size_t)o.chunk * chunk, chunk, ncclUint8, o.peer_proc,
+                              c->world, st));
+            if (with_ints) NCCL_TRY(ncclSend(send_ints + (size_t)o.chunk * ipp, ipp, ncclInt32, o.peer_proc, c->world, st));
+        } else {
+            NCCL_TRY(ncclRecv((char *)recv_rows + (size_t)o.chunk * chunk, chunk, ncclUint8, o.peer_proc, c->world, st));
+            if (with_ints) NCCL_TRY(ncclRecv(recv_ints + (size_t)o.chunk * ipp, ipp, ncclInt32, o.peer_proc, c->world, st));
+        }
     }
     NCCL_TRY(ncclGroupEnd());
     return SMILE_OK;

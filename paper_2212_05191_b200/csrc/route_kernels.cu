@@ -68,6 +68,88 @@ __device__ __forceinline__ void warp_zero_row(int4 *dst, int nvec, int lane) {
     for (int i = lane; i < nvec; i += 32) dst[i] = z;
 }
 
+// a1: fused router for one block's tokens.  One warp computes RT tokens at a time: each
+// lane loads 16-byte chunks of the RT rows of x, multiplies them with the matching
+// chunk of every router row (fp32, staged in smem when KW*d*4 <= kRouterSmem), and the
+// partial dot products are reduced with a butterfly (fixed order: deterministic).
+constexpr int kRT = 4;
+constexpr int kRouterSmem = 48 * 1024;
+
+template <bool BF16>
+__device__ void router_tile(const GateArgs &a, float *s_lg, float *s_w, int64_t tok0, int nt) {
+    constexpr int EPV = BF16 ? 8 : 4;          // elements per 16-byte vector
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const int KW = a.KW, d = a.d, nchunk = d / EPV;
+    const bool wsm = (size_t)KW * d * 4 <= (size_t)kRouterSmem;
+    if (wsm) {
+        const float4 *src = reinterpret_cast<const float4 *>(a.w);
+        float4 *dst = reinterpret_cast<float4 *>(s_w);
+        for (int i = threadIdx.x; i < KW * d / 4; i += blockDim.x) dst[i] = __ldg(src + i);
+        __syncthreads();
+    }
+    const float *W = wsm ? s_w : a.w;
+    for (int tt0 = w * kRT; tt0 < nt; tt0 += NW * kRT) {
+        for (int k0 = 0; k0 < KW; k0 += 8) {
+            float acc[kRT][8];
+#pragma unroll
+            for (int r = 0; r < kRT; ++r)
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) acc[r][kk] = 0.f;
+            for (int c = lane; c < nchunk; c += 32) {
+                float xv[kRT][EPV];
+#pragma unroll
+                for (int r = 0; r < kRT; ++r) {
+                    if (tt0 + r < nt) {
+                        const int4 u = __ldg(reinterpret_cast<const int4 *>(
+                            static_cast<const char *>(a.x) + ((tok0 + tt0 + r) * d + (int64_t)c * EPV) * (BF16 ? 2 : 4)));
+                        if (BF16) {
+                            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+                            for (int z = 0; z < 4; ++z) {
+                                const float2 f = __bfloat1622float2(h[z]);
+                                xv[r][2 * z] = f.x;
+                                xv[r][2 * z + 1] = f.y;
+                            }
+                        } else {
+                            const float *f = reinterpret_cast<const float *>(&u);
+#pragma unroll
+                            for (int z = 0; z < EPV; ++z) xv[r][z] = f[z];
+                        }
+                    } else {
+#pragma unroll
+                        for (int z = 0; z < EPV; ++z) xv[r][z] = 0.f;
+                    }
+                }
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    if (k0 + kk >= KW) break;
+                    const float *wr = W + (int64_t)(k0 + kk) * d + c * EPV;
+                    float wv[EPV];
+#pragma unroll
+                    for (int z = 0; z < EPV; z += 4) {
+                        const float4 q = wsm ? *reinterpret_cast<const float4 *>(wr + z)
+                                             : __ldg(reinterpret_cast<const float4 *>(wr + z));
+                        wv[z] = q.x; wv[z + 1] = q.y; wv[z + 2] = q.z; wv[z + 3] = q.w;
+                    }
+#pragma unroll
+                    for (int r = 0; r < kRT; ++r)
+#pragma unroll
+                        for (int z = 0; z < EPV; ++z) acc[r][kk] = fmaf(xv[r][z], wv[z], acc[r][kk]);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kRT; ++r)
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    float v = acc[r][kk];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+                    if (lane == 0 && k0 + kk < KW && tt0 + r < nt) s_lg[(tt0 + r) * KW + k0 + kk] = v;
+                }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // a1-a3: level-1 gate.  grid (nblk, V), block TB threads (one token per thread).
 // smem: logits tile [TB][KW] fp32 | s_j [TB] | warp hist [NW][K1] | block hist [K1]
@@ -78,6 +160,7 @@ __global__ void gate1_kernel(GateArgs a) {
     int *s_j = reinterpret_cast<int *>(s_lg + (size_t)a.TB * a.KW);
     int *s_wh = s_j + a.TB;
     int *s_bh = s_wh + (a.TB / 32) * a.K1;
+    float *s_w = reinterpret_cast<float *>(s_bh + ((a.K1 + 3) & ~3));   // [KW, d] when it fits
 
     const int v = blockIdx.y, blk = blockIdx.x, tid = threadIdx.x;
     const int64_t t0 = (int64_t)blk * a.TB;
@@ -89,30 +172,10 @@ __global__ void gate1_kernel(GateArgs a) {
     if (a.logits) {
         const float *src = a.logits + tok0 * KW;
         for (int i = tid; i < nt * KW; i += blockDim.x) s_lg[i] = __ldg(src + i);
+    } else if (a.bf16) {
+        router_tile<true>(a, s_lg, s_w, tok0, nt);
     } else {
-        // Fused router: one warp per token, lanes stride over d, fp32 FMA, butterfly
-        // reduction (fixed order => deterministic).  W is read through L1 (__ldg).
-        const int lane = tid & 31, w = tid >> 5, NW = blockDim.x >> 5;
-        for (int tt = w; tt < nt; tt += NW) {
-            const int64_t xoff = (tok0 + tt) * a.d;
-            for (int k0 = 0; k0 < KW; k0 += 8) {
-                float acc[8];
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) acc[kk] = 0.f;
-                for (int c = lane; c < a.d; c += 32) {
-                    const float xv = load_elem(a.x, xoff + c, a.bf16);
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk)
-                        if (k0 + kk < KW) acc[kk] = fmaf(xv, __ldg(a.w + (int64_t)(k0 + kk) * a.d + c), acc[kk]);
-                }
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    float s = acc[kk];
-                    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-                    if (lane == 0 && k0 + kk < KW) s_lg[tt * KW + k0 + kk] = s;
-                }
-            }
-        }
+        router_tile<false>(a, s_lg, s_w, tok0, nt);
     }
     __syncthreads();
     if (a.logits_out && !a.logits)
@@ -421,10 +484,11 @@ inline int grid_for(int64_t warps_needed, int per_block_warps, int cap) {
 
 void launch_gate1(const GateArgs &a, cudaStream_t st) {
     if (a.T == 0) return;
-    const size_t smem = (size_t)a.TB * a.KW * 4 + (size_t)a.TB * 4 + (size_t)(a.TB / 32) * a.K1 * 4 + (size_t)a.K1 * 4;
+    size_t smem = (size_t)a.TB * a.KW * 4 + (size_t)a.TB * 4 + (size_t)(a.TB / 32) * a.K1 * 4 + (size_t)((a.K1 + 3) & ~3) * 4;
+    if (!a.logits && (size_t)a.KW * a.d * 4 <= (size_t)kRouterSmem) smem += (size_t)a.KW * a.d * 4;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(gate1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(gate1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         attr_set = true;
     }
     gate1_kernel<<<dim3(a.nblk, a.V), a.TB, smem, st>>>(a);

@@ -76,7 +76,7 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.smile_version.restype = C.c_int
         L.smile_strerror.restype = C.c_char_p
-        for name in ("smile_plan", "smile_group", "smile_get_unique_id", "smile_create", "smile_destroy",
+        for name in ("smile_plan", "smile_group", "smile_exchange_plan", "smile_get_unique_id", "smile_create", "smile_destroy",
                      "smile_query", "smile_get_error", "smile_gate_inter", "smile_dispatch", "smile_gate_intra",
                      "smile_all2all", "smile_all2all_inter", "smile_all2all_intra", "smile_expert_ffn",
                      "smile_combine", "smile_aux_loss", "smile_forward_ws", "smile_forward", "smile_forward_host"):
@@ -111,6 +111,22 @@ def group(n: int, m: int, level: int, r: int) -> list[int]:
     cnt = C.c_int32()
     _check(lib().smile_group(C.byref(sh), level, r, buf, C.byref(cnt)), "smile_group")
     return list(buf[: cnt.value])
+
+
+class XOp(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("peer_proc", C.c_int32), ("src", C.c_int32), ("dst", C.c_int32),
+                ("chunk", C.c_int32)]
+
+
+def exchange_plan(level: int, **kw) -> list[tuple]:
+    """Host-only: the (kind, peer_proc, src, dst, chunk) transfers smile_all2all posts
+    for the cross-process pairs of `level` (smile_exchange_plan)."""
+    sh = _shape(**kw)
+    cnt = C.c_int32()
+    lib().smile_exchange_plan(C.byref(sh), level, None, 0, C.byref(cnt))
+    ops = (XOp * max(1, cnt.value))()
+    _check(lib().smile_exchange_plan(C.byref(sh), level, ops, cnt.value, C.byref(cnt)), "smile_exchange_plan")
+    return [(o.kind, o.peer_proc, o.src, o.dst, o.chunk) for o in ops[: cnt.value]]
 
 
 def unique_id() -> bytes:
