@@ -11,8 +11,10 @@
 //               (M = 128, N = BN, K = 16) into a double-buffered TMEM accumulator
 //               (2 x 256 columns) and commits to the empty / tmem_full mbarriers
 //   warp 2      TMEM allocator (512 columns)
-//   warps 4-7   epilogue: tcgen05.ld 32x32b -> +bias -> GELU -> bf16 -> masked global
-//               stores of the valid rows only; releases the accumulator buffer
+//   warps 4-11  epilogue: two warps per TMEM lane quadrant, each on half of the columns:
+//               tcgen05.ld 32x32b -> +bias -> GELU -> bf16 -> a 32x32 box in smem ->
+//               TMA tensor store (partial boxes at a segment's end: masked st.global of
+//               the valid rows only); the 8 warps release the accumulator buffer
 //
 // Work list: tiles of 128 rows of one segment x BN columns, enumerated on the device
 // from the segment counts (tiles.cuh), n fastest so the CTAs running concurrently share
@@ -25,10 +27,13 @@
 namespace smile {
 namespace {
 
-constexpr int BM = 128, BK = 64, STAGES = 4, NTHREADS = 256, MAXSEG = 4096;
+constexpr int BM = 128, BK = 64, STAGES = 4, MAXSEG = 1024;
+constexpr int EPI_WARPS = 8;                  // 2 warps per TMEM lane quadrant, split by columns
+constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
 constexpr int B_BYTES_MAX = 256 * BK * 2;     // 32 KB
 constexpr int ACC_COLS = 256;                 // TMEM columns per accumulator buffer
+constexpr int OUT_BOX_BYTES = 32 * 32 * 2;    // per epilogue warp: 32 rows x 32 bf16 staged for a TMA store
 
 struct TcArgs {
     const float *bias;       // [NE, N]
@@ -130,8 +135,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// GELU(z) = z Phi(z) = 0.5 z + 0.5 |z| erf(|z| / sqrt 2) (R21, erf form).  erf by Abramowitz &
+// Stegun 7.1.28, 1 - (1 + a1 x + ... + a6 x^6)^-16: |error| <= 1.8e-6 on erf and 8.8e-7 on GELU
+// over all z (checked against scipy in fp32 emulation), ~14 instructions with one
+// MUFU reciprocal instead of erff's ~30 -- the bf16 H it feeds has a half-ulp of >= 2^-9 |H|.
 __device__ __forceinline__ float gelu_erf(float z) {
-    return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f));   // R21: exact erf GELU
+    const float ax = fabsf(z) * 0.70710678118654752f;
+    float p = 4.30638e-5f;
+    p = fmaf(p, ax, 2.765672e-4f);
+    p = fmaf(p, ax, 1.520143e-4f);
+    p = fmaf(p, ax, 9.2705272e-3f);
+    p = fmaf(p, ax, 4.22820123e-2f);
+    p = fmaf(p, ax, 7.05230784e-2f);
+    p = fmaf(p, ax, 1.0f);
+    p = p * p;
+    p = p * p;
+    p = p * p;
+    p = p * p;
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p));
+    return fmaf(0.5f * fabsf(z), 1.0f - r, 0.5f * z);
 }
 
 struct TileInfo {
@@ -155,13 +178,15 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1)
-ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcArgs a) {
+ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                 const __grid_constant__ CUtensorMap mapD, TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte aligned carve-up: [A stages][B stages][barriers][tmem holder][prefix]
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;
     unsigned char *sB = sA + STAGES * A_BYTES;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + STAGES * B_BYTES_MAX);
+    unsigned char *sOut = sB + STAGES * B_BYTES_MAX;                 // EPI_WARPS x 2 KB
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sOut + EPI_WARPS * OUT_BOX_BYTES);
     uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
     int *s_warp = reinterpret_cast<int *>(tmem_holder + 4);
@@ -175,13 +200,14 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&tfull[s]), 1);
-            mbar_init(smem_u32(&tempty[s]), 4);
+            mbar_init(smem_u32(&tempty[s]), EPI_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapD)) : "memory");
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
@@ -241,9 +267,12 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             }
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue: 4 warps = 128 TMEM lanes = 128 rows ----------------
-        const int q = warp & 3;               // TMEM lane quadrant of this warp
+        // ---------------- epilogue: 8 warps; quadrant q = rows 32q..32q+31 ----------------
+        const int q = warp & 3;
+        const int half = (warp - 4) >> 2;
         const int row = q * 32 + lane;
+        const int nch = a.BN / 32;
+        const int c_beg = half ? (nch + 1) / 2 : 0, c_end = half ? nch : (nch + 1) / 2;
         int it = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
             const TileInfo t = tile_info(a, s_pref, tile, ntn);
@@ -251,22 +280,42 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS;
-            const float *bias = a.bias + t.expert * a.N + (int64_t)t.nt * a.BN;
+            const float4 *bias4 = reinterpret_cast<const float4 *>(a.bias + t.expert * a.N + (int64_t)t.nt * a.BN);
             __nv_bfloat16 *drow = a.D + (t.d_row + row) * (int64_t)a.N + (int64_t)t.nt * a.BN;
-            for (int c = 0; c < a.BN / 32; ++c) {
+            unsigned char *box = sOut + (warp - 4) * OUT_BOX_BYTES;
+            const bool full_box = q * 32 + 32 <= t.rows;
+            for (int c = c_beg; c < c_end; ++c) {
                 float v[32];
                 tmem_ld32(tbase + c * 32, v);
-                if (row < t.rows) {
-                    uint4 pk[4];
-                    uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
+                uint4 pk[4];
+                uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        float y0 = v[2 * i] + __ldg(bias + c * 32 + 2 * i);
-                        float y1 = v[2 * i + 1] + __ldg(bias + c * 32 + 2 * i + 1);
-                        if (a.gelu) { y0 = gelu_erf(y0); y1 = gelu_erf(y1); }
-                        __nv_bfloat162 h = __floats2bfloat162_rn(y0, y1);
-                        pw[i] = *reinterpret_cast<uint32_t *>(&h);
+                for (int i4 = 0; i4 < 8; ++i4) {
+                    const float4 b = __ldg(bias4 + c * 8 + i4);
+                    float y0 = v[4 * i4] + b.x, y1 = v[4 * i4 + 1] + b.y;
+                    float y2 = v[4 * i4 + 2] + b.z, y3 = v[4 * i4 + 3] + b.w;
+                    if (a.gelu) { y0 = gelu_erf(y0); y1 = gelu_erf(y1); y2 = gelu_erf(y2); y3 = gelu_erf(y3); }
+                    __nv_bfloat162 h0 = __floats2bfloat162_rn(y0, y1), h1 = __floats2bfloat162_rn(y2, y3);
+                    pw[2 * i4] = *reinterpret_cast<uint32_t *>(&h0);
+                    pw[2 * i4 + 1] = *reinterpret_cast<uint32_t *>(&h1);
+                }
+                if (full_box) {
+                    // stage the 32 x 32 box, then one TMA tensor store (full 64 B row segments)
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+                    uint4 *srow = reinterpret_cast<uint4 *>(box + lane * 64);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) srow[i] = pk[i];
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                         reinterpret_cast<uint64_t>(&mapD)),
+                                     "r"(t.nt * a.BN + c * 32), "r"((int)(t.d_row + q * 32)), "r"(smem_u32(box))
+                                     : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
+                } else if (row < t.rows) {
                     uint4 *dst = reinterpret_cast<uint4 *>(drow + c * 32);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) dst[i] = pk[i];
@@ -277,6 +326,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
         }
     }
+    if (warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
@@ -301,17 +351,18 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 2D bf16 row-major [rows, K] map with a (64 x box_rows) SWIZZLE_128B box.
-bool make_map(CUtensorMap *m, const void *ptr, int64_t rows, int64_t K, int box_rows) {
+// 2D bf16 row-major [rows, K] map with a (box_cols x box_rows) box, SWIZZLE_128B for the
+// 64-column operand boxes, none for the 32 x 32 output boxes.
+bool make_map(CUtensorMap *m, const void *ptr, int64_t rows, int64_t K, int box_rows, int box_cols = BK) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+              CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == BK ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int pick_bn(int N) {
@@ -321,15 +372,17 @@ int pick_bn(int N) {
 }
 
 size_t smem_bytes() {
-    return 1024 + STAGES * (A_BYTES + B_BYTES_MAX) + (2 * STAGES + 4) * 8 + 16 + 32 * 4 + (MAXSEG + 1) * 4;
+    return 1024 + STAGES * (A_BYTES + B_BYTES_MAX) + EPI_WARPS * OUT_BOX_BYTES + (2 * STAGES + 4) * 8 + 16 + 32 * 4 +
+           (MAXSEG + 1) * 4;
 }
 
 cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE, const float *bias, void *D,
                         const FfnArgs &f, int N, int K, int gelu, cudaStream_t st) {
     const int BN = pick_bn(N);
-    CUtensorMap mA, mB;
+    CUtensorMap mA, mB, mD;
     if (!make_map(&mA, A, rows_total, K, BM)) return cudaErrorNotSupported;
     if (!make_map(&mB, B, (int64_t)NE * N, K, BN)) return cudaErrorNotSupported;
+    if (!make_map(&mD, D, rows_total, N, 32, 32)) return cudaErrorNotSupported;
     TcArgs a;
     a.bias = bias; a.D = reinterpret_cast<__nv_bfloat16 *>(D); a.counts = f.counts;
     a.nseg = f.V * f.S * f.e; a.e = f.e; a.S = f.S; a.Cseg = f.Cseg; a.N = N; a.K = K; a.BN = BN; a.gelu = gelu;
@@ -340,7 +393,7 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
         cudaFuncSetAttribute(ffn_gemm_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    ffn_gemm_tcgen05<<<f.num_sms, NTHREADS, smem, st>>>(mA, mB, a);
+    ffn_gemm_tcgen05<<<f.num_sms, NTHREADS, smem, st>>>(mA, mB, mD, a);
     return cudaGetLastError();
 }
 

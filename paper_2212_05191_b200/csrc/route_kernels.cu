@@ -239,31 +239,68 @@ __global__ void gate1_kernel(GateArgs a) {
     }
 }
 
+// Warp-wide exclusive scan over n ints at stride `st` (in place), returns the total.
+__device__ int warp_exclusive_scan(const int32_t *p, int n, int64_t st, int32_t *out_excl) {
+    const int lane = threadIdx.x & 31;
+    int carry = 0;
+    for (int b0 = 0; b0 < n; b0 += 32) {
+        const int i = b0 + lane;
+        const int v = i < n ? p[(int64_t)i * st] : 0;
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        if (i < n) out_excl[(int64_t)i * st] = carry + x - v;
+        carry += __shfl_sync(kFull, x, 31);
+    }
+    return carry;
+}
+
+// Warp-wide fixed-order (lane-strided, then butterfly) fp64 / int sums: deterministic.
+__device__ double warp_sum_f64(const double *p, int n, int64_t st) {
+    const int lane = threadIdx.x & 31;
+    double acc = 0.0;
+    for (int i = lane; i < n; i += 32) acc += p[(int64_t)i * st];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    return acc;
+}
+__device__ int warp_sum_i32(const int32_t *p, int n, int64_t st) {
+    const int lane = threadIdx.x & 31;
+    int acc = 0;
+    for (int i = lane; i < n; i += 32) acc += p[(int64_t)i * st];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    return acc;
+}
+
 // Level-1 scan: per rank, exclusive prefix over blocks of each destination's count;
 // totals -> hist1, counts1 = min(hist1, C1); stats reduced over blocks in fixed order.
+// One warp per (destination or statistic), grid = V.
 __global__ void scan1_kernel(Scan1Args a) {
-    const int v = blockIdx.x;
+    const int v = blockIdx.x, w = threadIdx.x >> 5, NW = blockDim.x >> 5, lane = threadIdx.x & 31;
     const int KS = a.K1 + a.K2;
-    for (int k = threadIdx.x; k < a.K1; k += blockDim.x) {
-        int acc = 0;
-        for (int b = 0; b < a.nblk; ++b) {
-            const int64_t o = ((int64_t)v * a.nblk + b) * a.K1 + k;
-            a.blk_off1[o] = acc;
-            acc += a.blk_hist1[o];
+    const int jobs = a.K1 + KS + a.K2;
+    for (int j = w; j < jobs; j += NW) {
+        if (j < a.K1) {
+            const int k = j;
+            const int64_t o = (int64_t)v * a.nblk * a.K1 + k;
+            const int tot = warp_exclusive_scan(a.blk_hist1 + o, a.nblk, a.K1, a.blk_off1 + o);
+            if (lane == 0) {
+                a.stats.hist1[v * a.K1 + k] = tot;
+                a.counts1[v * a.K1 + k] = (int32_t)imin64(tot, a.C1);
+            }
+        } else if (j < a.K1 + KS) {
+            const int k = j - a.K1;
+            const double sum = warp_sum_f64(a.blk_psum + (int64_t)v * a.nblk * KS + k, a.nblk, KS);
+            if (lane == 0) {
+                if (k < a.K1) a.stats.psum1[v * a.K1 + k] = sum;
+                else a.stats.psum2[v * a.K2 + (k - a.K1)] = sum;
+            }
+        } else {
+            const int k = j - a.K1 - KS;
+            const int c = warp_sum_i32(a.blk_hist2a + (int64_t)v * a.nblk * a.K2 + k, a.nblk, a.K2);
+            if (lane == 0) a.stats.hist2[v * a.K2 + k] = c;
         }
-        a.stats.hist1[v * a.K1 + k] = acc;
-        a.counts1[v * a.K1 + k] = (int32_t)imin64(acc, a.C1);
-    }
-    for (int k = threadIdx.x; k < KS; k += blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < a.nblk; ++b) s += a.blk_psum[((int64_t)v * a.nblk + b) * KS + k];
-        if (k < a.K1) a.stats.psum1[v * a.K1 + k] = s;
-        else a.stats.psum2[v * a.K2 + (k - a.K1)] = s;
-    }
-    for (int k = threadIdx.x; k < a.K2; k += blockDim.x) {
-        int c = 0;
-        for (int b = 0; b < a.nblk; ++b) c += a.blk_hist2a[((int64_t)v * a.nblk + b) * a.K2 + k];
-        a.stats.hist2[v * a.K2 + k] = c;
     }
 }
 
@@ -286,142 +323,170 @@ __global__ void rank2_kernel(Rank2Args a) {
 }
 
 __global__ void scan2_kernel(Rank2Args a) {
-    const int v = blockIdx.x;
-    for (int k = threadIdx.x; k < a.K2; k += blockDim.x) {
-        int acc = 0;
-        for (int b = 0; b < a.nblk; ++b) {
-            const int64_t o = ((int64_t)v * a.nblk + b) * a.K2 + k;
-            a.blk_off2[o] = acc;
-            acc += a.blk_hist2[o];
-        }
-        a.counts2[v * a.K2 + k] = (int32_t)imin64(acc, a.C2);
+    const int v = blockIdx.x, w = threadIdx.x >> 5, NW = blockDim.x >> 5, lane = threadIdx.x & 31;
+    for (int k = w; k < a.K2; k += NW) {
+        const int64_t o = (int64_t)v * a.nblk * a.K2 + k;
+        const int tot = warp_exclusive_scan(a.blk_hist2 + o, a.nblk, a.K2, a.blk_off2 + o);
+        if (lane == 0) a.counts2[v * a.K2 + k] = (int32_t)imin64(tot, a.C2);
     }
 }
 
-// a4: level-1 permute.  One warp per token: slot1 = block offset + block-local rank;
-// kept rows are copied to send[v, i, slot1] with 16-byte vectors; meta = j.
-// The same launch fills meta = -1 for the empty slots [counts1[i], C1).
-__global__ void dispatch1_kernel(Dispatch1Args a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int nvec = (int)(a.rowbytes / 16);
-    const int64_t total = (int64_t)a.V * a.T;
-    for (int64_t g = gw; g < total; g += warps) {
+// Row movers (a4, a7, a11, a13) on the TMA bulk-copy engine.  Per batch of R rows the
+// block's threads resolve each row's source / destination (and the slot bookkeeping);
+// one thread then moves the rows with cp.async.bulk (global -> shared, completion on an
+// mbarrier) and cp.async.bulk (shared -> global, bulk groups), double-buffered so the
+// loads of batch b+1 are in flight while batch b is stored.  Rows that must be zero, or
+// scaled by the gate (a13), are rewritten in shared memory by the threads in between.
+enum MoveKind { MOVE_DISPATCH1 = 0, MOVE_DISPATCH2 = 1, MOVE_COMBINE2 = 2, MOVE_COMBINE1 = 3 };
+
+struct MoveArgs {
+    int kind;
+    int64_t rows;            // total rows (V * items)
+    int64_t rowbytes;
+    int R;                   // rows per batch
+    Dispatch1Args d1;
+    Dispatch2Args d2;
+    Combine2Args c2;
+    Combine1Args c1;
+};
+
+struct RowPlan {
+    const char *src;         // nullptr: zero row
+    char *dst;               // nullptr: nothing to store
+    float scale;             // != 1: multiply (combine1)
+};
+
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
+    RowPlan r{nullptr, nullptr, 1.f};
+    if (m.kind == MOVE_DISPATCH1) {
+        const Dispatch1Args &a = m.d1;
         const int v = (int)(g / a.T);
         const int64_t t = g - (int64_t)v * a.T;
         const int i = a.route.dest1[g];
-        const int blk = (int)(t / a.TB);
-        const int slot = a.blk_off1[((int64_t)v * a.nblk + blk) * a.K1 + i] + a.route.slot1[g];
-        __syncwarp();
-        if (lane == 0) a.route.slot1[g] = slot;
+        const int slot = a.blk_off1[((int64_t)v * a.nblk + t / a.TB) * a.K1 + i] + a.route.slot1[g];
+        a.route.slot1[g] = slot;                                      // finalise (R5, R8)
         if (slot < a.C1) {
             const int64_t dst_row = ((int64_t)v * a.K1 + i) * a.C1 + slot;
-            warp_copy_row(reinterpret_cast<int4 *>(static_cast<char *>(a.send) + dst_row * a.rowbytes),
-                          reinterpret_cast<const int4 *>(static_cast<const char *>(a.x) + g * a.rowbytes),
-                          nvec, lane);
-            if (a.meta && lane == 0) a.meta[dst_row] = a.route.dest2[g];
+            r.src = static_cast<const char *>(a.x) + g * a.rowbytes;
+            r.dst = static_cast<char *>(a.send) + dst_row * a.rowbytes;
+            if (a.meta) a.meta[dst_row] = a.route.dest2[g];
         }
-    }
-    if (a.meta) {
-        const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-        const int64_t tot = (int64_t)a.V * a.K1 * a.C1;
-        for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot; idx += nthr) {
-            const int64_t vi = idx / a.C1, c = idx - vi * a.C1;   // vi = v*K1 + i
-            const int64_t v = vi / a.K1, i = vi - v * a.K1;
-            const int64_t last = ((v * a.nblk) + a.nblk - 1) * a.K1 + i;   // total = off + hist of the last block
-            if (c >= (int64_t)a.blk_off1[last] + a.blk_hist1[last]) a.meta[idx] = -1;
-        }
-    }
-}
-
-// a7: level-2 permute at the intermediate.  One warp per received slot (s, c) with a
-// valid j: slot2 = block offset + block-local rank; kept rows go to send2[v, j, slot2].
-__global__ void dispatch2_kernel(Dispatch2Args a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int nvec = (int)(a.rowbytes / 16);
-    const int64_t total = (int64_t)a.V * a.items;
-    for (int64_t g = gw; g < total; g += warps) {
+    } else if (m.kind == MOVE_DISPATCH2) {
+        const Dispatch2Args &a = m.d2;
         const int j = a.recv_meta[g];
-        if (j < 0 || j >= a.K2) continue;
-        const int v = (int)(g / a.items);
-        const int64_t x = g - (int64_t)v * a.items;
-        const int blk = (int)(x / kRank2Items);
-        const int slot = a.blk_off2[((int64_t)v * a.nblk + blk) * a.K2 + j] + a.slot2[g];
-        __syncwarp();
-        if (lane == 0) a.slot2[g] = slot;
-        if (slot < a.C2) {
-            const int64_t dst_row = ((int64_t)v * a.K2 + j) * a.C2 + slot;
-            warp_copy_row(reinterpret_cast<int4 *>(static_cast<char *>(a.send2) + dst_row * a.rowbytes),
-                          reinterpret_cast<const int4 *>(static_cast<const char *>(a.recv1) + g * a.rowbytes),
-                          nvec, lane);
+        if (j >= 0 && j < a.K2) {
+            const int v = (int)(g / a.items);
+            const int64_t x = g - (int64_t)v * a.items;
+            const int slot = a.blk_off2[((int64_t)v * a.nblk + x / kRank2Items) * a.K2 + j] + a.slot2[g];
+            a.slot2[g] = slot;
+            if (slot < a.C2) {
+                r.src = static_cast<const char *>(a.recv1) + g * a.rowbytes;
+                r.dst = static_cast<char *>(a.send2) + (((int64_t)v * a.K2 + j) * a.C2 + slot) * a.rowbytes;
+            }
         }
-    }
-}
-
-// a11: level-2 un-permute: ret1[s, c] = keep2 ? ret2[j, slot2] : 0 for valid slots.
-__global__ void combine2_kernel(Combine2Args a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int nvec = (int)(a.rowbytes / 16);
-    const int64_t total = (int64_t)a.V * a.items;
-    for (int64_t g = gw; g < total; g += warps) {
+    } else if (m.kind == MOVE_COMBINE2) {
+        const Combine2Args &a = m.c2;
         const int j = a.recv_meta[g];
-        if (j < 0 || j >= a.K2) continue;
-        const int v = (int)(g / a.items);
-        const int s2 = a.slot2[g];
-        int4 *dst = reinterpret_cast<int4 *>(static_cast<char *>(a.ret1) + g * a.rowbytes);
-        if (s2 < a.C2) {
-            const int64_t src_row = ((int64_t)v * a.K2 + j) * a.C2 + s2;
-            warp_copy_row(dst, reinterpret_cast<const int4 *>(static_cast<const char *>(a.ret2) + src_row * a.rowbytes),
-                          nvec, lane);
-        } else {
-            warp_zero_row(dst, nvec, lane);
+        if (j >= 0 && j < a.K2) {
+            const int v = (int)(g / a.items);
+            const int s2 = a.slot2[g];
+            r.dst = static_cast<char *>(a.ret1) + g * a.rowbytes;
+            if (s2 < a.C2) r.src = static_cast<const char *>(a.ret2) + (((int64_t)v * a.K2 + j) * a.C2 + s2) * a.rowbytes;
         }
-    }
-}
-
-// a13: level-1 combine (Eq. 3): out[t] = keep1 ? dtype(gate * back1[i, slot1]) : 0.
-template <bool BF16>
-__global__ void combine1_kernel(Combine1Args a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    constexpr int kPer = BF16 ? 8 : 4;             // elements per 16-byte vector
-    const int nvec = a.d / kPer;
-    const int64_t total = (int64_t)a.V * a.T;
-    for (int64_t g = gw; g < total; g += warps) {
+    } else {
+        const Combine1Args &a = m.c1;
+        const int64_t rb = m.rowbytes;
         const int v = (int)(g / a.T);
         const int i = a.route.dest1[g];
         const int s1 = a.route.slot1[g];
-        int4 *dst = reinterpret_cast<int4 *>(static_cast<char *>(a.out) + g * (int64_t)a.d * (BF16 ? 2 : 4));
+        r.dst = static_cast<char *>(a.out) + g * rb;
         if (s1 < a.C1) {
-            const float gt = a.route.gate[g];
-            const int64_t src_row = ((int64_t)v * a.K1 + i) * a.C1 + s1;
-            const int4 *src = reinterpret_cast<const int4 *>(static_cast<const char *>(a.back1) +
-                                                             src_row * (int64_t)a.d * (BF16 ? 2 : 4));
-            for (int k = lane; k < nvec; k += 32) {
-                int4 u = __ldg(src + k);
-                if (BF16) {
-                    __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
-#pragma unroll
-                    for (int z = 0; z < 4; ++z) {
-                        float2 f = __bfloat1622float2(h[z]);
-                        h[z] = __floats2bfloat162_rn(__fmul_rn(gt, f.x), __fmul_rn(gt, f.y));
-                    }
-                } else {
-                    float *f = reinterpret_cast<float *>(&u);
-#pragma unroll
-                    for (int z = 0; z < 4; ++z) f[z] = __fmul_rn(gt, f[z]);
-                }
-                dst[k] = u;
-            }
+            r.src = static_cast<const char *>(a.back1) + (((int64_t)v * a.K1 + i) * a.C1 + s1) * rb;
+            r.scale = a.route.gate[g];
         } else {
-            warp_zero_row(dst, nvec, lane);
+            r.scale = 0.f;
         }
+    }
+    return r;
+}
+
+constexpr int kMoveThreads = 256;
+constexpr int kMoveRowsPerWarp = 4;     // rows whose metadata 4 lanes resolve in parallel
+constexpr int kMoveColUnroll = 3;       // 16-byte vectors per lane per row in flight
+
+// One warp moves kMoveRowsPerWarp rows at a time: lanes 0..3 resolve one row each
+// (independent dependent-load chains), the pointers are broadcast, then every lane keeps
+// rows x kMoveColUnroll 16-byte loads in flight before its stores.
+__global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nvec = (int)(m.rowbytes / 16);
+    const bool combine1 = m.kind == MOVE_COMBINE1;
+    const bool bf16 = m.c1.bf16 != 0;
+    constexpr int RW = kMoveRowsPerWarp, CU = kMoveColUnroll;
+    for (int64_t g0 = gw * RW; g0 < m.rows; g0 += warps * RW) {
+        RowPlan mine{nullptr, nullptr, 1.f};
+        if (lane < RW && g0 + lane < m.rows) mine = plan_row(m, g0 + lane);
+        const char *src[RW];
+        char *dst[RW];
+        float sc[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+            src[r] = reinterpret_cast<const char *>(__shfl_sync(kFull, reinterpret_cast<unsigned long long>(mine.src), r));
+            dst[r] = reinterpret_cast<char *>(__shfl_sync(kFull, reinterpret_cast<unsigned long long>(mine.dst), r));
+            sc[r] = __shfl_sync(kFull, mine.scale, r);
+        }
+        for (int c0 = lane; c0 < nvec; c0 += 32 * CU) {
+            int4 val[RW][CU];
+#pragma unroll
+            for (int r = 0; r < RW; ++r)
+#pragma unroll
+                for (int u = 0; u < CU; ++u) {
+                    const int c = c0 + 32 * u;
+                    val[r][u] = (dst[r] && src[r] && c < nvec) ? __ldg(reinterpret_cast<const int4 *>(src[r]) + c)
+                                                               : make_int4(0, 0, 0, 0);
+                }
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                if (!dst[r]) continue;
+#pragma unroll
+                for (int u = 0; u < CU; ++u) {
+                    const int c = c0 + 32 * u;
+                    if (c >= nvec) continue;
+                    int4 w = val[r][u];
+                    if (combine1 && sc[r] != 1.f) {
+                        if (bf16) {
+                            __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&w);
+#pragma unroll
+                            for (int z = 0; z < 4; ++z) {
+                                const float2 f = __bfloat1622float2(h[z]);
+                                h[z] = __floats2bfloat162_rn(__fmul_rn(sc[r], f.x), __fmul_rn(sc[r], f.y));
+                            }
+                        } else {
+                            float *f = reinterpret_cast<float *>(&w);
+#pragma unroll
+                            for (int z = 0; z < 4; ++z) f[z] = __fmul_rn(sc[r], f[z]);
+                        }
+                    }
+                    reinterpret_cast<int4 *>(dst[r])[c] = w;
+                }
+            }
+        }
+    }
+}
+
+// dispatch1 also fills meta = -1 for the empty slots [count, C1) of every destination.
+__global__ void meta_fill_kernel(Dispatch1Args a) {
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tot = (int64_t)a.V * a.K1 * a.C1;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot; idx += nthr) {
+        const int64_t vi = idx / a.C1, cc = idx - vi * a.C1;   // vi = v*K1 + i
+        const int64_t v = vi / a.K1, i = vi - v * a.K1;
+        const int64_t last = ((v * a.nblk) + a.nblk - 1) * a.K1 + i;   // total = off + hist of the last block
+        if (cc >= (int64_t)a.blk_off1[last] + a.blk_hist1[last]) a.meta[idx] = -1;
     }
 }
 
@@ -496,35 +561,50 @@ void launch_gate1(const GateArgs &a, cudaStream_t st) {
 
 void launch_scan1(const Scan1Args &a, cudaStream_t st) {
     if (a.T == 0) return;
-    scan1_kernel<<<a.V, 128, 0, st>>>(a);
+    scan1_kernel<<<a.V, 512, 0, st>>>(a);
 }
 
 void launch_rank2(const Rank2Args &a, cudaStream_t st) {
     if (a.items == 0) return;
     rank2_kernel<<<dim3(a.nblk, a.V), kRank2Items, 0, st>>>(a);
-    scan2_kernel<<<a.V, 128, 0, st>>>(a);
+    scan2_kernel<<<a.V, 512, 0, st>>>(a);
+}
+
+static void launch_move(MoveArgs &m, cudaStream_t st) {
+    if (m.rows <= 0) return;
+    const int64_t per_block = (int64_t)(kMoveThreads / 32) * kMoveRowsPerWarp;
+    int64_t grid = (m.rows + per_block - 1) / per_block;
+    if (grid > 148 * 8) grid = 148 * 8;
+    row_move_kernel<<<(int)grid, kMoveThreads, 0, st>>>(m);
 }
 
 void launch_dispatch1(const Dispatch1Args &a, cudaStream_t st) {
     if (a.T == 0) return;
-    dispatch1_kernel<<<grid_for((int64_t)a.V * a.T, 8, 148 * 16), 256, 0, st>>>(a);
+    MoveArgs m{};
+    m.kind = MOVE_DISPATCH1; m.rows = (int64_t)a.V * a.T; m.rowbytes = a.rowbytes; m.d1 = a;
+    launch_move(m, st);
+    if (a.meta) meta_fill_kernel<<<148 * 4, 256, 0, st>>>(a);
 }
 
 void launch_dispatch2(const Dispatch2Args &a, cudaStream_t st) {
     if (a.items == 0) return;
-    dispatch2_kernel<<<grid_for((int64_t)a.V * a.items, 8, 148 * 16), 256, 0, st>>>(a);
+    MoveArgs m{};
+    m.kind = MOVE_DISPATCH2; m.rows = (int64_t)a.V * a.items; m.rowbytes = a.rowbytes; m.d2 = a;
+    launch_move(m, st);
 }
 
 void launch_combine2(const Combine2Args &a, cudaStream_t st) {
     if (a.items == 0) return;
-    combine2_kernel<<<grid_for((int64_t)a.V * a.items, 8, 148 * 16), 256, 0, st>>>(a);
+    MoveArgs m{};
+    m.kind = MOVE_COMBINE2; m.rows = (int64_t)a.V * a.items; m.rowbytes = a.rowbytes; m.c2 = a;
+    launch_move(m, st);
 }
 
 void launch_combine1(const Combine1Args &a, cudaStream_t st) {
     if (a.T == 0) return;
-    const int g = grid_for((int64_t)a.V * a.T, 8, 148 * 16);
-    if (a.bf16) combine1_kernel<true><<<g, 256, 0, st>>>(a);
-    else combine1_kernel<false><<<g, 256, 0, st>>>(a);
+    MoveArgs m{};
+    m.kind = MOVE_COMBINE1; m.rows = (int64_t)a.V * a.T; m.rowbytes = (int64_t)a.d * (a.bf16 ? 2 : 4); m.c1 = a;
+    launch_move(m, st);
 }
 
 void launch_aux(const smile_stats &s, double alpha, double beta, double *loss, int V, int K1, int K2,

@@ -3,5 +3,5 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 timeout 300 python bench.py --steps 30 --warmup 5 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 B="python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --mode bilevel"
 timeout 300 $B > gpurun_out/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu1.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ffn_gemm|gate1|dispatch1|exchange_copy|combine|dispatch2" -s 14 -c 10 -o gpurun_out/prof_r01 $B > gpurun_out/ncu2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ffn_gemm|gate1|bulk_move" -s 12 -c 8 -o gpurun_out/prof_r01c $B > gpurun_out/ncu2.log 2>&1
 echo done

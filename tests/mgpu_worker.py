@@ -1,0 +1,75 @@
+"""torchrun worker for the multi-GPU parity test (tests/test_multigpu.py).
+
+Every process builds the whole seeded problem (synth), runs its V = G/nprocs resident
+ranks through libsmile (NCCL exchanges between processes, device copies inside one),
+and rank 0 gathers every output and compares it with the CPU oracle."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+from harness import Case, assert_close_scaled  # noqa: E402
+from paper_2212_05191_b200 import SmileLayer, smile as smb  # noqa: E402
+
+
+def main():
+    cases = json.loads(sys.argv[1])
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    failures = []
+    for c in cases:
+        case = Case(**c)
+        G, V = case.G, case.G // world
+        r0 = rank * V
+        buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(smb.unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        layer = SmileLayer(case.n, case.m, case.e, case.d, case.d_ff, case.T, case.cf, case.dtype, case.mode,
+                           nprocs=world, proc=rank, device=local, ffn_impl=case.ffn_impl,
+                           nccl_id=bytes(buf.cpu().numpy().tobytes()))
+        g = case.gpu_tensors(dev)
+        e = case.e
+        sl = lambda t, k=1: None if t is None else t[r0 * k:(r0 + V) * k].contiguous()
+        out = torch.empty_like(sl(g["x"]))
+        loss = torch.empty(V, dtype=torch.float64, device=dev)
+        layer.forward(sl(g["x"]), sl(g["W1t"], e), sl(g["b1"], e), sl(g["W2t"], e), sl(g["b2"], e), out, loss,
+                      logits=sl(g["logits"]), w_router=g["w_router"], alpha=case.alpha, beta=case.beta)
+        torch.cuda.synchronize()
+        err = layer.get_error()
+        outs = [torch.empty_like(out) for _ in range(world)]
+        losses = [torch.empty_like(loss) for _ in range(world)]
+        dist.all_gather(outs, out)
+        dist.all_gather(losses, loss)
+        if rank == 0:
+            try:
+                assert err == 0, f"device error {err}"
+                r = case.oracle_route()
+                got = torch.cat(outs).float().cpu().numpy().reshape(-1, case.d)
+                ref = case.oracle_out(r)
+                assert_close_scaled(got, ref, 2e-2 if case.dtype == "bf16" else 1e-5, f"mgpu {c}")
+                keep = r.keep.reshape(-1).astype(bool)
+                assert (got[~keep] == 0).all()
+                np.testing.assert_allclose(torch.cat(losses).cpu().numpy(), r.loss, rtol=1e-6)
+            except AssertionError as ex:
+                failures.append(f"{c}: {ex}")
+        layer.close()
+        dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print("MGPU_RESULT", json.dumps({"failures": failures, "cases": len(cases)}))
+        sys.exit(1 if failures else 0)
+
+
+if __name__ == "__main__":
+    main()
