@@ -46,7 +46,7 @@ METRIC = "MoE-layer tokens/sec (bi-level vs flat All2All) at 1/2/4/8 B200; kerne
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="both", choices=["both", "bilevel", "flat"])
@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay each step as a CUDA graph")
+    ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling period (0 = off)")
     return ap.parse_args()
 
 
@@ -69,26 +70,33 @@ def load_json(path):
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi samples of SM clock and throttle reasons during the timed region."""
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index, self.proc, self.lines = index, None, []
+    def __init__(self, index: int, period_ms: int = 100):
+        self.index, self.proc, self.lines, self.period = index, None, [], period_ms
 
     def start(self):
+        """Start nvidia-smi (writing to a file, no reader thread here) and wait for its first
+        sample: NVML initialisation stalls CUDA work of the process for up to ~1 s, so it
+        must be done before the timed region, never inside it."""
+        import tempfile
         try:
+            self.path = tempfile.mktemp(prefix="smile_clocks_", suffix=".csv")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-            time.sleep(0.15)
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period), "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            t0 = time.time()
+            while time.time() - t0 < 10:
+                if os.path.exists(self.path) and os.path.getsize(self.path) > 0:
+                    break
+                time.sleep(0.05)
+            time.sleep(2 * self.period / 1000.0)
         except Exception:
             self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def mark(self, which: str):
+        setattr(self, which, time.time())
 
     def stop(self):
         if not self.proc:
@@ -99,22 +107,39 @@ class ClockSampler:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
+        try:
+            with open(self.path) as f:
+                self.lines = [ln.strip() for ln in f]
+            os.remove(self.path)
+        except Exception:
+            self.lines = []
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        import datetime
+        t_beg, t_end = getattr(self, "t_beg", 0.0), getattr(self, "t_end", 1e18)
+        rows = []
         for ln in self.lines:
             p = [x.strip() for x in ln.split(",")]
-            if len(p) < 6:
+            if len(p) < 7:
                 continue
             try:
-                sm.append(float(p[0]))
-                mx.append(float(p[1]))
+                ts = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(p[1]), float(p[2]), p[3:7]))
             except ValueError:
                 continue
-            for nm, v in zip(names, p[2:6]):
+        inside = [r for r in rows if t_beg - 0.05 <= r[0] <= t_end + 0.05]
+        window = "timed region"
+        if not inside and rows:           # region shorter than the sampling period: nearest samples
+            inside = sorted(rows, key=lambda r: min(abs(r[0] - t_beg), abs(r[0] - t_end)))[:2]
+            window = "nearest samples to a timed region shorter than the sampling period"
+        for ts, a, b, rs in inside:
+            sm.append(a)
+            mx.append(b)
+            for nm, v in zip(names, rs):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window, "period_ms": self.period}
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -308,6 +333,9 @@ def run_ours(args):
     gen = torch.Generator(device=dev)
     results = {}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    sampler = ClockSampler(local, args.clock_ms) if rank == 0 and args.clock_ms > 0 else None
+    if sampler:
+        sampler.start()
     for mode in modes:
         # the two layers are measured one after the other; the second gets its own id
         if mode != modes[0] and world > 1:
@@ -343,30 +371,33 @@ def run_ours(args):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        clk = ClockSampler(local) if rank == 0 else None
-        if clk:
-            clk.start()
+        t_beg = time.time()
         for k in range(args.steps):
             flush.zero_()                       # L2 flush outside the step's events
             step(L, inp, evs[k])
         torch.cuda.synchronize()
-        clocks = clk.stop() if clk else None
+        t_end = time.time()
         if dist:
             dist.barrier()
         ph = [[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(nph)] for k in range(args.steps)]
         step_ms = [sum(p) for p in ph]
-        tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+        mine = torch.tensor([sum(step_ms) / args.steps] + [statistics.mean(p[i] for p in ph) for i in range(nph)],
+                            dtype=torch.float64, device=dev)
+        allr = [torch.empty_like(mine) for _ in range(world)] if dist else [mine]
         if dist:
-            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-        ms = tot.item() / args.steps
-        phase_ms = {phases[i]: statistics.mean(p[i] for p in ph) for i in range(nph)}
+            dist.all_gather(allr, mine)
+        allr = torch.stack(allr).cpu()
+        ms = allr[:, 0].max().item()                         # max over ranks
+        rank_ms = allr[:, 0].tolist()
+        phase_ms = {phases[i]: allr[:, 1 + i].max().item() for i in range(nph)}
         # algorithmic work of the dominant kernel (expert FFN): 4 * rows * d * d_ff flops
         w = L.view()
         rows = int(w["rcounts"].sum().item())
         kept = rows
         ffn_ms = phase_ms["ffn"]
         ffn_tc = cfgd["dtype"] == "bf16" and args.ffn != "simt" and smb.TCGEN05_DEFAULT
-        res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms, clocks=clocks,
+        res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, rank_ms=rank_ms, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms,
+                   t_beg=t_beg, t_end=t_end,
                    tokens=G * T, launches=launches_per_step(L, world))
         # e2e through smile_forward_host (pinned host x, D2H out + loss)
         if not args.no_e2e:
@@ -395,6 +426,10 @@ def run_ours(args):
                           "ms_per_step": et.item(), "steps": e2e_steps}
         results[mode] = res
         del evs
+    if sampler:
+        main_mode = results[modes[0]]
+        sampler.t_beg, sampler.t_end = main_mode["t_beg"], main_mode["t_end"]
+        results[modes[0]]["clocks"] = sampler.stop()
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -415,7 +450,7 @@ def run_ours(args):
                 "peak_source": "MEASURED_PEAKS.json " + ("bf16_tflops_sustained" if timed_s > 1.0 else "bf16_tflops")}
     else:
         # SIMT FFMA: 148 SMs x 128 lanes x 2 flop x sm clock
-        clk = (main["clocks"] or {}).get("sm_mhz") or 1965.0
+        clk = (main.get("clocks") or {}).get("sm_mhz") or 1965.0
         alu_peak = 148 * 128 * 2 * clk * 1e6 / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                 "frac": achieved / alu_peak, "peak_source": f"148 SM x 128 FP32 lanes x 2 x {clk:.0f} MHz"}
@@ -431,9 +466,10 @@ def run_ours(args):
                                f"e={e}/rank, T={T}/rank, d={d}, d_ff={d_ff}, cf={cfgd['cf']}, fused router; "
                                f"{V} ranks per GPU", "ranks_per_gpu": V, "mode": modes[0],
                    "l2": "flushed (256 MiB write) before every timed step, outside its events"},
-        "phase_ms": main["phase_ms"], "kept_tokens": main["kept"],
+        "phase_ms": main["phase_ms"], "phase_ms_note": "per phase: max over ranks of the mean over steps",
+        "rank_ms_per_step": main["rank_ms"], "kept_tokens": main["kept"],
         "roofline": roof, "gpu_launches": main["launches"] * args.steps,
-        "clocks": main["clocks"],
+        "clocks": main.get("clocks"),
     }
     if "e2e" in main:
         line["e2e"] = main["e2e"]

@@ -436,27 +436,32 @@ extern "C" smile_status smile_all2all(smile_ctx c, int32_t level, int32_t revers
     }
     if (c->shape.nprocs == 1) return SMILE_OK;
     if (nccl_alltoall) {
-        NCCL_TRY(ncclGroupStart());
-        NCCL_TRY(ncclAlltoAll(send_rows, recv_rows, chunk, ncclUint8, L.comm, st));
         if (with_ints) NCCL_TRY(ncclAlltoAll(send_ints, recv_ints, L.ints_per_peer, ncclInt32, L.comm, st));
-        NCCL_TRY(ncclGroupEnd());
+        NCCL_TRY(ncclAlltoAll(send_rows, recv_rows, chunk, ncclUint8, L.comm, st));
         return SMILE_OK;
     }
     if (!L.any_remote) return SMILE_OK;
-    // mixed: remote pairs over the world communicator, in smile_exchange_plan order
+    // mixed: remote pairs over the world communicator, in smile_exchange_plan order.  The
+    // side ints (meta / counts) go in their own group first: interleaving them with the
+    // multi-MB row messages of the same peer pair in one group serialised NCCL's p2p
+    // (measured 8 ms instead of 0.4 ms for the C2 inter exchange on 2 B200).
     std::vector<smile_xop> ops;
     exchange_ops(&c->shape, level, ops);
     const int ipp = L.ints_per_peer;
+    if (with_ints) {
+        NCCL_TRY(ncclGroupStart());
+        for (const smile_xop &o : ops) {
+            if (o.kind == 0) NCCL_TRY(ncclSend(send_ints + (size_t)o.chunk * ipp, ipp, ncclInt32, o.peer_proc, c->world, st));
+            else NCCL_TRY(ncclRecv(recv_ints + (size_t)o.chunk * ipp, ipp, ncclInt32, o.peer_proc, c->world, st));
+        }
+        NCCL_TRY(ncclGroupEnd());
+    }
     NCCL_TRY(ncclGroupStart());
     for (const smile_xop &o : ops) {
-        if (o.kind == 0) {
-            NCCL_TRY(ncclSend((const char *)send_rows + (size_t)o.chunk * chunk, chunk, ncclUint8, o.peer_proc,
-                              c->world, st));
-            if (with_ints) NCCL_TRY(ncclSend(send_ints + (size_t)o.chunk * ipp, ipp, ncclInt32, o.peer_proc, c->world, st));
-        } else {
+        if (o.kind == 0)
+            NCCL_TRY(ncclSend((const char *)send_rows + (size_t)o.chunk * chunk, chunk, ncclUint8, o.peer_proc, c->world, st));
+        else
             NCCL_TRY(ncclRecv((char *)recv_rows + (size_t)o.chunk * chunk, chunk, ncclUint8, o.peer_proc, c->world, st));
-            if (with_ints) NCCL_TRY(ncclRecv(recv_ints + (size_t)o.chunk * ipp, ipp, ncclInt32, o.peer_proc, c->world, st));
-        }
     }
     NCCL_TRY(ncclGroupEnd());
     return SMILE_OK;

@@ -154,7 +154,7 @@ __device__ void router_tile(const GateArgs &a, float *s_lg, float *s_w, int64_t 
 // a1-a3: level-1 gate.  grid (nblk, V), block TB threads (one token per thread).
 // smem: logits tile [TB][KW] fp32 | s_j [TB] | warp hist [NW][K1] | block hist [K1]
 // ---------------------------------------------------------------------------------
-__global__ void gate1_kernel(GateArgs a) {
+__global__ void __launch_bounds__(256, 3) gate1_kernel(GateArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *s_lg = reinterpret_cast<float *>(smem_raw);
     int *s_j = reinterpret_cast<int *>(s_lg + (size_t)a.TB * a.KW);
@@ -225,17 +225,23 @@ __global__ void gate1_kernel(GateArgs a) {
     if (tid < nt) a.route.slot1[tok0 + tid] = lr;
     const int64_t bo = (int64_t)v * a.nblk + blk;
     for (int k = tid; k < K1; k += blockDim.x) a.blk_hist1[bo * K1 + k] = s_bh[k];
-    // LB statistics partials, summed over the block's tokens in token order (fp64).
-    for (int k = tid; k < KW; k += blockDim.x) {
-        double acc = 0.0;
-        for (int tt = 0; tt < nt; ++tt) acc += (double)s_lg[tt * KW + k];
-        a.blk_psum[bo * (K1 + K2) + k] = acc;
-    }
-    if (a.flat && tid == 0) a.blk_psum[bo * (K1 + K2) + K1] = (double)nt;
-    for (int k = tid; k < K2; k += blockDim.x) {
-        int c = 0;
-        for (int tt = 0; tt < nt; ++tt) c += (s_j[tt] == k);
-        a.blk_hist2a[bo * K2 + k] = c;
+    // LB statistics partials of the block (fp64 for the probability sums): one warp per
+    // statistic, lanes stride over tokens, fixed butterfly order => deterministic.
+    {
+        const int lane = tid & 31, w = tid >> 5, NW = blockDim.x >> 5;
+        for (int k = w; k < KW; k += NW) {
+            double acc = 0.0;
+            for (int tt = lane; tt < nt; tt += 32) acc += (double)s_lg[tt * KW + k];
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+            if (lane == 0) a.blk_psum[bo * (K1 + K2) + k] = acc;
+        }
+        for (int k = w; k < K2; k += NW) {
+            int c = 0;
+            for (int tt = lane; tt < nt; tt += 32) c += (s_j[tt] == k);
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+            if (lane == 0) a.blk_hist2a[bo * K2 + k] = c;
+        }
+        if (a.flat && tid == 0) a.blk_psum[bo * (K1 + K2) + K1] = (double)nt;
     }
 }
 
