@@ -62,6 +62,10 @@ def lib():
         _lib.oracle_ffn_row.argtypes = [C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]
         _lib.oracle_out_rows.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32, _P, C.POINTER(_Route),
                                          _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]
+        _lib.oracle_objective.restype = C.c_double
+        _lib.oracle_objective.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32] + [_P] * 8 + [C.c_double, _P, _P]
+        _lib.oracle_backward.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32, _P, _P, _P, C.POINTER(_Route),
+                                         _P, _P, _P, _P, _P, C.c_double] + [_P] * 7
     return _lib
 
 
@@ -174,4 +178,40 @@ def out_rows(cfg: Config, r: Route, x: np.ndarray, W1=None, b1=None, W2=None, b2
     out = np.empty((rows.shape[0], d), np.float64)
     lib().oracle_out_rows(C.byref(cfg._c()), d, d_ff, _ptr(x), C.byref(r._s), _ptr(W1), _ptr(b1),
                           _ptr(W2), _ptr(b2), int(identity), rows.shape[0], _ptr(rows), _ptr(out))
+    return out
+
+
+def _ptr_or_none(a):
+    return None if a is None else _ptr(a)
+
+
+def objective(cfg: Config, x, W1, b1, W2, b2, gout, lam=1.0, W=None, logits=None):
+    """fp64 objective J = sum <gout, OUT> + lam * sum_r loss_r (smile_oracle.c).  Arrays are
+    taken as fp64 (x [G,T,d]; W [KW,d] or logits [G,T,KW]).  Returns (J, keep, dest)."""
+    f = lambda a: None if a is None else np.ascontiguousarray(a, np.float64)
+    x, W1, b1, W2, b2, gout, W, logits = map(f, (x, W1, b1, W2, b2, gout, W, logits))
+    keep = np.zeros(cfg.G * cfg.T, np.uint8)
+    dest = np.zeros(cfg.G * cfg.T * 2, np.int32)
+    J = lib().oracle_objective(C.byref(cfg._c()), x.shape[-1], W1.shape[-1], _ptr(x), _ptr_or_none(W),
+                               _ptr_or_none(logits), _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2), _ptr(gout), lam,
+                               _ptr(keep), _ptr(dest))
+    return J, keep, dest
+
+
+def backward(cfg: Config, r: Route, x, W1, b1, W2, b2, gout, lam=1.0, W=None, logits=None):
+    """Gradients of the objective (smile_oracle.c oracle_backward), fp64.  Returns a dict
+    with dlogits [G,T,KW], dx [G,T,d], dW [KW,d] (None without W), dW1, db1, dW2, db2."""
+    f = lambda a: None if a is None else np.ascontiguousarray(a, np.float32)
+    x, W1, b1, W2, b2, gout, W, logits = map(f, (x, W1, b1, W2, b2, gout, W, logits))
+    G, T, d = x.shape
+    d_ff = W1.shape[-1]
+    NE = W1.shape[0]
+    KW = cfg.logit_width
+    out = dict(dlogits=np.zeros((G, T, KW)), dx=np.zeros((G, T, d)), dW=None if W is None else np.zeros((KW, d)),
+               dW1=np.zeros((NE, d, d_ff)), db1=np.zeros((NE, d_ff)), dW2=np.zeros((NE, d_ff, d)),
+               db2=np.zeros((NE, d)))
+    lib().oracle_backward(C.byref(cfg._c()), d, d_ff, _ptr(x), _ptr_or_none(W), _ptr_or_none(logits), C.byref(r._s),
+                          _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2), _ptr(gout), lam, _ptr(out["dlogits"]),
+                          _ptr(out["dx"]), _ptr_or_none(out["dW"]), _ptr(out["dW1"]), _ptr(out["db1"]),
+                          _ptr(out["dW2"]), _ptr(out["db2"]))
     return out

@@ -289,3 +289,241 @@ void oracle_out_rows(const oracle_cfg *c, int32_t d, int32_t d_ff, const float *
         for (int32_t cc = 0; cc < d; ++cc) y[cc] *= gt;
     }
 }
+
+/* ===================================================================================
+ * Backward (configuration C3).  Not in the paper: Eq. (3) and
+ * Eq. (4) are differentiated by the chain rule, with the dispatch fractions f held
+ * constant (they are argmax indicators).  The objective differentiated is
+ *     J = sum_{r,t} < gout[r][t], OUT[r][t] >  +  lam * sum_r loss_r          (1)
+ * with OUT from Eq. (3) and loss_r from Eq. (4).  Routing decisions (argmax, slots, keep)
+ * are piecewise constant and do not carry gradient.
+ * =================================================================================== */
+
+static double gelu_d(double z) {           /* d/dz [z Phi(z)] = Phi(z) + z phi(z) */
+    const double phi = exp(-0.5 * z * z) / sqrt(2.0 * 3.14159265358979323846);
+    return 0.5 * (1.0 + erf(z / sqrt(2.0))) + z * phi;
+}
+
+/* Router logits in fp64 (no rounding): W [KW, d] given, or the supplied logits widened. */
+static void logits_f64(const oracle_cfg *c, int32_t d, int64_t KW, const double *x, const double *W,
+                       const double *logits, double *out) {
+    const int64_t rows = (int64_t)c->n * c->m * c->T;
+    for (int64_t r = 0; r < rows; ++r)
+        for (int64_t k = 0; k < KW; ++k) {
+            if (!W) { out[r * KW + k] = logits[r * KW + k]; continue; }
+            double acc = 0.0;
+            for (int32_t cc = 0; cc < d; ++cc) acc += x[r * d + cc] * W[k * d + cc];
+            out[r * KW + k] = acc;
+        }
+}
+
+static void softmax_d(const double *v, int64_t K, double *p) {
+    double mx = v[0], s = 0.0;
+    for (int64_t k = 1; k < K; ++k) if (v[k] > mx) mx = v[k];
+    for (int64_t k = 0; k < K; ++k) s += exp(v[k] - mx);
+    for (int64_t k = 0; k < K; ++k) p[k] = exp(v[k] - mx) / s;
+}
+
+static void ffn_fwd_d(int32_t d, int32_t d_ff, const double *x, const double *W1, const double *b1,
+                      const double *W2, const double *b2, double *a, double *h, double *y) {
+    for (int32_t f = 0; f < d_ff; ++f) a[f] = b1[f];
+    for (int32_t k = 0; k < d; ++k)
+        for (int32_t f = 0; f < d_ff; ++f) a[f] += x[k] * W1[(int64_t)k * d_ff + f];
+    for (int32_t f = 0; f < d_ff; ++f) h[f] = gelu(a[f]);
+    for (int32_t cc = 0; cc < d; ++cc) y[cc] = b2[cc];
+    for (int32_t f = 0; f < d_ff; ++f)
+        for (int32_t cc = 0; cc < d; ++cc) y[cc] += h[f] * W2[(int64_t)f * d + cc];
+}
+
+/*
+ * The objective (1) evaluated entirely in fp64 (used to pin oracle_backward by finite
+ * differences).  Routing decisions are taken exactly as in oracle_route, on the fp32
+ * rounding of the fp64 logits; they are returned in keep_out [G*T] / dest_out [G*T*2]
+ * so a caller can check that a perturbation did not flip one.  Returns J.
+ */
+double oracle_objective(const oracle_cfg *c, int32_t d, int32_t d_ff, const double *x, const double *W,
+                        const double *logits, const double *W1, const double *b1, const double *W2,
+                        const double *b2, const double *gout, double lam, uint8_t *keep_out,
+                        int32_t *dest_out) {
+    const int64_t G = (int64_t)c->n * c->m, T = c->T;
+    int64_t K1, K2, C1, C2;
+    oracle_sizes(c, &K1, &K2, &C1, &C2);
+    const int64_t KW = c->flat ? K1 : K1 + K2;
+    double *L = (double *)malloc(sizeof(double) * (size_t)(G * T * KW));
+    float *Lf = (float *)malloc(sizeof(float) * (size_t)(G * T * KW));
+    logits_f64(c, d, KW, x, W, logits, L);
+    for (int64_t i = 0; i < G * T * KW; ++i) Lf[i] = (float)L[i];
+    /* routing of Lf, as oracle_route (decisions only) */
+    const int64_t nc = c->n * (C1 > 0 ? C1 : 1);
+    oracle_route_out o;
+    int32_t *i32 = (int32_t *)calloc((size_t)(3 * G * T + G * K1 + G * K2 + 2 * G * nc), sizeof(int32_t));
+    uint8_t *u8 = (uint8_t *)calloc((size_t)(2 * G * T + G * nc), 1);
+    float *f32 = (float *)calloc((size_t)(3 * G * T), sizeof(float));
+    int64_t *i64 = (int64_t *)calloc((size_t)(G * (K1 + K2)), sizeof(int64_t));
+    double *f64 = (double *)calloc((size_t)(G * (K1 + K2) + G), sizeof(double));
+    o.dest1 = i32; o.dest2 = i32 + G * T; o.slot1 = i32 + 2 * G * T; o.counts1 = i32 + 3 * G * T;
+    o.counts2 = o.counts1 + G * K1; o.jin = o.counts2 + G * K2; o.slot2 = o.jin + G * nc;
+    o.keep1 = u8; o.keep = u8 + G * T; o.keep2 = u8 + 2 * G * T;
+    o.p = f32; o.q = f32 + G * T; o.gate = f32 + 2 * G * T;
+    o.A1 = i64; o.A2 = i64 + G * K1; o.S1 = f64; o.S2 = f64 + G * K1; o.loss = f64 + G * (K1 + K2);
+    double J = 0.0;
+    if (oracle_route(c, Lf, &o) == 0) {
+        double *pv = (double *)malloc(sizeof(double) * (size_t)(K1 + K2));
+        double *a = (double *)malloc(sizeof(double) * (size_t)d_ff), *h = (double *)malloc(sizeof(double) * (size_t)d_ff);
+        double *y = (double *)malloc(sizeof(double) * (size_t)d);
+        double *P1 = (double *)calloc((size_t)K1, sizeof(double)), *P2 = (double *)calloc((size_t)K2, sizeof(double));
+        for (int64_t r = 0; r < G; ++r) {
+            memset(P1, 0, sizeof(double) * (size_t)K1);
+            memset(P2, 0, sizeof(double) * (size_t)K2);
+            for (int64_t t = 0; t < T; ++t) {
+                const int64_t g = r * T + t;
+                const double *Lg = L + g * KW;
+                softmax_d(Lg, K1, pv);
+                for (int64_t k = 0; k < K1; ++k) P1[k] += pv[k] / (double)T;
+                double gate = pv[o.dest1[g]];
+                if (!c->flat) {
+                    softmax_d(Lg + K1, K2, pv + K1);
+                    for (int64_t k = 0; k < K2; ++k) P2[k] += pv[K1 + k] / (double)T;
+                    gate *= pv[K1 + o.dest2[g]];
+                }
+                if (keep_out) keep_out[g] = o.keep[g];
+                if (dest_out) { dest_out[2 * g] = o.dest1[g]; dest_out[2 * g + 1] = o.dest2[g]; }
+                if (!o.keep[g]) continue;
+                const int64_t ex = c->flat ? o.dest1[g] : (int64_t)o.dest1[g] * K2 + o.dest2[g];
+                ffn_fwd_d(d, d_ff, x + g * d, W1 + ex * (int64_t)d * d_ff, b1 + ex * (int64_t)d_ff,
+                          W2 + ex * (int64_t)d_ff * d, b2 + ex * (int64_t)d, a, h, y);
+                for (int32_t cc = 0; cc < d; ++cc) J += gout[g * d + cc] * gate * y[cc];
+            }
+            double l1 = 0.0, l2 = 0.0;
+            for (int64_t k = 0; k < K1; ++k) l1 += ((double)o.A1[r * K1 + k] / (double)T) * P1[k];
+            if (!c->flat)
+                for (int64_t k = 0; k < K2; ++k) l2 += ((double)o.A2[r * K2 + k] / (double)T) * P2[k];
+            J += lam * (c->alpha * (double)K1 * l1 + (c->flat ? 0.0 : c->beta * (double)K2 * l2));
+        }
+        free(pv); free(a); free(h); free(y); free(P1); free(P2);
+    } else {
+        J = NAN;
+    }
+    free(L); free(Lf); free(i32); free(u8); free(f32); free(i64); free(f64);
+    return J;
+}
+
+/*
+ * Gradient of the objective (1) (a16-a19) for the routing `o` of oracle_route (run on
+ * the fp32 logits) -- chain rule in the order of the backward pass:
+ *   a16 combine:  dy = gate * gout; dgate = <gout, y>; dp = q_j dgate, dq = p_i dgate
+ *   a17 FFN:      db2 += dy; dW2 += h dy^T; dz = (W2 dy) * GELU'(a); db1 += dz;
+ *                 dW1 += x dz^T; dx += W1 dz
+ *   a19 router:   dlogit1_k = dp p_i (delta_ki - p_k) + lam a K1/T p_k (f_k - sum_i f_i p_i)
+ *                 dlogit2_k = dq q_j (delta_kj - q_k) + lam b K2/T q_k (f2_k - sum f2 q)
+ *                 (FLAT: level 1 only, gate = p); dW += dlogit x^T; dx += W^T dlogit.
+ * Probabilities are the fp64 softmax of the fp64 logits (x W, or the widened supplied
+ * logits).  W may be NULL (supplied logits: dW and the router part of dx are skipped).
+ * dW sums over every rank's tokens (the router is tied).  All outputs fp64 and
+ * overwritten: dlogits [G*T*KW], dx [G*T*d], dW [KW*d], dW1 [NE*d*d_ff], db1 [NE*d_ff],
+ * dW2 [NE*d_ff*d], db2 [NE*d].
+ */
+void oracle_backward(const oracle_cfg *c, int32_t d, int32_t d_ff, const float *x, const float *W,
+                     const float *logits, const oracle_route_out *o, const float *W1, const float *b1,
+                     const float *W2, const float *b2, const float *gout, double lam, double *dlogits,
+                     double *dx, double *dW, double *dW1, double *db1, double *dW2, double *db2) {
+    const int64_t G = (int64_t)c->n * c->m, T = c->T, NE = G * c->e;
+    int64_t K1, K2, C1, C2;
+    oracle_sizes(c, &K1, &K2, &C1, &C2);
+    const int64_t KW = c->flat ? K1 : K1 + K2;
+    const int64_t nx = G * T * d;
+    double *xd = (double *)malloc(sizeof(double) * (size_t)nx);
+    for (int64_t i = 0; i < nx; ++i) xd[i] = (double)x[i];
+    double *Wd = NULL, *ld = NULL;
+    if (W) {
+        Wd = (double *)malloc(sizeof(double) * (size_t)(KW * d));
+        for (int64_t i = 0; i < KW * d; ++i) Wd[i] = (double)W[i];
+    } else {
+        ld = (double *)malloc(sizeof(double) * (size_t)(G * T * KW));
+        for (int64_t i = 0; i < G * T * KW; ++i) ld[i] = (double)logits[i];
+    }
+    double *L = (double *)malloc(sizeof(double) * (size_t)(G * T * KW));
+    logits_f64(c, d, KW, xd, Wd, ld, L);
+    memset(dlogits, 0, sizeof(double) * (size_t)(G * T * KW));
+    memset(dx, 0, sizeof(double) * (size_t)nx);
+    if (dW) memset(dW, 0, sizeof(double) * (size_t)(KW * d));
+    memset(dW1, 0, sizeof(double) * (size_t)(NE * d * d_ff));
+    memset(db1, 0, sizeof(double) * (size_t)(NE * d_ff));
+    memset(dW2, 0, sizeof(double) * (size_t)(NE * d_ff * d));
+    memset(db2, 0, sizeof(double) * (size_t)(NE * d));
+    double *pv = (double *)malloc(sizeof(double) * (size_t)(K1 + K2));
+    double *a = (double *)malloc(sizeof(double) * (size_t)d_ff), *h = (double *)malloc(sizeof(double) * (size_t)d_ff);
+    double *y = (double *)malloc(sizeof(double) * (size_t)d), *dy = (double *)malloc(sizeof(double) * (size_t)d);
+    double *dz = (double *)malloc(sizeof(double) * (size_t)d_ff);
+    double *w1 = (double *)malloc(sizeof(double) * (size_t)(d * d_ff)), *w2 = (double *)malloc(sizeof(double) * (size_t)(d * d_ff));
+    double *bb1 = (double *)malloc(sizeof(double) * (size_t)d_ff), *bb2 = (double *)malloc(sizeof(double) * (size_t)d);
+    for (int64_t r = 0; r < G; ++r) {
+        for (int64_t t = 0; t < T; ++t) {
+            const int64_t g = r * T + t;
+            const double *Lg = L + g * KW;
+            double *dl = dlogits + g * KW;
+            softmax_d(Lg, K1, pv);
+            if (!c->flat) softmax_d(Lg + K1, K2, pv + K1);
+            const int32_t i = o->dest1[g], j = o->dest2[g];
+            const double p = pv[i], q = c->flat ? 1.0 : pv[K1 + j];
+            double dgate = 0.0;
+            if (o->keep[g]) {                       /* a16, a17 */
+                const int64_t ex = c->flat ? i : (int64_t)i * K2 + j;
+                for (int64_t z = 0; z < (int64_t)d * d_ff; ++z) { w1[z] = W1[ex * d * d_ff + z]; w2[z] = W2[ex * d_ff * d + z]; }
+                for (int32_t f = 0; f < d_ff; ++f) bb1[f] = b1[ex * d_ff + f];
+                for (int32_t cc = 0; cc < d; ++cc) bb2[cc] = b2[ex * d + cc];
+                ffn_fwd_d(d, d_ff, xd + g * d, w1, bb1, w2, bb2, a, h, y);
+                const double gate = p * q;
+                for (int32_t cc = 0; cc < d; ++cc) {
+                    dgate += (double)gout[g * d + cc] * y[cc];
+                    dy[cc] = gate * (double)gout[g * d + cc];
+                    db2[ex * d + cc] += dy[cc];
+                }
+                for (int32_t f = 0; f < d_ff; ++f) {
+                    double dh = 0.0;
+                    for (int32_t cc = 0; cc < d; ++cc) {
+                        dW2[(ex * d_ff + f) * d + cc] += h[f] * dy[cc];
+                        dh += w2[(int64_t)f * d + cc] * dy[cc];
+                    }
+                    dz[f] = dh * gelu_d(a[f]);
+                    db1[ex * d_ff + f] += dz[f];
+                }
+                for (int32_t k = 0; k < d; ++k) {
+                    double s = 0.0;
+                    for (int32_t f = 0; f < d_ff; ++f) {
+                        dW1[(ex * d + k) * d_ff + f] += xd[g * d + k] * dz[f];
+                        s += w1[(int64_t)k * d_ff + f] * dz[f];
+                    }
+                    dx[g * d + k] += s;
+                }
+            }
+            /* a19: router */
+            const double dp = q * dgate, dq = p * dgate;
+            double fp = 0.0;
+            for (int64_t k = 0; k < K1; ++k) fp += ((double)o->A1[r * K1 + k] / (double)T) * pv[k];
+            for (int64_t k = 0; k < K1; ++k) {
+                const double fk = (double)o->A1[r * K1 + k] / (double)T;
+                dl[k] = dp * p * ((k == i ? 1.0 : 0.0) - pv[k]) +
+                        lam * c->alpha * (double)K1 / (double)T * pv[k] * (fk - fp);
+            }
+            if (!c->flat) {
+                double fq = 0.0;
+                for (int64_t k = 0; k < K2; ++k) fq += ((double)o->A2[r * K2 + k] / (double)T) * pv[K1 + k];
+                for (int64_t k = 0; k < K2; ++k) {
+                    const double fk = (double)o->A2[r * K2 + k] / (double)T;
+                    dl[K1 + k] = dq * q * ((k == j ? 1.0 : 0.0) - pv[K1 + k]) +
+                                 lam * c->beta * (double)K2 / (double)T * pv[K1 + k] * (fk - fq);
+                }
+            }
+            if (Wd) {
+                for (int64_t k = 0; k < KW; ++k)
+                    for (int32_t cc = 0; cc < d; ++cc) {
+                        if (dW) dW[k * d + cc] += dl[k] * xd[g * d + cc];
+                        dx[g * d + cc] += dl[k] * Wd[k * d + cc];
+                    }
+            }
+        }
+    }
+    free(xd); free(Wd); free(ld); free(L); free(pv); free(a); free(h); free(y); free(dy); free(dz);
+    free(w1); free(w2); free(bb1); free(bb2);
+}
