@@ -95,6 +95,7 @@ typedef struct {
     int32_t S;
     int64_t Cseg;
     size_t ws_bytes;        /* size of the workspace smile_forward needs (smile_forward_ws) */
+    size_t router_partial_bytes;   /* scratch of smile_router_bwd */
 } smile_sizes;
 
 typedef struct smile_ctx_s *smile_ctx;
@@ -234,6 +235,57 @@ smile_status smile_combine(smile_ctx ctx, int32_t level, const void *ret_rows,
 smile_status smile_aux_loss(smile_ctx ctx, const smile_stats *stats, double alpha, double beta,
                             double *loss, void *stream);
 
+/* ---------------- training: the backward pass (configuration C3) ----
+ * The paper trains the layer (Eq. 5) but gives no backward; these calls are
+ * the chain rule of Eq. (3) and Eq. (4) for the objective
+ *     J = sum_t <gout[t], out[t]> + lam * sum_v loss[v]
+ * with the dispatch fractions f held constant (argmax indicators).  Gradient rows travel
+ * the forward route (capacity slots and drops of the forward are reused, nothing is
+ * re-routed), and dX travels the return route. */
+
+/* Forward of the expert FFN that also stores the pre-activation A1 = X W1 + b1 (dtype,
+ * [V, S, e, Cseg, d_ff]) that GELU' needs in the backward. */
+smile_status smile_expert_ffn_train(smile_ctx ctx, const void *X, const int32_t *counts, const void *W1t,
+                                    const float *b1, const void *W2t, const float *b2, void *A1_ws, void *H_ws,
+                                    void *Y, void *stream);
+
+/* a16 + a19 (router part): combine backward at the source.  gout [V, T, d] = dJ/dout;
+ * back1 [V, K1, C1, d] the forward's returned expert rows (before the gate); logits
+ * [V, T, KW] fp32 the forward's router logits; route / stats of the forward.  Writes
+ * dsend [V, K1, C1, d] = gate * gout at (dest1, slot1) of every level-1-kept token and
+ * dlogits [V, T, KW] fp32 = dJ/dlogits (Eq. 3 through p_i q_j, Eq. 4 through P, Q). */
+smile_status smile_combine_bwd(smile_ctx ctx, const void *gout, const void *back1, const float *logits,
+                               const smile_route *route, const smile_stats *stats, double alpha, double beta,
+                               double lam, void *dsend, float *dlogits, void *stream);
+
+/* a16 (level 2): gradient rows at the intermediate follow the forward route:
+ * dsend2[v, j, slot2] = drecv1[v, s, c] for every kept received slot (BILEVEL). */
+smile_status smile_dispatch_grad(smile_ctx ctx, const void *drecv1, const int32_t *recv_meta,
+                                 const int32_t *slot2, void *dsend2, void *stream);
+
+/* a17: backward of every resident expert over its segments.  X, dY [V, S, e, Cseg, d];
+ * A1, H [V, S, e, Cseg, d_ff] saved by smile_expert_ffn_train; W1 [V*e, d, d_ff] and
+ * W2 [V*e, d_ff, d] in their math layouts (the transposes of the forward's W1t / W2t).
+ * Writes dZ_ws = (dY W2^T) . GELU'(A1) [V, S, e, Cseg, d_ff] (may alias A1),
+ * dX = dZ W1^T [V, S, e, Cseg, d] and fp32 dW1 [V*e, d, d_ff], db1 [V*e, d_ff],
+ * dW2 [V*e, d_ff, d], db2 [V*e, d] summed over the valid rows.  bf16: dZ and dX on
+ * tcgen05; the weight gradients on SIMT FFMA this round. */
+smile_status smile_expert_ffn_bwd(smile_ctx ctx, const void *X, const int32_t *counts, const void *A1,
+                                  const void *H, const void *dY, const void *W1, const void *W2, void *dZ_ws,
+                                  void *dX, float *dW1, float *db1, float *dW2, float *db2, void *stream);
+
+/* a18: the last step of the dX return: dx[t] = slot1 < C1 ? ret_rows[dest1, slot1] : 0
+ * (rows already carry the gate factor from smile_combine_bwd). */
+smile_status smile_combine_grad(smile_ctx ctx, const void *ret_rows, const smile_route *route, void *dx,
+                                void *stream);
+
+/* a19: fused-router gradient: dx += dlogits W (in place, dtype) and dW [KW, d] fp32 =
+ * sum over every resident token of dlogits^T x (the router is tied; summing
+ * across processes is the caller's data-parallel all-reduce).  partial_ws: scratch of
+ * smile_sizes.router_partial_bytes. */
+smile_status smile_router_bwd(smile_ctx ctx, const void *x, const float *w_router, const float *dlogits,
+                              void *dx, float *dW, void *partial_ws, void *stream);
+
 /* ---------------- whole layer ---------------- */
 
 /* Caller-owned buffers of one layer; shapes as in the step calls. */
@@ -246,7 +298,20 @@ typedef struct {
     double *loss;             /* [V] */
     double alpha, beta;
     void *ws;                 /* smile_sizes.ws_bytes bytes, 256-byte aligned */
+    int32_t train;            /* != 0: also save what smile_backward needs (A1, router logits) */
 } smile_layer_io;
+
+/* Gradients of one layer (smile_backward).  gout [V, T, d] dtype in; dx [V, T, d] dtype,
+ * dW_router [KW, d] fp32 (fused router only, else NULL), dW1 / db1 / dW2 / db2 fp32 out
+ * (shapes of smile_expert_ffn_bwd); W1 / W2 the math layouts of the expert weights. */
+typedef struct {
+    const void *gout;
+    void *dx;
+    float *dW_router;
+    const void *W1; const void *W2;
+    float *dW1; float *db1; float *dW2; float *db2;
+    double lam;               /* weight of the aux loss in J */
+} smile_grad_io;
 
 /* Device pointers into the workspace of smile_forward, for inspection. */
 typedef struct {
@@ -259,6 +324,9 @@ typedef struct {
     int32_t *rcounts;                       /* [V, S, e] valid rows per FFN segment */
     void *ffn_in; void *H; void *Y;         /* [V, S, e, Cseg, d|d_ff] */
     void *ret2; void *ret1; void *back1;    /* return-path buffers */
+    void *A1;                               /* [V, S, e, Cseg, d_ff] pre-activation (train) */
+    float *logits; float *dlogits;          /* [V, T, KW] saved logits (train), their gradient */
+    void *rpartial;                         /* router-gradient partial sums */
 } smile_ws_view;
 
 smile_status smile_forward_ws(smile_ctx ctx, void *ws, smile_ws_view *view);
@@ -274,6 +342,11 @@ smile_status smile_forward(smile_ctx ctx, const smile_layer_io *io, void *stream
  * to io->x / io->logits, runs smile_forward, copies io->out to host_out and io->loss to
  * host_loss, all on `stream`; synchronises `stream` before returning.  Host buffers
  * should be pinned for asynchronous copies. */
+/* The whole backward after a forward with io->train set, in reverse order of the forward:
+ * combine_bwd, exchange(1, gradient rows), dispatch_grad, exchange(2), expert_ffn_bwd,
+ * exchange(2, reverse), combine(2), exchange(1, reverse), combine_grad, router_bwd. */
+smile_status smile_backward(smile_ctx ctx, const smile_layer_io *io, const smile_grad_io *g, void *stream);
+
 smile_status smile_forward_host(smile_ctx ctx, const smile_layer_io *io, const void *host_x,
                                 const float *host_logits, void *host_out, double *host_loss,
                                 void *stream);

@@ -97,6 +97,10 @@ static void ws_layout(const smile_shape *s, const smile_sizes *z, WsLayout *L, s
         w.ret1 = take(V * z->K1 * z->C1 * rb);
     }
     w.back1 = take(V * z->K1 * z->C1 * rb);
+    w.A1 = take(ffn_rows * s->d_ff * eb);
+    w.logits = (float *)take(V * T * z->KW * 4);
+    w.dlogits = (float *)take(V * T * z->KW * 4);
+    w.rpartial = take(z->router_partial_bytes);
     if (L) L->total = o;
     if (view) *view = w;
 }
@@ -126,6 +130,7 @@ extern "C" smile_status smile_plan(const smile_shape *s, smile_sizes *out) {
     z.S = bi ? s->m : G;
     z.Cseg = bi ? z.C2 : z.C1;
     if (z.KW > 512 || z.K2 > 256) return SMILE_ENOTSUP;   // gate smem tile / level-2 rank limits
+    z.router_partial_bytes = router_bwd_partial_floats((int64_t)z.V * s->T, s->d, z.KW) * 4;
     WsLayout L;
     ws_layout(s, &z, &L, nullptr, nullptr);
     z.ws_bytes = L.total;
@@ -341,7 +346,7 @@ extern "C" smile_status smile_gate_inter(smile_ctx c, const void *x, const float
     if (!logits && (!x || !w_router)) return SMILE_EINVAL;
     if (c->shape.T == 0) return SMILE_OK;
     cudaSetDevice(c->shape.device);
-    GateArgs a;
+    GateArgs a{};
     a.x = x; a.w = w_router; a.logits = logits; a.logits_out = logits_out;
     a.route = *route;
     a.blk_hist1 = c->blk_hist1; a.blk_hist2a = c->blk_hist2a; a.blk_psum = c->blk_psum;
@@ -349,7 +354,7 @@ extern "C" smile_status smile_gate_inter(smile_ctx c, const void *x, const float
     a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1;
     a.flat = c->shape.mode == SMILE_FLAT; a.bf16 = c->shape.dtype == SMILE_BF16;
     launch_gate1(a, S(stream));
-    Scan1Args s;
+    Scan1Args s{};
     s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
     s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
     s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T;
@@ -367,7 +372,7 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
     if (level == 1) {
         if (!route || (bi && !send_meta)) return SMILE_EINVAL;
         if (c->shape.T == 0) return SMILE_OK;
-        Dispatch1Args a;
+        Dispatch1Args a{};
         a.x = rows_in; a.route = *route; a.blk_off1 = c->blk_off1; a.blk_hist1 = c->blk_hist1;
         a.send = send_rows; a.meta = bi ? send_meta : nullptr;
         a.V = c->sz.V; a.T = c->shape.T; a.rowbytes = rb; a.K1 = c->sz.K1; a.C1 = c->sz.C1;
@@ -379,7 +384,7 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
         if (!bi) return SMILE_EINVAL;
         if (!recv_meta || !slot2) return SMILE_EINVAL;
         if (c->shape.T == 0) return SMILE_OK;
-        Dispatch2Args a;
+        Dispatch2Args a{};
         a.recv1 = rows_in; a.recv_meta = recv_meta; a.slot2 = slot2; a.blk_off2 = c->blk_off2;
         a.send2 = send_rows; a.V = c->sz.V; a.items = (int64_t)c->shape.n * c->sz.C1; a.rowbytes = rb;
         a.K2 = c->sz.K2; a.C2 = c->sz.C2; a.nblk = c->nblk2;
@@ -395,7 +400,7 @@ extern "C" smile_status smile_gate_intra(smile_ctx c, const int32_t *recv_meta, 
     if (c->shape.mode != SMILE_BILEVEL) return SMILE_EINVAL;
     if (c->shape.T == 0) return SMILE_OK;
     cudaSetDevice(c->shape.device);
-    Rank2Args a;
+    Rank2Args a{};
     a.recv_meta = recv_meta; a.slot2 = slot2; a.blk_hist2 = c->blk_hist2; a.blk_off2 = c->blk_off2;
     a.counts2 = counts2; a.err = c->d_err; a.V = c->sz.V; a.items = (int64_t)c->shape.n * c->sz.C1;
     a.K2 = c->sz.K2; a.nblk = c->nblk2; a.C2 = c->sz.C2;
@@ -416,7 +421,7 @@ extern "C" smile_status smile_all2all(smile_ctx c, int32_t level, int32_t revers
     if (bi == (level == 0)) return SMILE_EINVAL;
     const Level &L = c->lv[level];
     const bool with_ints = !reverse && send_ints && recv_ints;
-    if (!reverse && (!send_ints || !recv_ints)) return SMILE_EINVAL;
+    if (!reverse && (!send_ints != !recv_ints)) return SMILE_EINVAL;   // forward: both or neither (rows only)
     if (c->shape.T == 0) return SMILE_OK;
     cudaSetDevice(c->shape.device);
     cudaStream_t st = S(stream);
@@ -425,7 +430,7 @@ extern "C" smile_status smile_all2all(smile_ctx c, int32_t level, int32_t revers
     const int V = c->sz.V, P = L.P;
     const bool nccl_alltoall = c->shape.nprocs > 1 && V == 1 && L.comm;
     if (!nccl_alltoall) {
-        CopyXArgs a;
+        CopyXArgs a{};
         a.send = (const char *)send_rows; a.recv = (char *)recv_rows;
         a.sint = with_ints ? send_ints : nullptr; a.rint = with_ints ? recv_ints : nullptr;
         a.cnt = fwd_counts; a.member_local = L.d_member_local; a.mypos = L.d_mypos;
@@ -485,7 +490,7 @@ extern "C" smile_status smile_expert_ffn(smile_ctx c, const void *X, const int32
     if (!c || !X || !counts || !W1t || !b1 || !W2t || !b2 || !H_ws || !Y) return SMILE_EINVAL;
     if (c->shape.T == 0) return SMILE_OK;
     cudaSetDevice(c->shape.device);
-    FfnArgs f;
+    FfnArgs f{};
     f.X = X; f.counts = counts; f.W1t = W1t; f.b1 = b1; f.W2t = W2t; f.b2 = b2; f.H = H_ws; f.Y = Y;
     f.V = c->sz.V; f.S = c->sz.S; f.e = c->shape.e; f.Cseg = c->sz.Cseg; f.d = c->shape.d; f.d_ff = c->shape.d_ff;
     f.bf16 = c->shape.dtype == SMILE_BF16; f.num_sms = c->num_sms;
@@ -510,7 +515,7 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
     const bool bf = c->shape.dtype == SMILE_BF16;
     if (level == 1) {
         if (!route) return SMILE_EINVAL;
-        Combine1Args a;
+        Combine1Args a{};
         a.back1 = ret_rows; a.route = *route; a.out = out; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
         a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = bf;
         launch_combine1(a, S(stream));
@@ -518,7 +523,7 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
     }
     if (level == 2) {
         if (c->shape.mode != SMILE_BILEVEL || !recv_meta || !slot2) return SMILE_EINVAL;
-        Combine2Args a;
+        Combine2Args a{};
         a.ret2 = ret_rows; a.recv_meta = recv_meta; a.slot2 = slot2; a.ret1 = out; a.V = c->sz.V;
         a.items = (int64_t)c->shape.n * c->sz.C1; a.rowbytes = (int64_t)c->shape.d * (bf ? 2 : 4);
         a.K2 = c->sz.K2; a.C2 = c->sz.C2;
@@ -535,6 +540,105 @@ extern "C" smile_status smile_aux_loss(smile_ctx c, const smile_stats *stats, do
     cudaSetDevice(c->shape.device);
     launch_aux(*stats, alpha, beta, loss, c->sz.V, c->sz.K1, c->sz.K2, c->shape.T,
                c->shape.mode == SMILE_FLAT, S(stream));
+    return post_launch();
+}
+
+static bool ffn_use_tc(smile_ctx c) {
+    int impl = c->shape.ffn_impl;
+    if (impl == SMILE_FFN_AUTO) impl = c->shape.dtype == SMILE_BF16 ? SMILE_FFN_TCGEN05 : SMILE_FFN_SIMT;
+    return impl == SMILE_FFN_TCGEN05;
+}
+
+extern "C" smile_status smile_expert_ffn_train(smile_ctx c, const void *X, const int32_t *counts, const void *W1t,
+                                               const float *b1, const void *W2t, const float *b2, void *A1_ws,
+                                               void *H_ws, void *Y, void *stream) {
+    if (!c || !X || !counts || !W1t || !b1 || !W2t || !b2 || !A1_ws || !H_ws || !Y) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c->shape.device);
+    FfnArgs f{};
+    f.X = X; f.counts = counts; f.W1t = W1t; f.b1 = b1; f.W2t = W2t; f.b2 = b2; f.H = H_ws; f.Y = Y;
+    f.V = c->sz.V; f.S = c->sz.S; f.e = c->shape.e; f.Cseg = c->sz.Cseg; f.d = c->shape.d; f.d_ff = c->shape.d_ff;
+    f.bf16 = c->shape.dtype == SMILE_BF16; f.num_sms = c->num_sms;
+    const bool tc = ffn_use_tc(c);
+    if (tc && !f.bf16) return SMILE_ENOTSUP;
+    if (!tc && !ffn_simt_supported(f.V * f.S * f.e, f.d, f.d_ff)) return SMILE_ENOTSUP;
+    cudaError_t e = launch_ffn_fwd_train(f, A1_ws, tc, S(stream));
+    if (e == cudaErrorNotSupported) return SMILE_ENOTSUP;
+    return e == cudaSuccess ? post_launch() : SMILE_ECUDA;
+}
+
+extern "C" smile_status smile_combine_bwd(smile_ctx c, const void *gout, const void *back1, const float *logits,
+                                          const smile_route *route, const smile_stats *stats, double alpha,
+                                          double beta, double lam, void *dsend, float *dlogits, void *stream) {
+    if (!c || !gout || !back1 || !logits || !route || !stats || !dsend || !dlogits) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c->shape.device);
+    CombineBwdArgs a{};
+    a.gout = gout; a.back1 = back1; a.logits = logits; a.route = *route; a.stats = *stats; a.dsend = dsend;
+    a.dlogits = dlogits; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d; a.K1 = c->sz.K1; a.K2 = c->sz.K2;
+    a.KW = c->sz.KW; a.C1 = c->sz.C1; a.alpha = alpha; a.beta = beta; a.lam = lam;
+    a.flat = c->shape.mode == SMILE_FLAT; a.bf16 = c->shape.dtype == SMILE_BF16;
+    launch_combine_bwd(a, S(stream));
+    return post_launch();
+}
+
+extern "C" smile_status smile_dispatch_grad(smile_ctx c, const void *drecv1, const int32_t *recv_meta,
+                                            const int32_t *slot2, void *dsend2, void *stream) {
+    if (!c || !drecv1 || !recv_meta || !slot2 || !dsend2) return SMILE_EINVAL;
+    if (c->shape.mode != SMILE_BILEVEL) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c->shape.device);
+    Dispatch2Args a{};
+    a.recv1 = drecv1; a.recv_meta = recv_meta; a.slot2 = const_cast<int32_t *>(slot2); a.blk_off2 = nullptr;
+    a.send2 = dsend2; a.V = c->sz.V; a.items = (int64_t)c->shape.n * c->sz.C1;
+    a.rowbytes = (int64_t)c->shape.d * (c->shape.dtype == SMILE_BF16 ? 2 : 4); a.K2 = c->sz.K2; a.C2 = c->sz.C2;
+    a.nblk = c->nblk2;
+    launch_grad_dispatch2(a, S(stream));
+    return post_launch();
+}
+
+extern "C" smile_status smile_expert_ffn_bwd(smile_ctx c, const void *X, const int32_t *counts, const void *A1,
+                                             const void *H, const void *dY, const void *W1, const void *W2,
+                                             void *dZ_ws, void *dX, float *dW1, float *db1, float *dW2, float *db2,
+                                             void *stream) {
+    if (!c || !X || !counts || !A1 || !H || !dY || !W1 || !W2 || !dZ_ws || !dX || !dW1 || !db1 || !dW2 || !db2)
+        return SMILE_EINVAL;
+    cudaSetDevice(c->shape.device);
+    FfnBwdArgs b{};
+    b.X = X; b.counts = counts; b.A1 = A1; b.H = H; b.dY = dY; b.W1 = W1; b.W2 = W2; b.dZ = dZ_ws; b.dX = dX;
+    b.dW1 = dW1; b.db1 = db1; b.dW2 = dW2; b.db2 = db2; b.V = c->sz.V; b.S = c->sz.S; b.e = c->shape.e;
+    b.Cseg = c->sz.Cseg; b.d = c->shape.d; b.d_ff = c->shape.d_ff; b.bf16 = c->shape.dtype == SMILE_BF16;
+    b.num_sms = c->num_sms;
+    const bool tc = ffn_use_tc(c);
+    if (tc && !b.bf16) return SMILE_ENOTSUP;
+    if (!ffn_simt_supported(b.V * b.S * b.e, b.d, b.d_ff)) return SMILE_ENOTSUP;
+    cudaError_t e = launch_ffn_bwd(b, tc, S(stream));
+    if (e == cudaErrorNotSupported) return SMILE_ENOTSUP;
+    return e == cudaSuccess ? post_launch() : SMILE_ECUDA;
+}
+
+extern "C" smile_status smile_combine_grad(smile_ctx c, const void *ret_rows, const smile_route *route, void *dx,
+                                           void *stream) {
+    if (!c || !ret_rows || !route || !dx) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c->shape.device);
+    Combine1Args a{};
+    a.back1 = ret_rows; a.route = *route; a.out = dx; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
+    a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = c->shape.dtype == SMILE_BF16; a.nogate = 1;
+    launch_combine1(a, S(stream));
+    return post_launch();
+}
+
+extern "C" smile_status smile_router_bwd(smile_ctx c, const void *x, const float *w_router, const float *dlogits,
+                                         void *dx, float *dW, void *partial_ws, void *stream) {
+    if (!c || !x || !w_router || !dlogits || !dx || !dW || !partial_ws) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c->shape.device);
+    RouterBwdArgs a{};
+    a.x = x; a.w = w_router; a.dlogits = dlogits; a.dx = dx; a.dW = dW; a.partial = (float *)partial_ws;
+    a.rows = (int64_t)c->sz.V * c->shape.T; a.d = c->shape.d; a.KW = c->sz.KW; a.nchunk = 0;
+    a.bf16 = c->shape.dtype == SMILE_BF16;
+    launch_router_bwd(a, S(stream));
     return post_launch();
 }
 
@@ -557,7 +661,9 @@ extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, voi
     smile_ws_view w;
     STEP(smile_forward_ws(c, io->ws, &w));
     if (c->shape.T == 0) return SMILE_OK;
-    STEP(smile_gate_inter(c, io->x, io->w_router, io->logits, nullptr, &w.route, &w.stats, w.counts1, stream));
+    const bool train = io->train != 0;
+    STEP(smile_gate_inter(c, io->x, io->w_router, io->logits, (train && !io->logits) ? w.logits : nullptr, &w.route,
+                          &w.stats, w.counts1, stream));
     STEP(smile_dispatch(c, 1, io->x, &w.route, nullptr, nullptr, w.send1, w.meta1, stream));
     if (c->shape.mode == SMILE_BILEVEL) {
         // the paper's "four sequential All2All operations"
@@ -565,17 +671,54 @@ extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, voi
         STEP(smile_gate_intra(c, w.rmeta1, w.slot2, w.counts2, stream));
         STEP(smile_dispatch(c, 2, w.recv1, nullptr, w.rmeta1, w.slot2, w.send2, nullptr, stream));
         STEP(smile_all2all_intra(c, 0, w.send2, w.recv2, w.counts2, w.rcounts, w.counts2, stream));
-        STEP(smile_expert_ffn(c, w.recv2, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.H, w.Y, stream));
+        if (train) STEP(smile_expert_ffn_train(c, w.recv2, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.A1, w.H, w.Y, stream));
+        else STEP(smile_expert_ffn(c, w.recv2, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.H, w.Y, stream));
         STEP(smile_all2all_intra(c, 1, w.Y, w.ret2, nullptr, nullptr, w.counts2, stream));
         STEP(smile_combine(c, 2, w.ret2, nullptr, w.rmeta1, w.slot2, w.ret1, stream));
         STEP(smile_all2all_inter(c, 1, w.ret1, w.back1, nullptr, nullptr, w.counts1, stream));
     } else {
         STEP(smile_all2all(c, 0, 0, w.send1, w.recv1, w.counts1, w.rcounts, w.counts1, stream));
-        STEP(smile_expert_ffn(c, w.recv1, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.H, w.Y, stream));
+        if (train) STEP(smile_expert_ffn_train(c, w.recv1, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.A1, w.H, w.Y, stream));
+        else STEP(smile_expert_ffn(c, w.recv1, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.H, w.Y, stream));
         STEP(smile_all2all(c, 0, 1, w.Y, w.back1, nullptr, nullptr, w.counts1, stream));
     }
     STEP(smile_combine(c, 1, w.back1, &w.route, nullptr, nullptr, io->out, stream));
     STEP(smile_aux_loss(c, &w.stats, io->alpha, io->beta, io->loss, stream));
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_backward(smile_ctx c, const smile_layer_io *io, const smile_grad_io *g, void *stream) {
+    if (!c || !io || !g || !io->ws || !g->gout || !g->dx || !g->W1 || !g->W2 || !g->dW1 || !g->db1 || !g->dW2 ||
+        !g->db2)
+        return SMILE_EINVAL;
+    if (io->w_router && !io->logits && !g->dW_router) return SMILE_EINVAL;
+    smile_ws_view w;
+    STEP(smile_forward_ws(c, io->ws, &w));
+    if (c->shape.T == 0) return SMILE_OK;
+    const float *lg = io->logits ? io->logits : w.logits;
+    // a16: gradient rows into the level-1 send layout (send1 is free after the forward)
+    STEP(smile_combine_bwd(c, g->gout, w.back1, lg, &w.route, &w.stats, io->alpha, io->beta, g->lam, w.send1,
+                           w.dlogits, stream));
+    if (c->shape.mode == SMILE_BILEVEL) {
+        STEP(smile_all2all_inter(c, 0, w.send1, w.recv1, nullptr, nullptr, w.counts1, stream));
+        STEP(smile_dispatch_grad(c, w.recv1, w.rmeta1, w.slot2, w.send2, stream));
+        // dY lands in the Y buffer (X = recv2 is still needed for dW1)
+        STEP(smile_all2all_intra(c, 0, w.send2, w.Y, nullptr, nullptr, w.counts2, stream));
+        STEP(smile_expert_ffn_bwd(c, w.recv2, w.rcounts, w.A1, w.H, w.Y, g->W1, g->W2, w.A1, w.send2, g->dW1, g->db1,
+                                  g->dW2, g->db2, stream));
+        // a18: dX back along the return route
+        STEP(smile_all2all_intra(c, 1, w.send2, w.ret2, nullptr, nullptr, w.counts2, stream));
+        STEP(smile_combine(c, 2, w.ret2, nullptr, w.rmeta1, w.slot2, w.ret1, stream));
+        STEP(smile_all2all_inter(c, 1, w.ret1, w.back1, nullptr, nullptr, w.counts1, stream));
+    } else {
+        STEP(smile_all2all(c, 0, 0, w.send1, w.Y, nullptr, nullptr, w.counts1, stream));
+        STEP(smile_expert_ffn_bwd(c, w.recv1, w.rcounts, w.A1, w.H, w.Y, g->W1, g->W2, w.A1, w.send1, g->dW1, g->db1,
+                                  g->dW2, g->db2, stream));
+        STEP(smile_all2all(c, 0, 1, w.send1, w.back1, nullptr, nullptr, w.counts1, stream));
+    }
+    STEP(smile_combine_grad(c, w.back1, &w.route, g->dx, stream));
+    if (io->w_router && !io->logits)
+        STEP(smile_router_bwd(c, io->x, io->w_router, w.dlogits, g->dx, g->dW_router, w.rpartial, stream));
     return SMILE_OK;
 }
 

@@ -16,9 +16,12 @@ namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16, NTHR = 256, MAXSEG = 4096;
 
+// mode: 0 = act(acc + bias) (act = GELU when gelu), 1 = also D2 = acc + bias (training),
+//       2 = acc * GELU'(aux) (backward dZ), 3 = acc (backward dX).
 struct GemmArgs {
     const void *A; const void *B; const float *bias; void *D; const int32_t *counts;
     int nseg, e, S; int64_t Cseg; int N, K; int gelu; int bf16;
+    int mode; void *D2; const void *aux;
 };
 
 __device__ __forceinline__ float ld(const void *p, int64_t i, int bf16) {
@@ -28,6 +31,15 @@ __device__ __forceinline__ float ld(const void *p, int64_t i, int bf16) {
 
 __device__ __forceinline__ float gelu_erf(float z) {
     return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f));   // R21: exact erf GELU
+}
+
+__device__ __forceinline__ float gelu_grad(float z) {            // Phi(z) + z phi(z)
+    return 0.5f * (1.0f + erff(z * 0.70710678118654752f)) + z * 0.3989422804014327f * expf(-0.5f * z * z);
+}
+
+__device__ __forceinline__ void st(void *p, int64_t o, float v, int bf16) {
+    if (bf16) reinterpret_cast<__nv_bfloat16 *>(p)[o] = __float2bfloat16_rn(v);
+    else reinterpret_cast<float *>(p)[o] = v;
 }
 
 __global__ void __launch_bounds__(NTHR) grouped_gemm_simt(GemmArgs a) {
@@ -85,11 +97,13 @@ __global__ void __launch_bounds__(NTHR) grouped_gemm_simt(GemmArgs a) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int n = n0 + tx * 4 + j;
-                float y = acc[i][j] + a.bias[expert * a.N + n];
-                if (a.gelu) y = gelu_erf(y);
                 const int64_t o = (row0 + r) * a.N + n;
-                if (a.bf16) reinterpret_cast<__nv_bfloat16 *>(a.D)[o] = __float2bfloat16_rn(y);
-                else reinterpret_cast<float *>(a.D)[o] = y;
+                float y = acc[i][j];
+                if (a.mode <= 1) y += a.bias[expert * a.N + n];
+                if (a.mode == 1) st(a.D2, o, y, a.bf16);
+                if ((a.mode == 0 && a.gelu) || a.mode == 1) y = gelu_erf(y);
+                if (a.mode == 2) y *= gelu_grad(ld(a.aux, o, a.bf16));
+                st(a.D, o, y, a.bf16);
             }
         }
     }
@@ -100,10 +114,125 @@ __global__ void __launch_bounds__(NTHR) grouped_gemm_simt(GemmArgs a) {
 void launch_ffn_simt(const FfnArgs &f, cudaStream_t st) {
     const int nseg = f.V * f.S * f.e;
     const int grid = f.num_sms * 4;
-    GemmArgs g1{f.X, f.W1t, f.b1, f.H, f.counts, nseg, f.e, f.S, f.Cseg, f.d_ff, f.d, 1, f.bf16};
+    GemmArgs g1{f.X, f.W1t, f.b1, f.H, f.counts, nseg, f.e, f.S, f.Cseg, f.d_ff, f.d, 1, f.bf16, 0, nullptr, nullptr};
     grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g1);
-    GemmArgs g2{f.H, f.W2t, f.b2, f.Y, f.counts, nseg, f.e, f.S, f.Cseg, f.d, f.d_ff, 0, f.bf16};
+    GemmArgs g2{f.H, f.W2t, f.b2, f.Y, f.counts, nseg, f.e, f.S, f.Cseg, f.d, f.d_ff, 0, f.bf16, 0, nullptr, nullptr};
     grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g2);
+}
+
+cudaError_t launch_ffn_tcgen05_train(const FfnArgs &f, void *A1, cudaStream_t st);
+cudaError_t launch_ffn_tcgen05_dgrad(const FfnBwdArgs &b, cudaStream_t st);
+
+cudaError_t launch_ffn_fwd_train(const FfnArgs &f, void *A1, bool tc, cudaStream_t st) {
+    if (tc) return launch_ffn_tcgen05_train(f, A1, st);
+    const int nseg = f.V * f.S * f.e;
+    const int grid = f.num_sms * 4;
+    GemmArgs g1{f.X, f.W1t, f.b1, f.H, f.counts, nseg, f.e, f.S, f.Cseg, f.d_ff, f.d, 1, f.bf16, 1, A1, nullptr};
+    grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g1);
+    GemmArgs g2{f.H, f.W2t, f.b2, f.Y, f.counts, nseg, f.e, f.S, f.Cseg, f.d, f.d_ff, 0, f.bf16, 0, nullptr, nullptr};
+    grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g2);
+    return cudaGetLastError();
+}
+
+namespace {
+
+// Weight gradient of one expert (a17): Dw[e][m][n] = sum over the expert's valid rows r
+// of A[r][m] * B[r][n] (A [rows, M], B [rows, N] row-major, segment-padded like X).
+// Tile 64 x 64 per block, rows in chunks of 16 staged through smem; fp32 accumulation.
+struct WgradArgs {
+    const void *A; const void *B; float *Dw; const int32_t *counts;
+    int e, S; int64_t Cseg; int M, N; int bf16;
+};
+
+__global__ void __launch_bounds__(NTHR) wgrad_simt(WgradArgs a) {
+    __shared__ float As[BK][BM + 4];
+    __shared__ float Bs[BK][BN + 4];
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+    const int ex = blockIdx.z, v = ex / a.e, k = ex % a.e;
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int s = 0; s < a.S; ++s) {
+        const int g = (v * a.S + s) * a.e + k;
+        const int cnt = a.counts[g];
+        const int64_t base = (int64_t)g * a.Cseg;
+        for (int r0 = 0; r0 < cnt; r0 += BK) {
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+                const int idx = tid + z * NTHR;      // [16 rows][64 cols]
+                const int rr = idx / BM, cc = idx % BM;
+                const bool ok = r0 + rr < cnt;
+                As[rr][cc] = (ok && m0 + cc < a.M) ? ld(a.A, (base + r0 + rr) * a.M + m0 + cc, a.bf16) : 0.f;
+                Bs[rr][cc] = (ok && n0 + cc < a.N) ? ld(a.B, (base + r0 + rr) * a.N + n0 + cc, a.bf16) : 0.f;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int kk = 0; kk < BK; ++kk) {
+                float av[4], bv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) { av[i] = As[kk][ty * 4 + i]; bv[i] = Bs[kk][tx * 4 + i]; }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+            }
+            __syncthreads();
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+            if (m < a.M && n < a.N) a.Dw[((int64_t)ex * a.M + m) * a.N + n] = acc[i][j];
+        }
+}
+
+// Bias gradient: db[e][n] = sum over the expert's valid rows of B[r][n].
+__global__ void colsum_kernel(WgradArgs a) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ex = blockIdx.y, v = ex / a.e, k = ex % a.e;
+    if (n >= a.N) return;
+    float s = 0.f;
+    for (int sg = 0; sg < a.S; ++sg) {
+        const int g = (v * a.S + sg) * a.e + k;
+        const int cnt = a.counts[g];
+        const int64_t base = (int64_t)g * a.Cseg;
+        for (int r = 0; r < cnt; ++r) s += ld(a.B, (base + r) * a.N + n, a.bf16);
+    }
+    a.Dw[(int64_t)ex * a.N + n] = s;
+}
+
+}  // namespace
+
+cudaError_t launch_ffn_bwd(const FfnBwdArgs &b, bool tc, cudaStream_t st) {
+    const int nseg = b.V * b.S * b.e;
+    const int NE = b.V * b.e;
+    if (tc) {
+        cudaError_t e = launch_ffn_tcgen05_dgrad(b, st);
+        if (e != cudaSuccess) return e;
+    } else {
+        const int grid = b.num_sms * 4;
+        // dZ = (dY W2^T) . GELU'(A1): B operand = W2 [NE, d_ff, d] as [N = d_ff, K = d]
+        GemmArgs g1{b.dY, b.W2, nullptr, b.dZ, b.counts, nseg, b.e, b.S, b.Cseg, b.d_ff, b.d, 0, b.bf16, 2, nullptr, b.A1};
+        grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g1);
+        // dX = dZ W1^T: B operand = W1 [NE, d, d_ff] as [N = d, K = d_ff]
+        GemmArgs g2{b.dZ, b.W1, nullptr, b.dX, b.counts, nseg, b.e, b.S, b.Cseg, b.d, b.d_ff, 0, b.bf16, 3, nullptr, nullptr};
+        grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g2);
+    }
+    // dW2 = H^T dY  [NE, d_ff, d];  dW1 = X^T dZ  [NE, d, d_ff]
+    WgradArgs w2{b.H, b.dY, b.dW2, b.counts, b.e, b.S, b.Cseg, b.d_ff, b.d, b.bf16};
+    wgrad_simt<<<dim3((b.d + BN - 1) / BN, (b.d_ff + BM - 1) / BM, NE), NTHR, 0, st>>>(w2);
+    WgradArgs w1{b.X, b.dZ, b.dW1, b.counts, b.e, b.S, b.Cseg, b.d, b.d_ff, b.bf16};
+    wgrad_simt<<<dim3((b.d_ff + BN - 1) / BN, (b.d + BM - 1) / BM, NE), NTHR, 0, st>>>(w1);
+    WgradArgs c2{nullptr, b.dY, b.db2, b.counts, b.e, b.S, b.Cseg, 0, b.d, b.bf16};
+    colsum_kernel<<<dim3((b.d + 255) / 256, NE), 256, 0, st>>>(c2);
+    WgradArgs c1{nullptr, b.dZ, b.db1, b.counts, b.e, b.S, b.Cseg, 0, b.d_ff, b.bf16};
+    colsum_kernel<<<dim3((b.d_ff + 255) / 256, NE), 256, 0, st>>>(c1);
+    return cudaGetLastError();
 }
 
 bool ffn_simt_supported(int nseg, int d, int d_ff) {

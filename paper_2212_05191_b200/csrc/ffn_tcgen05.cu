@@ -23,6 +23,7 @@
 #include "tiles.cuh"
 
 #include <cuda.h>
+#include <string.h>
 
 namespace smile {
 namespace {
@@ -38,13 +39,23 @@ constexpr int OUT_BOX_BYTES = 32 * 32 * 2;    // per epilogue warp: 32 rows x 32
 struct TcArgs {
     const float *bias;       // [NE, N]
     __nv_bfloat16 *D;        // [rows_total, N]
+    __nv_bfloat16 *D2;       // EPI_BIAS_SAVE: the pre-activation output
     const int32_t *counts;   // [nseg]
     int nseg, e, S;
     int64_t Cseg;
     int N, K, BN;
     int gelu;
+    int mode;                  // EPI_* below
+    const __nv_bfloat16 *aux;  // EPI_DGELU: the saved pre-activation A1 [rows_total, N]
+    int stages;                // smem pipeline depth (3 when two output boxes per warp)
     int *err;
 };
+
+// Epilogue modes of the grouped GEMM.
+enum { EPI_BIAS = 0,        // D = act(acc + bias), act = GELU when gelu != 0 (forward)
+       EPI_BIAS_SAVE = 1,   // D = GELU(acc + bias) and D2 = acc + bias (training forward: H and A1)
+       EPI_DGELU = 2,       // D = acc * GELU'(aux) (backward: dZ = dH . GELU'(A1))
+       EPI_PLAIN = 3 };     // D = acc (backward: dX)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -157,6 +168,27 @@ __device__ __forceinline__ float gelu_erf(float z) {
     return fmaf(0.5f * fabsf(z), 1.0f - r, 0.5f * z);
 }
 
+// GELU'(z) = Phi(z) + z phi(z), with Phi from the same erf approximation.
+__device__ __forceinline__ float gelu_grad(float z) {
+    const float ax = fabsf(z) * 0.70710678118654752f;
+    float p = 4.30638e-5f;
+    p = fmaf(p, ax, 2.765672e-4f);
+    p = fmaf(p, ax, 1.520143e-4f);
+    p = fmaf(p, ax, 9.2705272e-3f);
+    p = fmaf(p, ax, 4.22820123e-2f);
+    p = fmaf(p, ax, 7.05230784e-2f);
+    p = fmaf(p, ax, 1.0f);
+    p = p * p;
+    p = p * p;
+    p = p * p;
+    p = p * p;
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p));
+    const float erf_abs = 1.0f - r;
+    const float Phi = 0.5f + 0.5f * copysignf(erf_abs, z);
+    return Phi + z * 0.3989422804014327f * __expf(-0.5f * z * z);
+}
+
 struct TileInfo {
     int g, mt, nt, rows;
     int64_t a_row, b_row, d_row, expert;
@@ -179,14 +211,16 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref
 
 __global__ void __launch_bounds__(NTHREADS, 1)
 ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                 const __grid_constant__ CUtensorMap mapD, TcArgs a) {
+                 const __grid_constant__ CUtensorMap mapD, const __grid_constant__ CUtensorMap mapD2, TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte aligned carve-up: [A stages][B stages][barriers][tmem holder][prefix]
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;
+    const int STAGES = a.stages;
+    const int nbox = a.mode == EPI_BIAS_SAVE ? 2 : 1;
     unsigned char *sB = sA + STAGES * A_BYTES;
-    unsigned char *sOut = sB + STAGES * B_BYTES_MAX;                 // EPI_WARPS x 2 KB
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sOut + EPI_WARPS * OUT_BOX_BYTES);
+    unsigned char *sOut = sB + STAGES * B_BYTES_MAX;                 // EPI_WARPS x nbox x 2 KB
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sOut + nbox * EPI_WARPS * OUT_BOX_BYTES);
     uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
     int *s_warp = reinterpret_cast<int *>(tmem_holder + 4);
@@ -208,6 +242,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapD)) : "memory");
+        if (nbox == 2) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapD2)) : "memory");
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
@@ -280,45 +315,90 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS;
+            const bool has_bias = a.mode == EPI_BIAS || a.mode == EPI_BIAS_SAVE;
             const float4 *bias4 = reinterpret_cast<const float4 *>(a.bias + t.expert * a.N + (int64_t)t.nt * a.BN);
-            __nv_bfloat16 *drow = a.D + (t.d_row + row) * (int64_t)a.N + (int64_t)t.nt * a.BN;
-            unsigned char *box = sOut + (warp - 4) * OUT_BOX_BYTES;
+            const int64_t dcol0 = (int64_t)t.nt * a.BN;
+            __nv_bfloat16 *drow = a.D + (t.d_row + row) * (int64_t)a.N + dcol0;
+            unsigned char *box = sOut + (warp - 4) * nbox * OUT_BOX_BYTES;
             const bool full_box = q * 32 + 32 <= t.rows;
             for (int c = c_beg; c < c_end; ++c) {
                 float v[32];
                 tmem_ld32(tbase + c * 32, v);
-                uint4 pk[4];
-                uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
+                if (has_bias) {
 #pragma unroll
-                for (int i4 = 0; i4 < 8; ++i4) {
-                    const float4 b = __ldg(bias4 + c * 8 + i4);
-                    float y0 = v[4 * i4] + b.x, y1 = v[4 * i4 + 1] + b.y;
-                    float y2 = v[4 * i4 + 2] + b.z, y3 = v[4 * i4 + 3] + b.w;
-                    if (a.gelu) { y0 = gelu_erf(y0); y1 = gelu_erf(y1); y2 = gelu_erf(y2); y3 = gelu_erf(y3); }
-                    __nv_bfloat162 h0 = __floats2bfloat162_rn(y0, y1), h1 = __floats2bfloat162_rn(y2, y3);
-                    pw[2 * i4] = *reinterpret_cast<uint32_t *>(&h0);
-                    pw[2 * i4 + 1] = *reinterpret_cast<uint32_t *>(&h1);
+                    for (int i4 = 0; i4 < 8; ++i4) {
+                        const float4 b = __ldg(bias4 + c * 8 + i4);
+                        v[4 * i4] += b.x; v[4 * i4 + 1] += b.y; v[4 * i4 + 2] += b.z; v[4 * i4 + 3] += b.w;
+                    }
+                }
+                uint4 pk[4], pk2[4];
+                uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
+                uint32_t *pw2 = reinterpret_cast<uint32_t *>(pk2);
+                if (a.mode == EPI_BIAS_SAVE) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+                        pw2[i] = *reinterpret_cast<uint32_t *>(&h);
+                    }
+                }
+                if (a.mode == EPI_DGELU && row < t.rows) {
+                    const uint4 *ap = reinterpret_cast<const uint4 *>(a.aux + (t.d_row + row) * (int64_t)a.N + dcol0 + c * 32);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint4 u = __ldg(ap + i);
+                        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+                        for (int z = 0; z < 4; ++z) {
+                            const float2 f = __bfloat1622float2(h[z]);
+                            v[8 * i + 2 * z] *= gelu_grad(f.x);
+                            v[8 * i + 2 * z + 1] *= gelu_grad(f.y);
+                        }
+                    }
+                }
+                const bool act = (a.mode == EPI_BIAS && a.gelu) || a.mode == EPI_BIAS_SAVE;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    float y0 = v[2 * i], y1 = v[2 * i + 1];
+                    if (act) { y0 = gelu_erf(y0); y1 = gelu_erf(y1); }
+                    __nv_bfloat162 h = __floats2bfloat162_rn(y0, y1);
+                    pw[i] = *reinterpret_cast<uint32_t *>(&h);
                 }
                 if (full_box) {
-                    // stage the 32 x 32 box, then one TMA tensor store (full 64 B row segments)
+                    // stage the 32 x 32 box(es), then TMA tensor stores (full 64 B row segments)
                     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     __syncwarp();
                     uint4 *srow = reinterpret_cast<uint4 *>(box + lane * 64);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) srow[i] = pk[i];
+                    if (nbox == 2) {
+                        uint4 *srow2 = reinterpret_cast<uint4 *>(box + OUT_BOX_BYTES + lane * 64);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) srow2[i] = pk2[i];
+                    }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) {
                         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                          reinterpret_cast<uint64_t>(&mapD)),
-                                     "r"(t.nt * a.BN + c * 32), "r"((int)(t.d_row + q * 32)), "r"(smem_u32(box))
+                                     "r"((int)dcol0 + c * 32), "r"((int)(t.d_row + q * 32)), "r"(smem_u32(box))
                                      : "memory");
+                        if (nbox == 2)
+                            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                             reinterpret_cast<uint64_t>(&mapD2)),
+                                         "r"((int)dcol0 + c * 32), "r"((int)(t.d_row + q * 32)),
+                                         "r"(smem_u32(box + OUT_BOX_BYTES))
+                                         : "memory");
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
                 } else if (row < t.rows) {
                     uint4 *dst = reinterpret_cast<uint4 *>(drow + c * 32);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) dst[i] = pk[i];
+                    if (nbox == 2) {
+                        uint4 *dst2 = reinterpret_cast<uint4 *>(a.D2 + (t.d_row + row) * (int64_t)a.N + dcol0 + c * 32);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) dst2[i] = pk2[i];
+                    }
                 }
             }
             tc_fence_before();
@@ -371,44 +451,80 @@ int pick_bn(int N) {
     return 0;
 }
 
-size_t smem_bytes() {
-    return 1024 + STAGES * (A_BYTES + B_BYTES_MAX) + EPI_WARPS * OUT_BOX_BYTES + (2 * STAGES + 4) * 8 + 16 + 32 * 4 +
-           (MAXSEG + 1) * 4;
+size_t smem_bytes(int stages, int nbox) {
+    return 1024 + stages * (A_BYTES + B_BYTES_MAX) + nbox * EPI_WARPS * OUT_BOX_BYTES + (2 * stages + 4) * 8 + 16 +
+           32 * 4 + (MAXSEG + 1) * 4;
 }
 
+// One grouped GEMM launch: D[rows, N] = epi(A[rows, K] . B[expert][N, K]^T).
 cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE, const float *bias, void *D,
-                        const FfnArgs &f, int N, int K, int gelu, cudaStream_t st) {
+                        void *D2, const void *aux, const FfnArgs &f, int N, int K, int mode, int gelu,
+                        cudaStream_t st) {
     const int BN = pick_bn(N);
-    CUtensorMap mA, mB, mD;
+    CUtensorMap mA, mB, mD, mD2;
     if (!make_map(&mA, A, rows_total, K, BM)) return cudaErrorNotSupported;
     if (!make_map(&mB, B, (int64_t)NE * N, K, BN)) return cudaErrorNotSupported;
     if (!make_map(&mD, D, rows_total, N, 32, 32)) return cudaErrorNotSupported;
+    mD2 = mD;
+    if (D2 && !make_map(&mD2, D2, rows_total, N, 32, 32)) return cudaErrorNotSupported;
     TcArgs a;
-    a.bias = bias; a.D = reinterpret_cast<__nv_bfloat16 *>(D); a.counts = f.counts;
+    memset(&a, 0, sizeof(a));
+    a.bias = bias; a.D = reinterpret_cast<__nv_bfloat16 *>(D); a.D2 = reinterpret_cast<__nv_bfloat16 *>(D2);
+    a.counts = f.counts;
     a.nseg = f.V * f.S * f.e; a.e = f.e; a.S = f.S; a.Cseg = f.Cseg; a.N = N; a.K = K; a.BN = BN; a.gelu = gelu;
+    a.mode = mode; a.aux = reinterpret_cast<const __nv_bfloat16 *>(aux);
+    const int nbox = mode == EPI_BIAS_SAVE ? 2 : 1;
+    a.stages = nbox == 2 ? 3 : STAGES;
     a.err = nullptr;
+    const size_t smem = smem_bytes(a.stages, nbox);
     static bool attr = false;
-    const size_t smem = smem_bytes();
     if (!attr) {
-        cudaFuncSetAttribute(ffn_gemm_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ffn_gemm_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(STAGES, 1));
         attr = true;
     }
-    ffn_gemm_tcgen05<<<f.num_sms, NTHREADS, smem, st>>>(mA, mB, mD, a);
+    ffn_gemm_tcgen05<<<f.num_sms, NTHREADS, smem, st>>>(mA, mB, mD, mD2, a);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_ffn_tcgen05(const FfnArgs &f, cudaStream_t st) {
+static bool tc_supported(const FfnArgs &f) {
     const int nseg = f.V * f.S * f.e;
-    if (!f.bf16 || nseg > MAXSEG || f.d % BK || f.d_ff % BK || !pick_bn(f.d) || !pick_bn(f.d_ff))
-        return cudaErrorNotSupported;
-    const int64_t rows_total = (int64_t)nseg * f.Cseg;
-    if (rows_total >= ((int64_t)1 << 31)) return cudaErrorNotSupported;
+    if (!f.bf16 || nseg > MAXSEG || f.d % BK || f.d_ff % BK || !pick_bn(f.d) || !pick_bn(f.d_ff)) return false;
+    return (int64_t)nseg * f.Cseg < ((int64_t)1 << 31);
+}
+
+cudaError_t launch_ffn_tcgen05(const FfnArgs &f, cudaStream_t st) {
+    if (!tc_supported(f)) return cudaErrorNotSupported;
+    const int64_t rows_total = (int64_t)f.V * f.S * f.e * f.Cseg;
     const int NE = f.V * f.e;
-    cudaError_t e = launch_gemm(f.X, rows_total, f.W1t, NE, f.b1, f.H, f, f.d_ff, f.d, 1, st);
+    cudaError_t e = launch_gemm(f.X, rows_total, f.W1t, NE, f.b1, f.H, nullptr, nullptr, f, f.d_ff, f.d, EPI_BIAS, 1, st);
     if (e != cudaSuccess) return e;
-    return launch_gemm(f.H, rows_total, f.W2t, NE, f.b2, f.Y, f, f.d, f.d_ff, 0, st);
+    return launch_gemm(f.H, rows_total, f.W2t, NE, f.b2, f.Y, nullptr, nullptr, f, f.d, f.d_ff, EPI_BIAS, 0, st);
+}
+
+// Training forward on tcgen05: GEMM1 also stores the pre-activation A1 (for GELU').
+cudaError_t launch_ffn_tcgen05_train(const FfnArgs &f, void *A1, cudaStream_t st) {
+    if (!tc_supported(f)) return cudaErrorNotSupported;
+    const int64_t rows_total = (int64_t)f.V * f.S * f.e * f.Cseg;
+    const int NE = f.V * f.e;
+    cudaError_t e = launch_gemm(f.X, rows_total, f.W1t, NE, f.b1, f.H, A1, nullptr, f, f.d_ff, f.d, EPI_BIAS_SAVE, 1, st);
+    if (e != cudaSuccess) return e;
+    return launch_gemm(f.H, rows_total, f.W2t, NE, f.b2, f.Y, nullptr, nullptr, f, f.d, f.d_ff, EPI_BIAS, 0, st);
+}
+
+// Backward data GEMMs on tcgen05 (a17): dZ = (dY W2^T) . GELU'(A1); dX = dZ W1^T.
+// W1 [NE, d, d_ff] and W2 [NE, d_ff, d] in their math layouts are the K-major B operands.
+cudaError_t launch_ffn_tcgen05_dgrad(const FfnBwdArgs &b, cudaStream_t st) {
+    FfnArgs f{};
+    f.counts = b.counts; f.V = b.V; f.S = b.S; f.e = b.e; f.Cseg = b.Cseg; f.d = b.d; f.d_ff = b.d_ff; f.bf16 = b.bf16;
+    f.num_sms = b.num_sms;
+    if (!tc_supported(f)) return cudaErrorNotSupported;
+    const int64_t rows_total = (int64_t)f.V * f.S * f.e * f.Cseg;
+    const int NE = f.V * f.e;
+    cudaError_t e = launch_gemm(b.dY, rows_total, b.W2, NE, nullptr, b.dZ, nullptr, b.A1, f, f.d_ff, f.d, EPI_DGELU, 0, st);
+    if (e != cudaSuccess) return e;
+    return launch_gemm(b.dZ, rows_total, b.W1, NE, nullptr, b.dX, nullptr, nullptr, f, f.d, f.d_ff, EPI_PLAIN, 0, st);
 }
 
 }  // namespace smile

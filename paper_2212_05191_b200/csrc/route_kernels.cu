@@ -343,7 +343,7 @@ __global__ void scan2_kernel(Rank2Args a) {
 // mbarrier) and cp.async.bulk (shared -> global, bulk groups), double-buffered so the
 // loads of batch b+1 are in flight while batch b is stored.  Rows that must be zero, or
 // scaled by the gate (a13), are rewritten in shared memory by the threads in between.
-enum MoveKind { MOVE_DISPATCH1 = 0, MOVE_DISPATCH2 = 1, MOVE_COMBINE2 = 2, MOVE_COMBINE1 = 3 };
+enum MoveKind { MOVE_DISPATCH1 = 0, MOVE_DISPATCH2 = 1, MOVE_COMBINE2 = 2, MOVE_COMBINE1 = 3, MOVE_GRAD2 = 4 };
 
 struct MoveArgs {
     int kind;
@@ -392,6 +392,18 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
                 r.dst = static_cast<char *>(a.send2) + (((int64_t)v * a.K2 + j) * a.C2 + slot) * a.rowbytes;
             }
         }
+    } else if (m.kind == MOVE_GRAD2) {
+        // gradient rows follow the forward route with the forward's final slot2 (a16)
+        const Dispatch2Args &a = m.d2;
+        const int j = a.recv_meta[g];
+        if (j >= 0 && j < a.K2) {
+            const int v = (int)(g / a.items);
+            const int slot = a.slot2[g];
+            if (slot < a.C2) {
+                r.src = static_cast<const char *>(a.recv1) + g * a.rowbytes;
+                r.dst = static_cast<char *>(a.send2) + (((int64_t)v * a.K2 + j) * a.C2 + slot) * a.rowbytes;
+            }
+        }
     } else if (m.kind == MOVE_COMBINE2) {
         const Combine2Args &a = m.c2;
         const int j = a.recv_meta[g];
@@ -410,7 +422,7 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
         r.dst = static_cast<char *>(a.out) + g * rb;
         if (s1 < a.C1) {
             r.src = static_cast<const char *>(a.back1) + (((int64_t)v * a.K1 + i) * a.C1 + s1) * rb;
-            r.scale = a.route.gate[g];
+            r.scale = a.nogate ? 1.f : a.route.gate[g];
         } else {
             r.scale = 0.f;
         }
@@ -596,6 +608,13 @@ void launch_dispatch2(const Dispatch2Args &a, cudaStream_t st) {
     if (a.items == 0) return;
     MoveArgs m{};
     m.kind = MOVE_DISPATCH2; m.rows = (int64_t)a.V * a.items; m.rowbytes = a.rowbytes; m.d2 = a;
+    launch_move(m, st);
+}
+
+void launch_grad_dispatch2(const Dispatch2Args &a, cudaStream_t st) {
+    if (a.items == 0) return;
+    MoveArgs m{};
+    m.kind = MOVE_GRAD2; m.rows = (int64_t)a.V * a.items; m.rowbytes = a.rowbytes; m.d2 = a;
     launch_move(m, st);
 }
 

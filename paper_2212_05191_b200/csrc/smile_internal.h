@@ -96,9 +96,28 @@ void launch_combine2(const Combine2Args &a, cudaStream_t st);
 
 struct Combine1Args {
     const void *back1; smile_route route; void *out; int V; int64_t T; int d; int K1; int64_t C1;
-    int bf16;
+    int bf16; int nogate;      // nogate: gradient return (a18), rows copied unscaled
 };
 void launch_combine1(const Combine1Args &a, cudaStream_t st);
+
+// a7 for gradient rows (a16): dsend2[v, j, slot2] = drecv1[v, s, c] with the forward's final slot2.
+void launch_grad_dispatch2(const Dispatch2Args &a, cudaStream_t st);
+
+// a16 + a19 (router part): combine backward at the source.
+struct CombineBwdArgs {
+    const void *gout; const void *back1; const float *logits; smile_route route; smile_stats stats;
+    void *dsend; float *dlogits; int V; int64_t T; int d; int K1, K2, KW; int64_t C1;
+    double alpha, beta, lam; int flat; int bf16;
+};
+void launch_combine_bwd(const CombineBwdArgs &a, cudaStream_t st);
+
+// a19: router weight / input gradient: dx[t] += dlogits[t] W;  dW = sum_t dlogits[t]^T x[t].
+struct RouterBwdArgs {
+    const void *x; const float *w; const float *dlogits; void *dx; float *dW; float *partial;
+    int64_t rows; int d; int KW; int nchunk; int bf16;
+};
+void launch_router_bwd(const RouterBwdArgs &a, cudaStream_t st);
+size_t router_bwd_partial_floats(int64_t rows, int d, int KW);
 
 void launch_aux(const smile_stats &s, double alpha, double beta, double *loss, int V, int K1,
                 int K2, int64_t T, int flat, cudaStream_t st);
@@ -116,6 +135,17 @@ struct FfnArgs {
     int num_sms;
 };
 void launch_ffn_simt(const FfnArgs &a, cudaStream_t st);
+
+// Training forward / backward of the expert FFN.
+struct FfnBwdArgs {
+    const void *X; const int32_t *counts; const void *A1; const void *H; const void *dY;
+    const void *W1; const void *W2;          // math layouts: W1 [NE, d, d_ff], W2 [NE, d_ff, d]
+    void *dZ; void *dX; float *dW1; float *db1; float *dW2; float *db2;
+    int V, S, e; int64_t Cseg; int d, d_ff; int bf16; int num_sms;
+};
+cudaError_t launch_ffn_bwd(const FfnBwdArgs &a, bool tc, cudaStream_t st);
+// Forward that also stores the pre-activation A1 = X W1 + b1 (training).
+cudaError_t launch_ffn_fwd_train(const FfnArgs &a, void *A1, bool tc, cudaStream_t st);
 // Returns cudaErrorNotSupported when the shape cannot run on the tcgen05 path.
 cudaError_t launch_ffn_tcgen05(const FfnArgs &a, cudaStream_t st);
 

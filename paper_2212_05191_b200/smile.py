@@ -40,7 +40,7 @@ class Shape(C.Structure):
 class Sizes(C.Structure):
     _fields_ = [("G", C.c_int32), ("V", C.c_int32), ("rank0", C.c_int32), ("K1", C.c_int32),
                 ("K2", C.c_int32), ("KW", C.c_int32), ("C1", C.c_int64), ("C2", C.c_int64),
-                ("S", C.c_int32), ("Cseg", C.c_int64), ("ws_bytes", C.c_size_t)]
+                ("S", C.c_int32), ("Cseg", C.c_int64), ("ws_bytes", C.c_size_t), ("router_partial_bytes", C.c_size_t)]
 
 
 _P = C.c_void_p
@@ -57,13 +57,18 @@ class Stats(C.Structure):
 class LayerIO(C.Structure):
     _fields_ = [("x", _P), ("logits", _P), ("w_router", _P), ("W1t", _P), ("b1", _P), ("W2t", _P),
                 ("b2", _P), ("out", _P), ("loss", _P), ("alpha", C.c_double), ("beta", C.c_double),
-                ("ws", _P)]
+                ("ws", _P), ("train", C.c_int32)]
+
+
+class GradIO(C.Structure):
+    _fields_ = [("gout", _P), ("dx", _P), ("dW_router", _P), ("W1", _P), ("W2", _P), ("dW1", _P), ("db1", _P),
+                ("dW2", _P), ("db2", _P), ("lam", C.c_double)]
 
 
 class WsView(C.Structure):
     _fields_ = [("route", Route), ("stats", Stats)] + [(k, _P) for k in (
         "counts1", "send1", "meta1", "recv1", "rmeta1", "slot2", "counts2", "send2", "recv2", "rcounts",
-        "ffn_in", "H", "Y", "ret2", "ret1", "back1")]
+        "ffn_in", "H", "Y", "ret2", "ret1", "back1", "A1", "logits", "dlogits", "rpartial")]
 
 
 def lib():
@@ -79,7 +84,9 @@ def lib():
         for name in ("smile_plan", "smile_group", "smile_exchange_plan", "smile_get_unique_id", "smile_create", "smile_destroy",
                      "smile_query", "smile_get_error", "smile_gate_inter", "smile_dispatch", "smile_gate_intra",
                      "smile_all2all", "smile_all2all_inter", "smile_all2all_intra", "smile_expert_ffn",
-                     "smile_combine", "smile_aux_loss", "smile_forward_ws", "smile_forward", "smile_forward_host"):
+                     "smile_combine", "smile_aux_loss", "smile_forward_ws", "smile_forward", "smile_forward_host",
+                     "smile_expert_ffn_train", "smile_combine_bwd", "smile_dispatch_grad", "smile_expert_ffn_bwd",
+                     "smile_combine_grad", "smile_router_bwd", "smile_backward"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -207,6 +214,8 @@ class SmileLayer:
         out["psum2"] = self._slice(w.stats.psum2, (V, self.K2), f64)
         out["counts1"] = self._slice(w.counts1, (V, self.K1), i32)
         out["rcounts"] = self._slice(w.rcounts, (V, self.S, self.e), i32)
+        out["logits"] = self._slice(w.logits, (V, T, self.KW), f32)
+        out["dlogits"] = self._slice(w.dlogits, (V, T, self.KW), f32)
         if not self.flat:
             out["rmeta1"] = self._slice(w.rmeta1, (V, self.n * self.C1), i32)
             out["slot2"] = self._slice(w.slot2, (V, self.n * self.C1), i32)
@@ -218,19 +227,26 @@ class SmileLayer:
         return self._view.route
 
     def forward(self, x, W1t, b1, W2t, b2, out, loss, logits=None, w_router=None, alpha=0.005, beta=0.005,
-                stream=None):
+                stream=None, train=False):
         if self.ws is None:
             self.alloc_workspace()
         io = LayerIO(_ptr(x), _ptr(logits), _ptr(w_router), _ptr(W1t), _ptr(b1), _ptr(W2t), _ptr(b2), _ptr(out),
-                     _ptr(loss), alpha, beta, _ptr(self.ws))
+                     _ptr(loss), alpha, beta, _ptr(self.ws), int(train))
+        self._io = io
         _check(lib().smile_forward(self._ctx, C.byref(io), _stream(stream)), "smile_forward")
+
+    def backward(self, gout, dx, W1, W2, dW1, db1, dW2, db2, dW_router=None, lam=1.0, stream=None):
+        """smile_backward after forward(..., train=True) with the same buffers."""
+        g = GradIO(_ptr(gout), _ptr(dx), _ptr(dW_router), _ptr(W1), _ptr(W2), _ptr(dW1), _ptr(db1), _ptr(dW2),
+                   _ptr(db2), lam)
+        _check(lib().smile_backward(self._ctx, C.byref(self._io), C.byref(g), _stream(stream)), "smile_backward")
 
     def forward_host(self, x_dev, host_x, W1t, b1, W2t, b2, out, loss, host_out, host_loss, logits=None,
                      host_logits=None, w_router=None, alpha=0.005, beta=0.005, stream=None):
         if self.ws is None:
             self.alloc_workspace()
         io = LayerIO(_ptr(x_dev), _ptr(logits), _ptr(w_router), _ptr(W1t), _ptr(b1), _ptr(W2t), _ptr(b2),
-                     _ptr(out), _ptr(loss), alpha, beta, _ptr(self.ws))
+                     _ptr(out), _ptr(loss), alpha, beta, _ptr(self.ws), 0)
         _check(lib().smile_forward_host(self._ctx, C.byref(io), _ptr(host_x), _ptr(host_logits), _ptr(host_out),
                                         _ptr(host_loss), _stream(stream)), "smile_forward_host")
 

@@ -1,7 +1,4 @@
 set -x
+timeout 900 python -m pytest tests/test_gpu_backward.py -x -q > gpurun_out/pytest_bwd.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_bwd.log
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --steps 30 --warmup 5 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-B="python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --mode bilevel"
-timeout 300 $B > gpurun_out/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu1.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ffn_gemm|gate1|bulk_move" -s 12 -c 8 -o gpurun_out/prof_r01c $B > gpurun_out/ncu2.log 2>&1
 echo done

@@ -31,13 +31,21 @@ def _cases(ngpu):
     return cs
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-def test_multigpu_parity():
-    n = min(torch.cuda.device_count(), 4)
+def _run(n, cases, port):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", "--master-port=29611", os.path.join(ROOT, "tests", "mgpu_worker.py"),
-           json.dumps(_cases(n))]
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "mgpu_worker.py"),
+           json.dumps(cases)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     tail = (r.stdout + r.stderr)[-4000:]
     assert r.returncode == 0, tail
     assert "MGPU_RESULT" in r.stdout, tail
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_multigpu_parity_2():
+    _run(2, _cases(2), 29611)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
+def test_multigpu_parity_4():
+    _run(4, [c for c in _cases(4) if c not in _cases(2)], 29612)
