@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay each step as a CUDA graph")
     ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling period (0 = off)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "copy"],
+                    help="peer: fused permute -> peer-store exchange (CUDA IPC over NVLink); copy: device copies / NCCL")
     return ap.parse_args()
 
 
@@ -291,8 +293,11 @@ def step(L, inp, ev=None):
         rec(7)
 
 
-def launches_per_step(L, nprocs):
+def launches_per_step(L, nprocs, exchange="copy"):
     """Kernels of libsmile launched per step (NCCL kernels not counted)."""
+    if exchange == "peer":
+        nb = 0 if nprocs == 1 else (4 if not L.flat else 2)          # barrier kernels
+        return (2 + 2 + 2 + 1 + 2 + 1 + 1 + 1 + nb) if not L.flat else (2 + 2 + 2 + 1 + 1 + nb)
     V1 = nprocs > 1 and L.V == 1
     if not L.flat:
         # gate+scan, dispatch1, [copy], rank2+scan2, dispatch2, [copy], ffn x2, [copy], combine2, [copy], combine1, aux
@@ -345,6 +350,15 @@ def run_ours(args):
             dist.broadcast(buf, 0)
             nccl_id = bytes(buf.cpu().numpy().tobytes())
         L = make_layer(cfgd, mode, world, rank, local, args.ffn, nccl_id)
+        if args.exchange == "peer":
+            def allgather(b):
+                t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(dev)
+                outs = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(outs, t)
+                return b"".join(bytes(o.cpu().numpy().tobytes()) for o in outs)
+            L.enable_peer_exchange(allgather if world > 1 else None)
+            if dist:
+                dist.barrier()
         KW = L.KW
         gen.manual_seed(1000 + rank)
         x = torch.randn(V, T, d, generator=gen, device=dev, dtype=torch.float32).to(tdt)
@@ -398,7 +412,7 @@ def run_ours(args):
         ffn_tc = cfgd["dtype"] == "bf16" and args.ffn != "simt" and smb.TCGEN05_DEFAULT
         res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, rank_ms=rank_ms, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms,
                    t_beg=t_beg, t_end=t_end,
-                   tokens=G * T, launches=launches_per_step(L, world))
+                   tokens=G * T, launches=launches_per_step(L, world, args.exchange))
         # e2e through smile_forward_host (pinned host x, D2H out + loss)
         if not args.no_e2e:
             hx = x.cpu().pin_memory()
@@ -464,7 +478,8 @@ def run_ours(args):
         "data": "synthetic (N(0,1) tokens, U(+-1/sqrt(fan_in)) random-init router and experts)",
         "config": {"workload": f"{args.config}: one {modes[0]} MoE layer fwd, {G} ranks as 2x4 (n x m), "
                                f"e={e}/rank, T={T}/rank, d={d}, d_ff={d_ff}, cf={cfgd['cf']}, fused router; "
-                               f"{V} ranks per GPU", "ranks_per_gpu": V, "mode": modes[0],
+                               f"{V} ranks per GPU; exchange={args.exchange}", "ranks_per_gpu": V, "mode": modes[0],
+                   "exchange": args.exchange,
                    "l2": "flushed (256 MiB write) before every timed step, outside its events"},
         "phase_ms": main["phase_ms"], "phase_ms_note": "per phase: max over ranks of the mean over steps",
         "rank_ms_per_step": main["rank_ms"], "kept_tokens": main["kept"],

@@ -103,6 +103,10 @@ typedef struct smile_ctx_s *smile_ctx;
 /* ---------------- context ---------------- */
 
 int          smile_version(void);
+/* sizeof of smile_shape, smile_sizes, smile_route, smile_stats, smile_layer_io,
+ * smile_ws_view, smile_grad_io, smile_xop (in that order) into out[0..n), so a binding
+ * can verify its mirrors of the structs. */
+smile_status smile_struct_sizes(int64_t *out, int32_t n);
 const char  *smile_strerror(smile_status s);
 /* Pure host function, usable without a GPU: fills *out from *shape or returns
  * SMILE_EINVAL (n, m, e, d, d_ff < 1, T < 0, cf <= 0, nprocs not dividing G, ...). */
@@ -140,6 +144,27 @@ smile_status smile_destroy(smile_ctx ctx);
 smile_status smile_query(smile_ctx ctx, smile_sizes *out);
 /* Synchronises `stream`, then returns and clears the sticky device error flag. */
 smile_status smile_get_error(smile_ctx ctx, void *stream);
+
+/* ---------------- fused permute -> peer-store exchange ----------
+ * SMILE_XCHG_COPY (default): the permutes fill send buffers and each level's All2All is an
+ * explicit exchange (device copies between ranks of one process, NCCL between processes).
+ * SMILE_XCHG_PEER: smile_forward (inference; train == 0) skips the send buffers -- the
+ * level-1 / level-2 permutes store every kept row straight into the receive buffer of its
+ * destination rank (on this GPU, or another GPU's workspace mapped with CUDA IPC and
+ * written over NVLink), the return path loads rows straight from the peer's buffers, and
+ * the four All2Alls become four process-level flag barriers over NVLink.  Only valid rows
+ * move (no capacity padding on the wire).  One node only (CUDA IPC). */
+typedef enum { SMILE_XCHG_COPY = 0, SMILE_XCHG_PEER = 1 } smile_xchg;
+/* The 72-byte IPC description of workspace `ws` (64-byte cudaIpcMemHandle of the
+ * allocation containing it + the 8-byte offset of ws inside it), to be all-gathered by
+ * the caller. */
+smile_status smile_ipc_handle(smile_ctx ctx, const void *ws, uint8_t out[72]);
+/* Registers `ws` (smile_sizes.ws_bytes, 256-byte aligned) as the workspace of every later
+ * smile_forward and selects the exchange.  PEER with nprocs > 1: `handles` = the nprocs
+ * handles from smile_ipc_handle in process order (collective; the caller must barrier all
+ * processes after this call returns, before the first smile_forward); nprocs == 1:
+ * handles may be NULL.  Synchronises the device. */
+smile_status smile_register_workspace(smile_ctx ctx, void *ws, const uint8_t *handles, int32_t xchg);
 
 /* ---------------- the steps of the layer ---------------- */
 
@@ -327,6 +352,7 @@ typedef struct {
     void *A1;                               /* [V, S, e, Cseg, d_ff] pre-activation (train) */
     float *logits; float *dlogits;          /* [V, T, KW] saved logits (train), their gradient */
     void *rpartial;                         /* router-gradient partial sums */
+    void *flags;                            /* peer-exchange barrier flags */
 } smile_ws_view;
 
 smile_status smile_forward_ws(smile_ctx ctx, void *ws, smile_ws_view *view);

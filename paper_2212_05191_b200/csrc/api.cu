@@ -23,9 +23,24 @@ using namespace smile;
         if ((x) != ncclSuccess) return SMILE_ENCCL;   \
     } while (0)
 
+#define STEP(x)                            \
+    do {                                   \
+        smile_status _s = (x);             \
+        if (_s != SMILE_OK) return _s;     \
+    } while (0)
+
 static inline cudaStream_t S(void *p) { return reinterpret_cast<cudaStream_t>(p); }
 
 extern "C" int smile_version(void) { return SMILE_VERSION; }
+
+extern "C" smile_status smile_struct_sizes(int64_t *out, int32_t n) {
+    const int64_t s[8] = {(int64_t)sizeof(smile_shape),    (int64_t)sizeof(smile_sizes),  (int64_t)sizeof(smile_route),
+                          (int64_t)sizeof(smile_stats),    (int64_t)sizeof(smile_layer_io), (int64_t)sizeof(smile_ws_view),
+                          (int64_t)sizeof(smile_grad_io),  (int64_t)sizeof(smile_xop)};
+    if (!out || n < 0) return SMILE_EINVAL;
+    for (int i = 0; i < n && i < 8; ++i) out[i] = s[i];
+    return SMILE_OK;
+}
 
 extern "C" const char *smile_strerror(smile_status s) {
     switch (s) {
@@ -101,6 +116,7 @@ static void ws_layout(const smile_shape *s, const smile_sizes *z, WsLayout *L, s
     w.logits = (float *)take(V * T * z->KW * 4);
     w.dlogits = (float *)take(V * T * z->KW * 4);
     w.rpartial = take(z->router_partial_bytes);
+    w.flags = take(3 * kMaxProcs * 8);
     if (L) L->total = o;
     if (view) *view = w;
 }
@@ -311,6 +327,10 @@ extern "C" smile_status smile_destroy(smile_ctx c) {
     cudaFree(c->d_err);
     cudaFree(c->blk_hist1); cudaFree(c->blk_off1); cudaFree(c->blk_hist2a); cudaFree(c->blk_psum);
     cudaFree(c->blk_hist2); cudaFree(c->blk_off2);
+    for (int p = 0; p < kMaxProcs; ++p)
+        if (c->h_ipc[p]) cudaIpcCloseMemHandle(c->h_ipc[p]);
+    cudaFree(c->d_bases);
+    for (int l = 0; l < 3; ++l) cudaFree(c->d_peers[l]);
     for (auto &L : c->lv) {
         cudaFree(L.d_member_local); cudaFree(L.d_mypos);
         free(L.h_member); free(L.h_mypos);
@@ -325,6 +345,98 @@ extern "C" smile_status smile_query(smile_ctx c, smile_sizes *out) {
     return SMILE_OK;
 }
 
+// ---- fused permute -> peer-store exchange ----------------------------------------
+typedef int (*GetAddressRangeFn)(void **base, size_t *size, void *ptr);   // cuMemGetAddressRange_v2
+
+extern "C" smile_status smile_ipc_handle(smile_ctx c, const void *ws, uint8_t out[72]) {
+    if (!c || !ws || !out) return SMILE_EINVAL;
+    cudaSetDevice(c->shape.device);
+    static GetAddressRangeFn range_fn = nullptr;
+    if (!range_fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return SMILE_ECUDA;
+        range_fn = reinterpret_cast<GetAddressRangeFn>(p);
+    }
+    void *base = nullptr;
+    size_t size = 0;
+    if (range_fn(&base, &size, const_cast<void *>(ws)) != 0) return SMILE_ECUDA;
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, base));
+    const uint64_t off = (uint64_t)((const char *)ws - (const char *)base);
+    memcpy(out, &h, 64);
+    memcpy(out + 64, &off, 8);
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const uint8_t *handles, int32_t xchg) {
+    if (!c || !ws || (xchg != SMILE_XCHG_COPY && xchg != SMILE_XCHG_PEER)) return SMILE_EINVAL;
+    if (((uintptr_t)ws & 255) != 0) return SMILE_ESHAPE;
+    const int P = c->shape.nprocs, me = c->shape.proc;
+    if (P > kMaxProcs) return SMILE_ENOTSUP;
+    if (xchg == SMILE_XCHG_PEER && P > 1 && !handles) return SMILE_EINVAL;
+    cudaSetDevice(c->shape.device);
+    c->reg_ws = ws;
+    c->xchg = xchg;
+    if (xchg == SMILE_XCHG_COPY) return SMILE_OK;
+    smile_ws_view w;
+    ws_layout(&c->shape, &c->sz, nullptr, &w, (char *)ws);
+    auto off = [&](const void *ptr) { return (int64_t)((const char *)ptr - (const char *)ws); };
+    c->off_flags = off(w.flags);
+    CUDA_TRY(cudaMemset(w.flags, 0, 3 * kMaxProcs * 8));
+    for (int p = 0; p < P; ++p) {
+        if (p == me) { c->h_bases[p] = (char *)ws; continue; }
+        if (c->h_bases[p]) continue;                       // already opened
+        cudaIpcMemHandle_t h;
+        uint64_t o = 0;
+        memcpy(&h, handles + (size_t)p * 72, 64);
+        memcpy(&o, handles + (size_t)p * 72 + 64, 8);
+        void *base = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+        c->h_ipc[p] = base;
+        c->h_bases[p] = (char *)base + o;
+    }
+    if (!c->d_bases) CUDA_TRY(cudaMalloc(&c->d_bases, sizeof(char *) * kMaxProcs));
+    CUDA_TRY(cudaMemcpy(c->d_bases, c->h_bases, sizeof(char *) * kMaxProcs, cudaMemcpyHostToDevice));
+    // processes each level must synchronise with: owners of the members of our ranks' groups
+    const bool bi = c->shape.mode == SMILE_BILEVEL;
+    for (int level = 0; level < 3; ++level) {
+        std::vector<int32_t> peers;
+        if ((level == 0) != !bi) {
+            std::vector<int> mem;
+            for (int v = 0; v < c->sz.V; ++v) {
+                int mp = 0;
+                group_of(c->shape.n, c->shape.m, level, c->sz.rank0 + v, mem, &mp);
+                for (int q : mem) {
+                    const int pq = q / c->sz.V;
+                    if (pq != me && std::find(peers.begin(), peers.end(), pq) == peers.end()) peers.push_back(pq);
+                }
+            }
+            std::sort(peers.begin(), peers.end());
+        }
+        c->npeers[level] = (int)peers.size();
+        if (!c->d_peers[level]) CUDA_TRY(cudaMalloc(&c->d_peers[level], sizeof(int32_t) * kMaxProcs));
+        if (!peers.empty())
+            CUDA_TRY(cudaMemcpy(c->d_peers[level], peers.data(), sizeof(int32_t) * peers.size(), cudaMemcpyHostToDevice));
+        c->epoch[level] = 0;
+    }
+    PeerMap &pm = c->peer;
+    pm.bases = c->d_bases; pm.V = c->sz.V; pm.rank0 = c->sz.rank0; pm.n = bi ? c->shape.n : 0; pm.m = c->shape.m;
+    pm.e = c->shape.e; pm.G = c->sz.G;
+    pm.off_recv1 = off(w.recv1); pm.off_rmeta1 = bi ? off(w.rmeta1) : 0; pm.off_recv2 = bi ? off(w.recv2) : 0;
+    pm.off_rcounts = off(w.rcounts); pm.off_Y = off(w.Y); pm.off_ret1 = bi ? off(w.ret1) : 0;
+    CUDA_TRY(cudaDeviceSynchronize());
+    return SMILE_OK;
+}
+
+static void peer_barrier(smile_ctx c, int level, cudaStream_t st) {
+    if (c->shape.nprocs <= 1 || c->npeers[level] == 0) return;
+    launch_peer_barrier(c->d_bases, c->off_flags, c->shape.proc, c->d_peers[level], c->npeers[level], level,
+                        ++c->epoch[level], st);
+}
+
 extern "C" smile_status smile_get_error(smile_ctx c, void *stream) {
     if (!c) return SMILE_EINVAL;
     cudaSetDevice(c->shape.device);
@@ -333,6 +445,11 @@ extern "C" smile_status smile_get_error(smile_ctx c, void *stream) {
     CUDA_TRY(cudaMemcpy(&h, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemset(c->d_err, 0, sizeof(int)));
     return (smile_status)h;
+}
+
+// Peer map of the step calls: active in SMILE_XCHG_PEER mode (smile_register_workspace).
+static inline PeerMap peer_of(smile_ctx c) {
+    return c->xchg == SMILE_XCHG_PEER ? c->peer : PeerMap{};
 }
 
 static smile_status post_launch() {
@@ -357,7 +474,7 @@ extern "C" smile_status smile_gate_inter(smile_ctx c, const void *x, const float
     Scan1Args s{};
     s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
     s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
-    s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T;
+    s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T; s.peer = peer_of(c);
     launch_scan1(s, S(stream));
     return post_launch();
 }
@@ -376,7 +493,7 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
         a.x = rows_in; a.route = *route; a.blk_off1 = c->blk_off1; a.blk_hist1 = c->blk_hist1;
         a.send = send_rows; a.meta = bi ? send_meta : nullptr;
         a.V = c->sz.V; a.T = c->shape.T; a.rowbytes = rb; a.K1 = c->sz.K1; a.C1 = c->sz.C1;
-        a.TB = c->TB1; a.nblk = c->nblk1;
+        a.TB = c->TB1; a.nblk = c->nblk1; a.peer = peer_of(c);
         launch_dispatch1(a, S(stream));
         return post_launch();
     }
@@ -387,7 +504,7 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
         Dispatch2Args a{};
         a.recv1 = rows_in; a.recv_meta = recv_meta; a.slot2 = slot2; a.blk_off2 = c->blk_off2;
         a.send2 = send_rows; a.V = c->sz.V; a.items = (int64_t)c->shape.n * c->sz.C1; a.rowbytes = rb;
-        a.K2 = c->sz.K2; a.C2 = c->sz.C2; a.nblk = c->nblk2;
+        a.K2 = c->sz.K2; a.C2 = c->sz.C2; a.nblk = c->nblk2; a.peer = peer_of(c);
         launch_dispatch2(a, S(stream));
         return post_launch();
     }
@@ -403,7 +520,7 @@ extern "C" smile_status smile_gate_intra(smile_ctx c, const int32_t *recv_meta, 
     Rank2Args a{};
     a.recv_meta = recv_meta; a.slot2 = slot2; a.blk_hist2 = c->blk_hist2; a.blk_off2 = c->blk_off2;
     a.counts2 = counts2; a.err = c->d_err; a.V = c->sz.V; a.items = (int64_t)c->shape.n * c->sz.C1;
-    a.K2 = c->sz.K2; a.nblk = c->nblk2; a.C2 = c->sz.C2;
+    a.K2 = c->sz.K2; a.nblk = c->nblk2; a.C2 = c->sz.C2; a.peer = peer_of(c);
     launch_rank2(a, S(stream));
     return post_launch();
 }
@@ -425,6 +542,12 @@ extern "C" smile_status smile_all2all(smile_ctx c, int32_t level, int32_t revers
     if (c->shape.T == 0) return SMILE_OK;
     cudaSetDevice(c->shape.device);
     cudaStream_t st = S(stream);
+    if (c->xchg == SMILE_XCHG_PEER) {
+        // the permute already stored every row at its destination (and the combine loads
+        // from its source): the All2All of the level is a barrier of its processes
+        peer_barrier(c, level, st);
+        return cudaGetLastError() == cudaSuccess ? SMILE_OK : SMILE_ECUDA;
+    }
     const int64_t rb = (int64_t)c->shape.d * (c->shape.dtype == SMILE_BF16 ? 2 : 4);
     const size_t chunk = (size_t)L.nsub * L.Csub * rb;
     const int V = c->sz.V, P = L.P;
@@ -517,7 +640,7 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
         if (!route) return SMILE_EINVAL;
         Combine1Args a{};
         a.back1 = ret_rows; a.route = *route; a.out = out; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
-        a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = bf;
+        a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = bf; a.nogate = 0; a.peer = peer_of(c);
         launch_combine1(a, S(stream));
         return post_launch();
     }
@@ -526,7 +649,7 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
         Combine2Args a{};
         a.ret2 = ret_rows; a.recv_meta = recv_meta; a.slot2 = slot2; a.ret1 = out; a.V = c->sz.V;
         a.items = (int64_t)c->shape.n * c->sz.C1; a.rowbytes = (int64_t)c->shape.d * (bf ? 2 : 4);
-        a.K2 = c->sz.K2; a.C2 = c->sz.C2;
+        a.K2 = c->sz.K2; a.C2 = c->sz.C2; a.peer = peer_of(c);
         launch_combine2(a, S(stream));
         return post_launch();
     }
@@ -649,11 +772,6 @@ extern "C" smile_status smile_forward_ws(smile_ctx c, void *ws, smile_ws_view *v
     return SMILE_OK;
 }
 
-#define STEP(x)                            \
-    do {                                   \
-        smile_status _s = (x);             \
-        if (_s != SMILE_OK) return _s;     \
-    } while (0)
 
 extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, void *stream) {
     if (!c || !io || !io->x || !io->out || !io->loss || !io->ws) return SMILE_EINVAL;
@@ -662,6 +780,7 @@ extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, voi
     STEP(smile_forward_ws(c, io->ws, &w));
     if (c->shape.T == 0) return SMILE_OK;
     const bool train = io->train != 0;
+    if (c->xchg == SMILE_XCHG_PEER && (train || io->ws != c->reg_ws)) return SMILE_ENOTSUP;
     STEP(smile_gate_inter(c, io->x, io->w_router, io->logits, (train && !io->logits) ? w.logits : nullptr, &w.route,
                           &w.stats, w.counts1, stream));
     STEP(smile_dispatch(c, 1, io->x, &w.route, nullptr, nullptr, w.send1, w.meta1, stream));
@@ -692,6 +811,7 @@ extern "C" smile_status smile_backward(smile_ctx c, const smile_layer_io *io, co
         !g->db2)
         return SMILE_EINVAL;
     if (io->w_router && !io->logits && !g->dW_router) return SMILE_EINVAL;
+    if (c->xchg == SMILE_XCHG_PEER) return SMILE_ENOTSUP;        // training uses the copy / NCCL exchange
     smile_ws_view w;
     STEP(smile_forward_ws(c, io->ws, &w));
     if (c->shape.T == 0) return SMILE_OK;

@@ -294,6 +294,12 @@ __global__ void scan1_kernel(Scan1Args a) {
             if (lane == 0) {
                 a.stats.hist1[v * a.K1 + k] = tot;
                 a.counts1[v * a.K1 + k] = (int32_t)imin64(tot, a.C1);
+                if (a.peer.bases && a.flat) {      // counts travel with the rows: rcounts[q][src][k % e]
+                    const PeerMap &P = a.peer;
+                    const int rk = P.rank0 + v, q = k / P.e;
+                    reinterpret_cast<int32_t *>(P.bases[q / P.V] + P.off_rcounts)[((int64_t)(q % P.V) * P.G + rk) * P.e + k % P.e] =
+                        (int32_t)imin64(tot, a.C1);
+                }
             }
         } else if (j < a.K1 + KS) {
             const int k = j - a.K1;
@@ -333,7 +339,15 @@ __global__ void scan2_kernel(Rank2Args a) {
     for (int k = w; k < a.K2; k += NW) {
         const int64_t o = (int64_t)v * a.nblk * a.K2 + k;
         const int tot = warp_exclusive_scan(a.blk_hist2 + o, a.nblk, a.K2, a.blk_off2 + o);
-        if (lane == 0) a.counts2[v * a.K2 + k] = (int32_t)imin64(tot, a.C2);
+        if (lane == 0) {
+            a.counts2[v * a.K2 + k] = (int32_t)imin64(tot, a.C2);
+            if (a.peer.bases) {                    // rcounts[(i, k / e)][l][k % e] of the expert rank
+                const PeerMap &P = a.peer;
+                const int rk = P.rank0 + v, i = rk / P.m, l = rk % P.m, q = i * P.m + k / P.e;
+                reinterpret_cast<int32_t *>(P.bases[q / P.V] + P.off_rcounts)[((int64_t)(q % P.V) * P.m + l) * P.e + k % P.e] =
+                    (int32_t)imin64(tot, a.C2);
+            }
+        }
     }
 }
 
@@ -374,10 +388,29 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
         const int slot = a.blk_off1[((int64_t)v * a.nblk + t / a.TB) * a.K1 + i] + a.route.slot1[g];
         a.route.slot1[g] = slot;                                      // finalise (R5, R8)
         if (slot < a.C1) {
-            const int64_t dst_row = ((int64_t)v * a.K1 + i) * a.C1 + slot;
             r.src = static_cast<const char *>(a.x) + g * a.rowbytes;
-            r.dst = static_cast<char *>(a.send) + dst_row * a.rowbytes;
-            if (a.meta) a.meta[dst_row] = a.route.dest2[g];
+            if (a.peer.bases) {
+                // peer store straight into the receive buffer of the level-1 destination
+                const PeerMap &P = a.peer;
+                const int rk = P.rank0 + v;
+                int q;
+                int64_t row;
+                if (a.meta) {                      // bi-level: (s, l) -> intermediate (i, l), chunk s
+                    const int s_ = rk / P.m, l = rk % P.m;
+                    q = i * P.m + l;
+                    row = ((int64_t)(q % P.V) * P.n + s_) * a.C1 + slot;
+                } else {                           // flat: expert E = i on rank E / e, chunk (src, E % e)
+                    q = i / P.e;
+                    row = (((int64_t)(q % P.V) * P.G + rk) * P.e + i % P.e) * a.C1 + slot;
+                }
+                char *base = P.bases[q / P.V];
+                r.dst = base + P.off_recv1 + row * a.rowbytes;
+                if (a.meta) reinterpret_cast<int32_t *>(base + P.off_rmeta1)[row] = a.route.dest2[g];
+            } else {
+                const int64_t dst_row = ((int64_t)v * a.K1 + i) * a.C1 + slot;
+                r.dst = static_cast<char *>(a.send) + dst_row * a.rowbytes;
+                if (a.meta) a.meta[dst_row] = a.route.dest2[g];
+            }
         }
     } else if (m.kind == MOVE_DISPATCH2) {
         const Dispatch2Args &a = m.d2;
@@ -389,7 +422,16 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
             a.slot2[g] = slot;
             if (slot < a.C2) {
                 r.src = static_cast<const char *>(a.recv1) + g * a.rowbytes;
-                r.dst = static_cast<char *>(a.send2) + (((int64_t)v * a.K2 + j) * a.C2 + slot) * a.rowbytes;
+                if (a.peer.bases) {
+                    // peer store into the expert rank (i, j / e), chunk (l, j % e)
+                    const PeerMap &P = a.peer;
+                    const int rk = P.rank0 + v, i = rk / P.m, l = rk % P.m;
+                    const int q = i * P.m + j / P.e;
+                    const int64_t row = (((int64_t)(q % P.V) * P.m + l) * P.e + j % P.e) * a.C2 + slot;
+                    r.dst = P.bases[q / P.V] + P.off_recv2 + row * a.rowbytes;
+                } else {
+                    r.dst = static_cast<char *>(a.send2) + (((int64_t)v * a.K2 + j) * a.C2 + slot) * a.rowbytes;
+                }
             }
         }
     } else if (m.kind == MOVE_GRAD2) {
@@ -411,7 +453,18 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
             const int v = (int)(g / a.items);
             const int s2 = a.slot2[g];
             r.dst = static_cast<char *>(a.ret1) + g * a.rowbytes;
-            if (s2 < a.C2) r.src = static_cast<const char *>(a.ret2) + (((int64_t)v * a.K2 + j) * a.C2 + s2) * a.rowbytes;
+            if (s2 < a.C2) {
+                if (a.peer.bases) {
+                    // peer load of the expert output from rank (i, j / e), chunk (l, j % e)
+                    const PeerMap &P = a.peer;
+                    const int rk = P.rank0 + v, i = rk / P.m, l = rk % P.m;
+                    const int q = i * P.m + j / P.e;
+                    const int64_t row = (((int64_t)(q % P.V) * P.m + l) * P.e + j % P.e) * a.C2 + s2;
+                    r.src = P.bases[q / P.V] + P.off_Y + row * a.rowbytes;
+                } else {
+                    r.src = static_cast<const char *>(a.ret2) + (((int64_t)v * a.K2 + j) * a.C2 + s2) * a.rowbytes;
+                }
+            }
         }
     } else {
         const Combine1Args &a = m.c1;
@@ -421,7 +474,19 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
         const int s1 = a.route.slot1[g];
         r.dst = static_cast<char *>(a.out) + g * rb;
         if (s1 < a.C1) {
-            r.src = static_cast<const char *>(a.back1) + (((int64_t)v * a.K1 + i) * a.C1 + s1) * rb;
+            if (a.peer.bases) {
+                const PeerMap &P = a.peer;
+                const int rk = P.rank0 + v;
+                if (P.n > 0) {   // bi-level: peer load from the intermediate (i, l), chunk s
+                    const int s_ = rk / P.m, l = rk % P.m, u = i * P.m + l;
+                    r.src = P.bases[u / P.V] + P.off_ret1 + (((int64_t)(u % P.V) * P.n + s_) * a.C1 + s1) * rb;
+                } else {         // flat: peer load of Y from the expert rank E / e
+                    const int q = i / P.e;
+                    r.src = P.bases[q / P.V] + P.off_Y + ((((int64_t)(q % P.V) * P.G + rk) * P.e + i % P.e) * a.C1 + s1) * rb;
+                }
+            } else {
+                r.src = static_cast<const char *>(a.back1) + (((int64_t)v * a.K1 + i) * a.C1 + s1) * rb;
+            }
             r.scale = a.nogate ? 1.f : a.route.gate[g];
         } else {
             r.scale = 0.f;
@@ -498,13 +563,22 @@ __global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) {
 
 // dispatch1 also fills meta = -1 for the empty slots [count, C1) of every destination.
 __global__ void meta_fill_kernel(Dispatch1Args a) {
+    if (!a.meta && !a.peer.bases) return;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t tot = (int64_t)a.V * a.K1 * a.C1;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot; idx += nthr) {
         const int64_t vi = idx / a.C1, cc = idx - vi * a.C1;   // vi = v*K1 + i
         const int64_t v = vi / a.K1, i = vi - v * a.K1;
         const int64_t last = ((v * a.nblk) + a.nblk - 1) * a.K1 + i;   // total = off + hist of the last block
-        if (cc >= (int64_t)a.blk_off1[last] + a.blk_hist1[last]) a.meta[idx] = -1;
+        if (cc >= (int64_t)a.blk_off1[last] + a.blk_hist1[last]) {
+            if (a.peer.bases) {
+                const PeerMap &P = a.peer;
+                const int rk = P.rank0 + (int)v, s_ = rk / P.m, l = rk % P.m, q = (int)i * P.m + l;
+                reinterpret_cast<int32_t *>(P.bases[q / P.V] + P.off_rmeta1)[((int64_t)(q % P.V) * P.n + s_) * a.C1 + cc] = -1;
+            } else {
+                a.meta[idx] = -1;
+            }
+        }
     }
 }
 
@@ -557,6 +631,29 @@ __global__ void exchange_copy_kernel(CopyXArgs a) {
     }
 }
 
+// Process-level barrier over NVLink (peer-store exchange): after a fence, write `epoch`
+// into flag[level][me] of every peer process's workspace, then wait until every peer
+// has written at least `epoch` into ours.  One thread; bounded spin (traps, never hangs).
+__global__ void peer_barrier_kernel(char *const *bases, int64_t off_flags, int me, const int32_t *peers, int npeers,
+                                    int level, long long epoch) {
+    if (threadIdx.x != 0) return;
+    __threadfence_system();
+    for (int i = 0; i < npeers; ++i) {
+        long long *f = reinterpret_cast<long long *>(bases[peers[i]] + off_flags) + level * kMaxProcs + me;
+        asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+    }
+    const long long *mine = reinterpret_cast<const long long *>(bases[me] + off_flags) + level * kMaxProcs;
+    for (int i = 0; i < npeers; ++i) {
+        long long v = 0;
+        for (uint64_t spin = 0;; ++spin) {
+            asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(mine + peers[i]) : "memory");
+            if (v >= epoch) break;
+            if (spin > (1ull << 31)) __trap();
+        }
+    }
+    __threadfence_system();
+}
+
 inline int grid_for(int64_t warps_needed, int per_block_warps, int cap) {
     int64_t b = (warps_needed + per_block_warps - 1) / per_block_warps;
     if (b < 1) b = 1;
@@ -601,7 +698,7 @@ void launch_dispatch1(const Dispatch1Args &a, cudaStream_t st) {
     MoveArgs m{};
     m.kind = MOVE_DISPATCH1; m.rows = (int64_t)a.V * a.T; m.rowbytes = a.rowbytes; m.d1 = a;
     launch_move(m, st);
-    if (a.meta) meta_fill_kernel<<<148 * 4, 256, 0, st>>>(a);
+    if (a.meta || a.peer.bases && a.peer.n > 0) meta_fill_kernel<<<148 * 4, 256, 0, st>>>(a);
 }
 
 void launch_dispatch2(const Dispatch2Args &a, cudaStream_t st) {
@@ -635,6 +732,12 @@ void launch_combine1(const Combine1Args &a, cudaStream_t st) {
 void launch_aux(const smile_stats &s, double alpha, double beta, double *loss, int V, int K1, int K2,
                 int64_t T, int flat, cudaStream_t st) {
     aux_kernel<<<(V + 127) / 128, 128, 0, st>>>(s, alpha, beta, loss, V, K1, K2, T, flat);
+}
+
+void launch_peer_barrier(char *const *bases, int64_t off_flags, int me, const int32_t *peers, int npeers, int level,
+                         long long epoch, cudaStream_t st) {
+    if (npeers <= 0) return;
+    peer_barrier_kernel<<<1, 32, 0, st>>>(bases, off_flags, me, peers, npeers, level, epoch);
 }
 
 void launch_exchange_copy(const CopyXArgs &a, cudaStream_t st) {

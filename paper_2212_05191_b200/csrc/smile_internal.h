@@ -37,6 +37,17 @@ struct Level {
     ncclComm_t comm = nullptr;          // split comm when V == 1 (inter/intra) or world
 };
 
+// Fused permute -> peer-store exchange (SMILE_XCHG_PEER): every process's workspace
+// base (its own, or a CUDA-IPC mapping over NVLink) and the byte offsets of the receive
+// buffers inside a workspace (all processes share one layout).  bases == nullptr: the
+// classic path (permute into send buffers, then an explicit exchange).
+struct PeerMap {
+    char *const *bases;                // [nprocs] device array
+    int V, rank0, n, m, e, G;
+    int64_t off_recv1, off_rmeta1, off_recv2, off_rcounts, off_Y, off_ret1;
+};
+constexpr int kMaxProcs = 64;
+
 }  // namespace smile
 
 struct smile_ctx_s {
@@ -52,6 +63,17 @@ struct smile_ctx_s {
     ncclComm_t world = nullptr, inter = nullptr, intra = nullptr;
     smile::Level lv[3];        // 0 world, 1 inter, 2 intra
     int num_sms = 148;
+    // peer-store exchange (smile_register_workspace)
+    int xchg = 0;                            // smile_xchg
+    void *reg_ws = nullptr;                  // the registered workspace
+    char **d_bases = nullptr;                // [nprocs] device array of workspace bases
+    char *h_bases[smile::kMaxProcs] = {};    // host copy (own + IPC-opened, + offset)
+    void *h_ipc[smile::kMaxProcs] = {};      // bases returned by cudaIpcOpenMemHandle
+    int64_t off_flags = 0;                   // barrier flags inside a workspace
+    int32_t *d_peers[3] = {};                // per level: processes to synchronise with
+    int npeers[3] = {};
+    long long epoch[3] = {};
+    smile::PeerMap peer{};
 };
 
 namespace smile {
@@ -67,36 +89,42 @@ void launch_gate1(const GateArgs &a, cudaStream_t st);
 struct Scan1Args {
     const int32_t *blk_hist1, *blk_hist2a; const double *blk_psum; int32_t *blk_off1;
     smile_stats stats; int32_t *counts1; int V, nblk, K1, K2, KW; int64_t C1; int flat; int64_t T;
+    PeerMap peer;
 };
 void launch_scan1(const Scan1Args &a, cudaStream_t st);
 
 struct Rank2Args {
     const int32_t *recv_meta; int32_t *slot2; int32_t *blk_hist2; int32_t *blk_off2;
     int32_t *counts2; int *err; int V; int64_t items; int K2; int nblk; int64_t C2;
+    PeerMap peer;
 };
 void launch_rank2(const Rank2Args &a, cudaStream_t st);
 
 struct Dispatch1Args {
     const void *x; smile_route route; const int32_t *blk_off1; const int32_t *blk_hist1;
     void *send; int32_t *meta; int V; int64_t T; int64_t rowbytes; int K1; int64_t C1; int TB, nblk;
+    PeerMap peer;
 };
 void launch_dispatch1(const Dispatch1Args &a, cudaStream_t st);
 
 struct Dispatch2Args {
     const void *recv1; const int32_t *recv_meta; int32_t *slot2; const int32_t *blk_off2;
     void *send2; int V; int64_t items; int64_t rowbytes; int K2; int64_t C2; int nblk;
+    PeerMap peer;
 };
 void launch_dispatch2(const Dispatch2Args &a, cudaStream_t st);
 
 struct Combine2Args {
     const void *ret2; const int32_t *recv_meta; const int32_t *slot2; void *ret1;
     int V; int64_t items; int64_t rowbytes; int K2; int64_t C2;
+    PeerMap peer;
 };
 void launch_combine2(const Combine2Args &a, cudaStream_t st);
 
 struct Combine1Args {
     const void *back1; smile_route route; void *out; int V; int64_t T; int d; int K1; int64_t C1;
     int bf16; int nogate;      // nogate: gradient return (a18), rows copied unscaled
+    PeerMap peer;
 };
 void launch_combine1(const Combine1Args &a, cudaStream_t st);
 
@@ -118,6 +146,10 @@ struct RouterBwdArgs {
 };
 void launch_router_bwd(const RouterBwdArgs &a, cudaStream_t st);
 size_t router_bwd_partial_floats(int64_t rows, int d, int KW);
+
+// Process-level barrier of one level over NVLink flags (peer-store exchange).
+void launch_peer_barrier(char *const *bases, int64_t off_flags, int me, const int32_t *peers, int npeers, int level,
+                         long long epoch, cudaStream_t st);
 
 void launch_aux(const smile_stats &s, double alpha, double beta, double *loss, int V, int K1,
                 int K2, int64_t T, int flat, cudaStream_t st);

@@ -19,6 +19,7 @@ _lib = None
 BILEVEL, FLAT = 0, 1
 FP32, BF16 = 0, 1
 FFN_AUTO, FFN_SIMT, FFN_TCGEN05 = 0, 1, 2
+XCHG_COPY, XCHG_PEER = 0, 1
 TCGEN05_DEFAULT = True    # AUTO resolves bf16 to the tcgen05 FFN (api.cu smile_expert_ffn)
 _STATUS = {0: "ok", 1: "invalid argument", 2: "shape or layout mismatch", 3: "non-finite router logit",
            4: "CUDA error", 5: "NCCL error", 6: "unsupported configuration", 7: "routing index out of range"}
@@ -68,7 +69,7 @@ class GradIO(C.Structure):
 class WsView(C.Structure):
     _fields_ = [("route", Route), ("stats", Stats)] + [(k, _P) for k in (
         "counts1", "send1", "meta1", "recv1", "rmeta1", "slot2", "counts2", "send2", "recv2", "rcounts",
-        "ffn_in", "H", "Y", "ret2", "ret1", "back1", "A1", "logits", "dlogits", "rpartial")]
+        "ffn_in", "H", "Y", "ret2", "ret1", "back1", "A1", "logits", "dlogits", "rpartial", "flags")]
 
 
 def lib():
@@ -86,8 +87,15 @@ def lib():
                      "smile_all2all", "smile_all2all_inter", "smile_all2all_intra", "smile_expert_ffn",
                      "smile_combine", "smile_aux_loss", "smile_forward_ws", "smile_forward", "smile_forward_host",
                      "smile_expert_ffn_train", "smile_combine_bwd", "smile_dispatch_grad", "smile_expert_ffn_bwd",
-                     "smile_combine_grad", "smile_router_bwd", "smile_backward"):
+                     "smile_combine_grad", "smile_router_bwd", "smile_backward", "smile_ipc_handle",
+                     "smile_register_workspace", "smile_struct_sizes"):
             getattr(L, name).restype = C.c_int
+        # the ctypes mirrors must match the C structs byte for byte
+        sizes = (C.c_int64 * 8)()
+        _check(L.smile_struct_sizes(sizes, 8), "smile_struct_sizes")
+        mine = [C.sizeof(t) for t in (Shape, Sizes, Route, Stats, LayerIO, WsView, GradIO, XOp)]
+        if list(sizes) != mine:
+            raise ImportError(f"libsmile struct sizes {list(sizes)} != binding {mine}: rebuild or fix smile.py")
         _lib = L
     return _lib
 
@@ -193,6 +201,24 @@ class SmileLayer:
         self._view = WsView()
         _check(lib().smile_forward_ws(self._ctx, _ptr(self.ws), C.byref(self._view)), "smile_forward_ws")
         return self.ws
+
+    def enable_peer_exchange(self, allgather_bytes=None):
+        """Register the workspace and switch smile_forward to the fused permute -> peer-store
+        exchange (smile_register_workspace).  With several processes, `allgather_bytes(b)`
+        must return the concatenation of every process's `b` in process order (e.g. over
+        torch.distributed); all processes must barrier after this call."""
+        if self.ws is None:
+            self.alloc_workspace()
+        buf = None
+        if self.shape.nprocs > 1:
+            h = (C.c_uint8 * 72)()
+            _check(lib().smile_ipc_handle(self._ctx, _ptr(self.ws), h), "smile_ipc_handle")
+            allh = allgather_bytes(bytes(h))
+            buf = (C.c_uint8 * len(allh)).from_buffer_copy(allh)
+        _check(lib().smile_register_workspace(self._ctx, _ptr(self.ws), buf, XCHG_PEER), "smile_register_workspace")
+
+    def disable_peer_exchange(self):
+        _check(lib().smile_register_workspace(self._ctx, _ptr(self.ws), None, XCHG_COPY), "smile_register_workspace")
 
     def _slice(self, addr, shape, dtype):
         nel = 1

@@ -28,7 +28,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     failures = []
     for c in cases:
-        case = Case(**c)
+        case = Case(**{k: v for k, v in c.items() if not k.startswith("_")})
         G, V = case.G, case.G // world
         r0 = rank * V
         buf = torch.zeros(128, dtype=torch.uint8, device=dev)
@@ -38,6 +38,17 @@ def main():
         layer = SmileLayer(case.n, case.m, case.e, case.d, case.d_ff, case.T, case.cf, case.dtype, case.mode,
                            nprocs=world, proc=rank, device=local, ffn_impl=case.ffn_impl,
                            nccl_id=bytes(buf.cpu().numpy().tobytes()))
+        if c.get("_peer"):
+            layer.alloc_workspace()
+
+            def allgather(b):
+                t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(dev)
+                outs = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(outs, t)
+                return b"".join(bytes(o.cpu().numpy().tobytes()) for o in outs)
+
+            layer.enable_peer_exchange(allgather)
+            dist.barrier()
         g = case.gpu_tensors(dev)
         e = case.e
         sl = lambda t, k=1: None if t is None else t[r0 * k:(r0 + V) * k].contiguous()

@@ -221,3 +221,28 @@ def test_tcgen05_matches_simt():
     _, ob, lb, _ = b.run_gpu()
     assert torch.equal(la, lb)
     assert_close_scaled(oa.float().cpu().numpy(), ob.float().cpu().numpy(), 1e-2, "tcgen05 vs simt")
+
+
+# ---- fused permute -> peer-store exchange (SMILE_XCHG_PEER), all ranks on one GPU -------
+
+@pytest.mark.parametrize("n,m,e,T,d,d_ff,cf,dtype,mode", [
+    (2, 4, 1, 1024, 64, 256, 1.0, "fp32", "bilevel"),
+    (4, 2, 1, 1000, 64, 128, 1.25, "bf16", "bilevel"),
+    (2, 2, 2, 257, 64, 128, 0.5, "fp32", "bilevel"),
+    (2, 4, 2, 600, 128, 256, 1.0, "bf16", "flat"),
+    (1, 4, 1, 300, 64, 128, 1.0, "fp32", "bilevel"),
+    (4, 1, 1, 300, 64, 128, 1.0, "fp32", "bilevel"),
+])
+def test_peer_exchange_matches_copy_and_oracle(n, m, e, T, d, d_ff, cf, dtype, mode):
+    from paper_2212_05191_b200 import SmileLayer
+    case = Case(n, m, e, T, d, d_ff, cf, dtype=dtype, mode=mode, dist="skewed", seed=13)
+    layer, o_copy, l_copy, err = case.run_gpu()
+    assert err == 0
+    layer.enable_peer_exchange()
+    _, o_peer, l_peer, err = case.run_gpu(layer=layer)
+    assert err == 0
+    assert torch.equal(o_copy, o_peer) and torch.equal(l_copy, l_peer)   # same arithmetic, other data path
+    r = case.oracle_route()
+    check_route(case, layer, r, l_peer)
+    ref = case.oracle_out(r)
+    assert_close_scaled(o_peer.float().cpu().numpy().reshape(-1, d), ref, 2e-2 if dtype == "bf16" else 1e-5, "peer")

@@ -21,7 +21,8 @@ def built():
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "smile.h")).read()
-    return sorted(set(re.findall(r"\b(smile_[a-z0-9_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"^\s*(?:smile_status|int|const char\s*\*)\s*\*?\s*(smile_[a-z0-9_]+)\s*\(",
+                                 src, re.M)))
 
 
 def test_exports_every_declared_symbol():

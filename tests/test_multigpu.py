@@ -28,7 +28,8 @@ def _cases(ngpu):
         cs += [dict(n=2, m=2, e=1, cf=1.0, dtype="bf16", mode="bilevel", **base),     # V=1 all NCCL
                dict(n=2, m=2, e=2, cf=1.0, dtype="fp32", mode="flat", **base),
                dict(n=2, m=4, e=1, cf=2.0, dtype="bf16", mode="bilevel", **base)]     # V=2 mixed
-    return cs
+    # the same cases through the fused permute -> peer-store exchange (CUDA IPC + NVLink)
+    return cs + [dict(c, _peer=True) for c in cs]
 
 
 def _run(n, cases, port):
