@@ -404,7 +404,8 @@ extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const ui
     const bool bi = c->shape.mode == SMILE_BILEVEL;
     for (int level = 0; level < 3; ++level) {
         std::vector<int32_t> peers;
-        if ((level == 0) != !bi) {
+        const bool used = bi ? level != 0 : level == 0;        // BILEVEL: inter + intra; FLAT: world
+        if (used) {
             std::vector<int> mem;
             for (int v = 0; v < c->sz.V; ++v) {
                 int mp = 0;

@@ -643,12 +643,16 @@ __global__ void peer_barrier_kernel(char *const *bases, int64_t off_flags, int m
         asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
     }
     const long long *mine = reinterpret_cast<const long long *>(bases[me] + off_flags) + level * kMaxProcs;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (int i = 0; i < npeers; ++i) {
         long long v = 0;
-        for (uint64_t spin = 0;; ++spin) {
+        for (;;) {
             asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(mine + peers[i]) : "memory");
             if (v >= epoch) break;
-            if (spin > (1ull << 31)) __trap();
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 10000000000ull) __trap();       // 10 s without the peer: abort, never hang
         }
     }
     __threadfence_system();

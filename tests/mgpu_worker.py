@@ -74,8 +74,11 @@ def main():
                 np.testing.assert_allclose(torch.cat(losses).cpu().numpy(), r.loss, rtol=1e-6)
             except AssertionError as ex:
                 failures.append(f"{c}: {ex}")
+        torch.cuda.synchronize()
+        dist.barrier()          # every peer is done with our workspace before it is freed
         layer.close()
-        dist.barrier()
+        if rank == 0:
+            print("MGPU_CASE_DONE", c, flush=True)
     dist.destroy_process_group()
     if rank == 0:
         print("MGPU_RESULT", json.dumps({"failures": failures, "cases": len(cases)}))
