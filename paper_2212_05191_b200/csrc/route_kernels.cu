@@ -154,7 +154,7 @@ __device__ void router_tile(const GateArgs &a, float *s_lg, float *s_w, int64_t 
 // a1-a3: level-1 gate.  grid (nblk, V), block TB threads (one token per thread).
 // smem: logits tile [TB][KW] fp32 | s_j [TB] | warp hist [NW][K1] | block hist [K1]
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 3) gate1_kernel(GateArgs a) {
+__global__ void __launch_bounds__(256, 2) gate1_kernel(GateArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *s_lg = reinterpret_cast<float *>(smem_raw);
     int *s_j = reinterpret_cast<int *>(s_lg + (size_t)a.TB * a.KW);
