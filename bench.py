@@ -37,6 +37,8 @@ CONFIGS = {
     # tag: n, m, e, T (per rank), d, d_ff, cf, dtype
     "c1": dict(n=2, m=4, e=1, T=1024, d=64, d_ff=256, cf=1.0, dtype="fp32"),
     "c2": dict(n=2, m=4, e=1, T=16384, d=768, d_ff=3072, cf=2.0, dtype="bf16"),
+    "c3": dict(n=2, m=4, e=1, T=32768, d=768, d_ff=3072, cf=1.25, dtype="bf16", train=True),
+    "c3_4x2": dict(n=4, m=2, e=1, T=32768, d=768, d_ff=3072, cf=1.25, dtype="bf16", train=True),
     "c4": dict(n=2, m=4, e=8, T=65536, d=1024, d_ff=4096, cf=2.0, dtype="bf16"),
     "c5": dict(n=2, m=4, e=16, T=8192, d=1600, d_ff=6400, cf=2.0, dtype="bf16"),
 }
@@ -293,16 +295,38 @@ def step(L, inp, ev=None):
         rec(7)
 
 
-def launches_per_step(L, nprocs, exchange="copy"):
-    """Kernels of libsmile launched per step (NCCL kernels not counted)."""
-    if exchange == "peer":
-        nb = 0 if nprocs == 1 else (4 if not L.flat else 2)          # barrier kernels
-        return (2 + 2 + 2 + 1 + 2 + 1 + 1 + 1 + nb) if not L.flat else (2 + 2 + 2 + 1 + 1 + nb)
-    V1 = nprocs > 1 and L.V == 1
-    if not L.flat:
-        # gate+scan, dispatch1, [copy], rank2+scan2, dispatch2, [copy], ffn x2, [copy], combine2, [copy], combine1, aux
-        return 2 + 1 + 2 + 1 + 2 + 1 + 1 + 1 + (0 if V1 else 4)
-    return 2 + 1 + 2 + 1 + 1 + (0 if V1 else 2)
+PHASES_TRAIN = ["fwd", "bwd"]
+
+
+def step_train(L, inp, ev=None):
+    """C3: one training step of the layer -- smile_forward(train) then smile_backward
+    (a16-a19), the router gradient included."""
+    rec = (lambda i: ev[i].record()) if ev is not None else (lambda i: None)
+    rec(0)
+    L.forward(inp["x"], inp["W1t"], inp["b1"], inp["W2t"], inp["b2"], inp["out"], inp["loss"],
+              w_router=inp["w_router"], alpha=inp["alpha"], beta=inp["beta"], train=True)
+    rec(1)
+    L.backward(inp["gout"], inp["dx"], inp["W1"], inp["W2"], inp["dW1"], inp["db1"], inp["dW2"], inp["db2"],
+               dW_router=inp["dWr"])
+    rec(2)
+
+
+def hbm_phases(res, peaks):
+    """Achieved HBM GB/s of the HBM-bound phases (per process, max-over-ranks phase time):
+    algorithmic bytes / phase time, against MEASURED_PEAKS.json hbm_gbs.  A phase's time
+    includes its small side kernels (scan, meta fill), so the fraction is a lower bound
+    for the row kernel itself."""
+    peak = peaks.get("hbm_gbs")
+    out = {}
+    for ph, b in res["hbm_bytes"].items():
+        t = res["phase_ms"].get(ph)
+        if not t:
+            continue
+        gbs = b / (t / 1e3) / 1e9
+        out[ph] = {"bytes": b, "ms": t, "GB/s": gbs, "frac": gbs / peak if peak else None}
+    out["peak_GB/s"] = peak
+    out["peak_source"] = "MEASURED_PEAKS.json hbm_gbs"
+    return out
 
 
 def run_ours(args):
@@ -319,6 +343,8 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     cfgd = CONFIGS[args.config]
+    if cfgd.get("train") and args.exchange == "peer":
+        args.exchange = "copy"                 # smile_backward runs on the copy / NCCL exchange
     G = cfgd["n"] * cfgd["m"]
     if G % world:
         raise SystemExit(f"{world} processes do not divide {G} ranks")
@@ -373,10 +399,22 @@ def run_ours(args):
         out = torch.empty_like(x)
         loss = torch.empty(V, dtype=torch.float64, device=dev)
         inp = dict(x=x, w_router=w_router, W1t=W1t, W2t=W2t, b1=b1, b2=b2, out=out, loss=loss)
-        phases = PHASES_BI if mode == "bilevel" else PHASES_FLAT
+        train = bool(cfgd.get("train"))
+        if train:
+            f32 = dict(dtype=torch.float32, device=dev)
+            inp.update(alpha=0.005 if mode == "bilevel" else 0.01, beta=0.005 if mode == "bilevel" else 0.0,
+                       gout=torch.randn(V, T, d, generator=gen, device=dev, dtype=torch.float32).to(tdt),
+                       dx=torch.empty_like(x), W1=W1t.transpose(1, 2).contiguous(), W2=W2t.transpose(1, 2).contiguous(),
+                       dW1=torch.empty(V * e, d, d_ff, **f32), db1=torch.empty(V * e, d_ff, **f32),
+                       dW2=torch.empty(V * e, d_ff, d, **f32), db2=torch.empty(V * e, d, **f32),
+                       dWr=torch.empty(KW, d, **f32))
+            step_fn = step_train
+        else:
+            step_fn = step
+        phases = PHASES_TRAIN if train else (PHASES_BI if mode == "bilevel" else PHASES_FLAT)
         nph = len(phases)
         for _ in range(args.warmup):
-            step(L, inp)
+            step_fn(L, inp)
         torch.cuda.synchronize()
         err = L.get_error()
         if err:
@@ -385,12 +423,14 @@ def run_ours(args):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
+        lc0 = smb.launch_count()
         t_beg = time.time()
         for k in range(args.steps):
             flush.zero_()                       # L2 flush outside the step's events
-            step(L, inp, evs[k])
+            step_fn(L, inp, evs[k])
         torch.cuda.synchronize()
         t_end = time.time()
+        launched = smb.launch_count() - lc0           # libsmile kernels enqueued in the timed region
         if dist:
             dist.barrier()
         ph = [[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(nph)] for k in range(args.steps)]
@@ -408,13 +448,24 @@ def run_ours(args):
         w = L.view()
         rows = int(w["rcounts"].sum().item())
         kept = rows
-        ffn_ms = phase_ms["ffn"]
+        # algorithmic HBM bytes of the routing / data-movement phases:
+        # gate reads x and writes the 24 B route record per token; every row mover reads
+        # and writes each row it moves; combine1 also writes the zero rows of drops.
+        rb = d * (2 if cfgd["dtype"] == "bf16" else 4)
+        kept1 = int(w["counts1"].sum().item())
+        hbm = {"gate1": V * T * (rb + 24), "dispatch1": 2 * kept1 * rb, "combine1": (kept1 + V * T) * rb}
+        if mode == "bilevel":
+            recv2 = int(w["counts2"].sum().item())
+            hbm.update({"dispatch2": 2 * recv2 * rb, "combine2": 2 * recv2 * rb})
+        ffn_ms = phase_ms["ffn"] if not train else None
         ffn_tc = cfgd["dtype"] == "bf16" and args.ffn != "simt" and smb.TCGEN05_DEFAULT
         res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, rank_ms=rank_ms, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms,
                    t_beg=t_beg, t_end=t_end,
-                   tokens=G * T, launches=launches_per_step(L, world, args.exchange))
+                   tokens=G * T, launches=launched, hbm_bytes=hbm, train=train)
+        if train:
+            res["hbm_bytes"] = {}
         # e2e through smile_forward_host (pinned host x, D2H out + loss)
-        if not args.no_e2e:
+        if not args.no_e2e and not train:
             hx = x.cpu().pin_memory()
             ho = torch.empty_like(hx).pin_memory()
             hl = torch.empty(V, dtype=torch.float64).pin_memory()
@@ -457,7 +508,11 @@ def run_ours(args):
     bf16_peak = peaks.get("bf16_tflops_sustained" if timed_s > 1.0 else "bf16_tflops")
     ffn_is_tensor = main["ffn_tc"]
     traffic = load_json(os.path.join(ROOT, "profiles", "traffic.json")) or {}
-    achieved = flops / (main["ffn_ms"] / 1e3) / 1e12
+    if main.get("train"):
+        flops = 12.0 * main["rows"] * d * d_ff        # expert FFN fwd (2 GEMMs) + bwd (4 GEMMs)
+        achieved = flops / (ms / 1e3) / 1e12
+    else:
+        achieved = flops / (main["ffn_ms"] / 1e3) / 1e12
     if cfgd["dtype"] == "bf16" and ffn_is_tensor:
         roof = {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
                 "frac": achieved / bf16_peak if bf16_peak else None,
@@ -468,7 +523,8 @@ def run_ours(args):
         alu_peak = 148 * 128 * 2 * clk * 1e6 / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                 "frac": achieved / alu_peak, "peak_source": f"148 SM x 128 FP32 lanes x 2 x {clk:.0f} MHz"}
-    roof["kernel"] = "smile_expert_ffn (2 grouped GEMM launches)"
+    roof["kernel"] = ("whole training step (expert FFN fwd + bwd flops / step time; wgrad on SIMT)" if main.get("train")
+                      else "smile_expert_ffn (2 grouped GEMM launches)")
     roof["traffic"] = traffic.get(f"{args.config}_{modes[0]}_ffn")
     roof["algorithmic_flops_per_step"] = flops
     line = {
@@ -476,14 +532,18 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if cfgd["dtype"] == "bf16" else "f32",
         "data": "synthetic (N(0,1) tokens, U(+-1/sqrt(fan_in)) random-init router and experts)",
-        "config": {"workload": f"{args.config}: one {modes[0]} MoE layer fwd, {G} ranks as 2x4 (n x m), "
+        "config": {"workload": f"{args.config}: one {modes[0]} MoE layer {'fwd+bwd' if main.get('train') else 'fwd'}, "
+                               f"{G} ranks as {cfgd['n']}x{cfgd['m']} (n x m), "
                                f"e={e}/rank, T={T}/rank, d={d}, d_ff={d_ff}, cf={cfgd['cf']}, fused router; "
                                f"{V} ranks per GPU; exchange={args.exchange}", "ranks_per_gpu": V, "mode": modes[0],
                    "exchange": args.exchange,
                    "l2": "flushed (256 MiB write) before every timed step, outside its events"},
         "phase_ms": main["phase_ms"], "phase_ms_note": "per phase: max over ranks of the mean over steps",
         "rank_ms_per_step": main["rank_ms"], "kept_tokens": main["kept"],
-        "roofline": roof, "gpu_launches": main["launches"] * args.steps,
+        "roofline": roof,
+        "hbm_phases": hbm_phases(main, peaks),
+        "gpu_launches": main["launches"],
+        "gpu_launches_note": "libsmile kernels launched in the timed region (smile_launch_count delta; NCCL not counted)",
         "clocks": main.get("clocks"),
     }
     if "e2e" in main:

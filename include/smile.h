@@ -103,6 +103,10 @@ typedef struct smile_ctx_s *smile_ctx;
 /* ---------------- context ---------------- */
 
 int          smile_version(void);
+/* Host-side count of kernels libsmile has launched in this process (every launch site
+ * counts itself; NCCL's and CUDA's own kernels are not included).  Monotonic; a caller
+ * takes the difference around a region to know how many library kernels it enqueued. */
+int64_t      smile_launch_count(void);
 /* sizeof of smile_shape, smile_sizes, smile_route, smile_stats, smile_layer_io,
  * smile_ws_view, smile_grad_io, smile_xop (in that order) into out[0..n), so a binding
  * can verify its mirrors of the structs. */

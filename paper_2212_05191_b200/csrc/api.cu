@@ -6,6 +6,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <algorithm>
+#include <atomic>
 #include <vector>
 
 namespace smile {
@@ -273,6 +274,15 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, shape->device);
     const int V = z.V;
     c->TB1 = gate_tokens_per_block(z.KW);
+    {
+        const char *e = getenv("SMILE_GATE_TC");
+        const bool tc_on = !(e && e[0] == '0');
+        if (tc_on && gate_tc_supported(shape->dtype == SMILE_BF16, shape->d, z.KW)) {
+            c->TB1 = 128;                       // the tensor-core gate's token tile
+            const size_t wb = (size_t)gate_tc_np(z.KW) * shape->d * 2;
+            if (cudaMalloc(&c->wsplit, wb) != cudaSuccess) { delete c; return SMILE_ECUDA; }
+        }
+    }
     c->nblk1 = (int)((shape->T + c->TB1 - 1) / c->TB1);
     const int64_t items2 = (int64_t)shape->n * z.C1;
     c->nblk2 = shape->mode == SMILE_BILEVEL ? (int)((items2 + kRank2Items - 1) / kRank2Items) : 0;
@@ -325,6 +335,7 @@ extern "C" smile_status smile_destroy(smile_ctx c) {
     if (c->intra) ncclCommDestroy(c->intra);
     if (c->world) ncclCommDestroy(c->world);
     cudaFree(c->d_err);
+    cudaFree(c->wsplit);
     cudaFree(c->blk_hist1); cudaFree(c->blk_off1); cudaFree(c->blk_hist2a); cudaFree(c->blk_psum);
     cudaFree(c->blk_hist2); cudaFree(c->blk_off2);
     for (int p = 0; p < kMaxProcs; ++p)
@@ -453,6 +464,13 @@ static inline PeerMap peer_of(smile_ctx c) {
     return c->xchg == SMILE_XCHG_PEER ? c->peer : PeerMap{};
 }
 
+namespace smile {
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace smile
+
+extern "C" int64_t smile_launch_count(void) { return (int64_t)smile::g_launches.load(); }
+
 static smile_status post_launch() {
     return cudaGetLastError() == cudaSuccess ? SMILE_OK : SMILE_ECUDA;
 }
@@ -471,7 +489,12 @@ extern "C" smile_status smile_gate_inter(smile_ctx c, const void *x, const float
     a.err = c->d_err; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
     a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1;
     a.flat = c->shape.mode == SMILE_FLAT; a.bf16 = c->shape.dtype == SMILE_BF16;
-    launch_gate1(a, S(stream));
+    if (!logits && c->wsplit) {
+        const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, S(stream));
+        if (e != cudaSuccess) return SMILE_ECUDA;
+    } else {
+        launch_gate1(a, S(stream));
+    }
     Scan1Args s{};
     s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
     s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;

@@ -140,6 +140,7 @@ void launch_combine_bwd(const CombineBwdArgs &a, cudaStream_t st) {
     int64_t warps = (int64_t)a.V * a.T;
     int grid = (int)((warps + 7) / 8);
     if (grid > 148 * 16) grid = 148 * 16;
+    note_launch();
     combine_bwd_kernel<<<grid, 256, 0, st>>>(a);
 }
 
@@ -153,7 +154,9 @@ void launch_router_bwd(const RouterBwdArgs &a0, cudaStream_t st) {
     RouterBwdArgs a = a0;
     a.nchunk = (int)((a.rows + kRbTok - 1) / kRbTok);
     dim3 grid((a.d + kRbCols - 1) / kRbCols, a.nchunk);
+    note_launch();
     router_bwd_kernel<<<grid, kRbCols, 0, st>>>(a);
+    note_launch();
     router_bwd_reduce<<<148, 256, 0, st>>>(a);
 }
 

@@ -115,8 +115,10 @@ void launch_ffn_simt(const FfnArgs &f, cudaStream_t st) {
     const int nseg = f.V * f.S * f.e;
     const int grid = f.num_sms * 4;
     GemmArgs g1{f.X, f.W1t, f.b1, f.H, f.counts, nseg, f.e, f.S, f.Cseg, f.d_ff, f.d, 1, f.bf16, 0, nullptr, nullptr};
+    note_launch();
     grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g1);
     GemmArgs g2{f.H, f.W2t, f.b2, f.Y, f.counts, nseg, f.e, f.S, f.Cseg, f.d, f.d_ff, 0, f.bf16, 0, nullptr, nullptr};
+    note_launch();
     grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g2);
 }
 
@@ -128,8 +130,10 @@ cudaError_t launch_ffn_fwd_train(const FfnArgs &f, void *A1, bool tc, cudaStream
     const int nseg = f.V * f.S * f.e;
     const int grid = f.num_sms * 4;
     GemmArgs g1{f.X, f.W1t, f.b1, f.H, f.counts, nseg, f.e, f.S, f.Cseg, f.d_ff, f.d, 1, f.bf16, 1, A1, nullptr};
+    note_launch();
     grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g1);
     GemmArgs g2{f.H, f.W2t, f.b2, f.Y, f.counts, nseg, f.e, f.S, f.Cseg, f.d, f.d_ff, 0, f.bf16, 0, nullptr, nullptr};
+    note_launch();
     grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g2);
     return cudaGetLastError();
 }
@@ -218,19 +222,25 @@ cudaError_t launch_ffn_bwd(const FfnBwdArgs &b, bool tc, cudaStream_t st) {
         const int grid = b.num_sms * 4;
         // dZ = (dY W2^T) . GELU'(A1): B operand = W2 [NE, d_ff, d] as [N = d_ff, K = d]
         GemmArgs g1{b.dY, b.W2, nullptr, b.dZ, b.counts, nseg, b.e, b.S, b.Cseg, b.d_ff, b.d, 0, b.bf16, 2, nullptr, b.A1};
+        note_launch();
         grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g1);
         // dX = dZ W1^T: B operand = W1 [NE, d, d_ff] as [N = d, K = d_ff]
         GemmArgs g2{b.dZ, b.W1, nullptr, b.dX, b.counts, nseg, b.e, b.S, b.Cseg, b.d, b.d_ff, 0, b.bf16, 3, nullptr, nullptr};
+        note_launch();
         grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g2);
     }
     // dW2 = H^T dY  [NE, d_ff, d];  dW1 = X^T dZ  [NE, d, d_ff]
     WgradArgs w2{b.H, b.dY, b.dW2, b.counts, b.e, b.S, b.Cseg, b.d_ff, b.d, b.bf16};
+    note_launch();
     wgrad_simt<<<dim3((b.d + BN - 1) / BN, (b.d_ff + BM - 1) / BM, NE), NTHR, 0, st>>>(w2);
     WgradArgs w1{b.X, b.dZ, b.dW1, b.counts, b.e, b.S, b.Cseg, b.d, b.d_ff, b.bf16};
+    note_launch();
     wgrad_simt<<<dim3((b.d_ff + BN - 1) / BN, (b.d + BM - 1) / BM, NE), NTHR, 0, st>>>(w1);
     WgradArgs c2{nullptr, b.dY, b.db2, b.counts, b.e, b.S, b.Cseg, 0, b.d, b.bf16};
+    note_launch();
     colsum_kernel<<<dim3((b.d + 255) / 256, NE), 256, 0, st>>>(c2);
     WgradArgs c1{nullptr, b.dZ, b.db1, b.counts, b.e, b.S, b.Cseg, 0, b.d_ff, b.bf16};
+    note_launch();
     colsum_kernel<<<dim3((b.d_ff + 255) / 256, NE), 256, 0, st>>>(c1);
     return cudaGetLastError();
 }

@@ -21,14 +21,18 @@
 // the A tile and the expert's weights in L2.  One CTA per SM (grid = #SMs).
 #include "smile_internal.h"
 #include "tiles.cuh"
+#include "tc_util.cuh"
 
 #include <cuda.h>
+#include <stdlib.h>
 #include <string.h>
 
 namespace smile {
 namespace {
 
-constexpr int BM = 128, BK = 64, STAGES = 4, MAXSEG = 1024;
+using namespace tc;
+
+constexpr int BM = 128, BK = 64, MAXSEG = 1024;
 constexpr int EPI_WARPS = 8;                  // 2 warps per TMEM lane quadrant, split by columns
 constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
@@ -57,95 +61,6 @@ enum { EPI_BIAS = 0,        // D = act(acc + bias), act = GELU when gelu != 0 (f
        EPI_DGELU = 2,       // D = acc * GELU'(aux) (backward: dZ = dH . GELU'(A1))
        EPI_PLAIN = 3 };     // D = acc (backward: dX)
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t ok = 0;
-    for (uint32_t spin = 0;; ++spin) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(bar), "r"(parity)
-            : "memory");
-        if (ok) return;
-        if (spin > (1u << 26)) __trap();   // never hang the GPU: a lost arrival aborts the kernel
-    }
-}
-
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-        : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// Shared-memory matrix descriptor of a K-major SWIZZLE_128B tile (rows of 64 bf16 =
-// 128 B, 8-row atoms 1024 B apart): start>>4, LBO = 16 B (unused for this layout),
-// SBO = 1024 B, version 1 (sm_100), layout type 2 = SWIZZLE_128B.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-    d |= (uint64_t)1 << 16;
-    d |= (uint64_t)(1024 >> 4) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)2 << 61;
-    return d;
-}
-
-// kind::f16 instruction descriptor: D = F32, A = B = BF16, both K-major, M = 128, N.
-__device__ __forceinline__ uint32_t make_idesc(int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
 // GELU(z) = z Phi(z) = 0.5 z + 0.5 |z| erf(|z| / sqrt 2) (R21, erf form).  erf by Abramowitz &
 // Stegun 7.1.28, 1 - (1 + a1 x + ... + a6 x^6)^-16: |error| <= 1.8e-6 on erf and 8.8e-7 on GELU
 // over all z (checked against scipy in fp32 emulation), ~14 instructions with one
@@ -166,6 +81,57 @@ __device__ __forceinline__ float gelu_erf(float z) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p));
     return fmaf(0.5f * fabsf(z), 1.0f - r, 0.5f * z);
+}
+
+// The same GELU on a pair of values with Blackwell's packed fp32x2 pipe (FFMA2 / FMUL2:
+// two lanes of fp32 arithmetic per instruction, identical rounding per lane), which
+// halves the epilogue's ALU work -- the bias + GELU epilogue of the first FFN GEMM is
+// otherwise slower than its MMAs.  The polynomial is evaluated directly in |z| with the
+// coefficients a_i / sqrt(2)^i; (1 + ...)^-16 and the final combine as above.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pack2(float a, float b) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void unpack2(f32x2 r, float &a, float &b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f32x2 splat2(float a) { return pack2(a, a); }
+
+__device__ __forceinline__ f32x2 gelu_erf2(f32x2 z) {
+    const f32x2 az = z & 0x7fffffff7fffffffull;
+    // a_i / sqrt(2)^i, a_i of A&S 7.1.28
+    f32x2 p = splat2(4.30638e-5f * 0.125f);
+    p = fma2(p, az, splat2(2.765672e-4f * 0.17677669529663688f));
+    p = fma2(p, az, splat2(1.520143e-4f * 0.25f));
+    p = fma2(p, az, splat2(9.2705272e-3f * 0.35355339059327373f));
+    p = fma2(p, az, splat2(4.22820123e-2f * 0.5f));
+    p = fma2(p, az, splat2(7.05230784e-2f * 0.70710678118654752f));
+    p = fma2(p, az, splat2(1.0f));
+    p = mul2(p, p);
+    p = mul2(p, p);
+    p = mul2(p, p);
+    p = mul2(p, p);
+    float p0, p1, r0, r1;
+    unpack2(p, p0, p1);
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(p0));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(p1));
+    const f32x2 erfa = fma2(pack2(r0, r1), splat2(-1.0f), splat2(1.0f));   // erf(|z| / sqrt 2)
+    return mul2(fma2(az, erfa, z), splat2(0.5f));                          // (z + |z| erf) / 2
 }
 
 // GELU'(z) = Phi(z) + z phi(z), with Phi from the same erf approximation.
@@ -194,7 +160,11 @@ struct TileInfo {
     int64_t a_row, b_row, d_row, expert;
 };
 
-__device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref, int tile, int ntn) {
+// Tile `tile` of the work list: TM = CG * 128 rows of one segment x BN columns.  For a
+// CTA pair, `rank` selects this CTA's 128-row half of A and BN/2-row half of B; `rows`
+// is the number of valid rows of this CTA's half (may be <= 0).
+template <int CG>
+__device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref, int tile, int ntn, int rank) {
     TileInfo t;
     t.nt = tile % ntn;
     const int mtg = tile / ntn;
@@ -202,24 +172,30 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref
     t.mt = mtg - s_pref[t.g];
     const int v = t.g / (a.S * a.e), k = t.g % a.e;
     t.expert = (int64_t)v * a.e + k;
-    t.rows = min(BM, a.counts[t.g] - t.mt * BM);
-    t.a_row = (int64_t)t.g * a.Cseg + (int64_t)t.mt * BM;
+    const int r0 = t.mt * (BM * CG) + rank * BM;
+    t.rows = min(BM, a.counts[t.g] - r0);
+    t.a_row = (int64_t)t.g * a.Cseg + r0;
     t.d_row = t.a_row;
-    t.b_row = t.expert * a.N + (int64_t)t.nt * a.BN;
+    t.b_row = t.expert * a.N + (int64_t)t.nt * a.BN + rank * (a.BN / CG);
     return t;
 }
 
+// CG = 1: one CTA per tile (M = 128).  CG = 2: a CTA pair (cluster of 2) per tile
+// (M = 256, tcgen05.mma.cta_group::2 issued by the leader), each CTA loading half of A
+// and half of B, which halves the shared-memory operand traffic per SM.
+template <int CG>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ CUtensorMap mapD, const __grid_constant__ CUtensorMap mapD2, TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte aligned carve-up: [A stages][B stages][barriers][tmem holder][prefix]
+    // 1024-byte aligned carve-up: [A stages][B stages][out boxes][barriers][tmem holder][prefix]
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;
     const int STAGES = a.stages;
     const int nbox = a.mode == EPI_BIAS_SAVE ? 2 : 1;
+    const int b_stage_bytes = B_BYTES_MAX / CG;
     unsigned char *sB = sA + STAGES * A_BYTES;
-    unsigned char *sOut = sB + STAGES * B_BYTES_MAX;                 // EPI_WARPS x nbox x 2 KB
+    unsigned char *sOut = sB + STAGES * b_stage_bytes;                // EPI_WARPS x nbox x 2 KB
     uint64_t *bars = reinterpret_cast<uint64_t *>(sOut + nbox * EPI_WARPS * OUT_BOX_BYTES);
     uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
@@ -227,6 +203,9 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     int *s_pref = s_warp + 32;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
@@ -234,7 +213,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&tfull[s]), 1);
-            mbar_init(smem_u32(&tempty[s]), EPI_WARPS);
+            mbar_init(smem_u32(&tempty[s]), CG * EPI_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -245,43 +224,60 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         if (nbox == 2) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapD2)) : "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             smem_u32(tmem_holder))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             smem_u32(tmem_holder))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
-    tile_prefix<BM>(a.counts, a.nseg, s_pref, s_warp);   // ends with __syncthreads
+    tile_prefix<BM * CG>(a.counts, a.nseg, s_pref, s_warp);   // ends with __syncthreads
+    if (CG == 2) cluster_sync_all();                         // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const int ntn = a.N / a.BN;
     const int total = s_pref[a.nseg] * ntn;
     const int nk = a.K / BK;
-    const uint32_t b_bytes = (uint32_t)a.BN * BK * 2;
+    const uint32_t b_bytes = (uint32_t)(a.BN / CG) * BK * 2;
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- TMA producer ----------------
+            // ---------------- TMA producer (both CTAs of a pair) ----------------
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-                const TileInfo t = tile_info(a, s_pref, tile, ntn);
+            for (int tile = cid; tile < total; tile += ncl) {
+                const TileInfo t = tile_info<CG>(a, s_pref, tile, ntn, rank);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full[stage]);
-                    mbar_arrive_tx(fb, A_BYTES + b_bytes);
-                    tma_load_2d(smem_u32(sA + stage * A_BYTES), &mapA, kb * BK, (int)t.a_row, fb);
-                    tma_load_2d(smem_u32(sB + stage * B_BYTES_MAX), &mapB, kb * BK, (int)t.b_row, fb);
+                    if (CG == 1) {
+                        mbar_arrive_tx(fb, A_BYTES + b_bytes);
+                        tma_load_2d(smem_u32(sA + stage * A_BYTES), &mapA, kb * BK, (int)t.a_row, fb);
+                        tma_load_2d(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)t.b_row, fb);
+                    } else {
+                        // the leader's full barrier counts the bytes of both CTAs' loads
+                        if (leader) mbar_arrive_tx(fb, CG * (A_BYTES + b_bytes));
+                        const uint32_t fbl = mapa_shared(fb, 0);
+                        tma_load_2d_pair(smem_u32(sA + stage * A_BYTES), &mapA, kb * BK, (int)t.a_row, fbl);
+                        tma_load_2d_pair(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)t.b_row, fbl);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer (single thread) ----------------
-            const uint32_t idesc = make_idesc(a.BN);
+        if (lane == 0 && leader) {
+            // ---------------- MMA issuer (single thread of the leader) ----------------
+            const uint32_t idesc = make_idesc(BM * CG, a.BN);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+            for (int tile = cid; tile < total; tile += ncl, ++it) {
                 const int acc = it & 1;
                 const uint32_t use = (uint32_t)(it >> 1) & 1;
                 mbar_wait(smem_u32(&tempty[acc]), use ^ 1);
@@ -291,14 +287,21 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     mbar_wait(smem_u32(&full[stage]), phase);
                     tc_fence_after();
                     const uint64_t ad = sw128_desc(smem_u32(sA + stage * A_BYTES));
-                    const uint64_t bd = sw128_desc(smem_u32(sB + stage * B_BYTES_MAX));
+                    const uint64_t bd = sw128_desc(smem_u32(sB + stage * b_stage_bytes));
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)   // +32 B along K inside the 128 B swizzle atom
-                        mma_bf16(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (kb | k) ? 1u : 0u);
-                    mma_commit(smem_u32(&empty[stage]));
+                    for (int k = 0; k < BK / 16; ++k) {   // +32 B along K inside the 128 B swizzle atom
+                        if (CG == 1)
+                            mma_bf16(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (kb | k) ? 1u : 0u);
+                        else
+                            mma_bf16_pair(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc,
+                                          (kb | k) ? 1u : 0u);
+                    }
+                    if (CG == 1) mma_commit(smem_u32(&empty[stage]));
+                    else mma_commit_pair(smem_u32(&empty[stage]));
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(smem_u32(&tfull[acc]));
+                if (CG == 1) mma_commit(smem_u32(&tfull[acc]));
+                else mma_commit_pair(smem_u32(&tfull[acc]));
             }
         }
     } else if (warp >= 4) {
@@ -309,8 +312,8 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         const int nch = a.BN / 32;
         const int c_beg = half ? (nch + 1) / 2 : 0, c_end = half ? nch : (nch + 1) / 2;
         int it = 0;
-        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
-            const TileInfo t = tile_info(a, s_pref, tile, ntn);
+        for (int tile = cid; tile < total; tile += ncl, ++it) {
+            const TileInfo t = tile_info<CG>(a, s_pref, tile, ntn, rank);
             const int acc = it & 1;
             mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
             tc_fence_after();
@@ -321,14 +324,18 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             __nv_bfloat16 *drow = a.D + (t.d_row + row) * (int64_t)a.N + dcol0;
             unsigned char *box = sOut + (warp - 4) * nbox * OUT_BOX_BYTES;
             const bool full_box = q * 32 + 32 <= t.rows;
-            for (int c = c_beg; c < c_end; ++c) {
+            const bool any_row = q * 32 < t.rows;
+            for (int c = c_beg; c < c_end && any_row; ++c) {
                 float v[32];
                 tmem_ld32(tbase + c * 32, v);
                 if (has_bias) {
 #pragma unroll
                     for (int i4 = 0; i4 < 8; ++i4) {
                         const float4 b = __ldg(bias4 + c * 8 + i4);
-                        v[4 * i4] += b.x; v[4 * i4 + 1] += b.y; v[4 * i4 + 2] += b.z; v[4 * i4 + 3] += b.w;
+                        const f32x2 lo = add2(pack2(v[4 * i4], v[4 * i4 + 1]), pack2(b.x, b.y));
+                        const f32x2 hi = add2(pack2(v[4 * i4 + 2], v[4 * i4 + 3]), pack2(b.z, b.w));
+                        unpack2(lo, v[4 * i4], v[4 * i4 + 1]);
+                        unpack2(hi, v[4 * i4 + 2], v[4 * i4 + 3]);
                     }
                 }
                 uint4 pk[4], pk2[4];
@@ -359,7 +366,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     float y0 = v[2 * i], y1 = v[2 * i + 1];
-                    if (act) { y0 = gelu_erf(y0); y1 = gelu_erf(y1); }
+                    if (act) unpack2(gelu_erf2(pack2(y0, y1)), y0, y1);
                     __nv_bfloat162 h = __floats2bfloat162_rn(y0, y1);
                     pw[i] = *reinterpret_cast<uint32_t *>(&h);
                 }
@@ -403,57 +410,52 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+            if (lane == 0) {
+                if (CG == 1) mbar_arrive(smem_u32(&tempty[acc]));
+                else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));   // the leader's MMA waits on it
+            }
         }
     }
     if (warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncthreads();
+    if (CG == 2) cluster_sync_all();          // no remote arrive / MMA into a CTA that has left
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+        if (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
     }
 }
 
 // ---- host: tensor maps ------------------------------------------------------------
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiledFn>(p);
-    }
-    return fn;
-}
-
-// 2D bf16 row-major [rows, K] map with a (box_cols x box_rows) box, SWIZZLE_128B for the
-// 64-column operand boxes, none for the 32 x 32 output boxes.
-bool make_map(CUtensorMap *m, const void *ptr, int64_t rows, int64_t K, int box_rows, int box_cols = BK) {
-    EncodeTiledFn fn = encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == BK ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 int pick_bn(int N) {
     for (int bn = 256; bn >= 32; bn -= 32)
         if (N % bn == 0) return bn;
     return 0;
 }
 
-size_t smem_bytes(int stages, int nbox) {
-    return 1024 + stages * (A_BYTES + B_BYTES_MAX) + nbox * EPI_WARPS * OUT_BOX_BYTES + (2 * stages + 4) * 8 + 16 +
-           32 * 4 + (MAXSEG + 1) * 4;
+size_t smem_bytes(int CG, int stages, int nbox) {
+    return 1024 + stages * (A_BYTES + B_BYTES_MAX / CG) + nbox * EPI_WARPS * OUT_BOX_BYTES + (2 * stages + 4) * 8 +
+           16 + 32 * 4 + (MAXSEG + 1) * 4;
+}
+
+constexpr size_t kSmemLimit = 227 * 1024;
+
+int pick_stages(int CG, int nbox) {
+    int st = 8;
+    while (st > 2 && smem_bytes(CG, st, nbox) > kSmemLimit) --st;
+    return st;
+}
+
+// CTA pairs unless disabled (SMILE_FFN_CTA_PAIR=0) or the grid is odd.
+int pick_cg(int num_sms, int BN) {
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("SMILE_FFN_CTA_PAIR");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    return (env && num_sms >= 2 && (BN / 2) % 16 == 0) ? 2 : 1;
 }
 
 // One grouped GEMM launch: D[rows, N] = epi(A[rows, K] . B[expert][N, K]^T).
@@ -461,9 +463,10 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
                         void *D2, const void *aux, const FfnArgs &f, int N, int K, int mode, int gelu,
                         cudaStream_t st) {
     const int BN = pick_bn(N);
+    const int CG = pick_cg(f.num_sms, BN);
     CUtensorMap mA, mB, mD, mD2;
     if (!make_map(&mA, A, rows_total, K, BM)) return cudaErrorNotSupported;
-    if (!make_map(&mB, B, (int64_t)NE * N, K, BN)) return cudaErrorNotSupported;
+    if (!make_map(&mB, B, (int64_t)NE * N, K, BN / CG)) return cudaErrorNotSupported;
     if (!make_map(&mD, D, rows_total, N, 32, 32)) return cudaErrorNotSupported;
     mD2 = mD;
     if (D2 && !make_map(&mD2, D2, rows_total, N, 32, 32)) return cudaErrorNotSupported;
@@ -474,15 +477,38 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     a.nseg = f.V * f.S * f.e; a.e = f.e; a.S = f.S; a.Cseg = f.Cseg; a.N = N; a.K = K; a.BN = BN; a.gelu = gelu;
     a.mode = mode; a.aux = reinterpret_cast<const __nv_bfloat16 *>(aux);
     const int nbox = mode == EPI_BIAS_SAVE ? 2 : 1;
-    a.stages = nbox == 2 ? 3 : STAGES;
+    a.stages = pick_stages(CG, nbox);
     a.err = nullptr;
-    const size_t smem = smem_bytes(a.stages, nbox);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(ffn_gemm_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(STAGES, 1));
-        attr = true;
+    const size_t smem = smem_bytes(CG, a.stages, nbox);
+    if (CG == 2) {
+        static bool attr2 = false;
+        if (!attr2) {
+            cudaFuncSetAttribute(ffn_gemm_tcgen05<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
+            attr2 = true;
+        }
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof(cfg));
+        cfg.gridDim = dim3((unsigned)(f.num_sms & ~1));
+        cfg.blockDim = dim3(NTHREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attrs[1];
+        attrs[0].id = cudaLaunchAttributeClusterDimension;
+        attrs[0].val.clusterDim.x = 2;
+        attrs[0].val.clusterDim.y = 1;
+        attrs[0].val.clusterDim.z = 1;
+        cfg.attrs = attrs;
+        cfg.numAttrs = 1;
+        note_launch();
+        return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<2>, mA, mB, mD, mD2, a);
     }
-    ffn_gemm_tcgen05<<<f.num_sms, NTHREADS, smem, st>>>(mA, mB, mD, mD2, a);
+    static bool attr1 = false;
+    if (!attr1) {
+        cudaFuncSetAttribute(ffn_gemm_tcgen05<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
+        attr1 = true;
+    }
+    note_launch();
+    ffn_gemm_tcgen05<1><<<f.num_sms, NTHREADS, smem, st>>>(mA, mB, mD, mD2, a);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,250 @@
+// gate_tcgen05.cu -- the level-1 gate with the router on Blackwell tensor cores (SURVEY
+// §8(a) a1-a3, bf16 tokens, fused router).
+//
+// a1 (Eq. 1; tied routers W_p, W_q) is logit[t, k] = sum_c x[t, c] W[k, c]
+// with fp32 W and, by R3/R23, fp32 logits.  The tokens are bf16; the router rows are
+// split exactly into three bf16 pieces W = W^(0) + W^(1) + W^(2) (each piece the bf16
+// rounding of the remainder, so the split is exact to ~2^-27 |W|), every product
+// x * W^(p) is exact in fp32, and the tensor core accumulates in fp32: the logits match
+// an fp32 dot product to within fp32 accumulation error, while the token stream runs
+// at HBM speed on the tensor pipe instead of the FMA pipe (which cannot keep up once
+// K1 + K2 reaches a few tens: SURVEY §7 hard part 4).
+//
+// One persistent, warp-specialised kernel (grid = min(#tiles, #SMs), 256 threads):
+//   warp 0      TMA producer: the tile's x block (128 tokens x 64 columns, SWIZZLE_128B)
+//               and the matching block of the split router (NP x 64), into an smem ring
+//   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M = 128 tokens,
+//               N = NP = 4 * KW (columns 4k..4k+2 hold the three pieces of logit k),
+//               into a double-buffered TMEM accumulator
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue: tcgen05.ld the tile's accumulator (thread = token), sum the
+//               three pieces, logits to smem, release the accumulator, then the gate's
+//               phases B and C (gate_common.cuh) on named barrier 1.
+// Tiles are 128 consecutive tokens of one rank, the same tiles as the capacity scan's
+// (TB1 = 128): tile index = v * nblk + blk.
+#include "smile_internal.h"
+#include "gate_common.cuh"
+#include "tc_util.cuh"
+
+#include <string.h>
+
+namespace smile {
+namespace {
+
+using namespace tc;
+
+constexpr int GT_BM = 128, GT_BK = 64;
+constexpr int GT_THREADS = 256;
+constexpr int GT_A_BYTES = GT_BM * GT_BK * 2;   // 16 KB per stage
+constexpr int GT_MAX_NP = 384;                  // 4 * KW <= 384 (KW <= 96)
+
+// W fp32 [KW, d] -> Wb bf16 [NP, d]: row 4k+p = piece p of W[k] (p < 3), row 4k+3 and
+// rows >= 4 KW zero.  r0 = W, piece_p = bf16_rn(r_p), r_{p+1} = r_p - piece_p (exact).
+__global__ void router_split_kernel(const float *__restrict__ w, __nv_bfloat16 *__restrict__ wb, int KW, int d,
+                                    int NP) {
+    const int64_t n = (int64_t)NP * d;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / d), c = (int)(i - (int64_t)r * d);
+        const int k = r >> 2, p = r & 3;
+        float out = 0.f;
+        if (k < KW && p < 3) {
+            float rem = w[(int64_t)k * d + c];
+            for (int q = 0; q < p; ++q) rem -= __bfloat162float(__float2bfloat16_rn(rem));
+            out = rem;
+        }
+        wb[i] = __float2bfloat16_rn(out);
+    }
+}
+
+struct GateTcArgs {
+    GateArgs g;
+    int NP;          // accumulator columns (4 * KW rounded up to 32)
+    int nbuf;        // TMEM accumulator buffers (2 when 2 * NP <= 512)
+    int stages;
+    int ntiles;
+};
+
+__global__ void __launch_bounds__(GT_THREADS, 1)
+gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, GateTcArgs ta) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const GateArgs &a = ta.g;
+    const int NP = ta.NP, ST = ta.stages, KW = a.KW;
+    const int b_bytes = NP * GT_BK * 2;
+    unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char *sA = base;
+    unsigned char *sB = sA + ST * GT_A_BYTES;
+    float *s_lg = reinterpret_cast<float *>(sB + ST * b_bytes);              // [128][KW]
+    int *s_j = reinterpret_cast<int *>(s_lg + GT_BM * KW);                   // [128]
+    int *s_wh = s_j + GT_BM;                                                 // [4][K1]
+    int *s_bh = s_wh + 4 * a.K1;                                             // [K1]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(
+        ((uintptr_t)(s_bh + a.K1) + 7) & ~(uintptr_t)7);
+    uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(smem_u32(&full[s]), 1);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(smem_u32(&tfull[s]), 1);
+            mbar_init(smem_u32(&tempty[s]), 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapX)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapW)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    const int nk = a.d / GT_BK;
+    const int nbuf = ta.nbuf;
+    const int nchunk_n = NP > 256 ? 2 : 1;
+    const int NPc = NP / nchunk_n;                     // N of one MMA
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
+                const int v = tile / a.nblk, blk = tile - v * a.nblk;
+                const int row0 = (int)((int64_t)v * a.T + (int64_t)blk * GT_BM);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                    const uint32_t fb = smem_u32(&full[stage]);
+                    mbar_arrive_tx(fb, GT_A_BYTES + b_bytes);
+                    tma_load_2d(smem_u32(sA + stage * GT_A_BYTES), &mapX, kb * GT_BK, row0, fb);
+                    for (int h = 0; h < nchunk_n; ++h)
+                        tma_load_2d(smem_u32(sB + stage * b_bytes + h * NPc * 128), &mapW, kb * GT_BK, h * NPc, fb);
+                    if (++stage == ST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer ----------------
+            const uint32_t idesc = make_idesc(GT_BM, NPc);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
+                const int buf = it % nbuf;
+                const uint32_t use = (uint32_t)(it / nbuf) & 1;
+                mbar_wait(smem_u32(&tempty[buf]), use ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + buf * NP;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(smem_u32(&full[stage]), phase);
+                    tc_fence_after();
+                    const uint64_t ad = sw128_desc(smem_u32(sA + stage * GT_A_BYTES));
+#pragma unroll
+                    for (int k = 0; k < GT_BK / 16; ++k)
+                        for (int h = 0; h < nchunk_n; ++h) {
+                            const uint64_t bd = sw128_desc(smem_u32(sB + stage * b_bytes + h * NPc * 128));
+                            mma_bf16(tmem_d + h * NPc, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc,
+                                     (kb | k) ? 1u : 0u);
+                        }
+                    mma_commit(smem_u32(&empty[stage]));
+                    if (++stage == ST) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(smem_u32(&tfull[buf]));
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: thread = token (TMEM lane) ----------------
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
+            const int v = tile / a.nblk, blk = tile - v * a.nblk;
+            const int64_t t0 = (int64_t)blk * GT_BM;
+            const int nt = (int)(a.T - t0 < GT_BM ? a.T - t0 : GT_BM);
+            const int64_t tok0 = (int64_t)v * a.T + t0;
+            const int buf = it % nbuf;
+            mbar_wait(smem_u32(&tfull[buf]), (uint32_t)(it / nbuf) & 1);
+            tc_fence_after();
+            const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + buf * NP;
+            for (int c = 0; c < NP / 32; ++c) {
+                float vv[32];
+                tmem_ld32(tb + c * 32, vv);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int k = c * 8 + i;
+                    if (k < KW) s_lg[row * KW + k] = (vv[4 * i] + vv[4 * i + 1]) + vv[4 * i + 2];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+            EpiSync::sync();
+            if (a.logits_out) {
+                for (int i = EpiSync::tid(); i < nt * KW; i += 128) a.logits_out[tok0 * KW + i] = s_lg[i];
+                EpiSync::sync();
+            }
+            gate_finish<EpiSync>(a, s_lg, s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
+            EpiSync::sync();
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    }
+}
+
+size_t gate_tc_smem(int NP, int KW, int K1, int stages) {
+    return 1024 + (size_t)stages * (GT_A_BYTES + NP * GT_BK * 2) + (size_t)GT_BM * KW * 4 + GT_BM * 4 +
+           5 * (size_t)K1 * 4 + 8 + (2 * stages + 4) * 8 + 16;
+}
+
+}  // namespace
+
+int gate_tc_np(int KW) { return ((4 * KW + 31) / 32) * 32; }
+
+bool gate_tc_supported(int bf16, int d, int KW) {
+    return bf16 && d % GT_BK == 0 && d >= GT_BK && gate_tc_np(KW) <= GT_MAX_NP && encode_fn() != nullptr;
+}
+
+cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, cudaStream_t st) {
+    if (a.T == 0) return cudaSuccess;
+    if (a.TB != GT_BM || a.logits || !gate_tc_supported(a.bf16, a.d, a.KW)) return cudaErrorNotSupported;
+    const int NP = gate_tc_np(a.KW);
+    note_launch();
+    router_split_kernel<<<(NP * a.d + 255) / 256 < 1024 ? (NP * a.d + 255) / 256 : 1024, 256, 0, st>>>(
+        a.w, wsplit, a.KW, a.d, NP);
+    CUtensorMap mX, mW;
+    if (!make_map(&mX, a.x, (int64_t)a.V * a.T, a.d, GT_BM)) return cudaErrorNotSupported;
+    if (!make_map(&mW, wsplit, NP, a.d, NP > 256 ? NP / 2 : NP)) return cudaErrorNotSupported;
+    GateTcArgs ta;
+    memset(&ta, 0, sizeof(ta));
+    ta.g = a;
+    ta.NP = NP;
+    ta.nbuf = 2 * NP <= 512 ? 2 : 1;
+    ta.ntiles = a.V * a.nblk;
+    int stages = 8;
+    while (stages > 2 && gate_tc_smem(NP, a.KW, a.K1, stages) > 227 * 1024) --stages;
+    ta.stages = stages;
+    const size_t smem = gate_tc_smem(NP, a.KW, a.K1, stages);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gate1_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    const int grid = ta.ntiles < num_sms ? ta.ntiles : num_sms;
+    note_launch();
+    gate1_tc_kernel<<<grid, GT_THREADS, smem, st>>>(mX, mW, ta);
+    return cudaGetLastError();
+}
+
+}  // namespace smile

@@ -8,48 +8,19 @@
 // per-destination histogram; a scan kernel turns the histograms into per-block offsets;
 // the permute kernel adds the offset and moves the row.
 #include "smile_internal.h"
+#include "gate_common.cuh"
 
 #include <math.h>
 
 namespace smile {
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ float load_elem(const void *p, int64_t i, int bf16) {
     return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(p)[i])
                 : reinterpret_cast<const float *>(p)[i];
-}
-
-__device__ __forceinline__ void set_err(int *err, int code) {
-    if (err) atomicCAS(err, 0, code);
-}
-
-// Rank of this thread's item among the block's earlier items with the same bucket
-// (bucket < 0: no item).  s_wh: [NW][K] ints, s_bh: [K] ints.  Writes the block
-// histogram to s_bh and returns the block-local rank (or -1).  Items are ordered by
-// threadIdx.x, i.e. warp-major then lane, matching item order.
-__device__ int block_rank(int b, int K, int *s_wh, int *s_bh) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
-    for (int i = threadIdx.x; i < NW * K; i += blockDim.x) s_wh[i] = 0;
-    __syncthreads();
-    const unsigned peers = __match_any_sync(kFull, b);
-    const int lr = __popc(peers & ((1u << lane) - 1u));
-    if (b >= 0 && lane == __ffs(peers) - 1) s_wh[w * K + b] = __popc(peers);
-    __syncthreads();
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
-        int acc = 0;
-        for (int ww = 0; ww < NW; ++ww) {
-            const int c = s_wh[ww * K + k];
-            s_wh[ww * K + k] = acc;
-            acc += c;
-        }
-        s_bh[k] = acc;
-    }
-    __syncthreads();
-    return b >= 0 ? s_wh[w * K + b] + lr : -1;
 }
 
 // Copy one row of `nvec` 16-byte vectors with a warp (4 loads in flight per lane).
@@ -182,67 +153,7 @@ __global__ void __launch_bounds__(256, 2) gate1_kernel(GateArgs a) {
         for (int i = tid; i < nt * KW; i += blockDim.x) a.logits_out[tok0 * KW + i] = s_lg[i];
     if (a.logits_out && !a.logits) __syncthreads();
 
-    // Phase B: one thread per token -- argmax (R2, R3), top-1 probabilities (R4), and
-    // the softmax entries for the LB statistics, written back over the logits.
-    int i = -1, j = 0;
-    if (tid < nt) {
-        float *L = s_lg + tid * KW;
-        bool finite = true;
-        for (int k = 0; k < KW; ++k) finite &= isfinite(L[k]);
-        if (!finite) set_err(a.err, SMILE_ENONFINITE);
-        i = 0;
-        for (int k = 1; k < K1; ++k)
-            if (L[k] > L[i]) i = k;
-        float s1 = 0.f;
-        for (int k = 0; k < K1; ++k) s1 += expf(L[k] - L[i]);
-        const float p = __frcp_rn(s1);
-        float q = 1.f;
-        if (!a.flat) {
-            float *L2 = L + K1;
-            j = 0;
-            for (int k = 1; k < K2; ++k)
-                if (L2[k] > L2[j]) j = k;
-            float s2 = 0.f;
-            for (int k = 0; k < K2; ++k) s2 += expf(L2[k] - L2[j]);
-            q = __frcp_rn(s2);
-            const float mj = L2[j];
-            for (int k = 0; k < K2; ++k) L2[k] = __fdiv_rn(expf(L2[k] - mj), s2);
-        }
-        const float mi = L[i];
-        for (int k = 0; k < K1; ++k) L[k] = __fdiv_rn(expf(L[k] - mi), s1);
-        const int64_t g = tok0 + tid;
-        a.route.dest1[g] = i;
-        a.route.dest2[g] = j;
-        a.route.p[g] = p;
-        a.route.q[g] = q;
-        a.route.gate[g] = __fmul_rn(p, q);
-        if (i < 0 || i >= K1) set_err(a.err, SMILE_EINDEX);
-    }
-    s_j[tid] = (tid < nt) ? j : -1;
-
-    // Phase C: block-local capacity rank of dest1 (R5, R8).
-    const int lr = block_rank(i, K1, s_wh, s_bh);
-    if (tid < nt) a.route.slot1[tok0 + tid] = lr;
-    const int64_t bo = (int64_t)v * a.nblk + blk;
-    for (int k = tid; k < K1; k += blockDim.x) a.blk_hist1[bo * K1 + k] = s_bh[k];
-    // LB statistics partials of the block (fp64 for the probability sums): one warp per
-    // statistic, lanes stride over tokens, fixed butterfly order => deterministic.
-    {
-        const int lane = tid & 31, w = tid >> 5, NW = blockDim.x >> 5;
-        for (int k = w; k < KW; k += NW) {
-            double acc = 0.0;
-            for (int tt = lane; tt < nt; tt += 32) acc += (double)s_lg[tt * KW + k];
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-            if (lane == 0) a.blk_psum[bo * (K1 + K2) + k] = acc;
-        }
-        for (int k = w; k < K2; k += NW) {
-            int c = 0;
-            for (int tt = lane; tt < nt; tt += 32) c += (s_j[tt] == k);
-            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-            if (lane == 0) a.blk_hist2a[bo * K2 + k] = c;
-        }
-        if (a.flat && tid == 0) a.blk_psum[bo * (K1 + K2) + K1] = (double)nt;
-    }
+    gate_finish<BlockSync>(a, s_lg, s_j, s_wh, s_bh, tok0, nt, (int64_t)v * a.nblk + blk);
 }
 
 // Warp-wide exclusive scan over n ints at stride `st` (in place), returns the total.
@@ -328,7 +239,7 @@ __global__ void rank2_kernel(Rank2Args a) {
         b = a.recv_meta[(int64_t)v * a.items + x];
         if (b >= a.K2) { set_err(a.err, SMILE_EINDEX); b = -1; }
     }
-    const int lr = block_rank(b, a.K2, s_wh, s_bh);
+    const int lr = block_rank<BlockSync>(b, a.K2, s_wh, s_bh);
     if (x < a.items) a.slot2[(int64_t)v * a.items + x] = lr;
     for (int k = threadIdx.x; k < a.K2; k += blockDim.x)
         a.blk_hist2[((int64_t)v * a.nblk + blk) * a.K2 + k] = s_bh[k];
@@ -675,17 +586,21 @@ void launch_gate1(const GateArgs &a, cudaStream_t st) {
         cudaFuncSetAttribute(gate1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         attr_set = true;
     }
+    note_launch();
     gate1_kernel<<<dim3(a.nblk, a.V), a.TB, smem, st>>>(a);
 }
 
 void launch_scan1(const Scan1Args &a, cudaStream_t st) {
     if (a.T == 0) return;
+    note_launch();
     scan1_kernel<<<a.V, 512, 0, st>>>(a);
 }
 
 void launch_rank2(const Rank2Args &a, cudaStream_t st) {
     if (a.items == 0) return;
+    note_launch();
     rank2_kernel<<<dim3(a.nblk, a.V), kRank2Items, 0, st>>>(a);
+    note_launch();
     scan2_kernel<<<a.V, 512, 0, st>>>(a);
 }
 
@@ -694,6 +609,7 @@ static void launch_move(MoveArgs &m, cudaStream_t st) {
     const int64_t per_block = (int64_t)(kMoveThreads / 32) * kMoveRowsPerWarp;
     int64_t grid = (m.rows + per_block - 1) / per_block;
     if (grid > 148 * 8) grid = 148 * 8;
+    note_launch();
     row_move_kernel<<<(int)grid, kMoveThreads, 0, st>>>(m);
 }
 
@@ -702,7 +618,10 @@ void launch_dispatch1(const Dispatch1Args &a, cudaStream_t st) {
     MoveArgs m{};
     m.kind = MOVE_DISPATCH1; m.rows = (int64_t)a.V * a.T; m.rowbytes = a.rowbytes; m.d1 = a;
     launch_move(m, st);
-    if (a.meta || a.peer.bases && a.peer.n > 0) meta_fill_kernel<<<148 * 4, 256, 0, st>>>(a);
+    if (a.meta || a.peer.bases && a.peer.n > 0) {
+        note_launch();
+        meta_fill_kernel<<<148 * 4, 256, 0, st>>>(a);
+    }
 }
 
 void launch_dispatch2(const Dispatch2Args &a, cudaStream_t st) {
@@ -735,18 +654,21 @@ void launch_combine1(const Combine1Args &a, cudaStream_t st) {
 
 void launch_aux(const smile_stats &s, double alpha, double beta, double *loss, int V, int K1, int K2,
                 int64_t T, int flat, cudaStream_t st) {
+    note_launch();
     aux_kernel<<<(V + 127) / 128, 128, 0, st>>>(s, alpha, beta, loss, V, K1, K2, T, flat);
 }
 
 void launch_peer_barrier(char *const *bases, int64_t off_flags, int me, const int32_t *peers, int npeers, int level,
                          long long epoch, cudaStream_t st) {
     if (npeers <= 0) return;
+    note_launch();
     peer_barrier_kernel<<<1, 32, 0, st>>>(bases, off_flags, me, peers, npeers, level, epoch);
 }
 
 void launch_exchange_copy(const CopyXArgs &a, cudaStream_t st) {
     const int64_t chunks = (a.Csub + kCopyRows - 1) / kCopyRows;
     dim3 grid((unsigned)(a.V * a.P * a.nsub), (unsigned)(chunks > 0 ? chunks : 1));
+    note_launch();
     exchange_copy_kernel<<<grid, 256, 0, st>>>(a);
 }
 

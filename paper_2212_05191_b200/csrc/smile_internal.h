@@ -14,6 +14,10 @@ namespace smile {
 
 constexpr int kWarp = 32;
 
+// Host-side count of libsmile kernel launches (smile_launch_count); every launch site
+// calls it immediately before its <<<>>> / cudaLaunchKernelEx.
+void note_launch();
+
 // Tokens per block of the level-1 gate (sized so the logits tile stays <= 32 KB of smem).
 inline int gate_tokens_per_block(int KW) {
     if (KW <= 32) return 256;
@@ -74,6 +78,8 @@ struct smile_ctx_s {
     int npeers[3] = {};
     long long epoch[3] = {};
     smile::PeerMap peer{};
+    // tensor-core gate (bf16 fused router): the three-piece bf16 split of the router
+    __nv_bfloat16 *wsplit = nullptr;         // [gate_tc_np(KW), d], rewritten every fused gate call
 };
 
 namespace smile {
@@ -180,5 +186,10 @@ cudaError_t launch_ffn_bwd(const FfnBwdArgs &a, bool tc, cudaStream_t st);
 cudaError_t launch_ffn_fwd_train(const FfnArgs &a, void *A1, bool tc, cudaStream_t st);
 // Returns cudaErrorNotSupported when the shape cannot run on the tcgen05 path.
 cudaError_t launch_ffn_tcgen05(const FfnArgs &a, cudaStream_t st);
+
+// Level-1 gate with the router on tcgen05 (gate_tcgen05.cu); needs TB == 128.
+int gate_tc_np(int KW);
+bool gate_tc_supported(int bf16, int d, int KW);
+cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, cudaStream_t st);
 
 }  // namespace smile

@@ -82,6 +82,7 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.smile_version.restype = C.c_int
         L.smile_strerror.restype = C.c_char_p
+        L.smile_launch_count.restype = C.c_int64
         for name in ("smile_plan", "smile_group", "smile_exchange_plan", "smile_get_unique_id", "smile_create", "smile_destroy",
                      "smile_query", "smile_get_error", "smile_gate_inter", "smile_dispatch", "smile_gate_intra",
                      "smile_all2all", "smile_all2all_inter", "smile_all2all_intra", "smile_expert_ffn",
@@ -142,6 +143,11 @@ def exchange_plan(level: int, **kw) -> list[tuple]:
     ops = (XOp * max(1, cnt.value))()
     _check(lib().smile_exchange_plan(C.byref(sh), level, ops, cnt.value, C.byref(cnt)), "smile_exchange_plan")
     return [(o.kind, o.peer_proc, o.src, o.dst, o.chunk) for o in ops[: cnt.value]]
+
+
+def launch_count() -> int:
+    """Kernels libsmile has launched so far in this process (smile_launch_count)."""
+    return int(lib().smile_launch_count())
 
 
 def unique_id() -> bytes:

@@ -105,32 +105,45 @@ def test_identity_collapse_n1_equals_flat():
     assert torch.equal(oa, ob)
 
 
-@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
-def test_fused_router(dtype):
+@pytest.mark.parametrize("dtype,n,m,e,T,d,mode", [
+    ("fp32", 2, 4, 1, 700, 256, "bilevel"),
+    ("bf16", 2, 4, 1, 700, 256, "bilevel"),     # tensor-core router, KW = 6, ragged last tile
+    ("bf16", 2, 4, 8, 300, 128, "bilevel"),     # KW = 34 (C4's bi-level router)
+    ("bf16", 2, 4, 8, 257, 192, "flat"),        # KW = 64 (C4's flat router), N = 256
+    ("bf16", 4, 2, 12, 130, 64, "flat"),        # KW = 96: two N halves, one TMEM buffer
+    ("bf16", 2, 2, 1, 100, 64, "bilevel"),      # a single partial tile per rank
+])
+def test_fused_router(dtype, n, m, e, T, d, mode):
     """a1 fused into a2: logits within fp32 accumulation error of the fp64 oracle; the
-    routing taken on the GPU's own logits matches the oracle run on those logits."""
+    routing taken on the GPU's own logits matches the oracle run on those logits.  The
+    bf16 cases run the tcgen05 router (three-piece bf16 split of W, gate_tcgen05.cu)."""
     from paper_2212_05191_b200 import smile as smb
-    case = Case(2, 4, 1, 700, 256, 128, 1.0, dtype=dtype, fused=True, seed=5)
-    layer = smb.SmileLayer(2, 4, 1, 256, 128, 700, 1.0, dtype, "bilevel")
+    case = Case(n, m, e, T, d, 128, 1.0, dtype=dtype, fused=True, seed=5, mode=mode)
+    G, KW = n * m, case.cfg.logit_width
+    layer = smb.SmileLayer(n, m, e, d, 128, T, 1.0, dtype, mode)
     layer.alloc_workspace()
     g = case.gpu_tensors()
-    lg_out = torch.empty(8, 700, 6, dtype=torch.float32, device="cuda")
+    lg_out = torch.empty(G, T, KW, dtype=torch.float32, device="cuda")
     w = layer._view
     layer.gate_inter(g["x"], w.route, w.stats, C_ptr(w.counts1), w_router=g["w_router"], logits_out=lg_out)
-    layer.dispatch(1, g["x"], WsTensor(w.send1), route=w.route, send_meta=WsTensor(w.meta1))
+    layer.dispatch(1, g["x"], WsTensor(w.send1), route=w.route,
+                   send_meta=WsTensor(w.meta1) if mode == "bilevel" else None)
     torch.cuda.synchronize()
+    assert layer.get_error() == 0
     lg = lg_out.cpu().numpy()
-    ref = oracle.logits(case.x.reshape(-1, 256), case.w_router).reshape(8, 700, 6)
+    ref = oracle.logits(case.x.reshape(-1, d), case.w_router).reshape(G, T, KW)
     np.testing.assert_allclose(lg, ref, rtol=0, atol=2e-5)
     r = oracle.route(case.cfg, lg)
     v = {k: t.cpu().numpy() for k, t in layer.view().items()}
     np.testing.assert_array_equal(v["dest1"], r.dest1)
-    np.testing.assert_array_equal(v["dest2"], r.dest2)
+    if mode == "bilevel":
+        np.testing.assert_array_equal(v["dest2"], r.dest2)
     np.testing.assert_array_equal(v["slot1"], r.slot1)
     np.testing.assert_allclose(v["gate"], r.gate, rtol=1e-6)
     # decisions on the oracle's own logits agree wherever the top-2 margin exceeds 1e-4
     r0 = case.oracle_route()
-    srt = np.sort(ref[:, :, :2], axis=-1)
+    K1 = n if mode == "bilevel" else KW
+    srt = np.sort(ref[:, :, :K1], axis=-1)
     clear = (srt[..., -1] - srt[..., -2]) > 1e-4
     np.testing.assert_array_equal(r0.dest1[clear], v["dest1"][clear])
 

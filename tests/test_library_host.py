@@ -21,7 +21,7 @@ def built():
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "smile.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:smile_status|int|const char\s*\*)\s*\*?\s*(smile_[a-z0-9_]+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:smile_status|int|int64_t|const char\s*\*)\s*\*?\s*(smile_[a-z0-9_]+)\s*\(",
                                  src, re.M)))
 
 
@@ -33,6 +33,7 @@ def test_exports_every_declared_symbol():
         assert hasattr(L, s), s
     assert L.smile_version() == 100
     assert L.smile_strerror(3) == b"non-finite router logit"
+    assert smb.launch_count() == 0          # no kernel has been launched on this CPU-only host
 
 
 def test_group_examples_spec():
