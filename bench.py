@@ -435,7 +435,36 @@ def run_ours(args):
             dist.barrier()
         ph = [[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(nph)] for k in range(args.steps)]
         step_ms = [sum(p) for p in ph]
-        mine = torch.tensor([sum(step_ms) / args.steps] + [statistics.mean(p[i] for p in ph) for i in range(nph)],
+        eager_ms = sum(step_ms) / args.steps
+        graph_ms = None
+        if args.graph and world == 1:
+            # the same step captured once as a CUDA graph and replayed (the libsmile calls
+            # are stream-ordered with no host syncs); timed with events around each replay
+            cs = torch.cuda.Stream()
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                step_fn(L, inp)
+            torch.cuda.current_stream().wait_stream(cs)
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg):
+                step_fn(L, inp)
+            for _ in range(max(3, args.warmup)):
+                cg.replay()
+            g0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            g1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            torch.cuda.synchronize()
+            for k in range(args.steps):
+                flush.zero_()
+                g0[k].record()
+                cg.replay()
+                g1[k].record()
+            torch.cuda.synchronize()
+            graph_ms = statistics.mean(g0[k].elapsed_time(g1[k]) for k in range(args.steps))
+            if L.get_error():
+                raise SystemExit("device error in graph replay")
+            del cg
+        mine = torch.tensor([graph_ms if graph_ms is not None else eager_ms] +
+                            [statistics.mean(p[i] for p in ph) for i in range(nph)],
                             dtype=torch.float64, device=dev)
         allr = [torch.empty_like(mine) for _ in range(world)] if dist else [mine]
         if dist:
@@ -461,7 +490,7 @@ def run_ours(args):
         ffn_tc = cfgd["dtype"] == "bf16" and args.ffn != "simt" and smb.TCGEN05_DEFAULT
         res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, rank_ms=rank_ms, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms,
                    t_beg=t_beg, t_end=t_end,
-                   tokens=G * T, launches=launched, hbm_bytes=hbm, train=train)
+                   tokens=G * T, launches=launched, hbm_bytes=hbm, train=train, eager_ms=eager_ms, graph_ms=graph_ms)
         if train:
             res["hbm_bytes"] = {}
         # e2e through smile_forward_host (pinned host x, D2H out + loss)
@@ -540,6 +569,7 @@ def run_ours(args):
                    "l2": "flushed (256 MiB write) before every timed step, outside its events"},
         "phase_ms": main["phase_ms"], "phase_ms_note": "per phase: max over ranks of the mean over steps",
         "rank_ms_per_step": main["rank_ms"], "kept_tokens": main["kept"],
+        "cuda_graph": main["graph_ms"] is not None, "eager_ms_per_step": main["eager_ms"],
         "roofline": roof,
         "hbm_phases": hbm_phases(main, peaks),
         "gpu_launches": main["launches"],
@@ -550,7 +580,8 @@ def run_ours(args):
         line["e2e"] = main["e2e"]
     if "flat" in results and modes[0] != "flat":
         f = results["flat"]
-        line["flat"] = {"value": f["tokens"] / (f["ms"] / 1e3), "ms_per_step": f["ms"], "phase_ms": f["phase_ms"],
+        line["flat"] = {"value": f["tokens"] / (f["ms"] / 1e3), "ms_per_step": f["ms"], "eager_ms_per_step": f["eager_ms"],
+                        "phase_ms": f["phase_ms"],
                         "e2e": f.get("e2e"), "kept_tokens": f["kept"]}
         line["bilevel_over_flat"] = line["value"] / line["flat"]["value"]
     if not args.no_cpu and world == 1:           # rank 0 at N = 1 only

@@ -296,6 +296,10 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
     CUDA_TRY(cudaMalloc(&c->blk_psum, nb1 * (z.K1 + z.K2) * 8));
     CUDA_TRY(cudaMalloc(&c->blk_hist2, nb2 * z.K2 * 4));
     CUDA_TRY(cudaMalloc(&c->blk_off2, nb2 * z.K2 * 4));
+    {
+        const size_t cb = colsum_ws_bytes(V * shape->e, (int)z.S, z.Cseg, std::max(shape->d, shape->d_ff));
+        if (cudaMalloc(&c->colsum_ws, cb) != cudaSuccess) { smile_destroy(c); return SMILE_ECUDA; }
+    }
     const int n = shape->n, m = shape->m, e = shape->e, G = z.G;
     if (shape->mode == SMILE_BILEVEL) {
         st = build_level(c, 1, n, 1, z.C1, (int)z.C1);
@@ -336,6 +340,7 @@ extern "C" smile_status smile_destroy(smile_ctx c) {
     if (c->world) ncclCommDestroy(c->world);
     cudaFree(c->d_err);
     cudaFree(c->wsplit);
+    cudaFree(c->colsum_ws);
     cudaFree(c->blk_hist1); cudaFree(c->blk_off1); cudaFree(c->blk_hist2a); cudaFree(c->blk_psum);
     cudaFree(c->blk_hist2); cudaFree(c->blk_off2);
     for (int p = 0; p < kMaxProcs; ++p)
@@ -756,6 +761,7 @@ extern "C" smile_status smile_expert_ffn_bwd(smile_ctx c, const void *X, const i
     b.dW1 = dW1; b.db1 = db1; b.dW2 = dW2; b.db2 = db2; b.V = c->sz.V; b.S = c->sz.S; b.e = c->shape.e;
     b.Cseg = c->sz.Cseg; b.d = c->shape.d; b.d_ff = c->shape.d_ff; b.bf16 = c->shape.dtype == SMILE_BF16;
     b.num_sms = c->num_sms;
+    b.colsum_ws = c->colsum_ws;
     const bool tc = ffn_use_tc(c);
     if (tc && !b.bf16) return SMILE_ENOTSUP;
     if (!ffn_simt_supported(b.V * b.S * b.e, b.d, b.d_ff)) return SMILE_ENOTSUP;

@@ -195,21 +195,6 @@ __global__ void __launch_bounds__(NTHR) wgrad_simt(WgradArgs a) {
         }
 }
 
-// Bias gradient: db[e][n] = sum over the expert's valid rows of B[r][n].
-__global__ void colsum_kernel(WgradArgs a) {
-    const int n = blockIdx.x * blockDim.x + threadIdx.x;
-    const int ex = blockIdx.y, v = ex / a.e, k = ex % a.e;
-    if (n >= a.N) return;
-    float s = 0.f;
-    for (int sg = 0; sg < a.S; ++sg) {
-        const int g = (v * a.S + sg) * a.e + k;
-        const int cnt = a.counts[g];
-        const int64_t base = (int64_t)g * a.Cseg;
-        for (int r = 0; r < cnt; ++r) s += ld(a.B, (base + r) * a.N + n, a.bf16);
-    }
-    a.Dw[(int64_t)ex * a.N + n] = s;
-}
-
 }  // namespace
 
 cudaError_t launch_ffn_bwd(const FfnBwdArgs &b, bool tc, cudaStream_t st) {
@@ -230,18 +215,27 @@ cudaError_t launch_ffn_bwd(const FfnBwdArgs &b, bool tc, cudaStream_t st) {
         grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g2);
     }
     // dW2 = H^T dY  [NE, d_ff, d];  dW1 = X^T dZ  [NE, d, d_ff]
-    WgradArgs w2{b.H, b.dY, b.dW2, b.counts, b.e, b.S, b.Cseg, b.d_ff, b.d, b.bf16};
-    note_launch();
-    wgrad_simt<<<dim3((b.d + BN - 1) / BN, (b.d_ff + BM - 1) / BM, NE), NTHR, 0, st>>>(w2);
-    WgradArgs w1{b.X, b.dZ, b.dW1, b.counts, b.e, b.S, b.Cseg, b.d, b.d_ff, b.bf16};
-    note_launch();
-    wgrad_simt<<<dim3((b.d_ff + BN - 1) / BN, (b.d + BM - 1) / BM, NE), NTHR, 0, st>>>(w1);
-    WgradArgs c2{nullptr, b.dY, b.db2, b.counts, b.e, b.S, b.Cseg, 0, b.d, b.bf16};
-    note_launch();
-    colsum_kernel<<<dim3((b.d + 255) / 256, NE), 256, 0, st>>>(c2);
-    WgradArgs c1{nullptr, b.dZ, b.db1, b.counts, b.e, b.S, b.Cseg, 0, b.d_ff, b.bf16};
-    note_launch();
-    colsum_kernel<<<dim3((b.d_ff + 255) / 256, NE), 256, 0, st>>>(c1);
+    if (tc && wgrad_tc_supported(b.bf16, b.d, b.d_ff, b.S)) {
+        // tcgen05 wgrad: padding rows up to the next 64-row K block must be zero
+        launch_pad_rows_zero(const_cast<void *>(b.X), b.counts, nseg, b.Cseg, b.d, st);
+        launch_pad_rows_zero(const_cast<void *>(b.dY), b.counts, nseg, b.Cseg, b.d, st);
+        launch_pad_rows_zero(const_cast<void *>(b.H), b.counts, nseg, b.Cseg, b.d_ff, st);
+        launch_pad_rows_zero(b.dZ, b.counts, nseg, b.Cseg, b.d_ff, st);
+        cudaError_t e = launch_wgrad_tc(b.H, b.d_ff, b.dY, b.d, b.dW2, b.counts, b.V, b.S, b.e, b.Cseg, b.num_sms, st);
+        if (e != cudaSuccess) return e;
+        e = launch_wgrad_tc(b.X, b.d, b.dZ, b.d_ff, b.dW1, b.counts, b.V, b.S, b.e, b.Cseg, b.num_sms, st);
+        if (e != cudaSuccess) return e;
+    } else {
+        WgradArgs w2{b.H, b.dY, b.dW2, b.counts, b.e, b.S, b.Cseg, b.d_ff, b.d, b.bf16};
+        note_launch();
+        wgrad_simt<<<dim3((b.d + BN - 1) / BN, (b.d_ff + BM - 1) / BM, NE), NTHR, 0, st>>>(w2);
+        WgradArgs w1{b.X, b.dZ, b.dW1, b.counts, b.e, b.S, b.Cseg, b.d, b.d_ff, b.bf16};
+        note_launch();
+        wgrad_simt<<<dim3((b.d_ff + BN - 1) / BN, (b.d + BM - 1) / BM, NE), NTHR, 0, st>>>(w1);
+    }
+    // db2 = 1^T dY, db1 = 1^T dZ: fixed-order two-pass column sums
+    launch_colsum(b.dY, b.db2, b.colsum_ws, b.counts, NE, b.e, b.S, b.Cseg, b.d, b.bf16, st);
+    launch_colsum(b.dZ, b.db1, b.colsum_ws, b.counts, NE, b.e, b.S, b.Cseg, b.d_ff, b.bf16, st);
     return cudaGetLastError();
 }
 

@@ -38,7 +38,8 @@ constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
 constexpr int B_BYTES_MAX = 256 * BK * 2;     // 32 KB
 constexpr int ACC_COLS = 256;                 // TMEM columns per accumulator buffer
-constexpr int OUT_BOX_BYTES = 32 * 32 * 2;    // per epilogue warp: 32 rows x 32 bf16 staged for a TMA store
+constexpr int OUT_BOX_BYTES = 32 * 64 * 2;    // per epilogue warp: 32 rows x 64 bf16 staged for a TMA store
+constexpr int OUT_SLOTS = 2;                  // boxes per warp in flight (the store of chunk c overlaps chunk c+1)
 
 struct TcArgs {
     const float *bias;       // [NE, N]
@@ -51,7 +52,8 @@ struct TcArgs {
     int gelu;
     int mode;                  // EPI_* below
     const __nv_bfloat16 *aux;  // EPI_DGELU: the saved pre-activation A1 [rows_total, N]
-    int stages;                // smem pipeline depth (3 when two output boxes per warp)
+    int stages;                // smem pipeline depth
+    int slots;                 // output boxes in flight per epilogue warp (1 or 2)
     int *err;
 };
 
@@ -63,31 +65,13 @@ enum { EPI_BIAS = 0,        // D = act(acc + bias), act = GELU when gelu != 0 (f
 
 // GELU(z) = z Phi(z) = 0.5 z + 0.5 |z| erf(|z| / sqrt 2) (R21, erf form).  erf by Abramowitz &
 // Stegun 7.1.28, 1 - (1 + a1 x + ... + a6 x^6)^-16: |error| <= 1.8e-6 on erf and 8.8e-7 on GELU
-// over all z (checked against scipy in fp32 emulation), ~14 instructions with one
-// MUFU reciprocal instead of erff's ~30 -- the bf16 H it feeds has a half-ulp of >= 2^-9 |H|.
-__device__ __forceinline__ float gelu_erf(float z) {
-    const float ax = fabsf(z) * 0.70710678118654752f;
-    float p = 4.30638e-5f;
-    p = fmaf(p, ax, 2.765672e-4f);
-    p = fmaf(p, ax, 1.520143e-4f);
-    p = fmaf(p, ax, 9.2705272e-3f);
-    p = fmaf(p, ax, 4.22820123e-2f);
-    p = fmaf(p, ax, 7.05230784e-2f);
-    p = fmaf(p, ax, 1.0f);
-    p = p * p;
-    p = p * p;
-    p = p * p;
-    p = p * p;
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p));
-    return fmaf(0.5f * fabsf(z), 1.0f - r, 0.5f * z);
-}
-
-// The same GELU on a pair of values with Blackwell's packed fp32x2 pipe (FFMA2 / FMUL2:
-// two lanes of fp32 arithmetic per instruction, identical rounding per lane), which
-// halves the epilogue's ALU work -- the bias + GELU epilogue of the first FFN GEMM is
-// otherwise slower than its MMAs.  The polynomial is evaluated directly in |z| with the
-// coefficients a_i / sqrt(2)^i; (1 + ...)^-16 and the final combine as above.
+// over all z (checked against scipy in fp32 emulation), with one MUFU reciprocal
+// instead of erff's ~30 instructions -- the bf16 H it feeds has a half-ulp of >= 2^-9 |H|.
+// Evaluated on pairs of values with Blackwell's packed fp32x2 pipe (FFMA2 / FMUL2: two
+// lanes of fp32 arithmetic per instruction, identical rounding per lane), which halves
+// the epilogue's ALU work -- the bias + GELU epilogue of the first FFN GEMM is otherwise
+// slower than its MMAs.  The polynomial is evaluated directly in |z| with the
+// coefficients a_i / sqrt(2)^i.
 typedef unsigned long long f32x2;
 __device__ __forceinline__ f32x2 pack2(float a, float b) {
     f32x2 r;
@@ -156,27 +140,24 @@ __device__ __forceinline__ float gelu_grad(float z) {
 }
 
 struct TileInfo {
-    int g, mt, nt, rows;
-    int64_t a_row, b_row, d_row, expert;
+    int nt, E, u0;            // n-tile, expert, first strip of this CTA
+    int64_t b_row;
 };
 
-// Tile `tile` of the work list: TM = CG * 128 rows of one segment x BN columns.  For a
-// CTA pair, `rank` selects this CTA's 128-row half of A and BN/2-row half of B; `rows`
-// is the number of valid rows of this CTA's half (may be <= 0).
+// Tile `tile` of the work list: 4 * CG strips (32 rows each) of one expert x BN columns.
+// For a CTA pair, `rank` selects this CTA's 4 strips (its 128 rows of the M = 256 MMA)
+// and its BN/2-row half of B.  Strip u0 + j of the expert goes to TMEM lanes 32j..32j+31;
+// a missing strip (the expert's last tile) has 0 rows and points at row 0 (loaded,
+// computed, never stored).
 template <int CG>
 __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref, int tile, int ntn, int rank) {
     TileInfo t;
     t.nt = tile % ntn;
     const int mtg = tile / ntn;
-    t.g = tile_segment(s_pref, a.nseg, mtg);
-    t.mt = mtg - s_pref[t.g];
-    const int v = t.g / (a.S * a.e), k = t.g % a.e;
-    t.expert = (int64_t)v * a.e + k;
-    const int r0 = t.mt * (BM * CG) + rank * BM;
-    t.rows = min(BM, a.counts[t.g] - r0);
-    t.a_row = (int64_t)t.g * a.Cseg + r0;
-    t.d_row = t.a_row;
-    t.b_row = t.expert * a.N + (int64_t)t.nt * a.BN + rank * (a.BN / CG);
+    const int NE = a.nseg / a.S;
+    t.E = tile_segment(s_pref, NE, mtg);
+    t.u0 = ((mtg - s_pref[t.E]) * CG + rank) * 4;
+    t.b_row = (int64_t)t.E * a.N + (int64_t)t.nt * a.BN + rank * (a.BN / CG);
     return t;
 }
 
@@ -196,11 +177,13 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     const int b_stage_bytes = B_BYTES_MAX / CG;
     unsigned char *sB = sA + STAGES * A_BYTES;
     unsigned char *sOut = sB + STAGES * b_stage_bytes;                // EPI_WARPS x nbox x 2 KB
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sOut + nbox * EPI_WARPS * OUT_BOX_BYTES);
+    const int slots = nbox == 2 ? 1 : a.slots;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sOut + slots * nbox * EPI_WARPS * OUT_BOX_BYTES);
     uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
     int *s_warp = reinterpret_cast<int *>(tmem_holder + 4);
     int *s_pref = s_warp + 32;
+    int *s_cnt = s_pref + MAXSEG + 1;                                 // [nseg] segment row counts
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
@@ -236,12 +219,14 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         }
     }
-    tile_prefix<BM * CG>(a.counts, a.nseg, s_pref, s_warp);   // ends with __syncthreads
+    for (int g = threadIdx.x; g < a.nseg; g += blockDim.x) s_cnt[g] = a.counts[g];
+    __syncthreads();
+    expert_tile_prefix<4 * CG>(s_cnt, a.nseg / a.S, a.S, a.e, s_pref, s_warp);   // ends with __syncthreads
     if (CG == 2) cluster_sync_all();                         // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const int ntn = a.N / a.BN;
-    const int total = s_pref[a.nseg] * ntn;
+    const int total = s_pref[a.nseg / a.S] * ntn;
     const int nk = a.K / BK;
     const uint32_t b_bytes = (uint32_t)(a.BN / CG) * BK * 2;
 
@@ -252,18 +237,32 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             uint32_t phase = 0;
             for (int tile = cid; tile < total; tile += ncl) {
                 const TileInfo t = tile_info<CG>(a, s_pref, tile, ntn, rank);
+                // A: four 32-row strip boxes per K block (4 KB each, stacked = one 128-row
+                // SW128 tile), their rows resolved once per tile
+                int srow[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    int64_t r;
+                    int nr;
+                    expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + j, r, nr);
+                    srow[j] = (int)r;
+                }
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full[stage]);
                     if (CG == 1) {
                         mbar_arrive_tx(fb, A_BYTES + b_bytes);
-                        tma_load_2d(smem_u32(sA + stage * A_BYTES), &mapA, kb * BK, (int)t.a_row, fb);
+                        for (int j = 0; j < 4; ++j)
+                            tma_load_2d(smem_u32(sA + stage * A_BYTES + j * (A_BYTES / 4)), &mapA, kb * BK,
+                                        srow[j], fb);
                         tma_load_2d(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)t.b_row, fb);
                     } else {
                         // the leader's full barrier counts the bytes of both CTAs' loads
                         if (leader) mbar_arrive_tx(fb, CG * (A_BYTES + b_bytes));
                         const uint32_t fbl = mapa_shared(fb, 0);
-                        tma_load_2d_pair(smem_u32(sA + stage * A_BYTES), &mapA, kb * BK, (int)t.a_row, fbl);
+                        for (int j = 0; j < 4; ++j)
+                            tma_load_2d_pair(smem_u32(sA + stage * A_BYTES + j * (A_BYTES / 4)), &mapA, kb * BK,
+                                             srow[j], fbl);
                         tma_load_2d_pair(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)t.b_row, fbl);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -306,12 +305,15 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: 8 warps; quadrant q = rows 32q..32q+31 ----------------
+        // Each warp owns half of the tile's columns and walks them in steps of 64: two
+        // tcgen05.ld (one wait), bias / activation in packed fp32x2, bf16, then one
+        // 32 x 64 SWIZZLE_128B box per output tensor in smem and one TMA tensor store.
         const int q = warp & 3;
         const int half = (warp - 4) >> 2;
-        const int row = q * 32 + lane;
         const int nch = a.BN / 32;
         const int c_beg = half ? (nch + 1) / 2 : 0, c_end = half ? nch : (nch + 1) / 2;
         int it = 0;
+        uint32_t nstore = 0;                      // this warp's box stores so far (slot = nstore % slots)
         for (int tile = cid; tile < total; tile += ncl, ++it) {
             const TileInfo t = tile_info<CG>(a, s_pref, tile, ntn, rank);
             const int acc = it & 1;
@@ -319,92 +321,115 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS;
             const bool has_bias = a.mode == EPI_BIAS || a.mode == EPI_BIAS_SAVE;
-            const float4 *bias4 = reinterpret_cast<const float4 *>(a.bias + t.expert * a.N + (int64_t)t.nt * a.BN);
+            const bool act = (a.mode == EPI_BIAS && a.gelu) || a.mode == EPI_BIAS_SAVE;
+            const float4 *bias4 = reinterpret_cast<const float4 *>(a.bias + (int64_t)t.E * a.N + (int64_t)t.nt * a.BN);
             const int64_t dcol0 = (int64_t)t.nt * a.BN;
-            __nv_bfloat16 *drow = a.D + (t.d_row + row) * (int64_t)a.N + dcol0;
-            unsigned char *box = sOut + (warp - 4) * nbox * OUT_BOX_BYTES;
-            const bool full_box = q * 32 + 32 <= t.rows;
-            const bool any_row = q * 32 < t.rows;
-            for (int c = c_beg; c < c_end && any_row; ++c) {
-                float v[32];
-                tmem_ld32(tbase + c * 32, v);
-                if (has_bias) {
+            unsigned char *box0 = sOut + (warp - 4) * slots * nbox * OUT_BOX_BYTES;
+            int64_t d_row;                                  // this warp's strip
+            int srows;
+            expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + q, d_row, srows);
+            const bool full_box = srows == 32;
+            const bool any_row = srows > 0;
+            for (int c = c_beg; c < c_end && any_row; c += 2) {
+                const int nc = c + 1 < c_end ? 2 : 1;          // 32-column chunks in this step
+                float v[2][32];
+                tmem_ld32_nowait(tbase + c * 32, v[0]);
+                if (nc == 2) tmem_ld32_nowait(tbase + c * 32 + 32, v[1]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                uint4 pk[2][4], pks[2][4];
 #pragma unroll
-                    for (int i4 = 0; i4 < 8; ++i4) {
-                        const float4 b = __ldg(bias4 + c * 8 + i4);
-                        const f32x2 lo = add2(pack2(v[4 * i4], v[4 * i4 + 1]), pack2(b.x, b.y));
-                        const f32x2 hi = add2(pack2(v[4 * i4 + 2], v[4 * i4 + 3]), pack2(b.z, b.w));
-                        unpack2(lo, v[4 * i4], v[4 * i4 + 1]);
-                        unpack2(hi, v[4 * i4 + 2], v[4 * i4 + 3]);
-                    }
-                }
-                uint4 pk[4], pk2[4];
-                uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
-                uint32_t *pw2 = reinterpret_cast<uint32_t *>(pk2);
-                if (a.mode == EPI_BIAS_SAVE) {
+                for (int h = 0; h < 2; ++h) {
+                    if (h >= nc) break;
+                    float *w = v[h];
+                    const int cc = c + h;
+                    if (has_bias) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-                        pw2[i] = *reinterpret_cast<uint32_t *>(&h);
-                    }
-                }
-                if (a.mode == EPI_DGELU && row < t.rows) {
-                    const uint4 *ap = reinterpret_cast<const uint4 *>(a.aux + (t.d_row + row) * (int64_t)a.N + dcol0 + c * 32);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint4 u = __ldg(ap + i);
-                        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
-#pragma unroll
-                        for (int z = 0; z < 4; ++z) {
-                            const float2 f = __bfloat1622float2(h[z]);
-                            v[8 * i + 2 * z] *= gelu_grad(f.x);
-                            v[8 * i + 2 * z + 1] *= gelu_grad(f.y);
+                        for (int i4 = 0; i4 < 8; ++i4) {
+                            const float4 b = __ldg(bias4 + cc * 8 + i4);
+                            const f32x2 lo = add2(pack2(w[4 * i4], w[4 * i4 + 1]), pack2(b.x, b.y));
+                            const f32x2 hi = add2(pack2(w[4 * i4 + 2], w[4 * i4 + 3]), pack2(b.z, b.w));
+                            unpack2(lo, w[4 * i4], w[4 * i4 + 1]);
+                            unpack2(hi, w[4 * i4 + 2], w[4 * i4 + 3]);
                         }
                     }
-                }
-                const bool act = (a.mode == EPI_BIAS && a.gelu) || a.mode == EPI_BIAS_SAVE;
+                    if (a.mode == EPI_BIAS_SAVE) {
+                        uint32_t *pw2 = reinterpret_cast<uint32_t *>(pks[h]);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    float y0 = v[2 * i], y1 = v[2 * i + 1];
-                    if (act) unpack2(gelu_erf2(pack2(y0, y1)), y0, y1);
-                    __nv_bfloat162 h = __floats2bfloat162_rn(y0, y1);
-                    pw[i] = *reinterpret_cast<uint32_t *>(&h);
+                        for (int i = 0; i < 16; ++i) {
+                            __nv_bfloat162 hh = __floats2bfloat162_rn(w[2 * i], w[2 * i + 1]);
+                            pw2[i] = *reinterpret_cast<uint32_t *>(&hh);
+                        }
+                    }
+                    if (a.mode == EPI_DGELU && lane < srows) {
+                        const uint4 *ap =
+                            reinterpret_cast<const uint4 *>(a.aux + (d_row + lane) * (int64_t)a.N + dcol0 + cc * 32);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const uint4 u = __ldg(ap + i);
+                            const __nv_bfloat162 *hh = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+                            for (int z = 0; z < 4; ++z) {
+                                const float2 f = __bfloat1622float2(hh[z]);
+                                w[8 * i + 2 * z] *= gelu_grad(f.x);
+                                w[8 * i + 2 * z + 1] *= gelu_grad(f.y);
+                            }
+                        }
+                    }
+                    uint32_t *pw = reinterpret_cast<uint32_t *>(pk[h]);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        float y0 = w[2 * i], y1 = w[2 * i + 1];
+                        if (act) unpack2(gelu_erf2(pack2(y0, y1)), y0, y1);
+                        __nv_bfloat162 hh = __floats2bfloat162_rn(y0, y1);
+                        pw[i] = *reinterpret_cast<uint32_t *>(&hh);
+                    }
                 }
-                if (full_box) {
-                    // stage the 32 x 32 box(es), then TMA tensor stores (full 64 B row segments)
-                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                if (full_box && nc == 2) {
+                    // the slot's previous store has finished reading smem; then the 32 x 64
+                    // box in the SWIZZLE_128B layout (16-byte chunk j of row r at j ^ (r & 7))
+                    unsigned char *box = box0 + (nstore % slots) * nbox * OUT_BOX_BYTES;
+                    ++nstore;
+                    if (lane == 0) {
+                        if (slots == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    }
                     __syncwarp();
-                    uint4 *srow = reinterpret_cast<uint4 *>(box + lane * 64);
+                    uint4 *srow = reinterpret_cast<uint4 *>(box + lane * 128);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) srow[i] = pk[i];
+                    for (int j = 0; j < 8; ++j) srow[j ^ (lane & 7)] = pk[j >> 2][j & 3];
                     if (nbox == 2) {
-                        uint4 *srow2 = reinterpret_cast<uint4 *>(box + OUT_BOX_BYTES + lane * 64);
+                        uint4 *srow2 = reinterpret_cast<uint4 *>(box + OUT_BOX_BYTES + lane * 128);
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) srow2[i] = pk2[i];
+                        for (int j = 0; j < 8; ++j) srow2[j ^ (lane & 7)] = pks[j >> 2][j & 3];
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) {
                         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                          reinterpret_cast<uint64_t>(&mapD)),
-                                     "r"((int)dcol0 + c * 32), "r"((int)(t.d_row + q * 32)), "r"(smem_u32(box))
+                                     "r"((int)dcol0 + c * 32), "r"((int)d_row), "r"(smem_u32(box))
                                      : "memory");
                         if (nbox == 2)
                             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                              reinterpret_cast<uint64_t>(&mapD2)),
-                                         "r"((int)dcol0 + c * 32), "r"((int)(t.d_row + q * 32)),
+                                         "r"((int)dcol0 + c * 32), "r"((int)d_row),
                                          "r"(smem_u32(box + OUT_BOX_BYTES))
                                          : "memory");
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
-                } else if (row < t.rows) {
-                    uint4 *dst = reinterpret_cast<uint4 *>(drow + c * 32);
+                } else if (lane < srows) {
+                    // partial strips (a segment's last rows) and a 32-column tail: masked stores
+                    __nv_bfloat16 *drow = a.D + (d_row + lane) * (int64_t)a.N + dcol0 + c * 32;
+                    for (int h = 0; h < nc; ++h) {
+                        uint4 *dst = reinterpret_cast<uint4 *>(drow + h * 32);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) dst[i] = pk[i];
-                    if (nbox == 2) {
-                        uint4 *dst2 = reinterpret_cast<uint4 *>(a.D2 + (t.d_row + row) * (int64_t)a.N + dcol0 + c * 32);
+                        for (int i = 0; i < 4; ++i) dst[i] = pk[h][i];
+                        if (nbox == 2) {
+                            uint4 *dst2 = reinterpret_cast<uint4 *>(a.D2 + (d_row + lane) * (int64_t)a.N + dcol0 +
+                                                                    c * 32 + h * 32);
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) dst2[i] = pk2[i];
+                            for (int i = 0; i < 4; ++i) dst2[i] = pks[h][i];
+                        }
                     }
                 }
             }
@@ -435,16 +460,28 @@ int pick_bn(int N) {
     return 0;
 }
 
-size_t smem_bytes(int CG, int stages, int nbox) {
-    return 1024 + stages * (A_BYTES + B_BYTES_MAX / CG) + nbox * EPI_WARPS * OUT_BOX_BYTES + (2 * stages + 4) * 8 +
-           16 + 32 * 4 + (MAXSEG + 1) * 4;
+size_t smem_bytes(int CG, int stages, int nbox, int slots) {
+    return 1024 + stages * (A_BYTES + B_BYTES_MAX / CG) + (nbox == 2 ? 1 : slots) * nbox * EPI_WARPS * OUT_BOX_BYTES +
+           (2 * stages + 4) * 8 +
+           16 + 32 * 4 + (MAXSEG + 1) * 4 + MAXSEG * 4;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
-int pick_stages(int CG, int nbox) {
+// Output boxes in flight per epilogue warp: SMILE_FFN_OUT_SLOTS (1 or 2, default 1: the
+// smem it frees buys one more operand stage).
+int pick_slots() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SMILE_FFN_OUT_SLOTS");
+        v = (e && e[0] == '2') ? 2 : 1;
+    }
+    return v;
+}
+
+int pick_stages(int CG, int nbox, int slots) {
     int st = 8;
-    while (st > 2 && smem_bytes(CG, st, nbox) > kSmemLimit) --st;
+    while (st > 2 && smem_bytes(CG, st, nbox, slots) > kSmemLimit) --st;
     return st;
 }
 
@@ -465,11 +502,11 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     const int BN = pick_bn(N);
     const int CG = pick_cg(f.num_sms, BN);
     CUtensorMap mA, mB, mD, mD2;
-    if (!make_map(&mA, A, rows_total, K, BM)) return cudaErrorNotSupported;
+    if (!make_map(&mA, A, rows_total, K, 32)) return cudaErrorNotSupported;        // 32-row strip boxes
     if (!make_map(&mB, B, (int64_t)NE * N, K, BN / CG)) return cudaErrorNotSupported;
-    if (!make_map(&mD, D, rows_total, N, 32, 32)) return cudaErrorNotSupported;
+    if (!make_map(&mD, D, rows_total, N, 32, 64)) return cudaErrorNotSupported;     // 32 x 64, SWIZZLE_128B
     mD2 = mD;
-    if (D2 && !make_map(&mD2, D2, rows_total, N, 32, 32)) return cudaErrorNotSupported;
+    if (D2 && !make_map(&mD2, D2, rows_total, N, 32, 64)) return cudaErrorNotSupported;
     TcArgs a;
     memset(&a, 0, sizeof(a));
     a.bias = bias; a.D = reinterpret_cast<__nv_bfloat16 *>(D); a.D2 = reinterpret_cast<__nv_bfloat16 *>(D2);
@@ -477,9 +514,10 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     a.nseg = f.V * f.S * f.e; a.e = f.e; a.S = f.S; a.Cseg = f.Cseg; a.N = N; a.K = K; a.BN = BN; a.gelu = gelu;
     a.mode = mode; a.aux = reinterpret_cast<const __nv_bfloat16 *>(aux);
     const int nbox = mode == EPI_BIAS_SAVE ? 2 : 1;
-    a.stages = pick_stages(CG, nbox);
+    a.slots = pick_slots();
+    a.stages = pick_stages(CG, nbox, a.slots);
     a.err = nullptr;
-    const size_t smem = smem_bytes(CG, a.stages, nbox);
+    const size_t smem = smem_bytes(CG, a.stages, nbox, a.slots);
     if (CG == 2) {
         static bool attr2 = false;
         if (!attr2) {

@@ -23,10 +23,12 @@ struct BlockSync {
     static __device__ __forceinline__ int nthr() { return blockDim.x; }
 };
 
-// The 4 epilogue warps (threads 128..255) of the tensor-core gate, on named barrier 1.
+// Epilogue group G (4 warps, threads 128 + 128 G .. 255 + 128 G) of the tensor-core
+// gate, on named barrier 1 + G.
+template <int G>
 struct EpiSync {
-    static __device__ __forceinline__ void sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-    static __device__ __forceinline__ int tid() { return threadIdx.x - 128; }
+    static __device__ __forceinline__ void sync() { asm volatile("bar.sync %0, 128;" ::"n"(1 + G) : "memory"); }
+    static __device__ __forceinline__ int tid() { return threadIdx.x - 128 - 128 * G; }
     static __device__ __forceinline__ int nthr() { return 128; }
 };
 
@@ -57,28 +59,40 @@ __device__ int block_rank(int b, int K, int *s_wh, int *s_bh) {
     return b >= 0 ? s_wh[w * K + b] + lr : -1;
 }
 
+// Odd row stride for a [tokens][KW] fp32 tile that threads (tokens) walk in lockstep:
+// conflict-free shared-memory banks for any KW (KW = 64 would otherwise be 32-way).
+__host__ __device__ __forceinline__ int gate_lds(int KW) { return KW | 1; }
+
 // Phases B and C of the level-1 gate over one tile of nt <= Sync::nthr() tokens whose
-// logits are s_lg [nt][KW] (rows 0..K1-1: inter router W_p; K1..: intra router W_q).
+// logits are s_lg [nt][lds] (entries 0..K1-1: inter router W_p; K1..KW-1: intra W_q).
 // tok0: global index of the tile's first token; bo: the tile's index in the per-tile
 // tables.  Must be entered by all Sync threads after the logits are visible to them.
 template <class Sync>
-__device__ void gate_finish(const GateArgs &a, float *s_lg, int *s_j, int *s_wh, int *s_bh, int64_t tok0, int nt,
-                            int64_t bo) {
+__device__ void gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j, int *s_wh, int *s_bh, int64_t tok0,
+                            int nt, int64_t bo) {
     const int tid = Sync::tid(), nthr = Sync::nthr();
     const int KW = a.KW, K1 = a.K1, K2 = a.K2;
     // Phase B: one thread per token -- argmax (R2, R3), top-1 probabilities (R4), and
     // the softmax entries for the LB statistics, written back over the logits.
     int i = -1, j = 0;
     if (tid < nt) {
-        float *L = s_lg + tid * KW;
+        float *L = s_lg + tid * lds;
         bool finite = true;
         for (int k = 0; k < KW; ++k) finite &= isfinite(L[k]);
         if (!finite) set_err(a.err, SMILE_ENONFINITE);
         i = 0;
         for (int k = 1; k < K1; ++k)
             if (L[k] > L[i]) i = k;
+        // one expf per entry: e_k = exp(r_k - r_max) is kept, the softmax entry for the
+        // statistics is e_k * (1 / sum) (within 1.5 ulp of e_k / sum; the LB loss
+        // tolerance is 1e-6 relative), and the top-1 probability is 1 / sum exactly.
+        const float mi = L[i];
         float s1 = 0.f;
-        for (int k = 0; k < K1; ++k) s1 += expf(L[k] - L[i]);
+        for (int k = 0; k < K1; ++k) {
+            const float ek = expf(L[k] - mi);
+            L[k] = ek;
+            s1 += ek;
+        }
         const float p = __frcp_rn(s1);
         float q = 1.f;
         if (!a.flat) {
@@ -86,14 +100,17 @@ __device__ void gate_finish(const GateArgs &a, float *s_lg, int *s_j, int *s_wh,
             j = 0;
             for (int k = 1; k < K2; ++k)
                 if (L2[k] > L2[j]) j = k;
-            float s2 = 0.f;
-            for (int k = 0; k < K2; ++k) s2 += expf(L2[k] - L2[j]);
-            q = __frcp_rn(s2);
             const float mj = L2[j];
-            for (int k = 0; k < K2; ++k) L2[k] = __fdiv_rn(expf(L2[k] - mj), s2);
+            float s2 = 0.f;
+            for (int k = 0; k < K2; ++k) {
+                const float ek = expf(L2[k] - mj);
+                L2[k] = ek;
+                s2 += ek;
+            }
+            q = __frcp_rn(s2);
+            for (int k = 0; k < K2; ++k) L2[k] *= q;
         }
-        const float mi = L[i];
-        for (int k = 0; k < K1; ++k) L[k] = __fdiv_rn(expf(L[k] - mi), s1);
+        for (int k = 0; k < K1; ++k) L[k] *= p;
         const int64_t g = tok0 + tid;
         a.route.dest1[g] = i;
         a.route.dest2[g] = j;
@@ -114,7 +131,7 @@ __device__ void gate_finish(const GateArgs &a, float *s_lg, int *s_j, int *s_wh,
         const int lane = tid & 31, w = tid >> 5, NW = nthr >> 5;
         for (int k = w; k < KW; k += NW) {
             double acc = 0.0;
-            for (int tt = lane; tt < nt; tt += 32) acc += (double)s_lg[tt * KW + k];
+            for (int tt = lane; tt < nt; tt += 32) acc += (double)s_lg[tt * lds + k];
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
             if (lane == 0) a.blk_psum[bo * (K1 + K2) + k] = acc;
         }

@@ -14,12 +14,14 @@
 //   warp 0      TMA producer: the tile's x block (128 tokens x 64 columns, SWIZZLE_128B)
 //               and the matching block of the split router (NP x 64), into an smem ring
 //   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M = 128 tokens,
-//               N = NP = 4 * KW (columns 4k..4k+2 hold the three pieces of logit k),
-//               into a double-buffered TMEM accumulator
+//               N = NP = 3 * KW rounded up to 32 (columns 3k..3k+2 hold the three
+//               pieces of logit k), into a double-buffered TMEM accumulator
 //   warp 2      TMEM allocator
-//   warps 4-7   epilogue: tcgen05.ld the tile's accumulator (thread = token), sum the
-//               three pieces, logits to smem, release the accumulator, then the gate's
-//               phases B and C (gate_common.cuh) on named barrier 1.
+//   warps 4-11  two epilogue groups of 4 warps, taking alternate tiles (group g owns
+//               accumulator buffer g): tcgen05.ld the tile's accumulator (thread =
+//               token), sum the three pieces in order, logits to the group's smem,
+//               release the accumulator, then the gate's phases B and C
+//               (gate_common.cuh) on named barrier 1 + g.
 // Tiles are 128 consecutive tokens of one rank, the same tiles as the capacity scan's
 // (TB1 = 128): tile index = v * nblk + blk.
 #include "smile_internal.h"
@@ -34,20 +36,20 @@ namespace {
 using namespace tc;
 
 constexpr int GT_BM = 128, GT_BK = 64;
-constexpr int GT_THREADS = 256;
+constexpr int GT_THREADS = 384;
 constexpr int GT_A_BYTES = GT_BM * GT_BK * 2;   // 16 KB per stage
-constexpr int GT_MAX_NP = 384;                  // 4 * KW <= 384 (KW <= 96)
+constexpr int GT_MAX_NP = 384;                  // 3 * KW <= 384 (KW <= 128)
 
-// W fp32 [KW, d] -> Wb bf16 [NP, d]: row 4k+p = piece p of W[k] (p < 3), row 4k+3 and
-// rows >= 4 KW zero.  r0 = W, piece_p = bf16_rn(r_p), r_{p+1} = r_p - piece_p (exact).
+// W fp32 [KW, d] -> Wb bf16 [NP, d]: row 3k+p = piece p of W[k], rows >= 3 KW zero.
+// r0 = W, piece_p = bf16_rn(r_p), r_{p+1} = r_p - piece_p (exact in fp32).
 __global__ void router_split_kernel(const float *__restrict__ w, __nv_bfloat16 *__restrict__ wb, int KW, int d,
                                     int NP) {
     const int64_t n = (int64_t)NP * d;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(i / d), c = (int)(i - (int64_t)r * d);
-        const int k = r >> 2, p = r & 3;
+        const int k = r / 3, p = r - 3 * k;
         float out = 0.f;
-        if (k < KW && p < 3) {
+        if (k < KW) {
             float rem = w[(int64_t)k * d + c];
             for (int q = 0; q < p; ++q) rem -= __bfloat162float(__float2bfloat16_rn(rem));
             out = rem;
@@ -58,11 +60,27 @@ __global__ void router_split_kernel(const float *__restrict__ w, __nv_bfloat16 *
 
 struct GateTcArgs {
     GateArgs g;
-    int NP;          // accumulator columns (4 * KW rounded up to 32)
+    int NP;          // accumulator columns (3 * KW rounded up to 32)
     int nbuf;        // TMEM accumulator buffers (2 when 2 * NP <= 512)
     int stages;
     int ntiles;
 };
+
+// After the group's logits of one tile are in smem: (optional) logits_out copy, then the
+// gate's phases B and C.
+template <class Sync>
+__device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int *s_j, int *s_wh, int *s_bh,
+                                            int64_t tok0, int nt, int tile) {
+    Sync::sync();
+    if (a.logits_out) {
+        const int lds = gate_lds(a.KW);
+        for (int i = Sync::tid(); i < nt * a.KW; i += Sync::nthr())
+            a.logits_out[tok0 * a.KW + i] = s_lg[(i / a.KW) * lds + i % a.KW];
+        Sync::sync();
+    }
+    gate_finish<Sync>(a, s_lg, gate_lds(a.KW), s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
+    Sync::sync();
+}
 
 __global__ void __launch_bounds__(GT_THREADS, 1)
 gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, GateTcArgs ta) {
@@ -73,12 +91,11 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;
     unsigned char *sB = sA + ST * GT_A_BYTES;
-    float *s_lg = reinterpret_cast<float *>(sB + ST * b_bytes);              // [128][KW]
-    int *s_j = reinterpret_cast<int *>(s_lg + GT_BM * KW);                   // [128]
-    int *s_wh = s_j + GT_BM;                                                 // [4][K1]
-    int *s_bh = s_wh + 4 * a.K1;                                             // [K1]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(
-        ((uintptr_t)(s_bh + a.K1) + 7) & ~(uintptr_t)7);
+    // per epilogue group g: logits [128][lds] | s_j [128] | s_wh [4][K1] | s_bh [K1]
+    const int lds = gate_lds(KW);
+    const int grp_ints = GT_BM * lds + GT_BM + 5 * a.K1;
+    int *grp0 = reinterpret_cast<int *>(sB + ST * b_bytes);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(grp0 + ta.nbuf * grp_ints) + 7) & ~(uintptr_t)7);
     uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 4);
 
@@ -163,10 +180,19 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: thread = token (TMEM lane) ----------------
+        const int grp = (warp - 4) >> 2;
         const int q = warp & 3;
         const int row = q * 32 + lane;
-        int it = 0;
-        for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
+        float *s_lg = reinterpret_cast<float *>(grp0 + grp * grp_ints);
+        int *s_j = reinterpret_cast<int *>(s_lg + GT_BM * lds);
+        int *s_wh = s_j + GT_BM;
+        int *s_bh = s_wh + 4 * a.K1;
+        // with a single accumulator buffer (NP > 256) one group takes every tile: the
+        // tfull / tempty parities then count every tile of the CTA
+        const int ngrp = nbuf;
+        int it = grp;
+        for (int tile = blockIdx.x + grp * gridDim.x; grp < ngrp && tile < ta.ntiles;
+             tile += ngrp * gridDim.x, it += ngrp) {
             const int v = tile / a.nblk, blk = tile - v * a.nblk;
             const int64_t t0 = (int64_t)blk * GT_BM;
             const int nt = (int)(a.T - t0 < GT_BM ? a.T - t0 : GT_BM);
@@ -175,25 +201,26 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
             mbar_wait(smem_u32(&tfull[buf]), (uint32_t)(it / nbuf) & 1);
             tc_fence_after();
             const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + buf * NP;
+            // logit k = (piece0 + piece1) + piece2 from columns 3k, 3k+1, 3k+2
+            float accv = 0.f;
             for (int c = 0; c < NP / 32; ++c) {
                 float vv[32];
                 tmem_ld32(tb + c * 32, vv);
+                int k = (c * 32) / 3, pc = (c * 32) - 3 * k;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int k = c * 8 + i;
-                    if (k < KW) s_lg[row * KW + k] = (vv[4 * i] + vv[4 * i + 1]) + vv[4 * i + 2];
+                for (int i = 0; i < 32; ++i) {
+                    if (k < KW) {
+                        accv = pc == 0 ? vv[i] : accv + vv[i];
+                        if (pc == 2) s_lg[row * lds + k] = accv;
+                    }
+                    if (++pc == 3) { pc = 0; ++k; }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
-            EpiSync::sync();
-            if (a.logits_out) {
-                for (int i = EpiSync::tid(); i < nt * KW; i += 128) a.logits_out[tok0 * KW + i] = s_lg[i];
-                EpiSync::sync();
-            }
-            gate_finish<EpiSync>(a, s_lg, s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
-            EpiSync::sync();
+            if (grp == 0) finish_tile<EpiSync<0>>(a, s_lg, s_j, s_wh, s_bh, tok0, nt, tile);
+            else finish_tile<EpiSync<1>>(a, s_lg, s_j, s_wh, s_bh, tok0, nt, tile);
         }
     }
     __syncthreads();
@@ -204,13 +231,14 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
 }
 
 size_t gate_tc_smem(int NP, int KW, int K1, int stages) {
-    return 1024 + (size_t)stages * (GT_A_BYTES + NP * GT_BK * 2) + (size_t)GT_BM * KW * 4 + GT_BM * 4 +
-           5 * (size_t)K1 * 4 + 8 + (2 * stages + 4) * 8 + 16;
+    const int groups = 2 * NP <= 512 ? 2 : 1;          // = nbuf
+    return 1024 + (size_t)stages * (GT_A_BYTES + NP * GT_BK * 2) + groups * ((size_t)GT_BM * gate_lds(KW) + GT_BM + 5 * K1) * 4 + 8 +
+           (2 * stages + 4) * 8 + 16;
 }
 
 }  // namespace
 
-int gate_tc_np(int KW) { return ((4 * KW + 31) / 32) * 32; }
+int gate_tc_np(int KW) { return ((3 * KW + 31) / 32) * 32; }
 
 bool gate_tc_supported(int bf16, int d, int KW) {
     return bf16 && d % GT_BK == 0 && d >= GT_BK && gate_tc_np(KW) <= GT_MAX_NP && encode_fn() != nullptr;

@@ -47,7 +47,7 @@ constexpr int kRT = 4;
 constexpr int kRouterSmem = 48 * 1024;
 
 template <bool BF16>
-__device__ void router_tile(const GateArgs &a, float *s_lg, float *s_w, int64_t tok0, int nt) {
+__device__ void router_tile(const GateArgs &a, float *s_lg, int lds, float *s_w, int64_t tok0, int nt) {
     constexpr int EPV = BF16 ? 8 : 4;          // elements per 16-byte vector
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const int KW = a.KW, d = a.d, nchunk = d / EPV;
@@ -115,7 +115,7 @@ __device__ void router_tile(const GateArgs &a, float *s_lg, float *s_w, int64_t 
                     float v = acc[r][kk];
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-                    if (lane == 0 && k0 + kk < KW && tt0 + r < nt) s_lg[(tt0 + r) * KW + k0 + kk] = v;
+                    if (lane == 0 && k0 + kk < KW && tt0 + r < nt) s_lg[(tt0 + r) * lds + k0 + kk] = v;
                 }
         }
     }
@@ -123,14 +123,15 @@ __device__ void router_tile(const GateArgs &a, float *s_lg, float *s_w, int64_t 
 
 // ---------------------------------------------------------------------------------
 // a1-a3: level-1 gate.  grid (nblk, V), block TB threads (one token per thread).
-// smem: logits tile [TB][KW] fp32 | s_j [TB] | warp hist [NW][K1] | block hist [K1]
+// smem: logits tile [TB][lds] fp32 | s_j [TB] | warp hist [NW][K1] | block hist [K1]
 // ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256, 2) gate1_kernel(GateArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *s_lg = reinterpret_cast<float *>(smem_raw);
-    int *s_j = reinterpret_cast<int *>(s_lg + (size_t)a.TB * a.KW);
+    const int lds = gate_lds(a.KW);
+    int *s_j = reinterpret_cast<int *>(s_lg + (size_t)a.TB * lds);
     int *s_wh = s_j + a.TB;
-    int *s_bh = s_wh + (a.TB / 32) * a.K1;
+    int *s_bh = s_wh + (((a.TB / 32) * a.K1 + 3) & ~3);               // 16-byte aligned s_w below
     float *s_w = reinterpret_cast<float *>(s_bh + ((a.K1 + 3) & ~3));   // [KW, d] when it fits
 
     const int v = blockIdx.y, blk = blockIdx.x, tid = threadIdx.x;
@@ -142,18 +143,18 @@ __global__ void __launch_bounds__(256, 2) gate1_kernel(GateArgs a) {
     // Phase A: the block's logits tile (Eq. 1: r = W x).
     if (a.logits) {
         const float *src = a.logits + tok0 * KW;
-        for (int i = tid; i < nt * KW; i += blockDim.x) s_lg[i] = __ldg(src + i);
+        for (int i = tid; i < nt * KW; i += blockDim.x) s_lg[(i / KW) * lds + i % KW] = __ldg(src + i);
     } else if (a.bf16) {
-        router_tile<true>(a, s_lg, s_w, tok0, nt);
+        router_tile<true>(a, s_lg, lds, s_w, tok0, nt);
     } else {
-        router_tile<false>(a, s_lg, s_w, tok0, nt);
+        router_tile<false>(a, s_lg, lds, s_w, tok0, nt);
     }
     __syncthreads();
     if (a.logits_out && !a.logits)
-        for (int i = tid; i < nt * KW; i += blockDim.x) a.logits_out[tok0 * KW + i] = s_lg[i];
+        for (int i = tid; i < nt * KW; i += blockDim.x) a.logits_out[tok0 * KW + i] = s_lg[(i / KW) * lds + i % KW];
     if (a.logits_out && !a.logits) __syncthreads();
 
-    gate_finish<BlockSync>(a, s_lg, s_j, s_wh, s_bh, tok0, nt, (int64_t)v * a.nblk + blk);
+    gate_finish<BlockSync>(a, s_lg, lds, s_j, s_wh, s_bh, tok0, nt, (int64_t)v * a.nblk + blk);
 }
 
 // Warp-wide exclusive scan over n ints at stride `st` (in place), returns the total.
@@ -579,7 +580,8 @@ inline int grid_for(int64_t warps_needed, int per_block_warps, int cap) {
 
 void launch_gate1(const GateArgs &a, cudaStream_t st) {
     if (a.T == 0) return;
-    size_t smem = (size_t)a.TB * a.KW * 4 + (size_t)a.TB * 4 + (size_t)(a.TB / 32) * a.K1 * 4 + (size_t)((a.K1 + 3) & ~3) * 4;
+    size_t smem = (size_t)a.TB * gate_lds(a.KW) * 4 + (size_t)a.TB * 4 + (size_t)(((a.TB / 32) * a.K1 + 3) & ~3) * 4 +
+                  (size_t)((a.K1 + 3) & ~3) * 4;
     if (!a.logits && (size_t)a.KW * a.d * 4 <= (size_t)kRouterSmem) smem += (size_t)a.KW * a.d * 4;
     static bool attr_set = false;
     if (!attr_set) {

@@ -80,6 +80,7 @@ struct smile_ctx_s {
     smile::PeerMap peer{};
     // tensor-core gate (bf16 fused router): the three-piece bf16 split of the router
     __nv_bfloat16 *wsplit = nullptr;         // [gate_tc_np(KW), d], rewritten every fused gate call
+    float *colsum_ws = nullptr;              // bias-gradient partials of smile_expert_ffn_bwd
 };
 
 namespace smile {
@@ -180,12 +181,22 @@ struct FfnBwdArgs {
     const void *W1; const void *W2;          // math layouts: W1 [NE, d, d_ff], W2 [NE, d_ff, d]
     void *dZ; void *dX; float *dW1; float *db1; float *dW2; float *db2;
     int V, S, e; int64_t Cseg; int d, d_ff; int bf16; int num_sms;
+    float *colsum_ws;                        // bias-gradient partials (colsum_ws_bytes)
 };
 cudaError_t launch_ffn_bwd(const FfnBwdArgs &a, bool tc, cudaStream_t st);
 // Forward that also stores the pre-activation A1 = X W1 + b1 (training).
 cudaError_t launch_ffn_fwd_train(const FfnArgs &a, void *A1, bool tc, cudaStream_t st);
 // Returns cudaErrorNotSupported when the shape cannot run on the tcgen05 path.
 cudaError_t launch_ffn_tcgen05(const FfnArgs &a, cudaStream_t st);
+
+// Weight / bias gradients (wgrad_tcgen05.cu).
+size_t colsum_ws_bytes(int NE, int S, int64_t Cseg, int maxN);
+void launch_colsum(const void *B, float *db, float *part, const int32_t *counts, int NE, int e, int S, int64_t Cseg,
+                   int N, int bf16, cudaStream_t st);
+bool wgrad_tc_supported(int bf16, int d, int d_ff, int S);
+cudaError_t launch_wgrad_tc(const void *A, int M, const void *B, int N, float *Dw, const int32_t *counts, int V, int S,
+                            int e, int64_t Cseg, int num_sms, cudaStream_t st);
+void launch_pad_rows_zero(void *buf, const int32_t *counts, int nseg, int64_t Cseg, int cols, cudaStream_t st);
 
 // Level-1 gate with the router on tcgen05 (gate_tcgen05.cu); needs TB == 128.
 int gate_tc_np(int KW);

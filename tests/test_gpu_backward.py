@@ -2,7 +2,9 @@
 pinned fp64 backward oracle (tests/test_oracle_backward.py): router dlogits, dx, the
 router weight gradient and every expert weight / bias gradient, on seeded inputs with
 drops at both levels.  Tolerances (atol = rtol * max|ref|): fp32 1e-4 (fp32 GEMMs and
-softmax derivatives against fp64), bf16 3e-2 (bf16 dY / dZ / H / returned expert rows)."""
+softmax derivatives against fp64), bf16 3e-2 (bf16 dY / dZ / H / returned expert rows).
+bf16 cases with d, d_ff multiples of 128 run the tcgen05 weight gradients (MN-major
+operands, wgrad_tcgen05.cu); the others the SIMT ones."""
 import numpy as np
 import pytest
 import torch
@@ -66,6 +68,8 @@ def run_bwd(case, lam=2.0, seed=0):
     (2, 4, 1, 600, 128, 256, 1.25, "bf16", "bilevel", True, "tcgen05"),   # C3-like 2x4, tcgen05 dgrad
     (4, 2, 1, 600, 128, 256, 1.25, "bf16", "bilevel", False, "tcgen05"),  # C3-like 4x2
     (2, 2, 2, 400, 64, 128, 1.0, "bf16", "flat", True, "tcgen05"),
+    (2, 2, 2, 700, 128, 384, 1.0, "bf16", "flat", True, "tcgen05"),     # tcgen05 wgrad, e = 2, BN 128 / 192
+    (2, 4, 1, 2000, 256, 512, 1.25, "bf16", "bilevel", False, "tcgen05"),  # wgrad over many K blocks
 ])
 def test_backward_parity(n, m, e, T, d, d_ff, cf, dtype, mode, fused, ffn):
     case = Case(n, m, e, T, d, d_ff, cf, dtype=dtype, mode=mode, dist="skewed", seed=21, fused=fused, ffn_impl=ffn)
