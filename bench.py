@@ -329,6 +329,49 @@ def hbm_phases(res, peaks):
     return out
 
 
+def nvlink_levels(res, world, mode, exchange):
+    """Per exchange level: bytes this process sends to other GPUs in one direction
+    (valid rows only; the reverse path moves the same bytes back) and the achieved
+    NVLink GB/s over the phases that carry them.  PEER: the permute / combine kernels
+    store / load remote rows, so a level's time is its mover phase plus its barrier;
+    COPY: the NCCL all-to-all phase (which moves capacity-padded chunks)."""
+    if world == 1:
+        return None
+    ph = res["phase_ms"]
+    if mode == "bilevel":
+        legs = {"inter": (("dispatch1", "a2a_inter"), ("combine1", "a2a_inter_rev")),
+                "intra": (("dispatch2", "a2a_intra"), ("combine2", "a2a_intra_rev"))}
+    else:
+        legs = {"world": (("dispatch1", "a2a_world"), ("combine1", "a2a_world_rev"))}
+    out = {}
+    for lvl, (fwd, rev) in legs.items():
+        b = res["nvl_bytes"].get(lvl, 0)
+        tf = sum(ph[p] for p in fwd) if exchange == "peer" else ph[fwd[1]]
+        tr = sum(ph[p] for p in rev) if exchange == "peer" else ph[rev[1]]
+        out[lvl] = {"bytes_per_direction": b, "fwd_ms": tf, "rev_ms": tr,
+                    "fwd_GB/s": b / (tf / 1e3) / 1e9 if tf else None, "rev_GB/s": b / (tr / 1e3) / 1e9 if tr else None}
+    out["note"] = ("rank-0 process, valid rows only; peer: mover + barrier phases, copy: NCCL phase; "
+                   "measured NVLink reference 770 GB/s per direction (B200_PROFILING.md)")
+    return out
+
+
+def layer_roofline(res, cfgd, peaks, world, flops):
+    """layer time bound = HBM bytes / HBM peak + NVLink bytes / 770 GB/s +
+    FFN flops / bf16 peak (serial) or max(HBM + NVLink, FFN) (perfect overlap), per
+    process; tokens/s of the whole job = G*T / that time."""
+    hbm_b = sum(res["hbm_bytes"].values())
+    nvl_b = 2 * sum(res["nvl_bytes"].values()) if world > 1 else 0
+    t_h = hbm_b / (peaks.get("hbm_gbs", 6449.1) * 1e9)
+    t_n = nvl_b / 770e9
+    t_f = flops / (peaks.get("bf16_tflops", 1620.5) * 1e12)
+    ser, ovl = t_h + t_n + t_f, max(t_h + t_n, t_f)
+    tok = res["tokens"]
+    return {"t_hbm_ms": t_h * 1e3, "t_nvlink_ms": t_n * 1e3, "t_ffn_ms": t_f * 1e3,
+            "serial_tokens_per_s": tok / ser, "overlap_tokens_per_s": tok / ovl,
+            "frac_serial": (tok / (res["ms"] / 1e3)) / (tok / ser), "frac_overlap": (tok / (res["ms"] / 1e3)) / (tok / ovl),
+            "note": "per process (max over ranks of the measured step); HBM bytes as hbm_phases, FFN flops as roofline"}
+
+
 def run_ours(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -486,11 +529,26 @@ def run_ours(args):
         if mode == "bilevel":
             recv2 = int(w["counts2"].sum().item())
             hbm.update({"dispatch2": 2 * recv2 * rb, "combine2": 2 * recv2 * rb})
+        # rows this process sends to ranks of OTHER processes (NVLink), per level
+        c1 = w["counts1"].cpu().numpy()
+        r0 = rank * V
+        nvl = {}
+        if mode == "bilevel":
+            m_ = cfgd["m"]
+            rem1 = sum(int(c1[v, i]) for v in range(V) for i in range(cfgd["n"])
+                       if (i * m_ + (r0 + v) % m_) // V != rank)
+            c2 = w["counts2"].cpu().numpy()
+            rem2 = sum(int(c2[v, k]) for v in range(V) for k in range(c2.shape[1])
+                       if (((r0 + v) // m_) * m_ + k // e) // V != rank)
+            nvl = {"inter": rem1 * rb, "intra": rem2 * rb}
+        else:
+            nvl = {"world": sum(int(c1[v, E]) for v in range(V) for E in range(c1.shape[1]) if (E // e) // V != rank) * rb}
         ffn_ms = phase_ms["ffn"] if not train else None
         ffn_tc = cfgd["dtype"] == "bf16" and args.ffn != "simt" and smb.TCGEN05_DEFAULT
         res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, rank_ms=rank_ms, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms,
                    t_beg=t_beg, t_end=t_end,
-                   tokens=G * T, launches=launched, hbm_bytes=hbm, train=train, eager_ms=eager_ms, graph_ms=graph_ms)
+                   tokens=G * T, launches=launched, hbm_bytes=hbm, train=train, eager_ms=eager_ms, graph_ms=graph_ms,
+                   nvl_bytes=nvl)
         if train:
             res["hbm_bytes"] = {}
         # e2e through smile_forward_host (pinned host x, D2H out + loss)
@@ -554,7 +612,11 @@ def run_ours(args):
                 "frac": achieved / alu_peak, "peak_source": f"148 SM x 128 FP32 lanes x 2 x {clk:.0f} MHz"}
     roof["kernel"] = ("whole training step (expert FFN fwd + bwd flops / step time; wgrad on SIMT)" if main.get("train")
                       else "smile_expert_ffn (2 grouped GEMM launches)")
-    roof["traffic"] = traffic.get(f"{args.config}_{modes[0]}_ffn")
+    tr = traffic.get(f"{args.config}_{modes[0]}_ffn")
+    roof["traffic"] = tr["bytes_per_step"] if tr else None
+    if tr:
+        roof["traffic_note"] = (f"DRAM read+write bytes of the FFN's {tr['launches']} GEMM launches of one step, "
+                                f"ncu --set full ({tr['source']})")
     roof["algorithmic_flops_per_step"] = flops
     line = {
         "metric": METRIC, "value": main["tokens"] / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
@@ -572,6 +634,8 @@ def run_ours(args):
         "cuda_graph": main["graph_ms"] is not None, "eager_ms_per_step": main["eager_ms"],
         "roofline": roof,
         "hbm_phases": hbm_phases(main, peaks),
+        "nvlink": nvlink_levels(main, world, modes[0], args.exchange),
+        "layer_roofline": None if main.get("train") else layer_roofline(main, cfgd, peaks, world, flops),
         "gpu_launches": main["launches"],
         "gpu_launches_note": "libsmile kernels launched in the timed region (smile_launch_count delta; NCCL not counted)",
         "clocks": main.get("clocks"),

@@ -33,13 +33,12 @@ namespace {
 using namespace tc;
 
 constexpr int BM = 128, BK = 64, MAXSEG = 1024;
-constexpr int EPI_WARPS = 8;                  // 2 warps per TMEM lane quadrant, split by columns
+constexpr int EPI_WARPS = 16;                 // 4 warps per TMEM lane quadrant, split by columns
 constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
 constexpr int B_BYTES_MAX = 256 * BK * 2;     // 32 KB
 constexpr int ACC_COLS = 256;                 // TMEM columns per accumulator buffer
-constexpr int OUT_BOX_BYTES = 32 * 64 * 2;    // per epilogue warp: 32 rows x 64 bf16 staged for a TMA store
-constexpr int OUT_SLOTS = 2;                  // boxes per warp in flight (the store of chunk c overlaps chunk c+1)
+constexpr int OUT_BOX_BYTES = 32 * 32 * 2;    // per epilogue warp: 32 rows x 32 bf16 staged for a TMA store
 
 struct TcArgs {
     const float *bias;       // [NE, N]
@@ -53,7 +52,7 @@ struct TcArgs {
     int mode;                  // EPI_* below
     const __nv_bfloat16 *aux;  // EPI_DGELU: the saved pre-activation A1 [rows_total, N]
     int stages;                // smem pipeline depth
-    int slots;                 // output boxes in flight per epilogue warp (1 or 2)
+    int tma_store;             // 1: full 32 x 32 boxes leave through smem + TMA; 0: st.global from registers
     int *err;
 };
 
@@ -166,7 +165,8 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref
 // and half of B, which halves the shared-memory operand traffic per SM.
 template <int CG>
 __global__ void __launch_bounds__(NTHREADS, 1)
-ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA128,
+                 const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ CUtensorMap mapD, const __grid_constant__ CUtensorMap mapD2, TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte aligned carve-up: [A stages][B stages][out boxes][barriers][tmem holder][prefix]
@@ -177,8 +177,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     const int b_stage_bytes = B_BYTES_MAX / CG;
     unsigned char *sB = sA + STAGES * A_BYTES;
     unsigned char *sOut = sB + STAGES * b_stage_bytes;                // EPI_WARPS x nbox x 2 KB
-    const int slots = nbox == 2 ? 1 : a.slots;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sOut + slots * nbox * EPI_WARPS * OUT_BOX_BYTES);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sOut + (a.tma_store ? nbox * EPI_WARPS * OUT_BOX_BYTES : 0));
     uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
     int *s_warp = reinterpret_cast<int *>(tmem_holder + 4);
@@ -202,6 +201,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     }
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA128)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapD)) : "memory");
         if (nbox == 2) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapD2)) : "memory");
@@ -237,8 +237,10 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             uint32_t phase = 0;
             for (int tile = cid; tile < total; tile += ncl) {
                 const TileInfo t = tile_info<CG>(a, s_pref, tile, ntn, rank);
-                // A: four 32-row strip boxes per K block (4 KB each, stacked = one 128-row
-                // SW128 tile), their rows resolved once per tile
+                // A: one 128-row box when the tile's 4 strips are consecutive rows (fewer
+                // TMA requests: the L2 -> SM path is what bounds these GEMMs), else four
+                // 32-row strip boxes (4 KB each, stacked = the same SW128 tile); rows
+                // resolved once per tile
                 int srow[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -247,22 +249,29 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + j, r, nr);
                     srow[j] = (int)r;
                 }
+                const bool contig = srow[1] == srow[0] + 32 && srow[2] == srow[0] + 64 && srow[3] == srow[0] + 96;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full[stage]);
                     if (CG == 1) {
                         mbar_arrive_tx(fb, A_BYTES + b_bytes);
-                        for (int j = 0; j < 4; ++j)
-                            tma_load_2d(smem_u32(sA + stage * A_BYTES + j * (A_BYTES / 4)), &mapA, kb * BK,
-                                        srow[j], fb);
+                        if (contig)
+                            tma_load_2d(smem_u32(sA + stage * A_BYTES), &mapA128, kb * BK, srow[0], fb);
+                        else
+                            for (int j = 0; j < 4; ++j)
+                                tma_load_2d(smem_u32(sA + stage * A_BYTES + j * (A_BYTES / 4)), &mapA, kb * BK,
+                                            srow[j], fb);
                         tma_load_2d(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)t.b_row, fb);
                     } else {
                         // the leader's full barrier counts the bytes of both CTAs' loads
                         if (leader) mbar_arrive_tx(fb, CG * (A_BYTES + b_bytes));
                         const uint32_t fbl = mapa_shared(fb, 0);
-                        for (int j = 0; j < 4; ++j)
-                            tma_load_2d_pair(smem_u32(sA + stage * A_BYTES + j * (A_BYTES / 4)), &mapA, kb * BK,
-                                             srow[j], fbl);
+                        if (contig)
+                            tma_load_2d_pair(smem_u32(sA + stage * A_BYTES), &mapA128, kb * BK, srow[0], fbl);
+                        else
+                            for (int j = 0; j < 4; ++j)
+                                tma_load_2d_pair(smem_u32(sA + stage * A_BYTES + j * (A_BYTES / 4)), &mapA,
+                                                 kb * BK, srow[j], fbl);
                         tma_load_2d_pair(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)t.b_row, fbl);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -304,16 +313,18 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             }
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue: 8 warps; quadrant q = rows 32q..32q+31 ----------------
-        // Each warp owns half of the tile's columns and walks them in steps of 64: two
-        // tcgen05.ld (one wait), bias / activation in packed fp32x2, bf16, then one
-        // 32 x 64 SWIZZLE_128B box per output tensor in smem and one TMA tensor store.
+        // ---------------- epilogue: 16 warps ----------------
+        // Warp w reads TMEM lane quadrant q = w & 3 (the tile's strip q) and column group
+        // h = (w - 4) >> 2 of 4, in 32-column chunks: tcgen05.ld -> bias / GELU in packed
+        // fp32x2 -> bf16 -> a 32 x 32 SWIZZLE_64B box in smem -> one TMA tensor store.
+        // Four warps per quadrant keep enough independent work in flight to hide the
+        // TMEM / global / fixed-latency dependencies of the epilogue behind the MMAs.
         const int q = warp & 3;
-        const int half = (warp - 4) >> 2;
+        const int h = (warp - 4) >> 2;
         const int nch = a.BN / 32;
-        const int c_beg = half ? (nch + 1) / 2 : 0, c_end = half ? nch : (nch + 1) / 2;
+        const int c_beg = (h * nch) / 4, c_end = ((h + 1) * nch) / 4;
         int it = 0;
-        uint32_t nstore = 0;                      // this warp's box stores so far (slot = nstore % slots)
+        unsigned char *box = sOut + (warp - 4) * nbox * OUT_BOX_BYTES;
         for (int tile = cid; tile < total; tile += ncl, ++it) {
             const TileInfo t = tile_info<CG>(a, s_pref, tile, ntn, rank);
             const int acc = it & 1;
@@ -324,83 +335,68 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             const bool act = (a.mode == EPI_BIAS && a.gelu) || a.mode == EPI_BIAS_SAVE;
             const float4 *bias4 = reinterpret_cast<const float4 *>(a.bias + (int64_t)t.E * a.N + (int64_t)t.nt * a.BN);
             const int64_t dcol0 = (int64_t)t.nt * a.BN;
-            unsigned char *box0 = sOut + (warp - 4) * slots * nbox * OUT_BOX_BYTES;
             int64_t d_row;                                  // this warp's strip
             int srows;
             expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + q, d_row, srows);
             const bool full_box = srows == 32;
-            const bool any_row = srows > 0;
-            for (int c = c_beg; c < c_end && any_row; c += 2) {
-                const int nc = c + 1 < c_end ? 2 : 1;          // 32-column chunks in this step
-                float v[2][32];
-                tmem_ld32_nowait(tbase + c * 32, v[0]);
-                if (nc == 2) tmem_ld32_nowait(tbase + c * 32 + 32, v[1]);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                uint4 pk[2][4], pks[2][4];
+            for (int c = c_beg; c < c_end && srows > 0; ++c) {
+                float w[32];
+                tmem_ld32(tbase + c * 32, w);
+                if (has_bias) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (h >= nc) break;
-                    float *w = v[h];
-                    const int cc = c + h;
-                    if (has_bias) {
-#pragma unroll
-                        for (int i4 = 0; i4 < 8; ++i4) {
-                            const float4 b = __ldg(bias4 + cc * 8 + i4);
-                            const f32x2 lo = add2(pack2(w[4 * i4], w[4 * i4 + 1]), pack2(b.x, b.y));
-                            const f32x2 hi = add2(pack2(w[4 * i4 + 2], w[4 * i4 + 3]), pack2(b.z, b.w));
-                            unpack2(lo, w[4 * i4], w[4 * i4 + 1]);
-                            unpack2(hi, w[4 * i4 + 2], w[4 * i4 + 3]);
-                        }
-                    }
-                    if (a.mode == EPI_BIAS_SAVE) {
-                        uint32_t *pw2 = reinterpret_cast<uint32_t *>(pks[h]);
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            __nv_bfloat162 hh = __floats2bfloat162_rn(w[2 * i], w[2 * i + 1]);
-                            pw2[i] = *reinterpret_cast<uint32_t *>(&hh);
-                        }
-                    }
-                    if (a.mode == EPI_DGELU && lane < srows) {
-                        const uint4 *ap =
-                            reinterpret_cast<const uint4 *>(a.aux + (d_row + lane) * (int64_t)a.N + dcol0 + cc * 32);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const uint4 u = __ldg(ap + i);
-                            const __nv_bfloat162 *hh = reinterpret_cast<const __nv_bfloat162 *>(&u);
-#pragma unroll
-                            for (int z = 0; z < 4; ++z) {
-                                const float2 f = __bfloat1622float2(hh[z]);
-                                w[8 * i + 2 * z] *= gelu_grad(f.x);
-                                w[8 * i + 2 * z + 1] *= gelu_grad(f.y);
-                            }
-                        }
-                    }
-                    uint32_t *pw = reinterpret_cast<uint32_t *>(pk[h]);
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        float y0 = w[2 * i], y1 = w[2 * i + 1];
-                        if (act) unpack2(gelu_erf2(pack2(y0, y1)), y0, y1);
-                        __nv_bfloat162 hh = __floats2bfloat162_rn(y0, y1);
-                        pw[i] = *reinterpret_cast<uint32_t *>(&hh);
+                    for (int i4 = 0; i4 < 8; ++i4) {
+                        const float4 b = __ldg(bias4 + c * 8 + i4);
+                        const f32x2 lo = add2(pack2(w[4 * i4], w[4 * i4 + 1]), pack2(b.x, b.y));
+                        const f32x2 hi = add2(pack2(w[4 * i4 + 2], w[4 * i4 + 3]), pack2(b.z, b.w));
+                        unpack2(lo, w[4 * i4], w[4 * i4 + 1]);
+                        unpack2(hi, w[4 * i4 + 2], w[4 * i4 + 3]);
                     }
                 }
-                if (full_box && nc == 2) {
-                    // the slot's previous store has finished reading smem; then the 32 x 64
-                    // box in the SWIZZLE_128B layout (16-byte chunk j of row r at j ^ (r & 7))
-                    unsigned char *box = box0 + (nstore % slots) * nbox * OUT_BOX_BYTES;
-                    ++nstore;
-                    if (lane == 0) {
-                        if (slots == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                        else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                uint4 pk[4], pks[4];
+                if (a.mode == EPI_BIAS_SAVE) {
+                    uint32_t *pw2 = reinterpret_cast<uint32_t *>(pks);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        __nv_bfloat162 hh = __floats2bfloat162_rn(w[2 * i], w[2 * i + 1]);
+                        pw2[i] = *reinterpret_cast<uint32_t *>(&hh);
                     }
+                }
+                if (a.mode == EPI_DGELU && lane < srows) {
+                    const uint4 *ap =
+                        reinterpret_cast<const uint4 *>(a.aux + (d_row + lane) * (int64_t)a.N + dcol0 + c * 32);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint4 u = __ldg(ap + i);
+                        const __nv_bfloat162 *hh = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+                        for (int z = 0; z < 4; ++z) {
+                            const float2 f = __bfloat1622float2(hh[z]);
+                            w[8 * i + 2 * z] *= gelu_grad(f.x);
+                            w[8 * i + 2 * z + 1] *= gelu_grad(f.y);
+                        }
+                    }
+                }
+                uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    float y0 = w[2 * i], y1 = w[2 * i + 1];
+                    if (act) unpack2(gelu_erf2(pack2(y0, y1)), y0, y1);
+                    __nv_bfloat162 hh = __floats2bfloat162_rn(y0, y1);
+                    pw[i] = *reinterpret_cast<uint32_t *>(&hh);
+                }
+                if (full_box && a.tma_store) {
+                    // the box's previous store has finished reading smem; then the 32 x 32 box
+                    // in the SWIZZLE_64B layout (16-byte chunk j of row r at j ^ ((r >> 1) & 3))
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     __syncwarp();
-                    uint4 *srow = reinterpret_cast<uint4 *>(box + lane * 128);
+                    uint4 *srow = reinterpret_cast<uint4 *>(box + lane * 64);
+                    const int sw = (lane >> 1) & 3;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) srow[j ^ (lane & 7)] = pk[j >> 2][j & 3];
+                    for (int j = 0; j < 4; ++j) srow[j ^ sw] = pk[j];
                     if (nbox == 2) {
-                        uint4 *srow2 = reinterpret_cast<uint4 *>(box + OUT_BOX_BYTES + lane * 128);
+                        uint4 *srow2 = reinterpret_cast<uint4 *>(box + OUT_BOX_BYTES + lane * 64);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) srow2[j ^ (lane & 7)] = pks[j >> 2][j & 3];
+                        for (int j = 0; j < 4; ++j) srow2[j ^ sw] = pks[j];
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
@@ -412,24 +408,20 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                         if (nbox == 2)
                             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                              reinterpret_cast<uint64_t>(&mapD2)),
-                                         "r"((int)dcol0 + c * 32), "r"((int)d_row),
-                                         "r"(smem_u32(box + OUT_BOX_BYTES))
+                                         "r"((int)dcol0 + c * 32), "r"((int)d_row), "r"(smem_u32(box + OUT_BOX_BYTES))
                                          : "memory");
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
                 } else if (lane < srows) {
-                    // partial strips (a segment's last rows) and a 32-column tail: masked stores
-                    __nv_bfloat16 *drow = a.D + (d_row + lane) * (int64_t)a.N + dcol0 + c * 32;
-                    for (int h = 0; h < nc; ++h) {
-                        uint4 *dst = reinterpret_cast<uint4 *>(drow + h * 32);
+                    // partial strips (a segment's last rows), or tma_store == 0: st.global of
+                    // this lane's row (64 contiguous bytes per output), valid rows only
+                    uint4 *dst = reinterpret_cast<uint4 *>(a.D + (d_row + lane) * (int64_t)a.N + dcol0 + c * 32);
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) dst[i] = pk[h][i];
-                        if (nbox == 2) {
-                            uint4 *dst2 = reinterpret_cast<uint4 *>(a.D2 + (d_row + lane) * (int64_t)a.N + dcol0 +
-                                                                    c * 32 + h * 32);
+                    for (int i = 0; i < 4; ++i) dst[i] = pk[i];
+                    if (nbox == 2) {
+                        uint4 *dst2 = reinterpret_cast<uint4 *>(a.D2 + (d_row + lane) * (int64_t)a.N + dcol0 + c * 32);
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) dst2[i] = pks[h][i];
-                        }
+                        for (int i = 0; i < 4; ++i) dst2[i] = pks[i];
                     }
                 }
             }
@@ -460,28 +452,30 @@ int pick_bn(int N) {
     return 0;
 }
 
-size_t smem_bytes(int CG, int stages, int nbox, int slots) {
-    return 1024 + stages * (A_BYTES + B_BYTES_MAX / CG) + (nbox == 2 ? 1 : slots) * nbox * EPI_WARPS * OUT_BOX_BYTES +
+size_t smem_bytes(int CG, int stages, int nbox, int tma_store) {
+    return 1024 + stages * (A_BYTES + B_BYTES_MAX / CG) + (tma_store ? nbox * EPI_WARPS * OUT_BOX_BYTES : 0) +
            (2 * stages + 4) * 8 +
            16 + 32 * 4 + (MAXSEG + 1) * 4 + MAXSEG * 4;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
-// Output boxes in flight per epilogue warp: SMILE_FFN_OUT_SLOTS (1 or 2, default 1: the
-// smem it frees buys one more operand stage).
-int pick_slots() {
+// Epilogue output path: full 32 x 32 boxes staged in smem and written by TMA tensor
+// stores (default), or SMILE_FFN_TMA_STORE=0: st.global from registers.  Measured at C2:
+// GEMM1 (which writes H, 4x the bytes of Y) 687 us with st.global vs ~600 us with TMA
+// stores; the FFN 1.15 vs 1.04 ms.
+int pick_tma_store() {
     static int v = -1;
     if (v < 0) {
-        const char *e = getenv("SMILE_FFN_OUT_SLOTS");
-        v = (e && e[0] == '2') ? 2 : 1;
+        const char *e = getenv("SMILE_FFN_TMA_STORE");
+        v = (e && e[0] == '0') ? 0 : 1;
     }
     return v;
 }
 
-int pick_stages(int CG, int nbox, int slots) {
+int pick_stages(int CG, int nbox, int tma_store) {
     int st = 8;
-    while (st > 2 && smem_bytes(CG, st, nbox, slots) > kSmemLimit) --st;
+    while (st > 2 && smem_bytes(CG, st, nbox, tma_store) > kSmemLimit) --st;
     return st;
 }
 
@@ -501,12 +495,13 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
                         cudaStream_t st) {
     const int BN = pick_bn(N);
     const int CG = pick_cg(f.num_sms, BN);
-    CUtensorMap mA, mB, mD, mD2;
+    CUtensorMap mA, mA128, mB, mD, mD2;
     if (!make_map(&mA, A, rows_total, K, 32)) return cudaErrorNotSupported;        // 32-row strip boxes
+    if (!make_map(&mA128, A, rows_total, K, BM)) return cudaErrorNotSupported;     // 128-row tile box
     if (!make_map(&mB, B, (int64_t)NE * N, K, BN / CG)) return cudaErrorNotSupported;
-    if (!make_map(&mD, D, rows_total, N, 32, 64)) return cudaErrorNotSupported;     // 32 x 64, SWIZZLE_128B
+    if (!make_map(&mD, D, rows_total, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorNotSupported;
     mD2 = mD;
-    if (D2 && !make_map(&mD2, D2, rows_total, N, 32, 64)) return cudaErrorNotSupported;
+    if (D2 && !make_map(&mD2, D2, rows_total, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorNotSupported;
     TcArgs a;
     memset(&a, 0, sizeof(a));
     a.bias = bias; a.D = reinterpret_cast<__nv_bfloat16 *>(D); a.D2 = reinterpret_cast<__nv_bfloat16 *>(D2);
@@ -514,10 +509,10 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     a.nseg = f.V * f.S * f.e; a.e = f.e; a.S = f.S; a.Cseg = f.Cseg; a.N = N; a.K = K; a.BN = BN; a.gelu = gelu;
     a.mode = mode; a.aux = reinterpret_cast<const __nv_bfloat16 *>(aux);
     const int nbox = mode == EPI_BIAS_SAVE ? 2 : 1;
-    a.slots = pick_slots();
-    a.stages = pick_stages(CG, nbox, a.slots);
+    a.tma_store = pick_tma_store();
+    a.stages = pick_stages(CG, nbox, a.tma_store);
     a.err = nullptr;
-    const size_t smem = smem_bytes(CG, a.stages, nbox, a.slots);
+    const size_t smem = smem_bytes(CG, a.stages, nbox, a.tma_store);
     if (CG == 2) {
         static bool attr2 = false;
         if (!attr2) {
@@ -538,7 +533,7 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
         cfg.attrs = attrs;
         cfg.numAttrs = 1;
         note_launch();
-        return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<2>, mA, mB, mD, mD2, a);
+        return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<2>, mA, mA128, mB, mD, mD2, a);
     }
     static bool attr1 = false;
     if (!attr1) {
@@ -546,7 +541,7 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
         attr1 = true;
     }
     note_launch();
-    ffn_gemm_tcgen05<1><<<f.num_sms, NTHREADS, smem, st>>>(mA, mB, mD, mD2, a);
+    ffn_gemm_tcgen05<1><<<f.num_sms, NTHREADS, smem, st>>>(mA, mA128, mB, mD, mD2, a);
     return cudaGetLastError();
 }
 

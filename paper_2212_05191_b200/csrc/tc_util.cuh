@@ -213,18 +213,20 @@ static inline EncodeTiledFn encode_fn() {
 
 // 2D bf16 row-major [rows, K] map with a (box_cols x box_rows) box, SWIZZLE_128B for the
 // 64-column (128-byte) operand boxes, none for the 32 x 32 output boxes.
-static inline bool make_map(CUtensorMap *m, const void *ptr, int64_t rows, int64_t K, int box_rows, int box_cols = 64) {
+static inline bool make_map(CUtensorMap *m, const void *ptr, int64_t rows, int64_t K, int box_rows, int box_cols = 64,
+                            int swizzle = -1) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)K * 2};
     cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle sw = swizzle >= 0 ? (CUtensorMapSwizzle)swizzle
+                                               : (box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-
 
 // 3-D bf16 map [planes][rows][cols] (cols contiguous) with a (64 cols x box_rows x 1)
 // SWIZZLE_128B box: rows beyond `rows` of a plane are out of bounds (zero-filled), so a
