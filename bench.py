@@ -634,7 +634,7 @@ def run_ours(args):
         "cuda_graph": main["graph_ms"] is not None, "eager_ms_per_step": main["eager_ms"],
         "roofline": roof,
         "hbm_phases": hbm_phases(main, peaks),
-        "nvlink": nvlink_levels(main, world, modes[0], args.exchange),
+        "nvlink": None if main.get("train") else nvlink_levels(main, world, modes[0], args.exchange),
         "layer_roofline": None if main.get("train") else layer_roofline(main, cfgd, peaks, world, flops),
         "gpu_launches": main["launches"],
         "gpu_launches_note": "libsmile kernels launched in the timed region (smile_launch_count delta; NCCL not counted)",

@@ -143,27 +143,35 @@ struct TileInfo {
     int64_t b_row;
 };
 
-// Tile `tile` of the work list: 4 * CG strips (32 rows each) of one expert x BN columns.
+// Tile `tile` of the work list: 4 * CG * NPAIR strips (32 rows each) of one expert x BN
+// columns (with NPAIR = 2 the cluster's two pairs take consecutive 8-strip M-tiles and
+// share the N-tile).
 // For a CTA pair, `rank` selects this CTA's 4 strips (its 128 rows of the M = 256 MMA)
 // and its BN/2-row half of B.  Strip u0 + j of the expert goes to TMEM lanes 32j..32j+31;
 // a missing strip (the expert's last tile) has 0 rows and points at row 0 (loaded,
 // computed, never stored).
-template <int CG>
-__device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref, int tile, int ntn, int rank) {
+template <int CG, int NPAIR>
+__device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref, int tile, int ntn, int rank,
+                                              int pair) {
     TileInfo t;
     t.nt = tile % ntn;
     const int mtg = tile / ntn;
     const int NE = a.nseg / a.S;
     t.E = tile_segment(s_pref, NE, mtg);
-    t.u0 = ((mtg - s_pref[t.E]) * CG + rank) * 4;
+    t.u0 = (((mtg - s_pref[t.E]) * NPAIR + pair) * CG + rank) * 4;
     t.b_row = (int64_t)t.E * a.N + (int64_t)t.nt * a.BN + rank * (a.BN / CG);
     return t;
 }
 
+// NPAIR = 2 (CG = 2): a cluster of 4 = two pairs on consecutive M-tiles of one expert and
+// the same N-tile; each CTA TMA-loads a quarter of the B tile and multicasts it to its
+// counterpart in the other pair, so B's L2 -> SM traffic halves (the FFN GEMMs are
+// bound by that path, not by the MMAs).  A stage is refilled only after BOTH pairs'
+// MMAs released it (empty barriers count one commit per pair).
 // CG = 1: one CTA per tile (M = 128).  CG = 2: a CTA pair (cluster of 2) per tile
 // (M = 256, tcgen05.mma.cta_group::2 issued by the leader), each CTA loading half of A
 // and half of B, which halves the shared-memory operand traffic per SM.
-template <int CG>
+template <int CG, int NPAIR>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA128,
                  const __grid_constant__ CUtensorMap mapB,
@@ -185,13 +193,16 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     int *s_cnt = s_pref + MAXSEG + 1;                                 // [nseg] segment row counts
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+    constexpr int CS = CG * NPAIR;                              // cluster size
+    const int crank = CS > 1 ? (int)cluster_ctarank() : 0;
+    const int rank = crank % CG, pair = crank / CG;
     const bool leader = rank == 0;
-    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+    const uint32_t lead = (uint32_t)(pair * CG);                // cluster rank of this pair's leader
+    const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
-            mbar_init(smem_u32(&empty[s]), 1);
+            mbar_init(smem_u32(&empty[s]), NPAIR);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&tfull[s]), 1);
@@ -221,8 +232,8 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     }
     for (int g = threadIdx.x; g < a.nseg; g += blockDim.x) s_cnt[g] = a.counts[g];
     __syncthreads();
-    expert_tile_prefix<4 * CG>(s_cnt, a.nseg / a.S, a.S, a.e, s_pref, s_warp);   // ends with __syncthreads
-    if (CG == 2) cluster_sync_all();                         // peer barriers initialised before any remote arrive
+    expert_tile_prefix<4 * CG * NPAIR>(s_cnt, a.nseg / a.S, a.S, a.e, s_pref, s_warp);   // ends with __syncthreads
+    if (CS > 1) cluster_sync_all();                          // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const int ntn = a.N / a.BN;
@@ -236,7 +247,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = cid; tile < total; tile += ncl) {
-                const TileInfo t = tile_info<CG>(a, s_pref, tile, ntn, rank);
+                const TileInfo t = tile_info<CG, NPAIR>(a, s_pref, tile, ntn, rank, pair);
                 // A: one 128-row box when the tile's 4 strips are consecutive rows (fewer
                 // TMA requests: the L2 -> SM path is what bounds these GEMMs), else four
                 // 32-row strip boxes (4 KB each, stacked = the same SW128 tile); rows
@@ -265,14 +276,22 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     } else {
                         // the leader's full barrier counts the bytes of both CTAs' loads
                         if (leader) mbar_arrive_tx(fb, CG * (A_BYTES + b_bytes));
-                        const uint32_t fbl = mapa_shared(fb, 0);
+                        const uint32_t fbl = mapa_shared(fb, lead);
                         if (contig)
                             tma_load_2d_pair(smem_u32(sA + stage * A_BYTES), &mapA128, kb * BK, srow[0], fbl);
                         else
                             for (int j = 0; j < 4; ++j)
                                 tma_load_2d_pair(smem_u32(sA + stage * A_BYTES + j * (A_BYTES / 4)), &mapA,
                                                  kb * BK, srow[j], fbl);
-                        tma_load_2d_pair(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)t.b_row, fbl);
+                        if (NPAIR == 1) {
+                            tma_load_2d_pair(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)t.b_row, fbl);
+                        } else {
+                            // quarter `pair` of this CTA's B half, to the same rank in both pairs
+                            const int qrows = a.BN / (CG * NPAIR);
+                            tma_load_2d_pair_mc(smem_u32(sB + stage * b_stage_bytes + pair * qrows * 128), &mapB,
+                                                kb * BK, (int)t.b_row + pair * qrows, fbl,
+                                                (uint16_t)((1u << rank) | (1u << (CG + rank))));
+                        }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -305,11 +324,11 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                                           (kb | k) ? 1u : 0u);
                     }
                     if (CG == 1) mma_commit(smem_u32(&empty[stage]));
-                    else mma_commit_pair(smem_u32(&empty[stage]));
+                    else mma_commit_pair(smem_u32(&empty[stage]), NPAIR == 2 ? (uint16_t)0xF : (uint16_t)3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 if (CG == 1) mma_commit(smem_u32(&tfull[acc]));
-                else mma_commit_pair(smem_u32(&tfull[acc]));
+                else mma_commit_pair(smem_u32(&tfull[acc]), (uint16_t)(3u << lead));
             }
         }
     } else if (warp >= 4) {
@@ -326,7 +345,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         int it = 0;
         unsigned char *box = sOut + (warp - 4) * nbox * OUT_BOX_BYTES;
         for (int tile = cid; tile < total; tile += ncl, ++it) {
-            const TileInfo t = tile_info<CG>(a, s_pref, tile, ntn, rank);
+            const TileInfo t = tile_info<CG, NPAIR>(a, s_pref, tile, ntn, rank, pair);
             const int acc = it & 1;
             mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
             tc_fence_after();
@@ -429,13 +448,13 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             __syncwarp();
             if (lane == 0) {
                 if (CG == 1) mbar_arrive(smem_u32(&tempty[acc]));
-                else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));   // the leader's MMA waits on it
+                else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), lead));   // the leader's MMA waits on it
             }
         }
     }
     if (warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncthreads();
-    if (CG == 2) cluster_sync_all();          // no remote arrive / MMA into a CTA that has left
+    if (CS > 1) cluster_sync_all();           // no remote arrive / MMA into a CTA that has left
     if (warp == 2) {
         tc_fence_after();
         if (CG == 2)
@@ -489,16 +508,75 @@ int pick_cg(int num_sms, int BN) {
     return (env && num_sms >= 2 && (BN / 2) % 16 == 0) ? 2 : 1;
 }
 
+// Pairs per cluster for the CTA-pair GEMM: SMILE_FFN_PAIRS=2 (clusters of 4 sharing B by
+// multicast) or 1 (default: clusters of 2).
+int pick_npair() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SMILE_FFN_PAIRS");
+        v = (e && e[0] == '2') ? 2 : 1;
+    }
+    return v;
+}
+
+template <int CG, int NPAIR>
+cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUtensorMap &mB, const CUtensorMap &mD,
+                      const CUtensorMap &mD2, const TcArgs &a, size_t smem, int num_sms, cudaStream_t st) {
+    constexpr int CS = CG * NPAIR;
+    static int grid = 0;
+    if (!grid) {
+        cudaFuncSetAttribute(ffn_gemm_tcgen05<CG, NPAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
+        grid = num_sms / CS * CS;
+        if (CS > 2) {
+            // clusters of 4 need 4 free SMs in one GPC: size the grid to what can be resident
+            cudaLaunchConfig_t q;
+            memset(&q, 0, sizeof(q));
+            q.gridDim = dim3((unsigned)grid);
+            q.blockDim = dim3(NTHREADS);
+            q.dynamicSmemBytes = kSmemLimit;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            q.attrs = at;
+            q.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, ffn_gemm_tcgen05<CG, NPAIR>, &q) == cudaSuccess && ncl > 0 &&
+                ncl * CS < grid)
+                grid = ncl * CS;
+        }
+    }
+    note_launch();
+    if (CS == 1) {
+        ffn_gemm_tcgen05<CG, NPAIR><<<grid, NTHREADS, smem, st>>>(mA, mA128, mB, mD, mD2, a);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = CS;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<CG, NPAIR>, mA, mA128, mB, mD, mD2, a);
+}
+
 // One grouped GEMM launch: D[rows, N] = epi(A[rows, K] . B[expert][N, K]^T).
 cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE, const float *bias, void *D,
                         void *D2, const void *aux, const FfnArgs &f, int N, int K, int mode, int gelu,
                         cudaStream_t st) {
     const int BN = pick_bn(N);
     const int CG = pick_cg(f.num_sms, BN);
+    const int NPAIR = (CG == 2 && (BN / 4) % 8 == 0) ? pick_npair() : 1;
     CUtensorMap mA, mA128, mB, mD, mD2;
     if (!make_map(&mA, A, rows_total, K, 32)) return cudaErrorNotSupported;        // 32-row strip boxes
     if (!make_map(&mA128, A, rows_total, K, BM)) return cudaErrorNotSupported;     // 128-row tile box
-    if (!make_map(&mB, B, (int64_t)NE * N, K, BN / CG)) return cudaErrorNotSupported;
+    if (!make_map(&mB, B, (int64_t)NE * N, K, BN / (CG * NPAIR))) return cudaErrorNotSupported;
     if (!make_map(&mD, D, rows_total, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorNotSupported;
     mD2 = mD;
     if (D2 && !make_map(&mD2, D2, rows_total, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorNotSupported;
@@ -513,36 +591,9 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     a.stages = pick_stages(CG, nbox, a.tma_store);
     a.err = nullptr;
     const size_t smem = smem_bytes(CG, a.stages, nbox, a.tma_store);
-    if (CG == 2) {
-        static bool attr2 = false;
-        if (!attr2) {
-            cudaFuncSetAttribute(ffn_gemm_tcgen05<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
-            attr2 = true;
-        }
-        cudaLaunchConfig_t cfg;
-        memset(&cfg, 0, sizeof(cfg));
-        cfg.gridDim = dim3((unsigned)(f.num_sms & ~1));
-        cfg.blockDim = dim3(NTHREADS);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attrs[1];
-        attrs[0].id = cudaLaunchAttributeClusterDimension;
-        attrs[0].val.clusterDim.x = 2;
-        attrs[0].val.clusterDim.y = 1;
-        attrs[0].val.clusterDim.z = 1;
-        cfg.attrs = attrs;
-        cfg.numAttrs = 1;
-        note_launch();
-        return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<2>, mA, mA128, mB, mD, mD2, a);
-    }
-    static bool attr1 = false;
-    if (!attr1) {
-        cudaFuncSetAttribute(ffn_gemm_tcgen05<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
-        attr1 = true;
-    }
-    note_launch();
-    ffn_gemm_tcgen05<1><<<f.num_sms, NTHREADS, smem, st>>>(mA, mA128, mB, mD, mD2, a);
-    return cudaGetLastError();
+    if (CG == 2 && NPAIR == 2) return launch_tc<2, 2>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
+    if (CG == 2) return launch_tc<2, 1>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
+    return launch_tc<1, 1>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
 }
 
 }  // namespace

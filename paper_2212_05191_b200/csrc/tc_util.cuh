@@ -138,6 +138,18 @@ static __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUte
         : "memory");
 }
 
+// The 2-SM TMA load multicast to the CTAs in `mask` (same smem offset in each); every
+// destination's pair leader gets the complete_tx on the barrier at the offset of
+// `bar_cluster` (pass this CTA's pair leader's barrier).
+static __device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                                          uint32_t bar_cluster, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster), "h"(mask)
+        : "memory");
+}
+
 static __device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                               uint32_t accumulate) {
     asm volatile(
@@ -148,11 +160,12 @@ static __device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t a
         : "memory");
 }
 
-// commit the leader's MMAs to the mbarrier at offset `bar` in BOTH CTAs of the pair
-static __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+// commit the leader's MMAs to the mbarrier at offset `bar` in every CTA of `mask`
+// (default: both CTAs of the pair in a cluster of 2)
+static __device__ __forceinline__ void mma_commit_pair(uint32_t bar, uint16_t mask = 3) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-        "h"((uint16_t)3)
+        "h"(mask)
         : "memory");
 }
 
