@@ -381,6 +381,20 @@ smile_status smile_forward_host(smile_ctx ctx, const smile_layer_io *io, const v
                                 const float *host_logits, void *host_out, double *host_loss,
                                 void *stream);
 
+/* Streams nb batches through the layer from pinned host memory with copy / compute
+ * overlap: batch b's host->device copy (one copy engine) runs while batch b-1 is in the
+ * layer and batch b-2's result is copied back (the other copy engine).  Every batch's
+ * H2D and D2H are part of the call.  x_dev[2], out_dev[2]: caller-owned device
+ * ping-pong buffers [V, T, d] (dtype); io->x / io->out are ignored (the ping-pong
+ * buffers are used), io->loss holds V doubles (device) and is copied to
+ * host_loss + b*V after each batch.  host_x[b] / host_out[b]: pinned [V, T, d].
+ * Supplied logits are not streamed (io->logits must be NULL: fused router).  The
+ * library's own copy streams and events are created with the context; `stream` is the
+ * compute stream.  Blocks until the last D2H has completed. */
+smile_status smile_forward_host_stream(smile_ctx ctx, const smile_layer_io *io, void *const *x_dev,
+                                       void *const *out_dev, int32_t nb, const void *const *host_x,
+                                       void *const *host_out, double *host_loss, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -296,6 +296,13 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
     CUDA_TRY(cudaMalloc(&c->blk_psum, nb1 * (z.K1 + z.K2) * 8));
     CUDA_TRY(cudaMalloc(&c->blk_hist2, nb2 * z.K2 * 4));
     CUDA_TRY(cudaMalloc(&c->blk_off2, nb2 * z.K2 * 4));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        CUDA_TRY(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->ev_comp[i], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming));
+    }
     {
         const size_t cb = colsum_ws_bytes(V * shape->e, (int)z.S, z.Cseg, std::max(shape->d, shape->d_ff));
         if (cudaMalloc(&c->colsum_ws, cb) != cudaSuccess) { smile_destroy(c); return SMILE_ECUDA; }
@@ -341,6 +348,13 @@ extern "C" smile_status smile_destroy(smile_ctx c) {
     cudaFree(c->d_err);
     cudaFree(c->wsplit);
     cudaFree(c->colsum_ws);
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+    for (int i = 0; i < 2; ++i) {
+        if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
+        if (c->ev_comp[i]) cudaEventDestroy(c->ev_comp[i]);
+        if (c->ev_d2h[i]) cudaEventDestroy(c->ev_d2h[i]);
+    }
     cudaFree(c->blk_hist1); cudaFree(c->blk_off1); cudaFree(c->blk_hist2a); cudaFree(c->blk_psum);
     cudaFree(c->blk_hist2); cudaFree(c->blk_off2);
     for (int p = 0; p < kMaxProcs; ++p)
@@ -833,6 +847,43 @@ extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, voi
     }
     STEP(smile_combine(c, 1, w.back1, &w.route, nullptr, nullptr, io->out, stream));
     STEP(smile_aux_loss(c, &w.stats, io->alpha, io->beta, io->loss, stream));
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_forward_host_stream(smile_ctx c, const smile_layer_io *io, void *const *x_dev,
+                                                  void *const *out_dev, int32_t nb, const void *const *host_x,
+                                                  void *const *host_out, double *host_loss, void *stream) {
+    if (!c || !io || !x_dev || !out_dev || !host_x || !host_out || !host_loss || nb < 0) return SMILE_EINVAL;
+    if (io->logits || !x_dev[0] || !x_dev[1] || !out_dev[0] || !out_dev[1] || !io->loss) return SMILE_EINVAL;
+    cudaSetDevice(c->shape.device);
+    cudaStream_t st = S(stream);
+    const size_t xb = (size_t)c->sz.V * c->shape.T * c->shape.d * (c->shape.dtype == SMILE_BF16 ? 2 : 4);
+    const size_t lb = (size_t)c->sz.V * 8;
+    // the copy streams start after the work already queued on the compute stream
+    CUDA_TRY(cudaEventRecord(c->ev_d2h[0], st));
+    CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, c->ev_d2h[0], 0));
+    CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->ev_d2h[0], 0));
+    for (int b = 0; b < nb; ++b) {
+        const int k = b & 1;
+        // x_dev[k] is free once batch b-2's layer has read it
+        if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, c->ev_comp[k], 0));
+        CUDA_TRY(cudaMemcpyAsync(x_dev[k], host_x[b], xb, cudaMemcpyHostToDevice, c->s_h2d));
+        CUDA_TRY(cudaEventRecord(c->ev_h2d[k], c->s_h2d));
+        // the layer: after its input landed and after out_dev[k]'s previous D2H
+        CUDA_TRY(cudaStreamWaitEvent(st, c->ev_h2d[k], 0));
+        if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_d2h[k], 0));
+        smile_layer_io l = *io;
+        l.x = x_dev[k];
+        l.out = out_dev[k];
+        STEP(smile_forward(c, &l, stream));
+        CUDA_TRY(cudaMemcpyAsync(host_loss + (size_t)b * c->sz.V, io->loss, lb, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaEventRecord(c->ev_comp[k], st));
+        CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->ev_comp[k], 0));
+        CUDA_TRY(cudaMemcpyAsync(host_out[b], out_dev[k], xb, cudaMemcpyDeviceToHost, c->s_d2h));
+        CUDA_TRY(cudaEventRecord(c->ev_d2h[k], c->s_d2h));
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->s_d2h));
+    CUDA_TRY(cudaStreamSynchronize(st));
     return SMILE_OK;
 }
 

@@ -81,6 +81,9 @@ struct smile_ctx_s {
     // tensor-core gate (bf16 fused router): the three-piece bf16 split of the router
     __nv_bfloat16 *wsplit = nullptr;         // [gate_tc_np(KW), d], rewritten every fused gate call
     float *colsum_ws = nullptr;              // bias-gradient partials of smile_expert_ffn_bwd
+    // smile_forward_host_stream: copy streams and ping-pong events (created with the ctx)
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
 };
 
 namespace smile {

@@ -89,7 +89,7 @@ def lib():
                      "smile_combine", "smile_aux_loss", "smile_forward_ws", "smile_forward", "smile_forward_host",
                      "smile_expert_ffn_train", "smile_combine_bwd", "smile_dispatch_grad", "smile_expert_ffn_bwd",
                      "smile_combine_grad", "smile_router_bwd", "smile_backward", "smile_ipc_handle",
-                     "smile_register_workspace", "smile_struct_sizes"):
+                     "smile_register_workspace", "smile_struct_sizes", "smile_forward_host_stream"):
             getattr(L, name).restype = C.c_int
         # the ctypes mirrors must match the C structs byte for byte
         sizes = (C.c_int64 * 8)()
@@ -281,6 +281,25 @@ class SmileLayer:
                      _ptr(out), _ptr(loss), alpha, beta, _ptr(self.ws), 0)
         _check(lib().smile_forward_host(self._ctx, C.byref(io), _ptr(host_x), _ptr(host_logits), _ptr(host_out),
                                         _ptr(host_loss), _stream(stream)), "smile_forward_host")
+
+    def forward_host_stream(self, x_dev2, out_dev2, host_xs, host_outs, host_loss, W1t, b1, W2t, b2, loss,
+                            w_router=None, alpha=0.005, beta=0.005, stream=None):
+        """smile_forward_host_stream: len(host_xs) batches from pinned host memory with the
+        H2D / layer / D2H of consecutive batches overlapped.  x_dev2, out_dev2: two device
+        buffers each; host_loss: pinned float64 [nb, V]."""
+        if self.ws is None:
+            self.alloc_workspace()
+        io = LayerIO(0, 0, _ptr(w_router), _ptr(W1t), _ptr(b1), _ptr(W2t), _ptr(b2), 0, _ptr(loss), alpha, beta,
+                     _ptr(self.ws), 0)
+        nb = len(host_xs)
+        P2 = C.c_void_p * 2
+        PN = C.c_void_p * max(nb, 1)
+        xd = P2(*[_ptr(t) for t in x_dev2])
+        od = P2(*[_ptr(t) for t in out_dev2])
+        hx = PN(*[_ptr(t) for t in host_xs])
+        ho = PN(*[_ptr(t) for t in host_outs])
+        _check(lib().smile_forward_host_stream(self._ctx, C.byref(io), xd, od, nb, hx, ho, _ptr(host_loss),
+                                               _stream(stream)), "smile_forward_host_stream")
 
     def get_error(self, stream=None) -> int:
         return lib().smile_get_error(self._ctx, _stream(stream))

@@ -179,6 +179,35 @@ def test_determinism_and_forward_host():
     assert torch.equal(ho, o1.cpu()) and torch.equal(hloss, l1.cpu())
 
 
+def test_forward_host_stream_matches_forward():
+    """smile_forward_host_stream (copy / compute overlap over ping-pong buffers): three
+    different token batches through one layer (fused router), each bit-identical to a
+    plain smile_forward of the same batch (which the other tests pin to the oracle)."""
+    from paper_2212_05191_b200 import SmileLayer
+    cases = [Case(2, 4, 1, 700, 128, 256, 1.25, dtype="bf16", dist="balanced", seed=s, fused=True) for s in (31, 32, 33)]
+    c0 = cases[0]
+    layer = SmileLayer(2, 4, 1, 128, 256, 700, 1.25, "bf16", "bilevel")
+    g0 = c0.gpu_tensors()
+    xs = [torch.from_numpy(c.x).to(torch.bfloat16).contiguous().pin_memory() for c in cases]
+    outs = [torch.empty_like(xs[0]).pin_memory() for _ in cases]
+    hl = torch.empty(3, 8, dtype=torch.float64).pin_memory()
+    xd2 = [torch.empty_like(g0["x"]) for _ in range(2)]
+    od2 = [torch.empty_like(g0["x"]) for _ in range(2)]
+    loss = torch.empty(8, dtype=torch.float64, device="cuda")
+    layer.forward_host_stream(xd2, od2, xs, outs, hl, g0["W1t"], g0["b1"], g0["W2t"], g0["b2"], loss,
+                              w_router=g0["w_router"], alpha=c0.alpha, beta=c0.beta)
+    assert layer.get_error() == 0
+    for b, c in enumerate(cases):
+        xdev = xs[b].cuda()
+        out = torch.empty_like(xdev)
+        l1 = torch.empty(8, dtype=torch.float64, device="cuda")
+        layer.forward(xdev, g0["W1t"], g0["b1"], g0["W2t"], g0["b2"], out, l1, w_router=g0["w_router"],
+                      alpha=c0.alpha, beta=c0.beta)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[b], out.cpu()), f"batch {b}"
+        assert torch.equal(hl[b], l1.cpu()), f"batch {b} loss"
+
+
 def test_nonfinite_sets_sticky_flag():
     case = Case(2, 2, 1, 64, 64, 64, 1.0, seed=7)
     case.logits[1, 5, 2] = np.inf
