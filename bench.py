@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay each step as a CUDA graph")
+    ap.add_argument("--chunks", type=int, default=1,
+                    help="> 1: the layer as c pipelined micro-batches on two streams (SURVEY 8(f) row 2)")
     ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling period (0 = off)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "copy"],
                     help="peer: fused permute -> peer-store exchange (CUDA IPC over NVLink); copy: device copies / NCCL")
@@ -293,6 +295,169 @@ def step(L, inp, ev=None):
         rec(6)
         L.aux_loss(w.stats, inp["loss"], 0.01, 0.0)
         rec(7)
+
+
+def stage_front(L, inp):
+    """a1-a8 of one (chunk) layer: gate, level-1 permute + exchange, level-2 gate, level-2
+    permute + exchange (flat: gate, permute + exchange)."""
+    w, A = L._view, Addr
+    L.gate_inter(inp["x"], w.route, w.stats, A(w.counts1), w_router=inp["w_router"])
+    L.dispatch(1, inp["x"], A(w.send1), route=w.route, send_meta=A(w.meta1) if not L.flat else None)
+    if not L.flat:
+        L.all2all_inter(0, A(w.send1), A(w.recv1), A(w.meta1), A(w.rmeta1), A(w.counts1))
+        L.gate_intra(A(w.rmeta1), A(w.slot2), A(w.counts2))
+        L.dispatch(2, A(w.recv1), A(w.send2), recv_meta=A(w.rmeta1), slot2=A(w.slot2))
+        L.all2all_intra(0, A(w.send2), A(w.recv2), A(w.counts2), A(w.rcounts), A(w.counts2))
+    else:
+        L.all2all(0, 0, A(w.send1), A(w.recv1), A(w.counts1), A(w.rcounts), A(w.counts1))
+
+
+def stage_ffn(L, inp):
+    w, A = L._view, Addr
+    X = A(w.recv2) if not L.flat else A(w.recv1)
+    L.expert_ffn(X, A(w.rcounts), inp["W1t"], inp["b1"], inp["W2t"], inp["b2"], A(w.H), A(w.Y))
+
+
+def stage_back(L, inp):
+    """a10-a14: reverse exchanges, un-permute, combine, aux loss."""
+    w, A = L._view, Addr
+    if not L.flat:
+        L.all2all_intra(1, A(w.Y), A(w.ret2), fwd_counts=A(w.counts2))
+        L.combine(2, A(w.ret2), A(w.ret1), recv_meta=A(w.rmeta1), slot2=A(w.slot2))
+        L.all2all_inter(1, A(w.ret1), A(w.back1), fwd_counts=A(w.counts1))
+        L.combine(1, A(w.back1), inp["out"], route=w.route)
+        L.aux_loss(w.stats, inp["loss"], 0.005, 0.005)
+    else:
+        L.all2all(0, 1, A(w.Y), A(w.back1), fwd_counts=A(w.counts1))
+        L.combine(1, A(w.back1), inp["out"], route=w.route)
+        L.aux_loss(w.stats, inp["loss"], 0.01, 0.0)
+
+
+def step_pipelined(Ls, inps, s2, evf, eve):
+    """SURVEY §8(f) row 2 / P:L391-405: the batch split into c chunks (independent
+    micro-batches with their own capacities), software-pipelined on two streams: the
+    expert FFN of chunk k (stream 2) overlaps the gate + permutes + exchanges of chunk k+1
+    and the return path of chunk k-1 (stream 1)."""
+    import torch
+    s1 = torch.cuda.current_stream()
+    c = len(Ls)
+    stage_front(Ls[0], inps[0])
+    evf[0].record(s1)
+    for k in range(c):
+        s2.wait_event(evf[k])
+        with torch.cuda.stream(s2):
+            stage_ffn(Ls[k], inps[k])
+        eve[k].record(s2)
+        if k + 1 < c:
+            stage_front(Ls[k + 1], inps[k + 1])
+            evf[k + 1].record(s1)
+        s1.wait_event(eve[k])
+        stage_back(Ls[k], inps[k])
+
+
+def run_pipelined(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2212_05191_b200 import smile as smb
+    cfgd = dict(CONFIGS[args.config])
+    G, c = cfgd["n"] * cfgd["m"], args.chunks
+    V, T, d, d_ff, e = G // world, cfgd["T"], cfgd["d"], cfgd["d_ff"], cfgd["e"]
+    if T % c:
+        raise SystemExit(f"T={T} not divisible into {c} chunks")
+    Tc = T // c
+    tdt = torch.bfloat16 if cfgd["dtype"] == "bf16" else torch.float32
+    modes = ["bilevel", "flat"] if args.mode == "both" else [args.mode]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out_modes = {}
+    for mode in modes:
+        Ls, inps = [], []
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(7)
+        KW = None
+        for k in range(c):
+            nid = None
+            if world > 1:
+                buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+                if rank == 0:
+                    buf.copy_(torch.frombuffer(bytearray(smb.unique_id()), dtype=torch.uint8))
+                dist.broadcast(buf, 0)
+                nid = bytes(buf.cpu().numpy().tobytes())
+            ck = dict(cfgd, T=Tc)
+            L = make_layer(ck, mode, world, rank, local, args.ffn, nid)
+
+            def allgather(b):
+                t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(dev)
+                outs = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(outs, t)
+                return b"".join(bytes(o.cpu().numpy().tobytes()) for o in outs)
+            L.enable_peer_exchange(allgather if world > 1 else None)
+            if dist:
+                dist.barrier()
+            Ls.append(L)
+            KW = L.KW
+        gen.manual_seed(7)
+        w_router = (torch.rand(KW, d, generator=gen, device=dev) * 2 - 1) / math.sqrt(d)
+        gen.manual_seed(2000 + rank)
+        W1t = ((torch.rand(V * e, d_ff, d, generator=gen, device=dev) * 2 - 1) / math.sqrt(d)).to(tdt)
+        W2t = ((torch.rand(V * e, d, d_ff, generator=gen, device=dev) * 2 - 1) / math.sqrt(d_ff)).to(tdt)
+        b1 = torch.zeros(V * e, d_ff, device=dev)
+        b2 = torch.zeros(V * e, d, device=dev)
+        gen.manual_seed(1000 + rank)
+        x = torch.randn(V, T, d, generator=gen, device=dev, dtype=torch.float32).to(tdt)
+        for k in range(c):
+            xk = x[:, k * Tc:(k + 1) * Tc].contiguous()
+            inps.append(dict(x=xk, w_router=w_router, W1t=W1t, W2t=W2t, b1=b1, b2=b2, out=torch.empty_like(xk),
+                             loss=torch.empty(V, dtype=torch.float64, device=dev)))
+        s2 = torch.cuda.Stream()
+        evf = [torch.cuda.Event() for _ in range(c)]
+        eve = [torch.cuda.Event() for _ in range(c)]
+        for _ in range(args.warmup):
+            step_pipelined(Ls, inps, s2, evf, eve)
+        torch.cuda.synchronize()
+        if any(L.get_error() for L in Ls):
+            raise SystemExit("device error")
+        t0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        t1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.zero_()
+            t0[k].record()
+            step_pipelined(Ls, inps, s2, evf, eve)
+            t1[k].record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([statistics.mean(t0[k].elapsed_time(t1[k]) for k in range(args.steps))], dtype=torch.float64,
+                          device=dev)
+        if dist:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        out_modes[mode] = ms.item()
+        if dist:
+            dist.barrier()
+        for L in Ls:
+            L.close()
+    if rank == 0:
+        m0 = modes[0]
+        line = {"metric": METRIC, "value": G * T / (out_modes[m0] / 1e3), "unit": "tokens/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": out_modes[m0], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if cfgd["dtype"] == "bf16" else "f32",
+                "data": "synthetic", "config": {"workload": f"{args.config}: {m0} layer fwd, {c} pipelined chunks of "
+                                                            f"T={Tc}/rank on 2 streams (SURVEY 8(f) row 2)",
+                                                 "chunks": c, "ffn_max_ctas": os.environ.get("SMILE_FFN_MAX_CTAS"),
+                                                 "exchange": "peer"},
+                "modes_ms": out_modes}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
 
 
 PHASES_TRAIN = ["fwd", "bwd"]
@@ -664,6 +829,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.chunks > 1:
+        return run_pipelined(args)
     return run_ours(args)
 
 

@@ -527,6 +527,12 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
     if (!grid) {
         cudaFuncSetAttribute(ffn_gemm_tcgen05<CG, NPAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
         grid = num_sms / CS * CS;
+        // SMILE_FFN_MAX_CTAS caps the persistent grid (leaves SMs to kernels of other
+        // streams, e.g. the permutes of the next chunk in the pipelined layer)
+        if (const char *e = getenv("SMILE_FFN_MAX_CTAS")) {
+            const int cap = atoi(e) / CS * CS;
+            if (cap >= CS && cap < grid) grid = cap;
+        }
         if (CS > 2) {
             // clusters of 4 need 4 free SMs in one GPC: size the grid to what can be resident
             cudaLaunchConfig_t q;

@@ -422,9 +422,11 @@ __global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) {
     const bool combine1 = m.kind == MOVE_COMBINE1;
     const bool bf16 = m.c1.bf16 != 0;
     constexpr int RW = kMoveRowsPerWarp, CU = kMoveColUnroll;
+    // The next batch's row plan (dependent metadata loads: slot offsets, routes) is
+    // resolved while the current batch's row loads are in flight.
+    RowPlan mine{nullptr, nullptr, 1.f};
+    if (lane < RW && gw * RW + lane < m.rows) mine = plan_row(m, gw * RW + lane);
     for (int64_t g0 = gw * RW; g0 < m.rows; g0 += warps * RW) {
-        RowPlan mine{nullptr, nullptr, 1.f};
-        if (lane < RW && g0 + lane < m.rows) mine = plan_row(m, g0 + lane);
         const char *src[RW];
         char *dst[RW];
         float sc[RW];
@@ -434,6 +436,8 @@ __global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) {
             dst[r] = reinterpret_cast<char *>(__shfl_sync(kFull, reinterpret_cast<unsigned long long>(mine.dst), r));
             sc[r] = __shfl_sync(kFull, mine.scale, r);
         }
+        const int64_t gn = g0 + warps * RW;
+        bool planned = false;
         for (int c0 = lane; c0 < nvec; c0 += 32 * CU) {
             int4 val[RW][CU];
 #pragma unroll
@@ -444,6 +448,12 @@ __global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) {
                     val[r][u] = (dst[r] && src[r] && c < nvec) ? __ldg(reinterpret_cast<const int4 *>(src[r]) + c)
                                                                : make_int4(0, 0, 0, 0);
                 }
+            if (!planned) {
+                RowPlan nxt{nullptr, nullptr, 1.f};
+                if (lane < RW && gn + lane < m.rows) nxt = plan_row(m, gn + lane);
+                mine = nxt;
+                planned = true;
+            }
 #pragma unroll
             for (int r = 0; r < RW; ++r) {
                 if (!dst[r]) continue;
@@ -469,6 +479,11 @@ __global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) {
                     reinterpret_cast<int4 *>(dst[r])[c] = w;
                 }
             }
+        }
+        if (!planned) {                        // rows narrower than this lane's first vector
+            RowPlan nxt{nullptr, nullptr, 1.f};
+            if (lane < RW && gn + lane < m.rows) nxt = plan_row(m, gn + lane);
+            mine = nxt;
         }
     }
 }

@@ -73,6 +73,17 @@ def run_and_check(case, rows=None):
 C1 = dict(n=2, m=4, e=1, T=1024, d=64, d_ff=256, cf=1.0, dtype="fp32")
 
 
+@pytest.mark.parametrize("mode,cf", [("bilevel", 8.0), ("flat", 8.0)])
+def test_dropless(mode, cf):
+    """SURVEY 8(f) row 4, dropless routing: with cf >= n * K2 (bi-level: C1 >= T and
+    C2 >= n * T, everything a level can receive) resp. cf >= K (flat), no token is
+    dropped even under skewed routing, and the layer equals the oracle (which applies
+    the same capacity rule, R5-R7)."""
+    case = Case(2, 2, 2, 300, 64, 128, cf, dtype="bf16", mode=mode, dist="skewed", seed=17)
+    _, _, _, r = run_and_check(case)
+    assert r.keep.all()
+
+
 @pytest.mark.parametrize("dist", ["balanced", "skewed", "ties"])
 @pytest.mark.parametrize("mode", ["bilevel", "flat"])
 def test_c1_full(dist, mode):
