@@ -551,8 +551,6 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     cfgd = CONFIGS[args.config]
-    if cfgd.get("train") and args.exchange == "peer":
-        args.exchange = "copy"                 # smile_backward runs on the copy / NCCL exchange
     G = cfgd["n"] * cfgd["m"]
     if G % world:
         raise SystemExit(f"{world} processes do not divide {G} ranks")

@@ -288,7 +288,9 @@ smile_status smile_combine_bwd(smile_ctx ctx, const void *gout, const void *back
                                double lam, void *dsend, float *dlogits, void *stream);
 
 /* a16 (level 2): gradient rows at the intermediate follow the forward route:
- * dsend2[v, j, slot2] = drecv1[v, s, c] for every kept received slot (BILEVEL). */
+ * dsend2[v, j, slot2] = drecv1[v, s, c] for every kept received slot (BILEVEL).  With
+ * the peer-store exchange the row is stored straight into the expert's Y buffer (the
+ * row its forward input used), and dsend2 is not written. */
 smile_status smile_dispatch_grad(smile_ctx ctx, const void *drecv1, const int32_t *recv_meta,
                                  const int32_t *slot2, void *dsend2, void *stream);
 
@@ -297,8 +299,10 @@ smile_status smile_dispatch_grad(smile_ctx ctx, const void *drecv1, const int32_
  * W2 [V*e, d_ff, d] in their math layouts (the transposes of the forward's W1t / W2t).
  * Writes dZ_ws = (dY W2^T) . GELU'(A1) [V, S, e, Cseg, d_ff] (may alias A1),
  * dX = dZ W1^T [V, S, e, Cseg, d] and fp32 dW1 [V*e, d, d_ff], db1 [V*e, d_ff],
- * dW2 [V*e, d_ff, d], db2 [V*e, d] summed over the valid rows.  bf16: dZ and dX on
- * tcgen05; the weight gradients on SIMT FFMA this round. */
+ * dW2 [V*e, d_ff, d], db2 [V*e, d] summed over the valid rows.  dX may alias dY (every
+ * read of dY precedes the dX GEMM).  bf16: dZ, dX on tcgen05, and dW1, dW2 too when d
+ * and d_ff are multiples of 128 (MN-major operands; else SIMT); biases by fixed-order
+ * two-pass column sums (deterministic). */
 smile_status smile_expert_ffn_bwd(smile_ctx ctx, const void *X, const int32_t *counts, const void *A1,
                                   const void *H, const void *dY, const void *W1, const void *W2, void *dZ_ws,
                                   void *dX, float *dW1, float *db1, float *dW2, float *db2, void *stream);
@@ -374,7 +378,10 @@ smile_status smile_forward(smile_ctx ctx, const smile_layer_io *io, void *stream
  * should be pinned for asynchronous copies. */
 /* The whole backward after a forward with io->train set, in reverse order of the forward:
  * combine_bwd, exchange(1, gradient rows), dispatch_grad, exchange(2), expert_ffn_bwd,
- * exchange(2, reverse), combine(2), exchange(1, reverse), combine_grad, router_bwd. */
+ * exchange(2, reverse), combine(2), exchange(1, reverse), combine_grad, router_bwd.
+ * Works over both exchanges; with the peer-store exchange (smile_register_workspace)
+ * the gradient rows are stored at / loaded from their owners and every exchange is a
+ * barrier, as in the forward. */
 smile_status smile_backward(smile_ctx ctx, const smile_layer_io *io, const smile_grad_io *g, void *stream);
 
 smile_status smile_forward_host(smile_ctx ctx, const smile_layer_io *io, const void *host_x,

@@ -743,7 +743,7 @@ extern "C" smile_status smile_combine_bwd(smile_ctx c, const void *gout, const v
     a.gout = gout; a.back1 = back1; a.logits = logits; a.route = *route; a.stats = *stats; a.dsend = dsend;
     a.dlogits = dlogits; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d; a.K1 = c->sz.K1; a.K2 = c->sz.K2;
     a.KW = c->sz.KW; a.C1 = c->sz.C1; a.alpha = alpha; a.beta = beta; a.lam = lam;
-    a.flat = c->shape.mode == SMILE_FLAT; a.bf16 = c->shape.dtype == SMILE_BF16;
+    a.flat = c->shape.mode == SMILE_FLAT; a.bf16 = c->shape.dtype == SMILE_BF16; a.peer = peer_of(c);
     launch_combine_bwd(a, S(stream));
     return post_launch();
 }
@@ -758,7 +758,7 @@ extern "C" smile_status smile_dispatch_grad(smile_ctx c, const void *drecv1, con
     a.recv1 = drecv1; a.recv_meta = recv_meta; a.slot2 = const_cast<int32_t *>(slot2); a.blk_off2 = nullptr;
     a.send2 = dsend2; a.V = c->sz.V; a.items = (int64_t)c->shape.n * c->sz.C1;
     a.rowbytes = (int64_t)c->shape.d * (c->shape.dtype == SMILE_BF16 ? 2 : 4); a.K2 = c->sz.K2; a.C2 = c->sz.C2;
-    a.nblk = c->nblk2;
+    a.nblk = c->nblk2; a.peer = peer_of(c);
     launch_grad_dispatch2(a, S(stream));
     return post_launch();
 }
@@ -791,7 +791,7 @@ extern "C" smile_status smile_combine_grad(smile_ctx c, const void *ret_rows, co
     cudaSetDevice(c->shape.device);
     Combine1Args a{};
     a.back1 = ret_rows; a.route = *route; a.out = dx; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
-    a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = c->shape.dtype == SMILE_BF16; a.nogate = 1;
+    a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = c->shape.dtype == SMILE_BF16; a.nogate = 1; a.peer = peer_of(c);
     launch_combine1(a, S(stream));
     return post_launch();
 }
@@ -824,7 +824,7 @@ extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, voi
     STEP(smile_forward_ws(c, io->ws, &w));
     if (c->shape.T == 0) return SMILE_OK;
     const bool train = io->train != 0;
-    if (c->xchg == SMILE_XCHG_PEER && (train || io->ws != c->reg_ws)) return SMILE_ENOTSUP;
+    if (c->xchg == SMILE_XCHG_PEER && io->ws != c->reg_ws) return SMILE_ENOTSUP;
     STEP(smile_gate_inter(c, io->x, io->w_router, io->logits, (train && !io->logits) ? w.logits : nullptr, &w.route,
                           &w.stats, w.counts1, stream));
     STEP(smile_dispatch(c, 1, io->x, &w.route, nullptr, nullptr, w.send1, w.meta1, stream));
@@ -892,7 +892,11 @@ extern "C" smile_status smile_backward(smile_ctx c, const smile_layer_io *io, co
         !g->db2)
         return SMILE_EINVAL;
     if (io->w_router && !io->logits && !g->dW_router) return SMILE_EINVAL;
-    if (c->xchg == SMILE_XCHG_PEER) return SMILE_ENOTSUP;        // training uses the copy / NCCL exchange
+    const bool peer = c->xchg == SMILE_XCHG_PEER;
+    if (peer && io->ws != c->reg_ws) return SMILE_ENOTSUP;
+    // PEER: every exchange below is a barrier; the gradient rows are stored at / loaded
+    // from their owners by combine_bwd, dispatch_grad, combine and combine_grad, and the
+    // FFN backward writes dX over dY in the Y buffer (where the return path loads it)
     smile_ws_view w;
     STEP(smile_forward_ws(c, io->ws, &w));
     if (c->shape.T == 0) return SMILE_OK;
@@ -905,16 +909,16 @@ extern "C" smile_status smile_backward(smile_ctx c, const smile_layer_io *io, co
         STEP(smile_dispatch_grad(c, w.recv1, w.rmeta1, w.slot2, w.send2, stream));
         // dY lands in the Y buffer (X = recv2 is still needed for dW1)
         STEP(smile_all2all_intra(c, 0, w.send2, w.Y, nullptr, nullptr, w.counts2, stream));
-        STEP(smile_expert_ffn_bwd(c, w.recv2, w.rcounts, w.A1, w.H, w.Y, g->W1, g->W2, w.A1, w.send2, g->dW1, g->db1,
-                                  g->dW2, g->db2, stream));
+        STEP(smile_expert_ffn_bwd(c, w.recv2, w.rcounts, w.A1, w.H, w.Y, g->W1, g->W2, w.A1, peer ? w.Y : w.send2,
+                                  g->dW1, g->db1, g->dW2, g->db2, stream));
         // a18: dX back along the return route
         STEP(smile_all2all_intra(c, 1, w.send2, w.ret2, nullptr, nullptr, w.counts2, stream));
         STEP(smile_combine(c, 2, w.ret2, nullptr, w.rmeta1, w.slot2, w.ret1, stream));
         STEP(smile_all2all_inter(c, 1, w.ret1, w.back1, nullptr, nullptr, w.counts1, stream));
     } else {
         STEP(smile_all2all(c, 0, 0, w.send1, w.Y, nullptr, nullptr, w.counts1, stream));
-        STEP(smile_expert_ffn_bwd(c, w.recv1, w.rcounts, w.A1, w.H, w.Y, g->W1, g->W2, w.A1, w.send1, g->dW1, g->db1,
-                                  g->dW2, g->db2, stream));
+        STEP(smile_expert_ffn_bwd(c, w.recv1, w.rcounts, w.A1, w.H, w.Y, g->W1, g->W2, w.A1, peer ? w.Y : w.send1,
+                                  g->dW1, g->db1, g->dW2, g->db2, stream));
         STEP(smile_all2all(c, 0, 1, w.send1, w.back1, nullptr, nullptr, w.counts1, stream));
     }
     STEP(smile_combine_grad(c, w.back1, &w.route, g->dx, stream));

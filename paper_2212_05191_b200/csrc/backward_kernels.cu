@@ -58,12 +58,80 @@ __global__ void combine_bwd_kernel(CombineBwdArgs a) {
         float dgate = 0.f;
         if (s1 < a.C1) {
             const float gt = a.route.gate[g];
-            const int64_t row = ((int64_t)v * a.K1 + i) * a.C1 + s1;
+            const void *bsrc = a.back1;
+            void *gdst = a.dsend;
+            int64_t brow = ((int64_t)v * a.K1 + i) * a.C1 + s1, grow = brow;
+            if (a.peer.bases) {
+                // PEER: the forward output row lives at its owner (bi-level: the intermediate's
+                // ret1; flat: the expert's Y) and the gradient row goes where the forward row
+                // went (bi-level: the intermediate's recv1; flat: the expert's Y, read first)
+                const PeerMap &P = a.peer;
+                const int rk = P.rank0 + v;
+                const int64_t esz = a.bf16 ? 2 : 4;
+                if (P.n > 0) {
+                    const int s_ = rk / P.m, l = rk % P.m, u = i * P.m + l;
+                    const int64_t row = ((int64_t)(u % P.V) * P.n + s_) * a.C1 + s1;
+                    bsrc = P.bases[u / P.V] + P.off_ret1;
+                    gdst = P.bases[u / P.V] + P.off_recv1;
+                    brow = grow = row;
+                } else {
+                    const int q = i / P.e;
+                    const int64_t row = (((int64_t)(q % P.V) * P.G + rk) * P.e + i % P.e) * a.C1 + s1;
+                    bsrc = P.bases[q / P.V] + P.off_Y;
+                    gdst = P.bases[q / P.V] + P.off_Y;
+                    brow = grow = row;
+                }
+                (void)esz;
+            }
+            // 16-byte vectors: lane handles elements [8v, 8v + 8) (bf16) / [4v, 4v + 4) (fp32)
+            const int epv = a.bf16 ? 8 : 4, nv = a.d / epv;
+            const int64_t esz = a.bf16 ? 2 : 4;
+            const uint4 *gv = reinterpret_cast<const uint4 *>(static_cast<const char *>(a.gout) + g * a.d * esz);
+            const uint4 *bv = reinterpret_cast<const uint4 *>(static_cast<const char *>(bsrc) + brow * a.d * esz);
+            uint4 *dv = reinterpret_cast<uint4 *>(static_cast<char *>(gdst) + grow * a.d * esz);
             float acc = 0.f;
-            for (int c = lane; c < a.d; c += 32) {
-                const float go = ld_el(a.gout, g * a.d + c, a.bf16);
-                acc = fmaf(go, ld_el(a.back1, row * a.d + c, a.bf16), acc);
-                st_el(a.dsend, row * a.d + c, gt * go, a.bf16);
+            uint4 gk[4];
+            int nk = 0;
+            for (int vi = lane; vi < nv; vi += 32) {
+                const uint4 gg = gv[vi], bb = bv[vi];
+                if (nk < 4) gk[nk] = gg;
+                ++nk;
+                if (a.bf16) {
+                    const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gg);
+                    const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&bb);
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) {
+                        const float2 fg = __bfloat1622float2(g2[z]), fb = __bfloat1622float2(b2[z]);
+                        acc = fmaf(fg.x, fb.x, acc);
+                        acc = fmaf(fg.y, fb.y, acc);
+                    }
+                } else {
+                    const float *fg = reinterpret_cast<const float *>(&gg);
+                    const float *fb = reinterpret_cast<const float *>(&bb);
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) acc = fmaf(fg[z], fb[z], acc);
+                }
+            }
+            __syncwarp();                      // (flat PEER: the row is read before it is overwritten)
+            nk = 0;
+            for (int vi = lane; vi < nv; vi += 32, ++nk) {
+                const uint4 gg = nk < 4 ? gk[nk] : gv[vi];
+                uint4 o;
+                if (a.bf16) {
+                    const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gg);
+                    __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) {
+                        const float2 fg = __bfloat1622float2(g2[z]);
+                        o2[z] = __floats2bfloat162_rn(gt * fg.x, gt * fg.y);
+                    }
+                } else {
+                    const float *fg = reinterpret_cast<const float *>(&gg);
+                    float *fo = reinterpret_cast<float *>(&o);
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) fo[z] = gt * fg[z];
+                }
+                dv[vi] = o;
             }
             dgate = warp_sum(acc);
         }
@@ -81,21 +149,36 @@ __global__ void combine_bwd_kernel(CombineBwdArgs a) {
 }
 
 // a19 router: dx[t, c] += sum_k dlogits[t, k] W[k, c]; partial[chunk, k, c] = sum over the
-// chunk's tokens of dlogits[t, k] x[t, c] (thread per column; fixed order).
-constexpr int kRbCols = 128, kRbTok = 512, kRbK = 8;
+// chunk's tokens of dlogits[t, k] x[t, c] (fixed order).  A thread owns 2 adjacent
+// columns; the chunk's dlogits are staged in smem 64 tokens at a time, and 4 tokens' x
+// and dx pairs are loaded before any is used (memory-level parallelism: the kernel is a
+// stream over x and dx).
+constexpr int kRbCols = 256, kRbTok = 512, kRbK = 8, kRbU = 4;
 
-__global__ void router_bwd_kernel(RouterBwdArgs a) {
+__device__ __forceinline__ float2 ld_pair(const void *p, int64_t i, int bf16) {
+    if (bf16) return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(static_cast<const __nv_bfloat16 *>(p) + i));
+    return *reinterpret_cast<const float2 *>(static_cast<const float *>(p) + i);
+}
+
+__device__ __forceinline__ void st_pair(void *p, int64_t i, float2 v, int bf16) {
+    if (bf16) *reinterpret_cast<__nv_bfloat162 *>(static_cast<__nv_bfloat16 *>(p) + i) = __floats2bfloat162_rn(v.x, v.y);
+    else *reinterpret_cast<float2 *>(static_cast<float *>(p) + i) = v;
+}
+
+__global__ void __launch_bounds__(kRbCols / 2) router_bwd_kernel(RouterBwdArgs a) {
     __shared__ float s_dl[64][kRbK];
-    const int c = blockIdx.x * kRbCols + threadIdx.x;
+    const int c = blockIdx.x * kRbCols + 2 * threadIdx.x;          // columns c, c + 1
     const int64_t t0 = (int64_t)blockIdx.y * kRbTok;
     const int64_t t1 = (t0 + kRbTok < a.rows) ? t0 + kRbTok : a.rows;
+    const bool ok = c < a.d;
     for (int k0 = 0; k0 < a.KW; k0 += kRbK) {
         const int nk = min(kRbK, a.KW - k0);
-        float acc[kRbK], w[kRbK];
+        float acc0[kRbK], acc1[kRbK], w0[kRbK], w1[kRbK];
 #pragma unroll
         for (int k = 0; k < kRbK; ++k) {
-            acc[k] = 0.f;
-            w[k] = (k < nk && c < a.d) ? a.w[(int64_t)(k0 + k) * a.d + c] : 0.f;
+            acc0[k] = acc1[k] = 0.f;
+            w0[k] = (k < nk && ok) ? a.w[(int64_t)(k0 + k) * a.d + c] : 0.f;
+            w1[k] = (k < nk && ok) ? a.w[(int64_t)(k0 + k) * a.d + c + 1] : 0.f;
         }
         for (int64_t tb = t0; tb < t1; tb += 64) {
             __syncthreads();
@@ -104,23 +187,41 @@ __global__ void router_bwd_kernel(RouterBwdArgs a) {
                 s_dl[tt][k] = (tb + tt < t1 && k < nk) ? a.dlogits[(tb + tt) * a.KW + k0 + k] : 0.f;
             }
             __syncthreads();
-            if (c < a.d) {
-                const int nt = (int)((t1 - tb) < 64 ? (t1 - tb) : 64);
-                for (int tt = 0; tt < nt; ++tt) {
-                    const int64_t t = tb + tt;
-                    const float xv = ld_el(a.x, t * a.d + c, a.bf16);
-                    float dxa = 0.f;
+            if (!ok) continue;
+            const int nt = (int)((t1 - tb) < 64 ? (t1 - tb) : 64);
+            for (int tt0 = 0; tt0 < nt; tt0 += kRbU) {
+                float2 xv[kRbU], dv[kRbU];
+#pragma unroll
+                for (int u = 0; u < kRbU; ++u) {
+                    const int64_t t = tb + tt0 + u;
+                    if (tt0 + u < nt) {
+                        xv[u] = ld_pair(a.x, t * a.d + c, a.bf16);
+                        dv[u] = ld_pair(a.dx, t * a.d + c, a.bf16);
+                    } else {
+                        xv[u] = dv[u] = make_float2(0.f, 0.f);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kRbU; ++u) {
+                    if (tt0 + u >= nt) break;
+                    float d0 = 0.f, d1 = 0.f;
 #pragma unroll
                     for (int k = 0; k < kRbK; ++k) {
-                        acc[k] = fmaf(s_dl[tt][k], xv, acc[k]);
-                        dxa = fmaf(s_dl[tt][k], w[k], dxa);
+                        const float dl = s_dl[tt0 + u][k];
+                        acc0[k] = fmaf(dl, xv[u].x, acc0[k]);
+                        acc1[k] = fmaf(dl, xv[u].y, acc1[k]);
+                        d0 = fmaf(dl, w0[k], d0);
+                        d1 = fmaf(dl, w1[k], d1);
                     }
-                    st_el(a.dx, t * a.d + c, ld_el(a.dx, t * a.d + c, a.bf16) + dxa, a.bf16);
+                    st_pair(a.dx, (tb + tt0 + u) * a.d + c, make_float2(dv[u].x + d0, dv[u].y + d1), a.bf16);
                 }
             }
         }
-        if (c < a.d)
-            for (int k = 0; k < nk; ++k) a.partial[((int64_t)blockIdx.y * a.KW + k0 + k) * a.d + c] = acc[k];
+        if (ok)
+            for (int k = 0; k < nk; ++k) {
+                a.partial[((int64_t)blockIdx.y * a.KW + k0 + k) * a.d + c] = acc0[k];
+                a.partial[((int64_t)blockIdx.y * a.KW + k0 + k) * a.d + c + 1] = acc1[k];
+            }
     }
 }
 
@@ -155,7 +256,7 @@ void launch_router_bwd(const RouterBwdArgs &a0, cudaStream_t st) {
     a.nchunk = (int)((a.rows + kRbTok - 1) / kRbTok);
     dim3 grid((a.d + kRbCols - 1) / kRbCols, a.nchunk);
     note_launch();
-    router_bwd_kernel<<<grid, kRbCols, 0, st>>>(a);
+    router_bwd_kernel<<<grid, kRbCols / 2, 0, st>>>(a);
     note_launch();
     router_bwd_reduce<<<148, 256, 0, st>>>(a);
 }

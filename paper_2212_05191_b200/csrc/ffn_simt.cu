@@ -123,7 +123,7 @@ void launch_ffn_simt(const FfnArgs &f, cudaStream_t st) {
 }
 
 cudaError_t launch_ffn_tcgen05_train(const FfnArgs &f, void *A1, cudaStream_t st);
-cudaError_t launch_ffn_tcgen05_dgrad(const FfnBwdArgs &b, cudaStream_t st);
+cudaError_t launch_ffn_tcgen05_dgrad(const FfnBwdArgs &b, int part, cudaStream_t st);
 
 cudaError_t launch_ffn_fwd_train(const FfnArgs &f, void *A1, bool tc, cudaStream_t st) {
     if (tc) return launch_ffn_tcgen05_train(f, A1, st);
@@ -197,25 +197,24 @@ __global__ void __launch_bounds__(NTHR) wgrad_simt(WgradArgs a) {
 
 }  // namespace
 
+// Order: dZ, then everything that reads dY (dW2, db2), then dX -- so dX may overwrite dY
+// in place (the peer-store exchange returns dX from the Y buffer) -- then dW1, db1.
 cudaError_t launch_ffn_bwd(const FfnBwdArgs &b, bool tc, cudaStream_t st) {
     const int nseg = b.V * b.S * b.e;
     const int NE = b.V * b.e;
+    const int grid = b.num_sms * 4;
+    const bool tcw = tc && wgrad_tc_supported(b.bf16, b.d, b.d_ff, b.S);
+    // dZ = (dY W2^T) . GELU'(A1): B operand = W2 [NE, d_ff, d] as [N = d_ff, K = d]
     if (tc) {
-        cudaError_t e = launch_ffn_tcgen05_dgrad(b, st);
+        cudaError_t e = launch_ffn_tcgen05_dgrad(b, 1, st);
         if (e != cudaSuccess) return e;
     } else {
-        const int grid = b.num_sms * 4;
-        // dZ = (dY W2^T) . GELU'(A1): B operand = W2 [NE, d_ff, d] as [N = d_ff, K = d]
         GemmArgs g1{b.dY, b.W2, nullptr, b.dZ, b.counts, nseg, b.e, b.S, b.Cseg, b.d_ff, b.d, 0, b.bf16, 2, nullptr, b.A1};
         note_launch();
         grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g1);
-        // dX = dZ W1^T: B operand = W1 [NE, d, d_ff] as [N = d, K = d_ff]
-        GemmArgs g2{b.dZ, b.W1, nullptr, b.dX, b.counts, nseg, b.e, b.S, b.Cseg, b.d, b.d_ff, 0, b.bf16, 3, nullptr, nullptr};
-        note_launch();
-        grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g2);
     }
-    // dW2 = H^T dY  [NE, d_ff, d];  dW1 = X^T dZ  [NE, d, d_ff]
-    if (tc && wgrad_tc_supported(b.bf16, b.d, b.d_ff, b.S)) {
+    // dW2 = H^T dY [NE, d_ff, d]; db2 = 1^T dY (fixed-order two-pass column sums)
+    if (tcw) {
         // tcgen05 wgrad: padding rows up to the next 64-row K block must be zero
         launch_pad_rows_zero(const_cast<void *>(b.X), b.counts, nseg, b.Cseg, b.d, st);
         launch_pad_rows_zero(const_cast<void *>(b.dY), b.counts, nseg, b.Cseg, b.d, st);
@@ -223,18 +222,30 @@ cudaError_t launch_ffn_bwd(const FfnBwdArgs &b, bool tc, cudaStream_t st) {
         launch_pad_rows_zero(b.dZ, b.counts, nseg, b.Cseg, b.d_ff, st);
         cudaError_t e = launch_wgrad_tc(b.H, b.d_ff, b.dY, b.d, b.dW2, b.counts, b.V, b.S, b.e, b.Cseg, b.num_sms, st);
         if (e != cudaSuccess) return e;
-        e = launch_wgrad_tc(b.X, b.d, b.dZ, b.d_ff, b.dW1, b.counts, b.V, b.S, b.e, b.Cseg, b.num_sms, st);
-        if (e != cudaSuccess) return e;
     } else {
         WgradArgs w2{b.H, b.dY, b.dW2, b.counts, b.e, b.S, b.Cseg, b.d_ff, b.d, b.bf16};
         note_launch();
         wgrad_simt<<<dim3((b.d + BN - 1) / BN, (b.d_ff + BM - 1) / BM, NE), NTHR, 0, st>>>(w2);
+    }
+    launch_colsum(b.dY, b.db2, b.colsum_ws, b.counts, NE, b.e, b.S, b.Cseg, b.d, b.bf16, st);
+    // dX = dZ W1^T: B operand = W1 [NE, d, d_ff] as [N = d, K = d_ff]
+    if (tc) {
+        cudaError_t e = launch_ffn_tcgen05_dgrad(b, 2, st);
+        if (e != cudaSuccess) return e;
+    } else {
+        GemmArgs g2{b.dZ, b.W1, nullptr, b.dX, b.counts, nseg, b.e, b.S, b.Cseg, b.d, b.d_ff, 0, b.bf16, 3, nullptr, nullptr};
+        note_launch();
+        grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g2);
+    }
+    // dW1 = X^T dZ [NE, d, d_ff]; db1 = 1^T dZ
+    if (tcw) {
+        cudaError_t e = launch_wgrad_tc(b.X, b.d, b.dZ, b.d_ff, b.dW1, b.counts, b.V, b.S, b.e, b.Cseg, b.num_sms, st);
+        if (e != cudaSuccess) return e;
+    } else {
         WgradArgs w1{b.X, b.dZ, b.dW1, b.counts, b.e, b.S, b.Cseg, b.d, b.d_ff, b.bf16};
         note_launch();
         wgrad_simt<<<dim3((b.d_ff + BN - 1) / BN, (b.d + BM - 1) / BM, NE), NTHR, 0, st>>>(w1);
     }
-    // db2 = 1^T dY, db1 = 1^T dZ: fixed-order two-pass column sums
-    launch_colsum(b.dY, b.db2, b.colsum_ws, b.counts, NE, b.e, b.S, b.Cseg, b.d, b.bf16, st);
     launch_colsum(b.dZ, b.db1, b.colsum_ws, b.counts, NE, b.e, b.S, b.Cseg, b.d_ff, b.bf16, st);
     return cudaGetLastError();
 }

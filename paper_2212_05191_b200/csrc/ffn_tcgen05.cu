@@ -117,25 +117,35 @@ __device__ __forceinline__ f32x2 gelu_erf2(f32x2 z) {
     return mul2(fma2(az, erfa, z), splat2(0.5f));                          // (z + |z| erf) / 2
 }
 
-// GELU'(z) = Phi(z) + z phi(z), with Phi from the same erf approximation.
-__device__ __forceinline__ float gelu_grad(float z) {
-    const float ax = fabsf(z) * 0.70710678118654752f;
-    float p = 4.30638e-5f;
-    p = fmaf(p, ax, 2.765672e-4f);
-    p = fmaf(p, ax, 1.520143e-4f);
-    p = fmaf(p, ax, 9.2705272e-3f);
-    p = fmaf(p, ax, 4.22820123e-2f);
-    p = fmaf(p, ax, 7.05230784e-2f);
-    p = fmaf(p, ax, 1.0f);
-    p = p * p;
-    p = p * p;
-    p = p * p;
-    p = p * p;
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p));
-    const float erf_abs = 1.0f - r;
-    const float Phi = 0.5f + 0.5f * copysignf(erf_abs, z);
-    return Phi + z * 0.3989422804014327f * __expf(-0.5f * z * z);
+// GELU'(z) on a pair (packed fp32x2, as gelu_erf2): Phi(z) + z phi(z), Phi from the same
+// erf approximation, phi(z) = exp(-z^2 / 2) / sqrt(2 pi) via ex2.approx.
+__device__ __forceinline__ f32x2 gelu_grad2(f32x2 z) {
+    const f32x2 az = z & 0x7fffffff7fffffffull;
+    f32x2 p = splat2(4.30638e-5f * 0.125f);
+    p = fma2(p, az, splat2(2.765672e-4f * 0.17677669529663688f));
+    p = fma2(p, az, splat2(1.520143e-4f * 0.25f));
+    p = fma2(p, az, splat2(9.2705272e-3f * 0.35355339059327373f));
+    p = fma2(p, az, splat2(4.22820123e-2f * 0.5f));
+    p = fma2(p, az, splat2(7.05230784e-2f * 0.70710678118654752f));
+    p = fma2(p, az, splat2(1.0f));
+    p = mul2(p, p);
+    p = mul2(p, p);
+    p = mul2(p, p);
+    p = mul2(p, p);
+    float p0, p1, r0, r1;
+    unpack2(p, p0, p1);
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(p0));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(p1));
+    f32x2 erfa = fma2(pack2(r0, r1), splat2(-1.0f), splat2(1.0f));       // erf(|z| / sqrt 2) >= 0
+    erfa |= z & 0x8000000080000000ull;                                    // signed: erf(z / sqrt 2)
+    const f32x2 Phi = fma2(erfa, splat2(0.5f), splat2(0.5f));
+    // exp(-z^2/2) = 2^(-z^2 log2(e) / 2)
+    const f32x2 ex = mul2(mul2(z, z), splat2(-0.72134752044448170f));
+    float e0, e1;
+    unpack2(ex, e0, e1);
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(e0));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(e1));
+    return fma2(mul2(z, splat2(0.3989422804014327f)), pack2(e0, e1), Phi);
 }
 
 struct TileInfo {
@@ -390,8 +400,9 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 #pragma unroll
                         for (int z = 0; z < 4; ++z) {
                             const float2 f = __bfloat1622float2(hh[z]);
-                            w[8 * i + 2 * z] *= gelu_grad(f.x);
-                            w[8 * i + 2 * z + 1] *= gelu_grad(f.y);
+                            const f32x2 gg = mul2(pack2(w[8 * i + 2 * z], w[8 * i + 2 * z + 1]),
+                                                  gelu_grad2(pack2(f.x, f.y)));
+                            unpack2(gg, w[8 * i + 2 * z], w[8 * i + 2 * z + 1]);
                         }
                     }
                 }
@@ -629,17 +640,18 @@ cudaError_t launch_ffn_tcgen05_train(const FfnArgs &f, void *A1, cudaStream_t st
     return launch_gemm(f.H, rows_total, f.W2t, NE, f.b2, f.Y, nullptr, nullptr, f, f.d, f.d_ff, EPI_BIAS, 0, st);
 }
 
-// Backward data GEMMs on tcgen05 (a17): dZ = (dY W2^T) . GELU'(A1); dX = dZ W1^T.
-// W1 [NE, d, d_ff] and W2 [NE, d_ff, d] in their math layouts are the K-major B operands.
-cudaError_t launch_ffn_tcgen05_dgrad(const FfnBwdArgs &b, cudaStream_t st) {
+// Backward data GEMMs on tcgen05 (a17): part 1: dZ = (dY W2^T) . GELU'(A1); part 2:
+// dX = dZ W1^T.  W1 [NE, d, d_ff] and W2 [NE, d_ff, d] in their math layouts are the
+// K-major B operands.
+cudaError_t launch_ffn_tcgen05_dgrad(const FfnBwdArgs &b, int part, cudaStream_t st) {
     FfnArgs f{};
     f.counts = b.counts; f.V = b.V; f.S = b.S; f.e = b.e; f.Cseg = b.Cseg; f.d = b.d; f.d_ff = b.d_ff; f.bf16 = b.bf16;
     f.num_sms = b.num_sms;
     if (!tc_supported(f)) return cudaErrorNotSupported;
     const int64_t rows_total = (int64_t)f.V * f.S * f.e * f.Cseg;
     const int NE = f.V * f.e;
-    cudaError_t e = launch_gemm(b.dY, rows_total, b.W2, NE, nullptr, b.dZ, nullptr, b.A1, f, f.d_ff, f.d, EPI_DGELU, 0, st);
-    if (e != cudaSuccess) return e;
+    if (part == 1)
+        return launch_gemm(b.dY, rows_total, b.W2, NE, nullptr, b.dZ, nullptr, b.A1, f, f.d_ff, f.d, EPI_DGELU, 0, st);
     return launch_gemm(b.dZ, rows_total, b.W1, NE, nullptr, b.dX, nullptr, nullptr, f, f.d, f.d_ff, EPI_PLAIN, 0, st);
 }
 

@@ -355,7 +355,17 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
             const int slot = a.slot2[g];
             if (slot < a.C2) {
                 r.src = static_cast<const char *>(a.recv1) + g * a.rowbytes;
-                r.dst = static_cast<char *>(a.send2) + (((int64_t)v * a.K2 + j) * a.C2 + slot) * a.rowbytes;
+                if (a.peer.bases) {
+                    // PEER: straight into the expert's Y buffer (where dY is consumed), at the
+                    // row the forward permute used for this token
+                    const PeerMap &P = a.peer;
+                    const int rk = P.rank0 + v, i = rk / P.m, l = rk % P.m;
+                    const int q = i * P.m + j / P.e;
+                    const int64_t row = (((int64_t)(q % P.V) * P.m + l) * P.e + j % P.e) * a.C2 + slot;
+                    r.dst = P.bases[q / P.V] + P.off_Y + row * a.rowbytes;
+                } else {
+                    r.dst = static_cast<char *>(a.send2) + (((int64_t)v * a.K2 + j) * a.C2 + slot) * a.rowbytes;
+                }
             }
         }
     } else if (m.kind == MOVE_COMBINE2) {

@@ -146,6 +146,7 @@ struct CombineBwdArgs {
     const void *gout; const void *back1; const float *logits; smile_route route; smile_stats stats;
     void *dsend; float *dlogits; int V; int64_t T; int d; int K1, K2, KW; int64_t C1;
     double alpha, beta, lam; int flat; int bf16;
+    PeerMap peer;            // PEER: back1 rows are loaded from, and gradient rows stored to, their owner
 };
 void launch_combine_bwd(const CombineBwdArgs &a, cudaStream_t st);
 

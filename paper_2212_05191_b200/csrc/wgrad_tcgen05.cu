@@ -196,26 +196,50 @@ struct ColsumArgs {
     int e, S; int64_t Cseg; int N, NE, nch; int bf16;
 };
 
-// part[E][s * nch + c][n] = sum of rows [512 c, 512 c + 512) of segment s (valid rows only)
+// part[E][s * nch + c][n] = sum of rows [512 c, 512 c + 512) of segment s (valid rows
+// only).  A thread owns 8 (bf16) / 4 (fp32) adjacent columns: 16-byte loads, 4 rows in
+// flight; rows summed in order (deterministic).
 __global__ void colsum_partial_kernel(ColsumArgs a) {
-    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int epv = a.bf16 ? 8 : 4;
+    const int n0 = (blockIdx.x * blockDim.x + threadIdx.x) * epv;
     const int E = blockIdx.y, sc = blockIdx.z;
     const int s = sc / a.nch, c = sc % a.nch;
-    if (n >= a.N) return;
+    if (n0 >= a.N) return;
     const int v = E / a.e, k = E % a.e;
     const int g = (v * a.S + s) * a.e + k;
     const int cnt = a.counts[g];
     const int r0 = c * COLSUM_ROWS, r1 = min(cnt, r0 + COLSUM_ROWS);
     const int64_t base = (int64_t)g * a.Cseg;
-    float acc = 0.f;
-    if (a.bf16) {
-        const __nv_bfloat16 *B = static_cast<const __nv_bfloat16 *>(a.B);
-        for (int r = r0; r < r1; ++r) acc += __bfloat162float(B[(base + r) * a.N + n]);
-    } else {
-        const float *B = static_cast<const float *>(a.B);
-        for (int r = r0; r < r1; ++r) acc += B[(base + r) * a.N + n];
+    const int64_t esz = a.bf16 ? 2 : 4;
+    const char *B = static_cast<const char *>(a.B);
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    for (int r = r0; r < r1; r += 4) {
+        uint4 u[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            u[q] = r + q < r1 ? *reinterpret_cast<const uint4 *>(B + ((base + r + q) * a.N + n0) * esz)
+                              : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (a.bf16) {
+                const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u[q]);
+#pragma unroll
+                for (int z = 0; z < 4; ++z) {
+                    const float2 f = __bfloat1622float2(h[z]);
+                    acc[2 * z] += f.x;
+                    acc[2 * z + 1] += f.y;
+                }
+            } else {
+                const float *f = reinterpret_cast<const float *>(&u[q]);
+#pragma unroll
+                for (int z = 0; z < 4; ++z) acc[z] += f[z];
+            }
+        }
     }
-    a.part[((int64_t)E * a.S * a.nch + sc) * a.N + n] = acc;
+    float *dst = a.part + ((int64_t)E * a.S * a.nch + sc) * a.N + n0;
+    for (int i = 0; i < epv; ++i) dst[i] = acc[i];
 }
 
 __global__ void colsum_reduce_kernel(ColsumArgs a) {
@@ -245,7 +269,8 @@ void launch_colsum(const void *B, float *db, float *part, const int32_t *counts,
     ColsumArgs a{B, part, db, counts, e, S, Cseg, N, NE, (int)((Cseg + COLSUM_ROWS - 1) / COLSUM_ROWS), bf16};
     if (a.nch < 1) a.nch = 1;
     note_launch();
-    colsum_partial_kernel<<<dim3((N + 255) / 256, NE, S * a.nch), 256, 0, st>>>(a);
+    const int per_blk = 128 * (bf16 ? 8 : 4);
+    colsum_partial_kernel<<<dim3((N + per_blk - 1) / per_blk, NE, S * a.nch), 128, 0, st>>>(a);
     note_launch();
     colsum_reduce_kernel<<<dim3((N + 255) / 256, NE), 256, 0, st>>>(a);
 }

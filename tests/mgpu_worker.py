@@ -15,6 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
+import oracle  # noqa: E402
 from harness import Case, assert_close_scaled  # noqa: E402
 from paper_2212_05191_b200 import SmileLayer, smile as smb  # noqa: E402
 
@@ -54,14 +55,48 @@ def main():
         sl = lambda t, k=1: None if t is None else t[r0 * k:(r0 + V) * k].contiguous()
         out = torch.empty_like(sl(g["x"]))
         loss = torch.empty(V, dtype=torch.float64, device=dev)
+        bwd = bool(c.get("_bwd"))
         layer.forward(sl(g["x"]), sl(g["W1t"], e), sl(g["b1"], e), sl(g["W2t"], e), sl(g["b2"], e), out, loss,
-                      logits=sl(g["logits"]), w_router=g["w_router"], alpha=case.alpha, beta=case.beta)
+                      logits=sl(g["logits"]), w_router=g["w_router"], alpha=case.alpha, beta=case.beta, train=bwd)
+        grads = None
+        if bwd:
+            # a16-a19 over the same exchange; gout seeded identically on every process
+            tdt = g["x"].dtype
+            rs = np.random.default_rng(100)
+            gout_np = rs.normal(size=(case.G, case.T, case.d)).astype(np.float32)
+            if case.dtype == "bf16":
+                import synth
+                gout_np = synth.round_bf16(gout_np)
+            gout = torch.from_numpy(gout_np).to(dev).to(tdt)
+            W1 = torch.from_numpy(case.W1).to(dev).to(tdt)
+            W2 = torch.from_numpy(case.W2).to(dev).to(tdt)
+            f32 = dict(dtype=torch.float32, device=dev)
+            NEl = V * e
+            grads = dict(dx=torch.empty_like(out), dW1=torch.empty(NEl, case.d, case.d_ff, **f32),
+                         db1=torch.empty(NEl, case.d_ff, **f32), dW2=torch.empty(NEl, case.d_ff, case.d, **f32),
+                         db2=torch.empty(NEl, case.d, **f32),
+                         dW=torch.empty(case.cfg.logit_width, case.d, **f32) if case.fused else None)
+            layer.backward(sl(gout), grads["dx"], sl(W1, e), sl(W2, e), grads["dW1"], grads["db1"], grads["dW2"],
+                           grads["db2"], dW_router=grads["dW"], lam=2.0)
         torch.cuda.synchronize()
         err = layer.get_error()
         outs = [torch.empty_like(out) for _ in range(world)]
         losses = [torch.empty_like(loss) for _ in range(world)]
         dist.all_gather(outs, out)
         dist.all_gather(losses, loss)
+        gathered = {}
+        if grads is not None:
+            for k, t in grads.items():
+                if t is None:
+                    continue
+                if k == "dW":                     # each process holds its ranks' share of the tied router gradient
+                    tot = t.clone()
+                    dist.all_reduce(tot)
+                    gathered[k] = tot
+                else:
+                    parts = [torch.empty_like(t) for _ in range(world)]
+                    dist.all_gather(parts, t)
+                    gathered[k] = torch.cat(parts)
         if rank == 0:
             try:
                 assert err == 0, f"device error {err}"
@@ -72,6 +107,13 @@ def main():
                 keep = r.keep.reshape(-1).astype(bool)
                 assert (got[~keep] == 0).all()
                 np.testing.assert_allclose(torch.cat(losses).cpu().numpy(), r.loss, rtol=1e-6)
+                if gathered:
+                    ref = oracle.backward(case.cfg, r, case.x, case.W1, case.b1, case.W2, case.b2, gout_np, lam=2.0,
+                                          W=case.w_router if case.fused else None,
+                                          logits=None if case.fused else case.logits)
+                    tol = 3e-2 if case.dtype == "bf16" else 1e-4
+                    for k, t in gathered.items():
+                        assert_close_scaled(t.float().cpu().numpy().reshape(ref[k].shape), ref[k], tol, f"mgpu bwd {k}")
             except AssertionError as ex:
                 failures.append(f"{c}: {ex}")
         torch.cuda.synchronize()

@@ -15,10 +15,12 @@ from harness import Case, assert_close_scaled
 pytestmark = pytest.mark.gpu
 
 
-def run_bwd(case, lam=2.0, seed=0):
+def run_bwd(case, lam=2.0, seed=0, peer=False):
     from paper_2212_05191_b200 import SmileLayer
     G, T, d, d_ff, e = case.G, case.T, case.d, case.d_ff, case.e
     layer = SmileLayer(case.n, case.m, e, d, d_ff, T, case.cf, case.dtype, case.mode, ffn_impl=case.ffn_impl)
+    if peer:
+        layer.enable_peer_exchange()
     g = case.gpu_tensors()
     tdt = g["x"].dtype
     rs = np.random.default_rng(100 + seed)
@@ -74,4 +76,17 @@ def run_bwd(case, lam=2.0, seed=0):
 def test_backward_parity(n, m, e, T, d, d_ff, cf, dtype, mode, fused, ffn):
     case = Case(n, m, e, T, d, d_ff, cf, dtype=dtype, mode=mode, dist="skewed", seed=21, fused=fused, ffn_impl=ffn)
     r = run_bwd(case)
+    assert (r.keep == 0).any()
+
+
+@pytest.mark.parametrize("n,m,e,T,d,d_ff,cf,dtype,mode,fused,ffn", [
+    (2, 4, 1, 600, 128, 256, 1.25, "bf16", "bilevel", True, "tcgen05"),
+    (2, 2, 2, 700, 128, 384, 1.0, "bf16", "flat", True, "tcgen05"),
+    (2, 2, 2, 257, 64, 64, 0.75, "fp32", "bilevel", True, "simt"),
+])
+def test_backward_parity_peer(n, m, e, T, d, d_ff, cf, dtype, mode, fused, ffn):
+    """The training step over the peer-store exchange (gradient rows stored at / loaded
+    from their owners, every exchange a barrier): same oracle bar as the copy path."""
+    case = Case(n, m, e, T, d, d_ff, cf, dtype=dtype, mode=mode, dist="skewed", seed=21, fused=fused, ffn_impl=ffn)
+    r = run_bwd(case, peer=True)
     assert (r.keep == 0).any()
