@@ -149,37 +149,30 @@ __global__ void combine_bwd_kernel(CombineBwdArgs a) {
 }
 
 // a19 router: dx[t, c] += sum_k dlogits[t, k] W[k, c]; partial[chunk, k, c] = sum over the
-// chunk's tokens of dlogits[t, k] x[t, c] (fixed order).  A thread owns 2 adjacent
-// columns; the chunk's dlogits are staged in smem 64 tokens at a time, and 4 tokens' x
-// and dx pairs are loaded before any is used (memory-level parallelism: the kernel is a
-// stream over x and dx).
-constexpr int kRbCols = 256, kRbTok = 512, kRbK = 8, kRbU = 4;
+// chunk's tokens of dlogits[t, k] x[t, c] (fixed order).  A thread owns RB_C adjacent
+// columns (one 16-byte vector of x / dx: 8 bf16 or 4 fp32); the chunk's dlogits are
+// staged in smem 64 tokens at a time and RB_U tokens' x and dx vectors are loaded before
+// any is used (the kernel is a stream over x and dx).
+constexpr int kRbTok = 256, kRbK = 8, kRbU = 4, kRbThreads = 128;
 
-__device__ __forceinline__ float2 ld_pair(const void *p, int64_t i, int bf16) {
-    if (bf16) return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(static_cast<const __nv_bfloat16 *>(p) + i));
-    return *reinterpret_cast<const float2 *>(static_cast<const float *>(p) + i);
-}
-
-__device__ __forceinline__ void st_pair(void *p, int64_t i, float2 v, int bf16) {
-    if (bf16) *reinterpret_cast<__nv_bfloat162 *>(static_cast<__nv_bfloat16 *>(p) + i) = __floats2bfloat162_rn(v.x, v.y);
-    else *reinterpret_cast<float2 *>(static_cast<float *>(p) + i) = v;
-}
-
-__global__ void __launch_bounds__(kRbCols / 2) router_bwd_kernel(RouterBwdArgs a) {
+template <bool BF16>
+__global__ void __launch_bounds__(kRbThreads) router_bwd_kernel(RouterBwdArgs a) {
+    constexpr int RB_C = BF16 ? 8 : 4;
     __shared__ float s_dl[64][kRbK];
-    const int c = blockIdx.x * kRbCols + 2 * threadIdx.x;          // columns c, c + 1
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * RB_C;
     const int64_t t0 = (int64_t)blockIdx.y * kRbTok;
     const int64_t t1 = (t0 + kRbTok < a.rows) ? t0 + kRbTok : a.rows;
     const bool ok = c < a.d;
     for (int k0 = 0; k0 < a.KW; k0 += kRbK) {
         const int nk = min(kRbK, a.KW - k0);
-        float acc0[kRbK], acc1[kRbK], w0[kRbK], w1[kRbK];
+        float acc[kRbK][RB_C], w[kRbK][RB_C];
 #pragma unroll
-        for (int k = 0; k < kRbK; ++k) {
-            acc0[k] = acc1[k] = 0.f;
-            w0[k] = (k < nk && ok) ? a.w[(int64_t)(k0 + k) * a.d + c] : 0.f;
-            w1[k] = (k < nk && ok) ? a.w[(int64_t)(k0 + k) * a.d + c + 1] : 0.f;
-        }
+        for (int k = 0; k < kRbK; ++k)
+#pragma unroll
+            for (int j = 0; j < RB_C; ++j) {
+                acc[k][j] = 0.f;
+                w[k][j] = (k < nk && ok) ? a.w[(int64_t)(k0 + k) * a.d + c + j] : 0.f;
+            }
         for (int64_t tb = t0; tb < t1; tb += 64) {
             __syncthreads();
             for (int z = threadIdx.x; z < 64 * kRbK; z += blockDim.x) {
@@ -190,38 +183,62 @@ __global__ void __launch_bounds__(kRbCols / 2) router_bwd_kernel(RouterBwdArgs a
             if (!ok) continue;
             const int nt = (int)((t1 - tb) < 64 ? (t1 - tb) : 64);
             for (int tt0 = 0; tt0 < nt; tt0 += kRbU) {
-                float2 xv[kRbU], dv[kRbU];
+                uint4 xv[kRbU], dv[kRbU];
 #pragma unroll
                 for (int u = 0; u < kRbU; ++u) {
                     const int64_t t = tb + tt0 + u;
                     if (tt0 + u < nt) {
-                        xv[u] = ld_pair(a.x, t * a.d + c, a.bf16);
-                        dv[u] = ld_pair(a.dx, t * a.d + c, a.bf16);
+                        xv[u] = *reinterpret_cast<const uint4 *>(static_cast<const char *>(a.x) + (t * a.d + c) * (BF16 ? 2 : 4));
+                        dv[u] = *reinterpret_cast<const uint4 *>(static_cast<const char *>(a.dx) + (t * a.d + c) * (BF16 ? 2 : 4));
                     } else {
-                        xv[u] = dv[u] = make_float2(0.f, 0.f);
+                        xv[u] = dv[u] = make_uint4(0, 0, 0, 0);
                     }
                 }
 #pragma unroll
                 for (int u = 0; u < kRbU; ++u) {
                     if (tt0 + u >= nt) break;
-                    float d0 = 0.f, d1 = 0.f;
+                    float xf[RB_C], df[RB_C];
+                    if (BF16) {
+                        const __nv_bfloat162 *hx = reinterpret_cast<const __nv_bfloat162 *>(&xv[u]);
+                        const __nv_bfloat162 *hd = reinterpret_cast<const __nv_bfloat162 *>(&dv[u]);
+#pragma unroll
+                        for (int z = 0; z < RB_C / 2; ++z) {
+                            const float2 fx = __bfloat1622float2(hx[z]), fd = __bfloat1622float2(hd[z]);
+                            xf[2 * z] = fx.x; xf[2 * z + 1] = fx.y; df[2 * z] = fd.x; df[2 * z + 1] = fd.y;
+                        }
+                    } else {
+                        const float *fx = reinterpret_cast<const float *>(&xv[u]);
+                        const float *fd = reinterpret_cast<const float *>(&dv[u]);
+#pragma unroll
+                        for (int z = 0; z < RB_C; ++z) { xf[z] = fx[z]; df[z] = fd[z]; }
+                    }
 #pragma unroll
                     for (int k = 0; k < kRbK; ++k) {
                         const float dl = s_dl[tt0 + u][k];
-                        acc0[k] = fmaf(dl, xv[u].x, acc0[k]);
-                        acc1[k] = fmaf(dl, xv[u].y, acc1[k]);
-                        d0 = fmaf(dl, w0[k], d0);
-                        d1 = fmaf(dl, w1[k], d1);
+#pragma unroll
+                        for (int j = 0; j < RB_C; ++j) {
+                            acc[k][j] = fmaf(dl, xf[j], acc[k][j]);
+                            df[j] = fmaf(dl, w[k][j], df[j]);
+                        }
                     }
-                    st_pair(a.dx, (tb + tt0 + u) * a.d + c, make_float2(dv[u].x + d0, dv[u].y + d1), a.bf16);
+                    uint4 o;
+                    if (BF16) {
+                        __nv_bfloat162 *ho = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+                        for (int z = 0; z < RB_C / 2; ++z) ho[z] = __floats2bfloat162_rn(df[2 * z], df[2 * z + 1]);
+                    } else {
+                        float *fo = reinterpret_cast<float *>(&o);
+#pragma unroll
+                        for (int z = 0; z < RB_C; ++z) fo[z] = df[z];
+                    }
+                    *reinterpret_cast<uint4 *>(static_cast<char *>(a.dx) + ((tb + tt0 + u) * a.d + c) * (BF16 ? 2 : 4)) = o;
                 }
             }
         }
         if (ok)
-            for (int k = 0; k < nk; ++k) {
-                a.partial[((int64_t)blockIdx.y * a.KW + k0 + k) * a.d + c] = acc0[k];
-                a.partial[((int64_t)blockIdx.y * a.KW + k0 + k) * a.d + c + 1] = acc1[k];
-            }
+            for (int k = 0; k < nk; ++k)
+#pragma unroll
+                for (int j = 0; j < RB_C; ++j) a.partial[((int64_t)blockIdx.y * a.KW + k0 + k) * a.d + c + j] = acc[k][j];
     }
 }
 
@@ -254,9 +271,13 @@ void launch_router_bwd(const RouterBwdArgs &a0, cudaStream_t st) {
     if (a0.rows == 0) return;
     RouterBwdArgs a = a0;
     a.nchunk = (int)((a.rows + kRbTok - 1) / kRbTok);
-    dim3 grid((a.d + kRbCols - 1) / kRbCols, a.nchunk);
+    const int per = a.bf16 ? 8 : 4;                       // columns per thread
+    int thr = ((a.d / per + 31) / 32) * 32;
+    thr = thr < 32 ? 32 : (thr > kRbThreads ? kRbThreads : thr);
+    dim3 grid((a.d + thr * per - 1) / (thr * per), a.nchunk);
     note_launch();
-    router_bwd_kernel<<<grid, kRbCols / 2, 0, st>>>(a);
+    if (a.bf16) router_bwd_kernel<true><<<grid, thr, 0, st>>>(a);
+    else router_bwd_kernel<false><<<grid, thr, 0, st>>>(a);
     note_launch();
     router_bwd_reduce<<<148, 256, 0, st>>>(a);
 }

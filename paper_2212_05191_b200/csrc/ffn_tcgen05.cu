@@ -181,7 +181,7 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref
 // CG = 1: one CTA per tile (M = 128).  CG = 2: a CTA pair (cluster of 2) per tile
 // (M = 256, tcgen05.mma.cta_group::2 issued by the leader), each CTA loading half of A
 // and half of B, which halves the shared-memory operand traffic per SM.
-template <int CG, int NPAIR>
+template <int CG, int NPAIR, bool DG>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA128,
                  const __grid_constant__ CUtensorMap mapB,
@@ -357,18 +357,30 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         for (int tile = cid; tile < total; tile += ncl, ++it) {
             const TileInfo t = tile_info<CG, NPAIR>(a, s_pref, tile, ntn, rank, pair);
             const int acc = it & 1;
-            mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
-            tc_fence_after();
-            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS;
             const bool has_bias = a.mode == EPI_BIAS || a.mode == EPI_BIAS_SAVE;
             const bool act = (a.mode == EPI_BIAS && a.gelu) || a.mode == EPI_BIAS_SAVE;
+            constexpr bool dgelu = DG;                      // EPI_DGELU has its own instantiation
             const float4 *bias4 = reinterpret_cast<const float4 *>(a.bias + (int64_t)t.E * a.N + (int64_t)t.nt * a.BN);
             const int64_t dcol0 = (int64_t)t.nt * a.BN;
             int64_t d_row;                                  // this warp's strip
             int srows;
             expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + q, d_row, srows);
             const bool full_box = srows == 32;
+            // EPI_DGELU: chunk c's saved pre-activation is loaded before its accumulator
+            // columns (the first chunk's while this tile's MMAs still run)
+            const uint4 *aux_row =
+                reinterpret_cast<const uint4 *>(a.aux + (d_row + (lane < srows ? lane : 0)) * (int64_t)a.N + dcol0);
+            uint4 acur[4];
+            if (dgelu && c_beg < c_end && srows > 0)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acur[i] = __ldg(aux_row + c_beg * 4 + i);
+            mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS;
             for (int c = c_beg; c < c_end && srows > 0; ++c) {
+                if (dgelu && c > c_beg)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acur[i] = __ldg(aux_row + c * 4 + i);
                 float w[32];
                 tmem_ld32(tbase + c * 32, w);
                 if (has_bias) {
@@ -390,12 +402,10 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                         pw2[i] = *reinterpret_cast<uint32_t *>(&hh);
                     }
                 }
-                if (a.mode == EPI_DGELU && lane < srows) {
-                    const uint4 *ap =
-                        reinterpret_cast<const uint4 *>(a.aux + (d_row + lane) * (int64_t)a.N + dcol0 + c * 32);
+                if (dgelu) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const uint4 u = __ldg(ap + i);
+                        const uint4 u = acur[i];
                         const __nv_bfloat162 *hh = reinterpret_cast<const __nv_bfloat162 *>(&u);
 #pragma unroll
                         for (int z = 0; z < 4; ++z) {
@@ -530,13 +540,13 @@ int pick_npair() {
     return v;
 }
 
-template <int CG, int NPAIR>
+template <int CG, int NPAIR, bool DG>
 cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUtensorMap &mB, const CUtensorMap &mD,
                       const CUtensorMap &mD2, const TcArgs &a, size_t smem, int num_sms, cudaStream_t st) {
     constexpr int CS = CG * NPAIR;
     static int grid = 0;
     if (!grid) {
-        cudaFuncSetAttribute(ffn_gemm_tcgen05<CG, NPAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
+        cudaFuncSetAttribute(ffn_gemm_tcgen05<CG, NPAIR, DG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
         grid = num_sms / CS * CS;
         // SMILE_FFN_MAX_CTAS caps the persistent grid (leaves SMs to kernels of other
         // streams, e.g. the permutes of the next chunk in the pipelined layer)
@@ -557,14 +567,14 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
             q.attrs = at;
             q.numAttrs = 1;
             int ncl = 0;
-            if (cudaOccupancyMaxActiveClusters(&ncl, ffn_gemm_tcgen05<CG, NPAIR>, &q) == cudaSuccess && ncl > 0 &&
+            if (cudaOccupancyMaxActiveClusters(&ncl, ffn_gemm_tcgen05<CG, NPAIR, DG>, &q) == cudaSuccess && ncl > 0 &&
                 ncl * CS < grid)
                 grid = ncl * CS;
         }
     }
     note_launch();
     if (CS == 1) {
-        ffn_gemm_tcgen05<CG, NPAIR><<<grid, NTHREADS, smem, st>>>(mA, mA128, mB, mD, mD2, a);
+        ffn_gemm_tcgen05<CG, NPAIR, DG><<<grid, NTHREADS, smem, st>>>(mA, mA128, mB, mD, mD2, a);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg;
@@ -580,7 +590,7 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<CG, NPAIR>, mA, mA128, mB, mD, mD2, a);
+    return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<CG, NPAIR, DG>, mA, mA128, mB, mD, mD2, a);
 }
 
 // One grouped GEMM launch: D[rows, N] = epi(A[rows, K] . B[expert][N, K]^T).
@@ -608,9 +618,15 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     a.stages = pick_stages(CG, nbox, a.tma_store);
     a.err = nullptr;
     const size_t smem = smem_bytes(CG, a.stages, nbox, a.tma_store);
-    if (CG == 2 && NPAIR == 2) return launch_tc<2, 2>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
-    if (CG == 2) return launch_tc<2, 1>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
-    return launch_tc<1, 1>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
+    const bool dg = mode == EPI_DGELU;
+    if (CG == 2 && NPAIR == 2)
+        return dg ? launch_tc<2, 2, true>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)
+                  : launch_tc<2, 2, false>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
+    if (CG == 2)
+        return dg ? launch_tc<2, 1, true>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)
+                  : launch_tc<2, 1, false>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
+    return dg ? launch_tc<1, 1, true>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)
+              : launch_tc<1, 1, false>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
 }
 
 }  // namespace

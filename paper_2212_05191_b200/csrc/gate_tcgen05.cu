@@ -37,7 +37,7 @@ using namespace tc;
 
 constexpr int GT_BM = 128, GT_BK = 64;
 constexpr int GT_THREADS = 384;
-constexpr int GT_A_BYTES = GT_BM * GT_BK * 2;   // 16 KB per stage
+constexpr int GT_A_BYTES = GT_BM * GT_BK * 2;   // 16 KB per 64-column sub-block
 constexpr int GT_MAX_NP = 384;                  // 3 * KW <= 384 (KW <= 128)
 
 // W fp32 [KW, d] -> Wb bf16 [NP, d]: row 3k+p = piece p of W[k], rows >= 3 KW zero.
@@ -64,6 +64,8 @@ struct GateTcArgs {
     int nbuf;        // TMEM accumulator buffers (2 when 2 * NP <= 512)
     int stages;
     int ntiles;
+    int nsub;        // 64-column sub-blocks per pipeline stage (2 when d % 128 == 0: fewer,
+                     // larger stages -- the single MMA thread's per-stage overhead halves)
 };
 
 // After the group's logits of one tile are in smem: (optional) logits_out copy, then the
@@ -87,10 +89,12 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const GateArgs &a = ta.g;
     const int NP = ta.NP, ST = ta.stages, KW = a.KW;
-    const int b_bytes = NP * GT_BK * 2;
+    const int nsub = ta.nsub;
+    const int a_bytes = nsub * GT_A_BYTES;                 // per stage
+    const int b_bytes = nsub * NP * GT_BK * 2;
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;
-    unsigned char *sB = sA + ST * GT_A_BYTES;
+    unsigned char *sB = sA + ST * a_bytes;
     // per epilogue group g: logits [128][lds] | s_j [128] | s_wh [4][K1] | s_bh [K1]
     const int lds = gate_lds(KW);
     const int grp_ints = GT_BM * lds + GT_BM + 5 * a.K1;
@@ -124,7 +128,7 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
-    const int nk = a.d / GT_BK;
+    const int nk = a.d / (GT_BK * nsub);
     const int nbuf = ta.nbuf;
     const int nchunk_n = NP > 256 ? 2 : 1;
     const int NPc = NP / nchunk_n;                     // N of one MMA
@@ -140,10 +144,14 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full[stage]);
-                    mbar_arrive_tx(fb, GT_A_BYTES + b_bytes);
-                    tma_load_2d(smem_u32(sA + stage * GT_A_BYTES), &mapX, kb * GT_BK, row0, fb);
-                    for (int h = 0; h < nchunk_n; ++h)
-                        tma_load_2d(smem_u32(sB + stage * b_bytes + h * NPc * 128), &mapW, kb * GT_BK, h * NPc, fb);
+                    mbar_arrive_tx(fb, a_bytes + b_bytes);
+                    for (int u = 0; u < nsub; ++u) {
+                        const int col = (kb * nsub + u) * GT_BK;
+                        tma_load_2d(smem_u32(sA + stage * a_bytes + u * GT_A_BYTES), &mapX, col, row0, fb);
+                        for (int h = 0; h < nchunk_n; ++h)
+                            tma_load_2d(smem_u32(sB + stage * b_bytes + u * NP * 128 + h * NPc * 128), &mapW, col,
+                                        h * NPc, fb);
+                    }
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
             }
@@ -164,14 +172,17 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&full[stage]), phase);
                     tc_fence_after();
-                    const uint64_t ad = sw128_desc(smem_u32(sA + stage * GT_A_BYTES));
+                    for (int u = 0; u < nsub; ++u) {
+                        const uint64_t ad = sw128_desc(smem_u32(sA + stage * a_bytes + u * GT_A_BYTES));
 #pragma unroll
-                    for (int k = 0; k < GT_BK / 16; ++k)
-                        for (int h = 0; h < nchunk_n; ++h) {
-                            const uint64_t bd = sw128_desc(smem_u32(sB + stage * b_bytes + h * NPc * 128));
-                            mma_bf16(tmem_d + h * NPc, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc,
-                                     (kb | k) ? 1u : 0u);
-                        }
+                        for (int k = 0; k < GT_BK / 16; ++k)
+                            for (int h = 0; h < nchunk_n; ++h) {
+                                const uint64_t bd =
+                                    sw128_desc(smem_u32(sB + stage * b_bytes + u * NP * 128 + h * NPc * 128));
+                                mma_bf16(tmem_d + h * NPc, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc,
+                                         (kb | u | k) ? 1u : 0u);
+                            }
+                    }
                     mma_commit(smem_u32(&empty[stage]));
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
@@ -230,9 +241,9 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     }
 }
 
-size_t gate_tc_smem(int NP, int KW, int K1, int stages) {
+size_t gate_tc_smem(int NP, int KW, int K1, int stages, int nsub) {
     const int groups = 2 * NP <= 512 ? 2 : 1;          // = nbuf
-    return 1024 + (size_t)stages * (GT_A_BYTES + NP * GT_BK * 2) + groups * ((size_t)GT_BM * gate_lds(KW) + GT_BM + 5 * K1) * 4 + 8 +
+    return 1024 + (size_t)stages * nsub * (GT_A_BYTES + NP * GT_BK * 2) + groups * ((size_t)GT_BM * gate_lds(KW) + GT_BM + 5 * K1) * 4 + 8 +
            (2 * stages + 4) * 8 + 16;
 }
 
@@ -260,10 +271,12 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
     ta.NP = NP;
     ta.nbuf = 2 * NP <= 512 ? 2 : 1;
     ta.ntiles = a.V * a.nblk;
+    // two 64-column sub-blocks per stage when d allows and 3+ such stages fit
+    ta.nsub = (a.d % (2 * GT_BK) == 0 && gate_tc_smem(NP, a.KW, a.K1, 3, 2) <= 227 * 1024) ? 2 : 1;
     int stages = 8;
-    while (stages > 2 && gate_tc_smem(NP, a.KW, a.K1, stages) > 227 * 1024) --stages;
+    while (stages > 2 && gate_tc_smem(NP, a.KW, a.K1, stages, ta.nsub) > 227 * 1024) --stages;
     ta.stages = stages;
-    const size_t smem = gate_tc_smem(NP, a.KW, a.K1, stages);
+    const size_t smem = gate_tc_smem(NP, a.KW, a.K1, stages, ta.nsub);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(gate1_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
