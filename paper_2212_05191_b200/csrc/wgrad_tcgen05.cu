@@ -20,7 +20,7 @@
 // n fastest; the K loop walks every segment of the expert.
 //
 // Bias gradients: two passes with fixed-order sums (deterministic): per (expert, segment,
-// 512-row chunk) column partials, then their sum in chunk order.
+// 128-row chunk) column partials, then their sum in chunk order.
 #include "smile_internal.h"
 #include "tc_util.cuh"
 
@@ -36,7 +36,7 @@ constexpr int WG_THREADS = 256;
 constexpr int WG_A_BYTES = WG_BM * WG_BK * 2;        // 16 KB: two 64-column boxes
 constexpr int WG_BOX_BYTES = 64 * WG_BK * 2;         // 8 KB: one 64 x 64 box
 constexpr int WG_MAXSEG_S = 64;                      // segments per expert (S <= world size)
-constexpr int COLSUM_ROWS = 512;
+constexpr int COLSUM_ROWS = 128;     // rows per partial: short sequential chains, many blocks
 
 __global__ void pad_rows_zero_kernel(void *buf, const int32_t *counts, int nseg, int64_t Cseg, int cols) {
     // rows [count, min(ceil64(count), Cseg)) of every segment; cols % 8 == 0 (16-byte stores)
@@ -196,7 +196,7 @@ struct ColsumArgs {
     int e, S; int64_t Cseg; int N, NE, nch; int bf16;
 };
 
-// part[E][s * nch + c][n] = sum of rows [512 c, 512 c + 512) of segment s (valid rows
+// part[E][s * nch + c][n] = sum of rows [128 c, 128 c + 128) of segment s (valid rows
 // only).  A thread owns 8 (bf16) / 4 (fp32) adjacent columns: 16-byte loads, 4 rows in
 // flight; rows summed in order (deterministic).
 __global__ void colsum_partial_kernel(ColsumArgs a) {
