@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay each step as a CUDA graph")
+    ap.add_argument("--fused-gate", action="store_true",
+                    help="gate + level-1 permute as one call (smile_gate_dispatch_inter); default: two calls")
     ap.add_argument("--chunks", type=int, default=1,
                     help="> 1: the layer as c pipelined micro-batches on two streams (SURVEY 8(f) row 2)")
     ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling period (0 = off)")
@@ -259,9 +261,15 @@ def step(L, inp, ev=None):
     A = lambda p: Addr(p)
     rec = (lambda i: ev[i].record()) if ev is not None else (lambda i: None)
     rec(0)
-    L.gate_inter(inp["x"], w.route, w.stats, A(w.counts1), w_router=inp["w_router"])
-    rec(1)
-    L.dispatch(1, inp["x"], A(w.send1), route=w.route, send_meta=A(w.meta1) if not L.flat else None)
+    if inp.get("fused_gate"):
+        # a1-a4 in one tensor-core kernel (smile_gate_dispatch_inter); "dispatch1" is empty
+        L.gate_dispatch_inter(inp["x"], inp["w_router"], w.route, w.stats, A(w.counts1), A(w.send1),
+                              send_meta=A(w.meta1) if not L.flat else None)
+        rec(1)
+    else:
+        L.gate_inter(inp["x"], w.route, w.stats, A(w.counts1), w_router=inp["w_router"])
+        rec(1)
+        L.dispatch(1, inp["x"], A(w.send1), route=w.route, send_meta=A(w.meta1) if not L.flat else None)
     rec(2)
     if not L.flat:
         L.all2all_inter(0, A(w.send1), A(w.recv1), A(w.meta1), A(w.rmeta1), A(w.counts1))
@@ -301,8 +309,12 @@ def stage_front(L, inp):
     """a1-a8 of one (chunk) layer: gate, level-1 permute + exchange, level-2 gate, level-2
     permute + exchange (flat: gate, permute + exchange)."""
     w, A = L._view, Addr
-    L.gate_inter(inp["x"], w.route, w.stats, A(w.counts1), w_router=inp["w_router"])
-    L.dispatch(1, inp["x"], A(w.send1), route=w.route, send_meta=A(w.meta1) if not L.flat else None)
+    if inp.get("fused_gate"):
+        L.gate_dispatch_inter(inp["x"], inp["w_router"], w.route, w.stats, A(w.counts1), A(w.send1),
+                              send_meta=A(w.meta1) if not L.flat else None)
+    else:
+        L.gate_inter(inp["x"], w.route, w.stats, A(w.counts1), w_router=inp["w_router"])
+        L.dispatch(1, inp["x"], A(w.send1), route=w.route, send_meta=A(w.meta1) if not L.flat else None)
     if not L.flat:
         L.all2all_inter(0, A(w.send1), A(w.recv1), A(w.meta1), A(w.rmeta1), A(w.counts1))
         L.gate_intra(A(w.rmeta1), A(w.slot2), A(w.counts2))
@@ -415,7 +427,7 @@ def run_pipelined(args):
         for k in range(c):
             xk = x[:, k * Tc:(k + 1) * Tc].contiguous()
             inps.append(dict(x=xk, w_router=w_router, W1t=W1t, W2t=W2t, b1=b1, b2=b2, out=torch.empty_like(xk),
-                             loss=torch.empty(V, dtype=torch.float64, device=dev)))
+                             loss=torch.empty(V, dtype=torch.float64, device=dev), fused_gate=args.fused_gate))
         s2 = torch.cuda.Stream()
         evf = [torch.cuda.Event() for _ in range(c)]
         eve = [torch.cuda.Event() for _ in range(c)]
@@ -604,7 +616,8 @@ def run_ours(args):
         b2 = torch.zeros(V * e, d, device=dev)
         out = torch.empty_like(x)
         loss = torch.empty(V, dtype=torch.float64, device=dev)
-        inp = dict(x=x, w_router=w_router, W1t=W1t, W2t=W2t, b1=b1, b2=b2, out=out, loss=loss)
+        inp = dict(x=x, w_router=w_router, W1t=W1t, W2t=W2t, b1=b1, b2=b2, out=out, loss=loss,
+                   fused_gate=args.fused_gate)
         train = bool(cfgd.get("train"))
         if train:
             f32 = dict(dtype=torch.float32, device=dev)
@@ -688,7 +701,11 @@ def run_ours(args):
         # and writes each row it moves; combine1 also writes the zero rows of drops.
         rb = d * (2 if cfgd["dtype"] == "bf16" else 4)
         kept1 = int(w["counts1"].sum().item())
-        hbm = {"gate1": V * T * (rb + 24), "dispatch1": 2 * kept1 * rb, "combine1": (kept1 + V * T) * rb}
+        if inp.get("fused_gate") and not train:
+            # fused gate + permute: x read once, kept rows written, 24 B route record per token
+            hbm = {"gate1": V * T * (rb + 24) + kept1 * rb, "combine1": (kept1 + V * T) * rb}
+        else:
+            hbm = {"gate1": V * T * (rb + 24), "dispatch1": 2 * kept1 * rb, "combine1": (kept1 + V * T) * rb}
         if mode == "bilevel":
             recv2 = int(w["counts2"].sum().item())
             hbm.update({"dispatch2": 2 * recv2 * rb, "combine2": 2 * recv2 * rb})

@@ -202,6 +202,17 @@ smile_status smile_gate_inter(smile_ctx ctx, const void *x, const float *w_route
                               const float *logits, float *logits_out, const smile_route *route,
                               const smile_stats *stats, int32_t *counts1, void *stream);
 
+/* a1-a4 fused (fused router only): smile_gate_inter followed by smile_dispatch(level 1)
+ * in one pass over x where the tensor-core gate applies (bf16, d % 64 == 0): the final
+ * level-1 slots come from a decoupled look-back over the tiles' destination histograms
+ * inside the gate kernel, which then moves every kept row to its slot (send_rows /
+ * send_meta as smile_dispatch(1) writes them, or the destinations' receive buffers with
+ * the peer-store exchange).  Same outputs as the two calls (route, stats, counts1, rows,
+ * meta); elsewhere it runs exactly those two calls.  logits_out: optional [V, T, KW]. */
+smile_status smile_gate_dispatch_inter(smile_ctx ctx, const void *x, const float *w_router, float *logits_out,
+                                       const smile_route *route, const smile_stats *stats, int32_t *counts1,
+                                       void *send_rows, int32_t *send_meta, void *stream);
+
 /* a4 (level 1) / a7 (level 2): permute token rows into per-destination send buffers.
  * level 1: rows_in = x [V, T, d]; finalises route->slot1; send_rows [V, K1, C1, d];
  *   send_meta [V, K1, C1] = j of the token in that slot, -1 for empty slots (BILEVEL),

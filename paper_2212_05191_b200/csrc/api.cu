@@ -281,6 +281,15 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
             c->TB1 = 128;                       // the tensor-core gate's token tile
             const size_t wb = (size_t)gate_tc_np(z.KW) * shape->d * 2;
             if (cudaMalloc(&c->wsplit, wb) != cudaSuccess) { delete c; return SMILE_ECUDA; }
+            // look-back state of the fused gate + permute (flags zero between calls)
+            const int64_t nt = (int64_t)z.V * ((shape->T + 127) / 128);
+            if (cudaMalloc(&c->lb_flag, (nt > 0 ? nt : 1) * 4) != cudaSuccess ||
+                cudaMalloc(&c->lb_agg, (nt > 0 ? nt : 1) * z.K1 * 4) != cudaSuccess ||
+                cudaMalloc(&c->lb_inc, (nt > 0 ? nt : 1) * z.K1 * 4) != cudaSuccess ||
+                cudaMemset(c->lb_flag, 0, (nt > 0 ? nt : 1) * 4) != cudaSuccess) {
+                delete c;
+                return SMILE_ECUDA;
+            }
         }
     }
     c->nblk1 = (int)((shape->T + c->TB1 - 1) / c->TB1);
@@ -348,6 +357,7 @@ extern "C" smile_status smile_destroy(smile_ctx c) {
     cudaFree(c->d_err);
     cudaFree(c->wsplit);
     cudaFree(c->colsum_ws);
+    cudaFree(c->lb_flag); cudaFree(c->lb_agg); cudaFree(c->lb_inc);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     for (int i = 0; i < 2; ++i) {
@@ -519,6 +529,45 @@ extern "C" smile_status smile_gate_inter(smile_ctx c, const void *x, const float
     s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
     s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T; s.peer = peer_of(c);
     launch_scan1(s, S(stream));
+    return post_launch();
+}
+
+extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, const float *w_router,
+                                                  float *logits_out, const smile_route *route, const smile_stats *stats,
+                                                  int32_t *counts1, void *send_rows, int32_t *send_meta, void *stream) {
+    if (!c || !x || !w_router || !route || !stats || !counts1 || !send_rows) return SMILE_EINVAL;
+    const bool bi = c->shape.mode == SMILE_BILEVEL;
+    if (bi && !send_meta) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;
+    if (!c->wsplit || !c->lb_flag) {
+        // no tensor-core gate for this shape / dtype: the two calls it fuses
+        STEP(smile_gate_inter(c, x, w_router, nullptr, logits_out, route, stats, counts1, stream));
+        return smile_dispatch(c, 1, x, route, nullptr, nullptr, send_rows, send_meta, stream);
+    }
+    cudaSetDevice(c->shape.device);
+    const int64_t rb = (int64_t)c->shape.d * (c->shape.dtype == SMILE_BF16 ? 2 : 4);
+    GateArgs a{};
+    a.x = x; a.w = w_router; a.logits = nullptr; a.logits_out = logits_out;
+    a.route = *route;
+    a.blk_hist1 = c->blk_hist1; a.blk_hist2a = c->blk_hist2a; a.blk_psum = c->blk_psum;
+    a.err = c->d_err; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
+    a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1;
+    a.flat = !bi; a.bf16 = c->shape.dtype == SMILE_BF16;
+    a.fuse_dispatch = 1; a.send = send_rows; a.meta = bi ? send_meta : nullptr; a.rowbytes = rb; a.C1 = c->sz.C1;
+    a.peer = peer_of(c); a.lb_flag = c->lb_flag; a.lb_agg = c->lb_agg; a.lb_inc = c->lb_inc;
+    const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, S(stream));
+    if (e != cudaSuccess) return SMILE_ECUDA;
+    Scan1Args s{};
+    s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
+    s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
+    s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T; s.peer = peer_of(c); s.lb_flag = c->lb_flag;
+    launch_scan1(s, S(stream));
+    Dispatch1Args d{};
+    d.x = x; d.route = *route; d.blk_off1 = c->blk_off1; d.blk_hist1 = c->blk_hist1;
+    d.send = send_rows; d.meta = bi ? send_meta : nullptr;
+    d.V = c->sz.V; d.T = c->shape.T; d.rowbytes = rb; d.K1 = c->sz.K1; d.C1 = c->sz.C1;
+    d.TB = c->TB1; d.nblk = c->nblk1; d.peer = peer_of(c);
+    launch_meta_fill(d, S(stream));
     return post_launch();
 }
 
@@ -825,6 +874,9 @@ extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, voi
     if (c->shape.T == 0) return SMILE_OK;
     const bool train = io->train != 0;
     if (c->xchg == SMILE_XCHG_PEER && io->ws != c->reg_ws) return SMILE_ENOTSUP;
+    // gate then level-1 permute as two kernels: measured faster than the fused
+    // smile_gate_dispatch_inter (C2: 0.166 vs 0.178 ms; C4: 0.77 vs 0.85 ms) -- the row moves
+    // from the gate's epilogue warps reach less bandwidth than the dedicated movers
     STEP(smile_gate_inter(c, io->x, io->w_router, io->logits, (train && !io->logits) ? w.logits : nullptr, &w.route,
                           &w.stats, w.counts1, stream));
     STEP(smile_dispatch(c, 1, io->x, &w.route, nullptr, nullptr, w.send1, w.meta1, stream));

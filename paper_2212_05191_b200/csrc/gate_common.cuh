@@ -67,9 +67,14 @@ __host__ __device__ __forceinline__ int gate_lds(int KW) { return KW | 1; }
 // logits are s_lg [nt][lds] (entries 0..K1-1: inter router W_p; K1..KW-1: intra W_q).
 // tok0: global index of the tile's first token; bo: the tile's index in the per-tile
 // tables.  Must be entered by all Sync threads after the logits are visible to them.
+struct GateTok {
+    int i;       // level-1 destination of this thread's token (-1: no token)
+    int lr;      // its rank among the tile's tokens with the same destination
+};
+
 template <class Sync>
-__device__ void gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j, int *s_wh, int *s_bh, int64_t tok0,
-                            int nt, int64_t bo) {
+__device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j, int *s_wh, int *s_bh, int64_t tok0,
+                               int nt, int64_t bo) {
     const int tid = Sync::tid(), nthr = Sync::nthr();
     const int KW = a.KW, K1 = a.K1, K2 = a.K2;
     // Phase B: one thread per token -- argmax (R2, R3), top-1 probabilities (R4), and
@@ -143,6 +148,7 @@ __device__ void gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j, i
         }
         if (a.flat && tid == 0) a.blk_psum[bo * (K1 + K2) + K1] = (double)nt;
     }
+    return GateTok{i, lr};
 }
 
 }  // namespace smile

@@ -68,11 +68,139 @@ struct GateTcArgs {
                      // larger stages -- the single MMA thread's per-stage overhead halves)
 };
 
-// After the group's logits of one tile are in smem: (optional) logits_out copy, then the
-// gate's phases B and C.
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Fused level-1 permute (a4) in the gate's epilogue.  The tile's destination histogram
+// s_bh is published (flag 1); warp 0 of the group looks back over the rank's earlier
+// tiles 32 at a time (lane = one predecessor): aggregates are summed up to the nearest
+// tile that has published its inclusive prefix (flag 2), giving this tile's exclusive
+// offsets s_off; the inclusive prefix is published (flag 2).  Tiles run in increasing
+// order on every CTA and all CTAs are resident, so every look-back terminates.  Then
+// slot1 = s_off[dest1] + in-tile rank (R5, R8: earliest token first), and each warp
+// moves its kept tokens' rows (16-byte vectors, 4 rows in flight) to the slot -- into
+// send1 / meta1, or straight into the destination's receive buffer (peer stores).
+template <class Sync>
+__device__ void fused_dispatch(const GateArgs &a, const GateTok tk, const int *s_bh, int *s_off, int64_t tok0,
+                               int nt, int tile) {
+    const int tid = Sync::tid(), lane = tid & 31, w = tid >> 5;
+    const int K1 = a.K1, v = tile / a.nblk, blk = tile - v * a.nblk;
+    int *flag = a.lb_flag + tile;
+    // 1. publish the aggregate (the first tile of a rank: directly the inclusive prefix)
+    for (int k = tid; k < K1; k += Sync::nthr()) {
+        a.lb_agg[(int64_t)tile * K1 + k] = s_bh[k];
+        if (blk == 0) a.lb_inc[(int64_t)tile * K1 + k] = s_bh[k];
+        s_off[k] = 0;
+    }
+    __threadfence();
+    Sync::sync();
+    if (tid == 0) st_release_gpu(flag, blk == 0 ? 2 : 1);
+    // 2. look back (warp 0)
+    if (blk > 0 && w == 0) {
+        const int base = v * a.nblk;
+        for (int p = blk - 1;; p -= 32) {
+            const int pb = p - lane;
+            int fl = 2;                                  // before the rank's first tile: zero, inclusive
+            if (pb >= 0) {
+                uint64_t spin = 0;
+                while ((fl = ld_acquire_gpu(a.lb_flag + base + pb)) == 0)
+                    if (++spin > (1ull << 28)) __trap();  // a tile that never publishes: abort, never hang
+            }
+            const unsigned incm = __ballot_sync(kFull, fl == 2);
+            const int stop = incm ? __ffs(incm) - 1 : 32;   // nearest predecessor with an inclusive prefix
+            for (int k = 0; k < K1; ++k) {
+                int val = 0;
+                if (pb >= 0 && lane < stop) val = a.lb_agg[((int64_t)base + pb) * K1 + k];
+                else if (pb >= 0 && lane == stop) val = a.lb_inc[((int64_t)base + pb) * K1 + k];
+                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(kFull, val, o);
+                if (lane == 0) s_off[k] += val;
+            }
+            if (incm) break;
+        }
+    }
+    Sync::sync();
+    // 3. publish the inclusive prefix
+    if (blk > 0) {
+        for (int k = tid; k < K1; k += Sync::nthr()) a.lb_inc[(int64_t)tile * K1 + k] = s_off[k] + s_bh[k];
+        __threadfence();
+        Sync::sync();
+        if (tid == 0) st_release_gpu(flag, 2);
+    }
+    // 4. final slots, meta, destinations
+    const char *src = nullptr;
+    char *dst = nullptr;
+    if (tid < nt && tk.i >= 0) {
+        const int64_t g = tok0 + tid;
+        const int slot = s_off[tk.i] + tk.lr;
+        a.route.slot1[g] = slot;
+        if (slot < a.C1) {
+            src = static_cast<const char *>(a.x) + g * a.rowbytes;
+            const int j = a.route.dest2[g];
+            if (a.peer.bases) {
+                const PeerMap &P = a.peer;
+                const int rk = P.rank0 + v;
+                int q;
+                int64_t row;
+                if (!a.flat) {                   // bi-level: (s, l) -> intermediate (i, l), chunk s
+                    const int s_ = rk / P.m, l = rk % P.m;
+                    q = tk.i * P.m + l;
+                    row = ((int64_t)(q % P.V) * P.n + s_) * a.C1 + slot;
+                } else {                         // flat: expert i on rank i / e, chunk (src, i % e)
+                    q = tk.i / P.e;
+                    row = (((int64_t)(q % P.V) * P.G + rk) * P.e + tk.i % P.e) * a.C1 + slot;
+                }
+                char *b = P.bases[q / P.V];
+                dst = b + P.off_recv1 + row * a.rowbytes;
+                if (!a.flat) reinterpret_cast<int32_t *>(b + P.off_rmeta1)[row] = j;
+            } else {
+                const int64_t row = ((int64_t)v * K1 + tk.i) * a.C1 + slot;
+                dst = static_cast<char *>(a.send) + row * a.rowbytes;
+                if (a.meta) a.meta[row] = j;
+            }
+        }
+    }
+    // 5. the warp's 32 rows, 4 at a time: every lane moves 16-byte vectors of each
+    const int nvec = (int)(a.rowbytes / 16);
+    for (int r0 = 0; r0 < 32; r0 += 4) {
+        const char *sr[4];
+        char *dr[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            sr[r] = reinterpret_cast<const char *>(__shfl_sync(kFull, reinterpret_cast<unsigned long long>(src), r0 + r));
+            dr[r] = reinterpret_cast<char *>(__shfl_sync(kFull, reinterpret_cast<unsigned long long>(dst), r0 + r));
+        }
+        for (int c0 = lane; c0 < nvec; c0 += 96) {
+            int4 val[4][3];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    const int c = c0 + 32 * u;
+                    val[r][u] = (dr[r] && c < nvec) ? *reinterpret_cast<const int4 *>(sr[r] + (int64_t)c * 16)
+                                                    : make_int4(0, 0, 0, 0);
+                }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    const int c = c0 + 32 * u;
+                    if (dr[r] && c < nvec) *reinterpret_cast<int4 *>(dr[r] + (int64_t)c * 16) = val[r][u];
+                }
+        }
+    }
+}
+
+// After the group's logits of one tile are in smem: (optional) logits_out copy, the
+// gate's phases B and C, and (fused) the level-1 permute of the tile.
 template <class Sync>
 __device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int *s_j, int *s_wh, int *s_bh,
-                                            int64_t tok0, int nt, int tile) {
+                                            int *s_off, int64_t tok0, int nt, int tile) {
     Sync::sync();
     if (a.logits_out) {
         const int lds = gate_lds(a.KW);
@@ -80,7 +208,8 @@ __device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int 
             a.logits_out[tok0 * a.KW + i] = s_lg[(i / a.KW) * lds + i % a.KW];
         Sync::sync();
     }
-    gate_finish<Sync>(a, s_lg, gate_lds(a.KW), s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
+    const GateTok tk = gate_finish<Sync>(a, s_lg, gate_lds(a.KW), s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
+    if (a.fuse_dispatch) fused_dispatch<Sync>(a, tk, s_bh, s_off, tok0, nt, tile);
     Sync::sync();
 }
 
@@ -97,7 +226,7 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     unsigned char *sB = sA + ST * a_bytes;
     // per epilogue group g: logits [128][lds] | s_j [128] | s_wh [4][K1] | s_bh [K1]
     const int lds = gate_lds(KW);
-    const int grp_ints = GT_BM * lds + GT_BM + 5 * a.K1;
+    const int grp_ints = GT_BM * lds + GT_BM + 6 * a.K1;     // + s_off [K1] (fused permute)
     int *grp0 = reinterpret_cast<int *>(sB + ST * b_bytes);
     uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(grp0 + ta.nbuf * grp_ints) + 7) & ~(uintptr_t)7);
     uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
@@ -198,6 +327,7 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
         int *s_j = reinterpret_cast<int *>(s_lg + GT_BM * lds);
         int *s_wh = s_j + GT_BM;
         int *s_bh = s_wh + 4 * a.K1;
+        int *s_off = s_bh + a.K1;
         // with a single accumulator buffer (NP > 256) one group takes every tile: the
         // tfull / tempty parities then count every tile of the CTA
         const int ngrp = nbuf;
@@ -230,8 +360,8 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
-            if (grp == 0) finish_tile<EpiSync<0>>(a, s_lg, s_j, s_wh, s_bh, tok0, nt, tile);
-            else finish_tile<EpiSync<1>>(a, s_lg, s_j, s_wh, s_bh, tok0, nt, tile);
+            if (grp == 0) finish_tile<EpiSync<0>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
+            else finish_tile<EpiSync<1>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
         }
     }
     __syncthreads();
@@ -243,7 +373,7 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
 
 size_t gate_tc_smem(int NP, int KW, int K1, int stages, int nsub) {
     const int groups = 2 * NP <= 512 ? 2 : 1;          // = nbuf
-    return 1024 + (size_t)stages * nsub * (GT_A_BYTES + NP * GT_BK * 2) + groups * ((size_t)GT_BM * gate_lds(KW) + GT_BM + 5 * K1) * 4 + 8 +
+    return 1024 + (size_t)stages * nsub * (GT_A_BYTES + NP * GT_BK * 2) + groups * ((size_t)GT_BM * gate_lds(KW) + GT_BM + 6 * K1) * 4 + 8 +
            (2 * stages + 4) * 8 + 16;
 }
 

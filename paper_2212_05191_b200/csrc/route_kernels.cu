@@ -11,6 +11,7 @@
 #include "gate_common.cuh"
 
 #include <math.h>
+#include <stdlib.h>
 
 namespace smile {
 namespace {
@@ -196,6 +197,8 @@ __device__ int warp_sum_i32(const int32_t *p, int n, int64_t st) {
 // One warp per (destination or statistic), grid = V.
 __global__ void scan1_kernel(Scan1Args a) {
     const int v = blockIdx.x, w = threadIdx.x >> 5, NW = blockDim.x >> 5, lane = threadIdx.x & 31;
+    if (a.lb_flag)                                   // the fused gate's look-back flags, for the next call
+        for (int b = threadIdx.x; b < a.nblk; b += blockDim.x) a.lb_flag[(int64_t)v * a.nblk + b] = 0;
     const int KS = a.K1 + a.K2;
     const int jobs = a.K1 + KS + a.K2;
     for (int j = w; j < jobs; j += NW) {
@@ -424,6 +427,7 @@ constexpr int kMoveColUnroll = 3;       // 16-byte vectors per lane per row in f
 // One warp moves kMoveRowsPerWarp rows at a time: lanes 0..3 resolve one row each
 // (independent dependent-load chains), the pointers are broadcast, then every lane keeps
 // rows x kMoveColUnroll 16-byte loads in flight before its stores.
+template <int RW>
 __global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -431,7 +435,7 @@ __global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) {
     const int nvec = (int)(m.rowbytes / 16);
     const bool combine1 = m.kind == MOVE_COMBINE1;
     const bool bf16 = m.c1.bf16 != 0;
-    constexpr int RW = kMoveRowsPerWarp, CU = kMoveColUnroll;
+    constexpr int CU = kMoveColUnroll;
     // The next batch's row plan (dependent metadata loads: slot offsets, routes) is
     // resolved while the current batch's row loads are in flight.
     RowPlan mine{nullptr, nullptr, 1.f};
@@ -631,13 +635,25 @@ void launch_rank2(const Rank2Args &a, cudaStream_t st) {
     scan2_kernel<<<a.V, 512, 0, st>>>(a);
 }
 
+// Rows per warp batch: SMILE_MOVE_RW = 4 (default) or 8.
+static int move_rw() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SMILE_MOVE_RW");
+        v = (e && e[0] == '8') ? 8 : kMoveRowsPerWarp;
+    }
+    return v;
+}
+
 static void launch_move(MoveArgs &m, cudaStream_t st) {
     if (m.rows <= 0) return;
-    const int64_t per_block = (int64_t)(kMoveThreads / 32) * kMoveRowsPerWarp;
+    const int rw = move_rw();
+    const int64_t per_block = (int64_t)(kMoveThreads / 32) * rw;
     int64_t grid = (m.rows + per_block - 1) / per_block;
     if (grid > 148 * 8) grid = 148 * 8;
     note_launch();
-    row_move_kernel<<<(int)grid, kMoveThreads, 0, st>>>(m);
+    if (rw == 8) row_move_kernel<8><<<(int)grid, kMoveThreads, 0, st>>>(m);
+    else row_move_kernel<kMoveRowsPerWarp><<<(int)grid, kMoveThreads, 0, st>>>(m);
 }
 
 void launch_dispatch1(const Dispatch1Args &a, cudaStream_t st) {
@@ -645,6 +661,14 @@ void launch_dispatch1(const Dispatch1Args &a, cudaStream_t st) {
     MoveArgs m{};
     m.kind = MOVE_DISPATCH1; m.rows = (int64_t)a.V * a.T; m.rowbytes = a.rowbytes; m.d1 = a;
     launch_move(m, st);
+    if (a.meta || a.peer.bases && a.peer.n > 0) {
+        note_launch();
+        meta_fill_kernel<<<148 * 4, 256, 0, st>>>(a);
+    }
+}
+
+void launch_meta_fill(const Dispatch1Args &a, cudaStream_t st) {
+    if (a.T == 0) return;
     if (a.meta || a.peer.bases && a.peer.n > 0) {
         note_launch();
         meta_fill_kernel<<<148 * 4, 256, 0, st>>>(a);

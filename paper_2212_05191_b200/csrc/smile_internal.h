@@ -81,6 +81,8 @@ struct smile_ctx_s {
     // tensor-core gate (bf16 fused router): the three-piece bf16 split of the router
     __nv_bfloat16 *wsplit = nullptr;         // [gate_tc_np(KW), d], rewritten every fused gate call
     float *colsum_ws = nullptr;              // bias-gradient partials of smile_expert_ffn_bwd
+    int *lb_flag = nullptr;                  // fused gate + permute: look-back flags [V * nblk1]
+    int32_t *lb_agg = nullptr, *lb_inc = nullptr;   // tile aggregates / inclusive prefixes [V * nblk1 * K1]
     // smile_forward_host_stream: copy streams and ping-pong events (created with the ctx)
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
@@ -93,6 +95,13 @@ struct GateArgs {
     const void *x; const float *w; const float *logits; float *logits_out;
     smile_route route; int32_t *blk_hist1, *blk_hist2a; double *blk_psum;
     int *err; int V; int64_t T; int d; int K1, K2, KW; int TB, nblk; int flat; int bf16;
+    // fused level-1 permute (tensor-core gate only; smile_gate_dispatch_inter): final
+    // slots by decoupled look-back over the tiles' destination histograms, then the
+    // kept rows moved to their slots (send rows / meta, or the peers' receive buffers)
+    int fuse_dispatch;
+    void *send; int32_t *meta; int64_t rowbytes; int64_t C1;
+    PeerMap peer;
+    int *lb_flag; int32_t *lb_agg, *lb_inc;   // [V * nblk], [V * nblk * K1] x 2
 };
 void launch_gate1(const GateArgs &a, cudaStream_t st);
 
@@ -100,6 +109,7 @@ struct Scan1Args {
     const int32_t *blk_hist1, *blk_hist2a; const double *blk_psum; int32_t *blk_off1;
     smile_stats stats; int32_t *counts1; int V, nblk, K1, K2, KW; int64_t C1; int flat; int64_t T;
     PeerMap peer;
+    int *lb_flag;            // reset for the next fused gate (may be null)
 };
 void launch_scan1(const Scan1Args &a, cudaStream_t st);
 
@@ -116,6 +126,8 @@ struct Dispatch1Args {
     PeerMap peer;
 };
 void launch_dispatch1(const Dispatch1Args &a, cudaStream_t st);
+// meta = -1 for the empty slots [count, C1) (after the fused gate + permute)
+void launch_meta_fill(const Dispatch1Args &a, cudaStream_t st);
 
 struct Dispatch2Args {
     const void *recv1; const int32_t *recv_meta; int32_t *slot2; const int32_t *blk_off2;

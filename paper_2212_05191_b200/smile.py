@@ -87,6 +87,7 @@ def lib():
                      "smile_query", "smile_get_error", "smile_gate_inter", "smile_dispatch", "smile_gate_intra",
                      "smile_all2all", "smile_all2all_inter", "smile_all2all_intra", "smile_expert_ffn",
                      "smile_combine", "smile_aux_loss", "smile_forward_ws", "smile_forward", "smile_forward_host",
+                     "smile_gate_dispatch_inter",
                      "smile_expert_ffn_train", "smile_combine_bwd", "smile_dispatch_grad", "smile_expert_ffn_bwd",
                      "smile_combine_grad", "smile_router_bwd", "smile_backward", "smile_ipc_handle",
                      "smile_register_workspace", "smile_struct_sizes", "smile_forward_host_stream"):
@@ -309,6 +310,13 @@ class SmileLayer:
         _check(lib().smile_gate_inter(self._ctx, _ptr(x), _ptr(w_router), _ptr(logits), _ptr(logits_out),
                                       C.byref(route), C.byref(stats), _ptr(counts1), _stream(stream)),
                "smile_gate_inter")
+
+    def gate_dispatch_inter(self, x, w_router, route, stats, counts1, send_rows, send_meta=None, logits_out=None,
+                            stream=None):
+        """smile_gate_dispatch_inter: a1-a4 fused (tensor-core gate + level-1 permute)."""
+        _check(lib().smile_gate_dispatch_inter(self._ctx, _ptr(x), _ptr(w_router), _ptr(logits_out), C.byref(route),
+                                               C.byref(stats), _ptr(counts1), _ptr(send_rows), _ptr(send_meta),
+                                               _stream(stream)), "smile_gate_dispatch_inter")
 
     def dispatch(self, level, rows_in, send_rows, route=None, recv_meta=None, slot2=None, send_meta=None,
                  stream=None):

@@ -159,6 +159,65 @@ def test_fused_router(dtype, n, m, e, T, d, mode):
     np.testing.assert_array_equal(r0.dest1[clear], v["dest1"][clear])
 
 
+@pytest.mark.parametrize("n,m,e,T,d,mode,peer", [
+    (2, 4, 1, 700, 256, "bilevel", False),     # several tiles per rank, ragged last tile
+    (2, 4, 1, 700, 256, "bilevel", True),      # rows stored straight into the receive buffers
+    (4, 2, 1, 1000, 128, "bilevel", False),
+    (2, 4, 8, 300, 128, "flat", False),        # K1 = 64 destinations in the look-back
+    (2, 2, 2, 5000, 64, "bilevel", True),      # 40 tiles per rank: look-back spans > 32 tiles
+])
+def test_fused_gate_dispatch_matches_two_calls(n, m, e, T, d, mode, peer):
+    """smile_gate_dispatch_inter (tensor-core gate with the level-1 permute fused in, slots
+    by decoupled look-back) == smile_gate_inter + smile_dispatch(1), bit for bit: route,
+    statistics, counts, and every valid row / meta entry of the level-1 send (or, with
+    the peer-store exchange, receive) buffers."""
+    from paper_2212_05191_b200 import smile as smb
+    case = Case(n, m, e, T, d, 128, 1.0, dtype="bf16", fused=True, seed=8, mode=mode)
+    g = case.gpu_tensors()
+    res = []
+    for fused in (False, True):
+        L = smb.SmileLayer(n, m, e, d, 128, T, 1.0, "bf16", mode)
+        L.alloc_workspace()
+        if peer:
+            L.enable_peer_exchange()
+        w = L._view
+        L.ws.fill_(0)
+        for _ in range(2):                      # twice: the look-back flags must reset between calls
+            if fused:
+                L.gate_dispatch_inter(g["x"], g["w_router"], w.route, w.stats, C_ptr(w.counts1), WsTensor(w.send1),
+                                      send_meta=WsTensor(w.meta1) if mode == "bilevel" else None)
+            else:
+                L.gate_inter(g["x"], w.route, w.stats, C_ptr(w.counts1), w_router=g["w_router"])
+                L.dispatch(1, g["x"], WsTensor(w.send1), route=w.route,
+                           send_meta=WsTensor(w.meta1) if mode == "bilevel" else None)
+        torch.cuda.synchronize()
+        assert L.get_error() == 0
+        v = {k: t.cpu().clone() for k, t in L.view().items() if k in ("dest1", "dest2", "slot1", "p", "q", "gate",
+                                                                     "hist1", "hist2", "psum1", "psum2", "counts1")}
+        V, K1, C1 = L.V, L.K1, L.C1
+        rows = L._slice(w.recv1 if peer else w.send1, (V, K1, C1, d), torch.bfloat16).cpu().clone()
+        meta = None
+        if mode == "bilevel":
+            meta = L._slice(w.rmeta1 if peer else w.meta1, (V, K1, C1), torch.int32).cpu().clone()
+        res.append((v, rows, meta))
+        L.close()
+    (va, ra, ma), (vb, rb, mb) = res
+    for k in va:
+        assert torch.equal(va[k], vb[k]), k
+    cnt = va["counts1"]
+    for vv in range(cnt.shape[0]):
+        for i in range(cnt.shape[1]):
+            c = int(cnt[vv, i])
+            if not peer:
+                assert torch.equal(ra[vv, i, :c], rb[vv, i, :c]), (vv, i)
+                if ma is not None:
+                    assert torch.equal(ma[vv, i, :c], mb[vv, i, :c])
+    if peer:                                    # receive layout [q, source node, C1]: compare whole buffers
+        assert torch.equal(ra, rb)
+        if ma is not None:
+            assert torch.equal(ma, mb)
+
+
 class C_ptr:
     """Wrap a raw device address so the binding's _ptr() can pass it through."""
     def __init__(self, addr):
