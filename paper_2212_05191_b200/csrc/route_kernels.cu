@@ -645,12 +645,23 @@ static int move_rw() {
     return v;
 }
 
+// Grid cap of the movers in blocks per SM: SMILE_MOVE_GRIDMUL (default 8).
+static int move_gridmul() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SMILE_MOVE_GRIDMUL");
+        v = e ? atoi(e) : 8;
+        if (v < 1) v = 8;
+    }
+    return v;
+}
+
 static void launch_move(MoveArgs &m, cudaStream_t st) {
     if (m.rows <= 0) return;
     const int rw = move_rw();
     const int64_t per_block = (int64_t)(kMoveThreads / 32) * rw;
     int64_t grid = (m.rows + per_block - 1) / per_block;
-    if (grid > 148 * 8) grid = 148 * 8;
+    if (grid > 148 * move_gridmul()) grid = 148 * move_gridmul();
     note_launch();
     if (rw == 8) row_move_kernel<8><<<(int)grid, kMoveThreads, 0, st>>>(m);
     else row_move_kernel<kMoveRowsPerWarp><<<(int)grid, kMoveThreads, 0, st>>>(m);
