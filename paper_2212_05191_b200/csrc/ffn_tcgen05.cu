@@ -53,6 +53,7 @@ struct TcArgs {
     const __nv_bfloat16 *aux;  // EPI_DGELU: the saved pre-activation A1 [rows_total, N]
     int stages;                // smem pipeline depth
     int tma_store;             // 1: full 32 x 32 boxes leave through smem + TMA; 0: st.global from registers
+    int box64;                 // 1: 32 x 64 boxes (two chunks per TMA store; every warp owns 2k chunks)
     int *err;
 };
 
@@ -195,7 +196,8 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     const int b_stage_bytes = B_BYTES_MAX / CG;
     unsigned char *sB = sA + STAGES * A_BYTES;
     unsigned char *sOut = sB + STAGES * b_stage_bytes;                // EPI_WARPS x nbox x 2 KB
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sOut + (a.tma_store ? nbox * EPI_WARPS * OUT_BOX_BYTES : 0));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(
+        sOut + (a.tma_store ? nbox * EPI_WARPS * OUT_BOX_BYTES * (a.box64 ? 2 : 1) : 0));
     uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
     int *s_warp = reinterpret_cast<int *>(tmem_holder + 4);
@@ -353,7 +355,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         const int nch = a.BN / 32;
         const int c_beg = (h * nch) / 4, c_end = ((h + 1) * nch) / 4;
         int it = 0;
-        unsigned char *box = sOut + (warp - 4) * nbox * OUT_BOX_BYTES;
+        unsigned char *box = sOut + (warp - 4) * nbox * OUT_BOX_BYTES * (a.box64 ? 2 : 1);
         for (int tile = cid; tile < total; tile += ncl, ++it) {
             const TileInfo t = tile_info<CG, NPAIR>(a, s_pref, tile, ntn, rank, pair);
             const int acc = it & 1;
@@ -424,7 +426,30 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     __nv_bfloat162 hh = __floats2bfloat162_rn(y0, y1);
                     pw[i] = *reinterpret_cast<uint32_t *>(&hh);
                 }
-                if (full_box && a.tma_store) {
+                if (full_box && a.tma_store && a.box64) {
+                    // 32 x 64 box (SWIZZLE_128B: 16-byte unit j of row r at j ^ (r & 7)) over
+                    // two consecutive chunks: the first waits for the box's previous store,
+                    // the second fences and issues one TMA store (128-byte row segments)
+                    const int hf = (c - c_beg) & 1;
+                    if (hf == 0) {
+                        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        __syncwarp();
+                    }
+                    uint4 *srow = reinterpret_cast<uint4 *>(box + lane * 128);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) srow[(4 * hf + j) ^ (lane & 7)] = pk[j];
+                    if (hf == 1) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) {
+                            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                             reinterpret_cast<uint64_t>(&mapD)),
+                                         "r"((int)dcol0 + (c - 1) * 32), "r"((int)d_row), "r"(smem_u32(box))
+                                         : "memory");
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
+                    }
+                } else if (full_box && a.tma_store) {
                     // the box's previous store has finished reading smem; then the 32 x 32 box
                     // in the SWIZZLE_64B layout (16-byte chunk j of row r at j ^ ((r >> 1) & 3))
                     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -492,8 +517,9 @@ int pick_bn(int N) {
     return 0;
 }
 
-size_t smem_bytes(int CG, int stages, int nbox, int tma_store) {
-    return 1024 + stages * (A_BYTES + B_BYTES_MAX / CG) + (tma_store ? nbox * EPI_WARPS * OUT_BOX_BYTES : 0) +
+size_t smem_bytes(int CG, int stages, int nbox, int tma_store, int box64 = 0) {
+    return 1024 + stages * (A_BYTES + B_BYTES_MAX / CG) +
+           (tma_store ? nbox * EPI_WARPS * OUT_BOX_BYTES * (box64 ? 2 : 1) : 0) +
            (2 * stages + 4) * 8 +
            16 + 32 * 4 + (MAXSEG + 1) * 4 + MAXSEG * 4;
 }
@@ -513,9 +539,9 @@ int pick_tma_store() {
     return v;
 }
 
-int pick_stages(int CG, int nbox, int tma_store) {
+int pick_stages(int CG, int nbox, int tma_store, int box64) {
     int st = 8;
-    while (st > 2 && smem_bytes(CG, st, nbox, tma_store) > kSmemLimit) --st;
+    while (st > 2 && smem_bytes(CG, st, nbox, tma_store, box64) > kSmemLimit) --st;
     return st;
 }
 
@@ -605,6 +631,8 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     if (!make_map(&mA128, A, rows_total, K, BM)) return cudaErrorNotSupported;     // 128-row tile box
     if (!make_map(&mB, B, (int64_t)NE * N, K, BN / (CG * NPAIR))) return cudaErrorNotSupported;
     if (!make_map(&mD, D, rows_total, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorNotSupported;
+    CUtensorMap mD64;
+    if (!make_map(&mD64, D, rows_total, N, 32, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorNotSupported;
     mD2 = mD;
     if (D2 && !make_map(&mD2, D2, rows_total, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorNotSupported;
     TcArgs a;
@@ -615,10 +643,22 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     a.mode = mode; a.aux = reinterpret_cast<const __nv_bfloat16 *>(aux);
     const int nbox = mode == EPI_BIAS_SAVE ? 2 : 1;
     a.tma_store = pick_tma_store();
-    a.stages = pick_stages(CG, nbox, a.tma_store);
+    if (nbox == 2) {                      // training forward (H and A1): SMILE_FFN_SAVE_TMA=0 -> st.global
+        const char *e = getenv("SMILE_FFN_SAVE_TMA");
+        if (e && e[0] == '0') a.tma_store = 0;
+    }
+    // 32 x 64 output boxes for the GELU GEMM (the one that writes H, 4x the bytes of Y)
+    // when every epilogue warp owns an even number of 32-column chunks
+    {
+        const char *e = getenv("SMILE_FFN_BOX64");
+        const bool want = e ? e[0] == '1' : false;
+        a.box64 = (want && a.tma_store && nbox == 1 && gelu && (BN / 32) % 8 == 0) ? 1 : 0;
+    }
+    a.stages = pick_stages(CG, nbox, a.tma_store, a.box64);
     a.err = nullptr;
-    const size_t smem = smem_bytes(CG, a.stages, nbox, a.tma_store);
+    const size_t smem = smem_bytes(CG, a.stages, nbox, a.tma_store, a.box64);
     const bool dg = mode == EPI_DGELU;
+    if (a.box64) mD = mD64;                   // the output map with 32 x 64 SWIZZLE_128B boxes
     if (CG == 2 && NPAIR == 2)
         return dg ? launch_tc<2, 2, true>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)
                   : launch_tc<2, 2, false>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
