@@ -28,6 +28,7 @@
 #include "gate_common.cuh"
 #include "tc_util.cuh"
 
+#include <stdlib.h>
 #include <string.h>
 
 namespace smile {
@@ -66,6 +67,9 @@ struct GateTcArgs {
     int ntiles;
     int nsub;        // 64-column sub-blocks per pipeline stage (2 when d % 128 == 0: fewer,
                      // larger stages -- the single MMA thread's per-stage overhead halves)
+    int resident_b;  // 1: every CTA builds the split router (NP x d bf16, SWIZZLE_128B K-major)
+                     // in its own smem at start from the fp32 W -- no split kernel, and the
+                     // pipeline stages carry x only
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int *p) {
@@ -220,17 +224,20 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     const int NP = ta.NP, ST = ta.stages, KW = a.KW;
     const int nsub = ta.nsub;
     const int a_bytes = nsub * GT_A_BYTES;                 // per stage
-    const int b_bytes = nsub * NP * GT_BK * 2;
+    const bool resb = ta.resident_b != 0;
+    const int b_bytes = resb ? 0 : nsub * NP * GT_BK * 2;     // per stage (streamed split router)
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;
-    unsigned char *sB = sA + ST * a_bytes;
+    unsigned char *sB = sA + ST * a_bytes;                   // resident: [d / 64][NP rows][128 B]
+    const int b_region = resb ? NP * a.d * 2 : ST * b_bytes;
     // per epilogue group g: logits [128][lds] | s_j [128] | s_wh [4][K1] | s_bh [K1]
     const int lds = gate_lds(KW);
     const int grp_ints = GT_BM * lds + GT_BM + 6 * a.K1;     // + s_off [K1] (fused permute)
-    int *grp0 = reinterpret_cast<int *>(sB + ST * b_bytes);
+    int *grp0 = reinterpret_cast<int *>(sB + b_region);
     uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(grp0 + ta.nbuf * grp_ints) + 7) & ~(uintptr_t)7);
     uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 4);
+    uint64_t *b_ready = bars + 2 * ST + 4;                     // resident split router built
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 5);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -242,6 +249,7 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
             mbar_init(smem_u32(&tfull[s]), 1);
             mbar_init(smem_u32(&tempty[s]), 4);
         }
+        mbar_init(smem_u32(b_ready), (GT_THREADS - 96) / 32);        // one arrive per building warp
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0 && lane == 0) {
@@ -262,6 +270,38 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     const int nchunk_n = NP > 256 ? 2 : 1;
     const int NPc = NP / nchunk_n;                     // N of one MMA
 
+    if (resb && warp >= 3) {
+        // warps 3.. build the exact 3-piece bf16 split of W (row 3k + p = piece p of W[k];
+        // rows >= 3 KW zero) in the canonical SWIZZLE_128B K-major layout the MMA reads
+        // (per 64-column block: rows of 128 B, 16-byte unit u of row r at u ^ (r & 7)),
+        // while the producer already streams x; the MMA thread waits on b_ready.
+        __nv_bfloat16 *bs = reinterpret_cast<__nv_bfloat16 *>(sB);
+        const int nthr = GT_THREADS - 96, t0 = threadIdx.x - 96;
+        const int total = NP * a.d;
+        for (int i0 = t0; i0 < total; i0 += nthr * 4) {
+            float wv[4];
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+                const int idx = i0 + z * nthr;
+                const int r = idx / a.d, c = idx - r * a.d, k = r / 3;
+                wv[z] = (idx < total && k < KW) ? __ldg(a.w + (int64_t)k * a.d + c) : 0.f;
+            }
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+                const int idx = i0 + z * nthr;
+                if (idx >= total) break;
+                const int r = idx / a.d, c = idx - r * a.d, k = r / 3, p = r - 3 * k;
+                float rem = wv[z];
+                for (int q = 0; q < p; ++q) rem -= __bfloat162float(__float2bfloat16_rn(rem));
+                const int kb = c >> 6, u = (c & 63) >> 3;
+                bs[((size_t)kb * NP + r) * 64 + ((u ^ (r & 7)) << 3) + (c & 7)] = __float2bfloat16_rn(k < KW ? rem : 0.f);
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(b_ready));
+    }
+
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer ----------------
@@ -277,9 +317,10 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
                     for (int u = 0; u < nsub; ++u) {
                         const int col = (kb * nsub + u) * GT_BK;
                         tma_load_2d(smem_u32(sA + stage * a_bytes + u * GT_A_BYTES), &mapX, col, row0, fb);
-                        for (int h = 0; h < nchunk_n; ++h)
-                            tma_load_2d(smem_u32(sB + stage * b_bytes + u * NP * 128 + h * NPc * 128), &mapW, col,
-                                        h * NPc, fb);
+                        if (!resb)
+                            for (int h = 0; h < nchunk_n; ++h)
+                                tma_load_2d(smem_u32(sB + stage * b_bytes + u * NP * 128 + h * NPc * 128), &mapW,
+                                            col, h * NPc, fb);
                     }
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
@@ -288,6 +329,7 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     } else if (warp == 1) {
         if (lane == 0) {
             // ---------------- MMA issuer ----------------
+            if (resb) mbar_wait(smem_u32(b_ready), 0);
             const uint32_t idesc = make_idesc(GT_BM, NPc);
             int stage = 0;
             uint32_t phase = 0;
@@ -306,8 +348,9 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
 #pragma unroll
                         for (int k = 0; k < GT_BK / 16; ++k)
                             for (int h = 0; h < nchunk_n; ++h) {
-                                const uint64_t bd =
-                                    sw128_desc(smem_u32(sB + stage * b_bytes + u * NP * 128 + h * NPc * 128));
+                                const uint64_t bd = sw128_desc(smem_u32(
+                                    resb ? sB + ((size_t)(kb * nsub + u) * NP + h * NPc) * 128
+                                         : sB + stage * b_bytes + u * NP * 128 + h * NPc * 128));
                                 mma_bf16(tmem_d + h * NPc, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc,
                                          (kb | u | k) ? 1u : 0u);
                             }
@@ -371,9 +414,10 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     }
 }
 
-size_t gate_tc_smem(int NP, int KW, int K1, int stages, int nsub) {
+size_t gate_tc_smem(int NP, int KW, int K1, int stages, int nsub, int resident_b = 0, int d = 0) {
     const int groups = 2 * NP <= 512 ? 2 : 1;          // = nbuf
-    return 1024 + (size_t)stages * nsub * (GT_A_BYTES + NP * GT_BK * 2) + groups * ((size_t)GT_BM * gate_lds(KW) + GT_BM + 6 * K1) * 4 + 8 +
+    return 1024 + (size_t)stages * nsub * (GT_A_BYTES + (resident_b ? 0 : NP * GT_BK * 2)) +
+           (resident_b ? (size_t)NP * d * 2 : 0) + 8 + groups * ((size_t)GT_BM * gate_lds(KW) + GT_BM + 6 * K1) * 4 + 8 +
            (2 * stages + 4) * 8 + 16;
 }
 
@@ -389,9 +433,21 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
     if (a.T == 0) return cudaSuccess;
     if (a.TB != GT_BM || a.logits || !gate_tc_supported(a.bf16, a.d, a.KW)) return cudaErrorNotSupported;
     const int NP = gate_tc_np(a.KW);
-    note_launch();
-    router_split_kernel<<<(NP * a.d + 255) / 256 < 1024 ? (NP * a.d + 255) / 256 : 1024, 256, 0, st>>>(
-        a.w, wsplit, a.KW, a.d, NP);
+    // The split router is made once per call by router_split_kernel and streamed by TMA
+    // with x.  SMILE_GATE_RESIDENT_B=1: small routers (<= 64 KB) are instead built by every
+    // CTA in its own smem -- measured slower at C2 (69 vs ~45 us: each CTA's MMAs wait for
+    // its ~10 us build, and a CTA only has ~7 tiles), so off by default.
+    static int env_resb = -1;
+    if (env_resb < 0) {
+        const char *e = getenv("SMILE_GATE_RESIDENT_B");
+        env_resb = (e && e[0] == '1') ? 1 : 0;
+    }
+    const int resb = (env_resb && (size_t)NP * a.d * 2 <= 64 * 1024) ? 1 : 0;
+    if (!resb) {
+        note_launch();
+        router_split_kernel<<<(NP * a.d + 255) / 256 < 1024 ? (NP * a.d + 255) / 256 : 1024, 256, 0, st>>>(
+            a.w, wsplit, a.KW, a.d, NP);
+    }
     CUtensorMap mX, mW;
     if (!make_map(&mX, a.x, (int64_t)a.V * a.T, a.d, GT_BM)) return cudaErrorNotSupported;
     if (!make_map(&mW, wsplit, NP, a.d, NP > 256 ? NP / 2 : NP)) return cudaErrorNotSupported;
@@ -401,12 +457,13 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
     ta.NP = NP;
     ta.nbuf = 2 * NP <= 512 ? 2 : 1;
     ta.ntiles = a.V * a.nblk;
+    ta.resident_b = resb;
     // two 64-column sub-blocks per stage when d allows and 3+ such stages fit
-    ta.nsub = (a.d % (2 * GT_BK) == 0 && gate_tc_smem(NP, a.KW, a.K1, 3, 2) <= 227 * 1024) ? 2 : 1;
+    ta.nsub = (a.d % (2 * GT_BK) == 0 && gate_tc_smem(NP, a.KW, a.K1, 3, 2, resb, a.d) <= 227 * 1024) ? 2 : 1;
     int stages = 8;
-    while (stages > 2 && gate_tc_smem(NP, a.KW, a.K1, stages, ta.nsub) > 227 * 1024) --stages;
+    while (stages > 2 && gate_tc_smem(NP, a.KW, a.K1, stages, ta.nsub, resb, a.d) > 227 * 1024) --stages;
     ta.stages = stages;
-    const size_t smem = gate_tc_smem(NP, a.KW, a.K1, stages, ta.nsub);
+    const size_t smem = gate_tc_smem(NP, a.KW, a.K1, stages, ta.nsub, resb, a.d);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(gate1_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
