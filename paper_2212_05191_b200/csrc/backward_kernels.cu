@@ -24,22 +24,20 @@ __device__ __forceinline__ void st_el(void *p, int64_t i, float v, int bf16) {
     else reinterpret_cast<float *>(p)[i] = v;
 }
 
-// Softmax derivative terms of one level for one token, lanes over k (warp-cooperative).
+// Softmax derivative terms of one level for one token (serial over k):
 //   dl_k = dtop * ptop * (delta_k,top - p_k) + coef * p_k * (f_k - sum_i f_i p_i)
-__device__ void level_dlogits(const float *L, int K, int top, float dtop, float coef, const int32_t *hist,
-                              float invT, float *dl) {
-    const int lane = threadIdx.x & 31;
+__device__ void level_dlogits_thread(const float *L, int K, int top, float dtop, float coef, const int32_t *hist,
+                                     float invT, float *dl) {
     const float mx = L[top];
-    float s = 0.f, fp = 0.f;
-    for (int k = lane; k < K; k += 32) s += expf(L[k] - mx);
-    s = warp_sum(s);
-    for (int k = lane; k < K; k += 32) fp += (float)hist[k] * invT * __fdiv_rn(expf(L[k] - mx), s);
-    fp = warp_sum(fp);
-    const float ptop = __frcp_rn(s);
-    for (int k = lane; k < K; k += 32) {
-        const float pk = __fdiv_rn(expf(L[k] - mx), s);
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += expf(L[k] - mx);
+    const float inv = __frcp_rn(s);
+    float fp = 0.f;
+    for (int k = 0; k < K; ++k) fp += (float)hist[k] * invT * (expf(L[k] - mx) * inv);
+    for (int k = 0; k < K; ++k) {
+        const float pk = expf(L[k] - mx) * inv;
         const float fk = (float)hist[k] * invT;
-        dl[k] = dtop * ptop * ((k == top ? 1.f : 0.f) - pk) + coef * pk * (fk - fp);
+        dl[k] = dtop * inv * ((k == top ? 1.f : 0.f) - pk) + coef * pk * (fk - fp);
     }
 }
 
@@ -51,7 +49,13 @@ __global__ void combine_bwd_kernel(CombineBwdArgs a) {
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int64_t total = (int64_t)a.V * a.T;
     const float invT = 1.f / (float)a.T;
-    for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < total; g += warps) {
+    // a warp takes 32 consecutive tokens: their rows one after the other (16-byte
+    // vectors, warp-wide dot product for dgate), then lane t computes token t's dlogits
+    const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int64_t g0 = wg * 32; g0 < total; g0 += warps * 32) {
+      float my_dgate = 0.f;
+      for (int tt = 0; tt < 32 && g0 + tt < total; ++tt) {
+        const int64_t g = g0 + tt;
         const int v = (int)(g / a.T);
         const int i = a.route.dest1[g];
         const int s1 = a.route.slot1[g];
@@ -135,16 +139,22 @@ __global__ void combine_bwd_kernel(CombineBwdArgs a) {
             }
             dgate = warp_sum(acc);
         }
+        if (lane == tt) my_dgate = dgate;
+      }
+      const int64_t g = g0 + lane;
+      if (g < total) {
+        const int v = (int)(g / a.T);
         const float *L = a.logits + g * a.KW;
         float *dl = a.dlogits + g * a.KW;
         const float p = a.route.p[g], q = a.route.q[g];
         const float c1 = (float)(a.lam * a.alpha * (double)a.K1) * invT;
-        level_dlogits(L, a.K1, i, q * dgate, c1, a.stats.hist1 + (int64_t)v * a.K1, invT, dl);
+        level_dlogits_thread(L, a.K1, a.route.dest1[g], q * my_dgate, c1, a.stats.hist1 + (int64_t)v * a.K1, invT, dl);
         if (!a.flat) {
             const float c2 = (float)(a.lam * a.beta * (double)a.K2) * invT;
-            level_dlogits(L + a.K1, a.K2, a.route.dest2[g], p * dgate, c2, a.stats.hist2 + (int64_t)v * a.K2, invT,
-                          dl + a.K1);
+            level_dlogits_thread(L + a.K1, a.K2, a.route.dest2[g], p * my_dgate, c2,
+                                 a.stats.hist2 + (int64_t)v * a.K2, invT, dl + a.K1);
         }
+      }
     }
 }
 
@@ -242,12 +252,30 @@ __global__ void __launch_bounds__(kRbThreads) router_bwd_kernel(RouterBwdArgs a)
     }
 }
 
-__global__ void router_bwd_reduce(RouterBwdArgs a) {
+// dW[i] = sum over chunks of partial[chunk][i]: a block owns 32 consecutive elements,
+// warp w sums chunks w, w + 8, ... (4 loads in flight), then the 8 warp sums are added in
+// warp order (fixed order: deterministic).
+__global__ void __launch_bounds__(256) router_bwd_reduce(RouterBwdArgs a) {
+    __shared__ float s_part[8][32];
     const int64_t n = (int64_t)a.KW * a.d;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        float s = 0.f;
-        for (int ch = 0; ch < a.nchunk; ++ch) s += a.partial[(int64_t)ch * n + i];
-        a.dW[i] = s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+    float s = 0.f;
+    if (i < n) {
+        int ch = w;
+        for (; ch + 24 < a.nchunk; ch += 32) {
+            const float v0 = a.partial[(int64_t)ch * n + i], v1 = a.partial[(int64_t)(ch + 8) * n + i];
+            const float v2 = a.partial[(int64_t)(ch + 16) * n + i], v3 = a.partial[(int64_t)(ch + 24) * n + i];
+            s += v0; s += v1; s += v2; s += v3;
+        }
+        for (; ch < a.nchunk; ch += 8) s += a.partial[(int64_t)ch * n + i];
+    }
+    s_part[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && i < n) {
+        float t = 0.f;
+        for (int k = 0; k < 8; ++k) t += s_part[k][lane];
+        a.dW[i] = t;
     }
 }
 
@@ -255,7 +283,7 @@ __global__ void router_bwd_reduce(RouterBwdArgs a) {
 
 void launch_combine_bwd(const CombineBwdArgs &a, cudaStream_t st) {
     if (a.T == 0) return;
-    int64_t warps = (int64_t)a.V * a.T;
+    int64_t warps = ((int64_t)a.V * a.T + 31) / 32;          // 32 tokens per warp
     int grid = (int)((warps + 7) / 8);
     if (grid > 148 * 16) grid = 148 * 16;
     note_launch();
@@ -279,7 +307,7 @@ void launch_router_bwd(const RouterBwdArgs &a0, cudaStream_t st) {
     if (a.bf16) router_bwd_kernel<true><<<grid, thr, 0, st>>>(a);
     else router_bwd_kernel<false><<<grid, thr, 0, st>>>(a);
     note_launch();
-    router_bwd_reduce<<<148, 256, 0, st>>>(a);
+    router_bwd_reduce<<<(int)(((int64_t)a.KW * a.d + 31) / 32), 256, 0, st>>>(a);
 }
 
 }  // namespace smile
