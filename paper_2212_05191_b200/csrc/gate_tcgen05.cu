@@ -458,12 +458,12 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
     ta.nbuf = 2 * NP <= 512 ? 2 : 1;
     ta.ntiles = a.V * a.nblk;
     ta.resident_b = resb;
-    // SMILE_GATE_NSUB=2: two 64-column sub-blocks per stage when d allows and 3+ such
-    // stages fit (measured at C2: 55 vs 48 us, so one sub-block per stage by default)
+    // two 64-column sub-blocks per stage when d allows and 3+ such stages fit (same box,
+    // C2: 53-55 us vs 58-59 us with one; SMILE_GATE_NSUB=1 forces one)
     static int env_nsub = -1;
     if (env_nsub < 0) {
         const char *e = getenv("SMILE_GATE_NSUB");
-        env_nsub = (e && e[0] == '2') ? 2 : 1;
+        env_nsub = (e && e[0] == '1') ? 1 : 2;
     }
     ta.nsub = (env_nsub == 2 && a.d % (2 * GT_BK) == 0 &&
                gate_tc_smem(NP, a.KW, a.K1, 3, 2, resb, a.d) <= 227 * 1024) ? 2 : 1;
