@@ -138,6 +138,15 @@ static __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUte
         : "memory");
 }
 
+// 3-D TMA load of one CTA of a pair, completion on the pair leader's barrier.
+static __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                                        uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
+        : "memory");
+}
+
 // The 2-SM TMA load multicast to the CTAs in `mask` (same smem offset in each); every
 // destination's pair leader gets the complete_tx on the barrier at the offset of
 // `bar_cluster` (pass this CTA's pair leader's barrier).

@@ -24,6 +24,7 @@
 #include "smile_internal.h"
 #include "tc_util.cuh"
 
+#include <stdlib.h>
 #include <string.h>
 
 namespace smile {
@@ -59,11 +60,15 @@ struct WgArgs {
     int M, N, BN, NE;
 };
 
+// CG = 2: a CTA pair (cluster of 2) per 256-row tile of dW, tcgen05.mma.cta_group::2
+// issued by the leader; each CTA loads its 128 rows of A and half of B's columns, which
+// cuts the bytes each SM receives per MAC by a third (the wgrad GEMMs are bound by that).
+template <int CG>
 __global__ void __launch_bounds__(WG_THREADS, 1)
 wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, WgArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    const int b_bytes = (a.BN / 64) * WG_BOX_BYTES;
+    const int b_bytes = (a.BN / CG / 64) * WG_BOX_BYTES;       // this CTA's share of B per stage
     unsigned char *sA = base;
     unsigned char *sB = sA + WG_STAGES * WG_A_BYTES;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sB + WG_STAGES * b_bytes);
@@ -72,6 +77,9 @@ wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
     int *s_kb = reinterpret_cast<int *>(tmem_holder + 4);     // [NE] K-blocks of each expert
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
     if (threadIdx.x == 0) {
         for (int s = 0; s < WG_STAGES; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
@@ -79,14 +87,22 @@ wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&tfull[s]), 1);
-            mbar_init(smem_u32(&tempty[s]), 4);
+            mbar_init(smem_u32(&tempty[s]), 4 * CG);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             smem_u32(tmem_holder))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             smem_u32(tmem_holder))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     for (int E = threadIdx.x; E < a.NE; E += blockDim.x) {
         const int v = E / a.e, k = E % a.e;
@@ -96,9 +112,10 @@ wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
     }
     tc_fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync_all();          // the leader's barriers exist before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
-    const int mtn = a.M / WG_BM, ntn = a.N / a.BN;
+    const int mtn = a.M / (WG_BM * CG), ntn = a.N / a.BN;
     const int total = a.NE * mtn * ntn;
 
     if (warp == 0) {
@@ -106,9 +123,9 @@ wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
             // ---------------- TMA producer ----------------
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+            for (int tile = cid; tile < total; tile += ncl) {
                 const int E = tile / (mtn * ntn), rem = tile % (mtn * ntn);
-                const int m0 = (rem / ntn) * WG_BM, n0 = (rem % ntn) * a.BN;
+                const int m0 = (rem / ntn) * WG_BM * CG + rank * WG_BM, n0 = (rem % ntn) * a.BN + rank * (a.BN / CG);
                 const int v = E / a.e, k = E % a.e;
                 for (int s = 0; s < a.S; ++s) {
                     const int g = (v * a.S + s) * a.e + k;
@@ -116,25 +133,35 @@ wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
                     for (int r0 = 0; r0 < cnt; r0 += WG_BK) {
                         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                         const uint32_t fb = smem_u32(&full[stage]);
-                        mbar_arrive_tx(fb, WG_A_BYTES + b_bytes);
                         unsigned char *pa = sA + stage * WG_A_BYTES, *pb = sB + stage * b_bytes;
-                        tma_load_3d(smem_u32(pa), &mapA, m0, r0, g, fb);
-                        tma_load_3d(smem_u32(pa + WG_BOX_BYTES), &mapA, m0 + 64, r0, g, fb);
-                        for (int j = 0; j < a.BN / 64; ++j)
-                            tma_load_3d(smem_u32(pb + j * WG_BOX_BYTES), &mapB, n0 + 64 * j, r0, g, fb);
+                        if (CG == 1) {
+                            mbar_arrive_tx(fb, WG_A_BYTES + b_bytes);
+                            tma_load_3d(smem_u32(pa), &mapA, m0, r0, g, fb);
+                            tma_load_3d(smem_u32(pa + WG_BOX_BYTES), &mapA, m0 + 64, r0, g, fb);
+                            for (int j = 0; j < a.BN / 64; ++j)
+                                tma_load_3d(smem_u32(pb + j * WG_BOX_BYTES), &mapB, n0 + 64 * j, r0, g, fb);
+                        } else {
+                            // the leader's full barrier counts both CTAs' bytes
+                            if (leader) mbar_arrive_tx(fb, CG * (WG_A_BYTES + b_bytes));
+                            const uint32_t fbl = mapa_shared(fb, 0);
+                            tma_load_3d_pair(smem_u32(pa), &mapA, m0, r0, g, fbl);
+                            tma_load_3d_pair(smem_u32(pa + WG_BOX_BYTES), &mapA, m0 + 64, r0, g, fbl);
+                            for (int j = 0; j < a.BN / CG / 64; ++j)
+                                tma_load_3d_pair(smem_u32(pb + j * WG_BOX_BYTES), &mapB, n0 + 64 * j, r0, g, fbl);
+                        }
                         if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && leader) {
             // ---------------- MMA issuer: A and B both MN-major ----------------
-            const uint32_t idesc = make_idesc(WG_BM, a.BN) | (1u << 15) | (1u << 16);
+            const uint32_t idesc = make_idesc(WG_BM * CG, a.BN) | (1u << 15) | (1u << 16);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+            for (int tile = cid; tile < total; tile += ncl, ++it) {
                 const int E = tile / (mtn * ntn);
                 const int nk = s_kb[E];
                 const int acc = it & 1;
@@ -147,13 +174,20 @@ wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
                     const uint64_t ad = sw128_mn_desc(smem_u32(sA + stage * WG_A_BYTES), WG_BOX_BYTES);
                     const uint64_t bd = sw128_mn_desc(smem_u32(sB + stage * b_bytes), WG_BOX_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < WG_BK / 16; ++kk)   // 16 K-rows = two 1024 B swizzle atoms
-                        mma_bf16(tmem_d, ad + (uint64_t)(kk * 128), bd + (uint64_t)(kk * 128), idesc,
-                                 (kb | kk) ? 1u : 0u);
-                    mma_commit(smem_u32(&empty[stage]));
+                    for (int kk = 0; kk < WG_BK / 16; ++kk) {  // 16 K-rows = two 1024 B swizzle atoms
+                        if (CG == 1)
+                            mma_bf16(tmem_d, ad + (uint64_t)(kk * 128), bd + (uint64_t)(kk * 128), idesc,
+                                     (kb | kk) ? 1u : 0u);
+                        else
+                            mma_bf16_pair(tmem_d, ad + (uint64_t)(kk * 128), bd + (uint64_t)(kk * 128), idesc,
+                                          (kb | kk) ? 1u : 0u);
+                    }
+                    if (CG == 1) mma_commit(smem_u32(&empty[stage]));
+                    else mma_commit_pair(smem_u32(&empty[stage]));
                     if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(smem_u32(&tfull[acc]));
+                if (CG == 1) mma_commit(smem_u32(&tfull[acc]));
+                else mma_commit_pair(smem_u32(&tfull[acc]));
             }
         }
     } else if (warp >= 4) {
@@ -161,9 +195,9 @@ wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
         const int q = warp & 3;
         const int row = q * 32 + lane;
         int it = 0;
-        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+        for (int tile = cid; tile < total; tile += ncl, ++it) {
             const int E = tile / (mtn * ntn), rem = tile % (mtn * ntn);
-            const int m0 = (rem / ntn) * WG_BM, n0 = (rem % ntn) * a.BN;
+            const int m0 = (rem / ntn) * WG_BM * CG + rank * WG_BM, n0 = (rem % ntn) * a.BN;
             const bool empty_k = s_kb[E] == 0;                    // no rows: the gradient is 0
             const int acc = it & 1;
             mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
@@ -180,13 +214,20 @@ wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+            if (lane == 0) {
+                if (CG == 1) mbar_arrive(smem_u32(&tempty[acc]));
+                else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+            }
         }
     }
     __syncthreads();
+    if (CG == 2) cluster_sync_all();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+        if (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
     }
 }
 
@@ -285,23 +326,48 @@ cudaError_t launch_wgrad_tc(const void *A, int M, const void *B, int N, float *D
                             int e, int64_t Cseg, int num_sms, cudaStream_t st) {
     const int nseg = V * S * e, NE = V * e;
     const int BN = pick_wg_bn(N);
-    CUtensorMap mA, mB;
+    CUtensorMap mA, mB;           // 64 x 64 boxes: A (M-major) two per CTA, B (N-major) BN / CG / 64 per CTA
     if (!make_map_3d(&mA, A, nseg, Cseg, M, WG_BK)) return cudaErrorNotSupported;
     if (!make_map_3d(&mB, B, nseg, Cseg, N, WG_BK)) return cudaErrorNotSupported;
     WgArgs a;
     memset(&a, 0, sizeof(a));
     a.Dw = Dw; a.counts = counts; a.e = e; a.S = S; a.Cseg = Cseg; a.M = M; a.N = N; a.BN = BN; a.NE = NE;
-    const size_t smem = 1024 + WG_STAGES * (WG_A_BYTES + (BN / 64) * WG_BOX_BYTES) + (2 * WG_STAGES + 4) * 8 + 16 +
+    // CTA pairs when the 256-row tiles divide M and half of BN is whole 64-column boxes
+    const char *ep = getenv("SMILE_WGRAD_CTA_PAIR");
+    const int CG = (!(ep && ep[0] == '0') && M % (2 * WG_BM) == 0 && (BN / 2) % 64 == 0 && num_sms >= 2) ? 2 : 1;
+    const size_t smem = 1024 + WG_STAGES * (WG_A_BYTES + (BN / CG / 64) * WG_BOX_BYTES) + (2 * WG_STAGES + 4) * 8 + 16 +
                         (size_t)NE * 4;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(wgrad_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
-    const int total = NE * (M / WG_BM) * (N / BN);
+    const int total = NE * (M / (WG_BM * CG)) * (N / BN);
     note_launch();
-    wgrad_tcgen05<<<total < num_sms ? total : num_sms, WG_THREADS, smem, st>>>(mA, mB, a);
-    return cudaGetLastError();
+    if (CG == 1) {
+        static bool attr1 = false;
+        if (!attr1) {
+            cudaFuncSetAttribute(wgrad_tcgen05<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr1 = true;
+        }
+        wgrad_tcgen05<1><<<total < num_sms ? total : num_sms, WG_THREADS, smem, st>>>(mA, mB, a);
+        return cudaGetLastError();
+    }
+    static bool attr2 = false;
+    if (!attr2) {
+        cudaFuncSetAttribute(wgrad_tcgen05<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr2 = true;
+    }
+    const int grid = 2 * (total < num_sms / 2 ? total : num_sms / 2);
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(WG_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, wgrad_tcgen05<2>, mA, mB, a);
 }
 
 void launch_pad_rows_zero(void *buf, const int32_t *counts, int nseg, int64_t Cseg, int cols, cudaStream_t st) {
