@@ -278,11 +278,11 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
         const char *e = getenv("SMILE_GATE_TC");
         const bool tc_on = !(e && e[0] == '0');
         if (tc_on && gate_tc_supported(shape->dtype == SMILE_BF16, shape->d, z.KW)) {
-            c->TB1 = 128;                       // the tensor-core gate's token tile
-            const size_t wb = (size_t)gate_tc_np(z.KW) * shape->d * 2;
+            c->TB1 = gate_tc_tile(z.KW);        // the tensor-core gate's token tile (128 or 256)
+            const size_t wb = (size_t)gate_tc_rows(z.KW) * shape->d * 2;
             if (cudaMalloc(&c->wsplit, wb) != cudaSuccess) { delete c; return SMILE_ECUDA; }
             // look-back state of the fused gate + permute (flags zero between calls)
-            const int64_t nt = (int64_t)z.V * ((shape->T + 127) / 128);
+            const int64_t nt = (int64_t)z.V * ((shape->T + 127) / 128);   // (the fused path's 128-token tiles)
             if (cudaMalloc(&c->lb_flag, (nt > 0 ? nt : 1) * 4) != cudaSuccess ||
                 cudaMalloc(&c->lb_agg, (nt > 0 ? nt : 1) * z.K1 * 4) != cudaSuccess ||
                 cudaMalloc(&c->lb_inc, (nt > 0 ? nt : 1) * z.K1 * 4) != cudaSuccess ||
@@ -539,7 +539,7 @@ extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, co
     const bool bi = c->shape.mode == SMILE_BILEVEL;
     if (bi && !send_meta) return SMILE_EINVAL;
     if (c->shape.T == 0) return SMILE_OK;
-    if (!c->wsplit || !c->lb_flag) {
+    if (!c->wsplit || !c->lb_flag || c->TB1 != 128) {
         // no tensor-core gate for this shape / dtype: the two calls it fuses
         STEP(smile_gate_inter(c, x, w_router, nullptr, logits_out, route, stats, counts1, stream));
         return smile_dispatch(c, 1, x, route, nullptr, nullptr, send_rows, send_meta, stream);

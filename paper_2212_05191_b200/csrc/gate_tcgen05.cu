@@ -43,12 +43,20 @@ constexpr int GT_MAX_NP = 384;                  // 3 * KW <= 384 (KW <= 128)
 
 // W fp32 [KW, d] -> Wb bf16 [NP, d]: row 3k+p = piece p of W[k], rows >= 3 KW zero.
 // r0 = W, piece_p = bf16_rn(r_p), r_{p+1} = r_p - piece_p (exact in fp32).
+// quad10 = 1 (the swapped kernel): row r = 32 Q + w holds piece w % 3 of logit 10 Q + w / 3
+// for w < 30 (rows 30, 31 of every 32-row group zero), so a logit's three pieces share a
+// 32-lane TMEM quadrant.
 __global__ void router_split_kernel(const float *__restrict__ w, __nv_bfloat16 *__restrict__ wb, int KW, int d,
-                                    int NP) {
+                                    int NP, int quad10) {
     const int64_t n = (int64_t)NP * d;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(i / d), c = (int)(i - (int64_t)r * d);
-        const int k = r / 3, p = r - 3 * k;
+        int k = r / 3, p = r - 3 * k;
+        if (quad10) {
+            const int q = r >> 5, ww = r & 31;
+            k = ww < 30 ? 10 * q + ww / 3 : KW;
+            p = ww % 3;
+        }
         float out = 0.f;
         if (k < KW) {
             float rem = w[(int64_t)k * d + c];
@@ -414,6 +422,172 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Swapped-role tensor-core gate (default for KW <= 40): M = the split router (its
+// 32 * ceil(KW / 10) rows zero-padded to 128 by TMA), N = 256 TOKENS per MMA.  With the
+// tokens on M (gate1_tc_kernel) every tcgen05.mma is 128 x NP x 16 with NP as small as
+// 32, and the MMA count per token -- each costs a near-fixed ~350 cycles there (ncu:
+// the producer waits on stage releases while the MMA thread never waits for data) -- is
+// what bounds the kernel; here one MMA covers 256 tokens.  The accumulator [piece rows x
+// 256 tokens] is transposed by the epilogue: lane r of quadrant q holds piece r % 3 of
+// logit 10 q + r / 3 for 32 tokens; two shuffles sum the pieces in order, and the logits
+// land in s_lg [token][KW] for the same gate_finish (8 warps, 256 tokens per tile).
+// ---------------------------------------------------------------------------------
+constexpr int GS_TOK = 256, GS_THREADS = 128 + 256;
+constexpr int GS_X_BYTES = GS_TOK * GT_BK * 2;    // 32 KB per stage
+constexpr int GS_W_BYTES = 128 * GT_BK * 2;       // 16 KB per stage
+
+template <int G>
+struct EpiSync256 {
+    static __device__ __forceinline__ void sync() { asm volatile("bar.sync %0, 256;" ::"n"(1 + G) : "memory"); }
+    static __device__ __forceinline__ int tid() { return threadIdx.x - 128; }
+    static __device__ __forceinline__ int nthr() { return 256; }
+};
+
+struct GateTArgs {
+    GateArgs g;
+    int NPT;         // split-router rows (32 * ceil(KW / 10))
+    int stages;
+    int ntiles;
+};
+
+__global__ void __launch_bounds__(GS_THREADS, 1)
+gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, GateTArgs ta) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const GateArgs &a = ta.g;
+    const int ST = ta.stages, KW = a.KW, NQ = ta.NPT / 32;
+    unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char *sW = base;
+    unsigned char *sX = sW + ST * GS_W_BYTES;
+    const int lds = gate_lds(KW);
+    float *s_lg = reinterpret_cast<float *>(sX + ST * GS_X_BYTES);    // [256][lds]
+    int *s_j = reinterpret_cast<int *>(s_lg + GS_TOK * lds);          // [256]
+    int *s_wh = s_j + GS_TOK;                                         // [8][K1]
+    int *s_bh = s_wh + 8 * a.K1;                                      // [K1]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(s_bh + a.K1) + 7) & ~(uintptr_t)7);
+    uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(smem_u32(&full[s]), 1);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(smem_u32(&tfull[s]), 1);
+            mbar_init(smem_u32(&tempty[s]), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapX)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapW)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    const int nk = a.d / GT_BK;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
+                const int v = tile / a.nblk, blk = tile - v * a.nblk;
+                const int row0 = (int)((int64_t)v * a.T + (int64_t)blk * GS_TOK);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                    const uint32_t fb = smem_u32(&full[stage]);
+                    mbar_arrive_tx(fb, GS_W_BYTES + GS_X_BYTES);
+                    tma_load_2d(smem_u32(sW + stage * GS_W_BYTES), &mapW, kb * GT_BK, 0, fb);
+                    tma_load_2d(smem_u32(sX + stage * GS_X_BYTES), &mapX, kb * GT_BK, row0, fb);
+                    if (++stage == ST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc(128, GS_TOK);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
+                const int buf = it & 1;
+                mbar_wait(smem_u32(&tempty[buf]), ((uint32_t)(it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + buf * GS_TOK;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(smem_u32(&full[stage]), phase);
+                    tc_fence_after();
+                    const uint64_t ad = sw128_desc(smem_u32(sW + stage * GS_W_BYTES));
+                    const uint64_t bd = sw128_desc(smem_u32(sX + stage * GS_X_BYTES));
+#pragma unroll
+                    for (int k = 0; k < GT_BK / 16; ++k)
+                        mma_bf16(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (kb | k) ? 1u : 0u);
+                    mma_commit(smem_u32(&empty[stage]));
+                    if (++stage == ST) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(smem_u32(&tfull[buf]));
+            }
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3, hc = (warp - 4) >> 2;    // TMEM lane quadrant, token-column half
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
+            const int v = tile / a.nblk, blk = tile - v * a.nblk;
+            const int64_t t0 = (int64_t)blk * GS_TOK;
+            const int nt = (int)(a.T - t0 < GS_TOK ? a.T - t0 : GS_TOK);
+            const int64_t tok0 = (int64_t)v * a.T + t0;
+            const int buf = it & 1;
+            mbar_wait(smem_u32(&tfull[buf]), (uint32_t)(it >> 1) & 1);
+            tc_fence_after();
+            if (q < NQ) {
+                const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + buf * GS_TOK + hc * 128;
+                const int k = 10 * q + lane / 3;
+                const bool head = (lane % 3 == 0) && lane < 30 && k < KW;
+                for (int c = 0; c < 4; ++c) {
+                    float vv[32];
+                    tmem_ld32(tb + c * 32, vv);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float p1 = __shfl_down_sync(kFull, vv[j], 1);
+                        const float p2 = __shfl_down_sync(kFull, vv[j], 2);
+                        if (head) s_lg[(hc * 128 + c * 32 + j) * lds + k] = (vv[j] + p1) + p2;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+            EpiSync256<0>::sync();
+            if (a.logits_out) {
+                for (int i = EpiSync256<0>::tid(); i < nt * KW; i += 256)
+                    a.logits_out[tok0 * KW + i] = s_lg[(i / KW) * lds + i % KW];
+                EpiSync256<0>::sync();
+            }
+            gate_finish<EpiSync256<0>>(a, s_lg, lds, s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
+            EpiSync256<0>::sync();
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    }
+}
+
+size_t gate_tcT_smem(int KW, int K1, int stages) {
+    return 1024 + (size_t)stages * (GS_W_BYTES + GS_X_BYTES) + ((size_t)GS_TOK * gate_lds(KW) + GS_TOK + 9 * K1) * 4 +
+           8 + (2 * stages + 4) * 8 + 16;
+}
+
 size_t gate_tc_smem(int NP, int KW, int K1, int stages, int nsub, int resident_b = 0, int d = 0) {
     const int groups = 2 * NP <= 512 ? 2 : 1;          // = nbuf
     return 1024 + (size_t)stages * nsub * (GT_A_BYTES + (resident_b ? 0 : NP * GT_BK * 2)) +
@@ -425,13 +599,54 @@ size_t gate_tc_smem(int NP, int KW, int K1, int stages, int nsub, int resident_b
 
 int gate_tc_np(int KW) { return ((3 * KW + 31) / 32) * 32; }
 
+// The swapped-role kernel (256-token tiles) for KW <= 40 unless SMILE_GATE_SWAP=0.
+int gate_tc_tile(int KW) {                    // read at every smile_create
+    const char *e = getenv("SMILE_GATE_SWAP");
+    const bool on = !(e && e[0] == '0');
+    return (on && KW <= 40) ? GS_TOK : GT_BM;
+}
+
+int gate_tc_rows(int KW) {                    // rows of the split-router buffer (both layouts)
+    const int a = gate_tc_np(KW), b = 32 * ((KW + 9) / 10);
+    return a > b ? a : b;
+}
+
 bool gate_tc_supported(int bf16, int d, int KW) {
     return bf16 && d % GT_BK == 0 && d >= GT_BK && gate_tc_np(KW) <= GT_MAX_NP && encode_fn() != nullptr;
 }
 
 cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, cudaStream_t st) {
     if (a.T == 0) return cudaSuccess;
-    if (a.TB != GT_BM || a.logits || !gate_tc_supported(a.bf16, a.d, a.KW)) return cudaErrorNotSupported;
+    if (a.logits || !gate_tc_supported(a.bf16, a.d, a.KW)) return cudaErrorNotSupported;
+    if (a.TB == GS_TOK) {
+        if (a.fuse_dispatch) return cudaErrorNotSupported;          // the fused permute has 128-token tiles
+        const int NPT = 32 * ((a.KW + 9) / 10);
+        note_launch();
+        router_split_kernel<<<(NPT * a.d + 255) / 256 < 1024 ? (NPT * a.d + 255) / 256 : 1024, 256, 0, st>>>(
+            a.w, wsplit, a.KW, a.d, NPT, 1);
+        CUtensorMap mX, mW;
+        if (!make_map(&mX, a.x, (int64_t)a.V * a.T, a.d, GS_TOK)) return cudaErrorNotSupported;
+        if (!make_map(&mW, wsplit, NPT, a.d, 128)) return cudaErrorNotSupported;    // rows >= NPT: zero fill
+        GateTArgs ta;
+        memset(&ta, 0, sizeof(ta));
+        ta.g = a;
+        ta.NPT = NPT;
+        ta.ntiles = a.V * a.nblk;
+        int stages = 8;
+        while (stages > 2 && gate_tcT_smem(a.KW, a.K1, stages) > 227 * 1024) --stages;
+        ta.stages = stages;
+        const size_t smem = gate_tcT_smem(a.KW, a.K1, stages);
+        static bool attrT = false;
+        if (!attrT) {
+            cudaFuncSetAttribute(gate1_tcT_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attrT = true;
+        }
+        const int grid = ta.ntiles < num_sms ? ta.ntiles : num_sms;
+        note_launch();
+        gate1_tcT_kernel<<<grid, GS_THREADS, smem, st>>>(mX, mW, ta);
+        return cudaGetLastError();
+    }
+    if (a.TB != GT_BM) return cudaErrorNotSupported;
     const int NP = gate_tc_np(a.KW);
     // The split router is made once per call by router_split_kernel and streamed by TMA
     // with x.  SMILE_GATE_RESIDENT_B=1: small routers (<= 64 KB) are instead built by every
@@ -446,7 +661,7 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
     if (!resb) {
         note_launch();
         router_split_kernel<<<(NP * a.d + 255) / 256 < 1024 ? (NP * a.d + 255) / 256 : 1024, 256, 0, st>>>(
-            a.w, wsplit, a.KW, a.d, NP);
+            a.w, wsplit, a.KW, a.d, NP, 0);
     }
     CUtensorMap mX, mW;
     if (!make_map(&mX, a.x, (int64_t)a.V * a.T, a.d, GT_BM)) return cudaErrorNotSupported;

@@ -216,6 +216,8 @@ void launch_pad_rows_zero(void *buf, const int32_t *counts, int nseg, int64_t Cs
 
 // Level-1 gate with the router on tcgen05 (gate_tcgen05.cu); needs TB == 128.
 int gate_tc_np(int KW);
+int gate_tc_tile(int KW);            // token tile of the tensor-core gate (128, or 256 for the swapped kernel)
+int gate_tc_rows(int KW);            // rows of the split-router buffer
 bool gate_tc_supported(int bf16, int d, int KW);
 cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, cudaStream_t st);
 

@@ -123,15 +123,24 @@ def test_identity_collapse_n1_equals_flat():
     ("bf16", 2, 4, 8, 257, 192, "flat"),        # KW = 64 (C4's flat router), N = 256
     ("bf16", 4, 2, 12, 130, 64, "flat"),        # KW = 96: two N halves, one TMEM buffer
     ("bf16", 2, 2, 1, 100, 64, "bilevel"),      # a single partial tile per rank
+    ("bf16", 3, 7, 1, 300, 128, "flat"),        # KW = 21: swapped layout needs 96 router rows (3 quadrants)
 ])
-def test_fused_router(dtype, n, m, e, T, d, mode):
+@pytest.mark.parametrize("swap", ["1", "0"])
+def test_fused_router(dtype, n, m, e, T, d, mode, swap):
     """a1 fused into a2: logits within fp32 accumulation error of the fp64 oracle; the
     routing taken on the GPU's own logits matches the oracle run on those logits.  The
-    bf16 cases run the tcgen05 router (three-piece bf16 split of W, gate_tcgen05.cu)."""
+    bf16 cases run the tcgen05 router (three-piece bf16 split of W, gate_tcgen05.cu):
+    swap = 1 the swapped-role kernel (256 tokens per MMA, KW <= 40), swap = 0 the
+    128-token one."""
     from paper_2212_05191_b200 import smile as smb
+    import os
     case = Case(n, m, e, T, d, 128, 1.0, dtype=dtype, fused=True, seed=5, mode=mode)
     G, KW = n * m, case.cfg.logit_width
-    layer = smb.SmileLayer(n, m, e, d, 128, T, 1.0, dtype, mode)
+    os.environ["SMILE_GATE_SWAP"] = swap
+    try:
+        layer = smb.SmileLayer(n, m, e, d, 128, T, 1.0, dtype, mode)
+    finally:
+        del os.environ["SMILE_GATE_SWAP"]
     layer.alloc_workspace()
     g = case.gpu_tensors()
     lg_out = torch.empty(G, T, KW, dtype=torch.float32, device="cuda")
@@ -172,11 +181,16 @@ def test_fused_gate_dispatch_matches_two_calls(n, m, e, T, d, mode, peer):
     statistics, counts, and every valid row / meta entry of the level-1 send (or, with
     the peer-store exchange, receive) buffers."""
     from paper_2212_05191_b200 import smile as smb
+    import os
     case = Case(n, m, e, T, d, 128, 1.0, dtype="bf16", fused=True, seed=8, mode=mode)
     g = case.gpu_tensors()
     res = []
     for fused in (False, True):
-        L = smb.SmileLayer(n, m, e, d, 128, T, 1.0, "bf16", mode)
+        os.environ["SMILE_GATE_SWAP"] = "0"      # the fused permute lives in the 128-token gate
+        try:
+            L = smb.SmileLayer(n, m, e, d, 128, T, 1.0, "bf16", mode)
+        finally:
+            del os.environ["SMILE_GATE_SWAP"]
         L.alloc_workspace()
         if peer:
             L.enable_peer_exchange()
