@@ -380,21 +380,25 @@ smile_status smile_forward_ws(smile_ctx ctx, void *ws, smile_ws_view *view);
  * sequential All2Alls): gate_inter, dispatch(1), all2all_inter, gate_intra, dispatch(2),
  * all2all_intra, expert_ffn, all2all_intra(rev), combine(2), all2all_inter(rev),
  * combine(1), aux_loss.  FLAT: gate, dispatch(1), all2all(world), ffn,
- * all2all(world, rev), combine(1), aux_loss. */
+ * all2all(world, rev), combine(1), aux_loss.
+ * T == 0: returns SMILE_OK without touching any buffer (x, out may be NULL; the loss,
+ * which divides by T, is not written). */
 smile_status smile_forward(smile_ctx ctx, const smile_layer_io *io, void *stream);
 
-/* End to end from HOST memory: copies host_x [V, T, d] (and host_logits when non-NULL)
- * to io->x / io->logits, runs smile_forward, copies io->out to host_out and io->loss to
- * host_loss, all on `stream`; synchronises `stream` before returning.  Host buffers
- * should be pinned for asynchronous copies. */
 /* The whole backward after a forward with io->train set, in reverse order of the forward:
  * combine_bwd, exchange(1, gradient rows), dispatch_grad, exchange(2), expert_ffn_bwd,
  * exchange(2, reverse), combine(2), exchange(1, reverse), combine_grad, router_bwd.
  * Works over both exchanges; with the peer-store exchange (smile_register_workspace)
  * the gradient rows are stored at / loaded from their owners and every exchange is a
- * barrier, as in the forward. */
+ * barrier, as in the forward.
+ * T == 0: the weight gradients (dW1, db1, dW2, db2 and dW_router when given) are sums
+ * over no tokens and are set to 0; nothing else is touched (gout, dx may be NULL). */
 smile_status smile_backward(smile_ctx ctx, const smile_layer_io *io, const smile_grad_io *g, void *stream);
 
+/* End to end from HOST memory: copies host_x [V, T, d] (and host_logits when non-NULL)
+ * to io->x / io->logits, runs smile_forward, copies io->out to host_out and io->loss to
+ * host_loss, all on `stream`; synchronises `stream` before returning.  Host buffers
+ * should be pinned for asynchronous copies. */
 smile_status smile_forward_host(smile_ctx ctx, const smile_layer_io *io, const void *host_x,
                                 const float *host_logits, void *host_out, double *host_loss,
                                 void *stream);

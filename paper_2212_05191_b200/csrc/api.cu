@@ -867,7 +867,9 @@ extern "C" smile_status smile_forward_ws(smile_ctx c, void *ws, smile_ws_view *v
 
 
 extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, void *stream) {
-    if (!c || !io || !io->x || !io->out || !io->loss || !io->ws) return SMILE_EINVAL;
+    if (!c || !io) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;                 // no tokens: nothing to compute
+    if (!io->x || !io->out || !io->loss || !io->ws) return SMILE_EINVAL;
     if (!io->logits && !io->w_router) return SMILE_EINVAL;
     smile_ws_view w;
     STEP(smile_forward_ws(c, io->ws, &w));
@@ -940,7 +942,21 @@ extern "C" smile_status smile_forward_host_stream(smile_ctx c, const smile_layer
 }
 
 extern "C" smile_status smile_backward(smile_ctx c, const smile_layer_io *io, const smile_grad_io *g, void *stream) {
-    if (!c || !io || !g || !io->ws || !g->gout || !g->dx || !g->W1 || !g->W2 || !g->dW1 || !g->db1 || !g->dW2 ||
+    if (!c || !io || !g) return SMILE_EINVAL;
+    if (c->shape.T == 0) {
+        // the weight gradients are sums over no tokens
+        if (!g->dW1 || !g->db1 || !g->dW2 || !g->db2) return SMILE_EINVAL;
+        cudaSetDevice(c->shape.device);
+        const size_t NEl = (size_t)c->sz.V * c->shape.e, d = c->shape.d, f = c->shape.d_ff;
+        cudaStream_t st = S(stream);
+        CUDA_TRY(cudaMemsetAsync(g->dW1, 0, NEl * d * f * 4, st));
+        CUDA_TRY(cudaMemsetAsync(g->db1, 0, NEl * f * 4, st));
+        CUDA_TRY(cudaMemsetAsync(g->dW2, 0, NEl * f * d * 4, st));
+        CUDA_TRY(cudaMemsetAsync(g->db2, 0, NEl * d * 4, st));
+        if (g->dW_router) CUDA_TRY(cudaMemsetAsync(g->dW_router, 0, (size_t)c->sz.KW * d * 4, st));
+        return SMILE_OK;
+    }
+    if (!io->ws || !g->gout || !g->dx || !g->W1 || !g->W2 || !g->dW1 || !g->db1 || !g->dW2 ||
         !g->db2)
         return SMILE_EINVAL;
     if (io->w_router && !io->logits && !g->dW_router) return SMILE_EINVAL;

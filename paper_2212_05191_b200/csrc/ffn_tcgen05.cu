@@ -54,6 +54,9 @@ struct TcArgs {
     int stages;                // smem pipeline depth
     int tma_store;             // 1: full 32 x 32 boxes leave through smem + TMA; 0: st.global from registers
     int box64;                 // 1: 32 x 64 boxes (two chunks per TMA store; every warp owns 2k chunks)
+    int diag;                  // measurement only (SMILE_FFN_DIAG; wrong results): 1 no activation,
+                               // 2 no stores, 4 no TMEM reads / epilogue math (release only),
+                               // 8 TMA stores into rows [0, 1024) only (L2-resident)
     int *err;
 };
 
@@ -360,14 +363,15 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             const TileInfo t = tile_info<CG, NPAIR>(a, s_pref, tile, ntn, rank, pair);
             const int acc = it & 1;
             const bool has_bias = a.mode == EPI_BIAS || a.mode == EPI_BIAS_SAVE;
-            const bool act = (a.mode == EPI_BIAS && a.gelu) || a.mode == EPI_BIAS_SAVE;
+            const bool act = ((a.mode == EPI_BIAS && a.gelu) || a.mode == EPI_BIAS_SAVE) && !(a.diag & 1);
             constexpr bool dgelu = DG;                      // EPI_DGELU has its own instantiation
             const float4 *bias4 = reinterpret_cast<const float4 *>(a.bias + (int64_t)t.E * a.N + (int64_t)t.nt * a.BN);
             const int64_t dcol0 = (int64_t)t.nt * a.BN;
             int64_t d_row;                                  // this warp's strip
             int srows;
             expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + q, d_row, srows);
-            const bool full_box = srows == 32;
+            const int st_row = (a.diag & 8) ? (int)(d_row & 1023) : (int)d_row;   // diag 8: L2-resident store window
+            const bool full_box = srows == 32 && !(a.diag & 2);
             // EPI_DGELU: chunk c's saved pre-activation is loaded before its accumulator
             // columns (the first chunk's while this tile's MMAs still run)
             const uint4 *aux_row =
@@ -379,7 +383,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS;
-            for (int c = c_beg; c < c_end && srows > 0; ++c) {
+            for (int c = c_beg; c < c_end && srows > 0 && !(a.diag & 4); ++c) {
                 if (dgelu && c > c_beg)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) acur[i] = __ldg(aux_row + c * 4 + i);
@@ -444,7 +448,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                         if (lane == 0) {
                             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                              reinterpret_cast<uint64_t>(&mapD)),
-                                         "r"((int)dcol0 + (c - 1) * 32), "r"((int)d_row), "r"(smem_u32(box))
+                                         "r"((int)dcol0 + (c - 1) * 32), "r"(st_row), "r"(smem_u32(box))
                                          : "memory");
                             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                         }
@@ -468,7 +472,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     if (lane == 0) {
                         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                          reinterpret_cast<uint64_t>(&mapD)),
-                                     "r"((int)dcol0 + c * 32), "r"((int)d_row), "r"(smem_u32(box))
+                                     "r"((int)dcol0 + c * 32), "r"(st_row), "r"(smem_u32(box))
                                      : "memory");
                         if (nbox == 2)
                             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
@@ -477,7 +481,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                                          : "memory");
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
-                } else if (lane < srows) {
+                } else if (lane < srows && !(a.diag & 2)) {
                     // partial strips (a segment's last rows), or tma_store == 0: st.global of
                     // this lane's row (64 contiguous bytes per output), valid rows only
                     uint4 *dst = reinterpret_cast<uint4 *>(a.D + (d_row + lane) * (int64_t)a.N + dcol0 + c * 32);
@@ -651,10 +655,15 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     // when every epilogue warp owns an even number of 32-column chunks
     {
         const char *e = getenv("SMILE_FFN_BOX64");
-        const bool want = e ? e[0] == '1' : false;
-        a.box64 = (want && a.tma_store && nbox == 1 && gelu && (BN / 32) % 8 == 0) ? 1 : 0;
+        const bool want = e ? (e[0] == '1' && gelu) || e[0] == '2' : false;     // 2: both GEMMs
+        a.box64 = (want && a.tma_store && nbox == 1 && mode != EPI_DGELU && (BN / 32) % 8 == 0) ? 1 : 0;
     }
     a.stages = pick_stages(CG, nbox, a.tma_store, a.box64);
+    if (const char *e = getenv("SMILE_FFN_STAGES")) {
+        const int s = atoi(e);
+        if (s >= 2 && s < a.stages) a.stages = s;
+    }
+    if (const char *e = getenv("SMILE_FFN_DIAG")) a.diag = atoi(e);
     a.err = nullptr;
     const size_t smem = smem_bytes(CG, a.stages, nbox, a.tma_store, a.box64);
     const bool dg = mode == EPI_DGELU;

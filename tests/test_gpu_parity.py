@@ -372,3 +372,34 @@ def test_peer_exchange_matches_copy_and_oracle(n, m, e, T, d, d_ff, cf, dtype, m
     check_route(case, layer, r, l_peer)
     ref = case.oracle_out(r)
     assert_close_scaled(o_peer.float().cpu().numpy().reshape(-1, d), ref, 2e-2 if dtype == "bf16" else 1e-5, "peer")
+
+
+@pytest.mark.parametrize("mode", ["bilevel", "flat"])
+def test_empty_input_T0(mode):
+    """T = 0 (no tokens): forward is a no-op, backward zeroes the weight gradients (sums
+    over no tokens), and the aux loss, which divides by T, is refused (smile.h)."""
+    from paper_2212_05191_b200 import SmileLayer
+    from paper_2212_05191_b200.smile import SmileError
+    n, m, e, d, d_ff = 2, 2, 1, 64, 128
+    layer = SmileLayer(n, m, e, d, d_ff, 0, 1.0, "bf16", mode)
+    V, KW, NEl = layer.V, layer.KW, layer.V * e
+    bf = dict(dtype=torch.bfloat16, device="cuda")
+    f32 = dict(dtype=torch.float32, device="cuda")
+    x = torch.empty(V, 0, d, **bf)
+    out = torch.empty_like(x)
+    W1t, W2t = torch.randn(NEl, d_ff, d, **f32).bfloat16(), torch.randn(NEl, d, d_ff, **f32).bfloat16()
+    b1, b2 = torch.zeros(NEl, d_ff, **f32), torch.zeros(NEl, d, **f32)
+    w_router = torch.randn(KW, d, **f32)
+    loss = torch.full((V,), 7.0, dtype=torch.float64, device="cuda")
+    layer.forward(x, W1t, b1, W2t, b2, out, loss, w_router=w_router, train=True)
+    grads = [torch.full(s, 3.0, **f32) for s in ((NEl, d, d_ff), (NEl, d_ff), (NEl, d_ff, d), (NEl, d), (KW, d))]
+    layer.backward(torch.empty_like(x), torch.empty_like(x), W1t.transpose(1, 2).contiguous(),
+                   W2t.transpose(1, 2).contiguous(), *grads[:4], dW_router=grads[4])
+    torch.cuda.synchronize()
+    assert layer.get_error() == 0
+    assert torch.equal(loss.cpu(), torch.full((V,), 7.0, dtype=torch.float64))    # not written
+    for gt in grads:
+        assert not gt.any()
+    with pytest.raises(SmileError):
+        layer.aux_loss(layer._view.stats, loss)
+    layer.close()
