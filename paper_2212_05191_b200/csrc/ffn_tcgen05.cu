@@ -157,35 +157,37 @@ struct TileInfo {
     int64_t b_row;
 };
 
-// Tile `tile` of the work list: 4 * CG * NPAIR strips (32 rows each) of one expert x BN
-// columns (with NPAIR = 2 the cluster's two pairs take consecutive 8-strip M-tiles and
-// share the N-tile).
+// Tile `tile` of the work list: 4 * CG * NSUB strips (32 rows each) of one expert x BN
+// columns.  With NSUB = 2 a CTA pair computes two M = 256 sub-tiles (consecutive 8-strip
+// M-tiles of the expert) that share the N-tile: `sub` selects one.
 // For a CTA pair, `rank` selects this CTA's 4 strips (its 128 rows of the M = 256 MMA)
 // and its BN/2-row half of B.  Strip u0 + j of the expert goes to TMEM lanes 32j..32j+31;
 // a missing strip (the expert's last tile) has 0 rows and points at row 0 (loaded,
 // computed, never stored).
-template <int CG, int NPAIR>
+template <int CG, int NSUB>
 __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref, int tile, int ntn, int rank,
-                                              int pair) {
+                                              int sub) {
     TileInfo t;
     t.nt = tile % ntn;
     const int mtg = tile / ntn;
     const int NE = a.nseg / a.S;
     t.E = tile_segment(s_pref, NE, mtg);
-    t.u0 = (((mtg - s_pref[t.E]) * NPAIR + pair) * CG + rank) * 4;
+    t.u0 = (((mtg - s_pref[t.E]) * NSUB + sub) * CG + rank) * 4;
     t.b_row = (int64_t)t.E * a.N + (int64_t)t.nt * a.BN + rank * (a.BN / CG);
     return t;
 }
 
-// NPAIR = 2 (CG = 2): a cluster of 4 = two pairs on consecutive M-tiles of one expert and
-// the same N-tile; each CTA TMA-loads a quarter of the B tile and multicasts it to its
-// counterpart in the other pair, so B's L2 -> SM traffic halves (the FFN GEMMs are
-// bound by that path, not by the MMAs).  A stage is refilled only after BOTH pairs'
-// MMAs released it (empty barriers count one commit per pair).
 // CG = 1: one CTA per tile (M = 128).  CG = 2: a CTA pair (cluster of 2) per tile
 // (M = 256, tcgen05.mma.cta_group::2 issued by the leader), each CTA loading half of A
 // and half of B, which halves the shared-memory operand traffic per SM.
-template <int CG, int NPAIR, bool DG>
+// NSUB = 2 (CG = 2): every stage holds two A tiles and one B tile; the two sub-tiles'
+// accumulators fill TMEM (2 x 256 columns), so each B byte delivered from L2 feeds twice
+// the MACs: 24 instead of 32 KB per CTA per 128 x 256 x 64 MACs.  The GEMMs are bound by
+// L2 -> SM operand delivery (profiles/r01_ffn_epilogue_diagnostics.md).  The price is the
+// double-buffered accumulator: the epilogue drains sub-tile 0 first and releases it, and
+// the next tile's MMAs run the first K blocks on sub-tile 0 alone until sub-tile 1 is
+// drained too.
+template <int CG, int NSUB, bool DG>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA128,
                  const __grid_constant__ CUtensorMap mapB,
@@ -197,7 +199,8 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     const int STAGES = a.stages;
     const int nbox = a.mode == EPI_BIAS_SAVE ? 2 : 1;
     const int b_stage_bytes = B_BYTES_MAX / CG;
-    unsigned char *sB = sA + STAGES * A_BYTES;
+    constexpr int A_STAGE = NSUB * A_BYTES;                           // NSUB A tiles per stage
+    unsigned char *sB = sA + STAGES * A_STAGE;
     unsigned char *sOut = sB + STAGES * b_stage_bytes;                // EPI_WARPS x nbox x 2 KB
     uint64_t *bars = reinterpret_cast<uint64_t *>(
         sOut + (a.tma_store ? nbox * EPI_WARPS * OUT_BOX_BYTES * (a.box64 ? 2 : 1) : 0));
@@ -205,19 +208,18 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
     int *s_warp = reinterpret_cast<int *>(tmem_holder + 4);
     int *s_pref = s_warp + 32;
-    int *s_cnt = s_pref + MAXSEG + 1;                                 // [nseg] segment row counts
+    int *s_cnt = s_pref + a.nseg + 1;                                 // [nseg] segment row counts
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int CS = CG * NPAIR;                              // cluster size
-    const int crank = CS > 1 ? (int)cluster_ctarank() : 0;
-    const int rank = crank % CG, pair = crank / CG;
+    constexpr int CS = CG;                                      // cluster size
+    const int rank = CS > 1 ? (int)cluster_ctarank() : 0;
     const bool leader = rank == 0;
-    const uint32_t lead = (uint32_t)(pair * CG);                // cluster rank of this pair's leader
+    const uint32_t lead = 0;                                    // cluster rank of the pair's leader
     const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
-            mbar_init(smem_u32(&empty[s]), NPAIR);
+            mbar_init(smem_u32(&empty[s]), 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&tfull[s]), 1);
@@ -247,7 +249,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     }
     for (int g = threadIdx.x; g < a.nseg; g += blockDim.x) s_cnt[g] = a.counts[g];
     __syncthreads();
-    expert_tile_prefix<4 * CG * NPAIR>(s_cnt, a.nseg / a.S, a.S, a.e, s_pref, s_warp);   // ends with __syncthreads
+    expert_tile_prefix<4 * CG * NSUB>(s_cnt, a.nseg / a.S, a.S, a.e, s_pref, s_warp);   // ends with __syncthreads
     if (CS > 1) cluster_sync_all();                          // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
@@ -262,51 +264,57 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = cid; tile < total; tile += ncl) {
-                const TileInfo t = tile_info<CG, NPAIR>(a, s_pref, tile, ntn, rank, pair);
-                // A: one 128-row box when the tile's 4 strips are consecutive rows (fewer
+                // A: one 128-row box when a sub-tile's 4 strips are consecutive rows (fewer
                 // TMA requests: the L2 -> SM path is what bounds these GEMMs), else four
                 // 32-row strip boxes (4 KB each, stacked = the same SW128 tile); rows
                 // resolved once per tile
-                int srow[4];
+                int srow[NSUB][4];
+                bool contig[NSUB];
+                int64_t b_row = 0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    int64_t r;
-                    int nr;
-                    expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + j, r, nr);
-                    srow[j] = (int)r;
+                for (int u = 0; u < NSUB; ++u) {
+                    const TileInfo t = tile_info<CG, NSUB>(a, s_pref, tile, ntn, rank, u);
+                    b_row = t.b_row;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        int64_t r;
+                        int nr;
+                        expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + j, r, nr);
+                        srow[u][j] = (int)r;
+                    }
+                    contig[u] = srow[u][1] == srow[u][0] + 32 && srow[u][2] == srow[u][0] + 64 &&
+                                srow[u][3] == srow[u][0] + 96;
                 }
-                const bool contig = srow[1] == srow[0] + 32 && srow[2] == srow[0] + 64 && srow[3] == srow[0] + 96;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full[stage]);
+                    unsigned char *sAs = sA + stage * A_STAGE;
                     if (CG == 1) {
-                        mbar_arrive_tx(fb, A_BYTES + b_bytes);
-                        if (contig)
-                            tma_load_2d(smem_u32(sA + stage * A_BYTES), &mapA128, kb * BK, srow[0], fb);
-                        else
-                            for (int j = 0; j < 4; ++j)
-                                tma_load_2d(smem_u32(sA + stage * A_BYTES + j * (A_BYTES / 4)), &mapA, kb * BK,
-                                            srow[j], fb);
-                        tma_load_2d(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)t.b_row, fb);
+                        mbar_arrive_tx(fb, A_STAGE + b_bytes);
+#pragma unroll
+                        for (int u = 0; u < NSUB; ++u) {
+                            if (contig[u])
+                                tma_load_2d(smem_u32(sAs + u * A_BYTES), &mapA128, kb * BK, srow[u][0], fb);
+                            else
+                                for (int j = 0; j < 4; ++j)
+                                    tma_load_2d(smem_u32(sAs + u * A_BYTES + j * (A_BYTES / 4)), &mapA, kb * BK,
+                                                srow[u][j], fb);
+                        }
+                        tma_load_2d(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)b_row, fb);
                     } else {
                         // the leader's full barrier counts the bytes of both CTAs' loads
-                        if (leader) mbar_arrive_tx(fb, CG * (A_BYTES + b_bytes));
+                        if (leader) mbar_arrive_tx(fb, CG * (A_STAGE + b_bytes));
                         const uint32_t fbl = mapa_shared(fb, lead);
-                        if (contig)
-                            tma_load_2d_pair(smem_u32(sA + stage * A_BYTES), &mapA128, kb * BK, srow[0], fbl);
-                        else
-                            for (int j = 0; j < 4; ++j)
-                                tma_load_2d_pair(smem_u32(sA + stage * A_BYTES + j * (A_BYTES / 4)), &mapA,
-                                                 kb * BK, srow[j], fbl);
-                        if (NPAIR == 1) {
-                            tma_load_2d_pair(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)t.b_row, fbl);
-                        } else {
-                            // quarter `pair` of this CTA's B half, to the same rank in both pairs
-                            const int qrows = a.BN / (CG * NPAIR);
-                            tma_load_2d_pair_mc(smem_u32(sB + stage * b_stage_bytes + pair * qrows * 128), &mapB,
-                                                kb * BK, (int)t.b_row + pair * qrows, fbl,
-                                                (uint16_t)((1u << rank) | (1u << (CG + rank))));
+#pragma unroll
+                        for (int u = 0; u < NSUB; ++u) {
+                            if (contig[u])
+                                tma_load_2d_pair(smem_u32(sAs + u * A_BYTES), &mapA128, kb * BK, srow[u][0], fbl);
+                            else
+                                for (int j = 0; j < 4; ++j)
+                                    tma_load_2d_pair(smem_u32(sAs + u * A_BYTES + j * (A_BYTES / 4)), &mapA,
+                                                     kb * BK, srow[u][j], fbl);
                         }
+                        tma_load_2d_pair(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)b_row, fbl);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -319,31 +327,71 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int tile = cid; tile < total; tile += ncl, ++it) {
-                const int acc = it & 1;
-                const uint32_t use = (uint32_t)(it >> 1) & 1;
-                mbar_wait(smem_u32(&tempty[acc]), use ^ 1);
-                tc_fence_after();
+            // the 4 K = 16 MMAs of one K block of sub-tile / buffer `acc` on stage `st`
+            auto kblock = [&](int st, int u, int acc, bool first) {
                 const uint32_t tmem_d = tmem_base + acc * ACC_COLS;
-                for (int kb = 0; kb < nk; ++kb) {
-                    mbar_wait(smem_u32(&full[stage]), phase);
-                    tc_fence_after();
-                    const uint64_t ad = sw128_desc(smem_u32(sA + stage * A_BYTES));
-                    const uint64_t bd = sw128_desc(smem_u32(sB + stage * b_stage_bytes));
+                const uint64_t ad = sw128_desc(smem_u32(sA + st * A_STAGE + u * A_BYTES));
+                const uint64_t bd = sw128_desc(smem_u32(sB + st * b_stage_bytes));
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {   // +32 B along K inside the 128 B swizzle atom
-                        if (CG == 1)
-                            mma_bf16(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (kb | k) ? 1u : 0u);
-                        else
-                            mma_bf16_pair(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc,
-                                          (kb | k) ? 1u : 0u);
-                    }
-                    if (CG == 1) mma_commit(smem_u32(&empty[stage]));
-                    else mma_commit_pair(smem_u32(&empty[stage]), NPAIR == 2 ? (uint16_t)0xF : (uint16_t)3);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                for (int k = 0; k < BK / 16; ++k) {   // +32 B along K inside the 128 B swizzle atom
+                    const uint32_t accum = (first && k == 0) ? 0u : 1u;
+                    if (CG == 1) mma_bf16(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, accum);
+                    else mma_bf16_pair(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, accum);
                 }
-                if (CG == 1) mma_commit(smem_u32(&tfull[acc]));
-                else mma_commit_pair(smem_u32(&tfull[acc]), (uint16_t)(3u << lead));
+            };
+            auto release = [&](uint64_t *bar) {
+                if (CG == 1) mma_commit(smem_u32(bar));
+                else mma_commit_pair(smem_u32(bar), (uint16_t)3);
+            };
+            for (int tile = cid; tile < total; tile += ncl, ++it) {
+                if (NSUB == 1) {
+                    // double-buffered accumulator: tile `it` uses buffer it & 1
+                    const int acc = it & 1;
+                    mbar_wait(smem_u32(&tempty[acc]), ((uint32_t)(it >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    for (int kb = 0; kb < nk; ++kb) {
+                        mbar_wait(smem_u32(&full[stage]), phase);
+                        tc_fence_after();
+                        kblock(stage, 0, acc, kb == 0);
+                        release(&empty[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    release(&tfull[acc]);
+                } else {
+                    // sub-tile u accumulates in buffer u; both are drained after every tile.
+                    // The first P K blocks go to sub-tile 0 alone (their stages stay held)
+                    // while the epilogue still drains sub-tile 1; then sub-tile 1 catches up.
+                    const uint32_t par = ((uint32_t)it & 1) ^ 1;
+                    const int P = min(nk, STAGES);
+                    mbar_wait(smem_u32(&tempty[0]), par);
+                    tc_fence_after();
+                    const int st0 = stage;
+                    const uint32_t ph0 = phase;
+                    for (int kb = 0; kb < P; ++kb) {
+                        mbar_wait(smem_u32(&full[stage]), phase);
+                        tc_fence_after();
+                        kblock(stage, 0, 0, kb == 0);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    mbar_wait(smem_u32(&tempty[1]), par);
+                    tc_fence_after();
+                    stage = st0;
+                    phase = ph0;
+                    for (int kb = 0; kb < P; ++kb) {
+                        kblock(stage, 1, 1, kb == 0);
+                        release(&empty[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    for (int kb = P; kb < nk; ++kb) {
+                        mbar_wait(smem_u32(&full[stage]), phase);
+                        tc_fence_after();
+                        kblock(stage, 0, 0, false);
+                        kblock(stage, 1, 1, false);
+                        release(&empty[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    release(&tfull[0]);
+                }
             }
         }
     } else if (warp >= 4) {
@@ -359,9 +407,9 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         const int c_beg = (h * nch) / 4, c_end = ((h + 1) * nch) / 4;
         int it = 0;
         unsigned char *box = sOut + (warp - 4) * nbox * OUT_BOX_BYTES * (a.box64 ? 2 : 1);
-        for (int tile = cid; tile < total; tile += ncl, ++it) {
-            const TileInfo t = tile_info<CG, NPAIR>(a, s_pref, tile, ntn, rank, pair);
-            const int acc = it & 1;
+        for (int tile = cid, sub = 0; tile < total;) {
+            const TileInfo t = tile_info<CG, NSUB>(a, s_pref, tile, ntn, rank, sub);
+            const int acc = NSUB == 2 ? sub : it & 1;
             const bool has_bias = a.mode == EPI_BIAS || a.mode == EPI_BIAS_SAVE;
             const bool act = ((a.mode == EPI_BIAS && a.gelu) || a.mode == EPI_BIAS_SAVE) && !(a.diag & 1);
             constexpr bool dgelu = DG;                      // EPI_DGELU has its own instantiation
@@ -380,7 +428,8 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             if (dgelu && c_beg < c_end && srows > 0)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) acur[i] = __ldg(aux_row + c_beg * 4 + i);
-            mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
+            if (NSUB == 1) mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
+            else if (sub == 0) mbar_wait(smem_u32(&tfull[0]), (uint32_t)it & 1);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS;
             for (int c = c_beg; c < c_end && srows > 0 && !(a.diag & 4); ++c) {
@@ -500,6 +549,11 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                 if (CG == 1) mbar_arrive(smem_u32(&tempty[acc]));
                 else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), lead));   // the leader's MMA waits on it
             }
+            if (++sub == NSUB) {
+                sub = 0;
+                tile += ncl;
+                ++it;
+            }
         }
     }
     if (warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -521,11 +575,11 @@ int pick_bn(int N) {
     return 0;
 }
 
-size_t smem_bytes(int CG, int stages, int nbox, int tma_store, int box64 = 0) {
-    return 1024 + stages * (A_BYTES + B_BYTES_MAX / CG) +
+size_t smem_bytes(int CG, int nsub, int stages, int nbox, int tma_store, int box64, int nseg) {
+    return 1024 + stages * (nsub * A_BYTES + B_BYTES_MAX / CG) +
            (tma_store ? nbox * EPI_WARPS * OUT_BOX_BYTES * (box64 ? 2 : 1) : 0) +
            (2 * stages + 4) * 8 +
-           16 + 32 * 4 + (MAXSEG + 1) * 4 + MAXSEG * 4;
+           16 + 32 * 4 + (nseg + 1) * 4 + nseg * 4;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -543,9 +597,9 @@ int pick_tma_store() {
     return v;
 }
 
-int pick_stages(int CG, int nbox, int tma_store, int box64) {
+int pick_stages(int CG, int nsub, int nbox, int tma_store, int box64, int nseg) {
     int st = 8;
-    while (st > 2 && smem_bytes(CG, st, nbox, tma_store, box64) > kSmemLimit) --st;
+    while (st > 2 && smem_bytes(CG, nsub, st, nbox, tma_store, box64, nseg) > kSmemLimit) --st;
     return st;
 }
 
@@ -559,24 +613,24 @@ int pick_cg(int num_sms, int BN) {
     return (env && num_sms >= 2 && (BN / 2) % 16 == 0) ? 2 : 1;
 }
 
-// Pairs per cluster for the CTA-pair GEMM: SMILE_FFN_PAIRS=2 (clusters of 4 sharing B by
-// multicast) or 1 (default: clusters of 2).
-int pick_npair() {
+// Sub-tiles per CTA-pair tile: SMILE_FFN_NSUB=2 (two M = 256 sub-tiles sharing each B
+// stage; TMEM holds both accumulators) or 1 (one sub-tile, double-buffered accumulator).
+int pick_nsub() {
     static int v = -1;
     if (v < 0) {
-        const char *e = getenv("SMILE_FFN_PAIRS");
+        const char *e = getenv("SMILE_FFN_NSUB");
         v = (e && e[0] == '2') ? 2 : 1;
     }
     return v;
 }
 
-template <int CG, int NPAIR, bool DG>
+template <int CG, int NSUB, bool DG>
 cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUtensorMap &mB, const CUtensorMap &mD,
                       const CUtensorMap &mD2, const TcArgs &a, size_t smem, int num_sms, cudaStream_t st) {
-    constexpr int CS = CG * NPAIR;
+    constexpr int CS = CG;
     static int grid = 0;
     if (!grid) {
-        cudaFuncSetAttribute(ffn_gemm_tcgen05<CG, NPAIR, DG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
+        cudaFuncSetAttribute(ffn_gemm_tcgen05<CG, NSUB, DG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
         grid = num_sms / CS * CS;
         // SMILE_FFN_MAX_CTAS caps the persistent grid (leaves SMs to kernels of other
         // streams, e.g. the permutes of the next chunk in the pipelined layer)
@@ -584,27 +638,10 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
             const int cap = atoi(e) / CS * CS;
             if (cap >= CS && cap < grid) grid = cap;
         }
-        if (CS > 2) {
-            // clusters of 4 need 4 free SMs in one GPC: size the grid to what can be resident
-            cudaLaunchConfig_t q;
-            memset(&q, 0, sizeof(q));
-            q.gridDim = dim3((unsigned)grid);
-            q.blockDim = dim3(NTHREADS);
-            q.dynamicSmemBytes = kSmemLimit;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-            q.attrs = at;
-            q.numAttrs = 1;
-            int ncl = 0;
-            if (cudaOccupancyMaxActiveClusters(&ncl, ffn_gemm_tcgen05<CG, NPAIR, DG>, &q) == cudaSuccess && ncl > 0 &&
-                ncl * CS < grid)
-                grid = ncl * CS;
-        }
     }
     note_launch();
     if (CS == 1) {
-        ffn_gemm_tcgen05<CG, NPAIR, DG><<<grid, NTHREADS, smem, st>>>(mA, mA128, mB, mD, mD2, a);
+        ffn_gemm_tcgen05<CG, NSUB, DG><<<grid, NTHREADS, smem, st>>>(mA, mA128, mB, mD, mD2, a);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg;
@@ -620,7 +657,7 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<CG, NPAIR, DG>, mA, mA128, mB, mD, mD2, a);
+    return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<CG, NSUB, DG>, mA, mA128, mB, mD, mD2, a);
 }
 
 // One grouped GEMM launch: D[rows, N] = epi(A[rows, K] . B[expert][N, K]^T).
@@ -629,11 +666,11 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
                         cudaStream_t st) {
     const int BN = pick_bn(N);
     const int CG = pick_cg(f.num_sms, BN);
-    const int NPAIR = (CG == 2 && (BN / 4) % 8 == 0) ? pick_npair() : 1;
+    const int NSUB = CG == 2 ? pick_nsub() : 1;
     CUtensorMap mA, mA128, mB, mD, mD2;
     if (!make_map(&mA, A, rows_total, K, 32)) return cudaErrorNotSupported;        // 32-row strip boxes
     if (!make_map(&mA128, A, rows_total, K, BM)) return cudaErrorNotSupported;     // 128-row tile box
-    if (!make_map(&mB, B, (int64_t)NE * N, K, BN / (CG * NPAIR))) return cudaErrorNotSupported;
+    if (!make_map(&mB, B, (int64_t)NE * N, K, BN / CG)) return cudaErrorNotSupported;
     if (!make_map(&mD, D, rows_total, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorNotSupported;
     CUtensorMap mD64;
     if (!make_map(&mD64, D, rows_total, N, 32, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorNotSupported;
@@ -658,17 +695,17 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
         const bool want = e ? (e[0] == '1' && gelu) || e[0] == '2' : false;     // 2: both GEMMs
         a.box64 = (want && a.tma_store && nbox == 1 && mode != EPI_DGELU && (BN / 32) % 8 == 0) ? 1 : 0;
     }
-    a.stages = pick_stages(CG, nbox, a.tma_store, a.box64);
+    a.stages = pick_stages(CG, NSUB, nbox, a.tma_store, a.box64, a.nseg);
     if (const char *e = getenv("SMILE_FFN_STAGES")) {
         const int s = atoi(e);
         if (s >= 2 && s < a.stages) a.stages = s;
     }
     if (const char *e = getenv("SMILE_FFN_DIAG")) a.diag = atoi(e);
     a.err = nullptr;
-    const size_t smem = smem_bytes(CG, a.stages, nbox, a.tma_store, a.box64);
+    const size_t smem = smem_bytes(CG, NSUB, a.stages, nbox, a.tma_store, a.box64, a.nseg);
     const bool dg = mode == EPI_DGELU;
     if (a.box64) mD = mD64;                   // the output map with 32 x 64 SWIZZLE_128B boxes
-    if (CG == 2 && NPAIR == 2)
+    if (CG == 2 && NSUB == 2)
         return dg ? launch_tc<2, 2, true>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)
                   : launch_tc<2, 2, false>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
     if (CG == 2)

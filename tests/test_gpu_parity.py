@@ -319,6 +319,36 @@ def test_skewed_drops_full_size_sampled():
     run_and_check(case, rows=rows)
 
 
+def test_bench_launch_config_full_size_sampled():
+    """configs[1] exactly as bench.py times it: fused tensor-core router (w_router), the
+    peer-store exchange, the tcgen05 FFN, full size.  The routing is checked bit-exactly
+    against the oracle run on the GPU's own fp32 logits (which must be within fp32
+    accumulation error of the oracle's fp64 logits); outputs on sampled tokens."""
+    case = Case(2, 4, 1, 16384, 768, 3072, 2.0, dtype="bf16", fused=True, seed=4)
+    from paper_2212_05191_b200 import SmileLayer
+    layer = SmileLayer(2, 4, 1, 768, 3072, 16384, 2.0, "bf16", "bilevel")
+    layer.enable_peer_exchange()
+    layer, out, loss, err = case.run_gpu(layer=layer)
+    assert err == 0
+    g = case.gpu_tensors()
+    lg_gpu = torch.empty(case.G, case.T, case.cfg.logit_width, dtype=torch.float32, device="cuda")
+    w = layer._view
+    layer.gate_inter(g["x"], w.route, w.stats, C_ptr(w.counts1), w_router=g["w_router"], logits_out=lg_gpu)
+    torch.cuda.synchronize()
+    lg = lg_gpu.cpu().numpy()
+    ref = oracle.logits(case.x.reshape(-1, case.d), case.w_router).reshape(lg.shape)
+    np.testing.assert_allclose(lg, ref, rtol=0, atol=2e-5)
+    r = case.oracle_route(logits=lg)
+    check_route(case, layer, r, loss)
+    rs = np.random.default_rng(4)
+    keep = r.keep.reshape(-1).astype(bool)
+    rows = np.unique(np.concatenate([rs.integers(0, 8 * 16384, 64), [0, 8 * 16384 - 1],
+                                     np.flatnonzero(~keep)[:8]]))
+    got = out.float().cpu().numpy().reshape(-1, case.d)[rows]
+    assert_close_scaled(got, case.oracle_out(r, rows=rows), 2e-2, "bench config output")
+    assert (got[~keep[rows]] == 0).all()
+
+
 # ---- tcgen05 / TMEM / TMA expert FFN (bf16 product path) -------------------------------
 
 @pytest.mark.parametrize("n,m,e,T,d,d_ff,cf,mode", [
