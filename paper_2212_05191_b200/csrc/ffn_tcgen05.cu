@@ -182,11 +182,11 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref
 // and half of B, which halves the shared-memory operand traffic per SM.
 // NSUB = 2 (CG = 2): every stage holds two A tiles and one B tile; the two sub-tiles'
 // accumulators fill TMEM (2 x 256 columns), so each B byte delivered from L2 feeds twice
-// the MACs: 24 instead of 32 KB per CTA per 128 x 256 x 64 MACs.  The GEMMs are bound by
-// L2 -> SM operand delivery (profiles/r01_ffn_epilogue_diagnostics.md).  The price is the
+// the MACs: 24 instead of 32 KB per CTA per 128 x 256 x 64 MACs.  The price is the
 // double-buffered accumulator: the epilogue drains sub-tile 0 first and releases it, and
 // the next tile's MMAs run the first K blocks on sub-tile 0 alone until sub-tile 1 is
-// drained too.
+// drained too.  Measured slower at C2 (GEMM1 705 vs 572 us, GEMM2 449 vs 455 us: the main
+// loop is at the tensor peak already; profiles/r01_ffn_epilogue_diagnostics.md), so opt-in.
 template <int CG, int NSUB, bool DG>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA128,
@@ -265,7 +265,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             uint32_t phase = 0;
             for (int tile = cid; tile < total; tile += ncl) {
                 // A: one 128-row box when a sub-tile's 4 strips are consecutive rows (fewer
-                // TMA requests: the L2 -> SM path is what bounds these GEMMs), else four
+                // TMA requests), else four
                 // 32-row strip boxes (4 KB each, stacked = the same SW128 tile); rows
                 // resolved once per tile
                 int srow[NSUB][4];
