@@ -330,10 +330,14 @@ def test_bench_launch_config_full_size_sampled():
     layer.enable_peer_exchange()
     layer, out, loss, err = case.run_gpu(layer=layer)
     assert err == 0
+    # the GPU's logits from the same gate kernel on a second context (the layer's own
+    # route must stay as the forward left it: permute 1 finalises slot1)
     g = case.gpu_tensors()
     lg_gpu = torch.empty(case.G, case.T, case.cfg.logit_width, dtype=torch.float32, device="cuda")
-    w = layer._view
-    layer.gate_inter(g["x"], w.route, w.stats, C_ptr(w.counts1), w_router=g["w_router"], logits_out=lg_gpu)
+    aux = SmileLayer(2, 4, 1, 768, 3072, 16384, 2.0, "bf16", "bilevel")
+    aux.alloc_workspace()
+    w = aux._view
+    aux.gate_inter(g["x"], w.route, w.stats, C_ptr(w.counts1), w_router=g["w_router"], logits_out=lg_gpu)
     torch.cuda.synchronize()
     lg = lg_gpu.cpu().numpy()
     ref = oracle.logits(case.x.reshape(-1, case.d), case.w_router).reshape(lg.shape)
