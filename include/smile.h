@@ -283,10 +283,12 @@ smile_status smile_aux_loss(smile_ctx ctx, const smile_stats *stats, double alph
  * the forward route (capacity slots and drops of the forward are reused, nothing is
  * re-routed), and dX travels the return route. */
 
-/* Forward of the expert FFN that also stores the pre-activation A1 = X W1 + b1 (dtype,
- * [V, S, e, Cseg, d_ff]) that GELU' needs in the backward. */
+/* Forward of the expert FFN that also stores Gp = GELU'(A1), the activation derivative at
+ * the pre-activation A1 = X W1 + b1 (dtype, [V, S, e, Cseg, d_ff]), which is all the
+ * backward needs of A1 (dZ = dH . GELU'(A1)); computed in GEMM 1's epilogue from the same
+ * erf evaluation as H = GELU(A1). */
 smile_status smile_expert_ffn_train(smile_ctx ctx, const void *X, const int32_t *counts, const void *W1t,
-                                    const float *b1, const void *W2t, const float *b2, void *A1_ws, void *H_ws,
+                                    const float *b1, const void *W2t, const float *b2, void *Gp_ws, void *H_ws,
                                     void *Y, void *stream);
 
 /* a16 + a19 (router part): combine backward at the source.  gout [V, T, d] = dJ/dout;
@@ -306,15 +308,15 @@ smile_status smile_dispatch_grad(smile_ctx ctx, const void *drecv1, const int32_
                                  const int32_t *slot2, void *dsend2, void *stream);
 
 /* a17: backward of every resident expert over its segments.  X, dY [V, S, e, Cseg, d];
- * A1, H [V, S, e, Cseg, d_ff] saved by smile_expert_ffn_train; W1 [V*e, d, d_ff] and
- * W2 [V*e, d_ff, d] in their math layouts (the transposes of the forward's W1t / W2t).
- * Writes dZ_ws = (dY W2^T) . GELU'(A1) [V, S, e, Cseg, d_ff] (may alias A1),
+ * Gp = GELU'(A1), H [V, S, e, Cseg, d_ff] saved by smile_expert_ffn_train; W1 [V*e, d, d_ff]
+ * and W2 [V*e, d_ff, d] in their math layouts (the transposes of the forward's W1t / W2t).
+ * Writes dZ_ws = (dY W2^T) . Gp [V, S, e, Cseg, d_ff] (may alias Gp),
  * dX = dZ W1^T [V, S, e, Cseg, d] and fp32 dW1 [V*e, d, d_ff], db1 [V*e, d_ff],
  * dW2 [V*e, d_ff, d], db2 [V*e, d] summed over the valid rows.  dX may alias dY (every
  * read of dY precedes the dX GEMM).  bf16: dZ, dX on tcgen05, and dW1, dW2 too when d
  * and d_ff are multiples of 128 (MN-major operands; else SIMT); biases by fixed-order
  * two-pass column sums (deterministic). */
-smile_status smile_expert_ffn_bwd(smile_ctx ctx, const void *X, const int32_t *counts, const void *A1,
+smile_status smile_expert_ffn_bwd(smile_ctx ctx, const void *X, const int32_t *counts, const void *Gp,
                                   const void *H, const void *dY, const void *W1, const void *W2, void *dZ_ws,
                                   void *dX, float *dW1, float *db1, float *dW2, float *db2, void *stream);
 
@@ -342,7 +344,7 @@ typedef struct {
     double *loss;             /* [V] */
     double alpha, beta;
     void *ws;                 /* smile_sizes.ws_bytes bytes, 256-byte aligned */
-    int32_t train;            /* != 0: also save what smile_backward needs (A1, router logits) */
+    int32_t train;            /* != 0: also save what smile_backward needs (GELU'(A1), router logits) */
 } smile_layer_io;
 
 /* Gradients of one layer (smile_backward).  gout [V, T, d] dtype in; dx [V, T, d] dtype,
@@ -368,7 +370,7 @@ typedef struct {
     int32_t *rcounts;                       /* [V, S, e] valid rows per FFN segment */
     void *ffn_in; void *H; void *Y;         /* [V, S, e, Cseg, d|d_ff] */
     void *ret2; void *ret1; void *back1;    /* return-path buffers */
-    void *A1;                               /* [V, S, e, Cseg, d_ff] pre-activation (train) */
+    void *A1;                               /* [V, S, e, Cseg, d_ff] GELU'(pre-activation) (train) */
     float *logits; float *dlogits;          /* [V, T, KW] saved logits (train), their gradient */
     void *rpartial;                         /* router-gradient partial sums */
     void *flags;                            /* peer-exchange barrier flags */

@@ -158,97 +158,136 @@ __global__ void combine_bwd_kernel(CombineBwdArgs a) {
     }
 }
 
-// a19 router: dx[t, c] += sum_k dlogits[t, k] W[k, c]; partial[chunk, k, c] = sum over the
-// chunk's tokens of dlogits[t, k] x[t, c] (fixed order).  A thread owns RB_C adjacent
-// columns (one 16-byte vector of x / dx: 8 bf16 or 4 fp32); the chunk's dlogits are
-// staged in smem 64 tokens at a time and RB_U tokens' x and dx vectors are loaded before
-// any is used (the kernel is a stream over x and dx).
-constexpr int kRbTok = 256, kRbK = 8, kRbU = 4, kRbThreads = 128;
+// a19 router, two streams (each with few registers, so many tokens stay in flight):
+//   router_dx_kernel:  dx[t, c] += sum_k dlogits[t, k] W[k, c]   (reads + writes dx)
+//   router_dw_kernel:  partial[chunk, k, c] = sum over the chunk's tokens of
+//                      dlogits[t, k] x[t, c] (fixed order)       (reads x)
+// A thread owns RB_C adjacent columns (one 16-byte vector: 8 bf16 or 4 fp32) of kRbTok
+// tokens; router rows go kRbK at a time (W / the accumulators in registers), and kRbU
+// tokens' vectors are loaded before any is used.  The chunk's dlogits are staged in smem
+// once per pass (broadcast reads in the token loop).
+constexpr int kRbTok = 256, kRbK = 8, kRbU = 8, kRbUw = 16, kRbThreads = 128;   // kRbUw: dW stream (reads only)
 
 template <bool BF16>
-__global__ void __launch_bounds__(kRbThreads) router_bwd_kernel(RouterBwdArgs a) {
-    constexpr int RB_C = BF16 ? 8 : 4;
-    __shared__ float s_dl[64][kRbK];
+__device__ __forceinline__ void vec_to_float(const uint4 &v, float *f) {
+    if (BF16) {
+        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+            const float2 t = __bfloat1622float2(h[z]);
+            f[2 * z] = t.x;
+            f[2 * z + 1] = t.y;
+        }
+    } else {
+        const float *t = reinterpret_cast<const float *>(&v);
+#pragma unroll
+        for (int z = 0; z < 4; ++z) f[z] = t[z];
+    }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kRbThreads) router_dx_kernel(RouterBwdArgs a) {
+    constexpr int RB_C = BF16 ? 8 : 4, EB = BF16 ? 2 : 4;
+    __shared__ float s_dl[kRbTok][kRbK];
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * RB_C;
+    const bool ok = c < a.d;
     const int64_t t0 = (int64_t)blockIdx.y * kRbTok;
     const int64_t t1 = (t0 + kRbTok < a.rows) ? t0 + kRbTok : a.rows;
-    const bool ok = c < a.d;
+    char *__restrict__ dx = static_cast<char *>(a.dx);
     for (int k0 = 0; k0 < a.KW; k0 += kRbK) {
         const int nk = min(kRbK, a.KW - k0);
-        float acc[kRbK][RB_C], w[kRbK][RB_C];
+        __syncthreads();
+        for (int z = threadIdx.x; z < kRbTok * kRbK; z += blockDim.x) {
+            const int tt = z / kRbK, k = z % kRbK;
+            s_dl[tt][k] = (t0 + tt < t1 && k < nk) ? a.dlogits[(t0 + tt) * a.KW + k0 + k] : 0.f;
+        }
+        __syncthreads();
+        if (!ok) continue;
+        float w[kRbK][RB_C];
 #pragma unroll
         for (int k = 0; k < kRbK; ++k)
 #pragma unroll
-            for (int j = 0; j < RB_C; ++j) {
-                acc[k][j] = 0.f;
-                w[k][j] = (k < nk && ok) ? a.w[(int64_t)(k0 + k) * a.d + c + j] : 0.f;
-            }
-        for (int64_t tb = t0; tb < t1; tb += 64) {
-            __syncthreads();
-            for (int z = threadIdx.x; z < 64 * kRbK; z += blockDim.x) {
-                const int tt = z / kRbK, k = z % kRbK;
-                s_dl[tt][k] = (tb + tt < t1 && k < nk) ? a.dlogits[(tb + tt) * a.KW + k0 + k] : 0.f;
-            }
-            __syncthreads();
-            if (!ok) continue;
-            const int nt = (int)((t1 - tb) < 64 ? (t1 - tb) : 64);
-            for (int tt0 = 0; tt0 < nt; tt0 += kRbU) {
-                uint4 xv[kRbU], dv[kRbU];
+            for (int j = 0; j < RB_C; ++j) w[k][j] = k < nk ? a.w[(int64_t)(k0 + k) * a.d + c + j] : 0.f;
+        for (int64_t tb = t0; tb < t1; tb += kRbU) {
+            uint4 dv[kRbU];
 #pragma unroll
-                for (int u = 0; u < kRbU; ++u) {
-                    const int64_t t = tb + tt0 + u;
-                    if (tt0 + u < nt) {
-                        xv[u] = *reinterpret_cast<const uint4 *>(static_cast<const char *>(a.x) + (t * a.d + c) * (BF16 ? 2 : 4));
-                        dv[u] = *reinterpret_cast<const uint4 *>(static_cast<const char *>(a.dx) + (t * a.d + c) * (BF16 ? 2 : 4));
-                    } else {
-                        xv[u] = dv[u] = make_uint4(0, 0, 0, 0);
-                    }
+            for (int u = 0; u < kRbU; ++u)
+                dv[u] = tb + u < t1 ? *reinterpret_cast<const uint4 *>(dx + ((tb + u) * a.d + c) * EB)
+                                    : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < kRbU; ++u) {
+                if (tb + u >= t1) break;
+                const float *dl = s_dl[tb + u - t0];
+                float df[RB_C];
+                vec_to_float<BF16>(dv[u], df);
+#pragma unroll
+                for (int k = 0; k < kRbK; ++k) {
+                    const float l = dl[k];            // 0 for k >= nk
+#pragma unroll
+                    for (int j = 0; j < RB_C; ++j) df[j] = fmaf(l, w[k][j], df[j]);
                 }
+                uint4 o;
+                if (BF16) {
+                    __nv_bfloat162 *ho = reinterpret_cast<__nv_bfloat162 *>(&o);
 #pragma unroll
-                for (int u = 0; u < kRbU; ++u) {
-                    if (tt0 + u >= nt) break;
-                    float xf[RB_C], df[RB_C];
-                    if (BF16) {
-                        const __nv_bfloat162 *hx = reinterpret_cast<const __nv_bfloat162 *>(&xv[u]);
-                        const __nv_bfloat162 *hd = reinterpret_cast<const __nv_bfloat162 *>(&dv[u]);
+                    for (int z = 0; z < 4; ++z) ho[z] = __floats2bfloat162_rn(df[2 * z], df[2 * z + 1]);
+                } else {
+                    float *fo = reinterpret_cast<float *>(&o);
 #pragma unroll
-                        for (int z = 0; z < RB_C / 2; ++z) {
-                            const float2 fx = __bfloat1622float2(hx[z]), fd = __bfloat1622float2(hd[z]);
-                            xf[2 * z] = fx.x; xf[2 * z + 1] = fx.y; df[2 * z] = fd.x; df[2 * z + 1] = fd.y;
-                        }
-                    } else {
-                        const float *fx = reinterpret_cast<const float *>(&xv[u]);
-                        const float *fd = reinterpret_cast<const float *>(&dv[u]);
+                    for (int z = 0; z < 4; ++z) fo[z] = df[z];
+                }
+                *reinterpret_cast<uint4 *>(dx + ((tb + u) * a.d + c) * EB) = o;
+            }
+        }
+    }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kRbThreads) router_dw_kernel(RouterBwdArgs a) {
+    constexpr int RB_C = BF16 ? 8 : 4, EB = BF16 ? 2 : 4;
+    __shared__ float s_dl[kRbTok][kRbK];
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * RB_C;
+    const bool ok = c < a.d;
+    const int64_t t0 = (int64_t)blockIdx.y * kRbTok;
+    const int64_t t1 = (t0 + kRbTok < a.rows) ? t0 + kRbTok : a.rows;
+    const char *__restrict__ x = static_cast<const char *>(a.x);
+    for (int k0 = 0; k0 < a.KW; k0 += kRbK) {
+        const int nk = min(kRbK, a.KW - k0);
+        __syncthreads();
+        for (int z = threadIdx.x; z < kRbTok * kRbK; z += blockDim.x) {
+            const int tt = z / kRbK, k = z % kRbK;
+            s_dl[tt][k] = (t0 + tt < t1 && k < nk) ? a.dlogits[(t0 + tt) * a.KW + k0 + k] : 0.f;
+        }
+        __syncthreads();
+        if (!ok) continue;
+        float acc[kRbK][RB_C];
 #pragma unroll
-                        for (int z = 0; z < RB_C; ++z) { xf[z] = fx[z]; df[z] = fd[z]; }
-                    }
+        for (int k = 0; k < kRbK; ++k)
 #pragma unroll
-                    for (int k = 0; k < kRbK; ++k) {
-                        const float dl = s_dl[tt0 + u][k];
+            for (int j = 0; j < RB_C; ++j) acc[k][j] = 0.f;
+        for (int64_t tb = t0; tb < t1; tb += kRbUw) {
+            uint4 xv[kRbUw];
 #pragma unroll
-                        for (int j = 0; j < RB_C; ++j) {
-                            acc[k][j] = fmaf(dl, xf[j], acc[k][j]);
-                            df[j] = fmaf(dl, w[k][j], df[j]);
-                        }
-                    }
-                    uint4 o;
-                    if (BF16) {
-                        __nv_bfloat162 *ho = reinterpret_cast<__nv_bfloat162 *>(&o);
+            for (int u = 0; u < kRbUw; ++u)
+                xv[u] = tb + u < t1 ? __ldg(reinterpret_cast<const uint4 *>(x + ((tb + u) * a.d + c) * EB))
+                                    : make_uint4(0, 0, 0, 0);
 #pragma unroll
-                        for (int z = 0; z < RB_C / 2; ++z) ho[z] = __floats2bfloat162_rn(df[2 * z], df[2 * z + 1]);
-                    } else {
-                        float *fo = reinterpret_cast<float *>(&o);
+            for (int u = 0; u < kRbUw; ++u) {
+                if (tb + u >= t1) break;
+                const float *dl = s_dl[tb + u - t0];
+                float xf[RB_C];
+                vec_to_float<BF16>(xv[u], xf);
 #pragma unroll
-                        for (int z = 0; z < RB_C; ++z) fo[z] = df[z];
-                    }
-                    *reinterpret_cast<uint4 *>(static_cast<char *>(a.dx) + ((tb + tt0 + u) * a.d + c) * (BF16 ? 2 : 4)) = o;
+                for (int k = 0; k < kRbK; ++k) {
+                    const float l = dl[k];
+#pragma unroll
+                    for (int j = 0; j < RB_C; ++j) acc[k][j] = fmaf(l, xf[j], acc[k][j]);
                 }
             }
         }
-        if (ok)
-            for (int k = 0; k < nk; ++k)
+        for (int k = 0; k < nk; ++k)
 #pragma unroll
-                for (int j = 0; j < RB_C; ++j) a.partial[((int64_t)blockIdx.y * a.KW + k0 + k) * a.d + c + j] = acc[k][j];
+            for (int j = 0; j < RB_C; ++j) a.partial[((int64_t)blockIdx.y * a.KW + k0 + k) * a.d + c + j] = acc[k][j];
     }
 }
 
@@ -304,8 +343,11 @@ void launch_router_bwd(const RouterBwdArgs &a0, cudaStream_t st) {
     thr = thr < 32 ? 32 : (thr > kRbThreads ? kRbThreads : thr);
     dim3 grid((a.d + thr * per - 1) / (thr * per), a.nchunk);
     note_launch();
-    if (a.bf16) router_bwd_kernel<true><<<grid, thr, 0, st>>>(a);
-    else router_bwd_kernel<false><<<grid, thr, 0, st>>>(a);
+    if (a.bf16) router_dw_kernel<true><<<grid, thr, 0, st>>>(a);
+    else router_dw_kernel<false><<<grid, thr, 0, st>>>(a);
+    note_launch();
+    if (a.bf16) router_dx_kernel<true><<<grid, thr, 0, st>>>(a);
+    else router_dx_kernel<false><<<grid, thr, 0, st>>>(a);
     note_launch();
     router_bwd_reduce<<<(int)(((int64_t)a.KW * a.d + 31) / 32), 256, 0, st>>>(a);
 }

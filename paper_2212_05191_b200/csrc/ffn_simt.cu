@@ -16,8 +16,9 @@ namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16, NTHR = 256, MAXSEG = 4096;
 
-// mode: 0 = act(acc + bias) (act = GELU when gelu), 1 = also D2 = acc + bias (training),
-//       2 = acc * GELU'(aux) (backward dZ), 3 = acc (backward dX).
+// mode: 0 = act(acc + bias) (act = GELU when gelu), 1 = also D2 = GELU'(acc + bias)
+//       (training: the activation derivative the backward needs), 2 = acc * aux (backward
+//       dZ = dH . GELU'(A1) with aux = the saved GELU'(A1)), 3 = acc (backward dX).
 struct GemmArgs {
     const void *A; const void *B; const float *bias; void *D; const int32_t *counts;
     int nseg, e, S; int64_t Cseg; int N, K; int gelu; int bf16;
@@ -100,9 +101,9 @@ __global__ void __launch_bounds__(NTHR) grouped_gemm_simt(GemmArgs a) {
                 const int64_t o = (row0 + r) * a.N + n;
                 float y = acc[i][j];
                 if (a.mode <= 1) y += a.bias[expert * a.N + n];
-                if (a.mode == 1) st(a.D2, o, y, a.bf16);
+                if (a.mode == 1) st(a.D2, o, gelu_grad(y), a.bf16);
                 if ((a.mode == 0 && a.gelu) || a.mode == 1) y = gelu_erf(y);
-                if (a.mode == 2) y *= gelu_grad(ld(a.aux, o, a.bf16));
+                if (a.mode == 2) y *= ld(a.aux, o, a.bf16);
                 st(a.D, o, y, a.bf16);
             }
         }

@@ -50,7 +50,7 @@ struct TcArgs {
     int N, K, BN;
     int gelu;
     int mode;                  // EPI_* below
-    const __nv_bfloat16 *aux;  // EPI_DGELU: the saved pre-activation A1 [rows_total, N]
+    const __nv_bfloat16 *aux;  // EPI_DGELU: the saved GELU'(A1) [rows_total, N]
     int stages;                // smem pipeline depth
     int tma_store;             // 1: full 32 x 32 boxes leave through smem + TMA; 0: st.global from registers
     int box64;                 // 1: 32 x 64 boxes (two chunks per TMA store; every warp owns 2k chunks)
@@ -62,8 +62,9 @@ struct TcArgs {
 
 // Epilogue modes of the grouped GEMM.
 enum { EPI_BIAS = 0,        // D = act(acc + bias), act = GELU when gelu != 0 (forward)
-       EPI_BIAS_SAVE = 1,   // D = GELU(acc + bias) and D2 = acc + bias (training forward: H and A1)
-       EPI_DGELU = 2,       // D = acc * GELU'(aux) (backward: dZ = dH . GELU'(A1))
+       EPI_BIAS_SAVE = 1,   // D = GELU(acc + bias) and D2 = GELU'(acc + bias) (training forward:
+                            // H and the activation derivative, sharing one erf evaluation)
+       EPI_DGELU = 2,       // D = acc * aux (backward: dZ = dH . GELU'(A1), aux = saved GELU'(A1))
        EPI_PLAIN = 3 };     // D = acc (backward: dX)
 
 // GELU(z) = z Phi(z) = 0.5 z + 0.5 |z| erf(|z| / sqrt 2) (R21, erf form).  erf by Abramowitz &
@@ -121,9 +122,10 @@ __device__ __forceinline__ f32x2 gelu_erf2(f32x2 z) {
     return mul2(fma2(az, erfa, z), splat2(0.5f));                          // (z + |z| erf) / 2
 }
 
-// GELU'(z) on a pair (packed fp32x2, as gelu_erf2): Phi(z) + z phi(z), Phi from the same
-// erf approximation, phi(z) = exp(-z^2 / 2) / sqrt(2 pi) via ex2.approx.
-__device__ __forceinline__ f32x2 gelu_grad2(f32x2 z) {
+// GELU(z) and GELU'(z) = Phi(z) + z phi(z) on a pair from one erf evaluation (the training
+// forward saves GELU' for the backward's dZ): Phi from the same erf approximation, phi(z) =
+// exp(-z^2 / 2) / sqrt(2 pi) via ex2.approx (|error| <= 9e-7 on GELU').
+__device__ __forceinline__ void gelu_and_grad2(f32x2 z, f32x2 &g, f32x2 &gp) {
     const f32x2 az = z & 0x7fffffff7fffffffull;
     f32x2 p = splat2(4.30638e-5f * 0.125f);
     p = fma2(p, az, splat2(2.765672e-4f * 0.17677669529663688f));
@@ -140,16 +142,16 @@ __device__ __forceinline__ f32x2 gelu_grad2(f32x2 z) {
     unpack2(p, p0, p1);
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(p0));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(p1));
-    f32x2 erfa = fma2(pack2(r0, r1), splat2(-1.0f), splat2(1.0f));       // erf(|z| / sqrt 2) >= 0
-    erfa |= z & 0x8000000080000000ull;                                    // signed: erf(z / sqrt 2)
+    f32x2 erfa = fma2(pack2(r0, r1), splat2(-1.0f), splat2(1.0f));        // erf(|z| / sqrt 2)
+    g = mul2(fma2(az, erfa, z), splat2(0.5f));                             // (z + |z| erf) / 2
+    erfa |= z & 0x8000000080000000ull;                                     // erf(z / sqrt 2)
     const f32x2 Phi = fma2(erfa, splat2(0.5f), splat2(0.5f));
-    // exp(-z^2/2) = 2^(-z^2 log2(e) / 2)
     const f32x2 ex = mul2(mul2(z, z), splat2(-0.72134752044448170f));
     float e0, e1;
     unpack2(ex, e0, e1);
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(e0));
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(e1));
-    return fma2(mul2(z, splat2(0.3989422804014327f)), pack2(e0, e1), Phi);
+    gp = fma2(mul2(z, splat2(0.3989422804014327f)), pack2(e0, e1), Phi);
 }
 
 struct TileInfo {
@@ -420,7 +422,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + q, d_row, srows);
             const int st_row = (a.diag & 8) ? (int)(d_row & 1023) : (int)d_row;   // diag 8: L2-resident store window
             const bool full_box = srows == 32 && !(a.diag & 2);
-            // EPI_DGELU: chunk c's saved pre-activation is loaded before its accumulator
+            // EPI_DGELU: chunk c's saved GELU'(A1) is loaded before its accumulator
             // columns (the first chunk's while this tile's MMAs still run)
             const uint4 *aux_row =
                 reinterpret_cast<const uint4 *>(a.aux + (d_row + (lane < srows ? lane : 0)) * (int64_t)a.N + dcol0);
@@ -449,11 +451,18 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     }
                 }
                 uint4 pk[4], pks[4];
-                if (a.mode == EPI_BIAS_SAVE) {
+                const bool save = a.mode == EPI_BIAS_SAVE;
+                if (save) {
+                    // H = GELU(z) into w, GELU'(z) into pks (one erf evaluation for both)
                     uint32_t *pw2 = reinterpret_cast<uint32_t *>(pks);
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
-                        __nv_bfloat162 hh = __floats2bfloat162_rn(w[2 * i], w[2 * i + 1]);
+                        f32x2 gg, gp;
+                        gelu_and_grad2(pack2(w[2 * i], w[2 * i + 1]), gg, gp);
+                        unpack2(gg, w[2 * i], w[2 * i + 1]);
+                        float q0, q1;
+                        unpack2(gp, q0, q1);
+                        __nv_bfloat162 hh = __floats2bfloat162_rn(q0, q1);
                         pw2[i] = *reinterpret_cast<uint32_t *>(&hh);
                     }
                 }
@@ -465,8 +474,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 #pragma unroll
                         for (int z = 0; z < 4; ++z) {
                             const float2 f = __bfloat1622float2(hh[z]);
-                            const f32x2 gg = mul2(pack2(w[8 * i + 2 * z], w[8 * i + 2 * z + 1]),
-                                                  gelu_grad2(pack2(f.x, f.y)));
+                            const f32x2 gg = mul2(pack2(w[8 * i + 2 * z], w[8 * i + 2 * z + 1]), pack2(f.x, f.y));
                             unpack2(gg, w[8 * i + 2 * z], w[8 * i + 2 * z + 1]);
                         }
                     }
@@ -475,7 +483,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     float y0 = w[2 * i], y1 = w[2 * i + 1];
-                    if (act) unpack2(gelu_erf2(pack2(y0, y1)), y0, y1);
+                    if (act && !save) unpack2(gelu_erf2(pack2(y0, y1)), y0, y1);
                     __nv_bfloat162 hh = __floats2bfloat162_rn(y0, y1);
                     pw[i] = *reinterpret_cast<uint32_t *>(&hh);
                 }
@@ -732,7 +740,7 @@ cudaError_t launch_ffn_tcgen05(const FfnArgs &f, cudaStream_t st) {
     return launch_gemm(f.H, rows_total, f.W2t, NE, f.b2, f.Y, nullptr, nullptr, f, f.d, f.d_ff, EPI_BIAS, 0, st);
 }
 
-// Training forward on tcgen05: GEMM1 also stores the pre-activation A1 (for GELU').
+// Training forward on tcgen05: GEMM1 also stores GELU'(A1) (the backward's dZ multiplier).
 cudaError_t launch_ffn_tcgen05_train(const FfnArgs &f, void *A1, cudaStream_t st) {
     if (!tc_supported(f)) return cudaErrorNotSupported;
     const int64_t rows_total = (int64_t)f.V * f.S * f.e * f.Cseg;

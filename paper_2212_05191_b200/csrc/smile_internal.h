@@ -200,7 +200,7 @@ struct FfnBwdArgs {
     float *colsum_ws;                        // bias-gradient partials (colsum_ws_bytes)
 };
 cudaError_t launch_ffn_bwd(const FfnBwdArgs &a, bool tc, cudaStream_t st);
-// Forward that also stores the pre-activation A1 = X W1 + b1 (training).
+// Forward that also stores GELU'(A1), A1 = X W1 + b1 the pre-activation (training).
 cudaError_t launch_ffn_fwd_train(const FfnArgs &a, void *A1, bool tc, cudaStream_t st);
 // Returns cudaErrorNotSupported when the shape cannot run on the tcgen05 path.
 cudaError_t launch_ffn_tcgen05(const FfnArgs &a, cudaStream_t st);
