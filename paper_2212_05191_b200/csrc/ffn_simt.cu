@@ -207,8 +207,11 @@ cudaError_t launch_ffn_bwd(const FfnBwdArgs &b, bool tc, cudaStream_t st) {
     const bool tcw = tc && wgrad_tc_supported(b.bf16, b.d, b.d_ff, b.S);
     // dZ = (dY W2^T) . GELU'(A1): B operand = W2 [NE, d_ff, d] as [N = d_ff, K = d]
     if (tc) {
+        // the dZ GEMM's epilogue also writes per-strip column sums of dZ: db1 = 1^T dZ
+        // (reduced now, before the db2 column sums reuse the workspace)
         cudaError_t e = launch_ffn_tcgen05_dgrad(b, 1, st);
         if (e != cudaSuccess) return e;
+        launch_colsum_strips(b.colsum_ws, b.db1, b.counts, NE, b.e, b.S, (int)((b.Cseg + 31) / 32), b.d_ff, st);
     } else {
         GemmArgs g1{b.dY, b.W2, nullptr, b.dZ, b.counts, nseg, b.e, b.S, b.Cseg, b.d_ff, b.d, 0, b.bf16, 2, nullptr, b.A1};
         note_launch();
@@ -238,7 +241,7 @@ cudaError_t launch_ffn_bwd(const FfnBwdArgs &b, bool tc, cudaStream_t st) {
         note_launch();
         grouped_gemm_simt<<<grid, NTHR, 0, st>>>(g2);
     }
-    // dW1 = X^T dZ [NE, d, d_ff]; db1 = 1^T dZ
+    // dW1 = X^T dZ [NE, d, d_ff]; db1 = 1^T dZ (SIMT path; the tcgen05 dZ GEMM made it above)
     if (tcw) {
         cudaError_t e = launch_wgrad_tc(b.X, b.d, b.dZ, b.d_ff, b.dW1, b.counts, b.V, b.S, b.e, b.Cseg, b.num_sms, st);
         if (e != cudaSuccess) return e;
@@ -247,7 +250,7 @@ cudaError_t launch_ffn_bwd(const FfnBwdArgs &b, bool tc, cudaStream_t st) {
         note_launch();
         wgrad_simt<<<dim3((b.d_ff + BN - 1) / BN, (b.d + BM - 1) / BM, NE), NTHR, 0, st>>>(w1);
     }
-    launch_colsum(b.dZ, b.db1, b.colsum_ws, b.counts, NE, b.e, b.S, b.Cseg, b.d_ff, b.bf16, st);
+    if (!tc) launch_colsum(b.dZ, b.db1, b.colsum_ws, b.counts, NE, b.e, b.S, b.Cseg, b.d_ff, b.bf16, st);
     return cudaGetLastError();
 }
 

@@ -54,6 +54,9 @@ struct TcArgs {
     int stages;                // smem pipeline depth
     int tma_store;             // 1: full 32 x 32 boxes leave through smem + TMA; 0: st.global from registers
     int box64;                 // 1: 32 x 64 boxes (two chunks per TMA store; every warp owns 2k chunks)
+    float *colsum;             // EPI_DGELU: per-strip column sums of D (fp32, before rounding):
+                               // colsum[(seg * nstr + strip) * N + n], or nullptr
+    int nstr;                  // strips per segment, ceil(Cseg / 32)
     int diag;                  // measurement only (SMILE_FFN_DIAG; wrong results): 1 no activation,
                                // 2 no stores, 4 no TMEM reads / epilogue math (release only),
                                // 8 TMA stores into rows [0, 1024) only (L2-resident)
@@ -154,6 +157,21 @@ __device__ __forceinline__ void gelu_and_grad2(f32x2 z, f32x2 &g, f32x2 &gp) {
     gp = fma2(mul2(z, splat2(0.3989422804014327f)), pack2(e0, e1), Phi);
 }
 
+// Column sums of a warp's 32 x 32 tile (lane = row): 31 shuffles, after which lane j holds
+// the sum of column j in v[0].  Fixed order (deterministic).
+__device__ __forceinline__ void transpose_reduce32(float (&v)[32], int lane) {
+#pragma unroll
+    for (int h = 16; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const float send = up ? v[i] : v[i + h];
+            const float keep = up ? v[i + h] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        }
+    }
+}
+
 struct TileInfo {
     int nt, E, u0;            // n-tile, expert, first strip of this CTA
     int64_t b_row;
@@ -189,7 +207,9 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref
 // the next tile's MMAs run the first K blocks on sub-tile 0 alone until sub-tile 1 is
 // drained too.  Measured slower at C2 (GEMM1 705 vs 572 us, GEMM2 449 vs 455 us: the main
 // loop is at the tensor peak already; profiles/r01_ffn_epilogue_diagnostics.md), so opt-in.
-template <int CG, int NSUB, bool DG>
+// EK: epilogue kind, one instantiation each so the forward kernel carries no backward
+// registers: 0 = EPI_BIAS / EPI_PLAIN, 1 = EPI_BIAS_SAVE, 2 = EPI_DGELU.
+template <int CG, int NSUB, int EK>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA128,
                  const __grid_constant__ CUtensorMap mapB,
@@ -199,7 +219,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;
     const int STAGES = a.stages;
-    const int nbox = a.mode == EPI_BIAS_SAVE ? 2 : 1;
+    constexpr int nbox = EK == 1 ? 2 : 1;
     const int b_stage_bytes = B_BYTES_MAX / CG;
     constexpr int A_STAGE = NSUB * A_BYTES;                           // NSUB A tiles per stage
     unsigned char *sB = sA + STAGES * A_STAGE;
@@ -414,7 +434,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             const int acc = NSUB == 2 ? sub : it & 1;
             const bool has_bias = a.mode == EPI_BIAS || a.mode == EPI_BIAS_SAVE;
             const bool act = ((a.mode == EPI_BIAS && a.gelu) || a.mode == EPI_BIAS_SAVE) && !(a.diag & 1);
-            constexpr bool dgelu = DG;                      // EPI_DGELU has its own instantiation
+            constexpr bool dgelu = EK == 2;                 // EPI_DGELU / EPI_BIAS_SAVE: own instantiations
             const float4 *bias4 = reinterpret_cast<const float4 *>(a.bias + (int64_t)t.E * a.N + (int64_t)t.nt * a.BN);
             const int64_t dcol0 = (int64_t)t.nt * a.BN;
             int64_t d_row;                                  // this warp's strip
@@ -451,7 +471,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     }
                 }
                 uint4 pk[4], pks[4];
-                const bool save = a.mode == EPI_BIAS_SAVE;
+                constexpr bool save = EK == 1;
                 if (save) {
                     // H = GELU(z) into w, GELU'(z) into pks (one erf evaluation for both)
                     uint32_t *pw2 = reinterpret_cast<uint32_t *>(pks);
@@ -486,6 +506,16 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     if (act && !save) unpack2(gelu_erf2(pack2(y0, y1)), y0, y1);
                     __nv_bfloat162 hh = __floats2bfloat162_rn(y0, y1);
                     pw[i] = *reinterpret_cast<uint32_t *>(&hh);
+                }
+                if (dgelu && a.colsum) {
+                    // db1 (a17): this strip's column sums of dZ (valid rows only)
+                    if (lane >= srows)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) w[i] = 0.f;
+                    transpose_reduce32(w, lane);
+                    const int64_t seg = d_row / a.Cseg;
+                    const int64_t u = (d_row - seg * a.Cseg) >> 5;
+                    a.colsum[(seg * a.nstr + u) * a.N + dcol0 + c * 32 + lane] = w[0];
                 }
                 if (full_box && a.tma_store && a.box64) {
                     // 32 x 64 box (SWIZZLE_128B: 16-byte unit j of row r at j ^ (r & 7)) over
@@ -632,13 +662,13 @@ int pick_nsub() {
     return v;
 }
 
-template <int CG, int NSUB, bool DG>
+template <int CG, int NSUB, int EK>
 cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUtensorMap &mB, const CUtensorMap &mD,
                       const CUtensorMap &mD2, const TcArgs &a, size_t smem, int num_sms, cudaStream_t st) {
     constexpr int CS = CG;
     static int grid = 0;
     if (!grid) {
-        cudaFuncSetAttribute(ffn_gemm_tcgen05<CG, NSUB, DG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
+        cudaFuncSetAttribute(ffn_gemm_tcgen05<CG, NSUB, EK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
         grid = num_sms / CS * CS;
         // SMILE_FFN_MAX_CTAS caps the persistent grid (leaves SMs to kernels of other
         // streams, e.g. the permutes of the next chunk in the pipelined layer)
@@ -649,7 +679,7 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
     }
     note_launch();
     if (CS == 1) {
-        ffn_gemm_tcgen05<CG, NSUB, DG><<<grid, NTHREADS, smem, st>>>(mA, mA128, mB, mD, mD2, a);
+        ffn_gemm_tcgen05<CG, NSUB, EK><<<grid, NTHREADS, smem, st>>>(mA, mA128, mB, mD, mD2, a);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg;
@@ -665,13 +695,13 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<CG, NSUB, DG>, mA, mA128, mB, mD, mD2, a);
+    return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<CG, NSUB, EK>, mA, mA128, mB, mD, mD2, a);
 }
 
 // One grouped GEMM launch: D[rows, N] = epi(A[rows, K] . B[expert][N, K]^T).
 cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE, const float *bias, void *D,
                         void *D2, const void *aux, const FfnArgs &f, int N, int K, int mode, int gelu,
-                        cudaStream_t st) {
+                        cudaStream_t st, float *colsum = nullptr) {
     const int BN = pick_bn(N);
     const int CG = pick_cg(f.num_sms, BN);
     const int NSUB = CG == 2 ? pick_nsub() : 1;
@@ -709,18 +739,20 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
         if (s >= 2 && s < a.stages) a.stages = s;
     }
     if (const char *e = getenv("SMILE_FFN_DIAG")) a.diag = atoi(e);
+    a.colsum = colsum;
+    a.nstr = (int)((f.Cseg + 31) / 32);
     a.err = nullptr;
     const size_t smem = smem_bytes(CG, NSUB, a.stages, nbox, a.tma_store, a.box64, a.nseg);
-    const bool dg = mode == EPI_DGELU;
+    const int ek = mode == EPI_DGELU ? 2 : (mode == EPI_BIAS_SAVE ? 1 : 0);
     if (a.box64) mD = mD64;                   // the output map with 32 x 64 SWIZZLE_128B boxes
-    if (CG == 2 && NSUB == 2)
-        return dg ? launch_tc<2, 2, true>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)
-                  : launch_tc<2, 2, false>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
-    if (CG == 2)
-        return dg ? launch_tc<2, 1, true>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)
-                  : launch_tc<2, 1, false>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
-    return dg ? launch_tc<1, 1, true>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)
-              : launch_tc<1, 1, false>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
+#define SMILE_LAUNCH_TC(cg, ns)                                                                    \
+    return ek == 2 ? launch_tc<cg, ns, 2>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)          \
+                   : (ek == 1 ? launch_tc<cg, ns, 1>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st) \
+                              : launch_tc<cg, ns, 0>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st))
+    if (CG == 2 && NSUB == 2) SMILE_LAUNCH_TC(2, 2);
+    if (CG == 2) SMILE_LAUNCH_TC(2, 1);
+    SMILE_LAUNCH_TC(1, 1);
+#undef SMILE_LAUNCH_TC
 }
 
 }  // namespace
@@ -761,7 +793,8 @@ cudaError_t launch_ffn_tcgen05_dgrad(const FfnBwdArgs &b, int part, cudaStream_t
     const int64_t rows_total = (int64_t)f.V * f.S * f.e * f.Cseg;
     const int NE = f.V * f.e;
     if (part == 1)
-        return launch_gemm(b.dY, rows_total, b.W2, NE, nullptr, b.dZ, nullptr, b.A1, f, f.d_ff, f.d, EPI_DGELU, 0, st);
+        return launch_gemm(b.dY, rows_total, b.W2, NE, nullptr, b.dZ, nullptr, b.A1, f, f.d_ff, f.d, EPI_DGELU, 0, st,
+                           b.colsum_ws);
     return launch_gemm(b.dZ, rows_total, b.W1, NE, nullptr, b.dX, nullptr, nullptr, f, f.d, f.d_ff, EPI_PLAIN, 0, st);
 }
 

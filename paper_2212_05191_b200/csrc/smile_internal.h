@@ -209,6 +209,10 @@ cudaError_t launch_ffn_tcgen05(const FfnArgs &a, cudaStream_t st);
 size_t colsum_ws_bytes(int NE, int S, int64_t Cseg, int maxN);
 void launch_colsum(const void *B, float *db, float *part, const int32_t *counts, int NE, int e, int S, int64_t Cseg,
                    int N, int bf16, cudaStream_t st);
+// db[E][n] = sum over the expert's valid 32-row strips of part[(g * nstr + u) * N + n]
+// (strip partials written by the dZ GEMM's epilogue), fixed order.
+void launch_colsum_strips(const float *part, float *db, const int32_t *counts, int NE, int e, int S, int nstr, int N,
+                          cudaStream_t st);
 bool wgrad_tc_supported(int bf16, int d, int d_ff, int S);
 cudaError_t launch_wgrad_tc(const void *A, int M, const void *B, int N, float *Dw, const int32_t *counts, int V, int S,
                             int e, int64_t Cseg, int num_sms, cudaStream_t st);

@@ -301,8 +301,50 @@ int pick_wg_bn(int N) {
 }  // namespace
 
 size_t colsum_ws_bytes(int NE, int S, int64_t Cseg, int maxN) {
-    const int64_t nch = (Cseg + COLSUM_ROWS - 1) / COLSUM_ROWS;
-    return (size_t)NE * S * (nch > 0 ? nch : 1) * maxN * 4;
+    // room for either layout: 128-row chunk partials (launch_colsum) or 32-row strip
+    // partials of the dZ GEMM's epilogue (launch_colsum_strips)
+    const int64_t nstr = (Cseg + 31) / 32;
+    return (size_t)NE * S * (nstr > 0 ? nstr : 1) * maxN * 4;
+}
+
+namespace {
+// Block (32 columns, expert E): warp w sums strips u = w, w + 8, ... of every segment of E
+// in order (4 loads in flight), then the 8 warp sums are added in warp order.
+__global__ void __launch_bounds__(256) colsum_strip_reduce_kernel(const float *__restrict__ part, float *db,
+                                                                  const int32_t *counts, int e, int S, int nstr,
+                                                                  int N) {
+    __shared__ float s_w[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n = blockIdx.x * 32 + lane, E = blockIdx.y;
+    const int v = E / e, k = E % e;
+    float acc = 0.f;
+    if (n < N)
+        for (int s = 0; s < S; ++s) {
+            const int g = (v * S + s) * e + k;
+            const int ns = (counts[g] + 31) / 32;
+            const float *p = part + (int64_t)g * nstr * N + n;
+            int u = w;
+            for (; u + 24 < ns; u += 32) {
+                const float a0 = p[(int64_t)u * N], a1 = p[(int64_t)(u + 8) * N];
+                const float a2 = p[(int64_t)(u + 16) * N], a3 = p[(int64_t)(u + 24) * N];
+                acc += a0; acc += a1; acc += a2; acc += a3;
+            }
+            for (; u < ns; u += 8) acc += p[(int64_t)u * N];
+        }
+    s_w[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && n < N) {
+        float t = 0.f;
+        for (int i = 0; i < 8; ++i) t += s_w[i][lane];
+        db[(int64_t)E * N + n] = t;
+    }
+}
+}  // namespace
+
+void launch_colsum_strips(const float *part, float *db, const int32_t *counts, int NE, int e, int S, int nstr, int N,
+                          cudaStream_t st) {
+    note_launch();
+    colsum_strip_reduce_kernel<<<dim3((N + 31) / 32, NE), 256, 0, st>>>(part, db, counts, e, S, nstr, N);
 }
 
 void launch_colsum(const void *B, float *db, float *part, const int32_t *counts, int NE, int e, int S, int64_t Cseg,
