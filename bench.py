@@ -794,7 +794,7 @@ def run_ours(args):
         alu_peak = 148 * 128 * 2 * clk * 1e6 / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                 "frac": achieved / alu_peak, "peak_source": f"148 SM x 128 FP32 lanes x 2 x {clk:.0f} MHz"}
-    roof["kernel"] = ("whole training step (expert FFN fwd + bwd flops / step time; wgrad on SIMT)" if main.get("train")
+    roof["kernel"] = ("whole training step (expert FFN fwd + bwd flops / step time; all six GEMMs on tcgen05)" if main.get("train")
                       else "smile_expert_ffn (2 grouped GEMM launches)")
     tr = traffic.get(f"{args.config}_{modes[0]}_ffn")
     roof["traffic"] = tr["bytes_per_step"] if tr else None

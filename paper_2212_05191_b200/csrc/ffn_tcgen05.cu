@@ -641,14 +641,14 @@ int pick_stages(int CG, int nsub, int nbox, int tma_store, int box64, int nseg) 
     return st;
 }
 
-// CTA pairs unless disabled (SMILE_FFN_CTA_PAIR=0) or the grid is odd.
-int pick_cg(int num_sms, int BN) {
-    static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("SMILE_FFN_CTA_PAIR");
-        env = (e && e[0] == '0') ? 0 : 1;
-    }
-    return (env && num_sms >= 2 && (BN / 2) % 16 == 0) ? 2 : 1;
+// CTA pairs (256-row tiles) unless an expert can hold at most 2048 rows (S * Cseg: then
+// the experts' last, partly empty tiles dominate -- C5, ~512 rows per expert: 128-row
+// tiles 3.68 vs 3.93 ms), the grid is odd, or SMILE_FFN_CTA_PAIR=0 / =1 forces it.
+int pick_cg(int num_sms, int BN, int64_t rows_per_expert) {
+    const char *e = getenv("SMILE_FFN_CTA_PAIR");          // read per launch (tests switch it)
+    const int env = e ? (e[0] == '0' ? 0 : 1) : -1;
+    const bool want = env >= 0 ? env == 1 : rows_per_expert > 2048;
+    return (want && num_sms >= 2 && (BN / 2) % 16 == 0) ? 2 : 1;
 }
 
 // Sub-tiles per CTA-pair tile: SMILE_FFN_NSUB=2 (two M = 256 sub-tiles sharing each B
@@ -703,7 +703,7 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
                         void *D2, const void *aux, const FfnArgs &f, int N, int K, int mode, int gelu,
                         cudaStream_t st, float *colsum = nullptr) {
     const int BN = pick_bn(N);
-    const int CG = pick_cg(f.num_sms, BN);
+    const int CG = pick_cg(f.num_sms, BN, (int64_t)f.S * f.Cseg);
     const int NSUB = CG == 2 ? pick_nsub() : 1;
     CUtensorMap mA, mA128, mB, mD, mD2;
     if (!make_map(&mA, A, rows_total, K, 32)) return cudaErrorNotSupported;        // 32-row strip boxes

@@ -73,7 +73,14 @@ def run_bwd(case, lam=2.0, seed=0, peer=False):
     (2, 2, 2, 700, 128, 384, 1.0, "bf16", "flat", True, "tcgen05"),     # tcgen05 wgrad, e = 2, BN 128 / 192
     (2, 4, 1, 2000, 256, 512, 1.25, "bf16", "bilevel", False, "tcgen05"),  # wgrad over many K blocks
 ])
-def test_backward_parity(n, m, e, T, d, d_ff, cf, dtype, mode, fused, ffn):
+@pytest.mark.parametrize("cta_pair", [None, "1"])
+def test_backward_parity(n, m, e, T, d, d_ff, cf, dtype, mode, fused, ffn, cta_pair, monkeypatch):
+    """cta_pair None: the library's choice (these small capacities get 128-row tiles);
+    "1": CTA-pair 256-row tiles forced (SMILE_FFN_CTA_PAIR, the path of C2-C4)."""
+    if cta_pair is not None:
+        if ffn != "tcgen05":
+            pytest.skip("CTA pairs are a tcgen05 path")
+        monkeypatch.setenv("SMILE_FFN_CTA_PAIR", cta_pair)
     case = Case(n, m, e, T, d, d_ff, cf, dtype=dtype, mode=mode, dist="skewed", seed=21, fused=fused, ffn_impl=ffn)
     r = run_bwd(case)
     assert (r.keep == 0).any()
@@ -84,9 +91,10 @@ def test_backward_parity(n, m, e, T, d, d_ff, cf, dtype, mode, fused, ffn):
     (2, 2, 2, 700, 128, 384, 1.0, "bf16", "flat", True, "tcgen05"),
     (2, 2, 2, 257, 64, 64, 0.75, "fp32", "bilevel", True, "simt"),
 ])
-def test_backward_parity_peer(n, m, e, T, d, d_ff, cf, dtype, mode, fused, ffn):
+def test_backward_parity_peer(n, m, e, T, d, d_ff, cf, dtype, mode, fused, ffn, monkeypatch):
     """The training step over the peer-store exchange (gradient rows stored at / loaded
     from their owners, every exchange a barrier): same oracle bar as the copy path."""
+    monkeypatch.setenv("SMILE_FFN_CTA_PAIR", "1")
     case = Case(n, m, e, T, d, d_ff, cf, dtype=dtype, mode=mode, dist="skewed", seed=21, fused=fused, ffn_impl=ffn)
     r = run_bwd(case, peer=True)
     assert (r.keep == 0).any()

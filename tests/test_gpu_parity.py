@@ -362,7 +362,10 @@ def test_bench_launch_config_full_size_sampled():
     (2, 2, 1, 600, 1600, 6400, 2.0, "bilevel"),   # C5 widths: BN 160 for d = 1600
     (2, 4, 8, 512, 1024, 4096, 2.0, "bilevel"),   # C4 widths, 64 experts
 ])
-def test_tcgen05_ffn(n, m, e, T, d, d_ff, cf, mode):
+@pytest.mark.parametrize("cta_pair", [None, "1"])
+def test_tcgen05_ffn(n, m, e, T, d, d_ff, cf, mode, cta_pair, monkeypatch):
+    if cta_pair is not None:
+        monkeypatch.setenv("SMILE_FFN_CTA_PAIR", cta_pair)
     run_and_check(Case(n, m, e, T, d, d_ff, cf, dtype="bf16", mode=mode, dist="skewed", seed=9, ffn_impl="tcgen05"))
 
 
