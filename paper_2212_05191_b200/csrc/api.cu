@@ -73,7 +73,7 @@ struct WsLayout {
 };
 
 static void ws_layout(const smile_shape *s, const smile_sizes *z, WsLayout *L, smile_ws_view *view,
-                      char *base) {
+                      char *base, char **rrow_out = nullptr) {
     const int64_t V = z->V, T = s->T;
     const int64_t eb = s->dtype == SMILE_BF16 ? 2 : 4;
     const int64_t rb = (int64_t)s->d * eb;
@@ -118,6 +118,8 @@ static void ws_layout(const smile_shape *s, const smile_sizes *z, WsLayout *L, s
     w.dlogits = (float *)take(V * T * z->KW * 4);
     w.rpartial = take(z->router_partial_bytes);
     w.flags = take(3 * kMaxProcs * 8);
+    char *rrow = take(bi ? ffn_rows * 4 : 0);       // internal: ret1 row of each expert input row
+    if (rrow_out) *rrow_out = rrow;
     if (L) L->total = o;
     if (view) *view = w;
 }
@@ -422,7 +424,8 @@ extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const ui
     c->xchg = xchg;
     if (xchg == SMILE_XCHG_COPY) return SMILE_OK;
     smile_ws_view w;
-    ws_layout(&c->shape, &c->sz, nullptr, &w, (char *)ws);
+    char *rrow = nullptr;
+    ws_layout(&c->shape, &c->sz, nullptr, &w, (char *)ws, &rrow);
     auto off = [&](const void *ptr) { return (int64_t)((const char *)ptr - (const char *)ws); };
     c->off_flags = off(w.flags);
     CUDA_TRY(cudaMemset(w.flags, 0, 3 * kMaxProcs * 8));
@@ -468,6 +471,7 @@ extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const ui
     pm.e = c->shape.e; pm.G = c->sz.G;
     pm.off_recv1 = off(w.recv1); pm.off_rmeta1 = bi ? off(w.rmeta1) : 0; pm.off_recv2 = bi ? off(w.recv2) : 0;
     pm.off_rcounts = off(w.rcounts); pm.off_Y = off(w.Y); pm.off_ret1 = bi ? off(w.ret1) : 0;
+    pm.off_rrow = bi ? (int64_t)(rrow - (char *)ws) : 0;
     CUDA_TRY(cudaDeviceSynchronize());
     return SMILE_OK;
 }
@@ -597,6 +601,7 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
         a.recv1 = rows_in; a.recv_meta = recv_meta; a.slot2 = slot2; a.blk_off2 = c->blk_off2;
         a.send2 = send_rows; a.V = c->sz.V; a.items = (int64_t)c->shape.n * c->sz.C1; a.rowbytes = rb;
         a.K2 = c->sz.K2; a.C2 = c->sz.C2; a.nblk = c->nblk2; a.peer = peer_of(c);
+        if (a.peer.bases) a.ret1 = static_cast<char *>(c->reg_ws) + c->peer.off_ret1;
         launch_dispatch2(a, S(stream));
         return post_launch();
     }
@@ -699,6 +704,15 @@ extern "C" smile_status smile_all2all_intra(smile_ctx c, int32_t reverse, const 
     return smile_all2all(c, 2, reverse, send_rows, recv_rows, send_cnt, recv_cnt, fwd_counts, stream);
 }
 
+// PEER + BILEVEL + tcgen05: GEMM 2 stores its rows into the intermediates' ret1 (the
+// level-2 un-permute fused into the FFN); smile_combine(2) then has nothing left to do.
+static void set_ret_direct(smile_ctx c, FfnArgs &f) {
+    if (c->xchg != SMILE_XCHG_PEER || c->shape.mode != SMILE_BILEVEL) return;
+    if (getenv("SMILE_RET_DIRECT") && getenv("SMILE_RET_DIRECT")[0] == '0') return;
+    f.ret = c->peer;
+    f.rrow = reinterpret_cast<const int32_t *>(static_cast<char *>(c->reg_ws) + c->peer.off_rrow);
+}
+
 extern "C" smile_status smile_expert_ffn(smile_ctx c, const void *X, const int32_t *counts, const void *W1t,
                                          const float *b1, const void *W2t, const float *b2, void *H_ws, void *Y,
                                          void *stream) {
@@ -711,10 +725,13 @@ extern "C" smile_status smile_expert_ffn(smile_ctx c, const void *X, const int32
     f.bf16 = c->shape.dtype == SMILE_BF16; f.num_sms = c->num_sms;
     int impl = c->shape.ffn_impl;
     if (impl == SMILE_FFN_AUTO) impl = f.bf16 ? SMILE_FFN_TCGEN05 : SMILE_FFN_SIMT;
+    c->ret_direct = false;
     if (impl == SMILE_FFN_TCGEN05) {
         if (!f.bf16) return SMILE_ENOTSUP;
+        set_ret_direct(c, f);
         cudaError_t e = launch_ffn_tcgen05(f, S(stream));
         if (e == cudaErrorNotSupported) return SMILE_ENOTSUP;
+        c->ret_direct = f.ret.bases != nullptr;
         return e == cudaSuccess ? post_launch() : SMILE_ECUDA;
     }
     if (!ffn_simt_supported(f.V * f.S * f.e, f.d, f.d_ff)) return SMILE_ENOTSUP;
@@ -738,6 +755,10 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
     }
     if (level == 2) {
         if (c->shape.mode != SMILE_BILEVEL || !recv_meta || !slot2) return SMILE_EINVAL;
+        if (c->xchg == SMILE_XCHG_PEER && c->ret_direct) {
+            c->ret_direct = false;                 // the expert FFN already stored ret1
+            return SMILE_OK;
+        }
         Combine2Args a{};
         a.ret2 = ret_rows; a.recv_meta = recv_meta; a.slot2 = slot2; a.ret1 = out; a.V = c->sz.V;
         a.items = (int64_t)c->shape.n * c->sz.C1; a.rowbytes = (int64_t)c->shape.d * (bf ? 2 : 4);
@@ -777,8 +798,11 @@ extern "C" smile_status smile_expert_ffn_train(smile_ctx c, const void *X, const
     const bool tc = ffn_use_tc(c);
     if (tc && !f.bf16) return SMILE_ENOTSUP;
     if (!tc && !ffn_simt_supported(f.V * f.S * f.e, f.d, f.d_ff)) return SMILE_ENOTSUP;
+    c->ret_direct = false;
+    if (tc) set_ret_direct(c, f);
     cudaError_t e = launch_ffn_fwd_train(f, A1_ws, tc, S(stream));
     if (e == cudaErrorNotSupported) return SMILE_ENOTSUP;
+    c->ret_direct = f.ret.bases != nullptr;
     return e == cudaSuccess ? post_launch() : SMILE_ECUDA;
 }
 

@@ -57,6 +57,12 @@ struct TcArgs {
     float *colsum;             // EPI_DGELU: per-strip column sums of D (fp32, before rounding):
                                // colsum[(seg * nstr + strip) * N + n], or nullptr
     int nstr;                  // strips per segment, ceil(Cseg / 32)
+    // GEMM 2 in the peer-store exchange: each output row goes straight to its intermediate's
+    // ret1 (row rrow[row] of process (rank0 + v) / m * m + l's workspace), not to D
+    char *const *rbases;
+    const int32_t *rrow;
+    int64_t roff_ret1;
+    int rrank0, rm, rV;
     int diag;                  // measurement only (SMILE_FFN_DIAG; wrong results): 1 no activation,
                                // 2 no stores, 4 no TMEM reads / epilogue math (release only),
                                // 8 TMA stores into rows [0, 1024) only (L2-resident)
@@ -441,6 +447,14 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             int srows;
             expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + q, d_row, srows);
             const int st_row = (a.diag & 8) ? (int)(d_row & 1023) : (int)d_row;   // diag 8: L2-resident store window
+            char *rdst = nullptr;               // ret mode: this lane's row in its intermediate's ret1
+            if (EK == 0 && a.rbases && lane < srows) {
+                const int64_t grow = d_row + lane;
+                const int64_t seg = grow / a.Cseg;                     // (v * S + l) * e + k
+                const int vv = (int)(seg / ((int64_t)a.S * a.e)), l = (int)((seg / a.e) % a.S);
+                const int u = (a.rrank0 + vv) / a.rm * a.rm + l;       // intermediate (i, l)
+                rdst = a.rbases[u / a.rV] + a.roff_ret1 + (int64_t)a.rrow[grow] * a.N * 2 + dcol0 * 2;
+            }
             const bool full_box = srows == 32 && !(a.diag & 2);
             // EPI_DGELU: chunk c's saved GELU'(A1) is loaded before its accumulator
             // columns (the first chunk's while this tile's MMAs still run)
@@ -517,7 +531,13 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     const int64_t u = (d_row - seg * a.Cseg) >> 5;
                     a.colsum[(seg * a.nstr + u) * a.N + dcol0 + c * 32 + lane] = w[0];
                 }
-                if (full_box && a.tma_store && a.box64) {
+                if (EK == 0 && a.rbases) {
+                    if (rdst) {
+                        uint4 *d4 = reinterpret_cast<uint4 *>(rdst + c * 64);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) d4[i] = pk[i];
+                    }
+                } else if (full_box && a.tma_store && a.box64) {
                     // 32 x 64 box (SWIZZLE_128B: 16-byte unit j of row r at j ^ (r & 7)) over
                     // two consecutive chunks: the first waits for the box's previous store,
                     // the second fences and issues one TMA store (128-byte row segments)
@@ -741,6 +761,10 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     if (const char *e = getenv("SMILE_FFN_DIAG")) a.diag = atoi(e);
     a.colsum = colsum;
     a.nstr = (int)((f.Cseg + 31) / 32);
+    if (mode == EPI_BIAS && !gelu && f.ret.bases) {
+        a.rbases = f.ret.bases; a.rrow = f.rrow; a.roff_ret1 = f.ret.off_ret1;
+        a.rrank0 = f.ret.rank0; a.rm = f.ret.m; a.rV = f.ret.V;
+    }
     a.err = nullptr;
     const size_t smem = smem_bytes(CG, NSUB, a.stages, nbox, a.tma_store, a.box64, a.nseg);
     const int ek = mode == EPI_DGELU ? 2 : (mode == EPI_BIAS_SAVE ? 1 : 0);

@@ -338,15 +338,22 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
             if (slot < a.C2) {
                 r.src = static_cast<const char *>(a.recv1) + g * a.rowbytes;
                 if (a.peer.bases) {
-                    // peer store into the expert rank (i, j / e), chunk (l, j % e)
+                    // peer store into the expert rank (i, j / e), chunk (l, j % e), and the
+                    // row's place in this rank's ret1 (row g), where the expert's GEMM 2
+                    // will store its output (a10 + a11 fused into the FFN)
                     const PeerMap &P = a.peer;
                     const int rk = P.rank0 + v, i = rk / P.m, l = rk % P.m;
                     const int q = i * P.m + j / P.e;
                     const int64_t row = (((int64_t)(q % P.V) * P.m + l) * P.e + j % P.e) * a.C2 + slot;
                     r.dst = P.bases[q / P.V] + P.off_recv2 + row * a.rowbytes;
+                    reinterpret_cast<int32_t *>(P.bases[q / P.V] + P.off_rrow)[row] = (int32_t)g;
                 } else {
                     r.dst = static_cast<char *>(a.send2) + (((int64_t)v * a.K2 + j) * a.C2 + slot) * a.rowbytes;
                 }
+            } else if (a.peer.bases && a.ret1) {
+                // dropped at level 2 (R8): its return row is zero (written now; the fused
+                // GEMM 2 writes only kept rows)
+                r.dst = static_cast<char *>(a.ret1) + g * a.rowbytes;
             }
         }
     } else if (m.kind == MOVE_GRAD2) {

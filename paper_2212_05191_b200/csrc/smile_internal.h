@@ -49,6 +49,7 @@ struct PeerMap {
     char *const *bases;                // [nprocs] device array
     int V, rank0, n, m, e, G;
     int64_t off_recv1, off_rmeta1, off_recv2, off_rcounts, off_Y, off_ret1;
+    int64_t off_rrow;                  // BILEVEL: [V, S, e, Cseg] i32 ret1 row of each expert input row
 };
 constexpr int kMaxProcs = 64;
 
@@ -58,6 +59,7 @@ struct smile_ctx_s {
     smile_shape shape;
     smile_sizes sz;
     int TB1 = 256;             // gate tokens per block
+    bool ret_direct = false;   // PEER: the last expert FFN stored its output in the intermediates' ret1
     int nblk1 = 0;             // gate blocks per rank
     int nblk2 = 0;             // level-2 ranking blocks per rank
     int *d_err = nullptr;      // sticky device error flag (smile_status)
@@ -132,6 +134,7 @@ void launch_meta_fill(const Dispatch1Args &a, cudaStream_t st);
 struct Dispatch2Args {
     const void *recv1; const int32_t *recv_meta; int32_t *slot2; const int32_t *blk_off2;
     void *send2; int V; int64_t items; int64_t rowbytes; int K2; int64_t C2; int nblk;
+    void *ret1;                        // PEER: level-2-dropped rows get their zero return row here
     PeerMap peer;
 };
 void launch_dispatch2(const Dispatch2Args &a, cudaStream_t st);
@@ -188,6 +191,11 @@ struct FfnArgs {
     const void *X; const int32_t *counts; const void *W1t; const float *b1; const void *W2t;
     const float *b2; void *H; void *Y; int V, S, e; int64_t Cseg; int d, d_ff; int bf16;
     int num_sms;
+    // PEER, BILEVEL (ret.bases != nullptr): GEMM 2 stores each output row straight into
+    // its intermediate's ret1 (the level-2 un-permute, a10 + a11) instead of Y, at the row
+    // permute 2 recorded in rrow [V, S, e, Cseg] (this process's workspace)
+    PeerMap ret;
+    const int32_t *rrow;
 };
 void launch_ffn_simt(const FfnArgs &a, cudaStream_t st);
 
