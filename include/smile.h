@@ -160,11 +160,13 @@ smile_status smile_get_error(smile_ctx ctx, void *stream);
  * move (no capacity padding on the wire).  One node only (CUDA IPC).
  * BILEVEL with the tcgen05 FFN: the level-2 permute also records, at the expert, the row
  * of the intermediate's ret1 each input row came from, and GEMM 2 of smile_expert_ffn /
- * smile_expert_ffn_train stores every output row there (over NVLink when the intermediate
- * is on another GPU) instead of into Y -- the intra reverse exchange (a10) and the level-2
- * un-permute (a11) happen inside the FFN's epilogue, so the following smile_combine(2) has
- * nothing left to do and returns at once; level-2-dropped rows get their zero return row
- * from the level-2 permute.  SMILE_RET_DIRECT=0 keeps Y + smile_combine(2). */
+ * smile_expert_ffn_train stores the output rows of intermediates in the same process
+ * there instead of into Y -- the intra reverse exchange (a10) and the level-2 un-permute
+ * (a11) of those rows happen inside the FFN's epilogue; the following smile_combine(2)
+ * fetches only the rows of experts in other processes (with one process it returns at
+ * once).  Level-2-dropped rows get their zero return row from the level-2 permute.
+ * (Scattered 64-byte NVLink stores from the epilogue measured slower than the combine's
+ * loads, hence the split.)  SMILE_RET_DIRECT=0 keeps Y + smile_combine(2) for all rows. */
 typedef enum { SMILE_XCHG_COPY = 0, SMILE_XCHG_PEER = 1 } smile_xchg;
 /* The 72-byte IPC description of workspace `ws` (64-byte cudaIpcMemHandle of the
  * allocation containing it + the 8-byte offset of ws inside it), to be all-gathered by

@@ -755,14 +755,15 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
     }
     if (level == 2) {
         if (c->shape.mode != SMILE_BILEVEL || !recv_meta || !slot2) return SMILE_EINVAL;
-        if (c->xchg == SMILE_XCHG_PEER && c->ret_direct) {
-            c->ret_direct = false;                 // the expert FFN already stored ret1
-            return SMILE_OK;
-        }
+        const bool skip_local = c->xchg == SMILE_XCHG_PEER && c->ret_direct;
+        c->ret_direct = false;
+        // the expert FFN stored the rows of this process's experts in ret1 already; when
+        // every node (m consecutive ranks) lies inside one process that is every row
+        if (skip_local && (c->shape.nprocs == 1 || c->sz.V % c->shape.m == 0)) return SMILE_OK;
         Combine2Args a{};
         a.ret2 = ret_rows; a.recv_meta = recv_meta; a.slot2 = slot2; a.ret1 = out; a.V = c->sz.V;
         a.items = (int64_t)c->shape.n * c->sz.C1; a.rowbytes = (int64_t)c->shape.d * (bf ? 2 : 4);
-        a.K2 = c->sz.K2; a.C2 = c->sz.C2; a.peer = peer_of(c);
+        a.K2 = c->sz.K2; a.C2 = c->sz.C2; a.peer = peer_of(c); a.skip_local = skip_local ? 1 : 0;
         launch_combine2(a, S(stream));
         return post_launch();
     }

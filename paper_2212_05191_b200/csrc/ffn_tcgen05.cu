@@ -447,13 +447,19 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             int srows;
             expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + q, d_row, srows);
             const int st_row = (a.diag & 8) ? (int)(d_row & 1023) : (int)d_row;   // diag 8: L2-resident store window
-            char *rdst = nullptr;               // ret mode: this lane's row in its intermediate's ret1
-            if (EK == 0 && a.rbases && lane < srows) {
-                const int64_t grow = d_row + lane;
-                const int64_t seg = grow / a.Cseg;                     // (v * S + l) * e + k
+            // ret mode: rows whose intermediate (i, l) lives in this process go straight to
+            // its ret1 (this lane's row: rdst); a strip is one segment, so one l and one
+            // decision per warp.  Rows for other processes' intermediates go to D (Y) as
+            // usual and smile_combine(2) fetches them over NVLink.
+            bool rlocal = false;
+            char *rdst = nullptr;
+            if (EK == 0 && a.rbases && srows > 0) {
+                const int64_t seg = d_row / a.Cseg;                    // (v * S + l) * e + k
                 const int vv = (int)(seg / ((int64_t)a.S * a.e)), l = (int)((seg / a.e) % a.S);
                 const int u = (a.rrank0 + vv) / a.rm * a.rm + l;       // intermediate (i, l)
-                rdst = a.rbases[u / a.rV] + a.roff_ret1 + (int64_t)a.rrow[grow] * a.N * 2 + dcol0 * 2;
+                rlocal = u / a.rV == a.rrank0 / a.rV;
+                if (rlocal && lane < srows)
+                    rdst = a.rbases[u / a.rV] + a.roff_ret1 + (int64_t)a.rrow[d_row + lane] * a.N * 2 + dcol0 * 2;
             }
             const bool full_box = srows == 32 && !(a.diag & 2);
             // EPI_DGELU: chunk c's saved GELU'(A1) is loaded before its accumulator
@@ -531,7 +537,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     const int64_t u = (d_row - seg * a.Cseg) >> 5;
                     a.colsum[(seg * a.nstr + u) * a.N + dcol0 + c * 32 + lane] = w[0];
                 }
-                if (EK == 0 && a.rbases) {
+                if (EK == 0 && rlocal) {
                     if (rdst) {
                         uint4 *d4 = reinterpret_cast<uint4 *>(rdst + c * 64);
 #pragma unroll

@@ -391,6 +391,10 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
                     const PeerMap &P = a.peer;
                     const int rk = P.rank0 + v, i = rk / P.m, l = rk % P.m;
                     const int q = i * P.m + j / P.e;
+                    if (a.skip_local && q / P.V == P.rank0 / P.V) {
+                        r.dst = nullptr;              // stored here by the expert's GEMM 2
+                        return r;
+                    }
                     const int64_t row = (((int64_t)(q % P.V) * P.m + l) * P.e + j % P.e) * a.C2 + s2;
                     r.src = P.bases[q / P.V] + P.off_Y + row * a.rowbytes;
                 } else {

@@ -142,6 +142,7 @@ void launch_dispatch2(const Dispatch2Args &a, cudaStream_t st);
 struct Combine2Args {
     const void *ret2; const int32_t *recv_meta; const int32_t *slot2; void *ret1;
     int V; int64_t items; int64_t rowbytes; int K2; int64_t C2;
+    int skip_local;                    // PEER: rows of experts in this process are in ret1 already
     PeerMap peer;
 };
 void launch_combine2(const Combine2Args &a, cudaStream_t st);
