@@ -497,7 +497,9 @@ def hbm_phases(res, peaks):
     out = {}
     for ph, b in res["hbm_bytes"].items():
         t = res["phase_ms"].get(ph)
-        if not t:
+        if not t or not b:
+            if ph in res["phase_ms"] and not b:
+                out[ph] = {"bytes": 0, "ms": t, "note": "no rows to move (fused into the FFN's GEMM 2)"}
             continue
         gbs = b / (t / 1e3) / 1e9
         out[ph] = {"bytes": b, "ms": t, "GB/s": gbs, "frac": gbs / peak if peak else None}
@@ -725,6 +727,12 @@ def run_ours(args):
             nvl = {"world": sum(int(c1[v, E]) for v in range(V) for E in range(c1.shape[1]) if (E // e) // V != rank) * rb}
         ffn_ms = phase_ms["ffn"] if not train else None
         ffn_tc = cfgd["dtype"] == "bf16" and args.ffn != "simt" and smb.TCGEN05_DEFAULT
+        if (mode == "bilevel" and args.exchange == "peer" and ffn_tc
+                and os.environ.get("SMILE_RET_DIRECT", "1") != "0"):
+            # GEMM 2 wrote the rows of this process's intermediates straight into ret1
+            # (a11 fused into the FFN, no extra bytes); combine2 moves only rows of experts
+            # in other processes -- the level-2 rows this process sent away
+            hbm["combine2"] = 2 * nvl.get("intra", 0)
         res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, rank_ms=rank_ms, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms,
                    t_beg=t_beg, t_end=t_end,
                    tokens=G * T, launches=launched, hbm_bytes=hbm, train=train, eager_ms=eager_ms, graph_ms=graph_ms,
