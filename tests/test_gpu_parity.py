@@ -440,3 +440,24 @@ def test_empty_input_T0(mode):
     with pytest.raises(SmileError):
         layer.aux_loss(layer._view.stats, loss)
     layer.close()
+
+
+@pytest.mark.parametrize("n,m,e,T,d,d_ff,cf", [
+    (2, 4, 1, 1000, 128, 256, 1.25),       # level-2 drops
+    (4, 2, 2, 700, 64, 128, 1.0),
+])
+def test_ret_direct_bit_identical(n, m, e, T, d, d_ff, cf, monkeypatch):
+    """Peer exchange: GEMM 2 storing its rows straight into the intermediates' ret1
+    (SMILE_RET_DIRECT, default) gives bit-identical outputs and losses to Y + combine(2)."""
+    from paper_2212_05191_b200 import SmileLayer
+    case = Case(n, m, e, T, d, d_ff, cf, dtype="bf16", dist="skewed", seed=17, fused=True)
+    layer = SmileLayer(n, m, e, d, d_ff, T, cf, "bf16", "bilevel")
+    layer.enable_peer_exchange()
+    outs = {}
+    layer.ws.fill_(0x7f)                   # garbage everywhere: ret1 must be fully rewritten
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SMILE_RET_DIRECT", flag)
+        _, out, loss, err = case.run_gpu(layer=layer)
+        assert err == 0
+        outs[flag] = (out.clone(), loss.clone())
+    assert torch.equal(outs["0"][0], outs["1"][0]) and torch.equal(outs["0"][1], outs["1"][1])
