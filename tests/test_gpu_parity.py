@@ -452,9 +452,10 @@ def test_ret_direct_bit_identical(n, m, e, T, d, d_ff, cf, monkeypatch):
     from paper_2212_05191_b200 import SmileLayer
     case = Case(n, m, e, T, d, d_ff, cf, dtype="bf16", dist="skewed", seed=17, fused=True)
     layer = SmileLayer(n, m, e, d, d_ff, T, cf, "bf16", "bilevel")
+    layer.alloc_workspace()
+    layer.ws.fill_(0x7f)                   # garbage everywhere: ret1 must be fully rewritten
     layer.enable_peer_exchange()
     outs = {}
-    layer.ws.fill_(0x7f)                   # garbage everywhere: ret1 must be fully rewritten
     for flag in ("1", "0"):
         monkeypatch.setenv("SMILE_RET_DIRECT", flag)
         _, out, loss, err = case.run_gpu(layer=layer)
