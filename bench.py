@@ -621,6 +621,10 @@ def run_ours(args):
         inp = dict(x=x, w_router=w_router, W1t=W1t, W2t=W2t, b1=b1, b2=b2, out=out, loss=loss,
                    fused_gate=args.fused_gate)
         train = bool(cfgd.get("train"))
+        if args.exchange == "peer" and not train:
+            # the step calls then fuse the level-1 return for in-process tokens into GEMM 2
+            # (smile_set_output; smile_forward does the same for its io->out)
+            L.set_output(out)
         if train:
             f32 = dict(dtype=torch.float32, device=dev)
             inp.update(alpha=0.005 if mode == "bilevel" else 0.01, beta=0.005 if mode == "bilevel" else 0.0,
@@ -733,6 +737,20 @@ def run_ours(args):
             # (a11 fused into the FFN, no extra bytes); combine2 moves only rows of experts
             # in other processes -- the level-2 rows this process sent away
             hbm["combine2"] = 2 * nvl.get("intra", 0)
+            if not train and os.environ.get("SMILE_OUT_DIRECT", "1") != "0" and not inp.get("fused_gate"):
+                # ... and out[t] for tokens whose intermediate and expert are in this process
+                # too (a12 + a13 fused): combine1 moves the other kept tokens and zeroes drops
+                import numpy as np
+                d1 = w["dest1"].cpu().numpy()
+                d2 = w["dest2"].cpu().numpy()
+                s1 = w["slot1"].cpu().numpy()
+                m_ = cfgd["m"]
+                rk = rank * V + np.arange(V)[:, None]
+                u = d1 * m_ + rk % m_
+                q = d1 * m_ + d2 // e
+                kept_l1 = s1 < L.C1
+                remote = kept_l1 & ((u // V != rank) | (q // V != rank))
+                hbm["combine1"] = (2 * int(remote.sum()) + int((~kept_l1).sum())) * rb
         res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, rank_ms=rank_ms, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms,
                    t_beg=t_beg, t_end=t_end,
                    tokens=G * T, launches=launched, hbm_bytes=hbm, train=train, eager_ms=eager_ms, graph_ms=graph_ms,

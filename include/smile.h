@@ -178,6 +178,17 @@ smile_status smile_ipc_handle(smile_ctx ctx, const void *ws, uint8_t out[72]);
  * processes after this call returns, before the first smile_forward); nprocs == 1:
  * handles may be NULL.  Synchronises the device. */
 smile_status smile_register_workspace(smile_ctx ctx, void *ws, const uint8_t *handles, int32_t xchg);
+/* Binds the layer output out [V, T, d] (dtype) for the following step calls (NULL unbinds;
+ * smile_forward binds its io->out for the duration of an inference call by itself).  With
+ * the peer-store exchange, BILEVEL, bf16 and the tcgen05 FFN, an inference forward then
+ * also fuses the level-1 return: the level-1 permute records each row's source token at
+ * the intermediate, the level-2 permute forwards it to the expert, and GEMM 2 writes
+ * out[t] = bf16(gate[t] * bf16(y)) (R24, the same arithmetic as smile_combine(1)) for every
+ * token whose intermediate and expert share the process; smile_combine(1) into the same
+ * out fills only the other tokens, and tokens dropped at level 2 get their zero row from
+ * the level-2 permute.  Not used by smile_expert_ffn_train (the backward needs ret1).
+ * SMILE_OUT_DIRECT=0 disables it. */
+smile_status smile_set_output(smile_ctx ctx, void *out);
 
 /* ---------------- the steps of the layer ---------------- */
 

@@ -73,7 +73,8 @@ struct WsLayout {
 };
 
 static void ws_layout(const smile_shape *s, const smile_sizes *z, WsLayout *L, smile_ws_view *view,
-                      char *base, char **rrow_out = nullptr) {
+                      char *base, char **rrow_out = nullptr, char **rtok1_out = nullptr,
+                      char **rtok2_out = nullptr) {
     const int64_t V = z->V, T = s->T;
     const int64_t eb = s->dtype == SMILE_BF16 ? 2 : 4;
     const int64_t rb = (int64_t)s->d * eb;
@@ -120,6 +121,10 @@ static void ws_layout(const smile_shape *s, const smile_sizes *z, WsLayout *L, s
     w.flags = take(3 * kMaxProcs * 8);
     char *rrow = take(bi ? ffn_rows * 4 : 0);       // internal: ret1 row of each expert input row
     if (rrow_out) *rrow_out = rrow;
+    char *rtok1 = take(bi ? V * z->K1 * z->C1 * 4 : 0);   // internal: source token per received slot
+    char *rtok2 = take(bi ? ffn_rows * 4 : 0);            // internal: source token per expert row
+    if (rtok1_out) *rtok1_out = rtok1;
+    if (rtok2_out) *rtok2_out = rtok2;
     if (L) L->total = o;
     if (view) *view = w;
 }
@@ -424,8 +429,9 @@ extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const ui
     c->xchg = xchg;
     if (xchg == SMILE_XCHG_COPY) return SMILE_OK;
     smile_ws_view w;
-    char *rrow = nullptr;
-    ws_layout(&c->shape, &c->sz, nullptr, &w, (char *)ws, &rrow);
+    char *rrow = nullptr, *rtok1 = nullptr, *rtok2 = nullptr;
+    ws_layout(&c->shape, &c->sz, nullptr, &w, (char *)ws, &rrow, &rtok1, &rtok2);
+    c->ws_gate = w.route.gate;
     auto off = [&](const void *ptr) { return (int64_t)((const char *)ptr - (const char *)ws); };
     c->off_flags = off(w.flags);
     CUDA_TRY(cudaMemset(w.flags, 0, 3 * kMaxProcs * 8));
@@ -472,6 +478,8 @@ extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const ui
     pm.off_recv1 = off(w.recv1); pm.off_rmeta1 = bi ? off(w.rmeta1) : 0; pm.off_recv2 = bi ? off(w.recv2) : 0;
     pm.off_rcounts = off(w.rcounts); pm.off_Y = off(w.Y); pm.off_ret1 = bi ? off(w.ret1) : 0;
     pm.off_rrow = bi ? (int64_t)(rrow - (char *)ws) : 0;
+    pm.off_rtok1 = bi ? (int64_t)(rtok1 - (char *)ws) : 0;
+    pm.off_rtok2 = bi ? (int64_t)(rtok2 - (char *)ws) : 0;
     CUDA_TRY(cudaDeviceSynchronize());
     return SMILE_OK;
 }
@@ -543,6 +551,7 @@ extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, co
     const bool bi = c->shape.mode == SMILE_BILEVEL;
     if (bi && !send_meta) return SMILE_EINVAL;
     if (c->shape.T == 0) return SMILE_OK;
+    c->rtok1_valid = false;                  // this path does not record the source tokens
     if (!c->wsplit || !c->lb_flag || c->TB1 != 128) {
         // no tensor-core gate for this shape / dtype: the two calls it fuses
         STEP(smile_gate_inter(c, x, w_router, nullptr, logits_out, route, stats, counts1, stream));
@@ -575,6 +584,8 @@ extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, co
     return post_launch();
 }
 
+static bool out_direct_possible(smile_ctx c);
+
 extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *rows_in, const smile_route *route,
                                        const int32_t *recv_meta, int32_t *slot2, void *send_rows, int32_t *send_meta,
                                        void *stream) {
@@ -591,6 +602,7 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
         a.V = c->sz.V; a.T = c->shape.T; a.rowbytes = rb; a.K1 = c->sz.K1; a.C1 = c->sz.C1;
         a.TB = c->TB1; a.nblk = c->nblk1; a.peer = peer_of(c);
         launch_dispatch1(a, S(stream));
+        c->rtok1_valid = a.peer.bases != nullptr && bi;
         return post_launch();
     }
     if (level == 2) {
@@ -602,6 +614,8 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
         a.send2 = send_rows; a.V = c->sz.V; a.items = (int64_t)c->shape.n * c->sz.C1; a.rowbytes = rb;
         a.K2 = c->sz.K2; a.C2 = c->sz.C2; a.nblk = c->nblk2; a.peer = peer_of(c);
         if (a.peer.bases) a.ret1 = static_cast<char *>(c->reg_ws) + c->peer.off_ret1;
+        c->out_planned = out_direct_possible(c);
+        if (c->out_planned) { a.out = c->out_bound; a.T = c->shape.T; }
         launch_dispatch2(a, S(stream));
         return post_launch();
     }
@@ -704,6 +718,18 @@ extern "C" smile_status smile_all2all_intra(smile_ctx c, int32_t reverse, const 
     return smile_all2all(c, 2, reverse, send_rows, recv_rows, send_cnt, recv_cnt, fwd_counts, stream);
 }
 
+// PEER + BILEVEL inference with the output bound (smile_set_output) and the tcgen05 FFN:
+// GEMM 2 writes rows whose source rank is in this process straight to out (a12 + a13).
+static bool out_direct_possible(smile_ctx c) {
+    if (c->xchg != SMILE_XCHG_PEER || c->shape.mode != SMILE_BILEVEL || !c->out_bound || !c->rtok1_valid)
+        return false;
+    if (c->shape.dtype != SMILE_BF16 || c->shape.ffn_impl == SMILE_FFN_SIMT) return false;
+    const char *e = getenv("SMILE_OUT_DIRECT");
+    if (e && e[0] == '0') return false;
+    e = getenv("SMILE_RET_DIRECT");
+    return !(e && e[0] == '0');
+}
+
 // PEER + BILEVEL + tcgen05: GEMM 2 stores its rows into the intermediates' ret1 (the
 // level-2 un-permute fused into the FFN); smile_combine(2) then has nothing left to do.
 static void set_ret_direct(smile_ctx c, FfnArgs &f) {
@@ -726,12 +752,18 @@ extern "C" smile_status smile_expert_ffn(smile_ctx c, const void *X, const int32
     int impl = c->shape.ffn_impl;
     if (impl == SMILE_FFN_AUTO) impl = f.bf16 ? SMILE_FFN_TCGEN05 : SMILE_FFN_SIMT;
     c->ret_direct = false;
+    c->out_direct = false;
     if (impl == SMILE_FFN_TCGEN05) {
         if (!f.bf16) return SMILE_ENOTSUP;
         set_ret_direct(c, f);
+        if (f.ret.bases && c->out_planned) {
+            f.out = c->out_bound; f.gate = c->ws_gate; f.T = c->shape.T; f.C1 = c->sz.C1; f.n = c->shape.n;
+            f.rtok2 = reinterpret_cast<const int32_t *>(static_cast<char *>(c->reg_ws) + c->peer.off_rtok2);
+        }
         cudaError_t e = launch_ffn_tcgen05(f, S(stream));
         if (e == cudaErrorNotSupported) return SMILE_ENOTSUP;
         c->ret_direct = f.ret.bases != nullptr;
+        c->out_direct = f.out != nullptr;
         return e == cudaSuccess ? post_launch() : SMILE_ECUDA;
     }
     if (!ffn_simt_supported(f.V * f.S * f.e, f.d, f.d_ff)) return SMILE_ENOTSUP;
@@ -750,6 +782,8 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
         Combine1Args a{};
         a.back1 = ret_rows; a.route = *route; a.out = out; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
         a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = bf; a.nogate = 0; a.peer = peer_of(c);
+        a.skip_direct = (a.peer.bases && c->out_direct && out == c->out_bound) ? 1 : 0;
+        c->out_direct = false;
         launch_combine1(a, S(stream));
         return post_launch();
     }
@@ -800,6 +834,7 @@ extern "C" smile_status smile_expert_ffn_train(smile_ctx c, const void *X, const
     if (tc && !f.bf16) return SMILE_ENOTSUP;
     if (!tc && !ffn_simt_supported(f.V * f.S * f.e, f.d, f.d_ff)) return SMILE_ENOTSUP;
     c->ret_direct = false;
+    c->out_direct = false;                   // training keeps ret1 (combine_bwd reads it)
     if (tc) set_ret_direct(c, f);
     cudaError_t e = launch_ffn_fwd_train(f, A1_ws, tc, S(stream));
     if (e == cudaErrorNotSupported) return SMILE_ENOTSUP;
@@ -891,6 +926,12 @@ extern "C" smile_status smile_forward_ws(smile_ctx c, void *ws, smile_ws_view *v
 }
 
 
+extern "C" smile_status smile_set_output(smile_ctx c, void *out) {
+    if (!c) return SMILE_EINVAL;
+    c->out_bound = out;
+    return SMILE_OK;
+}
+
 extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, void *stream) {
     if (!c || !io) return SMILE_EINVAL;
     if (c->shape.T == 0) return SMILE_OK;                 // no tokens: nothing to compute
@@ -901,6 +942,12 @@ extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, voi
     if (c->shape.T == 0) return SMILE_OK;
     const bool train = io->train != 0;
     if (c->xchg == SMILE_XCHG_PEER && io->ws != c->reg_ws) return SMILE_ENOTSUP;
+    // inference binds io->out for this call (GEMM 2 may write in-process rows there)
+    struct OutBinding {
+        smile_ctx c; void *prev;
+        ~OutBinding() { c->out_bound = prev; }
+    } bind{c, c->out_bound};
+    c->out_bound = train ? nullptr : io->out;
     // gate then level-1 permute as two kernels: measured faster than the fused
     // smile_gate_dispatch_inter (C2: 0.166 vs 0.178 ms; C4: 0.77 vs 0.85 ms) -- the row moves
     // from the gate's epilogue warps reach less bandwidth than the dedicated movers

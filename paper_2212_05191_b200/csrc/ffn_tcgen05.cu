@@ -63,6 +63,13 @@ struct TcArgs {
     const int32_t *rrow;
     int64_t roff_ret1;
     int rrank0, rm, rV;
+    // ... and, with the layer output bound, rows whose source rank is in this process too go
+    // to out[t] as bf16(gate[t] * bf16(y)) (the level-1 combine's arithmetic, R24)
+    char *out;
+    const float *gate;
+    const int32_t *rtok2;
+    int64_t T, C1;
+    int n;
     int diag;                  // measurement only (SMILE_FFN_DIAG; wrong results): 1 no activation,
                                // 2 no stores, 4 no TMEM reads / epilogue math (release only),
                                // 8 TMA stores into rows [0, 1024) only (L2-resident)
@@ -451,15 +458,27 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             // its ret1 (this lane's row: rdst); a strip is one segment, so one l and one
             // decision per warp.  Rows for other processes' intermediates go to D (Y) as
             // usual and smile_combine(2) fetches them over NVLink.
-            bool rlocal = false;
+            bool rlocal = false, rout = false;
             char *rdst = nullptr;
+            float rgate = 0.f;
             if (EK == 0 && a.rbases && srows > 0) {
                 const int64_t seg = d_row / a.Cseg;                    // (v * S + l) * e + k
                 const int vv = (int)(seg / ((int64_t)a.S * a.e)), l = (int)((seg / a.e) % a.S);
                 const int u = (a.rrank0 + vv) / a.rm * a.rm + l;       // intermediate (i, l)
                 rlocal = u / a.rV == a.rrank0 / a.rV;
-                if (rlocal && lane < srows)
-                    rdst = a.rbases[u / a.rV] + a.roff_ret1 + (int64_t)a.rrow[d_row + lane] * a.N * 2 + dcol0 * 2;
+                if (rlocal && lane < srows) {
+                    const int32_t rr = a.rrow[d_row + lane];
+                    rdst = a.rbases[u / a.rV] + a.roff_ret1 + (int64_t)rr * a.N * 2 + dcol0 * 2;
+                    if (a.out) {
+                        const int us = (int)((rr % (a.n * a.C1)) / a.C1) * a.rm + l;   // source (s, l)
+                        if (us / a.rV == a.rrank0 / a.rV) {
+                            const int64_t tok = (int64_t)(us % a.rV) * a.T + a.rtok2[d_row + lane];
+                            rdst = a.out + tok * a.N * 2 + dcol0 * 2;
+                            rgate = a.gate[tok];
+                            rout = true;
+                        }
+                    }
+                }
             }
             const bool full_box = srows == 32 && !(a.diag & 2);
             // EPI_DGELU: chunk c's saved GELU'(A1) is loaded before its accumulator
@@ -539,6 +558,14 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                 }
                 if (EK == 0 && rlocal) {
                     if (rdst) {
+                        if (rout) {
+                            __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(pk);
+#pragma unroll
+                            for (int z = 0; z < 16; ++z) {
+                                const float2 f = __bfloat1622float2(h[z]);
+                                h[z] = __floats2bfloat162_rn(rgate * f.x, rgate * f.y);
+                            }
+                        }
                         uint4 *d4 = reinterpret_cast<uint4 *>(rdst + c * 64);
 #pragma unroll
                         for (int i = 0; i < 4; ++i) d4[i] = pk[i];
@@ -770,6 +797,10 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     if (mode == EPI_BIAS && !gelu && f.ret.bases) {
         a.rbases = f.ret.bases; a.rrow = f.rrow; a.roff_ret1 = f.ret.off_ret1;
         a.rrank0 = f.ret.rank0; a.rm = f.ret.m; a.rV = f.ret.V;
+        if (f.out) {
+            a.out = static_cast<char *>(f.out); a.gate = f.gate; a.rtok2 = f.rtok2;
+            a.T = f.T; a.C1 = f.C1; a.n = f.n;
+        }
     }
     a.err = nullptr;
     const size_t smem = smem_bytes(CG, NSUB, a.stages, nbox, a.tma_store, a.box64, a.nseg);

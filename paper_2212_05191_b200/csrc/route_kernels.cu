@@ -320,7 +320,10 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
                 }
                 char *base = P.bases[q / P.V];
                 r.dst = base + P.off_recv1 + row * a.rowbytes;
-                if (a.meta) reinterpret_cast<int32_t *>(base + P.off_rmeta1)[row] = a.route.dest2[g];
+                if (a.meta) {
+                    reinterpret_cast<int32_t *>(base + P.off_rmeta1)[row] = a.route.dest2[g];
+                    reinterpret_cast<int32_t *>(base + P.off_rtok1)[row] = (int32_t)t;   // source token
+                }
             } else {
                 const int64_t dst_row = ((int64_t)v * a.K1 + i) * a.C1 + slot;
                 r.dst = static_cast<char *>(a.send) + dst_row * a.rowbytes;
@@ -347,6 +350,8 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
                     const int64_t row = (((int64_t)(q % P.V) * P.m + l) * P.e + j % P.e) * a.C2 + slot;
                     r.dst = P.bases[q / P.V] + P.off_recv2 + row * a.rowbytes;
                     reinterpret_cast<int32_t *>(P.bases[q / P.V] + P.off_rrow)[row] = (int32_t)g;
+                    reinterpret_cast<int32_t *>(P.bases[q / P.V] + P.off_rtok2)[row] =
+                        reinterpret_cast<const int32_t *>(P.bases[P.rank0 / P.V] + P.off_rtok1)[g];
                 } else {
                     r.dst = static_cast<char *>(a.send2) + (((int64_t)v * a.K2 + j) * a.C2 + slot) * a.rowbytes;
                 }
@@ -354,6 +359,21 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
                 // dropped at level 2 (R8): its return row is zero (written now; the fused
                 // GEMM 2 writes only kept rows)
                 r.dst = static_cast<char *>(a.ret1) + g * a.rowbytes;
+                if (a.out) {
+                    // output bound: when the source rank and the expert share this process the
+                    // combine skips the token, so its zero output row is written here too
+                    const PeerMap &P = a.peer;
+                    const int rk = P.rank0 + v, i = rk / P.m, l = rk % P.m;
+                    const int us = (int)(x / (a.items / P.n)) * P.m + l;    // source (s, l): x = s C1 + c
+                    const int q = i * P.m + j / P.e;
+                    const int me = P.rank0 / P.V;
+                    if (us / P.V == me && q / P.V == me) {
+                        const int tt = reinterpret_cast<const int32_t *>(P.bases[me] + P.off_rtok1)[g];
+                        int4 *o = reinterpret_cast<int4 *>(static_cast<char *>(a.out) +
+                                                           ((int64_t)(us % P.V) * a.T + tt) * a.rowbytes);
+                        for (int k = 0; k < (int)(a.rowbytes / 16); ++k) o[k] = make_int4(0, 0, 0, 0);
+                    }
+                }
             }
         }
     } else if (m.kind == MOVE_GRAD2) {
@@ -415,6 +435,13 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
                 const int rk = P.rank0 + v;
                 if (P.n > 0) {   // bi-level: peer load from the intermediate (i, l), chunk s
                     const int s_ = rk / P.m, l = rk % P.m, u = i * P.m + l;
+                    if (a.skip_direct) {
+                        const int q = i * P.m + a.route.dest2[g] / P.e, me = P.rank0 / P.V;
+                        if (u / P.V == me && q / P.V == me) {     // written by the expert's GEMM 2
+                            r.dst = nullptr;
+                            return r;
+                        }
+                    }
                     r.src = P.bases[u / P.V] + P.off_ret1 + (((int64_t)(u % P.V) * P.n + s_) * a.C1 + s1) * rb;
                 } else {         // flat: peer load of Y from the expert rank E / e
                     const int q = i / P.e;

@@ -50,6 +50,8 @@ struct PeerMap {
     int V, rank0, n, m, e, G;
     int64_t off_recv1, off_rmeta1, off_recv2, off_rcounts, off_Y, off_ret1;
     int64_t off_rrow;                  // BILEVEL: [V, S, e, Cseg] i32 ret1 row of each expert input row
+    int64_t off_rtok1;                 // BILEVEL: [V, n, C1] i32 source token of each received slot
+    int64_t off_rtok2;                 // BILEVEL: [V, S, e, Cseg] i32 source token of each expert input row
 };
 constexpr int kMaxProcs = 64;
 
@@ -60,6 +62,11 @@ struct smile_ctx_s {
     smile_sizes sz;
     int TB1 = 256;             // gate tokens per block
     bool ret_direct = false;   // PEER: the last expert FFN stored its output in the intermediates' ret1
+    void *out_bound = nullptr; // smile_set_output: the layer output [V, T, d] of the next steps
+    bool rtok1_valid = false;  // PEER: the last level-1 permute recorded the source tokens
+    bool out_planned = false;  // PEER: this forward writes in-process rows straight to out
+    bool out_direct = false;   // ... and the last expert FFN did
+    const float *ws_gate = nullptr;   // route.gate in the registered workspace
     int nblk1 = 0;             // gate blocks per rank
     int nblk2 = 0;             // level-2 ranking blocks per rank
     int *d_err = nullptr;      // sticky device error flag (smile_status)
@@ -135,6 +142,8 @@ struct Dispatch2Args {
     const void *recv1; const int32_t *recv_meta; int32_t *slot2; const int32_t *blk_off2;
     void *send2; int V; int64_t items; int64_t rowbytes; int K2; int64_t C2; int nblk;
     void *ret1;                        // PEER: level-2-dropped rows get their zero return row here
+    void *out; int64_t T;              // PEER + output bound: ... or, for sources and experts in
+                                       // this process, a zero row in the layer output
     PeerMap peer;
 };
 void launch_dispatch2(const Dispatch2Args &a, cudaStream_t st);
@@ -151,6 +160,8 @@ struct Combine1Args {
     const void *back1; smile_route route; void *out; int V; int64_t T; int d; int K1; int64_t C1;
     int bf16; int nogate;      // nogate: gradient return (a18), rows copied unscaled
     PeerMap peer;
+    int skip_direct;           // PEER: tokens whose intermediate and expert are in this process
+                               // were written by the expert's GEMM 2 (smile_set_output)
 };
 void launch_combine1(const Combine1Args &a, cudaStream_t st);
 
@@ -197,6 +208,9 @@ struct FfnArgs {
     // permute 2 recorded in rrow [V, S, e, Cseg] (this process's workspace)
     PeerMap ret;
     const int32_t *rrow;
+    // inference with the layer output bound (smile_set_output): rows whose source rank is
+    // in this process too go straight to out[t] as gate * y (a12 + a13 fused as well)
+    void *out; const float *gate; const int32_t *rtok2; int64_t T, C1; int n;
 };
 void launch_ffn_simt(const FfnArgs &a, cudaStream_t st);
 

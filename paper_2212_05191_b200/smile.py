@@ -90,7 +90,7 @@ def lib():
                      "smile_gate_dispatch_inter",
                      "smile_expert_ffn_train", "smile_combine_bwd", "smile_dispatch_grad", "smile_expert_ffn_bwd",
                      "smile_combine_grad", "smile_router_bwd", "smile_backward", "smile_ipc_handle",
-                     "smile_register_workspace", "smile_struct_sizes", "smile_forward_host_stream"):
+                     "smile_register_workspace", "smile_struct_sizes", "smile_forward_host_stream", "smile_set_output"):
             getattr(L, name).restype = C.c_int
         # the ctypes mirrors must match the C structs byte for byte
         sizes = (C.c_int64 * 8)()
@@ -301,6 +301,10 @@ class SmileLayer:
         ho = PN(*[_ptr(t) for t in host_outs])
         _check(lib().smile_forward_host_stream(self._ctx, C.byref(io), xd, od, nb, hx, ho, _ptr(host_loss),
                                                _stream(stream)), "smile_forward_host_stream")
+
+    def set_output(self, out):
+        """smile_set_output: bind the layer output for the following step calls (None unbinds)."""
+        _check(lib().smile_set_output(self._ctx, _ptr(out)), "smile_set_output")
 
     def get_error(self, stream=None) -> int:
         return lib().smile_get_error(self._ctx, _stream(stream))

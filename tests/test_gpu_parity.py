@@ -462,3 +462,35 @@ def test_ret_direct_bit_identical(n, m, e, T, d, d_ff, cf, monkeypatch):
         assert err == 0
         outs[flag] = (out.clone(), loss.clone())
     assert torch.equal(outs["0"][0], outs["1"][0]) and torch.equal(outs["0"][1], outs["1"][1])
+
+
+@pytest.mark.parametrize("n,m,e,T,d,d_ff,cf", [
+    (2, 4, 1, 1000, 128, 256, 1.25),       # level-1 and level-2 drops
+    (4, 2, 2, 700, 64, 128, 1.0),
+    (1, 8, 1, 333, 128, 256, 2.0),         # one node: every token's return fused into GEMM 2
+])
+def test_out_direct_bit_identical(n, m, e, T, d, d_ff, cf, monkeypatch):
+    """Peer exchange, inference: GEMM 2 writing out[t] = bf16(gate * bf16(y)) for tokens whose
+    intermediate and expert share the process (SMILE_OUT_DIRECT, default) gives outputs
+    bit-identical to ret1 + combine(1), with out garbage-filled first, and matches the oracle."""
+    from paper_2212_05191_b200 import SmileLayer
+    case = Case(n, m, e, T, d, d_ff, cf, dtype="bf16", dist="skewed", seed=23)
+    layer = SmileLayer(n, m, e, d, d_ff, T, cf, "bf16", "bilevel")
+    layer.enable_peer_exchange()
+    g = case.gpu_tensors()
+    outs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SMILE_OUT_DIRECT", flag)
+        layer.ws.fill_(0x7f)
+        out = torch.full_like(g["x"], float("nan"))        # every row must be written
+        loss = torch.empty(layer.V, dtype=torch.float64, device=g["x"].device)
+        layer.forward(g["x"], g["W1t"], g["b1"], g["W2t"], g["b2"], out, loss, logits=g["logits"],
+                      w_router=g["w_router"], alpha=case.alpha, beta=case.beta)
+        torch.cuda.synchronize()
+        assert layer.get_error() == 0
+        outs[flag] = (out.clone(), loss.clone())
+    assert not torch.isnan(outs["1"][0].float()).any()
+    assert torch.equal(outs["0"][0], outs["1"][0]) and torch.equal(outs["0"][1], outs["1"][1])
+    assert_close_scaled(outs["1"][0].float().cpu().numpy().reshape(-1, d), case.oracle_out(case.oracle_route()),
+                        2e-2, "out-direct vs oracle")
+    layer.close()
