@@ -750,7 +750,13 @@ def run_ours(args):
                 q = d1 * m_ + d2 // e
                 kept_l1 = s1 < L.C1
                 remote = kept_l1 & ((u // V != rank) | (q // V != rank))
-                hbm["combine1"] = (2 * int(remote.sum()) + int((~kept_l1).sum())) * rb
+                if L.V == L.G:
+                    # every rank in this process: the level-1 permute writes the dropped tokens'
+                    # zero rows and combine1 is not launched
+                    hbm["dispatch1"] = hbm.get("dispatch1", 0) + int((~kept_l1).sum()) * rb
+                    hbm["combine1"] = 0
+                else:
+                    hbm["combine1"] = (2 * int(remote.sum()) + int((~kept_l1).sum())) * rb
         res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, rank_ms=rank_ms, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms,
                    t_beg=t_beg, t_end=t_end,
                    tokens=G * T, launches=launched, hbm_bytes=hbm, train=train, eager_ms=eager_ms, graph_ms=graph_ms,

@@ -552,6 +552,7 @@ extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, co
     if (bi && !send_meta) return SMILE_EINVAL;
     if (c->shape.T == 0) return SMILE_OK;
     c->rtok1_valid = false;                  // this path does not record the source tokens
+    c->l1_zeroed = false;
     if (!c->wsplit || !c->lb_flag || c->TB1 != 128) {
         // no tensor-core gate for this shape / dtype: the two calls it fuses
         STEP(smile_gate_inter(c, x, w_router, nullptr, logits_out, route, stats, counts1, stream));
@@ -584,6 +585,7 @@ extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, co
     return post_launch();
 }
 
+static bool out_direct_enabled(smile_ctx c);
 static bool out_direct_possible(smile_ctx c);
 
 extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *rows_in, const smile_route *route,
@@ -601,6 +603,10 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
         a.send = send_rows; a.meta = bi ? send_meta : nullptr;
         a.V = c->sz.V; a.T = c->shape.T; a.rowbytes = rb; a.K1 = c->sz.K1; a.C1 = c->sz.C1;
         a.TB = c->TB1; a.nblk = c->nblk1; a.peer = peer_of(c);
+        // every rank in this process: the whole level-1 return fuses into GEMM 2, so the
+        // zero rows of level-1-dropped tokens are written here and combine(1) is skipped
+        c->l1_zeroed = out_direct_enabled(c) && c->sz.V == c->sz.G;
+        if (c->l1_zeroed) a.out = c->out_bound;
         launch_dispatch1(a, S(stream));
         c->rtok1_valid = a.peer.bases != nullptr && bi;
         return post_launch();
@@ -720,15 +726,16 @@ extern "C" smile_status smile_all2all_intra(smile_ctx c, int32_t reverse, const 
 
 // PEER + BILEVEL inference with the output bound (smile_set_output) and the tcgen05 FFN:
 // GEMM 2 writes rows whose source rank is in this process straight to out (a12 + a13).
-static bool out_direct_possible(smile_ctx c) {
-    if (c->xchg != SMILE_XCHG_PEER || c->shape.mode != SMILE_BILEVEL || !c->out_bound || !c->rtok1_valid)
-        return false;
+static bool out_direct_enabled(smile_ctx c) {
+    if (c->xchg != SMILE_XCHG_PEER || c->shape.mode != SMILE_BILEVEL || !c->out_bound) return false;
     if (c->shape.dtype != SMILE_BF16 || c->shape.ffn_impl == SMILE_FFN_SIMT) return false;
     const char *e = getenv("SMILE_OUT_DIRECT");
     if (e && e[0] == '0') return false;
     e = getenv("SMILE_RET_DIRECT");
     return !(e && e[0] == '0');
 }
+
+static bool out_direct_possible(smile_ctx c) { return c->rtok1_valid && out_direct_enabled(c); }
 
 // PEER + BILEVEL + tcgen05: GEMM 2 stores its rows into the intermediates' ret1 (the
 // level-2 un-permute fused into the FFN); smile_combine(2) then has nothing left to do.
@@ -784,6 +791,13 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
         a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = bf; a.nogate = 0; a.peer = peer_of(c);
         a.skip_direct = (a.peer.bases && c->out_direct && out == c->out_bound) ? 1 : 0;
         c->out_direct = false;
+        if (a.skip_direct && c->l1_zeroed && c->sz.V == c->sz.G) {
+            // every token's intermediate and expert are in this process: GEMM 2 wrote the
+            // kept tokens, the level-1 permute the dropped ones -- nothing left to move
+            c->l1_zeroed = false;
+            return SMILE_OK;
+        }
+        c->l1_zeroed = false;
         launch_combine1(a, S(stream));
         return post_launch();
     }

@@ -329,6 +329,8 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
                 r.dst = static_cast<char *>(a.send) + dst_row * a.rowbytes;
                 if (a.meta) a.meta[dst_row] = a.route.dest2[g];
             }
+        } else if (a.out) {
+            r.dst = static_cast<char *>(a.out) + g * a.rowbytes;     // dropped (R8): zero output row
         }
     } else if (m.kind == MOVE_DISPATCH2) {
         const Dispatch2Args &a = m.d2;

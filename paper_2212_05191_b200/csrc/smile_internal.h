@@ -66,6 +66,7 @@ struct smile_ctx_s {
     bool rtok1_valid = false;  // PEER: the last level-1 permute recorded the source tokens
     bool out_planned = false;  // PEER: this forward writes in-process rows straight to out
     bool out_direct = false;   // ... and the last expert FFN did
+    bool l1_zeroed = false;    // ... and the level-1 permute wrote the level-1-dropped zero rows
     const float *ws_gate = nullptr;   // route.gate in the registered workspace
     int nblk1 = 0;             // gate blocks per rank
     int nblk2 = 0;             // level-2 ranking blocks per rank
@@ -133,6 +134,8 @@ struct Dispatch1Args {
     const void *x; smile_route route; const int32_t *blk_off1; const int32_t *blk_hist1;
     void *send; int32_t *meta; int V; int64_t T; int64_t rowbytes; int K1; int64_t C1; int TB, nblk;
     PeerMap peer;
+    void *out;                         // PEER + output bound, every rank in this process: tokens
+                                       // dropped at level 1 get their zero output row here
 };
 void launch_dispatch1(const Dispatch1Args &a, cudaStream_t st);
 // meta = -1 for the empty slots [count, C1) (after the fused gate + permute)
