@@ -468,7 +468,7 @@ constexpr int kMoveColUnroll = 3;       // 16-byte vectors per lane per row in f
 // (independent dependent-load chains), the pointers are broadcast, then every lane keeps
 // rows x kMoveColUnroll 16-byte loads in flight before its stores.
 template <int RW>
-__global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) {
+__device__ __forceinline__ void row_move_body(const MoveArgs &m) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -541,6 +541,13 @@ __global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) {
         }
     }
 }
+
+template <int RW>
+__global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) { row_move_body<RW>(m); }
+
+// the same with the register budget fitted to MINB resident blocks per SM (SMILE_MOVE_MINB)
+template <int RW, int MINB>
+__global__ void __launch_bounds__(kMoveThreads, MINB) row_move_kernel_mb(MoveArgs m) { row_move_body<RW>(m); }
 
 // dispatch1 also fills meta = -1 for the empty slots [count, C1) of every destination.
 __global__ void meta_fill_kernel(Dispatch1Args a) {
@@ -686,6 +693,18 @@ static int move_rw() {
 }
 
 // Grid cap of the movers in blocks per SM: SMILE_MOVE_GRIDMUL (default 8).
+// resident 256-thread blocks per SM the register budget is fitted to (SMILE_MOVE_MINB: 1 = the
+// unconstrained 118-register kernel, 2 blocks per SM; 3 = 80 registers, 216 B spilled)
+static int move_minb() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SMILE_MOVE_MINB");
+        v = e ? atoi(e) : 1;
+        if (v != 3) v = 1;
+    }
+    return v;
+}
+
 static int move_gridmul() {
     static int v = -1;
     if (v < 0) {
@@ -703,7 +722,9 @@ static void launch_move(MoveArgs &m, cudaStream_t st) {
     int64_t grid = (m.rows + per_block - 1) / per_block;
     if (grid > 148 * move_gridmul()) grid = 148 * move_gridmul();
     note_launch();
+    const int minb = move_minb();
     if (rw == 8) row_move_kernel<8><<<(int)grid, kMoveThreads, 0, st>>>(m);
+    else if (minb == 3) row_move_kernel_mb<kMoveRowsPerWarp, 3><<<(int)grid, kMoveThreads, 0, st>>>(m);
     else row_move_kernel<kMoveRowsPerWarp><<<(int)grid, kMoveThreads, 0, st>>>(m);
 }
 
