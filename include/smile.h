@@ -186,8 +186,12 @@ smile_status smile_register_workspace(smile_ctx ctx, void *ws, const uint8_t *ha
  * out[t] = bf16(gate[t] * bf16(y)) (R24, the same arithmetic as smile_combine(1)) for every
  * token whose intermediate and expert share the process; smile_combine(1) into the same
  * out fills only the other tokens, and tokens dropped at level 2 get their zero row from
- * the level-2 permute.  Not used by smile_expert_ffn_train (the backward needs ret1).
- * SMILE_OUT_DIRECT=0 disables it. */
+ * the level-2 permute.  When every rank of the job is in this process (G == V) the
+ * level-1 permute also writes the zero rows of tokens dropped at level 1, and
+ * smile_combine(1) into the bound out returns without launching anything.  After such a
+ * forward, smile_combine(1) into any other buffer fails with SMILE_EINVAL (the fused rows
+ * were never written to ret1).  Not used by smile_expert_ffn_train (the backward needs
+ * ret1).  SMILE_OUT_DIRECT=0 disables it. */
 smile_status smile_set_output(smile_ctx ctx, void *out);
 
 /* ---------------- the steps of the layer ---------------- */

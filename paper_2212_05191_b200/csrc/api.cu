@@ -789,7 +789,14 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
         Combine1Args a{};
         a.back1 = ret_rows; a.route = *route; a.out = out; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
         a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = bf; a.nogate = 0; a.peer = peer_of(c);
-        a.skip_direct = (a.peer.bases && c->out_direct && out == c->out_bound) ? 1 : 0;
+        if (c->out_direct && out != c->out_bound) {
+            // GEMM 2 wrote the in-process tokens to the bound output, not to ret1: a combine
+            // into another buffer would read stale rows
+            c->out_direct = false;
+            c->l1_zeroed = false;
+            return SMILE_EINVAL;
+        }
+        a.skip_direct = (a.peer.bases && c->out_direct) ? 1 : 0;
         c->out_direct = false;
         if (a.skip_direct && c->l1_zeroed && c->sz.V == c->sz.G) {
             // every token's intermediate and expert are in this process: GEMM 2 wrote the

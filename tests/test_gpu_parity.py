@@ -494,3 +494,48 @@ def test_out_direct_bit_identical(n, m, e, T, d, d_ff, cf, monkeypatch):
     assert_close_scaled(outs["1"][0].float().cpu().numpy().reshape(-1, d), case.oracle_out(case.oracle_route()),
                         2e-2, "out-direct vs oracle")
     layer.close()
+
+
+def test_out_direct_step_api():
+    """The bench's step calls with smile_set_output: same output as smile_forward (which
+    binds io->out itself) and as the unbound step sequence; a level-1 combine into a buffer
+    other than the bound one fails loudly instead of reading stale ret1 rows."""
+    import importlib.util
+    import os
+    from paper_2212_05191_b200 import SmileLayer, SmileError
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    n, m, e, T, d, d_ff, cf = 2, 4, 1, 640, 128, 256, 1.25
+    case = Case(n, m, e, T, d, d_ff, cf, dtype="bf16", dist="skewed", seed=29, fused=True)
+    layer = SmileLayer(n, m, e, d, d_ff, T, cf, "bf16", "bilevel")
+    layer.alloc_workspace()
+    layer.enable_peer_exchange()
+    g = case.gpu_tensors()
+    ref = torch.empty_like(g["x"])
+    loss_ref = torch.empty(layer.V, dtype=torch.float64, device="cuda")
+    layer.forward(g["x"], g["W1t"], g["b1"], g["W2t"], g["b2"], ref, loss_ref, w_router=g["w_router"],
+                  alpha=0.005, beta=0.005)
+    torch.cuda.synchronize()
+    outs = []
+    for bind in (True, False):
+        out = torch.full_like(g["x"], float("nan"))
+        loss = torch.empty(layer.V, dtype=torch.float64, device="cuda")
+        layer.set_output(out if bind else None)
+        bench.step(layer, dict(x=g["x"], w_router=g["w_router"], W1t=g["W1t"], W2t=g["W2t"], b1=g["b1"],
+                               b2=g["b2"], out=out, loss=loss, fused_gate=False))
+        torch.cuda.synchronize()
+        assert layer.get_error() == 0
+        outs.append((out, loss))
+    for out, loss in outs:
+        assert torch.equal(out, ref) and torch.equal(loss, loss_ref)
+    # bound to one buffer, combined into another: refused
+    other = torch.empty_like(g["x"])
+    layer.set_output(outs[0][0])
+    inp = dict(x=g["x"], w_router=g["w_router"], W1t=g["W1t"], W2t=g["W2t"], b1=g["b1"], b2=g["b2"],
+               out=other, loss=outs[0][1], fused_gate=False)
+    with pytest.raises(SmileError):
+        bench.step(layer, inp)
+    layer.set_output(None)
+    layer.close()
