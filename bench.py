@@ -578,6 +578,10 @@ def run_ours(args):
         nccl_id = bytes(buf.cpu().numpy().tobytes())
 
     modes = ["bilevel", "flat"] if args.mode == "both" else [args.mode]
+    if args.fused_gate:
+        # smile_gate_dispatch_inter is the 128-token tensor-core gate (it refuses the
+        # default swapped 256-token tile with SMILE_ENOTSUP): select that tile
+        os.environ["SMILE_GATE_SWAP"] = "0"
     V = G // world
     T, d, d_ff, e = cfgd["T"], cfgd["d"], cfgd["d_ff"], cfgd["e"]
     tdt = torch.bfloat16 if cfgd["dtype"] == "bf16" else torch.float32
@@ -731,6 +735,20 @@ def run_ours(args):
             nvl = {"world": sum(int(c1[v, E]) for v in range(V) for E in range(c1.shape[1]) if (E // e) // V != rank) * rb}
         ffn_ms = phase_ms["ffn"] if not train else None
         ffn_tc = cfgd["dtype"] == "bf16" and args.ffn != "simt" and smb.TCGEN05_DEFAULT
+        if (mode == "flat" and args.exchange == "peer" and ffn_tc and not train
+                and os.environ.get("SMILE_OUT_DIRECT", "1") != "0" and not inp.get("fused_gate")):
+            # FLAT gets the same GEMM 2 -> out fusion: out[t] for tokens whose expert is in this
+            # process; combine1 moves the other kept tokens and zeroes drops
+            import numpy as np
+            d1 = w["dest1"].cpu().numpy()
+            s1 = w["slot1"].cpu().numpy()
+            kept_l1 = s1 < L.C1
+            remote = kept_l1 & ((d1 // e) // V != rank)
+            if L.V == L.G:
+                hbm["dispatch1"] = hbm.get("dispatch1", 0) + int((~kept_l1).sum()) * rb
+                hbm["combine1"] = 0
+            else:
+                hbm["combine1"] = (2 * int(remote.sum()) + int((~kept_l1).sum())) * rb
         if (mode == "bilevel" and args.exchange == "peer" and ffn_tc
                 and os.environ.get("SMILE_RET_DIRECT", "1") != "0"):
             # GEMM 2 wrote the rows of this process's intermediates straight into ret1

@@ -61,7 +61,10 @@ typedef enum {
     SMILE_ECUDA = 4,       /* a CUDA runtime call failed */
     SMILE_ENCCL = 5,       /* an NCCL call failed */
     SMILE_ENOTSUP = 6,     /* valid but unsupported combination */
-    SMILE_EINDEX = 7       /* device: routing index out of range (corrupt route input) */
+    SMILE_EINDEX = 7,      /* device: routing index out of range (corrupt route input) */
+    SMILE_ETIMEOUT = 8     /* device: a peer process did not reach a peer-exchange barrier within
+                              the barrier timeout (smile_register_workspace); the step's data are
+                              not valid */
 } smile_status;
 
 typedef enum { SMILE_FP32 = 0, SMILE_BF16 = 1 } smile_dtype;
@@ -112,6 +115,12 @@ int64_t      smile_launch_count(void);
  * can verify its mirrors of the structs. */
 smile_status smile_struct_sizes(int64_t *out, int32_t n);
 const char  *smile_strerror(smile_status s);
+/* Pure host: the capacity of one (sending rank, destination) pair, ceil(cf * T / dests)
+ * (the capacity factor of P:L207 applied to the equal-split buffers of P:L67-71; R5),
+ * with a single-destination level having no capacity (dests == 1 -> T, R20) and T == 0
+ * -> 0.  Computed in double then rounded up (exact for the paper's cf in {1, 1.25, 2}).
+ * Returns -1 for T < 0, dests < 1 or cf <= 0 (or cf NaN). */
+int64_t      smile_capacity(int64_t T, int64_t dests, double cf);
 /* Pure host function, usable without a GPU: fills *out from *shape or returns
  * SMILE_EINVAL (n, m, e, d, d_ff < 1, T < 0, cf <= 0, nprocs not dividing G, ...). */
 smile_status smile_plan(const smile_shape *shape, smile_sizes *out);
@@ -176,22 +185,35 @@ smile_status smile_ipc_handle(smile_ctx ctx, const void *ws, uint8_t out[72]);
  * smile_forward and selects the exchange.  PEER with nprocs > 1: `handles` = the nprocs
  * handles from smile_ipc_handle in process order (collective; the caller must barrier all
  * processes after this call returns, before the first smile_forward); nprocs == 1:
- * handles may be NULL.  Synchronises the device. */
+ * handles may be NULL.  Synchronises the device.
+ * Barriers: each All2All of the peer exchange is a flag barrier of the processes of the
+ * level; its epoch counter lives on the device (one per level, advanced by the barrier
+ * kernel itself), so a captured CUDA graph of the steps stays correct on every replay.
+ * A barrier that waits longer than SMILE_BARRIER_TIMEOUT_MS (environment, read here;
+ * default 60000, 0 = wait forever) for a peer gives up, sets the sticky device flag to
+ * SMILE_ETIMEOUT (smile_get_error) and lets the stream continue (the step's results are
+ * then invalid) instead of hanging or trapping the context. */
 smile_status smile_register_workspace(smile_ctx ctx, void *ws, const uint8_t *handles, int32_t xchg);
 /* Binds the layer output out [V, T, d] (dtype) for the following step calls (NULL unbinds;
  * smile_forward binds its io->out for the duration of an inference call by itself).  With
- * the peer-store exchange, BILEVEL, bf16 and the tcgen05 FFN, an inference forward then
- * also fuses the level-1 return: the level-1 permute records each row's source token at
- * the intermediate, the level-2 permute forwards it to the expert, and GEMM 2 writes
- * out[t] = bf16(gate[t] * bf16(y)) (R24, the same arithmetic as smile_combine(1)) for every
- * token whose intermediate and expert share the process; smile_combine(1) into the same
- * out fills only the other tokens, and tokens dropped at level 2 get their zero row from
- * the level-2 permute.  When every rank of the job is in this process (G == V) the
- * level-1 permute also writes the zero rows of tokens dropped at level 1, and
- * smile_combine(1) into the bound out returns without launching anything.  After such a
- * forward, smile_combine(1) into any other buffer fails with SMILE_EINVAL (the fused rows
- * were never written to ret1).  Not used by smile_expert_ffn_train (the backward needs
- * ret1).  SMILE_OUT_DIRECT=0 disables it. */
+ * the peer-store exchange, bf16 and the tcgen05 FFN, an inference forward then also fuses
+ * the level-1 return into the expert FFN's GEMM 2, in both modes:
+ *  - BILEVEL: the level-1 permute records each row's source token at the intermediate,
+ *    the level-2 permute forwards it to the expert, and GEMM 2 writes
+ *    out[t] = bf16(gate[t] * bf16(y)) (R24, the same arithmetic as smile_combine(1)) for
+ *    every token whose intermediate and expert share the process; tokens dropped at
+ *    level 2 get their zero row from the level-2 permute.
+ *  - FLAT (the Switch layer, P:L43-47 with k = 1): the level-1 permute records each row's
+ *    source token at the expert, and GEMM 2 writes out[t] = bf16(p[t] * bf16(y)) for every
+ *    token whose expert shares the process.
+ * smile_combine(1) into the same out fills only the other tokens.  When every rank of the
+ * job is in this process (G == V) the level-1 permute also writes the zero rows of tokens
+ * dropped at level 1, and smile_combine(1) into the bound out returns without launching
+ * anything.  After such a forward, smile_combine(1) into any other buffer fails with
+ * SMILE_EINVAL -- every time, until the next level-1 dispatch (the fused rows were never
+ * written to ret1 / Y; they are already in the bound buffer).  The gate used is the
+ * route->gate passed to smile_dispatch(1).  Not used by smile_expert_ffn_train (the
+ * backward needs the return rows).  SMILE_OUT_DIRECT=0 disables it. */
 smile_status smile_set_output(smile_ctx ctx, void *out);
 
 /* ---------------- the steps of the layer ---------------- */
@@ -227,17 +249,22 @@ smile_status smile_gate_inter(smile_ctx ctx, const void *x, const float *w_route
                               const smile_stats *stats, int32_t *counts1, void *stream);
 
 /* a1-a4 fused (fused router only): smile_gate_inter followed by smile_dispatch(level 1)
- * in one pass over x where the tensor-core gate applies (bf16, d % 64 == 0): the final
+ * in one pass over x where the 128-token tensor-core gate applies (bf16, d % 64 == 0, the
+ * context created with the 128-token tile: KW > 40 or SMILE_GATE_SWAP=0): the final
  * level-1 slots come from a decoupled look-back over the tiles' destination histograms
  * inside the gate kernel, which then moves every kept row to its slot (send_rows /
  * send_meta as smile_dispatch(1) writes them, or the destinations' receive buffers with
  * the peer-store exchange).  Same outputs as the two calls (route, stats, counts1, rows,
- * meta); elsewhere it runs exactly those two calls.  logits_out: optional [V, T, KW]. */
+ * meta).  Returns SMILE_ENOTSUP (launching nothing) where the fused kernel does not apply,
+ * so a caller always knows which path ran.  logits_out: optional [V, T, KW]. */
 smile_status smile_gate_dispatch_inter(smile_ctx ctx, const void *x, const float *w_router, float *logits_out,
                                        const smile_route *route, const smile_stats *stats, int32_t *counts1,
                                        void *send_rows, int32_t *send_meta, void *stream);
 
-/* a4 (level 1) / a7 (level 2): permute token rows into per-destination send buffers.
+/* a4 (level 1) / a7 (level 2): permute token rows into per-destination send buffers --
+ * the per-peer offset layout of the paper's All2All ("sendbuff + r*rankdiff", P:L67-71,
+ * Fig. code_all2all_nccl) filled in the routing order of P:L107 (a token goes first to a
+ * node, then to a GPU of that node), capacity slots by R5/R8.
  * level 1: rows_in = x [V, T, d]; finalises route->slot1; send_rows [V, K1, C1, d];
  *   send_meta [V, K1, C1] = j of the token in that slot, -1 for empty slots (BILEVEL),
  *   unused (may be NULL) in FLAT.
@@ -249,7 +276,10 @@ smile_status smile_dispatch(smile_ctx ctx, int32_t level, const void *rows_in,
                             const smile_route *route, const int32_t *recv_meta, int32_t *slot2,
                             void *send_rows, int32_t *send_meta, void *stream);
 
-/* a6: level-2 gate at the intermediate rank (i, l): ranks the valid received slots of
+/* a6: level-2 gate at the intermediate rank (i, l) -- the intra-node router's decision
+ * "then assigned to a GPU via an intra-node router" applied where the token lands
+ * after the first of the "four sequential All2All operations"; j itself was
+ * computed at the source from the tied W_q (R12).  Ranks the valid received slots of
  * recv_meta [V, n, C1] per j in received order (source node ascending, then slot,
  * R8) into slot2 [V, n, C1] (block-local until smile_dispatch level 2) and writes
  * counts2 [V, K2] = min(#received per j, C2). */
@@ -276,7 +306,9 @@ smile_status smile_all2all_intra(smile_ctx ctx, int32_t reverse, const void *sen
                                  void *recv_rows, const int32_t *send_cnt, int32_t *recv_cnt,
                                  const int32_t *fwd_counts, void *stream);
 
-/* a9: expert FFN Y = GELU(X W1 + b1) W2 + b2 (exact erf GELU, R21) for every resident
+/* a9: expert FFN -- E_e(x) of P:L45-47 ("the sub-model (e.g. multi-layer perceptron) for
+ * expert e"), the FFN the MoE layer replaces with GELU activation (dropout omitted,
+ * R21): Y = GELU(X W1 + b1) W2 + b2 (exact erf GELU) for every resident
  * expert over its S segments: X, Y [V, S, e, Cseg, d], counts [V, S, e] valid rows per
  * segment; W1t [V*e, d_ff, d] and W2t [V*e, d, d_ff] (K-major transposes, dtype);
  * b1 [V*e, d_ff], b2 [V*e, d] fp32; H_ws [V, S, e, Cseg, d_ff] (dtype).  bf16: tcgen05

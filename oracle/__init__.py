@@ -29,8 +29,11 @@ def build(force: bool = False) -> str:
     contract, e.g. the strict '>' argmax and the fp64 softmax)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-fno-fast-math",
-                               "-ffp-contract=off", "-o", tmp, _SRC, "-lm"])
+        base = ["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-fno-fast-math", "-ffp-contract=off", "-o", tmp, _SRC]
+        try:   # OpenMP only distributes independent rows of the _mt functions (bit-identical results)
+            subprocess.check_call(base + ["-fopenmp", "-lm"], stderr=subprocess.DEVNULL)
+        except subprocess.CalledProcessError:
+            subprocess.check_call(base + ["-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -66,6 +69,11 @@ def lib():
         _lib.oracle_objective.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32] + [_P] * 8 + [C.c_double, _P, _P]
         _lib.oracle_backward.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32, _P, _P, _P, C.POINTER(_Route),
                                          _P, _P, _P, _P, _P, C.c_double] + [_P] * 7
+        _lib.oracle_logits_mt.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]
+        _lib.oracle_out_rows_mt.argtypes = _lib.oracle_out_rows.argtypes
+        _lib.oracle_threads.restype = C.c_int32
+        _lib.oracle_backward_sampled.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32, _P, _P, _P, C.POINTER(_Route),
+                                                 _P, _P, _P, _P, _P, C.c_double, C.c_int64, _P, C.c_int32, _P] + [_P] * 6
     return _lib
 
 
@@ -109,13 +117,20 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def logits(x: np.ndarray, W: np.ndarray) -> np.ndarray:
-    """Eq. (1) logits, fp32 of an fp64 accumulation.  x [rows, d], W [K, d]."""
+def logits(x: np.ndarray, W: np.ndarray, threads: bool = False) -> np.ndarray:
+    """Eq. (1) logits, fp32 of an fp64 accumulation.  x [rows, d], W [K, d].
+    threads=True: oracle_logits_mt (rows over OpenMP threads, bit-identical)."""
     x = np.ascontiguousarray(x, np.float32)
     W = np.ascontiguousarray(W, np.float32)
     out = np.empty((x.shape[0], W.shape[0]), np.float32)
-    lib().oracle_logits(x.shape[0], x.shape[1], W.shape[0], _ptr(x), _ptr(W), _ptr(out))
+    fn = lib().oracle_logits_mt if threads else lib().oracle_logits
+    fn(x.shape[0], x.shape[1], W.shape[0], _ptr(x), _ptr(W), _ptr(out))
     return out
+
+
+def threads() -> int:
+    """OpenMP threads of the _mt functions (1 when the oracle was built without OpenMP)."""
+    return int(lib().oracle_threads())
 
 
 class Route:
@@ -163,9 +178,10 @@ def ffn_row(x, W1, b1, W2, b2) -> np.ndarray:
 
 
 def out_rows(cfg: Config, r: Route, x: np.ndarray, W1=None, b1=None, W2=None, b2=None,
-             rows=None, identity: bool = False) -> np.ndarray:
+             rows=None, identity: bool = False, threads: bool = False) -> np.ndarray:
     """Eq. (3) layer output (fp64) for the global token rows g = rank*T + t.
-    x [G, T, d]; W1 [G*e, d, d_ff], b1 [G*e, d_ff], W2 [G*e, d_ff, d], b2 [G*e, d]."""
+    x [G, T, d]; W1 [G*e, d, d_ff], b1 [G*e, d_ff], W2 [G*e, d_ff, d], b2 [G*e, d].
+    threads=True: oracle_out_rows_mt (rows over OpenMP threads, bit-identical)."""
     x = np.ascontiguousarray(x, np.float32)
     d = x.shape[-1]
     if identity:
@@ -176,8 +192,9 @@ def out_rows(cfg: Config, r: Route, x: np.ndarray, W1=None, b1=None, W2=None, b2
         d_ff = W1.shape[-1]
     rows = np.arange(cfg.G * cfg.T, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
     out = np.empty((rows.shape[0], d), np.float64)
-    lib().oracle_out_rows(C.byref(cfg._c()), d, d_ff, _ptr(x), C.byref(r._s), _ptr(W1), _ptr(b1),
-                          _ptr(W2), _ptr(b2), int(identity), rows.shape[0], _ptr(rows), _ptr(out))
+    fn = lib().oracle_out_rows_mt if threads else lib().oracle_out_rows
+    fn(C.byref(cfg._c()), d, d_ff, _ptr(x), C.byref(r._s), _ptr(W1), _ptr(b1),
+       _ptr(W2), _ptr(b2), int(identity), rows.shape[0], _ptr(rows), _ptr(out))
     return out
 
 
@@ -214,4 +231,28 @@ def backward(cfg: Config, r: Route, x, W1, b1, W2, b2, gout, lam=1.0, W=None, lo
                           _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2), _ptr(gout), lam, _ptr(out["dlogits"]),
                           _ptr(out["dx"]), _ptr_or_none(out["dW"]), _ptr(out["dW1"]), _ptr(out["db1"]),
                           _ptr(out["dW2"]), _ptr(out["db2"]))
+    return out
+
+
+def backward_sampled(cfg: Config, r: Route, x, W1, b1, W2, b2, gout, tokens, cols, lam=1.0, W=None, logits=None):
+    """oracle_backward_sampled: the entries of oracle_backward a full-size test can afford
+    -- dlogits / dx of the listed global token rows, dW1[:, :, cols], db1[:, cols],
+    dW2[:, cols, :] and all of db2 -- bit-identical to the full function's.  Returns a dict
+    of fp64 arrays: dlogits [ntok, KW], dx [ntok, d], dW1c [NE, d, ncol], db1c [NE, ncol],
+    dW2r [NE, ncol, d], db2 [NE, d]."""
+    f = lambda a: None if a is None else np.ascontiguousarray(a, np.float32)
+    x, W1, b1, W2, b2, gout, W, logits = map(f, (x, W1, b1, W2, b2, gout, W, logits))
+    G, T, d = x.shape
+    d_ff = W1.shape[-1]
+    NE = W1.shape[0]
+    KW = cfg.logit_width
+    tokens = np.ascontiguousarray(tokens, np.int64)
+    cols = np.ascontiguousarray(cols, np.int32)
+    nt, nc = tokens.shape[0], cols.shape[0]
+    out = dict(dlogits=np.zeros((nt, KW)), dx=np.zeros((nt, d)), dW1c=np.zeros((NE, d, nc)), db1c=np.zeros((NE, nc)),
+               dW2r=np.zeros((NE, nc, d)), db2=np.zeros((NE, d)))
+    lib().oracle_backward_sampled(C.byref(cfg._c()), d, d_ff, _ptr(x), _ptr_or_none(W), _ptr_or_none(logits),
+                                  C.byref(r._s), _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2), _ptr(gout), lam, nt,
+                                  _ptr(tokens), nc, _ptr(cols), _ptr(out["dlogits"]), _ptr(out["dx"]),
+                                  _ptr(out["dW1c"]), _ptr(out["db1c"]), _ptr(out["dW2r"]), _ptr(out["db2"]))
     return out

@@ -28,6 +28,9 @@
  *   independent library cross-checks).
  */
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -526,4 +529,211 @@ void oracle_backward(const oracle_cfg *c, int32_t d, int32_t d_ff, const float *
     }
     free(xd); free(Wd); free(ld); free(L); free(pv); free(a); free(h); free(y); free(dy); free(dz);
     free(w1); free(w2); free(bb1); free(bb2);
+}
+
+/* ===================================================================================
+ * Full-size parity helpers ("Optional: OpenMP over tokens.  This is
+ * deterministic because tokens are independent").  Each function below evaluates exactly
+ * the arithmetic of a serial function above -- the same loops in the same order for every
+ * output element -- and only hands independent output rows (columns) to different
+ * threads, so its results are bit-identical to the serial function's (pinned in
+ * tests/test_oracle_parallel.py against oracle_logits, oracle_out_rows and
+ * oracle_backward).  Built with -fopenmp when gcc supports it; serial otherwise.
+ * =================================================================================== */
+
+/* oracle_logits over rows distributed to threads. */
+void oracle_logits_mt(int64_t rows, int32_t d, int32_t K, const float *x, const float *W, float *out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < rows; ++r)
+        oracle_logits(1, d, K, x + r * d, W, out + r * K);
+}
+
+/* oracle_out_rows over the listed rows distributed to threads. */
+void oracle_out_rows_mt(const oracle_cfg *c, int32_t d, int32_t d_ff, const float *x,
+                        const oracle_route_out *o, const float *W1, const float *b1,
+                        const float *W2, const float *b2, int32_t identity,
+                        int64_t nrows, const int64_t *rows, double *out) {
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t a = 0; a < nrows; ++a)
+        oracle_out_rows(c, d, d_ff, x, o, W1, b1, W2, b2, identity, 1, rows + a, out + a * d);
+}
+
+/* Number of threads the _mt functions use (1 without OpenMP). */
+int32_t oracle_threads(void) {
+#ifdef _OPENMP
+    int32_t n = 1;
+#pragma omp parallel
+    {
+#pragma omp single
+        n = (int32_t)omp_get_num_threads();
+    }
+    return n;
+#else
+    return 1;
+#endif
+}
+
+/*
+ * oracle_backward (the chain rule of Eq. (3) and Eq. (4), a16-a19) restricted to what a
+ * full-size configuration-C3 test can afford:
+ *   - for each listed token row g = tok[a]: dlogits_s[a][0..KW) and dx_s[a][0..d), the
+ *     values oracle_backward writes to dlogits[g] and dx[g];
+ *   - for each listed intermediate column f = col[b] and EVERY expert ex: dW1c[ex][k][b] =
+ *     dW1[ex][k][f] (all k), db1c[ex][b] = db1[ex][f] and dW2r[ex][b][cc] = dW2[ex][f][cc];
+ *   - db2[ex][cc] for every expert (all columns).
+ * Each of these sums runs over the expert's tokens in ascending global order with the
+ * same per-token factors (fp64 logits, fp64 softmax, gate = p*q, dy = gate*gout,
+ * a_f = b1_f + sum_k x_k W1[k][f] in ascending k, dh_f = sum_cc W2[f][cc] dy_cc in
+ * ascending cc) as oracle_backward, so every returned element equals that function's.
+ * W == NULL: supplied logits (no router part of dx).  All outputs overwritten.
+ */
+void oracle_backward_sampled(const oracle_cfg *c, int32_t d, int32_t d_ff, const float *x, const float *W,
+                             const float *logits, const oracle_route_out *o, const float *W1, const float *b1,
+                             const float *W2, const float *b2, const float *gout, double lam, int64_t ntok,
+                             const int64_t *tok, int32_t ncol, const int32_t *col, double *dlogits_s, double *dx_s,
+                             double *dW1c, double *db1c, double *dW2r, double *db2) {
+    const int64_t G = (int64_t)c->n * c->m, T = c->T, NE = G * c->e;
+    int64_t K1, K2, C1, C2;
+    oracle_sizes(c, &K1, &K2, &C1, &C2);
+    const int64_t KW = c->flat ? K1 : K1 + K2;
+    const int64_t NT = G * T;
+    /* fp64 logits of every token (as logits_f64), and the token -> expert map */
+    double *L = (double *)malloc(sizeof(double) * (size_t)(NT * KW));
+#pragma omp parallel for schedule(static)
+    for (int64_t g = 0; g < NT; ++g)
+        for (int64_t k = 0; k < KW; ++k) {
+            if (!W) { L[g * KW + k] = (double)logits[g * KW + k]; continue; }
+            double acc = 0.0;
+            for (int32_t cc = 0; cc < d; ++cc) acc += (double)x[g * d + cc] * (double)W[k * d + cc];
+            L[g * KW + k] = acc;
+        }
+    double *gate = (double *)malloc(sizeof(double) * (size_t)NT);
+    int64_t *ex_of = (int64_t *)malloc(sizeof(int64_t) * (size_t)NT);
+#pragma omp parallel
+    {
+        double *pv = (double *)malloc(sizeof(double) * (size_t)(K1 + K2));
+#pragma omp for schedule(static)
+        for (int64_t g = 0; g < NT; ++g) {
+            softmax_d(L + g * KW, K1, pv);
+            if (!c->flat) softmax_d(L + g * KW + K1, K2, pv + K1);
+            const int32_t i = o->dest1[g], j = o->dest2[g];
+            gate[g] = pv[i] * (c->flat ? 1.0 : pv[K1 + j]);
+            ex_of[g] = o->keep[g] ? (c->flat ? i : (int64_t)i * K2 + j) : -1;
+        }
+        free(pv);
+    }
+    /* per-expert columns: one (expert, column) task per thread, tokens ascending */
+#pragma omp parallel
+    {
+        double *a_ = (double *)malloc(sizeof(double) * (size_t)d);
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t task = 0; task < NE * (ncol + 1); ++task) {
+            const int64_t ex = task / (ncol + 1), b = task % (ncol + 1);
+            const double *unused = a_;
+            (void)unused;
+            if (b == ncol) {                        /* db2 of expert ex */
+                for (int32_t cc = 0; cc < d; ++cc) db2[ex * d + cc] = 0.0;
+                for (int64_t g = 0; g < NT; ++g) {
+                    if (ex_of[g] != ex) continue;
+                    for (int32_t cc = 0; cc < d; ++cc) db2[ex * d + cc] += gate[g] * (double)gout[g * d + cc];
+                }
+                continue;
+            }
+            const int32_t f = col[b];
+            const float *w1 = W1 + ex * (int64_t)d * d_ff, *w2 = W2 + ex * (int64_t)d_ff * d;
+            double *dW1col = dW1c + ex * (int64_t)d * ncol;
+            double *dW2row = dW2r + (ex * ncol + b) * (int64_t)d;
+            for (int32_t k = 0; k < d; ++k) dW1col[(int64_t)k * ncol + b] = 0.0;
+            for (int32_t cc = 0; cc < d; ++cc) dW2row[cc] = 0.0;
+            double db1f = 0.0;
+            for (int64_t g = 0; g < NT; ++g) {
+                if (ex_of[g] != ex) continue;
+                double af = (double)b1[ex * d_ff + f];
+                for (int32_t k = 0; k < d; ++k) af += (double)x[g * d + k] * (double)w1[(int64_t)k * d_ff + f];
+                const double hf = gelu(af);
+                double dh = 0.0;
+                for (int32_t cc = 0; cc < d; ++cc) {
+                    const double dy = gate[g] * (double)gout[g * d + cc];
+                    dW2row[cc] += hf * dy;
+                    dh += (double)w2[(int64_t)f * d + cc] * dy;
+                }
+                const double dz = dh * gelu_d(af);
+                db1f += dz;
+                for (int32_t k = 0; k < d; ++k) dW1col[(int64_t)k * ncol + b] += (double)x[g * d + k] * dz;
+            }
+            db1c[ex * ncol + b] = db1f;
+        }
+        free(a_);
+    }
+    /* listed tokens: dlogits and dx exactly as oracle_backward's per-token body */
+#pragma omp parallel
+    {
+        double *pv = (double *)malloc(sizeof(double) * (size_t)(K1 + K2));
+        double *a = (double *)malloc(sizeof(double) * (size_t)d_ff), *h = (double *)malloc(sizeof(double) * (size_t)d_ff);
+        double *y = (double *)malloc(sizeof(double) * (size_t)d), *dy = (double *)malloc(sizeof(double) * (size_t)d);
+        double *dz = (double *)malloc(sizeof(double) * (size_t)d_ff);
+        double *w1 = (double *)malloc(sizeof(double) * (size_t)(d * d_ff)), *w2 = (double *)malloc(sizeof(double) * (size_t)(d * d_ff));
+        double *bb1 = (double *)malloc(sizeof(double) * (size_t)d_ff), *bb2 = (double *)malloc(sizeof(double) * (size_t)d);
+        double *xd = (double *)malloc(sizeof(double) * (size_t)d);
+        int64_t ex_loaded = -1;
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t aa = 0; aa < ntok; ++aa) {
+            const int64_t g = tok[aa], r = g / T;
+            const double *Lg = L + g * KW;
+            double *dl = dlogits_s + aa * KW;
+            double *dxg = dx_s + aa * d;
+            for (int32_t cc = 0; cc < d; ++cc) { xd[cc] = (double)x[g * d + cc]; dxg[cc] = 0.0; }
+            softmax_d(Lg, K1, pv);
+            if (!c->flat) softmax_d(Lg + K1, K2, pv + K1);
+            const int32_t i = o->dest1[g], j = o->dest2[g];
+            const double p = pv[i], q = c->flat ? 1.0 : pv[K1 + j];
+            double dgate = 0.0;
+            if (o->keep[g]) {
+                const int64_t ex = c->flat ? i : (int64_t)i * K2 + j;
+                if (ex != ex_loaded) {
+                    for (int64_t z = 0; z < (int64_t)d * d_ff; ++z) { w1[z] = W1[ex * d * d_ff + z]; w2[z] = W2[ex * d_ff * d + z]; }
+                    for (int32_t f = 0; f < d_ff; ++f) bb1[f] = b1[ex * d_ff + f];
+                    for (int32_t cc = 0; cc < d; ++cc) bb2[cc] = b2[ex * d + cc];
+                    ex_loaded = ex;
+                }
+                ffn_fwd_d(d, d_ff, xd, w1, bb1, w2, bb2, a, h, y);
+                const double gt = p * q;
+                for (int32_t cc = 0; cc < d; ++cc) {
+                    dgate += (double)gout[g * d + cc] * y[cc];
+                    dy[cc] = gt * (double)gout[g * d + cc];
+                }
+                for (int32_t f = 0; f < d_ff; ++f) {
+                    double dh = 0.0;
+                    for (int32_t cc = 0; cc < d; ++cc) dh += w2[(int64_t)f * d + cc] * dy[cc];
+                    dz[f] = dh * gelu_d(a[f]);
+                }
+                for (int32_t k = 0; k < d; ++k) {
+                    double s = 0.0;
+                    for (int32_t f = 0; f < d_ff; ++f) s += w1[(int64_t)k * d_ff + f] * dz[f];
+                    dxg[k] += s;
+                }
+            }
+            const double dp = q * dgate, dq = p * dgate;
+            double fp = 0.0;
+            for (int64_t k = 0; k < K1; ++k) fp += ((double)o->A1[r * K1 + k] / (double)T) * pv[k];
+            for (int64_t k = 0; k < K1; ++k) {
+                const double fk = (double)o->A1[r * K1 + k] / (double)T;
+                dl[k] = dp * p * ((k == i ? 1.0 : 0.0) - pv[k]) + lam * c->alpha * (double)K1 / (double)T * pv[k] * (fk - fp);
+            }
+            if (!c->flat) {
+                double fq = 0.0;
+                for (int64_t k = 0; k < K2; ++k) fq += ((double)o->A2[r * K2 + k] / (double)T) * pv[K1 + k];
+                for (int64_t k = 0; k < K2; ++k) {
+                    const double fk = (double)o->A2[r * K2 + k] / (double)T;
+                    dl[K1 + k] = dq * q * ((k == j ? 1.0 : 0.0) - pv[K1 + k]) +
+                                 lam * c->beta * (double)K2 / (double)T * pv[K1 + k] * (fk - fq);
+                }
+            }
+            if (W)
+                for (int64_t k = 0; k < KW; ++k)
+                    for (int32_t cc = 0; cc < d; ++cc) dxg[cc] += dl[k] * (double)W[k * d + cc];
+        }
+        free(pv); free(a); free(h); free(y); free(dy); free(dz); free(w1); free(w2); free(bb1); free(bb2); free(xd);
+    }
+    free(L); free(gate); free(ex_of);
 }

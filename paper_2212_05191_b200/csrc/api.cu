@@ -53,6 +53,7 @@ extern "C" const char *smile_strerror(smile_status s) {
         case SMILE_ENCCL: return "NCCL error";
         case SMILE_ENOTSUP: return "unsupported configuration";
         case SMILE_EINDEX: return "routing index out of range";
+        case SMILE_ETIMEOUT: return "peer-exchange barrier timed out";
     }
     return "unknown status";
 }
@@ -62,6 +63,11 @@ static int64_t capacity(int64_t T, int64_t dests, double cf) {
     if (T <= 0) return 0;
     if (dests <= 1) return T;
     return (int64_t)ceil(cf * (double)T / (double)dests);
+}
+
+extern "C" int64_t smile_capacity(int64_t T, int64_t dests, double cf) {
+    if (T < 0 || dests < 1 || !(cf > 0.0)) return -1;
+    return capacity(T, dests, cf);
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -122,7 +128,7 @@ static void ws_layout(const smile_shape *s, const smile_sizes *z, WsLayout *L, s
     char *rrow = take(bi ? ffn_rows * 4 : 0);       // internal: ret1 row of each expert input row
     if (rrow_out) *rrow_out = rrow;
     char *rtok1 = take(bi ? V * z->K1 * z->C1 * 4 : 0);   // internal: source token per received slot
-    char *rtok2 = take(bi ? ffn_rows * 4 : 0);            // internal: source token per expert row
+    char *rtok2 = take(ffn_rows * 4);                     // internal: source token per expert row
     if (rtok1_out) *rtok1_out = rtok1;
     if (rtok2_out) *rtok2_out = rtok2;
     if (L) L->total = o;
@@ -431,10 +437,17 @@ extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const ui
     smile_ws_view w;
     char *rrow = nullptr, *rtok1 = nullptr, *rtok2 = nullptr;
     ws_layout(&c->shape, &c->sz, nullptr, &w, (char *)ws, &rrow, &rtok1, &rtok2);
-    c->ws_gate = w.route.gate;
     auto off = [&](const void *ptr) { return (int64_t)((const char *)ptr - (const char *)ws); };
     c->off_flags = off(w.flags);
     CUDA_TRY(cudaMemset(w.flags, 0, 3 * kMaxProcs * 8));
+    // barrier epochs live on the device (advanced by the barrier kernel: graph-replay safe)
+    if (!c->d_epoch) CUDA_TRY(cudaMalloc(&c->d_epoch, 3 * sizeof(long long)));
+    CUDA_TRY(cudaMemset(c->d_epoch, 0, 3 * sizeof(long long)));
+    {
+        const char *e = getenv("SMILE_BARRIER_TIMEOUT_MS");
+        const long long ms = e ? atoll(e) : 60000;
+        c->barrier_timeout_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
+    }
     for (int p = 0; p < P; ++p) {
         if (p == me) { c->h_bases[p] = (char *)ws; continue; }
         if (c->h_bases[p]) continue;                       // already opened
@@ -470,7 +483,6 @@ extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const ui
         if (!c->d_peers[level]) CUDA_TRY(cudaMalloc(&c->d_peers[level], sizeof(int32_t) * kMaxProcs));
         if (!peers.empty())
             CUDA_TRY(cudaMemcpy(c->d_peers[level], peers.data(), sizeof(int32_t) * peers.size(), cudaMemcpyHostToDevice));
-        c->epoch[level] = 0;
     }
     PeerMap &pm = c->peer;
     pm.bases = c->d_bases; pm.V = c->sz.V; pm.rank0 = c->sz.rank0; pm.n = bi ? c->shape.n : 0; pm.m = c->shape.m;
@@ -479,7 +491,7 @@ extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const ui
     pm.off_rcounts = off(w.rcounts); pm.off_Y = off(w.Y); pm.off_ret1 = bi ? off(w.ret1) : 0;
     pm.off_rrow = bi ? (int64_t)(rrow - (char *)ws) : 0;
     pm.off_rtok1 = bi ? (int64_t)(rtok1 - (char *)ws) : 0;
-    pm.off_rtok2 = bi ? (int64_t)(rtok2 - (char *)ws) : 0;
+    pm.off_rtok2 = (int64_t)(rtok2 - (char *)ws);
     CUDA_TRY(cudaDeviceSynchronize());
     return SMILE_OK;
 }
@@ -487,7 +499,7 @@ extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const ui
 static void peer_barrier(smile_ctx c, int level, cudaStream_t st) {
     if (c->shape.nprocs <= 1 || c->npeers[level] == 0) return;
     launch_peer_barrier(c->d_bases, c->off_flags, c->shape.proc, c->d_peers[level], c->npeers[level], level,
-                        ++c->epoch[level], st);
+                        c->d_epoch + level, c->barrier_timeout_ns, c->d_err, st);
 }
 
 extern "C" smile_status smile_get_error(smile_ctx c, void *stream) {
@@ -551,13 +563,13 @@ extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, co
     const bool bi = c->shape.mode == SMILE_BILEVEL;
     if (bi && !send_meta) return SMILE_EINVAL;
     if (c->shape.T == 0) return SMILE_OK;
+    // the fused kernel is the 128-token tensor-core gate; elsewhere refuse (the caller runs
+    // smile_gate_inter + smile_dispatch(1) and knows which path ran)
+    if (!c->wsplit || !c->lb_flag || c->TB1 != 128) return SMILE_ENOTSUP;
     c->rtok1_valid = false;                  // this path does not record the source tokens
+    c->out_planned = false;
     c->l1_zeroed = false;
-    if (!c->wsplit || !c->lb_flag || c->TB1 != 128) {
-        // no tensor-core gate for this shape / dtype: the two calls it fuses
-        STEP(smile_gate_inter(c, x, w_router, nullptr, logits_out, route, stats, counts1, stream));
-        return smile_dispatch(c, 1, x, route, nullptr, nullptr, send_rows, send_meta, stream);
-    }
+    c->l1_pending = false;
     cudaSetDevice(c->shape.device);
     const int64_t rb = (int64_t)c->shape.d * (c->shape.dtype == SMILE_BF16 ? 2 : 4);
     GateArgs a{};
@@ -607,8 +619,12 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
         // zero rows of level-1-dropped tokens are written here and combine(1) is skipped
         c->l1_zeroed = out_direct_enabled(c) && c->sz.V == c->sz.G;
         if (c->l1_zeroed) a.out = c->out_bound;
+        c->l1_pending = false;               // a new forward: the previous one's fused rows are history
+        c->d1_gate = route->gate;            // the gate GEMM 2 scales in-process rows by
         launch_dispatch1(a, S(stream));
-        c->rtok1_valid = a.peer.bases != nullptr && bi;
+        c->rtok1_valid = a.peer.bases != nullptr;   // the source token of each row is recorded
+        // FLAT: the permute wrote the rows' source tokens straight to the experts' rtok2
+        if (!bi) c->out_planned = out_direct_possible(c);
         return post_launch();
     }
     if (level == 2) {
@@ -724,10 +740,11 @@ extern "C" smile_status smile_all2all_intra(smile_ctx c, int32_t reverse, const 
     return smile_all2all(c, 2, reverse, send_rows, recv_rows, send_cnt, recv_cnt, fwd_counts, stream);
 }
 
-// PEER + BILEVEL inference with the output bound (smile_set_output) and the tcgen05 FFN:
-// GEMM 2 writes rows whose source rank is in this process straight to out (a12 + a13).
+// PEER inference with the output bound (smile_set_output) and the tcgen05 FFN: GEMM 2
+// writes rows whose source rank is in this process straight to out (BILEVEL: a12 + a13;
+// FLAT: the world reverse exchange + a13) -- both layers get the same fusion.
 static bool out_direct_enabled(smile_ctx c) {
-    if (c->xchg != SMILE_XCHG_PEER || c->shape.mode != SMILE_BILEVEL || !c->out_bound) return false;
+    if (c->xchg != SMILE_XCHG_PEER || !c->out_bound) return false;
     if (c->shape.dtype != SMILE_BF16 || c->shape.ffn_impl == SMILE_FFN_SIMT) return false;
     const char *e = getenv("SMILE_OUT_DIRECT");
     if (e && e[0] == '0') return false;
@@ -763,14 +780,19 @@ extern "C" smile_status smile_expert_ffn(smile_ctx c, const void *X, const int32
     if (impl == SMILE_FFN_TCGEN05) {
         if (!f.bf16) return SMILE_ENOTSUP;
         set_ret_direct(c, f);
+        if (c->shape.mode == SMILE_FLAT && c->out_planned && c->xchg == SMILE_XCHG_PEER) {
+            f.ret = c->peer;                 // bases / rank layout only (FLAT has no ret1)
+            f.flat_out = 1;
+        }
         if (f.ret.bases && c->out_planned) {
-            f.out = c->out_bound; f.gate = c->ws_gate; f.T = c->shape.T; f.C1 = c->sz.C1; f.n = c->shape.n;
+            f.out = c->out_bound; f.gate = c->d1_gate; f.T = c->shape.T; f.C1 = c->sz.C1; f.n = c->shape.n;
             f.rtok2 = reinterpret_cast<const int32_t *>(static_cast<char *>(c->reg_ws) + c->peer.off_rtok2);
         }
         cudaError_t e = launch_ffn_tcgen05(f, S(stream));
         if (e == cudaErrorNotSupported) return SMILE_ENOTSUP;
-        c->ret_direct = f.ret.bases != nullptr;
+        c->ret_direct = f.ret.bases != nullptr && !f.flat_out;
         c->out_direct = f.out != nullptr;
+        if (c->out_direct) c->l1_pending = true;
         return e == cudaSuccess ? post_launch() : SMILE_ECUDA;
     }
     if (!ffn_simt_supported(f.V * f.S * f.e, f.d, f.d_ff)) return SMILE_ENOTSUP;
@@ -789,13 +811,13 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
         Combine1Args a{};
         a.back1 = ret_rows; a.route = *route; a.out = out; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
         a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = bf; a.nogate = 0; a.peer = peer_of(c);
-        if (c->out_direct && out != c->out_bound) {
-            // GEMM 2 wrote the in-process tokens to the bound output, not to ret1: a combine
-            // into another buffer would read stale rows
-            c->out_direct = false;
-            c->l1_zeroed = false;
+        if (c->l1_pending && out != c->out_bound) {
+            // GEMM 2 wrote the in-process tokens to the bound output, not to ret1 / Y: a
+            // combine into another buffer would read stale rows -- refused until the next
+            // level-1 dispatch starts a new forward (sticky)
             return SMILE_EINVAL;
         }
+        c->l1_pending = false;
         a.skip_direct = (a.peer.bases && c->out_direct) ? 1 : 0;
         c->out_direct = false;
         if (a.skip_direct && c->l1_zeroed && c->sz.V == c->sz.G) {

@@ -70,6 +70,8 @@ struct TcArgs {
     const int32_t *rtok2;
     int64_t T, C1;
     int n;
+    int flat_out;              // FLAT: segment l of an expert holds source rank l's rows; rows of
+                               // in-process sources go to out[t] as bf16(p[t] * bf16(y))
     int diag;                  // measurement only (SMILE_FFN_DIAG; wrong results): 1 no activation,
                                // 2 no stores, 4 no TMEM reads / epilogue math (release only),
                                // 8 TMA stores into rows [0, 1024) only (L2-resident)
@@ -461,7 +463,18 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             bool rlocal = false, rout = false;
             char *rdst = nullptr;
             float rgate = 0.f;
-            if (EK == 0 && a.rbases && srows > 0) {
+            if (EK == 0 && a.rbases && srows > 0 && a.flat_out) {
+                // FLAT (Switch): segment l is source rank l; one decision per warp
+                const int64_t seg = d_row / a.Cseg;                    // (v * G + l) * e + k
+                const int l = (int)((seg / a.e) % a.S);
+                rlocal = l / a.rV == a.rrank0 / a.rV;
+                if (rlocal && lane < srows) {
+                    const int64_t tok = (int64_t)(l % a.rV) * a.T + a.rtok2[d_row + lane];
+                    rdst = a.out + tok * a.N * 2 + dcol0 * 2;
+                    rgate = a.gate[tok];
+                    rout = true;
+                }
+            } else if (EK == 0 && a.rbases && srows > 0) {
                 const int64_t seg = d_row / a.Cseg;                    // (v * S + l) * e + k
                 const int vv = (int)(seg / ((int64_t)a.S * a.e)), l = (int)((seg / a.e) % a.S);
                 const int u = (a.rrank0 + vv) / a.rm * a.rm + l;       // intermediate (i, l)
@@ -801,6 +814,8 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
             a.out = static_cast<char *>(f.out); a.gate = f.gate; a.rtok2 = f.rtok2;
             a.T = f.T; a.C1 = f.C1; a.n = f.n;
         }
+        a.flat_out = f.flat_out;
+        if (f.flat_out && !f.out) a.rbases = nullptr;       // nothing to fuse without the output
     }
     a.err = nullptr;
     const size_t smem = smem_bytes(CG, NSUB, a.stages, nbox, a.tma_store, a.box64, a.nseg);

@@ -323,6 +323,10 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
                 if (a.meta) {
                     reinterpret_cast<int32_t *>(base + P.off_rmeta1)[row] = a.route.dest2[g];
                     reinterpret_cast<int32_t *>(base + P.off_rtok1)[row] = (int32_t)t;   // source token
+                } else {
+                    // flat: the received row IS the expert's input row -- its source token
+                    // lets GEMM 2 write the output row straight to out[t] (smile_set_output)
+                    reinterpret_cast<int32_t *>(base + P.off_rtok2)[row] = (int32_t)t;
                 }
             } else {
                 const int64_t dst_row = ((int64_t)v * a.K1 + i) * a.C1 + slot;
@@ -447,6 +451,10 @@ __device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
                     r.src = P.bases[u / P.V] + P.off_ret1 + (((int64_t)(u % P.V) * P.n + s_) * a.C1 + s1) * rb;
                 } else {         // flat: peer load of Y from the expert rank E / e
                     const int q = i / P.e;
+                    if (a.skip_direct && q / P.V == P.rank0 / P.V) {   // written by the expert's GEMM 2
+                        r.dst = nullptr;
+                        return r;
+                    }
                     r.src = P.bases[q / P.V] + P.off_Y + ((((int64_t)(q % P.V) * P.G + rk) * P.e + i % P.e) * a.C1 + s1) * rb;
                 }
             } else {
@@ -619,12 +627,16 @@ __global__ void exchange_copy_kernel(CopyXArgs a) {
     }
 }
 
-// Process-level barrier over NVLink (peer-store exchange): after a fence, write `epoch`
-// into flag[level][me] of every peer process's workspace, then wait until every peer
-// has written at least `epoch` into ours.  One thread; bounded spin (traps, never hangs).
+// Process-level barrier over NVLink (peer-store exchange): advance this level's epoch
+// counter (device memory: every launch, graph replays included, gets the next epoch),
+// after a fence write it into flag[level][me] of every peer process's workspace, then
+// wait until every peer has written at least that epoch into ours.  One thread.  A wait
+// longer than timeout_ns (0 = forever) sets the sticky SMILE_ETIMEOUT flag and returns.
 __global__ void peer_barrier_kernel(char *const *bases, int64_t off_flags, int me, const int32_t *peers, int npeers,
-                                    int level, long long epoch) {
+                                    int level, long long *epoch_ctr, unsigned long long timeout_ns, int *err) {
     if (threadIdx.x != 0) return;
+    const long long epoch = *epoch_ctr + 1;
+    *epoch_ctr = epoch;
     __threadfence_system();
     for (int i = 0; i < npeers; ++i) {
         long long *f = reinterpret_cast<long long *>(bases[peers[i]] + off_flags) + level * kMaxProcs + me;
@@ -640,7 +652,11 @@ __global__ void peer_barrier_kernel(char *const *bases, int64_t off_flags, int m
             if (v >= epoch) break;
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > 10000000000ull) __trap();       // 10 s without the peer: abort, never hang
+            if (timeout_ns && t - t0 > timeout_ns) {     // the peer never came: report, never hang
+                set_err(err, SMILE_ETIMEOUT);
+                __threadfence_system();
+                return;
+            }
         }
     }
     __threadfence_system();
@@ -782,10 +798,10 @@ void launch_aux(const smile_stats &s, double alpha, double beta, double *loss, i
 }
 
 void launch_peer_barrier(char *const *bases, int64_t off_flags, int me, const int32_t *peers, int npeers, int level,
-                         long long epoch, cudaStream_t st) {
+                         long long *epoch, unsigned long long timeout_ns, int *err, cudaStream_t st) {
     if (npeers <= 0) return;
     note_launch();
-    peer_barrier_kernel<<<1, 32, 0, st>>>(bases, off_flags, me, peers, npeers, level, epoch);
+    peer_barrier_kernel<<<1, 32, 0, st>>>(bases, off_flags, me, peers, npeers, level, epoch, timeout_ns, err);
 }
 
 void launch_exchange_copy(const CopyXArgs &a, cudaStream_t st) {

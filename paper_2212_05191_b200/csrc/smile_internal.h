@@ -51,7 +51,7 @@ struct PeerMap {
     int64_t off_recv1, off_rmeta1, off_recv2, off_rcounts, off_Y, off_ret1;
     int64_t off_rrow;                  // BILEVEL: [V, S, e, Cseg] i32 ret1 row of each expert input row
     int64_t off_rtok1;                 // BILEVEL: [V, n, C1] i32 source token of each received slot
-    int64_t off_rtok2;                 // BILEVEL: [V, S, e, Cseg] i32 source token of each expert input row
+    int64_t off_rtok2;                 // [V, S, e, Cseg] i32 source token of each expert input row
 };
 constexpr int kMaxProcs = 64;
 
@@ -67,7 +67,9 @@ struct smile_ctx_s {
     bool out_planned = false;  // PEER: this forward writes in-process rows straight to out
     bool out_direct = false;   // ... and the last expert FFN did
     bool l1_zeroed = false;    // ... and the level-1 permute wrote the level-1-dropped zero rows
-    const float *ws_gate = nullptr;   // route.gate in the registered workspace
+    bool l1_pending = false;   // the last expert FFN wrote out rows directly: until the next level-1
+                               // dispatch, smile_combine(1) may only target the bound output
+    const float *d1_gate = nullptr;   // route->gate of the last smile_dispatch(1)
     int nblk1 = 0;             // gate blocks per rank
     int nblk2 = 0;             // level-2 ranking blocks per rank
     int *d_err = nullptr;      // sticky device error flag (smile_status)
@@ -86,7 +88,8 @@ struct smile_ctx_s {
     int64_t off_flags = 0;                   // barrier flags inside a workspace
     int32_t *d_peers[3] = {};                // per level: processes to synchronise with
     int npeers[3] = {};
-    long long epoch[3] = {};
+    long long *d_epoch = nullptr;            // [3] device barrier epochs (advanced by the barrier kernel)
+    unsigned long long barrier_timeout_ns = 0;   // 0: wait forever (SMILE_BARRIER_TIMEOUT_MS)
     smile::PeerMap peer{};
     // tensor-core gate (bf16 fused router): the three-piece bf16 split of the router
     __nv_bfloat16 *wsplit = nullptr;         // [gate_tc_np(KW), d], rewritten every fused gate call
@@ -189,8 +192,10 @@ void launch_router_bwd(const RouterBwdArgs &a, cudaStream_t st);
 size_t router_bwd_partial_floats(int64_t rows, int d, int KW);
 
 // Process-level barrier of one level over NVLink flags (peer-store exchange).
+// The epoch is a device counter advanced by the kernel (CUDA-graph replay safe); a wait
+// longer than timeout_ns (0 = forever) sets *err = SMILE_ETIMEOUT and returns.
 void launch_peer_barrier(char *const *bases, int64_t off_flags, int me, const int32_t *peers, int npeers, int level,
-                         long long epoch, cudaStream_t st);
+                         long long *epoch, unsigned long long timeout_ns, int *err, cudaStream_t st);
 
 void launch_aux(const smile_stats &s, double alpha, double beta, double *loss, int V, int K1,
                 int K2, int64_t T, int flat, cudaStream_t st);
@@ -214,6 +219,9 @@ struct FfnArgs {
     // inference with the layer output bound (smile_set_output): rows whose source rank is
     // in this process too go straight to out[t] as gate * y (a12 + a13 fused as well)
     void *out; const float *gate; const int32_t *rtok2; int64_t T, C1; int n;
+    // FLAT: ret carries only the process layout; segment s of an expert is source rank s,
+    // and rows of in-process sources go straight to out (rtok2 from the level-1 permute)
+    int flat_out;
 };
 void launch_ffn_simt(const FfnArgs &a, cudaStream_t st);
 

@@ -22,7 +22,8 @@ FFN_AUTO, FFN_SIMT, FFN_TCGEN05 = 0, 1, 2
 XCHG_COPY, XCHG_PEER = 0, 1
 TCGEN05_DEFAULT = True    # AUTO resolves bf16 to the tcgen05 FFN (api.cu smile_expert_ffn)
 _STATUS = {0: "ok", 1: "invalid argument", 2: "shape or layout mismatch", 3: "non-finite router logit",
-           4: "CUDA error", 5: "NCCL error", 6: "unsupported configuration", 7: "routing index out of range"}
+           4: "CUDA error", 5: "NCCL error", 6: "unsupported configuration", 7: "routing index out of range",
+           8: "peer-exchange barrier timed out"}
 
 
 class SmileError(RuntimeError):
@@ -83,6 +84,8 @@ def lib():
         L.smile_version.restype = C.c_int
         L.smile_strerror.restype = C.c_char_p
         L.smile_launch_count.restype = C.c_int64
+        L.smile_capacity.restype = C.c_int64
+        L.smile_capacity.argtypes = [C.c_int64, C.c_int64, C.c_double]
         for name in ("smile_plan", "smile_group", "smile_exchange_plan", "smile_get_unique_id", "smile_create", "smile_destroy",
                      "smile_query", "smile_get_error", "smile_gate_inter", "smile_dispatch", "smile_gate_intra",
                      "smile_all2all", "smile_all2all_inter", "smile_all2all_intra", "smile_expert_ffn",
@@ -119,6 +122,11 @@ def plan(**kw) -> Sizes:
     z = Sizes()
     _check(lib().smile_plan(C.byref(_shape(**kw)), C.byref(z)), "smile_plan")
     return z
+
+
+def capacity(T: int, dests: int, cf: float) -> int:
+    """Host-only: ceil(cf*T/dests) per (sending rank, destination) (smile_capacity; -1 if invalid)."""
+    return int(lib().smile_capacity(T, dests, cf))
 
 
 def group(n: int, m: int, level: int, r: int) -> list[int]:

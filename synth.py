@@ -9,7 +9,8 @@ Recipe:
   * x ~ N(0, 1) per rank, rounded to the layer dtype.
   * router W = [W_p; W_q] ~ U(+-1/sqrt(d)) (balanced routing, logit std ~0.58).
   * supplied logits: "balanced" N(0, 0.58); "skewed" N(0, 1) - ln(k+1) (Zipf-like
-    popularity, exercises drops); "ties" drawn from {-1, 0, 1} (plants exact ties).
+    popularity, exercises drops); "ties" drawn from {-1, 0, 1} (plants exact ties); "signed_zero" from {-1, -0.0, +0.0, 1}
+    (R28: signed-zero ties).
   * experts: W1 ~ U(+-1/sqrt(d)), W2 ~ U(+-1/sqrt(d_ff)); biases 0 for the bench,
     U(+-0.1) for parity runs.
 Seeds: stream (seed, rank, tag) through numpy's SeedSequence, so every rank's inputs are
@@ -62,6 +63,12 @@ def supplied_logits(G: int, T: int, K: int, seed: int = 0, dist: str = "balanced
             out[r] = g.standard_normal((T, K), dtype=np.float32) - np.log1p(k).astype(np.float32)
         elif dist == "ties":
             out[r] = g.integers(-1, 2, size=(T, K)).astype(np.float32)
+        elif dist == "signed_zero":
+            # R28: entries from {-1, -0.0, +0.0, +1} -- -0.0 and +0.0 compare equal under '>',
+            # so a row whose maxima are signed zeros is a tie the lowest index wins
+            v = g.integers(-1, 2, size=(T, K)).astype(np.float32)
+            neg = g.integers(0, 2, size=(T, K)).astype(bool)
+            out[r] = np.where((v == 0) & neg, np.float32(-0.0), v)
         else:
             raise ValueError(dist)
     return out

@@ -77,3 +77,37 @@ def assert_close_scaled(got, ref, rtol, what=""):
         idx = np.unravel_index(np.argmax(err), err.shape)
         raise AssertionError(f"{what}: {int((err > 0).sum())} mismatches; worst at {idx}: got {got[idx]} "
                              f"ref {ref[idx]} (rtol {rtol}, atol {atol:.3e})")
+
+
+def dense_rows(case, r, stride=32):
+    """Global token rows g = rank*T + t for full-size output parity:
+    at least one row of every `stride`-row strip of every expert segment (the tcgen05 FFN
+    works in 32-row strips, so stride 32 touches every strip and hence every M tile), the
+    first and last row of every segment, and every dropped token.  Pure index bookkeeping
+    on the oracle's route (no arithmetic of the method)."""
+    G, T, m, e = case.G, case.T, case.m, case.e
+    g = np.arange(G * T)
+    rr = g // T
+    d1 = r.dest1.reshape(-1).astype(np.int64)
+    s1 = r.slot1.reshape(-1).astype(np.int64)
+    keep = r.keep.reshape(-1).astype(bool)
+    if case.flat:
+        key = ((d1 // e) * G + rr) * e + d1 % e          # (expert rank, source rank, local expert)
+        pos = s1
+        cnt = r.counts1[rr, d1]
+    else:
+        K2, C1 = r.K2, r.C1
+        d2 = r.dest2.reshape(-1).astype(np.int64)
+        s, l = rr // m, rr % m
+        u = d1 * m + l
+        keep1 = r.keep1.reshape(-1).astype(bool)
+        pos = np.full(G * T, -1, np.int64)
+        pos[keep1] = r.slot2[u[keep1], s[keep1] * C1 + s1[keep1]]
+        key = ((d1 * m + d2 // e) * m + l) * e + d2 % e  # (expert rank, source intermediate, local expert)
+        cnt = r.counts2[u, d2]
+    sel = keep & ((pos % stride == 0) | (pos == cnt - 1))
+    rows = np.flatnonzero(sel | ~keep)
+    # every segment that holds rows contributes its first and last row
+    ks = key[keep]
+    assert np.unique(ks[(pos[keep] == 0)]).size == np.unique(ks).size
+    return rows

@@ -106,6 +106,24 @@ def test_shapes(n, m, e, T, cf, dtype, mode):
     run_and_check(Case(n, m, e, T, 64, 128, cf, dtype=dtype, mode=mode, dist="skewed", seed=3))
 
 
+@pytest.mark.parametrize("mode,n,m,e", [("bilevel", 2, 4, 1), ("bilevel", 4, 2, 2), ("flat", 2, 4, 1)])
+def test_signed_zero_ties(mode, n, m, e):
+    """R28: logits from {-1, -0.0, +0.0, +1}: -0.0 == +0.0 under the strict '>' scan, so a
+    row whose maximum is a signed zero routes to the LOWEST index holding +-0.0 -- GPU and
+    oracle must agree bit-exactly (a bitwise or fmaxf argmax would order the zeros)."""
+    case = Case(n, m, e, 777, 64, 128, 1.0, dtype="bf16", mode=mode, dist="signed_zero", seed=41)
+    K1 = n if mode == "bilevel" else case.G * e
+    lg1 = case.logits[:, :, :K1]
+    # the planted case really occurs: rows whose maximum is zero with -0.0 before +0.0
+    zmax = (lg1.max(-1) == 0)
+    first_neg = np.signbit(lg1) & (lg1 == 0)
+    assert (zmax & first_neg.any(-1)).sum() > 50
+    _, _, _, r = run_and_check(case)
+    # and the oracle itself picks the lowest zero index, signs ignored
+    g, t = np.argwhere(zmax)[0]
+    assert r.dest1[g, t] == int(np.flatnonzero(lg1[g, t] == 0)[0])
+
+
 def test_identity_collapse_n1_equals_flat():
     """n = 1 bi-level equals flat Switch over the intra router (R20): same outputs."""
     a = Case(1, 4, 1, 500, 64, 128, 1.0, mode="bilevel", dist="skewed", seed=4)
@@ -464,18 +482,21 @@ def test_ret_direct_bit_identical(n, m, e, T, d, d_ff, cf, monkeypatch):
     assert torch.equal(outs["0"][0], outs["1"][0]) and torch.equal(outs["0"][1], outs["1"][1])
 
 
-@pytest.mark.parametrize("n,m,e,T,d,d_ff,cf", [
-    (2, 4, 1, 1000, 128, 256, 1.25),       # level-1 and level-2 drops
-    (4, 2, 2, 700, 64, 128, 1.0),
-    (1, 8, 1, 333, 128, 256, 2.0),         # one node: every token's return fused into GEMM 2
+@pytest.mark.parametrize("n,m,e,T,d,d_ff,cf,mode", [
+    (2, 4, 1, 1000, 128, 256, 1.25, "bilevel"),       # level-1 and level-2 drops
+    (4, 2, 2, 700, 64, 128, 1.0, "bilevel"),
+    (1, 8, 1, 333, 128, 256, 2.0, "bilevel"),         # one node: every token's return fused into GEMM 2
+    (2, 4, 1, 1000, 128, 256, 1.25, "flat"),          # the Switch layer gets the same fusion (drops)
+    (4, 2, 2, 700, 64, 128, 0.75, "flat"),            # 16 experts, e = 2, heavy drops
 ])
-def test_out_direct_bit_identical(n, m, e, T, d, d_ff, cf, monkeypatch):
+def test_out_direct_bit_identical(n, m, e, T, d, d_ff, cf, mode, monkeypatch):
     """Peer exchange, inference: GEMM 2 writing out[t] = bf16(gate * bf16(y)) for tokens whose
-    intermediate and expert share the process (SMILE_OUT_DIRECT, default) gives outputs
-    bit-identical to ret1 + combine(1), with out garbage-filled first, and matches the oracle."""
+    intermediate and expert (FLAT: expert) share the process (SMILE_OUT_DIRECT, default)
+    gives outputs bit-identical to the unfused return + combine(1), with out garbage-filled
+    first, and matches the oracle (Eq. 3; FLAT: Switch Eq. 2 with k = 1)."""
     from paper_2212_05191_b200 import SmileLayer
-    case = Case(n, m, e, T, d, d_ff, cf, dtype="bf16", dist="skewed", seed=23)
-    layer = SmileLayer(n, m, e, d, d_ff, T, cf, "bf16", "bilevel")
+    case = Case(n, m, e, T, d, d_ff, cf, dtype="bf16", dist="skewed", seed=23, mode=mode)
+    layer = SmileLayer(n, m, e, d, d_ff, T, cf, "bf16", mode)
     layer.enable_peer_exchange()
     g = case.gpu_tensors()
     outs = {}
@@ -537,5 +558,10 @@ def test_out_direct_step_api():
                out=other, loss=outs[0][1], fused_gate=False)
     with pytest.raises(SmileError):
         bench.step(layer, inp)
+    w = layer._view
+    for _ in range(2):                     # sticky: refused again until the next level-1 dispatch
+        with pytest.raises(SmileError):
+            layer.combine(1, C_ptr(w.back1), other, route=w.route)
+    layer.combine(1, C_ptr(w.back1), outs[0][0], route=w.route)     # the bound output is still fine
     layer.set_output(None)
     layer.close()

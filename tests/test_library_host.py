@@ -84,3 +84,18 @@ def test_plan_sizes_and_validation():
     with pytest.raises(smb.SmileError) as ei:
         sm.plan(**{**bad, "d": 6})                  # rows must be 16-byte multiples
     assert ei.value.code == 2
+
+
+def test_capacity_matches_oracle():
+    """smile_capacity: ceil(cf*T/dests) per (sending rank, destination),
+    P:L207 + R5 / R20, against the pinned oracle_capacity (tests/test_oracle_routing.py)
+    over the paper's capacity factors, ragged T and the single-destination identity."""
+    import oracle
+    for T in (0, 1, 7, 8, 255, 1000, 16384, 32768, 65536, 1 << 30):
+        for dests in (1, 2, 3, 4, 7, 8, 32, 64, 128):
+            for cf in (0.5, 1.0, 1.25, 2.0, 8.0):
+                assert smb.capacity(T, dests, cf) == oracle.capacity(T, dests, cf), (T, dests, cf)
+    assert smb.capacity(8, 4, 2.0) == 4 and smb.capacity(7, 2, 1.0) == 4       # S:L281-283
+    assert smb.capacity(16384, 1, 2.0) == 16384                                 # R20: no capacity
+    for bad in ((-1, 2, 1.0), (10, 0, 1.0), (10, 2, 0.0), (10, 2, -1.0), (10, 2, float("nan"))):
+        assert smb.capacity(*bad) == -1, bad

@@ -30,6 +30,12 @@ def _cases(ngpu):
                dict(n=2, m=4, e=1, cf=2.0, dtype="bf16", mode="bilevel", **base)]     # V=2 mixed
     # the same cases through the fused permute -> peer-store exchange (CUDA IPC + NVLink)
     cs = cs + [dict(c, _peer=True) for c in cs]
+    # CUDA-graph replays of the peer exchange (device-side barrier epochs) on new inputs
+    if ngpu >= 2:
+        cs += [dict(n=2, m=4, e=1, cf=1.0, dtype="bf16", mode="bilevel", _peer=True, _graph=True, **base),
+               dict(n=2, m=1, e=2, cf=1.25, dtype="bf16", mode="flat", _peer=True, _graph=True, **base)]
+    if ngpu >= 4:
+        cs += [dict(n=2, m=2, e=1, cf=1.0, dtype="bf16", mode="bilevel", _peer=True, _graph=True, **base)]
     # training steps (a16-a19) over both exchanges
     bw = dict(T=400, d=128, d_ff=256, dist="skewed", seed=12)
     if ngpu >= 2:
