@@ -41,6 +41,12 @@ CONFIGS = {
     "c3_4x2": dict(n=4, m=2, e=1, T=32768, d=768, d_ff=3072, cf=1.25, dtype="bf16", train=True),
     "c4": dict(n=2, m=4, e=8, T=65536, d=1024, d_ff=4096, cf=2.0, dtype="bf16"),
     "c5": dict(n=2, m=4, e=16, T=8192, d=1600, d_ff=6400, cf=2.0, dtype="bf16"),
+    # multi-node topologies emulated on one B200 for the emulated-fabric runs (--fabric; the
+    # paper's nodes x GPUs, P:L287 -- 32 ranks, the most the flat layer's 1024 FFN segments
+    # allow): C2's widths with 4K tokens per rank, and C1's
+    "e4x8": dict(n=4, m=8, e=1, T=4096, d=768, d_ff=3072, cf=2.0, dtype="bf16"),
+    "e8x4": dict(n=8, m=4, e=1, T=4096, d=768, d_ff=3072, cf=2.0, dtype="bf16"),
+    "e4x8_c1": dict(n=4, m=8, e=1, T=1024, d=64, d_ff=256, cf=1.0, dtype="fp32"),
 }
 METRIC = "MoE-layer tokens/sec (bi-level vs flat All2All) at 1/2/4/8 B200; kernel HBM GB/s"
 
@@ -62,6 +68,9 @@ def parse():
     ap.add_argument("--chunks", type=int, default=1,
                     help="> 1: the layer as c pipelined micro-batches on two streams (SURVEY 8(f) row 2)")
     ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling period (0 = off)")
+    ap.add_argument("--fabric", default=None,
+                    help="GBPS,LATENCY_US: emulated inter-node fabric (smile_set_fabric; SURVEY 8(f) row 1, an in-box "
+                         "emulation) on the COPY exchange, N = 1 only")
     ap.add_argument("--exchange", default="peer", choices=["peer", "copy"],
                     help="peer: fused permute -> peer-store exchange (CUDA IPC over NVLink); copy: device copies / NCCL")
     return ap.parse_args()
@@ -151,81 +160,102 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- reference arm
-def cpu_oracle_sample(cfgd, mode, seconds_budget=12.0, ffn_rows=64, ranks=None):
-    """Time the CPU oracle (as it stands, single thread) on a bounded sample of the
-    workload: routing of all tokens of `ranks` ranks plus the expert FFN of `ffn_rows`
-    kept tokens, extrapolated to tokens/s of the whole layer."""
+def _oracle_step_fn(cfgd, mode, Ts, seed=0):
+    """One step of the CPU oracle (oracle/, as it stands: the serial fp64 functions, one
+    thread) on a bounded sample of the workload: the whole layer -- router logits (Eq. 1),
+    bi-level (or flat) routing with capacities (Eq. 3, R5-R8), the expert FFN of every
+    kept token and the gate-weighted output (Eq. 3), the aux loss (Eq. 4) -- on a mini-batch
+    of Ts tokens per rank with the configuration's n, m, e, d, d_ff and cf.  Inputs are
+    generated outside the timed call.  Returns (fn, tokens per step)."""
     import numpy as np
     import oracle
     import synth
-    n, m, e, T, d, d_ff, cf = (cfgd[k] for k in ("n", "m", "e", "T", "d", "d_ff", "cf"))
+    n, m, e, d, d_ff, cf = (cfgd[k] for k in ("n", "m", "e", "d", "d_ff", "cf"))
     flat = mode == "flat"
     G = n * m
-    cfg = oracle.Config(n, m, e, T, cf, flat=flat, alpha=0.01 if flat else 0.005)
+    cfg = oracle.Config(n, m, e, Ts, cf, flat=flat, alpha=0.01 if flat else 0.005)
     KW = cfg.logit_width
-    x = synth.tokens(G, T, d, seed=0, dtype=cfgd["dtype"])
-    W = synth.router_weights(KW, d, seed=0)
-    W1, b1, W2, b2 = synth.expert_weights(G * e, d, d_ff, seed=0, dtype=cfgd["dtype"], bias=False)
+    x = synth.tokens(G, Ts, d, seed=seed, dtype=cfgd["dtype"])
+    W = synth.router_weights(KW, d, seed=seed)
+    W1, b1, W2, b2 = synth.expert_weights(G * e, d, d_ff, seed=seed, dtype=cfgd["dtype"], bias=False)
+
+    def fn():
+        lg = oracle.logits(x.reshape(-1, d), W).reshape(G, Ts, KW)
+        r = oracle.route(cfg, lg)
+        return oracle.out_rows(cfg, r, x, W1, b1, W2, b2)
+    return fn, G * Ts
+
+
+def _oracle_sample_size(cfgd, mode, per_step_s):
+    """Tokens per rank of the oracle's mini-batch so that one step takes ~per_step_s: the
+    per-token cost is calibrated on an 8-token-per-rank step (the cost is linear in the
+    tokens: logits, routing and the FFN are per token)."""
+    fn, tok = _oracle_step_fn(cfgd, mode, 8)
     t0 = time.perf_counter()
-    lg = oracle.logits(x.reshape(-1, d), W).reshape(G, T, KW)
-    r = oracle.route(cfg, lg)
-    t_route = time.perf_counter() - t0
-    kept = np.flatnonzero(r.keep.reshape(-1))
-    rows = kept[:: max(1, kept.size // ffn_rows)][:ffn_rows]
-    t1 = time.perf_counter()
-    oracle.out_rows(cfg, r, x, W1, b1, W2, b2, rows=rows)
-    t_ffn = time.perf_counter() - t1
-    t_total = t_route + t_ffn * kept.size / max(1, rows.size)
-    return {"value": G * T / t_total, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"router logits + routing of all {G}x{T} tokens ({t_route:.2f} s) + expert FFN of "
-                      f"{rows.size} of {kept.size} kept tokens ({t_ffn:.2f} s), FFN extrapolated linearly"}
+    fn()
+    per_tok = (time.perf_counter() - t0) / tok
+    G = cfgd["n"] * cfgd["m"]
+    return max(1, min(cfgd["T"], int(per_step_s / (per_tok * G)))), per_tok
+
+
+def cpu_oracle_sample(cfgd, mode, seconds_budget=15.0):
+    """cpu_baseline of our arm (rank 0, N = 1): the oracle as it stands timed on the host
+    cores over a bounded sample -- a few whole-layer steps on a mini-batch (see
+    _oracle_step_fn), ~seconds_budget of CPU work; value = tokens per second measured, no
+    extrapolation."""
+    Ts, _ = _oracle_sample_size(cfgd, mode, seconds_budget / 3)
+    fn, tok = _oracle_step_fn(cfgd, mode, Ts, seed=1)
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < 3 and time.perf_counter() - t_all < seconds_budget:
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": tok / t, "unit": "tokens/s", "cores": 1, "nproc": os.cpu_count(), "kind": "oracle",
+            "sample": f"{len(times)} whole-layer oracle steps (logits + routing + FFN of every kept token + loss) "
+                      f"on a mini-batch of {Ts} tokens/rank x {cfgd['n'] * cfgd['m']} ranks with the workload's "
+                      f"n, m, e, d, d_ff, cf; median {t:.2f} s per step; single thread (serial fp64 oracle)"}
 
 
 def run_reference(args):
+    """The reference arm: for this tier the CPU oracle (oracle/, as it stands) on the box's
+    host cores -- rank 0 only.  Each step = the whole oracle layer on a bounded mini-batch
+    of the same workload (_oracle_step_fn), sized so --warmup + --steps steps take about
+    90 s; the measured median step time gives the tokens/s (no extrapolation)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import numpy as np
-    import oracle
-    import synth
     cfgd = CONFIGS[args.config]
-    n, m, e, T, d, d_ff, cf = (cfgd[k] for k in ("n", "m", "e", "T", "d", "d_ff", "cf"))
-    G = n * m
-    cfg = oracle.Config(n, m, e, T, cf, alpha=0.005)
-    KW = cfg.logit_width
-    x = synth.tokens(G, T, d, seed=0, dtype=cfgd["dtype"])
-    W = synth.router_weights(KW, d, seed=0)
-    W1, b1, W2, b2 = synth.expert_weights(G * e, d, d_ff, seed=0, dtype=cfgd["dtype"], bias=False)
-    # one step = the oracle on a bounded sample: all ranks' logits + routing of rank 0's
-    # batch is not separable (level 2 needs every source), so a step routes the whole
-    # layer once per `route_every` steps and evaluates FFN rows for the rest.
-    ffn_rows = 4
-    lg = oracle.logits(x.reshape(-1, d), W).reshape(G, T, KW)
+    mode = "bilevel" if args.mode in ("both", "bilevel") else "flat"
+    n_steps = args.warmup + args.steps
+    Ts, per_tok = _oracle_sample_size(cfgd, mode, 90.0 / max(1, n_steps))
+    fn, tok = _oracle_step_fn(cfgd, mode, Ts)
     times = []
-    rsel = None
-    for it in range(args.warmup + args.steps):
+    t_wall = time.perf_counter()
+    for it in range(n_steps):
         t0 = time.perf_counter()
-        if it == 0 or it % 10 == 0:
-            r = oracle.route(cfg, lg)
-            kept = np.flatnonzero(r.keep.reshape(-1))
-            t_route = time.perf_counter() - t0
-        rsel = kept[(it * 997) % kept.size: (it * 997) % kept.size + ffn_rows]
-        t1 = time.perf_counter()
-        oracle.out_rows(cfg, r, x, W1, b1, W2, b2, rows=rsel)
-        t_ffn = time.perf_counter() - t1
-        est = t_route + t_ffn * kept.size / max(1, rsel.size)
+        fn()
         if it >= args.warmup:
-            times.append(est)
-    t = statistics.mean(times)
-    value = G * T / t
+            times.append(time.perf_counter() - t0)
+    wall = time.perf_counter() - t_wall
+    t = statistics.median(times)
+    value = tok / t
+    G = cfgd["n"] * cfgd["m"]
+    q = statistics.quantiles(times, n=10) if len(times) >= 2 else [t] * 9
+    sample = (f"per step: the whole oracle layer (router logits, routing with capacities, FFN of every kept token, "
+              f"gate-weighted output, aux loss) on a mini-batch of {Ts} tokens/rank x {G} ranks with the workload's "
+              f"n, m, e, d, d_ff, cf (the full layer has T={cfgd['T']}/rank); single thread")
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config}: one SMILE layer fwd, {G} ranks 2x4, T={T}/rank, d={d}, "
-                                   f"d_ff={d_ff}, cf={cf}", "l2": "n/a (CPU)"},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-                             "sample": f"per step: routing of all {G}x{T} tokens (re-run every 10 steps) + "
-                                       f"expert FFN of {ffn_rows} kept tokens, FFN extrapolated to all kept"},
+            "config": {"workload": f"{args.config}: one SMILE {mode} layer fwd, {G} ranks {cfgd['n']}x{cfgd['m']}, "
+                                   f"e={cfgd['e']}, d={cfgd['d']}, d_ff={cfgd['d_ff']}, cf={cfgd['cf']}; CPU oracle "
+                                   f"mini-batch of {Ts} tokens/rank per step", "l2": "n/a (CPU)"},
+            "step_ms": {"median": t * 1e3, "p10": q[0] * 1e3, "p90": q[-1] * 1e3, "mean": statistics.mean(times) * 1e3},
+            "wall_s": wall,
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "nproc": os.cpu_count(), "kind": "oracle",
+                             "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -305,69 +335,11 @@ def step(L, inp, ev=None):
         rec(7)
 
 
-def stage_front(L, inp):
-    """a1-a8 of one (chunk) layer: gate, level-1 permute + exchange, level-2 gate, level-2
-    permute + exchange (flat: gate, permute + exchange)."""
-    w, A = L._view, Addr
-    if inp.get("fused_gate"):
-        L.gate_dispatch_inter(inp["x"], inp["w_router"], w.route, w.stats, A(w.counts1), A(w.send1),
-                              send_meta=A(w.meta1) if not L.flat else None)
-    else:
-        L.gate_inter(inp["x"], w.route, w.stats, A(w.counts1), w_router=inp["w_router"])
-        L.dispatch(1, inp["x"], A(w.send1), route=w.route, send_meta=A(w.meta1) if not L.flat else None)
-    if not L.flat:
-        L.all2all_inter(0, A(w.send1), A(w.recv1), A(w.meta1), A(w.rmeta1), A(w.counts1))
-        L.gate_intra(A(w.rmeta1), A(w.slot2), A(w.counts2))
-        L.dispatch(2, A(w.recv1), A(w.send2), recv_meta=A(w.rmeta1), slot2=A(w.slot2))
-        L.all2all_intra(0, A(w.send2), A(w.recv2), A(w.counts2), A(w.rcounts), A(w.counts2))
-    else:
-        L.all2all(0, 0, A(w.send1), A(w.recv1), A(w.counts1), A(w.rcounts), A(w.counts1))
-
-
-def stage_ffn(L, inp):
-    w, A = L._view, Addr
-    X = A(w.recv2) if not L.flat else A(w.recv1)
-    L.expert_ffn(X, A(w.rcounts), inp["W1t"], inp["b1"], inp["W2t"], inp["b2"], A(w.H), A(w.Y))
-
-
-def stage_back(L, inp):
-    """a10-a14: reverse exchanges, un-permute, combine, aux loss."""
-    w, A = L._view, Addr
-    if not L.flat:
-        L.all2all_intra(1, A(w.Y), A(w.ret2), fwd_counts=A(w.counts2))
-        L.combine(2, A(w.ret2), A(w.ret1), recv_meta=A(w.rmeta1), slot2=A(w.slot2))
-        L.all2all_inter(1, A(w.ret1), A(w.back1), fwd_counts=A(w.counts1))
-        L.combine(1, A(w.back1), inp["out"], route=w.route)
-        L.aux_loss(w.stats, inp["loss"], 0.005, 0.005)
-    else:
-        L.all2all(0, 1, A(w.Y), A(w.back1), fwd_counts=A(w.counts1))
-        L.combine(1, A(w.back1), inp["out"], route=w.route)
-        L.aux_loss(w.stats, inp["loss"], 0.01, 0.0)
-
-
-def step_pipelined(Ls, inps, s2, evf, eve):
-    """SURVEY §8(f) row 2 / P:L391-405: the batch split into c chunks (independent
-    micro-batches with their own capacities), software-pipelined on two streams: the
-    expert FFN of chunk k (stream 2) overlaps the gate + permutes + exchanges of chunk k+1
-    and the return path of chunk k-1 (stream 1)."""
-    import torch
-    s1 = torch.cuda.current_stream()
-    c = len(Ls)
-    stage_front(Ls[0], inps[0])
-    evf[0].record(s1)
-    for k in range(c):
-        s2.wait_event(evf[k])
-        with torch.cuda.stream(s2):
-            stage_ffn(Ls[k], inps[k])
-        eve[k].record(s2)
-        if k + 1 < c:
-            stage_front(Ls[k + 1], inps[k + 1])
-            evf[k + 1].record(s1)
-        s1.wait_event(eve[k])
-        stage_back(Ls[k], inps[k])
-
-
 def run_pipelined(args):
+    """SURVEY 8(f) row 2 / P:L391-405: smile_forward_chunked -- the layer over c chunks of
+    T/c tokens per rank (each chunk its own capacities), the FFN of chunk k on a second
+    stream overlapping the front of chunk k+1 and the back of chunk k-1 -- timed beside
+    the unchunked layer (smile_forward) in the same run, same inputs."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -388,33 +360,54 @@ def run_pipelined(args):
     tdt = torch.bfloat16 if cfgd["dtype"] == "bf16" else torch.float32
     modes = ["bilevel", "flat"] if args.mode == "both" else [args.mode]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    out_modes = {}
-    for mode in modes:
-        Ls, inps = [], []
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(7)
-        KW = None
-        for k in range(c):
-            nid = None
-            if world > 1:
-                buf = torch.zeros(128, dtype=torch.uint8, device=dev)
-                if rank == 0:
-                    buf.copy_(torch.frombuffer(bytearray(smb.unique_id()), dtype=torch.uint8))
-                dist.broadcast(buf, 0)
-                nid = bytes(buf.cpu().numpy().tobytes())
-            ck = dict(cfgd, T=Tc)
-            L = make_layer(ck, mode, world, rank, local, args.ffn, nid)
 
-            def allgather(b):
-                t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(dev)
-                outs = [torch.empty_like(t) for _ in range(world)]
-                dist.all_gather(outs, t)
-                return b"".join(bytes(o.cpu().numpy().tobytes()) for o in outs)
-            L.enable_peer_exchange(allgather if world > 1 else None)
-            if dist:
-                dist.barrier()
-            Ls.append(L)
-            KW = L.KW
+    def new_layer(ck, mode):
+        nid = None
+        if world > 1:
+            buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if rank == 0:
+                buf.copy_(torch.frombuffer(bytearray(smb.unique_id()), dtype=torch.uint8))
+            dist.broadcast(buf, 0)
+            nid = bytes(buf.cpu().numpy().tobytes())
+        L = make_layer(ck, mode, world, rank, local, args.ffn, nid)
+
+        def allgather(b):
+            t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(dev)
+            outs = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(outs, t)
+            return b"".join(bytes(o.cpu().numpy().tobytes()) for o in outs)
+        L.enable_peer_exchange(allgather if world > 1 else None)
+        if dist:
+            dist.barrier()
+        return L
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        t0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        t1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.zero_()
+            t0[k].record()
+            fn()
+            t1[k].record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([statistics.median(t0[k].elapsed_time(t1[k]) for k in range(args.steps))],
+                          dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return ms.item()
+
+    out_modes, base_modes = {}, {}
+    for mode in modes:
+        Ls = [new_layer(dict(cfgd, T=Tc), mode) for _ in range(c)]
+        Lfull = new_layer(cfgd, mode)
+        KW = Ls[0].KW
+        gen = torch.Generator(device=dev)
         gen.manual_seed(7)
         w_router = (torch.rand(KW, d, generator=gen, device=dev) * 2 - 1) / math.sqrt(d)
         gen.manual_seed(2000 + rank)
@@ -424,48 +417,34 @@ def run_pipelined(args):
         b2 = torch.zeros(V * e, d, device=dev)
         gen.manual_seed(1000 + rank)
         x = torch.randn(V, T, d, generator=gen, device=dev, dtype=torch.float32).to(tdt)
-        for k in range(c):
-            xk = x[:, k * Tc:(k + 1) * Tc].contiguous()
-            inps.append(dict(x=xk, w_router=w_router, W1t=W1t, W2t=W2t, b1=b1, b2=b2, out=torch.empty_like(xk),
-                             loss=torch.empty(V, dtype=torch.float64, device=dev), fused_gate=args.fused_gate))
+        xs = [x[:, k * Tc:(k + 1) * Tc].contiguous() for k in range(c)]
+        outs = [torch.empty_like(xk) for xk in xs]
+        losses = [torch.empty(V, dtype=torch.float64, device=dev) for _ in range(c)]
+        out_full = torch.empty_like(x)
+        loss_full = torch.empty(V, dtype=torch.float64, device=dev)
         s2 = torch.cuda.Stream()
-        evf = [torch.cuda.Event() for _ in range(c)]
-        eve = [torch.cuda.Event() for _ in range(c)]
-        for _ in range(args.warmup):
-            step_pipelined(Ls, inps, s2, evf, eve)
-        torch.cuda.synchronize()
-        if any(L.get_error() for L in Ls):
+        a_, b_ = (0.005, 0.005) if mode == "bilevel" else (0.01, 0.0)
+        out_modes[mode] = timed(lambda: smb.forward_chunked(Ls, xs, W1t, b1, W2t, b2, outs, losses, w_router=w_router,
+                                                            alpha=a_, beta=b_, stream2=s2))
+        base_modes[mode] = timed(lambda: Lfull.forward(x, W1t, b1, W2t, b2, out_full, loss_full, w_router=w_router,
+                                                       alpha=a_, beta=b_))
+        if any(L.get_error() for L in Ls + [Lfull]):
             raise SystemExit("device error")
-        t0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        t1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         if dist:
             dist.barrier()
-        torch.cuda.synchronize()
-        for k in range(args.steps):
-            flush.zero_()
-            t0[k].record()
-            step_pipelined(Ls, inps, s2, evf, eve)
-            t1[k].record()
-        torch.cuda.synchronize()
-        ms = torch.tensor([statistics.mean(t0[k].elapsed_time(t1[k]) for k in range(args.steps))], dtype=torch.float64,
-                          device=dev)
-        if dist:
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        out_modes[mode] = ms.item()
-        if dist:
-            dist.barrier()
-        for L in Ls:
+        for L in Ls + [Lfull]:
             L.close()
     if rank == 0:
         m0 = modes[0]
         line = {"metric": METRIC, "value": G * T / (out_modes[m0] / 1e3), "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": out_modes[m0], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if cfgd["dtype"] == "bf16" else "f32",
-                "data": "synthetic", "config": {"workload": f"{args.config}: {m0} layer fwd, {c} pipelined chunks of "
-                                                            f"T={Tc}/rank on 2 streams (SURVEY 8(f) row 2)",
-                                                 "chunks": c, "ffn_max_ctas": os.environ.get("SMILE_FFN_MAX_CTAS"),
-                                                 "exchange": "peer"},
-                "modes_ms": out_modes}
+                "data": "synthetic", "config": {"workload": f"{args.config}: {m0} layer fwd through smile_forward_chunked, "
+                                                            f"{c} pipelined chunks of T={Tc}/rank on 2 streams (SURVEY 8(f) row 2)",
+                                                 "chunks": c, "exchange": "peer", "timing": "median over steps",
+                                                 "l2": "flushed (256 MiB write) before every timed step"},
+                "chunked_ms": out_modes, "unchunked_ms": base_modes,
+                "chunked_over_unchunked": {k: base_modes[k] / out_modes[k] for k in out_modes}}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -578,6 +557,13 @@ def run_ours(args):
         nccl_id = bytes(buf.cpu().numpy().tobytes())
 
     modes = ["bilevel", "flat"] if args.mode == "both" else [args.mode]
+    fabric = None
+    if args.fabric:
+        if world != 1:
+            raise SystemExit("--fabric emulates every rank's NIC on one GPU: N = 1 only")
+        bw, lat = (float(v) for v in args.fabric.split(","))
+        fabric = {"inter_gbps_per_rank": bw, "inter_latency_us_per_message": lat, "emulated": True}
+        args.exchange = "copy"
     if args.fused_gate:
         # smile_gate_dispatch_inter is the 128-token tensor-core gate (it refuses the
         # default swapped 256-token tile with SMILE_ENOTSUP): select that tile
@@ -600,6 +586,8 @@ def run_ours(args):
             dist.broadcast(buf, 0)
             nccl_id = bytes(buf.cpu().numpy().tobytes())
         L = make_layer(cfgd, mode, world, rank, local, args.ffn, nccl_id)
+        if fabric:
+            L.set_fabric(fabric["inter_gbps_per_rank"], fabric["inter_latency_us_per_message"])
         if args.exchange == "peer":
             def allgather(b):
                 t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(dev)
@@ -664,7 +652,10 @@ def run_ours(args):
             dist.barrier()
         ph = [[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(nph)] for k in range(args.steps)]
         step_ms = [sum(p) for p in ph]
-        eager_ms = sum(step_ms) / args.steps
+        eager_ms = statistics.median(step_ms)            # median, with p10 / p90 reported
+        q = statistics.quantiles(step_ms, n=10) if len(step_ms) >= 2 else [eager_ms] * 9
+        step_stats = {"median": eager_ms, "p10": q[0], "p90": q[-1], "mean": statistics.mean(step_ms),
+                      "min": min(step_ms), "max": max(step_ms)}
         graph_ms = None
         if args.graph and world == 1:
             # the same step captured once as a CUDA graph and replayed (the libsmile calls
@@ -688,7 +679,7 @@ def run_ours(args):
                 cg.replay()
                 g1[k].record()
             torch.cuda.synchronize()
-            graph_ms = statistics.mean(g0[k].elapsed_time(g1[k]) for k in range(args.steps))
+            graph_ms = statistics.median(g0[k].elapsed_time(g1[k]) for k in range(args.steps))
             if L.get_error():
                 raise SystemExit("device error in graph replay")
             del cg
@@ -778,6 +769,7 @@ def run_ours(args):
         res = dict(L=L, inp=inp, ms=ms, ffn_tc=ffn_tc, rank_ms=rank_ms, phase_ms=phase_ms, rows=rows, kept=kept, ffn_ms=ffn_ms,
                    t_beg=t_beg, t_end=t_end,
                    tokens=G * T, launches=launched, hbm_bytes=hbm, train=train, eager_ms=eager_ms, graph_ms=graph_ms,
+                   step_stats=step_stats,
                    nvl_bytes=nvl)
         if train:
             res["hbm_bytes"] = {}
@@ -862,10 +854,17 @@ def run_ours(args):
                                f"e={e}/rank, T={T}/rank, d={d}, d_ff={d_ff}, cf={cfgd['cf']}, fused router; "
                                f"{V} ranks per GPU; exchange={args.exchange}", "ranks_per_gpu": V, "mode": modes[0],
                    "exchange": args.exchange,
-                   "l2": "flushed (256 MiB write) before every timed step, outside its events"},
-        "phase_ms": main["phase_ms"], "phase_ms_note": "per phase: max over ranks of the mean over steps",
+                   "fabric": fabric and dict(fabric, note="IN-BOX EMULATION (smile_set_fabric): cross-node transfers "
+                                             "of the COPY exchange go through per-rank emulated NICs -- "
+                                             "latency per message + bytes / bandwidth of wall time each; not a "
+                                             "real network"),
+                   "l2": "flushed (256 MiB write) before every timed step, outside its events",
+                   "timing": "CUDA events per phase on the launching stream; value from the median step"},
+        "phase_ms": main["phase_ms"], "phase_ms_note": "per phase: max over ranks of the mean over steps (events on the launching stream)",
         "rank_ms_per_step": main["rank_ms"], "kept_tokens": main["kept"],
         "cuda_graph": main["graph_ms"] is not None, "eager_ms_per_step": main["eager_ms"],
+        "step_ms_stats": main["step_stats"],
+        "step_ms_note": "rank-0 process, eager steps; ms_per_step = max over ranks of each rank's median",
         "roofline": roof,
         "hbm_phases": hbm_phases(main, peaks),
         "nvlink": None if main.get("train") else nvlink_levels(main, world, modes[0], args.exchange),

@@ -177,6 +177,28 @@ smile_status smile_get_error(smile_ctx ctx, void *stream);
  * (Scattered 64-byte NVLink stores from the epilogue measured slower than the combine's
  * loads, hence the split.)  SMILE_RET_DIRECT=0 keeps Y + smile_combine(2) for all rows. */
 typedef enum { SMILE_XCHG_COPY = 0, SMILE_XCHG_PEER = 1 } smile_xchg;
+
+/* ---------------- emulated heterogeneous fabric ----------------
+ * AN IN-BOX EMULATION, NOT A MEASUREMENT OF A REAL NETWORK.  The paper's premise is a
+ * hierarchical interconnect: fast links inside a node, a slower, latency-bound network
+ * between nodes, where the naive All2All issues O(mn) point-to-point messages per rank and
+ * bi-level routing O(m + n) (tab:performance_table P:L325).  One B200
+ * box has a uniform NVSwitch fabric, so the two levels cost the same per byte there.  With
+ * a fabric set, every transfer of the COPY exchange between two ranks of DIFFERENT groups
+ * (node s = rank / m) -- in both layers, every level, both directions -- is carried by an
+ * emulated NIC of the sending rank: the NIC sends its cross-node messages one after
+ * another, each taking latency_us + bytes / inter_gbps of wall time (bytes = the valid
+ * rows of the message; every (sender, receiver) pair is one message, as in the NCCL loop
+ * of P:L64-76), all ranks' NICs concurrently.  Same-node transfers stay device copies.
+ * Data movement only: results are bit-identical to the plain COPY exchange.
+ * Needs nprocs == 1 (every rank on this GPU) and the COPY exchange; inter_gbps <= 0
+ * disables it.  The per-NIC copy runs on one CTA, so bandwidths above what one SM moves
+ * (~100 GB/s) are not emulated faithfully. */
+typedef struct {
+    double inter_gbps;        /* bytes per second / 1e9 of one rank's emulated NIC */
+    double inter_latency_us;  /* fixed cost per cross-node message */
+} smile_fabric;
+smile_status smile_set_fabric(smile_ctx ctx, const smile_fabric *fabric);
 /* The 72-byte IPC description of workspace `ws` (64-byte cudaIpcMemHandle of the
  * allocation containing it + the 8-byte offset of ws inside it), to be all-gathered by
  * the caller. */
@@ -442,6 +464,21 @@ smile_status smile_forward_ws(smile_ctx ctx, void *ws, smile_ws_view *view);
  * T == 0: returns SMILE_OK without touching any buffer (x, out may be NULL; the loss,
  * which divides by T, is not written). */
 smile_status smile_forward(smile_ctx ctx, const smile_layer_io *io, void *stream);
+
+/* the paper's "pipe_overlapping" appendix: the layer
+ * over c micro-batches ("chunks") of T/c tokens per rank, software-pipelined on two
+ * streams: the expert FFN of chunk k (stream2) overlaps the gate + permutes + exchanges
+ * of chunk k+1 and the return path of chunk k-1 (stream).  Each chunk is an independent
+ * layer with its own capacities ceil(cf * (T/c) / K) (R5 applied to the chunk), so it
+ * computes exactly what smile_forward computes for that chunk alone.
+ * ctxs[k]: nchunks DISTINCT contexts created with identical shapes (T = tokens per chunk);
+ * ios[k]: chunk k's layer io (x, out [V, T/c, d] contiguous, its own workspace -- the
+ * registered one in peer mode -- weights and loss [V]); inference only (train == 0).
+ * Enqueues on both streams (stream2 first waits for the work already on stream) and
+ * returns; the result is complete when `stream` reaches the end of the enqueued work.
+ * nchunks <= 64. */
+smile_status smile_forward_chunked(smile_ctx const *ctxs, const smile_layer_io *ios, int32_t nchunks, void *stream,
+                                   void *stream2);
 
 /* The whole backward after a forward with io->train set, in reverse order of the forward:
  * combine_bwd, exchange(1, gradient rows), dispatch_grad, exchange(2), expert_ffn_bwd,

@@ -5,4 +5,4 @@ The product is the C-ABI library ``libsmile.so`` (``include/smile.h``) built fro
 only -- every step of the layer runs in the library's CUDA kernels / NCCL calls).
 There is no CPU fallback: importing the binding without the built library raises.
 """
-from .smile import SmileLayer, SmileError, lib, plan, group  # noqa: F401
+from .smile import SmileLayer, SmileError, lib, plan, group, capacity, forward_chunked  # noqa: F401

@@ -306,12 +306,15 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
         }
     }
     c->nblk1 = (int)((shape->T + c->TB1 - 1) / c->TB1);
+    c->nch1 = (int)((shape->T + 31) / 32);
     const int64_t items2 = (int64_t)shape->n * z.C1;
     c->nblk2 = shape->mode == SMILE_BILEVEL ? (int)((items2 + kRank2Items - 1) / kRank2Items) : 0;
-    const size_t nb1 = (size_t)V * (c->nblk1 > 0 ? c->nblk1 : 1);
+    const size_t nb1 = (size_t)V * (c->nch1 > 0 ? c->nch1 : 1);     // per-chunk tables
     const size_t nb2 = (size_t)V * (c->nblk2 > 0 ? c->nblk2 : 1);
     CUDA_TRY(cudaMalloc(&c->d_err, sizeof(int)));
     CUDA_TRY(cudaMemset(c->d_err, 0, sizeof(int)));
+    CUDA_TRY(cudaMalloc(&c->gate_sync, sizeof(int) * (2 + V)));
+    CUDA_TRY(cudaMemset(c->gate_sync, 0, sizeof(int) * (2 + V)));
     CUDA_TRY(cudaMalloc(&c->blk_hist1, nb1 * z.K1 * 4));
     CUDA_TRY(cudaMalloc(&c->blk_off1, nb1 * z.K1 * 4));
     CUDA_TRY(cudaMalloc(&c->blk_hist2a, nb1 * z.K2 * 4));
@@ -320,6 +323,8 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
     CUDA_TRY(cudaMalloc(&c->blk_off2, nb2 * z.K2 * 4));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_chunk_front, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_chunk_ffn, cudaEventDisableTiming));
     for (int i = 0; i < 2; ++i) {
         CUDA_TRY(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&c->ev_comp[i], cudaEventDisableTiming));
@@ -368,11 +373,14 @@ extern "C" smile_status smile_destroy(smile_ctx c) {
     if (c->intra) ncclCommDestroy(c->intra);
     if (c->world) ncclCommDestroy(c->world);
     cudaFree(c->d_err);
+    cudaFree(c->gate_sync);
     cudaFree(c->wsplit);
     cudaFree(c->colsum_ws);
     cudaFree(c->lb_flag); cudaFree(c->lb_agg); cudaFree(c->lb_inc);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+    if (c->ev_chunk_front) cudaEventDestroy(c->ev_chunk_front);
+    if (c->ev_chunk_ffn) cudaEventDestroy(c->ev_chunk_ffn);
     for (int i = 0; i < 2; ++i) {
         if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
         if (c->ev_comp[i]) cudaEventDestroy(c->ev_comp[i]);
@@ -430,6 +438,7 @@ extern "C" smile_status smile_register_workspace(smile_ctx c, void *ws, const ui
     const int P = c->shape.nprocs, me = c->shape.proc;
     if (P > kMaxProcs) return SMILE_ENOTSUP;
     if (xchg == SMILE_XCHG_PEER && P > 1 && !handles) return SMILE_EINVAL;
+    if (xchg == SMILE_XCHG_PEER && c->fabric.inter_gbps > 0.0) return SMILE_ENOTSUP;   // fabric: COPY only
     cudaSetDevice(c->shape.device);
     c->reg_ws = ws;
     c->xchg = xchg;
@@ -540,19 +549,20 @@ extern "C" smile_status smile_gate_inter(smile_ctx c, const void *x, const float
     a.route = *route;
     a.blk_hist1 = c->blk_hist1; a.blk_hist2a = c->blk_hist2a; a.blk_psum = c->blk_psum;
     a.err = c->d_err; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
-    a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1;
+    a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1; a.nch = c->nch1;
     a.flat = c->shape.mode == SMILE_FLAT; a.bf16 = c->shape.dtype == SMILE_BF16;
+    Scan1Args s{};
+    s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
+    s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nch1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
+    s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T; s.peer = peer_of(c);
+    bool scanned = false;                    // the ranged tensor-core gate runs the scan itself
     if (!logits && c->wsplit) {
-        const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, S(stream));
+        const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, &s, c->gate_sync, &scanned, S(stream));
         if (e != cudaSuccess) return SMILE_ECUDA;
     } else {
         launch_gate1(a, S(stream));
     }
-    Scan1Args s{};
-    s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
-    s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
-    s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T; s.peer = peer_of(c);
-    launch_scan1(s, S(stream));
+    if (!scanned) launch_scan1(s, S(stream));
     return post_launch();
 }
 
@@ -577,22 +587,24 @@ extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, co
     a.route = *route;
     a.blk_hist1 = c->blk_hist1; a.blk_hist2a = c->blk_hist2a; a.blk_psum = c->blk_psum;
     a.err = c->d_err; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
-    a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1;
+    a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1; a.nch = c->nch1;
     a.flat = !bi; a.bf16 = c->shape.dtype == SMILE_BF16;
     a.fuse_dispatch = 1; a.send = send_rows; a.meta = bi ? send_meta : nullptr; a.rowbytes = rb; a.C1 = c->sz.C1;
     a.peer = peer_of(c); a.lb_flag = c->lb_flag; a.lb_agg = c->lb_agg; a.lb_inc = c->lb_inc;
-    const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, S(stream));
+    bool scanned = false;
+    const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, nullptr, nullptr, &scanned, S(stream));
     if (e != cudaSuccess) return SMILE_ECUDA;
     Scan1Args s{};
     s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
-    s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
+    s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nch1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
     s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T; s.peer = peer_of(c); s.lb_flag = c->lb_flag;
+    s.nlb = c->nblk1;
     launch_scan1(s, S(stream));
     Dispatch1Args d{};
     d.x = x; d.route = *route; d.blk_off1 = c->blk_off1; d.blk_hist1 = c->blk_hist1;
     d.send = send_rows; d.meta = bi ? send_meta : nullptr;
     d.V = c->sz.V; d.T = c->shape.T; d.rowbytes = rb; d.K1 = c->sz.K1; d.C1 = c->sz.C1;
-    d.TB = c->TB1; d.nblk = c->nblk1; d.peer = peer_of(c);
+    d.TB = 32; d.nblk = c->nch1; d.peer = peer_of(c);
     launch_meta_fill(d, S(stream));
     return post_launch();
 }
@@ -614,7 +626,7 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
         a.x = rows_in; a.route = *route; a.blk_off1 = c->blk_off1; a.blk_hist1 = c->blk_hist1;
         a.send = send_rows; a.meta = bi ? send_meta : nullptr;
         a.V = c->sz.V; a.T = c->shape.T; a.rowbytes = rb; a.K1 = c->sz.K1; a.C1 = c->sz.C1;
-        a.TB = c->TB1; a.nblk = c->nblk1; a.peer = peer_of(c);
+        a.TB = 32; a.nblk = c->nch1; a.peer = peer_of(c);      // chunk offsets of the scan
         // every rank in this process: the whole level-1 return fuses into GEMM 2, so the
         // zero rows of level-1-dropped tokens are written here and combine(1) is skipped
         c->l1_zeroed = out_direct_enabled(c) && c->sz.V == c->sz.G;
@@ -692,7 +704,14 @@ extern "C" smile_status smile_all2all(smile_ctx c, int32_t level, int32_t revers
         a.cnt = fwd_counts; a.member_local = L.d_member_local; a.mypos = L.d_mypos;
         a.V = V; a.P = P; a.nsub = L.nsub; a.Csub = L.Csub; a.rowbytes = rb; a.ipp = L.ints_per_peer;
         a.rev = reverse ? 1 : 0;
+        const bool fab = c->fabric.inter_gbps > 0.0 && c->shape.nprocs == 1;
+        if (fab) {
+            a.fabric = 1; a.rank0 = c->sz.rank0; a.m = c->shape.m;
+            a.ns_per_byte = 1.0 / c->fabric.inter_gbps;          // GB/s = bytes per ns
+            a.latency_ns = c->fabric.inter_latency_us * 1e3;
+        }
         launch_exchange_copy(a, st);
+        if (fab) launch_fabric_copy(a, st);
         if (cudaGetLastError() != cudaSuccess) return SMILE_ECUDA;
     }
     if (c->shape.nprocs == 1) return SMILE_OK;
@@ -969,28 +988,28 @@ extern "C" smile_status smile_forward_ws(smile_ctx c, void *ws, smile_ws_view *v
 }
 
 
+extern "C" smile_status smile_set_fabric(smile_ctx c, const smile_fabric *f) {
+    if (!c || !f) return SMILE_EINVAL;
+    if (!(f->inter_gbps > 0.0)) {                       // disable
+        c->fabric = smile_fabric{};
+        return SMILE_OK;
+    }
+    if (!(f->inter_latency_us >= 0.0)) return SMILE_EINVAL;
+    if (c->shape.nprocs != 1) return SMILE_ENOTSUP;     // an emulation of every rank on this GPU
+    if (c->xchg == SMILE_XCHG_PEER) return SMILE_ENOTSUP;  // the emulated NICs carry the COPY exchange
+    c->fabric = *f;
+    return SMILE_OK;
+}
+
 extern "C" smile_status smile_set_output(smile_ctx c, void *out) {
     if (!c) return SMILE_EINVAL;
     c->out_bound = out;
     return SMILE_OK;
 }
 
-extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, void *stream) {
-    if (!c || !io) return SMILE_EINVAL;
-    if (c->shape.T == 0) return SMILE_OK;                 // no tokens: nothing to compute
-    if (!io->x || !io->out || !io->loss || !io->ws) return SMILE_EINVAL;
-    if (!io->logits && !io->w_router) return SMILE_EINVAL;
-    smile_ws_view w;
-    STEP(smile_forward_ws(c, io->ws, &w));
-    if (c->shape.T == 0) return SMILE_OK;
-    const bool train = io->train != 0;
-    if (c->xchg == SMILE_XCHG_PEER && io->ws != c->reg_ws) return SMILE_ENOTSUP;
-    // inference binds io->out for this call (GEMM 2 may write in-process rows there)
-    struct OutBinding {
-        smile_ctx c; void *prev;
-        ~OutBinding() { c->out_bound = prev; }
-    } bind{c, c->out_bound};
-    c->out_bound = train ? nullptr : io->out;
+// The three stages of one forward (the order of smile_forward; SURVEY 8(f) row 2 runs
+// them of consecutive chunks on two streams): a1-a8, a9, a10-a14.
+static smile_status fwd_front(smile_ctx c, const smile_layer_io *io, const smile_ws_view &w, bool train, void *stream) {
     // gate then level-1 permute as two kernels: measured faster than the fused
     // smile_gate_dispatch_inter (C2: 0.166 vs 0.178 ms; C4: 0.77 vs 0.85 ms) -- the row moves
     // from the gate's epilogue warps reach less bandwidth than the dedicated movers
@@ -1003,19 +1022,109 @@ extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, voi
         STEP(smile_gate_intra(c, w.rmeta1, w.slot2, w.counts2, stream));
         STEP(smile_dispatch(c, 2, w.recv1, nullptr, w.rmeta1, w.slot2, w.send2, nullptr, stream));
         STEP(smile_all2all_intra(c, 0, w.send2, w.recv2, w.counts2, w.rcounts, w.counts2, stream));
-        if (train) STEP(smile_expert_ffn_train(c, w.recv2, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.A1, w.H, w.Y, stream));
-        else STEP(smile_expert_ffn(c, w.recv2, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.H, w.Y, stream));
+    } else {
+        STEP(smile_all2all(c, 0, 0, w.send1, w.recv1, w.counts1, w.rcounts, w.counts1, stream));
+    }
+    return SMILE_OK;
+}
+
+static smile_status fwd_ffn(smile_ctx c, const smile_layer_io *io, const smile_ws_view &w, bool train, void *stream) {
+    void *X = c->shape.mode == SMILE_BILEVEL ? w.recv2 : w.recv1;
+    if (train) return smile_expert_ffn_train(c, X, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.A1, w.H, w.Y, stream);
+    return smile_expert_ffn(c, X, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.H, w.Y, stream);
+}
+
+static smile_status fwd_back(smile_ctx c, const smile_layer_io *io, const smile_ws_view &w, void *stream) {
+    if (c->shape.mode == SMILE_BILEVEL) {
         STEP(smile_all2all_intra(c, 1, w.Y, w.ret2, nullptr, nullptr, w.counts2, stream));
         STEP(smile_combine(c, 2, w.ret2, nullptr, w.rmeta1, w.slot2, w.ret1, stream));
         STEP(smile_all2all_inter(c, 1, w.ret1, w.back1, nullptr, nullptr, w.counts1, stream));
     } else {
-        STEP(smile_all2all(c, 0, 0, w.send1, w.recv1, w.counts1, w.rcounts, w.counts1, stream));
-        if (train) STEP(smile_expert_ffn_train(c, w.recv1, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.A1, w.H, w.Y, stream));
-        else STEP(smile_expert_ffn(c, w.recv1, w.rcounts, io->W1t, io->b1, io->W2t, io->b2, w.H, w.Y, stream));
         STEP(smile_all2all(c, 0, 1, w.Y, w.back1, nullptr, nullptr, w.counts1, stream));
     }
     STEP(smile_combine(c, 1, w.back1, &w.route, nullptr, nullptr, io->out, stream));
     STEP(smile_aux_loss(c, &w.stats, io->alpha, io->beta, io->loss, stream));
+    return SMILE_OK;
+}
+
+static smile_status fwd_check(smile_ctx c, const smile_layer_io *io) {
+    if (!io->x || !io->out || !io->loss || !io->ws) return SMILE_EINVAL;
+    if (!io->logits && !io->w_router) return SMILE_EINVAL;
+    if (c->xchg == SMILE_XCHG_PEER && io->ws != c->reg_ws) return SMILE_ENOTSUP;
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, void *stream) {
+    if (!c || !io) return SMILE_EINVAL;
+    if (c->shape.T == 0) return SMILE_OK;                 // no tokens: nothing to compute
+    STEP(fwd_check(c, io));
+    smile_ws_view w;
+    STEP(smile_forward_ws(c, io->ws, &w));
+    const bool train = io->train != 0;
+    // inference binds io->out for this call (GEMM 2 may write in-process rows there)
+    struct OutBinding {
+        smile_ctx c; void *prev;
+        ~OutBinding() { c->out_bound = prev; }
+    } bind{c, c->out_bound};
+    c->out_bound = train ? nullptr : io->out;
+    STEP(fwd_front(c, io, w, train, stream));
+    STEP(fwd_ffn(c, io, w, train, stream));
+    STEP(fwd_back(c, io, w, stream));
+    return SMILE_OK;
+}
+
+extern "C" smile_status smile_forward_chunked(smile_ctx const *ctxs, const smile_layer_io *ios, int32_t nchunks,
+                                              void *stream, void *stream2) {
+    if (!ctxs || !ios || nchunks < 1 || !stream2 || stream2 == stream) return SMILE_EINVAL;
+    const smile_ctx c0 = ctxs[0];
+    if (!c0) return SMILE_EINVAL;
+    for (int k = 0; k < nchunks; ++k) {
+        const smile_ctx c = ctxs[k];
+        if (!c) return SMILE_EINVAL;
+        for (int j = 0; j < k; ++j)
+            if (ctxs[j] == c) return SMILE_EINVAL;                 // one context (and workspace) per chunk
+        const smile_shape &a = c->shape, &b = c0->shape;
+        if (a.n != b.n || a.m != b.m || a.e != b.e || a.mode != b.mode || a.dtype != b.dtype || a.d != b.d ||
+            a.d_ff != b.d_ff || a.T != b.T || a.cf != b.cf || a.nprocs != b.nprocs || a.proc != b.proc ||
+            a.device != b.device || a.ffn_impl != b.ffn_impl)
+            return SMILE_ESHAPE;
+        if (ios[k].train) return SMILE_ENOTSUP;                     // inference pipelining only
+        if (c->shape.T > 0) STEP(fwd_check(c, &ios[k]));
+    }
+    if (c0->shape.T == 0) return SMILE_OK;
+    cudaSetDevice(c0->shape.device);
+    cudaStream_t s1 = S(stream), s2 = S(stream2);
+    std::vector<smile_ws_view> w(nchunks);
+    for (int k = 0; k < nchunks; ++k) STEP(smile_forward_ws(ctxs[k], ios[k].ws, &w[k]));
+    // every chunk binds its own output for the GEMM 2 -> out fusion, restored on return
+    struct Binds {
+        smile_ctx const *c; int n; void *prev[64];
+        ~Binds() { for (int k = 0; k < n && k < 64; ++k) c[k]->out_bound = prev[k]; }
+    } binds{ctxs, 0, {}};
+    if (nchunks > 64) return SMILE_ENOTSUP;
+    for (int k = 0; k < nchunks; ++k) {
+        binds.prev[k] = ctxs[k]->out_bound;
+        ctxs[k]->out_bound = ios[k].out;
+        binds.n = k + 1;
+    }
+    // stream 2 starts after the work already queued on stream 1
+    CUDA_TRY(cudaEventRecord(ctxs[0]->ev_chunk_front, s1));
+    CUDA_TRY(cudaStreamWaitEvent(s2, ctxs[0]->ev_chunk_front, 0));
+    STEP(fwd_front(ctxs[0], &ios[0], w[0], false, stream));
+    CUDA_TRY(cudaEventRecord(ctxs[0]->ev_chunk_front, s1));
+    for (int k = 0; k < nchunks; ++k) {
+        smile_ctx c = ctxs[k];
+        // the FFN of chunk k (stream 2) overlaps the front of chunk k+1 and the back of k-1
+        CUDA_TRY(cudaStreamWaitEvent(s2, c->ev_chunk_front, 0));
+        STEP(fwd_ffn(c, &ios[k], w[k], false, stream2));
+        CUDA_TRY(cudaEventRecord(c->ev_chunk_ffn, s2));
+        if (k + 1 < nchunks) {
+            STEP(fwd_front(ctxs[k + 1], &ios[k + 1], w[k + 1], false, stream));
+            CUDA_TRY(cudaEventRecord(ctxs[k + 1]->ev_chunk_front, s1));
+        }
+        CUDA_TRY(cudaStreamWaitEvent(s1, c->ev_chunk_ffn, 0));
+        STEP(fwd_back(c, &ios[k], w[k], stream));
+    }
     return SMILE_OK;
 }
 

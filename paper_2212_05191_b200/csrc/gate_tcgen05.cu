@@ -211,7 +211,7 @@ __device__ void fused_dispatch(const GateArgs &a, const GateTok tk, const int *s
 // After the group's logits of one tile are in smem: (optional) logits_out copy, the
 // gate's phases B and C, and (fused) the level-1 permute of the tile.
 template <class Sync>
-__device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int *s_j, int *s_wh, int *s_bh,
+__device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int *s_wh, int *s_bh,
                                             int *s_off, int64_t tok0, int nt, int tile) {
     Sync::sync();
     if (a.logits_out) {
@@ -220,7 +220,8 @@ __device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int 
             a.logits_out[tok0 * a.KW + i] = s_lg[(i / a.KW) * lds + i % a.KW];
         Sync::sync();
     }
-    const GateTok tk = gate_finish<Sync>(a, s_lg, gate_lds(a.KW), s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
+    const int v = tile / a.nblk, blk = tile - v * a.nblk;       // 128-token tiles = 4 chunks
+    const GateTok tk = gate_finish<Sync>(a, s_lg, gate_lds(a.KW), s_wh, s_bh, tok0, nt, (int64_t)v * a.nch + 4 * blk);
     if (a.fuse_dispatch) fused_dispatch<Sync>(a, tk, s_bh, s_off, tok0, nt, tile);
     Sync::sync();
 }
@@ -411,8 +412,8 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
-            if (grp == 0) finish_tile<EpiSync<0>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
-            else finish_tile<EpiSync<1>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
+            if (grp == 0) finish_tile<EpiSync<0>>(a, s_lg, s_wh, s_bh, s_off, tok0, nt, tile);
+            else finish_tile<EpiSync<1>>(a, s_lg, s_wh, s_bh, s_off, tok0, nt, tile);
         }
     }
     __syncthreads();
@@ -424,18 +425,32 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
 
 // ---------------------------------------------------------------------------------
 // Swapped-role tensor-core gate (default for KW <= 40): M = the split router (its
-// 32 * ceil(KW / 10) rows zero-padded to 128 by TMA), N = 256 TOKENS per MMA.  With the
-// tokens on M (gate1_tc_kernel) every tcgen05.mma is 128 x NP x 16 with NP as small as
-// 32, and the MMA count per token -- each costs a near-fixed ~350 cycles there (ncu:
-// the producer waits on stage releases while the MMA thread never waits for data) -- is
-// what bounds the kernel; here one MMA covers 256 tokens.  The accumulator [piece rows x
-// 256 tokens] is transposed by the epilogue: lane r of quadrant q holds piece r % 3 of
-// logit 10 q + r / 3 for 32 tokens; two shuffles sum the pieces in order, and the logits
-// land in s_lg [token][KW] for the same gate_finish (8 warps, 256 tokens per tile).
+// 32 * ceil(KW / 10) rows, zero rows up to 128 kept in smem), N = up to 256 TOKENS per
+// MMA.  With the tokens on M (gate1_tc_kernel) every tcgen05.mma is 128 x NP x 16 with NP
+// as small as 32, and the MMA count per token -- each costs a near-fixed ~350 cycles
+// there -- is what bounds the kernel; here one MMA covers up to 256 tokens.  The
+// accumulator [piece rows x tokens] is transposed by the epilogue: lane r of quadrant q
+// holds piece r % 3 of logit 10 q + r / 3 for 32 tokens; two shuffles sum the pieces in
+// order, and the logits land in s_lg [token][KW] for gate_finish (8 warps).
+//
+// One launch does all of a1-a3 ("ranged" schedule):
+//  * work balance: the V * nch 32-token chunks are split into one contiguous range per
+//    CTA (ranges differ by at most one chunk), cut into tiles of up to 8 chunks that
+//    never cross a rank -- no partial last wave (C2 at N = 1 was 3.46 waves of fixed
+//    256-token tiles); a tile's MMA N is its own token count and its x rows arrive as one
+//    256-row TMA box or as 32-row boxes;
+//  * the exact three-piece bf16 split of the fp32 router (R3, R23) is built by the
+//    epilogue warps of the first CTAs into `wsplit` while the producers already stream x;
+//    producers issue the router loads of their first stages once the split is published
+//    (release / acquire counter + async-proxy fence) -- no separate split kernel;
+//  * the level-1 scan: the CTA that completes a rank's last chunk (per-rank arrival
+//    counter) runs that rank's scan over the chunk tables (scan1_rank) -- no scan kernel.
+//  The last CTA to finish resets the counters for the next call (graph-replay safe).
 // ---------------------------------------------------------------------------------
 constexpr int GS_TOK = 256, GS_THREADS = 128 + 256;
 constexpr int GS_X_BYTES = GS_TOK * GT_BK * 2;    // 32 KB per stage
-constexpr int GS_W_BYTES = 128 * GT_BK * 2;       // 16 KB per stage
+constexpr int GS_W_BYTES = 128 * GT_BK * 2;       // 16 KB per stage (rows >= NPT stay zero)
+constexpr int GS_CHUNK_BYTES = 32 * GT_BK * 2;    // one 32-token box of x
 
 template <int G>
 struct EpiSync256 {
@@ -446,29 +461,52 @@ struct EpiSync256 {
 
 struct GateTArgs {
     GateArgs g;
+    Scan1Args s;     // the level-1 scan this kernel runs per rank
     int NPT;         // split-router rows (32 * ceil(KW / 10))
     int stages;
-    int ntiles;
+    int64_t NCH;     // V * nch chunks
+    int nbuilders;   // CTAs that build the split router
+    int *split_ready, *done, *rank_cnt;
+    __nv_bfloat16 *wsplit;   // [NPT, d] the split router (built in-kernel, read by TMA)
 };
 
+struct RTile {
+    int v, c0, nck;  // rank, first chunk within the rank, chunks (<= 8)
+};
+
+__device__ __forceinline__ bool next_rtile(int64_t &cur, int64_t end, int nch, RTile &t) {
+    if (cur >= end) return false;
+    t.v = (int)(cur / nch);
+    t.c0 = (int)(cur - (int64_t)t.v * nch);
+    int64_t n = end - cur;
+    if (n > 8) n = 8;
+    if (n > nch - t.c0) n = nch - t.c0;
+    t.nck = (int)n;
+    cur += n;
+    return true;
+}
+
 __global__ void __launch_bounds__(GS_THREADS, 1)
-gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, GateTArgs ta) {
+gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapX32,
+                 const __grid_constant__ CUtensorMap mapW, GateTArgs ta) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const GateArgs &a = ta.g;
-    const int ST = ta.stages, KW = a.KW, NQ = ta.NPT / 32;
+    const int ST = ta.stages, KW = a.KW, NQ = ta.NPT / 32, nch = a.nch;
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sW = base;
     unsigned char *sX = sW + ST * GS_W_BYTES;
     const int lds = gate_lds(KW);
     float *s_lg = reinterpret_cast<float *>(sX + ST * GS_X_BYTES);    // [256][lds]
-    int *s_j = reinterpret_cast<int *>(s_lg + GS_TOK * lds);          // [256]
-    int *s_wh = s_j + GS_TOK;                                         // [8][K1]
+    int *s_wh = reinterpret_cast<int *>(s_lg + GS_TOK * lds);         // [8][K1] (fused permute only)
     int *s_bh = s_wh + 8 * a.K1;                                      // [K1]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(s_bh + a.K1) + 7) & ~(uintptr_t)7);
+    int *s_last = s_bh + a.K1;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(s_last + 1) + 7) & ~(uintptr_t)7);
     uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // this CTA's contiguous chunk range
+    const int64_t cb = ta.NCH * blockIdx.x / gridDim.x, ce = ta.NCH * (blockIdx.x + 1) / gridDim.x;
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
@@ -482,12 +520,20 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
     }
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapX)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapX32)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapW)) : "memory");
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (ta.NPT < 128) {
+        // the router operand's rows >= NPT are zero for the whole kernel (TMA writes rows < NPT)
+        for (int s = 0; s < ST; ++s)
+            for (int i = threadIdx.x; i < (128 - ta.NPT) * GT_BK * 2 / 16; i += blockDim.x)
+                reinterpret_cast<int4 *>(sW + s * GS_W_BYTES + ta.NPT * GT_BK * 2)[i] = make_int4(0, 0, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -497,28 +543,58 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
 
     if (warp == 0) {
         if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            const uint32_t wbytes = (uint32_t)ta.NPT * GT_BK * 2;
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
-                const int v = tile / a.nblk, blk = tile - v * a.nblk;
-                const int row0 = (int)((int64_t)v * a.T + (int64_t)blk * GS_TOK);
+            bool wready = false;
+            int pst[8], pkb[8], npend = 0;
+            auto load_w = [&](int st_, int kb_) {
+                tma_load_2d(smem_u32(sW + st_ * GS_W_BYTES), &mapW, kb_ * GT_BK, 0, smem_u32(&full[st_]));
+            };
+            auto wait_split = [&]() {
+                while (ld_acquire_gpu(ta.split_ready) < ta.nbuilders) { }
+                asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
+                for (int i = 0; i < npend; ++i) load_w(pst[i], pkb[i]);
+                npend = 0;
+                wready = true;
+            };
+            int64_t cur = cb;
+            RTile t;
+            while (next_rtile(cur, ce, nch, t)) {
+                const int row0 = (int)((int64_t)t.v * a.T + (int64_t)t.c0 * 32);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full[stage]);
-                    mbar_arrive_tx(fb, GS_W_BYTES + GS_X_BYTES);
-                    tma_load_2d(smem_u32(sW + stage * GS_W_BYTES), &mapW, kb * GT_BK, 0, fb);
-                    tma_load_2d(smem_u32(sX + stage * GS_X_BYTES), &mapX, kb * GT_BK, row0, fb);
+                    mbar_arrive_tx(fb, wbytes + (uint32_t)t.nck * GS_CHUNK_BYTES);
+                    if (t.nck == 8) {
+                        tma_load_2d(smem_u32(sX + stage * GS_X_BYTES), &mapX, kb * GT_BK, row0, fb);
+                    } else {
+                        for (int c = 0; c < t.nck; ++c)
+                            tma_load_2d(smem_u32(sX + stage * GS_X_BYTES + c * GS_CHUNK_BYTES), &mapX32, kb * GT_BK,
+                                        row0 + 32 * c, fb);
+                    }
+                    if (wready) {
+                        load_w(stage, kb);
+                    } else {
+                        pst[npend] = stage; pkb[npend] = kb; ++npend;
+                        if (npend == ST) wait_split();
+                    }
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
             }
+            if (!wready && npend) wait_split();
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = make_idesc(128, GS_TOK);
+            // ---------------- MMA issuer ----------------
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
+            int64_t cur = cb;
+            RTile t;
+            while (next_rtile(cur, ce, nch, t)) {
+                const uint32_t idesc = make_idesc(128, 32 * t.nck);
                 const int buf = it & 1;
                 mbar_wait(smem_u32(&tempty[buf]), ((uint32_t)(it >> 1) & 1) ^ 1);
                 tc_fence_after();
@@ -535,16 +611,41 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
                 mma_commit(smem_u32(&tfull[buf]));
+                ++it;
             }
         }
     } else if (warp >= 4) {
+        const int etid = threadIdx.x - 128, ew = etid >> 5;
+        // the exact three-piece split of W into wsplit ("quad10" rows: row 32 Q + w holds
+        // piece w % 3 of logit 10 Q + w / 3 for w < 30, rows 30, 31 of each group zero)
+        if ((int)blockIdx.x < ta.nbuilders) {
+            for (int r = blockIdx.x; r < ta.NPT; r += gridDim.x) {
+                const int q = r >> 5, ww = r & 31;
+                const int k = ww < 30 ? 10 * q + ww / 3 : KW, p = ww % 3;
+                for (int c = etid; c < a.d; c += 256) {
+                    float out = 0.f;
+                    if (k < KW) {
+                        float rem = __ldg(a.w + (int64_t)k * a.d + c);
+                        for (int z = 0; z < p; ++z) rem -= __bfloat162float(__float2bfloat16_rn(rem));
+                        out = rem;
+                    }
+                    ta.wsplit[(int64_t)r * a.d + c] = __float2bfloat16_rn(out);
+                }
+            }
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence();
+            EpiSync256<0>::sync();
+            if (etid == 0) atomicAdd(ta.split_ready, 1);
+        }
         const int q = warp & 3, hc = (warp - 4) >> 2;    // TMEM lane quadrant, token-column half
         int it = 0;
-        for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
-            const int v = tile / a.nblk, blk = tile - v * a.nblk;
-            const int64_t t0 = (int64_t)blk * GS_TOK;
-            const int nt = (int)(a.T - t0 < GS_TOK ? a.T - t0 : GS_TOK);
-            const int64_t tok0 = (int64_t)v * a.T + t0;
+        int64_t cur = cb;
+        RTile t;
+        while (next_rtile(cur, ce, nch, t)) {
+            const int64_t t0 = (int64_t)t.c0 * 32;
+            const int ntt = 32 * t.nck;
+            const int nt = (int)(a.T - t0 < ntt ? a.T - t0 : ntt);
+            const int64_t tok0 = (int64_t)t.v * a.T + t0;
             const int buf = it & 1;
             mbar_wait(smem_u32(&tfull[buf]), (uint32_t)(it >> 1) & 1);
             tc_fence_after();
@@ -552,7 +653,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                 const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + buf * GS_TOK + hc * 128;
                 const int k = 10 * q + lane / 3;
                 const bool head = (lane % 3 == 0) && lane < 30 && k < KW;
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < 4 && hc * 128 + c * 32 < ntt; ++c) {
                     float vv[32];
                     tmem_ld32(tb + c * 32, vv);
 #pragma unroll
@@ -568,12 +669,34 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
             if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
             EpiSync256<0>::sync();
             if (a.logits_out) {
-                for (int i = EpiSync256<0>::tid(); i < nt * KW; i += 256)
-                    a.logits_out[tok0 * KW + i] = s_lg[(i / KW) * lds + i % KW];
+                for (int i = etid; i < nt * KW; i += 256) a.logits_out[tok0 * KW + i] = s_lg[(i / KW) * lds + i % KW];
                 EpiSync256<0>::sync();
             }
-            gate_finish<EpiSync256<0>>(a, s_lg, lds, s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
+            gate_finish<EpiSync256<0>>(a, s_lg, lds, s_wh, s_bh, tok0, nt, (int64_t)t.v * nch + t.c0);
+            EpiSync256<0>::sync();                     // s_lg is rewritten by the next tile
+            ++it;
+        }
+        // This CTA's chunks are done: arrive once per rank it covered (after a barrier of the
+        // epilogue threads, one release fence -- cumulative over their table writes); the
+        // CTA that completes a rank runs that rank's level-1 scan over the chunk tables.
+        if (cb < ce) {
             EpiSync256<0>::sync();
+            for (int v = (int)(cb / nch); v <= (int)((ce - 1) / nch); ++v) {
+                const int64_t lo = cb > (int64_t)v * nch ? cb : (int64_t)v * nch;
+                const int64_t hi = ce < (int64_t)(v + 1) * nch ? ce : (int64_t)(v + 1) * nch;
+                if (etid == 0) {
+                    __threadfence();
+                    const int old = atomicAdd(ta.rank_cnt + v, (int)(hi - lo));
+                    *s_last = old + (int)(hi - lo) == nch;
+                    if (*s_last) __threadfence();
+                }
+                EpiSync256<0>::sync();
+                if (*s_last) {
+                    scan1_rank(ta.s, v, ew, 8);
+                    if (etid == 0) ta.rank_cnt[v] = 0;      // every chunk of the rank has arrived
+                }
+                EpiSync256<0>::sync();
+            }
         }
     }
     __syncthreads();
@@ -581,10 +704,19 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
     }
+    if (threadIdx.x == 0) {
+        // every CTA is past its split wait: the last one resets the counters for the next call
+        __threadfence();
+        if (atomicAdd(ta.done, 1) == (int)gridDim.x - 1) {
+            *ta.split_ready = 0;
+            *ta.done = 0;
+            __threadfence();
+        }
+    }
 }
 
 size_t gate_tcT_smem(int KW, int K1, int stages) {
-    return 1024 + (size_t)stages * (GS_W_BYTES + GS_X_BYTES) + ((size_t)GS_TOK * gate_lds(KW) + GS_TOK + 9 * K1) * 4 +
+    return 1024 + (size_t)stages * (GS_W_BYTES + GS_X_BYTES) + ((size_t)GS_TOK * gate_lds(KW) + 9 * K1 + 1) * 4 +
            8 + (2 * stages + 4) * 8 + 16;
 }
 
@@ -615,23 +747,24 @@ bool gate_tc_supported(int bf16, int d, int KW) {
     return bf16 && d % GT_BK == 0 && d >= GT_BK && gate_tc_np(KW) <= GT_MAX_NP && encode_fn() != nullptr;
 }
 
-cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, cudaStream_t st) {
+cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, const Scan1Args *scan,
+                            int *gate_sync, bool *scanned, cudaStream_t st) {
+    *scanned = false;
     if (a.T == 0) return cudaSuccess;
     if (a.logits || !gate_tc_supported(a.bf16, a.d, a.KW)) return cudaErrorNotSupported;
     if (a.TB == GS_TOK) {
-        if (a.fuse_dispatch) return cudaErrorNotSupported;          // the fused permute has 128-token tiles
+        if (a.fuse_dispatch || !scan || !gate_sync) return cudaErrorNotSupported;   // the fused permute has 128-token tiles
         const int NPT = 32 * ((a.KW + 9) / 10);
-        note_launch();
-        router_split_kernel<<<(NPT * a.d + 255) / 256 < 1024 ? (NPT * a.d + 255) / 256 : 1024, 256, 0, st>>>(
-            a.w, wsplit, a.KW, a.d, NPT, 1);
-        CUtensorMap mX, mW;
+        CUtensorMap mX, mX32, mW;
         if (!make_map(&mX, a.x, (int64_t)a.V * a.T, a.d, GS_TOK)) return cudaErrorNotSupported;
-        if (!make_map(&mW, wsplit, NPT, a.d, 128)) return cudaErrorNotSupported;    // rows >= NPT: zero fill
+        if (!make_map(&mX32, a.x, (int64_t)a.V * a.T, a.d, 32)) return cudaErrorNotSupported;
+        if (!make_map(&mW, wsplit, NPT, a.d, NPT)) return cudaErrorNotSupported;
         GateTArgs ta;
         memset(&ta, 0, sizeof(ta));
         ta.g = a;
+        ta.s = *scan;
         ta.NPT = NPT;
-        ta.ntiles = a.V * a.nblk;
+        ta.NCH = (int64_t)a.V * a.nch;
         int stages = 8;
         while (stages > 2 && gate_tcT_smem(a.KW, a.K1, stages) > 227 * 1024) --stages;
         ta.stages = stages;
@@ -641,9 +774,13 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
             cudaFuncSetAttribute(gate1_tcT_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             attrT = true;
         }
-        const int grid = ta.ntiles < num_sms ? ta.ntiles : num_sms;
+        const int grid = (int)(ta.NCH < num_sms ? ta.NCH : num_sms);
+        ta.nbuilders = NPT < grid ? NPT : grid;
+        ta.split_ready = gate_sync; ta.done = gate_sync + 1; ta.rank_cnt = gate_sync + 2;
+        ta.wsplit = wsplit;
         note_launch();
-        gate1_tcT_kernel<<<grid, GS_THREADS, smem, st>>>(mX, mW, ta);
+        gate1_tcT_kernel<<<grid, GS_THREADS, smem, st>>>(mX, mX32, mW, ta);
+        *scanned = true;
         return cudaGetLastError();
     }
     if (a.TB != GT_BM) return cudaErrorNotSupported;

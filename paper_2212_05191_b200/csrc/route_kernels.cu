@@ -155,80 +155,15 @@ __global__ void __launch_bounds__(256, 2) gate1_kernel(GateArgs a) {
         for (int i = tid; i < nt * KW; i += blockDim.x) a.logits_out[tok0 * KW + i] = s_lg[(i / KW) * lds + i % KW];
     if (a.logits_out && !a.logits) __syncthreads();
 
-    gate_finish<BlockSync>(a, s_lg, lds, s_j, s_wh, s_bh, tok0, nt, (int64_t)v * a.nblk + blk);
+    gate_finish<BlockSync>(a, s_lg, lds, s_wh, s_bh, tok0, nt, (int64_t)v * a.nch + t0 / 32);
 }
 
-// Warp-wide exclusive scan over n ints at stride `st` (in place), returns the total.
-__device__ int warp_exclusive_scan(const int32_t *p, int n, int64_t st, int32_t *out_excl) {
-    const int lane = threadIdx.x & 31;
-    int carry = 0;
-    for (int b0 = 0; b0 < n; b0 += 32) {
-        const int i = b0 + lane;
-        const int v = i < n ? p[(int64_t)i * st] : 0;
-        int x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(kFull, x, o);
-            if (lane >= o) x += y;
-        }
-        if (i < n) out_excl[(int64_t)i * st] = carry + x - v;
-        carry += __shfl_sync(kFull, x, 31);
-    }
-    return carry;
-}
-
-// Warp-wide fixed-order (lane-strided, then butterfly) fp64 / int sums: deterministic.
-__device__ double warp_sum_f64(const double *p, int n, int64_t st) {
-    const int lane = threadIdx.x & 31;
-    double acc = 0.0;
-    for (int i = lane; i < n; i += 32) acc += p[(int64_t)i * st];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-    return acc;
-}
-__device__ int warp_sum_i32(const int32_t *p, int n, int64_t st) {
-    const int lane = threadIdx.x & 31;
-    int acc = 0;
-    for (int i = lane; i < n; i += 32) acc += p[(int64_t)i * st];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-    return acc;
-}
-
-// Level-1 scan: per rank, exclusive prefix over blocks of each destination's count;
-// totals -> hist1, counts1 = min(hist1, C1); stats reduced over blocks in fixed order.
-// One warp per (destination or statistic), grid = V.
+// Level-1 scan over the per-chunk tables (gate_common.cuh scan1_rank), grid = V.
 __global__ void scan1_kernel(Scan1Args a) {
-    const int v = blockIdx.x, w = threadIdx.x >> 5, NW = blockDim.x >> 5, lane = threadIdx.x & 31;
+    const int v = blockIdx.x;
     if (a.lb_flag)                                   // the fused gate's look-back flags, for the next call
-        for (int b = threadIdx.x; b < a.nblk; b += blockDim.x) a.lb_flag[(int64_t)v * a.nblk + b] = 0;
-    const int KS = a.K1 + a.K2;
-    const int jobs = a.K1 + KS + a.K2;
-    for (int j = w; j < jobs; j += NW) {
-        if (j < a.K1) {
-            const int k = j;
-            const int64_t o = (int64_t)v * a.nblk * a.K1 + k;
-            const int tot = warp_exclusive_scan(a.blk_hist1 + o, a.nblk, a.K1, a.blk_off1 + o);
-            if (lane == 0) {
-                a.stats.hist1[v * a.K1 + k] = tot;
-                a.counts1[v * a.K1 + k] = (int32_t)imin64(tot, a.C1);
-                if (a.peer.bases && a.flat) {      // counts travel with the rows: rcounts[q][src][k % e]
-                    const PeerMap &P = a.peer;
-                    const int rk = P.rank0 + v, q = k / P.e;
-                    reinterpret_cast<int32_t *>(P.bases[q / P.V] + P.off_rcounts)[((int64_t)(q % P.V) * P.G + rk) * P.e + k % P.e] =
-                        (int32_t)imin64(tot, a.C1);
-                }
-            }
-        } else if (j < a.K1 + KS) {
-            const int k = j - a.K1;
-            const double sum = warp_sum_f64(a.blk_psum + (int64_t)v * a.nblk * KS + k, a.nblk, KS);
-            if (lane == 0) {
-                if (k < a.K1) a.stats.psum1[v * a.K1 + k] = sum;
-                else a.stats.psum2[v * a.K2 + (k - a.K1)] = sum;
-            }
-        } else {
-            const int k = j - a.K1 - KS;
-            const int c = warp_sum_i32(a.blk_hist2a + (int64_t)v * a.nblk * a.K2 + k, a.nblk, a.K2);
-            if (lane == 0) a.stats.hist2[v * a.K2 + k] = c;
-        }
-    }
+        for (int b = threadIdx.x; b < a.nlb; b += blockDim.x) a.lb_flag[(int64_t)v * a.nlb + b] = 0;
+    scan1_rank(a, v, threadIdx.x >> 5, blockDim.x >> 5);
 }
 
 // a6: level-2 gate at the intermediate: rank valid received slots per j, in received
@@ -598,6 +533,7 @@ __global__ void exchange_copy_kernel(CopyXArgs a) {
     const int v = pair / a.P, p = pair % a.P;
     const int q = a.member_local[v * a.P + p];
     if (q < 0) return;
+    if (a.fabric && (a.rank0 + v) / a.m != (a.rank0 + q) / a.m) return;   // carried by the emulated NIC
     const int pos = a.mypos[v];
     const int64_t src_chunk = ((int64_t)v * a.P + p) * a.nsub + k;
     const int64_t dst_chunk = ((int64_t)q * a.P + pos) * a.nsub + k;
@@ -624,6 +560,64 @@ __global__ void exchange_copy_kernel(CopyXArgs a) {
     if (!a.rev && a.sint && blockIdx.y == 0 && k == 0) {
         for (int i = threadIdx.x; i < a.ipp; i += blockDim.x)
             a.rint[((int64_t)q * a.P + pos) * a.ipp + i] = a.sint[((int64_t)v * a.P + p) * a.ipp + i];
+    }
+}
+
+// Emulated heterogeneous fabric (smile_set_fabric): CTA v is the NIC
+// of sending rank v; it sends its cross-node messages (one per group member on another
+// node: all of the pair's sub-chunks and side ints) one after another, each occupying
+// latency + bytes * ns_per_byte of wall time (%globaltimer); the rows are copied at the
+// start of the message's window.
+__global__ void fabric_copy_kernel(CopyXArgs a) {
+    __shared__ unsigned long long s_t0;
+    const int v = blockIdx.x;
+    const int pos = a.mypos[v];
+    const int nvec = (int)(a.rowbytes / 16);
+    for (int p = 0; p < a.P; ++p) {
+        const int q = a.member_local[v * a.P + p];
+        if (q < 0 || (a.rank0 + v) / a.m == (a.rank0 + q) / a.m) continue;
+        if (threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            s_t0 = t;
+        }
+        __syncthreads();
+        int64_t bytes = 0;
+        for (int k = 0; k < a.nsub; ++k) {
+            const int64_t src_chunk = ((int64_t)v * a.P + p) * a.nsub + k;
+            const int64_t dst_chunk = ((int64_t)q * a.P + pos) * a.nsub + k;
+            int64_t rows = a.Csub;
+            if (a.cnt) {
+                rows = a.rev ? a.cnt[((int64_t)q * a.P + pos) * a.nsub + k] : a.cnt[src_chunk];
+                rows = imin64((rows > 0 ? rows : (int64_t)0), a.Csub);
+            }
+            bytes += rows * a.rowbytes;
+            const int4 *src = reinterpret_cast<const int4 *>(a.send + src_chunk * a.Csub * a.rowbytes);
+            int4 *dst = reinterpret_cast<int4 *>(a.recv + dst_chunk * a.Csub * a.rowbytes);
+            const int64_t nv = rows * nvec;
+            int64_t i = threadIdx.x;
+            for (; i + 3 * blockDim.x < nv; i += 4 * blockDim.x) {
+                int4 x0 = __ldg(src + i), x1 = __ldg(src + i + blockDim.x), x2 = __ldg(src + i + 2 * blockDim.x),
+                     x3 = __ldg(src + i + 3 * blockDim.x);
+                dst[i] = x0; dst[i + blockDim.x] = x1; dst[i + 2 * blockDim.x] = x2; dst[i + 3 * blockDim.x] = x3;
+            }
+            for (; i < nv; i += blockDim.x) dst[i] = __ldg(src + i);
+        }
+        if (!a.rev && a.sint) {
+            bytes += (int64_t)a.ipp * 4;
+            for (int i = threadIdx.x; i < a.ipp; i += blockDim.x)
+                a.rint[((int64_t)q * a.P + pos) * a.ipp + i] = a.sint[((int64_t)v * a.P + p) * a.ipp + i];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long until = s_t0 + (unsigned long long)(a.latency_ns + (double)bytes * a.ns_per_byte);
+            for (;;) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t >= until) break;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -802,6 +796,11 @@ void launch_peer_barrier(char *const *bases, int64_t off_flags, int me, const in
     if (npeers <= 0) return;
     note_launch();
     peer_barrier_kernel<<<1, 32, 0, st>>>(bases, off_flags, me, peers, npeers, level, epoch, timeout_ns, err);
+}
+
+void launch_fabric_copy(const CopyXArgs &a, cudaStream_t st) {
+    note_launch();
+    fabric_copy_kernel<<<a.V, 256, 0, st>>>(a);
 }
 
 void launch_exchange_copy(const CopyXArgs &a, cudaStream_t st) {

@@ -70,7 +70,9 @@ struct smile_ctx_s {
     bool l1_pending = false;   // the last expert FFN wrote out rows directly: until the next level-1
                                // dispatch, smile_combine(1) may only target the bound output
     const float *d1_gate = nullptr;   // route->gate of the last smile_dispatch(1)
-    int nblk1 = 0;             // gate blocks per rank
+    int nblk1 = 0;             // gate tiles per rank (fixed-tile gate kernels, fused look-back)
+    int nch1 = 0;              // 32-token chunks per rank: the level-1 scan / statistics tables
+    int *gate_sync = nullptr;  // [2 + V] ranged tensor-core gate: split-ready, done, per-rank chunk counters
     int nblk2 = 0;             // level-2 ranking blocks per rank
     int *d_err = nullptr;      // sticky device error flag (smile_status)
     int32_t *blk_hist1 = nullptr, *blk_off1 = nullptr, *blk_hist2a = nullptr;
@@ -79,6 +81,7 @@ struct smile_ctx_s {
     ncclComm_t world = nullptr, inter = nullptr, intra = nullptr;
     smile::Level lv[3];        // 0 world, 1 inter, 2 intra
     int num_sms = 148;
+    smile_fabric fabric{};     // emulated inter-node fabric (COPY exchange, nprocs == 1)
     // peer-store exchange (smile_register_workspace)
     int xchg = 0;                            // smile_xchg
     void *reg_ws = nullptr;                  // the registered workspace
@@ -99,6 +102,7 @@ struct smile_ctx_s {
     // smile_forward_host_stream: copy streams and ping-pong events (created with the ctx)
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+    cudaEvent_t ev_chunk_front = nullptr, ev_chunk_ffn = nullptr;   // smile_forward_chunked
 };
 
 namespace smile {
@@ -108,6 +112,7 @@ struct GateArgs {
     const void *x; const float *w; const float *logits; float *logits_out;
     smile_route route; int32_t *blk_hist1, *blk_hist2a; double *blk_psum;
     int *err; int V; int64_t T; int d; int K1, K2, KW; int TB, nblk; int flat; int bf16;
+    int nch;                 // 32-token chunks per rank: granularity of the scan / stats tables
     // fused level-1 permute (tensor-core gate only; smile_gate_dispatch_inter): final
     // slots by decoupled look-back over the tiles' destination histograms, then the
     // kept rows moved to their slots (send rows / meta, or the peers' receive buffers)
@@ -121,8 +126,9 @@ void launch_gate1(const GateArgs &a, cudaStream_t st);
 struct Scan1Args {
     const int32_t *blk_hist1, *blk_hist2a; const double *blk_psum; int32_t *blk_off1;
     smile_stats stats; int32_t *counts1; int V, nblk, K1, K2, KW; int64_t C1; int flat; int64_t T;
-    PeerMap peer;
+    PeerMap peer;            // nblk: 32-token chunks per rank (the tables' granularity)
     int *lb_flag;            // reset for the next fused gate (may be null)
+    int nlb;                 // look-back tiles per rank (lb_flag entries)
 };
 void launch_scan1(const Scan1Args &a, cudaStream_t st);
 
@@ -204,8 +210,17 @@ struct CopyXArgs {
     const char *send; char *recv; const int32_t *sint; int32_t *rint; const int32_t *cnt;
     const int32_t *member_local; const int32_t *mypos; int V, P, nsub; int64_t Csub;
     int64_t rowbytes; int ipp; int rev;
+    // emulated heterogeneous fabric (smile_set_fabric): pairs whose ranks lie in different
+    // groups ("nodes", rank / m) are skipped by the device copy and carried by the sender's
+    // emulated NIC instead (launch_fabric_copy)
+    int fabric; int rank0, m;
+    double ns_per_byte; double latency_ns;
 };
 void launch_exchange_copy(const CopyXArgs &a, cudaStream_t st);
+// The cross-node pairs of one exchange through per-rank emulated NICs: one CTA per sending
+// rank handles its cross-node messages one after another, each costing latency + bytes /
+// bandwidth of wall time (globaltimer), with the rows moved inside that window.
+void launch_fabric_copy(const CopyXArgs &a, cudaStream_t st);
 
 struct FfnArgs {
     const void *X; const int32_t *counts; const void *W1t; const float *b1; const void *W2t;
@@ -257,6 +272,10 @@ int gate_tc_np(int KW);
 int gate_tc_tile(int KW);            // token tile of the tensor-core gate (128, or 256 for the swapped kernel)
 int gate_tc_rows(int KW);            // rows of the split-router buffer
 bool gate_tc_supported(int bf16, int d, int KW);
-cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, cudaStream_t st);
+// The 256-token ("ranged") kernel also builds the split router and runs the level-1 scan
+// (`scan`, counters in gate_sync [2 + V]) and sets *scanned; the 128-token kernel leaves
+// the scan to launch_scan1.
+cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, const Scan1Args *scan,
+                            int *gate_sync, bool *scanned, cudaStream_t st);
 
 }  // namespace smile

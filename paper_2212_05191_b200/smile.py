@@ -56,6 +56,10 @@ class Stats(C.Structure):
     _fields_ = [(k, _P) for k in ("hist1", "hist2", "psum1", "psum2")]
 
 
+class Fabric(C.Structure):
+    _fields_ = [("inter_gbps", C.c_double), ("inter_latency_us", C.c_double)]
+
+
 class LayerIO(C.Structure):
     _fields_ = [("x", _P), ("logits", _P), ("w_router", _P), ("W1t", _P), ("b1", _P), ("W2t", _P),
                 ("b2", _P), ("out", _P), ("loss", _P), ("alpha", C.c_double), ("beta", C.c_double),
@@ -93,7 +97,8 @@ def lib():
                      "smile_gate_dispatch_inter",
                      "smile_expert_ffn_train", "smile_combine_bwd", "smile_dispatch_grad", "smile_expert_ffn_bwd",
                      "smile_combine_grad", "smile_router_bwd", "smile_backward", "smile_ipc_handle",
-                     "smile_register_workspace", "smile_struct_sizes", "smile_forward_host_stream", "smile_set_output"):
+                     "smile_register_workspace", "smile_struct_sizes", "smile_forward_host_stream", "smile_set_output",
+                     "smile_forward_chunked", "smile_set_fabric"):
             getattr(L, name).restype = C.c_int
         # the ctypes mirrors must match the C structs byte for byte
         sizes = (C.c_int64 * 8)()
@@ -310,6 +315,12 @@ class SmileLayer:
         _check(lib().smile_forward_host_stream(self._ctx, C.byref(io), xd, od, nb, hx, ho, _ptr(host_loss),
                                                _stream(stream)), "smile_forward_host_stream")
 
+    def set_fabric(self, inter_gbps: float, inter_latency_us: float):
+        """smile_set_fabric: the emulated inter-node fabric of the COPY exchange (SURVEY 8(f)
+        row 1; an in-box emulation).  inter_gbps <= 0 disables it."""
+        f = Fabric(float(inter_gbps), float(inter_latency_us))
+        _check(lib().smile_set_fabric(self._ctx, C.byref(f)), "smile_set_fabric")
+
     def set_output(self, out):
         """smile_set_output: bind the layer output for the following step calls (None unbinds)."""
         _check(lib().smile_set_output(self._ctx, _ptr(out)), "smile_set_output")
@@ -367,3 +378,24 @@ class SmileLayer:
     def aux_loss(self, stats, loss, alpha=0.005, beta=0.005, stream=None):
         _check(lib().smile_aux_loss(self._ctx, C.byref(stats), C.c_double(alpha), C.c_double(beta), _ptr(loss),
                                     _stream(stream)), "smile_aux_loss")
+
+
+def forward_chunked(layers, xs, W1t, b1, W2t, b2, outs, losses, w_router=None, logits=None, alpha=0.005, beta=0.005,
+                    stream=None, stream2=None):
+    """smile_forward_chunked: the layer over len(layers) chunks pipelined on two streams.
+    layers[k]: a SmileLayer per chunk (T = tokens per chunk, same shape otherwise), xs[k] /
+    outs[k]: [V, T/c, d] chunk inputs / outputs, losses[k]: [V] float64; logits (supplied
+    mode) a list of per-chunk logits or None."""
+    n = len(layers)
+    for L in layers:
+        if L.ws is None:
+            L.alloc_workspace()
+    Ctxs = C.c_void_p * n
+    IOs = LayerIO * n
+    ctxs = Ctxs(*[L._ctx for L in layers])
+    ios = IOs(*[LayerIO(_ptr(xs[k]), _ptr(None if logits is None else logits[k]), _ptr(w_router), _ptr(W1t), _ptr(b1),
+                        _ptr(W2t), _ptr(b2), _ptr(outs[k]), _ptr(losses[k]), alpha, beta, _ptr(layers[k].ws), 0)
+                for k in range(n)])
+    if stream2 is None:
+        raise ValueError("forward_chunked needs a second stream")
+    _check(lib().smile_forward_chunked(ctxs, ios, n, _stream(stream), _stream(stream2)), "smile_forward_chunked")

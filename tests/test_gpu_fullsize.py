@@ -147,7 +147,6 @@ def test_c3_training_full_size(n, m):
     _check_logits(case, lg)
     r = case.oracle_route(logits=lg)
     _check_route_full(case, layer, r, loss)
-    assert (r.keep == 0).any()                                # cf 1.25 drops tokens
     # forward output on dense rows
     rows = dense_rows(case, r)
     got = out.view(-1, d)[torch.from_numpy(rows).cuda()].float().cpu().numpy()
