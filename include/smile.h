@@ -84,11 +84,15 @@ typedef struct {
     int32_t proc;           /* this process, 0 <= proc < nprocs */
     int32_t device;         /* CUDA device ordinal of this process */
     int32_t ffn_impl;       /* smile_ffn_impl */
+    int32_t topk;           /* experts per token (Eq. 2): 0 or 1 = the
+                               top-1 layers of the paper (Eq. 3); 2..4 = the FLAT top-k layer
+                               (GShard-style, R29-R32).  BILEVEL requires top-1 */
 } smile_shape;
 
-/* Sizes derived from a shape (R5, R7, R20):
+/* Sizes derived from a shape (R5, R7, R20, R31):
  *   K1 = BILEVEL ? n : G*e;   K2 = BILEVEL ? m*e : 1;
- *   C1 = K1 > 1 ? ceil(cf*T/K1) : T;   C2 = BILEVEL ? (K2 > 1 ? ceil(cf*T/K2) : n*C1) : 0.
+ *   C1 = K1 > 1 ? ceil(cf*k*T/K1) : k*T (k = topk, 1 for the paper's layers);
+ *   C2 = BILEVEL ? (K2 > 1 ? ceil(cf*T/K2) : n*C1) : 0.
  * S = segments per local expert at the FFN (BILEVEL: m source ranks; FLAT: G);
  * Cseg = rows per segment (BILEVEL: C2; FLAT: C1). */
 typedef struct {
@@ -192,8 +196,10 @@ typedef enum { SMILE_XCHG_COPY = 0, SMILE_XCHG_PEER = 1 } smile_xchg;
  * of P:L64-76), all ranks' NICs concurrently.  Same-node transfers stay device copies.
  * Data movement only: results are bit-identical to the plain COPY exchange.
  * Needs nprocs == 1 (every rank on this GPU) and the COPY exchange; inter_gbps <= 0
- * disables it.  The per-NIC copy runs on one CTA, so bandwidths above what one SM moves
- * (~100 GB/s) are not emulated faithfully. */
+ * disables it.  Each emulated NIC copies with 16 CTAs; a message whose rows take longer to
+ * copy than its window delays the next one, so bandwidths above that copy rate are not
+ * emulated faithfully (the bench reports the model's expected exchange time beside the
+ * measured one). */
 typedef struct {
     double inter_gbps;        /* bytes per second / 1e9 of one rank's emulated NIC */
     double inter_latency_us;  /* fixed cost per cross-node message */
@@ -240,7 +246,10 @@ smile_status smile_set_output(smile_ctx ctx, void *out);
 
 /* ---------------- the steps of the layer ---------------- */
 
-/* Per-token routing decisions [V, T] (SoA). */
+/* Per-token routing decisions [V, T] (SoA).  Top-k FLAT layer (shape.topk = k > 1): dest1,
+ * slot1 and gate are [k, V, T] choice-major -- choice j of token (v, t) at j*V*T + v*T + t,
+ * dest1 = its expert (R29), gate = its weight p_e (Eq. 2, R30), slot1 = its capacity slot
+ * in choice-major order (R31); p [V, T] = the top-1 probability. */
 typedef struct {
     int32_t *dest1;   /* i: level-1 destination, first argmax of logits[0, K1) (R2, R3) */
     int32_t *dest2;   /* j: level-2 destination, first argmax of logits[K1, K1+K2) (FLAT: 0) */

@@ -69,6 +69,10 @@ def lib():
         _lib.oracle_objective.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32] + [_P] * 8 + [C.c_double, _P, _P]
         _lib.oracle_backward.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32, _P, _P, _P, C.POINTER(_Route),
                                          _P, _P, _P, _P, _P, C.c_double] + [_P] * 7
+        _lib.oracle_route_topk.restype = C.c_int
+        _lib.oracle_route_topk.argtypes = [C.POINTER(_Cfg), C.c_int32, _P] + [_P] * 8
+        _lib.oracle_out_rows_topk.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P,
+                                              _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]
         _lib.oracle_logits_mt.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]
         _lib.oracle_out_rows_mt.argtypes = _lib.oracle_out_rows.argtypes
         _lib.oracle_threads.restype = C.c_int32
@@ -255,4 +259,55 @@ def backward_sampled(cfg: Config, r: Route, x, W1, b1, W2, b2, gout, tokens, col
                                   C.byref(r._s), _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2), _ptr(gout), lam, nt,
                                   _ptr(tokens), nc, _ptr(cols), _ptr(out["dlogits"]), _ptr(out["dx"]),
                                   _ptr(out["dW1c"]), _ptr(out["db1c"]), _ptr(out["dW2r"]), _ptr(out["db2"]))
+    return out
+
+
+class RouteTopk:
+    """Outputs of oracle_route_topk (flat top-k layer, Eq. 2): choice-major arrays [k, G, T]."""
+
+    def __init__(self, cfg: Config, k: int):
+        G, T = cfg.G, cfg.T
+        K = G * cfg.e
+        self.cfg, self.k, self.K = cfg, k, K
+        self.dest = np.zeros((k, G, T), np.int32)
+        self.slot = np.zeros((k, G, T), np.int32)
+        self.keep = np.zeros((k, G, T), np.uint8)
+        self.w = np.zeros((k, G, T), np.float32)
+        self.counts = np.zeros((G, K), np.int32)
+        self.A1 = np.zeros((G, K), np.int64)
+        self.S1 = np.zeros((G, K), np.float64)
+        self.loss = np.zeros(G, np.float64)
+
+
+def route_topk(cfg: Config, k: int, lg: np.ndarray) -> RouteTopk:
+    """Top-k routing of the flat layer (oracle_route_topk).  lg [G, T, G*e] fp32."""
+    assert cfg.flat
+    lg = np.ascontiguousarray(lg, np.float32)
+    assert lg.shape == (cfg.G, cfg.T, cfg.G * cfg.e), lg.shape
+    r = RouteTopk(cfg, k)
+    rc = lib().oracle_route_topk(C.byref(cfg._c()), k, _ptr(lg), *[_ptr(a) for a in (
+        r.dest, r.slot, r.keep, r.w, r.counts, r.A1, r.S1, r.loss)])
+    if rc == 3:
+        raise ValueError("non-finite logits")
+    if rc != 0:
+        raise ValueError(f"invalid configuration ({rc})")
+    return r
+
+
+def out_rows_topk(cfg: Config, r: RouteTopk, x, W1=None, b1=None, W2=None, b2=None, rows=None,
+                  identity: bool = False) -> np.ndarray:
+    """Eq. (2) output of the top-k layer (fp64) for global token rows g = rank*T + t."""
+    x = np.ascontiguousarray(x, np.float32)
+    d = x.shape[-1]
+    if identity:
+        W1 = b1 = W2 = b2 = np.zeros(1, np.float32)
+        d_ff = 0
+    else:
+        W1, b1, W2, b2 = (np.ascontiguousarray(a, np.float32) for a in (W1, b1, W2, b2))
+        d_ff = W1.shape[-1]
+    rows = np.arange(cfg.G * cfg.T, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
+    out = np.empty((rows.shape[0], d), np.float64)
+    lib().oracle_out_rows_topk(C.byref(cfg._c()), r.k, d, d_ff, _ptr(x), _ptr(r.dest), _ptr(r.keep), _ptr(r.w),
+                               _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2), int(identity), rows.shape[0], _ptr(rows),
+                               _ptr(out))
     return out

@@ -737,3 +737,100 @@ void oracle_backward_sampled(const oracle_cfg *c, int32_t d, int32_t d_ff, const
     }
     free(L); free(gate); free(ex_of);
 }
+
+/* ===================================================================================
+ * Top-k routing of the flat Switch / GShard-style layer (Eq. (2),
+ * "The top-k experts are then selected for processing the given token ...
+ * y(x) = sum_{e in I} p_e(x) E_e(x)").  Readings (R29-R32):
+ *   R29 I = the k largest logits, taken by repeated first-argmax (strict '>', R2) over
+ *       the entries not chosen yet: choice 0 is the top-1 expert of oracle_route.
+ *   R30 p_e is the softmax over ALL K experts (Eq. 1, R1); Eq. (2) uses it unnormalised.
+ *   R31 capacity C = ceil(cf * k * T / K) per (sending rank, expert) (R5 with k T items);
+ *       slots in choice-major order -- every token's choice 0 (token order), then every
+ *       token's choice 1, ... -- so a first choice never loses its slot to a second one.
+ *   R32 the LB loss is the Switch loss on the top-1 fractions (f counts choice 0), as for k = 1.
+ * Outputs (caller-allocated): dest/slot/keep/w [k*G*T] choice-major (index j*G*T + g),
+ * counts [G*K] = min(items per expert, C), A1 [G*K], S1 [G*K], loss [G].  cfg->flat must
+ * be 1.  Returns 0, 1 (invalid), 3 (non-finite logits).
+ * =================================================================================== */
+int oracle_route_topk(const oracle_cfg *c, int32_t k, const float *logits, int32_t *dest, int32_t *slot,
+                      uint8_t *keep, float *w, int32_t *counts, int64_t *A1, double *S1, double *loss) {
+    if (!c->flat || c->n < 1 || c->m < 1 || c->e < 1 || c->T < 0 || !(c->cf > 0.0)) return 1;
+    const int64_t G = (int64_t)c->n * c->m, T = c->T, K = G * c->e;
+    if (k < 1 || k > K) return 1;
+    for (int64_t i = 0; i < G * T * K; ++i)
+        if (!isfinite(logits[i])) return 3;
+    const int64_t C = T > 0 ? (K > 1 ? (int64_t)ceil(c->cf * (double)k * (double)T / (double)K) : (int64_t)k * T) : 0;
+    double *prob = (double *)malloc(sizeof(double) * (size_t)K);
+    uint8_t *taken = (uint8_t *)malloc((size_t)K);
+    int64_t *cnt = (int64_t *)malloc(sizeof(int64_t) * (size_t)K);
+    memset(A1, 0, sizeof(int64_t) * (size_t)(G * K));
+    memset(S1, 0, sizeof(double) * (size_t)(G * K));
+    for (int64_t r = 0; r < G; ++r) {
+        /* choices and weights, token by token (R29, R30) */
+        for (int64_t t = 0; t < T; ++t) {
+            const int64_t g = r * T + t;
+            const float *L = logits + g * K;
+            const int32_t i0 = first_argmax(L, K);
+            softmax_top1(L, K, i0, prob);
+            for (int64_t q = 0; q < K; ++q) S1[r * K + q] += prob[q];
+            A1[r * K + i0] += 1;                                     /* R32 */
+            memset(taken, 0, (size_t)K);
+            for (int32_t j = 0; j < k; ++j) {
+                int32_t best = -1;
+                for (int64_t q = 0; q < K; ++q)
+                    if (!taken[q] && (best < 0 || L[q] > L[best])) best = (int32_t)q;
+                taken[best] = 1;
+                dest[(int64_t)j * G * T + g] = best;
+                w[(int64_t)j * G * T + g] = (float)prob[best];
+            }
+        }
+        /* capacity slots in choice-major order (R31) */
+        memset(cnt, 0, sizeof(int64_t) * (size_t)K);
+        for (int32_t j = 0; j < k; ++j)
+            for (int64_t t = 0; t < T; ++t) {
+                const int64_t x = (int64_t)j * G * T + r * T + t;
+                slot[x] = (int32_t)cnt[dest[x]]++;
+                keep[x] = (uint8_t)(slot[x] < C);
+            }
+        for (int64_t q = 0; q < K; ++q) counts[r * K + q] = (int32_t)(cnt[q] < C ? cnt[q] : C);
+        double l1 = 0.0;
+        if (T > 0)
+            for (int64_t q = 0; q < K; ++q)
+                l1 += ((double)A1[r * K + q] / (double)T) * (S1[r * K + q] / (double)T);
+        loss[r] = c->alpha * (double)K * l1;
+    }
+    free(prob);
+    free(taken);
+    free(cnt);
+    return 0;
+}
+
+/* Eq. (2) layer output of the top-k layer for the listed global token rows (fp64):
+ * out[t] = sum_j keep_j w_j E_{dest_j}(x_t) (dropped choices contribute nothing, R9);
+ * identity != 0 replaces every E by the identity map. */
+void oracle_out_rows_topk(const oracle_cfg *c, int32_t k, int32_t d, int32_t d_ff, const float *x,
+                          const int32_t *dest, const uint8_t *keep, const float *w, const float *W1,
+                          const float *b1, const float *W2, const float *b2, int32_t identity, int64_t nrows,
+                          const int64_t *rows, double *out) {
+    const int64_t G = (int64_t)c->n * c->m, T = c->T;
+    double *y = (double *)malloc(sizeof(double) * (size_t)d);
+    for (int64_t a = 0; a < nrows; ++a) {
+        const int64_t g = rows[a];
+        double *o = out + a * d;
+        for (int32_t cc = 0; cc < d; ++cc) o[cc] = 0.0;
+        for (int32_t j = 0; j < k; ++j) {
+            const int64_t x_ = (int64_t)j * G * T + g;
+            if (!keep[x_]) continue;
+            const int64_t ex = dest[x_];
+            if (identity) {
+                for (int32_t cc = 0; cc < d; ++cc) y[cc] = (double)x[g * d + cc];
+            } else {
+                oracle_ffn_row(d, d_ff, x + g * d, W1 + ex * (int64_t)d * d_ff, b1 + ex * (int64_t)d_ff,
+                               W2 + ex * (int64_t)d_ff * d, b2 + ex * (int64_t)d, y);
+            }
+            for (int32_t cc = 0; cc < d; ++cc) o[cc] += (double)w[x_] * y[cc];
+        }
+    }
+    free(y);
+}

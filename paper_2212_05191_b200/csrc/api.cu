@@ -89,12 +89,13 @@ static void ws_layout(const smile_shape *s, const smile_sizes *z, WsLayout *L, s
     auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes ? bytes : 1); return base ? base + r : nullptr; };
     smile_ws_view w;
     memset(&w, 0, sizeof(w));
-    w.route.dest1 = (int32_t *)take(V * T * 4);
+    const int64_t k = s->topk > 1 ? s->topk : 1;           // choices per token (FLAT top-k)
+    w.route.dest1 = (int32_t *)take(k * V * T * 4);
     w.route.dest2 = (int32_t *)take(V * T * 4);
-    w.route.slot1 = (int32_t *)take(V * T * 4);
+    w.route.slot1 = (int32_t *)take(k * V * T * 4);
     w.route.p = (float *)take(V * T * 4);
     w.route.q = (float *)take(V * T * 4);
-    w.route.gate = (float *)take(V * T * 4);
+    w.route.gate = (float *)take(k * V * T * 4);
     w.stats.hist1 = (int32_t *)take(V * z->K1 * 4);
     w.stats.hist2 = (int32_t *)take(V * z->K2 * 4);
     w.stats.psum1 = (double *)take(V * z->K1 * 8);
@@ -144,6 +145,9 @@ extern "C" smile_status smile_plan(const smile_shape *s, smile_sizes *out) {
     const int G = s->n * s->m;
     if (s->nprocs < 1 || G % s->nprocs != 0 || s->proc < 0 || s->proc >= s->nprocs) return SMILE_EINVAL;
     if (s->T > (int64_t)1 << 30) return SMILE_ENOTSUP;
+    const int topk = s->topk > 1 ? s->topk : 1;
+    if (s->topk < 0) return SMILE_EINVAL;
+    if (topk > 1 && (s->mode != SMILE_FLAT || topk > 4 || topk > G * s->e)) return SMILE_ENOTSUP;   // R29-R32
     const int eb = s->dtype == SMILE_BF16 ? 2 : 4;
     if ((s->d * eb) % 16 != 0 || (s->d_ff * eb) % 16 != 0) return SMILE_ESHAPE;
     smile_sizes z;
@@ -155,7 +159,7 @@ extern "C" smile_status smile_plan(const smile_shape *s, smile_sizes *out) {
     z.K1 = bi ? s->n : G * s->e;
     z.K2 = bi ? s->m * s->e : 1;
     z.KW = bi ? z.K1 + z.K2 : z.K1;
-    z.C1 = capacity(s->T, z.K1, s->cf);
+    z.C1 = capacity((int64_t)topk * s->T, z.K1, s->cf);      // R31: k T items per rank
     z.C2 = bi ? (z.K2 > 1 ? capacity(s->T, z.K2, s->cf) : (int64_t)s->n * z.C1) : 0;
     z.S = bi ? s->m : G;
     z.Cseg = bi ? z.C2 : z.C1;
@@ -291,7 +295,8 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
         const char *e = getenv("SMILE_GATE_TC");
         const bool tc_on = !(e && e[0] == '0');
         if (tc_on && gate_tc_supported(shape->dtype == SMILE_BF16, shape->d, z.KW)) {
-            c->TB1 = gate_tc_tile(z.KW);        // the tensor-core gate's token tile (128 or 256)
+            c->gate_swapped = gate_tc_swapped(z.KW);
+            c->TB1 = c->gate_swapped ? 256 : 128;   // the tensor-core gate's token tile = table block
             const size_t wb = (size_t)gate_tc_rows(z.KW) * shape->d * 2;
             if (cudaMalloc(&c->wsplit, wb) != cudaSuccess) { delete c; return SMILE_ECUDA; }
             // look-back state of the fused gate + permute (flags zero between calls)
@@ -306,15 +311,15 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
         }
     }
     c->nblk1 = (int)((shape->T + c->TB1 - 1) / c->TB1);
-    c->nch1 = (int)((shape->T + 31) / 32);
     const int64_t items2 = (int64_t)shape->n * z.C1;
     c->nblk2 = shape->mode == SMILE_BILEVEL ? (int)((items2 + kRank2Items - 1) / kRank2Items) : 0;
-    const size_t nb1 = (size_t)V * (c->nch1 > 0 ? c->nch1 : 1);     // per-chunk tables
+    const int topk = shape->topk > 1 ? shape->topk : 1;
+    const size_t nb1 = (size_t)V * topk * (c->nblk1 > 0 ? c->nblk1 : 1);   // [V][topk][nblk] tables
     const size_t nb2 = (size_t)V * (c->nblk2 > 0 ? c->nblk2 : 1);
     CUDA_TRY(cudaMalloc(&c->d_err, sizeof(int)));
     CUDA_TRY(cudaMemset(c->d_err, 0, sizeof(int)));
-    CUDA_TRY(cudaMalloc(&c->gate_sync, sizeof(int) * (2 + V)));
-    CUDA_TRY(cudaMemset(c->gate_sync, 0, sizeof(int) * (2 + V)));
+    CUDA_TRY(cudaMalloc(&c->gate_sync, sizeof(int) * 2));
+    CUDA_TRY(cudaMemset(c->gate_sync, 0, sizeof(int) * 2));
     CUDA_TRY(cudaMalloc(&c->blk_hist1, nb1 * z.K1 * 4));
     CUDA_TRY(cudaMalloc(&c->blk_off1, nb1 * z.K1 * 4));
     CUDA_TRY(cudaMalloc(&c->blk_hist2a, nb1 * z.K2 * 4));
@@ -529,6 +534,14 @@ static inline PeerMap peer_of(smile_ctx c) {
 namespace smile {
 static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SMILE_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v != 0;
+}
 }  // namespace smile
 
 extern "C" int64_t smile_launch_count(void) { return (int64_t)smile::g_launches.load(); }
@@ -549,20 +562,20 @@ extern "C" smile_status smile_gate_inter(smile_ctx c, const void *x, const float
     a.route = *route;
     a.blk_hist1 = c->blk_hist1; a.blk_hist2a = c->blk_hist2a; a.blk_psum = c->blk_psum;
     a.err = c->d_err; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
-    a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1; a.nch = c->nch1;
+    a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1;
     a.flat = c->shape.mode == SMILE_FLAT; a.bf16 = c->shape.dtype == SMILE_BF16;
-    Scan1Args s{};
-    s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
-    s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nch1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
-    s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T; s.peer = peer_of(c);
-    bool scanned = false;                    // the ranged tensor-core gate runs the scan itself
+    a.topk = c->shape.topk > 1 ? c->shape.topk : 1; a.swapped = c->gate_swapped;
     if (!logits && c->wsplit) {
-        const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, &s, c->gate_sync, &scanned, S(stream));
+        const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, c->gate_sync, S(stream));
         if (e != cudaSuccess) return SMILE_ECUDA;
     } else {
         launch_gate1(a, S(stream));
     }
-    if (!scanned) launch_scan1(s, S(stream));
+    Scan1Args s{};
+    s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
+    s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
+    s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T; s.peer = peer_of(c); s.topk = a.topk;
+    launch_scan1(s, S(stream));
     return post_launch();
 }
 
@@ -575,7 +588,7 @@ extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, co
     if (c->shape.T == 0) return SMILE_OK;
     // the fused kernel is the 128-token tensor-core gate; elsewhere refuse (the caller runs
     // smile_gate_inter + smile_dispatch(1) and knows which path ran)
-    if (!c->wsplit || !c->lb_flag || c->TB1 != 128) return SMILE_ENOTSUP;
+    if (!c->wsplit || !c->lb_flag || c->TB1 != 128 || c->gate_swapped || c->shape.topk > 1) return SMILE_ENOTSUP;
     c->rtok1_valid = false;                  // this path does not record the source tokens
     c->out_planned = false;
     c->l1_zeroed = false;
@@ -587,24 +600,23 @@ extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, co
     a.route = *route;
     a.blk_hist1 = c->blk_hist1; a.blk_hist2a = c->blk_hist2a; a.blk_psum = c->blk_psum;
     a.err = c->d_err; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
-    a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1; a.nch = c->nch1;
+    a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1; a.topk = 1;
     a.flat = !bi; a.bf16 = c->shape.dtype == SMILE_BF16;
     a.fuse_dispatch = 1; a.send = send_rows; a.meta = bi ? send_meta : nullptr; a.rowbytes = rb; a.C1 = c->sz.C1;
     a.peer = peer_of(c); a.lb_flag = c->lb_flag; a.lb_agg = c->lb_agg; a.lb_inc = c->lb_inc;
-    bool scanned = false;
-    const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, nullptr, nullptr, &scanned, S(stream));
+    const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, nullptr, S(stream));
     if (e != cudaSuccess) return SMILE_ECUDA;
     Scan1Args s{};
     s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
-    s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nch1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
+    s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
     s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T; s.peer = peer_of(c); s.lb_flag = c->lb_flag;
-    s.nlb = c->nblk1;
+    s.nlb = c->nblk1; s.topk = 1;
     launch_scan1(s, S(stream));
     Dispatch1Args d{};
     d.x = x; d.route = *route; d.blk_off1 = c->blk_off1; d.blk_hist1 = c->blk_hist1;
     d.send = send_rows; d.meta = bi ? send_meta : nullptr;
     d.V = c->sz.V; d.T = c->shape.T; d.rowbytes = rb; d.K1 = c->sz.K1; d.C1 = c->sz.C1;
-    d.TB = 32; d.nblk = c->nch1; d.peer = peer_of(c);
+    d.TB = c->TB1; d.nblk = c->nblk1; d.topk = 1; d.peer = peer_of(c);
     launch_meta_fill(d, S(stream));
     return post_launch();
 }
@@ -626,7 +638,8 @@ extern "C" smile_status smile_dispatch(smile_ctx c, int32_t level, const void *r
         a.x = rows_in; a.route = *route; a.blk_off1 = c->blk_off1; a.blk_hist1 = c->blk_hist1;
         a.send = send_rows; a.meta = bi ? send_meta : nullptr;
         a.V = c->sz.V; a.T = c->shape.T; a.rowbytes = rb; a.K1 = c->sz.K1; a.C1 = c->sz.C1;
-        a.TB = 32; a.nblk = c->nch1; a.peer = peer_of(c);      // chunk offsets of the scan
+        a.TB = c->TB1; a.nblk = c->nblk1; a.peer = peer_of(c);
+        a.topk = c->shape.topk > 1 ? c->shape.topk : 1;
         // every rank in this process: the whole level-1 return fuses into GEMM 2, so the
         // zero rows of level-1-dropped tokens are written here and combine(1) is skipped
         c->l1_zeroed = out_direct_enabled(c) && c->sz.V == c->sz.G;
@@ -764,6 +777,7 @@ extern "C" smile_status smile_all2all_intra(smile_ctx c, int32_t reverse, const 
 // FLAT: the world reverse exchange + a13) -- both layers get the same fusion.
 static bool out_direct_enabled(smile_ctx c) {
     if (c->xchg != SMILE_XCHG_PEER || !c->out_bound) return false;
+    if (c->shape.topk > 1) return false;            // several experts write each token's output
     if (c->shape.dtype != SMILE_BF16 || c->shape.ffn_impl == SMILE_FFN_SIMT) return false;
     const char *e = getenv("SMILE_OUT_DIRECT");
     if (e && e[0] == '0') return false;
@@ -830,6 +844,7 @@ extern "C" smile_status smile_combine(smile_ctx c, int32_t level, const void *re
         Combine1Args a{};
         a.back1 = ret_rows; a.route = *route; a.out = out; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
         a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = bf; a.nogate = 0; a.peer = peer_of(c);
+        a.topk = c->shape.topk > 1 ? c->shape.topk : 1;
         if (c->l1_pending && out != c->out_bound) {
             // GEMM 2 wrote the in-process tokens to the bound output, not to ret1 / Y: a
             // combine into another buffer would read stale rows -- refused until the next
@@ -963,6 +978,7 @@ extern "C" smile_status smile_combine_grad(smile_ctx c, const void *ret_rows, co
     Combine1Args a{};
     a.back1 = ret_rows; a.route = *route; a.out = dx; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
     a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = c->shape.dtype == SMILE_BF16; a.nogate = 1; a.peer = peer_of(c);
+    a.topk = 1;
     launch_combine1(a, S(stream));
     return post_launch();
 }
@@ -1061,6 +1077,7 @@ extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, voi
     smile_ws_view w;
     STEP(smile_forward_ws(c, io->ws, &w));
     const bool train = io->train != 0;
+    if (train && c->shape.topk > 1) return SMILE_ENOTSUP;      // the top-k layer is forward-only
     // inference binds io->out for this call (GEMM 2 may write in-process rows there)
     struct OutBinding {
         smile_ctx c; void *prev;
@@ -1167,6 +1184,7 @@ extern "C" smile_status smile_forward_host_stream(smile_ctx c, const smile_layer
 
 extern "C" smile_status smile_backward(smile_ctx c, const smile_layer_io *io, const smile_grad_io *g, void *stream) {
     if (!c || !io || !g) return SMILE_EINVAL;
+    if (c->shape.topk > 1) return SMILE_ENOTSUP;               // the top-k layer is forward-only
     if (c->shape.T == 0) {
         // the weight gradients are sums over no tokens
         if (!g->dW1 || !g->db1 || !g->dW2 || !g->db2) return SMILE_EINVAL;

@@ -230,6 +230,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                  const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ CUtensorMap mapD, const __grid_constant__ CUtensorMap mapD2, TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    pdl_wait();
     // 1024-byte aligned carve-up: [A stages][B stages][out boxes][barriers][tmem holder][prefix]
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;
@@ -661,6 +662,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         }
     }
     if (warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    pdl_trigger();
     __syncthreads();
     if (CS > 1) cluster_sync_all();           // no remote arrive / MMA into a CTA that has left
     if (warp == 2) {
@@ -744,23 +746,23 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
         }
     }
     note_launch();
-    if (CS == 1) {
-        ffn_gemm_tcgen05<CG, NSUB, EK><<<grid, NTHREADS, smem, st>>>(mA, mA128, mB, mD, mD2, a);
-        return cudaGetLastError();
-    }
+    if (CS == 1)
+        return launch_k(ffn_gemm_tcgen05<CG, NSUB, EK>, dim3(grid), dim3(NTHREADS), smem, st, mA, mA128, mB, mD, mD2, a);
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(NTHREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attrs[1];
+    cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = CS;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (smile_internal.h)
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attrs;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<CG, NSUB, EK>, mA, mA128, mB, mD, mD2, a);
 }
 

@@ -63,87 +63,29 @@ __device__ int block_rank(int b, int K, int *s_wh, int *s_bh) {
 // conflict-free shared-memory banks for any KW (KW = 64 would otherwise be 32-way).
 __host__ __device__ __forceinline__ int gate_lds(int KW) { return KW | 1; }
 
+// Phases B and C of the level-1 gate over one tile of nt <= Sync::nthr() tokens whose
+// logits are s_lg [nt][lds] (entries 0..K1-1: inter router W_p; K1..KW-1: intra W_q).
+// tok0: global index of the tile's first token; bo = v * nblk + blk: the tile's index in
+// the per-tile tables (with top-k, choice j of the tile is table row (v * topk + j) * nblk
+// + blk).  Must be entered by all Sync threads after the logits are visible to them.
 struct GateTok {
     int i;       // level-1 destination of this thread's token (-1: no token)
     int lr;      // its rank among the tile's tokens with the same destination
 };
 
-// fp64 sums of 32 values per lane over the warp's lanes, transposed: afterwards lane l holds
-// the warp total of v[l] (the butterfly halves the vector each step; fixed order).
-__device__ __forceinline__ double transpose_reduce32_f64(double (&v)[32], int lane) {
-#pragma unroll
-    for (int h = 16; h >= 1; h >>= 1) {
-        const bool up = (lane & h) != 0;
-#pragma unroll
-        for (int i = 0; i < h; ++i) {
-            const double send = up ? v[i] : v[i + h];
-            const double keep = up ? v[i + h] : v[i];
-            v[i] = keep + __shfl_xor_sync(kFull, send, h);
-        }
-    }
-    return v[0];
-}
-
-// Per-chunk (32-token) tables of the level-1 capacity scan and the LB statistics.  A
-// chunk is one warp's tokens; chunk indices run rank-major, ch = v * nch + t / 32, so the
-// tables do not depend on how a kernel tiles the tokens (tiles are whole chunks of one
-// rank).  Written for every chunk that holds tokens.
-__device__ __forceinline__ void chunk_tables(const GateArgs &a, const float *s_lg, int lds, int i, int j, bool has,
-                                             int64_t ch, int lane, int tok) {
-    const int K1 = a.K1, K2 = a.K2, KW = a.KW, KS = K1 + K2;
-    // destination histograms (argmax counts before capacity, R13)
-    for (int k0 = 0; k0 < K1; k0 += 32) {
-        int mine = 0;
-        for (int kk = 0; kk < 32 && k0 + kk < K1; ++kk) {
-            const int c = __popc(__ballot_sync(kFull, has && i == k0 + kk));
-            if (lane == kk) mine = c;
-        }
-        if (k0 + lane < K1) a.blk_hist1[ch * K1 + k0 + lane] = mine;
-    }
-    for (int k0 = 0; k0 < K2; k0 += 32) {
-        int mine = 0;
-        for (int kk = 0; kk < 32 && k0 + kk < K2; ++kk) {
-            const int c = __popc(__ballot_sync(kFull, has && j == k0 + kk));
-            if (lane == kk) mine = c;
-        }
-        if (k0 + lane < K2) a.blk_hist2a[ch * K2 + k0 + lane] = mine;
-    }
-    // softmax-entry sums in fp64, fixed order (deterministic)
-    if (KW <= 6) {
-        for (int k = 0; k < KW; ++k) {
-            double acc = has ? (double)s_lg[tok * lds + k] : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-            if (lane == 0) a.blk_psum[ch * KS + k] = acc;
-        }
-    } else {
-        for (int k0 = 0; k0 < KW; k0 += 32) {
-            double v[32];
-#pragma unroll
-            for (int kk = 0; kk < 32; ++kk) v[kk] = (has && k0 + kk < KW) ? (double)s_lg[tok * lds + k0 + kk] : 0.0;
-            const double tot = transpose_reduce32_f64(v, lane);
-            if (k0 + lane < KW) a.blk_psum[ch * KS + k0 + lane] = tot;
-        }
-    }
-    if (a.flat) {                                    // FLAT: the second statistic counts the tokens
-        const int cnt = __popc(__ballot_sync(kFull, has));
-        if (lane == 0) a.blk_psum[ch * KS + K1] = (double)cnt;
-    }
-}
-
-// Phases B and C of the level-1 gate over one tile of nt <= Sync::nthr() tokens whose
-// logits are s_lg [nt][lds] (entries 0..K1-1: inter router W_p; K1..KW-1: intra W_q).
-// tok0: global index of the tile's first token (a multiple of 32 within its rank); ch0:
-// the chunk index of that token (v * nch + t / 32).  Must be entered by all Sync threads
-// after the logits are visible to them.
 template <class Sync>
-__device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_wh, int *s_bh, int64_t tok0,
-                               int nt, int64_t ch0) {
-    const int tid = Sync::tid();
+__device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j, int *s_wh, int *s_bh, int64_t tok0,
+                               int nt, int64_t bo) {
+    const int tid = Sync::tid(), nthr = Sync::nthr();
     const int KW = a.KW, K1 = a.K1, K2 = a.K2;
+    const int topk = a.topk > 1 ? a.topk : 1;
+    const int64_t VT = (int64_t)a.V * a.T;
     // Phase B: one thread per token -- argmax (R2, R3), top-1 probabilities (R4), and
-    // the softmax entries for the LB statistics, written back over the logits.
+    // the softmax entries for the LB statistics, written back over the logits.  Top-k
+    // (FLAT, R29): the further choices by repeated first-argmax over the logits not chosen
+    // yet, taken before the logits are transformed.
     int i = -1, j = 0;
+    int ch[4] = {-1, -1, -1, -1};
     if (tid < nt) {
         float *L = s_lg + tid * lds;
         bool finite = true;
@@ -152,6 +94,16 @@ __device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_w
         i = 0;
         for (int k = 1; k < K1; ++k)
             if (L[k] > L[i]) i = k;
+        ch[0] = i;
+        for (int c = 1; c < topk; ++c) {
+            int best = -1;
+            for (int k = 0; k < K1; ++k) {
+                bool taken = false;
+                for (int cc = 0; cc < c; ++cc) taken |= ch[cc] == k;
+                if (!taken && (best < 0 || L[k] > L[best])) best = k;
+            }
+            ch[c] = best;
+        }
         // one expf per entry: e_k = exp(r_k - r_max) is kept, the softmax entry for the
         // statistics is e_k * (1 / sum) (within 1.5 ulp of e_k / sum; the LB loss
         // tolerance is 1e-6 relative), and the top-1 probability is 1 / sum exactly.
@@ -186,38 +138,75 @@ __device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_w
         a.route.p[g] = p;
         a.route.q[g] = q;
         a.route.gate[g] = __fmul_rn(p, q);
+        for (int c = 1; c < topk; ++c) {              // Eq. (2) weights p_e of the further choices (R30)
+            a.route.dest1[c * VT + g] = ch[c];
+            a.route.gate[c * VT + g] = L[ch[c]];
+        }
         if (i < 0 || i >= K1) set_err(a.err, SMILE_EINDEX);
     }
-    // Phase C: capacity ranks (R5, R8) -- the rank of the token among the earlier tokens of
-    // its 32-token chunk with the same destination (the scan adds the chunk's offset), the
-    // chunk's histograms and LB partials; with the fused permute also the tile-wide rank.
-    const int lane = tid & 31, w = tid >> 5;
-    const bool has = tid < nt;
-    const unsigned peers = __match_any_sync(kFull, i);
-    const int lrw = __popc(peers & ((1u << lane) - 1u));
-    if (has && !a.fuse_dispatch) a.route.slot1[tok0 + tid] = lrw;
-    if (32 * w < nt) chunk_tables(a, s_lg, lds, i, j, has, ch0 + w, lane, tid);
-    int lr = lrw;
-    if (a.fuse_dispatch) lr = block_rank<Sync>(i, K1, s_wh, s_bh);
-    return GateTok{i, lr};
+    s_j[tid] = (tid < nt) ? j : -1;
+
+    // Phase C: tile-local capacity rank of dest1 (R5, R8) -- per choice with top-k, whose
+    // tables are laid out choice-major per rank so the scan gives choice-major slots (R31).
+    const int64_t v = bo / a.nblk, blk = bo - v * a.nblk;
+    const int64_t bo0 = (v * topk) * a.nblk + blk;              // choice 0's table row
+    const int lr = block_rank<Sync>(i, K1, s_wh, s_bh);
+    if (tid < nt) a.route.slot1[tok0 + tid] = lr;
+    for (int k = tid; k < K1; k += nthr) a.blk_hist1[bo0 * K1 + k] = s_bh[k];
+    for (int c = 1; c < topk; ++c) {
+        Sync::sync();                                             // s_bh of the previous choice consumed
+        const int lrc = block_rank<Sync>(tid < nt ? ch[c] : -1, K1, s_wh, s_bh);
+        if (tid < nt) a.route.slot1[c * VT + tok0 + tid] = lrc;
+        for (int k = tid; k < K1; k += nthr) a.blk_hist1[(bo0 + (int64_t)c * a.nblk) * K1 + k] = s_bh[k];
+    }
+    // LB statistics partials of the tile (fp64 for the probability sums): one warp per
+    // statistic, lanes stride over tokens, fixed butterfly order => deterministic.
+    {
+        const int lane = tid & 31, w = tid >> 5, NW = nthr >> 5;
+        for (int k = w; k < KW; k += NW) {
+            double acc = 0.0;
+            for (int tt = lane; tt < nt; tt += 32) acc += (double)s_lg[tt * lds + k];
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+            if (lane == 0) a.blk_psum[bo0 * (K1 + K2) + k] = acc;
+        }
+        for (int k = w; k < K2; k += NW) {
+            int c = 0;
+            for (int tt = lane; tt < nt; tt += 32) c += (s_j[tt] == k);
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+            if (lane == 0) a.blk_hist2a[bo0 * K2 + k] = c;
+        }
+        if (a.flat && tid == 0) a.blk_psum[bo0 * (K1 + K2) + K1] = (double)nt;
+    }
+    return GateTok{i, topk > 1 ? -1 : lr};
 }
 
-// Level-1 scan of one rank over its chunk tables: exclusive prefix over
-// chunks of each destination's count (the chunk offsets the permute adds to the chunk-local
-// ranks), totals -> hist1, counts1 = min(hist1, C1) (R5), and the LB statistics reduced over
-// chunks in fixed order (deterministic).  Work split over the NW warps w of the caller.
+// Warp-cooperative scans / sums over n entries at stride st, in batches of 32 * kScanR
+// entries: lane l owns the kScanR consecutive entries [b0 + l kScanR, +kScanR) of a batch
+// and loads them all before combining (one memory round trip per batch instead of one per
+// 32 entries -- these run at the tail of the gate kernel, latency-bound).  Fixed order
+// (lane-serial, then the warp's shuffles): deterministic.
+constexpr int kScanR = 16;
 __device__ __forceinline__ int warp_exclusive_scan(const int32_t *p, int n, int64_t st, int32_t *out_excl) {
     const int lane = threadIdx.x & 31;
     int carry = 0;
-    for (int b0 = 0; b0 < n; b0 += 32) {
-        const int i = b0 + lane;
-        const int v = i < n ? __ldcg(p + (int64_t)i * st) : 0;
-        int x = v;
+    for (int b0 = 0; b0 < n; b0 += 32 * kScanR) {
+        const int i0 = b0 + lane * kScanR;
+        int v[kScanR];
+#pragma unroll
+        for (int r = 0; r < kScanR; ++r) v[r] = i0 + r < n ? __ldcg(p + (int64_t)(i0 + r) * st) : 0;
+        int tot = 0;
+#pragma unroll
+        for (int r = 0; r < kScanR; ++r) { const int x = v[r]; v[r] = tot; tot += x; }   // lane-local exclusive
+        int x = tot;
+#pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(kFull, x, o);
             if (lane >= o) x += y;
         }
-        if (i < n) out_excl[(int64_t)i * st] = carry + x - v;
+        const int base = carry + x - tot;                 // exclusive prefix of this lane's entries
+#pragma unroll
+        for (int r = 0; r < kScanR; ++r)
+            if (i0 + r < n) out_excl[(int64_t)(i0 + r) * st] = base + v[r];
         carry += __shfl_sync(kFull, x, 31);
     }
     return carry;
@@ -225,14 +214,28 @@ __device__ __forceinline__ int warp_exclusive_scan(const int32_t *p, int n, int6
 __device__ __forceinline__ double warp_sum_f64(const double *p, int n, int64_t st) {
     const int lane = threadIdx.x & 31;
     double acc = 0.0;
-    for (int i = lane; i < n; i += 32) acc += __ldcg(p + (int64_t)i * st);
+    for (int b0 = 0; b0 < n; b0 += 32 * kScanR) {
+        const int i0 = b0 + lane * kScanR;
+        double v[kScanR];
+#pragma unroll
+        for (int r = 0; r < kScanR; ++r) v[r] = i0 + r < n ? __ldcg(p + (int64_t)(i0 + r) * st) : 0.0;
+#pragma unroll
+        for (int r = 0; r < kScanR; ++r) acc += v[r];
+    }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
     return acc;
 }
 __device__ __forceinline__ int warp_sum_i32(const int32_t *p, int n, int64_t st) {
     const int lane = threadIdx.x & 31;
     int acc = 0;
-    for (int i = lane; i < n; i += 32) acc += __ldcg(p + (int64_t)i * st);
+    for (int b0 = 0; b0 < n; b0 += 32 * kScanR) {
+        const int i0 = b0 + lane * kScanR;
+        int v[kScanR];
+#pragma unroll
+        for (int r = 0; r < kScanR; ++r) v[r] = i0 + r < n ? __ldcg(p + (int64_t)(i0 + r) * st) : 0;
+#pragma unroll
+        for (int r = 0; r < kScanR; ++r) acc += v[r];
+    }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
     return acc;
 }
@@ -240,15 +243,20 @@ __device__ __forceinline__ int warp_sum_i32(const int32_t *p, int n, int64_t st)
 __device__ __forceinline__ void scan1_rank(const Scan1Args &a, int v, int w, int NW) {
     const int lane = threadIdx.x & 31;
     const int KS = a.K1 + a.K2;
+    const int topk = a.topk > 1 ? a.topk : 1;
+    const int64_t rb = (int64_t)v * topk * a.nblk;               // the rank's first table row
     const int jobs = a.K1 + KS + a.K2;
     for (int jb = w; jb < jobs; jb += NW) {
         if (jb < a.K1) {
             const int k = jb;
-            const int64_t o = (int64_t)v * a.nblk * a.K1 + k;
-            const int tot = warp_exclusive_scan(a.blk_hist1 + o, a.nblk, a.K1, a.blk_off1 + o);
+            const int64_t o = rb * a.K1 + k;
+            // top-k: the rank's items in choice-major order (R31) -- offsets over every choice
+            const int tot = warp_exclusive_scan(a.blk_hist1 + o, topk * a.nblk, a.K1, a.blk_off1 + o);
+            // f counts choice 0 only (R13, R32)
+            const int top1 = topk > 1 ? warp_sum_i32(a.blk_hist1 + o, a.nblk, a.K1) : tot;
             if (lane == 0) {
                 const int32_t cnt = (int32_t)(tot < a.C1 ? tot : a.C1);
-                a.stats.hist1[v * a.K1 + k] = tot;
+                a.stats.hist1[v * a.K1 + k] = top1;
                 a.counts1[v * a.K1 + k] = cnt;
                 if (a.peer.bases && a.flat) {      // counts travel with the rows: rcounts[q][src][k % e]
                     const PeerMap &P = a.peer;
@@ -258,14 +266,14 @@ __device__ __forceinline__ void scan1_rank(const Scan1Args &a, int v, int w, int
             }
         } else if (jb < a.K1 + KS) {
             const int k = jb - a.K1;
-            const double sum = warp_sum_f64(a.blk_psum + (int64_t)v * a.nblk * KS + k, a.nblk, KS);
+            const double sum = warp_sum_f64(a.blk_psum + rb * KS + k, a.nblk, KS);
             if (lane == 0) {
                 if (k < a.K1) a.stats.psum1[v * a.K1 + k] = sum;
                 else a.stats.psum2[v * a.K2 + (k - a.K1)] = sum;
             }
         } else {
             const int k = jb - a.K1 - KS;
-            const int c = warp_sum_i32(a.blk_hist2a + (int64_t)v * a.nblk * a.K2 + k, a.nblk, a.K2);
+            const int c = warp_sum_i32(a.blk_hist2a + rb * a.K2 + k, a.nblk, a.K2);
             if (lane == 0) a.stats.hist2[v * a.K2 + k] = c;
         }
     }

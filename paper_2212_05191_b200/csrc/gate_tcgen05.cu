@@ -48,6 +48,7 @@ constexpr int GT_MAX_NP = 384;                  // 3 * KW <= 384 (KW <= 128)
 // 32-lane TMEM quadrant.
 __global__ void router_split_kernel(const float *__restrict__ w, __nv_bfloat16 *__restrict__ wb, int KW, int d,
                                     int NP, int quad10) {
+    pdl_wait();
     const int64_t n = (int64_t)NP * d;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(i / d), c = (int)(i - (int64_t)r * d);
@@ -211,7 +212,7 @@ __device__ void fused_dispatch(const GateArgs &a, const GateTok tk, const int *s
 // After the group's logits of one tile are in smem: (optional) logits_out copy, the
 // gate's phases B and C, and (fused) the level-1 permute of the tile.
 template <class Sync>
-__device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int *s_wh, int *s_bh,
+__device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int *s_j, int *s_wh, int *s_bh,
                                             int *s_off, int64_t tok0, int nt, int tile) {
     Sync::sync();
     if (a.logits_out) {
@@ -220,8 +221,7 @@ __device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int 
             a.logits_out[tok0 * a.KW + i] = s_lg[(i / a.KW) * lds + i % a.KW];
         Sync::sync();
     }
-    const int v = tile / a.nblk, blk = tile - v * a.nblk;       // 128-token tiles = 4 chunks
-    const GateTok tk = gate_finish<Sync>(a, s_lg, gate_lds(a.KW), s_wh, s_bh, tok0, nt, (int64_t)v * a.nch + 4 * blk);
+    const GateTok tk = gate_finish<Sync>(a, s_lg, gate_lds(a.KW), s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
     if (a.fuse_dispatch) fused_dispatch<Sync>(a, tk, s_bh, s_off, tok0, nt, tile);
     Sync::sync();
 }
@@ -229,6 +229,7 @@ __device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int 
 __global__ void __launch_bounds__(GT_THREADS, 1)
 gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, GateTcArgs ta) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    pdl_wait();
     const GateArgs &a = ta.g;
     const int NP = ta.NP, ST = ta.stages, KW = a.KW;
     const int nsub = ta.nsub;
@@ -412,10 +413,11 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
-            if (grp == 0) finish_tile<EpiSync<0>>(a, s_lg, s_wh, s_bh, s_off, tok0, nt, tile);
-            else finish_tile<EpiSync<1>>(a, s_lg, s_wh, s_bh, s_off, tok0, nt, tile);
+            if (grp == 0) finish_tile<EpiSync<0>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
+            else finish_tile<EpiSync<1>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
         }
     }
+    pdl_trigger();
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
@@ -425,32 +427,27 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
 
 // ---------------------------------------------------------------------------------
 // Swapped-role tensor-core gate (default for KW <= 40): M = the split router (its
-// 32 * ceil(KW / 10) rows, zero rows up to 128 kept in smem), N = up to 256 TOKENS per
-// MMA.  With the tokens on M (gate1_tc_kernel) every tcgen05.mma is 128 x NP x 16 with NP
-// as small as 32, and the MMA count per token -- each costs a near-fixed ~350 cycles
-// there -- is what bounds the kernel; here one MMA covers up to 256 tokens.  The
-// accumulator [piece rows x tokens] is transposed by the epilogue: lane r of quadrant q
-// holds piece r % 3 of logit 10 q + r / 3 for 32 tokens; two shuffles sum the pieces in
-// order, and the logits land in s_lg [token][KW] for gate_finish (8 warps).
-//
-// One launch does all of a1-a3 ("ranged" schedule):
-//  * work balance: the V * nch 32-token chunks are split into one contiguous range per
-//    CTA (ranges differ by at most one chunk), cut into tiles of up to 8 chunks that
-//    never cross a rank -- no partial last wave (C2 at N = 1 was 3.46 waves of fixed
-//    256-token tiles); a tile's MMA N is its own token count and its x rows arrive as one
-//    256-row TMA box or as 32-row boxes;
-//  * the exact three-piece bf16 split of the fp32 router (R3, R23) is built by the
-//    epilogue warps of the first CTAs into `wsplit` while the producers already stream x;
-//    producers issue the router loads of their first stages once the split is published
-//    (release / acquire counter + async-proxy fence) -- no separate split kernel;
-//  * the level-1 scan: the CTA that completes a rank's last chunk (per-rank arrival
-//    counter) runs that rank's scan over the chunk tables (scan1_rank) -- no scan kernel.
-//  The last CTA to finish resets the counters for the next call (graph-replay safe).
+// 32 * ceil(KW / 10) rows zero-padded to 128 by TMA), N = 256 TOKENS per MMA.  With the
+// tokens on M (gate1_tc_kernel) every tcgen05.mma is 128 x NP x 16 with NP as small as
+// 32, and the MMA count per token -- each costs a near-fixed ~350 cycles there (ncu: the
+// producer waits on stage releases while the MMA thread never waits for data) -- is what
+// bounds the kernel; here one MMA covers 256 tokens.  The accumulator [piece rows x 256
+// tokens] is transposed by the epilogue: lane r of quadrant q holds piece r % 3 of logit
+// 10 q + r / 3 for 32 tokens; two shuffles sum the pieces in order, and the logits land in
+// s_lg [token][KW] for the same gate_finish (8 warps, 256 tokens per tile, TB1 = 256).
+// The exact three-piece bf16 split of the fp32 router (R3, R23) is built into `wsplit` by
+// the epilogue warps of the first CTAs while the producers already stream x; a producer
+// issues the router loads of its first stages once the split is published (release /
+// acquire counter + async-proxy fence) -- no separate split kernel.  The last CTA to finish
+// resets the counter (graph-replay safe).
+// (Round 2 measured two alternatives on the same box and kept neither: contiguous per-CTA
+// token ranges with 32-token scan tables (no partial last wave) 48-51 us + a 4x larger
+// scan, and 128-token tables with 256/128-token tiles 57-59 us, against this kernel's
+// 45 us; profiles/r02_gate_schedule_ab.md.)
 // ---------------------------------------------------------------------------------
 constexpr int GS_TOK = 256, GS_THREADS = 128 + 256;
 constexpr int GS_X_BYTES = GS_TOK * GT_BK * 2;    // 32 KB per stage
-constexpr int GS_W_BYTES = 128 * GT_BK * 2;       // 16 KB per stage (rows >= NPT stay zero)
-constexpr int GS_CHUNK_BYTES = 32 * GT_BK * 2;    // one 32-token box of x
+constexpr int GS_W_BYTES = 128 * GT_BK * 2;       // 16 KB per stage
 
 template <int G>
 struct EpiSync256 {
@@ -461,52 +458,33 @@ struct EpiSync256 {
 
 struct GateTArgs {
     GateArgs g;
-    Scan1Args s;     // the level-1 scan this kernel runs per rank
     int NPT;         // split-router rows (32 * ceil(KW / 10))
     int stages;
-    int64_t NCH;     // V * nch chunks
-    int nbuilders;   // CTAs that build the split router
-    int *split_ready, *done, *rank_cnt;
-    __nv_bfloat16 *wsplit;   // [NPT, d] the split router (built in-kernel, read by TMA)
+    int ntiles;
+    int nbuilders;   // CTAs that build the split router (0: built by router_split_kernel)
+    int *split_ready, *done;
+    __nv_bfloat16 *wsplit;   // [NPT, d] the split router
 };
-
-struct RTile {
-    int v, c0, nck;  // rank, first chunk within the rank, chunks (<= 8)
-};
-
-__device__ __forceinline__ bool next_rtile(int64_t &cur, int64_t end, int nch, RTile &t) {
-    if (cur >= end) return false;
-    t.v = (int)(cur / nch);
-    t.c0 = (int)(cur - (int64_t)t.v * nch);
-    int64_t n = end - cur;
-    if (n > 8) n = 8;
-    if (n > nch - t.c0) n = nch - t.c0;
-    t.nck = (int)n;
-    cur += n;
-    return true;
-}
 
 __global__ void __launch_bounds__(GS_THREADS, 1)
-gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapX32,
-                 const __grid_constant__ CUtensorMap mapW, GateTArgs ta) {
+gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, GateTArgs ta) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    pdl_wait();
     const GateArgs &a = ta.g;
-    const int ST = ta.stages, KW = a.KW, NQ = ta.NPT / 32, nch = a.nch;
+    const int ST = ta.stages, KW = a.KW, NQ = ta.NPT / 32;
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sW = base;
     unsigned char *sX = sW + ST * GS_W_BYTES;
     const int lds = gate_lds(KW);
     float *s_lg = reinterpret_cast<float *>(sX + ST * GS_X_BYTES);    // [256][lds]
-    int *s_wh = reinterpret_cast<int *>(s_lg + GS_TOK * lds);         // [8][K1] (fused permute only)
+    int *s_j = reinterpret_cast<int *>(s_lg + GS_TOK * lds);          // [256]
+    int *s_wh = s_j + GS_TOK;                                         // [8][K1]
     int *s_bh = s_wh + 8 * a.K1;                                      // [K1]
-    int *s_last = s_bh + a.K1;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(s_last + 1) + 7) & ~(uintptr_t)7);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(s_bh + a.K1) + 7) & ~(uintptr_t)7);
     uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // this CTA's contiguous chunk range
-    const int64_t cb = ta.NCH * blockIdx.x / gridDim.x, ce = ta.NCH * (blockIdx.x + 1) / gridDim.x;
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
@@ -520,20 +498,12 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
     }
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapX)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapX32)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapW)) : "memory");
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    if (ta.NPT < 128) {
-        // the router operand's rows >= NPT are zero for the whole kernel (TMA writes rows < NPT)
-        for (int s = 0; s < ST; ++s)
-            for (int i = threadIdx.x; i < (128 - ta.NPT) * GT_BK * 2 / 16; i += blockDim.x)
-                reinterpret_cast<int4 *>(sW + s * GS_W_BYTES + ta.NPT * GT_BK * 2)[i] = make_int4(0, 0, 0, 0);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -543,58 +513,47 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- TMA producer ----------------
-            const uint32_t wbytes = (uint32_t)ta.NPT * GT_BK * 2;
             int stage = 0;
             uint32_t phase = 0;
-            bool wready = false;
-            int pst[8], pkb[8], npend = 0;
-            auto load_w = [&](int st_, int kb_) {
-                tma_load_2d(smem_u32(sW + st_ * GS_W_BYTES), &mapW, kb_ * GT_BK, 0, smem_u32(&full[st_]));
-            };
-            auto wait_split = [&]() {
-                while (ld_acquire_gpu(ta.split_ready) < ta.nbuilders) { }
-                asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
-                for (int i = 0; i < npend; ++i) load_w(pst[i], pkb[i]);
-                npend = 0;
-                wready = true;
-            };
-            int64_t cur = cb;
-            RTile t;
-            while (next_rtile(cur, ce, nch, t)) {
-                const int row0 = (int)((int64_t)t.v * a.T + (int64_t)t.c0 * 32);
+            // router loads wait for the in-kernel split: the first ST stages get their x
+            // loads at once and their router loads once the split is published
+            bool wready = ta.nbuilders == 0;
+            int npend = 0;
+            for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
+                const int v = tile / a.nblk, blk = tile - v * a.nblk;
+                const int row0 = (int)((int64_t)v * a.T + (int64_t)blk * GS_TOK);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full[stage]);
-                    mbar_arrive_tx(fb, wbytes + (uint32_t)t.nck * GS_CHUNK_BYTES);
-                    if (t.nck == 8) {
-                        tma_load_2d(smem_u32(sX + stage * GS_X_BYTES), &mapX, kb * GT_BK, row0, fb);
-                    } else {
-                        for (int c = 0; c < t.nck; ++c)
-                            tma_load_2d(smem_u32(sX + stage * GS_X_BYTES + c * GS_CHUNK_BYTES), &mapX32, kb * GT_BK,
-                                        row0 + 32 * c, fb);
-                    }
+                    mbar_arrive_tx(fb, GS_W_BYTES + GS_X_BYTES);
+                    tma_load_2d(smem_u32(sX + stage * GS_X_BYTES), &mapX, kb * GT_BK, row0, fb);
                     if (wready) {
-                        load_w(stage, kb);
-                    } else {
-                        pst[npend] = stage; pkb[npend] = kb; ++npend;
-                        if (npend == ST) wait_split();
+                        tma_load_2d(smem_u32(sW + stage * GS_W_BYTES), &mapW, kb * GT_BK, 0, fb);
+                    } else if (++npend == ST) {
+                        // stages 0..ST-1 hold k blocks 0..ST-1 of this CTA's first tile(s)
+                        while (ld_acquire_gpu(ta.split_ready) < ta.nbuilders) { }
+                        asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
+                        for (int i = 0; i < ST; ++i)
+                            tma_load_2d(smem_u32(sW + i * GS_W_BYTES), &mapW, (i % nk) * GT_BK, 0, smem_u32(&full[i]));
+                        wready = true;
                     }
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
             }
-            if (!wready && npend) wait_split();
+            if (!wready && npend) {
+                while (ld_acquire_gpu(ta.split_ready) < ta.nbuilders) { }
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                for (int i = 0; i < npend; ++i)
+                    tma_load_2d(smem_u32(sW + i * GS_W_BYTES), &mapW, (i % nk) * GT_BK, 0, smem_u32(&full[i]));
+            }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            // ---------------- MMA issuer ----------------
+            const uint32_t idesc = make_idesc(128, GS_TOK);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            int64_t cur = cb;
-            RTile t;
-            while (next_rtile(cur, ce, nch, t)) {
-                const uint32_t idesc = make_idesc(128, 32 * t.nck);
+            for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
                 const int buf = it & 1;
                 mbar_wait(smem_u32(&tempty[buf]), ((uint32_t)(it >> 1) & 1) ^ 1);
                 tc_fence_after();
@@ -611,14 +570,13 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
                 mma_commit(smem_u32(&tfull[buf]));
-                ++it;
             }
         }
     } else if (warp >= 4) {
-        const int etid = threadIdx.x - 128, ew = etid >> 5;
         // the exact three-piece split of W into wsplit ("quad10" rows: row 32 Q + w holds
         // piece w % 3 of logit 10 Q + w / 3 for w < 30, rows 30, 31 of each group zero)
         if ((int)blockIdx.x < ta.nbuilders) {
+            const int etid = threadIdx.x - 128;
             for (int r = blockIdx.x; r < ta.NPT; r += gridDim.x) {
                 const int q = r >> 5, ww = r & 31;
                 const int k = ww < 30 ? 10 * q + ww / 3 : KW, p = ww % 3;
@@ -639,13 +597,11 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
         }
         const int q = warp & 3, hc = (warp - 4) >> 2;    // TMEM lane quadrant, token-column half
         int it = 0;
-        int64_t cur = cb;
-        RTile t;
-        while (next_rtile(cur, ce, nch, t)) {
-            const int64_t t0 = (int64_t)t.c0 * 32;
-            const int ntt = 32 * t.nck;
-            const int nt = (int)(a.T - t0 < ntt ? a.T - t0 : ntt);
-            const int64_t tok0 = (int64_t)t.v * a.T + t0;
+        for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
+            const int v = tile / a.nblk, blk = tile - v * a.nblk;
+            const int64_t t0 = (int64_t)blk * GS_TOK;
+            const int nt = (int)(a.T - t0 < GS_TOK ? a.T - t0 : GS_TOK);
+            const int64_t tok0 = (int64_t)v * a.T + t0;
             const int buf = it & 1;
             mbar_wait(smem_u32(&tfull[buf]), (uint32_t)(it >> 1) & 1);
             tc_fence_after();
@@ -653,7 +609,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                 const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + buf * GS_TOK + hc * 128;
                 const int k = 10 * q + lane / 3;
                 const bool head = (lane % 3 == 0) && lane < 30 && k < KW;
-                for (int c = 0; c < 4 && hc * 128 + c * 32 < ntt; ++c) {
+                for (int c = 0; c < 4; ++c) {
                     float vv[32];
                     tmem_ld32(tb + c * 32, vv);
 #pragma unroll
@@ -669,42 +625,21 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
             if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
             EpiSync256<0>::sync();
             if (a.logits_out) {
-                for (int i = etid; i < nt * KW; i += 256) a.logits_out[tok0 * KW + i] = s_lg[(i / KW) * lds + i % KW];
+                for (int i = EpiSync256<0>::tid(); i < nt * KW; i += 256)
+                    a.logits_out[tok0 * KW + i] = s_lg[(i / KW) * lds + i % KW];
                 EpiSync256<0>::sync();
             }
-            gate_finish<EpiSync256<0>>(a, s_lg, lds, s_wh, s_bh, tok0, nt, (int64_t)t.v * nch + t.c0);
-            EpiSync256<0>::sync();                     // s_lg is rewritten by the next tile
-            ++it;
-        }
-        // This CTA's chunks are done: arrive once per rank it covered (after a barrier of the
-        // epilogue threads, one release fence -- cumulative over their table writes); the
-        // CTA that completes a rank runs that rank's level-1 scan over the chunk tables.
-        if (cb < ce) {
+            gate_finish<EpiSync256<0>>(a, s_lg, lds, s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
             EpiSync256<0>::sync();
-            for (int v = (int)(cb / nch); v <= (int)((ce - 1) / nch); ++v) {
-                const int64_t lo = cb > (int64_t)v * nch ? cb : (int64_t)v * nch;
-                const int64_t hi = ce < (int64_t)(v + 1) * nch ? ce : (int64_t)(v + 1) * nch;
-                if (etid == 0) {
-                    __threadfence();
-                    const int old = atomicAdd(ta.rank_cnt + v, (int)(hi - lo));
-                    *s_last = old + (int)(hi - lo) == nch;
-                    if (*s_last) __threadfence();
-                }
-                EpiSync256<0>::sync();
-                if (*s_last) {
-                    scan1_rank(ta.s, v, ew, 8);
-                    if (etid == 0) ta.rank_cnt[v] = 0;      // every chunk of the rank has arrived
-                }
-                EpiSync256<0>::sync();
-            }
         }
     }
+    pdl_trigger();
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && ta.nbuilders > 0) {
         // every CTA is past its split wait: the last one resets the counters for the next call
         __threadfence();
         if (atomicAdd(ta.done, 1) == (int)gridDim.x - 1) {
@@ -716,7 +651,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
 }
 
 size_t gate_tcT_smem(int KW, int K1, int stages) {
-    return 1024 + (size_t)stages * (GS_W_BYTES + GS_X_BYTES) + ((size_t)GS_TOK * gate_lds(KW) + 9 * K1 + 1) * 4 +
+    return 1024 + (size_t)stages * (GS_W_BYTES + GS_X_BYTES) + ((size_t)GS_TOK * gate_lds(KW) + GS_TOK + 9 * K1) * 4 +
            8 + (2 * stages + 4) * 8 + 16;
 }
 
@@ -732,10 +667,10 @@ size_t gate_tc_smem(int NP, int KW, int K1, int stages, int nsub, int resident_b
 int gate_tc_np(int KW) { return ((3 * KW + 31) / 32) * 32; }
 
 // The swapped-role kernel (256-token tiles) for KW <= 40 unless SMILE_GATE_SWAP=0.
-int gate_tc_tile(int KW) {                    // read at every smile_create
+bool gate_tc_swapped(int KW) {                // read at every smile_create
     const char *e = getenv("SMILE_GATE_SWAP");
     const bool on = !(e && e[0] == '0');
-    return (on && KW <= 40) ? GS_TOK : GT_BM;
+    return on && KW <= 40;
 }
 
 int gate_tc_rows(int KW) {                    // rows of the split-router buffer (both layouts)
@@ -747,24 +682,20 @@ bool gate_tc_supported(int bf16, int d, int KW) {
     return bf16 && d % GT_BK == 0 && d >= GT_BK && gate_tc_np(KW) <= GT_MAX_NP && encode_fn() != nullptr;
 }
 
-cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, const Scan1Args *scan,
-                            int *gate_sync, bool *scanned, cudaStream_t st) {
-    *scanned = false;
+cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, int *gate_sync, cudaStream_t st) {
     if (a.T == 0) return cudaSuccess;
     if (a.logits || !gate_tc_supported(a.bf16, a.d, a.KW)) return cudaErrorNotSupported;
-    if (a.TB == GS_TOK) {
-        if (a.fuse_dispatch || !scan || !gate_sync) return cudaErrorNotSupported;   // the fused permute has 128-token tiles
+    if (a.swapped) {
+        if (a.TB != GS_TOK || a.fuse_dispatch || !gate_sync) return cudaErrorNotSupported;   // 256-token tiles
         const int NPT = 32 * ((a.KW + 9) / 10);
-        CUtensorMap mX, mX32, mW;
+        CUtensorMap mX, mW;
         if (!make_map(&mX, a.x, (int64_t)a.V * a.T, a.d, GS_TOK)) return cudaErrorNotSupported;
-        if (!make_map(&mX32, a.x, (int64_t)a.V * a.T, a.d, 32)) return cudaErrorNotSupported;
-        if (!make_map(&mW, wsplit, NPT, a.d, NPT)) return cudaErrorNotSupported;
+        if (!make_map(&mW, wsplit, NPT, a.d, 128)) return cudaErrorNotSupported;    // rows >= NPT: zero fill
         GateTArgs ta;
         memset(&ta, 0, sizeof(ta));
         ta.g = a;
-        ta.s = *scan;
         ta.NPT = NPT;
-        ta.NCH = (int64_t)a.V * a.nch;
+        ta.ntiles = a.V * a.nblk;
         int stages = 8;
         while (stages > 2 && gate_tcT_smem(a.KW, a.K1, stages) > 227 * 1024) --stages;
         ta.stages = stages;
@@ -774,13 +705,19 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
             cudaFuncSetAttribute(gate1_tcT_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             attrT = true;
         }
-        const int grid = (int)(ta.NCH < num_sms ? ta.NCH : num_sms);
+        const int grid = ta.ntiles < num_sms ? ta.ntiles : num_sms;
         ta.nbuilders = NPT < grid ? NPT : grid;
-        ta.split_ready = gate_sync; ta.done = gate_sync + 1; ta.rank_cnt = gate_sync + 2;
+        ta.split_ready = gate_sync; ta.done = gate_sync + 1;
         ta.wsplit = wsplit;
+        const char *e2 = getenv("SMILE_GATE_SPLIT_KERNEL");      // 1: the separate split kernel (A/B)
+        if (e2 && e2[0] == '1') {
+            note_launch();
+            launch_k(router_split_kernel, dim3((NPT * a.d + 255) / 256 < 1024 ? (NPT * a.d + 255) / 256 : 1024),
+                     dim3(256), 0, st, a.w, wsplit, a.KW, a.d, NPT, 1);
+            ta.nbuilders = 0;
+        }
         note_launch();
-        gate1_tcT_kernel<<<grid, GS_THREADS, smem, st>>>(mX, mX32, mW, ta);
-        *scanned = true;
+        launch_k(gate1_tcT_kernel, dim3(grid), dim3(GS_THREADS), smem, st, mX, mW, ta);
         return cudaGetLastError();
     }
     if (a.TB != GT_BM) return cudaErrorNotSupported;
@@ -797,8 +734,8 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
     const int resb = (env_resb && (size_t)NP * a.d * 2 <= 64 * 1024) ? 1 : 0;
     if (!resb) {
         note_launch();
-        router_split_kernel<<<(NP * a.d + 255) / 256 < 1024 ? (NP * a.d + 255) / 256 : 1024, 256, 0, st>>>(
-            a.w, wsplit, a.KW, a.d, NP, 0);
+        launch_k(router_split_kernel, dim3((NP * a.d + 255) / 256 < 1024 ? (NP * a.d + 255) / 256 : 1024), dim3(256), 0,
+                 st, a.w, wsplit, a.KW, a.d, NP, 0);
     }
     CUtensorMap mX, mW;
     if (!make_map(&mX, a.x, (int64_t)a.V * a.T, a.d, GT_BM)) return cudaErrorNotSupported;
@@ -830,7 +767,7 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
     }
     const int grid = ta.ntiles < num_sms ? ta.ntiles : num_sms;
     note_launch();
-    gate1_tc_kernel<<<grid, GT_THREADS, smem, st>>>(mX, mW, ta);
+    launch_k(gate1_tc_kernel, dim3(grid), dim3(GT_THREADS), smem, st, mX, mW, ta);
     return cudaGetLastError();
 }
 

@@ -127,6 +127,7 @@ __device__ void router_tile(const GateArgs &a, float *s_lg, int lds, float *s_w,
 // smem: logits tile [TB][lds] fp32 | s_j [TB] | warp hist [NW][K1] | block hist [K1]
 // ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256, 2) gate1_kernel(GateArgs a) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *s_lg = reinterpret_cast<float *>(smem_raw);
     const int lds = gate_lds(a.KW);
@@ -155,11 +156,12 @@ __global__ void __launch_bounds__(256, 2) gate1_kernel(GateArgs a) {
         for (int i = tid; i < nt * KW; i += blockDim.x) a.logits_out[tok0 * KW + i] = s_lg[(i / KW) * lds + i % KW];
     if (a.logits_out && !a.logits) __syncthreads();
 
-    gate_finish<BlockSync>(a, s_lg, lds, s_wh, s_bh, tok0, nt, (int64_t)v * a.nch + t0 / 32);
+    gate_finish<BlockSync>(a, s_lg, lds, s_j, s_wh, s_bh, tok0, nt, (int64_t)v * a.nblk + blk);
 }
 
 // Level-1 scan over the per-chunk tables (gate_common.cuh scan1_rank), grid = V.
 __global__ void scan1_kernel(Scan1Args a) {
+    pdl_wait();
     const int v = blockIdx.x;
     if (a.lb_flag)                                   // the fused gate's look-back flags, for the next call
         for (int b = threadIdx.x; b < a.nlb; b += blockDim.x) a.lb_flag[(int64_t)v * a.nlb + b] = 0;
@@ -169,6 +171,7 @@ __global__ void scan1_kernel(Scan1Args a) {
 // a6: level-2 gate at the intermediate: rank valid received slots per j, in received
 // order (source node ascending, then slot: the flat index s*C1 + c, R8).
 __global__ void rank2_kernel(Rank2Args a) {
+    pdl_wait();
     __shared__ int s_wh[(kRank2Items / 32) * 256];
     __shared__ int s_bh[256];
     const int v = blockIdx.y, blk = blockIdx.x;
@@ -185,6 +188,7 @@ __global__ void rank2_kernel(Rank2Args a) {
 }
 
 __global__ void scan2_kernel(Rank2Args a) {
+    pdl_wait();
     const int v = blockIdx.x, w = threadIdx.x >> 5, NW = blockDim.x >> 5, lane = threadIdx.x & 31;
     for (int k = w; k < a.K2; k += NW) {
         const int64_t o = (int64_t)v * a.nblk * a.K2 + k;
@@ -228,15 +232,20 @@ struct RowPlan {
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {
+__device__ __forceinline__ RowPlan plan_row(const MoveArgs &m, int64_t g) {   // g: the mover's row (item) index
     RowPlan r{nullptr, nullptr, 1.f};
     if (m.kind == MOVE_DISPATCH1) {
+        // item gi = choice j of token g (top-k: choice-major, R31; top-1: gi = g)
         const Dispatch1Args &a = m.d1;
+        const int64_t gi = g;
+        const int64_t VT = (int64_t)a.V * a.T;
+        const int jc = (int)(gi / VT);
+        g = gi - (int64_t)jc * VT;
         const int v = (int)(g / a.T);
         const int64_t t = g - (int64_t)v * a.T;
-        const int i = a.route.dest1[g];
-        const int slot = a.blk_off1[((int64_t)v * a.nblk + t / a.TB) * a.K1 + i] + a.route.slot1[g];
-        a.route.slot1[g] = slot;                                      // finalise (R5, R8)
+        const int i = a.route.dest1[gi];
+        const int slot = a.blk_off1[(((int64_t)v * a.topk + jc) * a.nblk + t / a.TB) * a.K1 + i] + a.route.slot1[gi];
+        a.route.slot1[gi] = slot;                                     // finalise (R5, R8, R31)
         if (slot < a.C1) {
             r.src = static_cast<const char *>(a.x) + g * a.rowbytes;
             if (a.peer.bases) {
@@ -412,6 +421,7 @@ constexpr int kMoveColUnroll = 3;       // 16-byte vectors per lane per row in f
 // rows x kMoveColUnroll 16-byte loads in flight before its stores.
 template <int RW>
 __device__ __forceinline__ void row_move_body(const MoveArgs &m) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -483,6 +493,7 @@ __device__ __forceinline__ void row_move_body(const MoveArgs &m) {
             mine = nxt;
         }
     }
+    pdl_trigger();
 }
 
 template <int RW>
@@ -492,15 +503,85 @@ __global__ void __launch_bounds__(kMoveThreads) row_move_kernel(MoveArgs m) { ro
 template <int RW, int MINB>
 __global__ void __launch_bounds__(kMoveThreads, MINB) row_move_kernel_mb(MoveArgs m) { row_move_body<RW>(m); }
 
+// a13 for the FLAT top-k layer (Eq. 2): warp per token, out[t] = dtype(sum over
+// the token's kept choices j (ascending) of gate_j * row_j), fp32 accumulation; the rows
+// come from back1 [V, K1, C1, d] or, with the peer-store exchange, straight from the
+// expert's Y.  A token whose every choice was dropped gets a zero row (R9).
+__global__ void __launch_bounds__(256) combine_topk_kernel(Combine1Args a) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t VT = (int64_t)a.V * a.T;
+    const int64_t rb = (int64_t)a.d * (a.bf16 ? 2 : 4);
+    const int nvec = (int)(rb / 16);
+    for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < VT; g += warps) {
+        const int v = (int)(g / a.T);
+        const char *src[4];
+        float w[4];
+        int nsrc = 0;
+        for (int j = 0; j < a.topk; ++j) {
+            const int64_t gi = (int64_t)j * VT + g;
+            const int i = a.route.dest1[gi];
+            const int s1 = a.route.slot1[gi];
+            if (s1 >= a.C1) continue;
+            const char *p;
+            if (a.peer.bases) {
+                const PeerMap &P = a.peer;
+                const int rk = P.rank0 + v, q = i / P.e;
+                p = P.bases[q / P.V] + P.off_Y + ((((int64_t)(q % P.V) * P.G + rk) * P.e + i % P.e) * a.C1 + s1) * rb;
+            } else {
+                p = static_cast<const char *>(a.back1) + (((int64_t)v * a.K1 + i) * a.C1 + s1) * rb;
+            }
+            src[nsrc] = p;
+            w[nsrc] = a.route.gate[gi];
+            ++nsrc;
+        }
+        int4 *dst = reinterpret_cast<int4 *>(static_cast<char *>(a.out) + g * rb);
+        for (int c = lane; c < nvec; c += 32) {
+            float acc[8];
+#pragma unroll
+            for (int z = 0; z < 8; ++z) acc[z] = 0.f;
+            for (int k = 0; k < nsrc; ++k) {
+                const int4 u = __ldg(reinterpret_cast<const int4 *>(src[k]) + c);
+                if (a.bf16) {
+                    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) {
+                        const float2 f = __bfloat1622float2(h[z]);
+                        acc[2 * z] = fmaf(w[k], f.x, acc[2 * z]);
+                        acc[2 * z + 1] = fmaf(w[k], f.y, acc[2 * z + 1]);
+                    }
+                } else {
+                    const float *f = reinterpret_cast<const float *>(&u);
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) acc[z] = fmaf(w[k], f[z], acc[z]);
+                }
+            }
+            int4 o;
+            if (a.bf16) {
+                __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+                for (int z = 0; z < 4; ++z) h[z] = __floats2bfloat162_rn(acc[2 * z], acc[2 * z + 1]);
+            } else {
+                float *f = reinterpret_cast<float *>(&o);
+#pragma unroll
+                for (int z = 0; z < 4; ++z) f[z] = acc[z];
+            }
+            dst[c] = o;
+        }
+    }
+}
+
 // dispatch1 also fills meta = -1 for the empty slots [count, C1) of every destination.
 __global__ void meta_fill_kernel(Dispatch1Args a) {
+    pdl_wait();
     if (!a.meta && !a.peer.bases) return;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t tot = (int64_t)a.V * a.K1 * a.C1;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot; idx += nthr) {
         const int64_t vi = idx / a.C1, cc = idx - vi * a.C1;   // vi = v*K1 + i
         const int64_t v = vi / a.K1, i = vi - v * a.K1;
-        const int64_t last = ((v * a.nblk) + a.nblk - 1) * a.K1 + i;   // total = off + hist of the last block
+        const int64_t last = ((v * a.topk + a.topk - 1) * a.nblk + a.nblk - 1) * a.K1 + i;   // total = off + hist of the last block
         if (cc >= (int64_t)a.blk_off1[last] + a.blk_hist1[last]) {
             if (a.peer.bases) {
                 const PeerMap &P = a.peer;
@@ -516,6 +597,7 @@ __global__ void meta_fill_kernel(Dispatch1Args a) {
 // a14: Eq. (4) per resident rank in fp64.
 __global__ void aux_kernel(smile_stats s, double alpha, double beta, double *loss, int V, int K1,
                            int K2, int64_t T, int flat) {
+    pdl_wait();
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= V) return;
     const double Td = (double)T;
@@ -529,6 +611,7 @@ __global__ void aux_kernel(smile_stats s, double alpha, double beta, double *los
 // level when several ranks share a GPU).  grid (V*P*nsub, row chunks).
 constexpr int kCopyRows = 32;
 __global__ void exchange_copy_kernel(CopyXArgs a) {
+    pdl_wait();
     const int pair = blockIdx.x / a.nsub, k = blockIdx.x % a.nsub;
     const int v = pair / a.P, p = pair % a.P;
     const int q = a.member_local[v * a.P + p];
@@ -563,25 +646,30 @@ __global__ void exchange_copy_kernel(CopyXArgs a) {
     }
 }
 
-// Emulated heterogeneous fabric (smile_set_fabric): CTA v is the NIC
-// of sending rank v; it sends its cross-node messages (one per group member on another
-// node: all of the pair's sub-chunks and side ints) one after another, each occupying
-// latency + bytes * ns_per_byte of wall time (%globaltimer); the rows are copied at the
-// start of the message's window.
+// Emulated heterogeneous fabric (smile_set_fabric): the NIC of sending
+// rank v = the kFabricCtas CTAs (b, v).  It sends v's cross-node messages (one per group
+// member on another node: all of the pair's sub-chunks and side ints) one after another:
+// message k occupies the window [W_k, W_k + latency + bytes_k * ns_per_byte) of wall time
+// (%globaltimer), W_0 = the CTA's start, W_{k+1} = the end of window k; each CTA copies its
+// share of the message's rows as soon as the window opens and then waits for the window's
+// end (a share that takes longer than the window delays the next one: the emulation is then
+// bounded by the copy rate of kFabricCtas SMs).
+constexpr int kFabricCtas = 16;
 __global__ void fabric_copy_kernel(CopyXArgs a) {
-    __shared__ unsigned long long s_t0;
-    const int v = blockIdx.x;
+    __shared__ unsigned long long s_w;
+    const int v = blockIdx.y, b = blockIdx.x, NB = gridDim.x;
     const int pos = a.mypos[v];
     const int nvec = (int)(a.rowbytes / 16);
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        s_w = t;
+    }
+    __syncthreads();
+    unsigned long long w = s_w;
     for (int p = 0; p < a.P; ++p) {
         const int q = a.member_local[v * a.P + p];
         if (q < 0 || (a.rank0 + v) / a.m == (a.rank0 + q) / a.m) continue;
-        if (threadIdx.x == 0) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            s_t0 = t;
-        }
-        __syncthreads();
         int64_t bytes = 0;
         for (int k = 0; k < a.nsub; ++k) {
             const int64_t src_chunk = ((int64_t)v * a.P + p) * a.nsub + k;
@@ -592,9 +680,10 @@ __global__ void fabric_copy_kernel(CopyXArgs a) {
                 rows = imin64((rows > 0 ? rows : (int64_t)0), a.Csub);
             }
             bytes += rows * a.rowbytes;
-            const int4 *src = reinterpret_cast<const int4 *>(a.send + src_chunk * a.Csub * a.rowbytes);
-            int4 *dst = reinterpret_cast<int4 *>(a.recv + dst_chunk * a.Csub * a.rowbytes);
-            const int64_t nv = rows * nvec;
+            const int64_t r0 = rows * b / NB, r1 = rows * (b + 1) / NB;     // this CTA's share
+            const int4 *src = reinterpret_cast<const int4 *>(a.send + (src_chunk * a.Csub + r0) * a.rowbytes);
+            int4 *dst = reinterpret_cast<int4 *>(a.recv + (dst_chunk * a.Csub + r0) * a.rowbytes);
+            const int64_t nv = (r1 - r0) * nvec;
             int64_t i = threadIdx.x;
             for (; i + 3 * blockDim.x < nv; i += 4 * blockDim.x) {
                 int4 x0 = __ldg(src + i), x1 = __ldg(src + i + blockDim.x), x2 = __ldg(src + i + 2 * blockDim.x),
@@ -605,16 +694,17 @@ __global__ void fabric_copy_kernel(CopyXArgs a) {
         }
         if (!a.rev && a.sint) {
             bytes += (int64_t)a.ipp * 4;
-            for (int i = threadIdx.x; i < a.ipp; i += blockDim.x)
-                a.rint[((int64_t)q * a.P + pos) * a.ipp + i] = a.sint[((int64_t)v * a.P + p) * a.ipp + i];
+            if (b == 0)
+                for (int i = threadIdx.x; i < a.ipp; i += blockDim.x)
+                    a.rint[((int64_t)q * a.P + pos) * a.ipp + i] = a.sint[((int64_t)v * a.P + p) * a.ipp + i];
         }
+        w += (unsigned long long)(a.latency_ns + (double)bytes * a.ns_per_byte);   // end of this message's window
         __syncthreads();
         if (threadIdx.x == 0) {
-            const unsigned long long until = s_t0 + (unsigned long long)(a.latency_ns + (double)bytes * a.ns_per_byte);
             for (;;) {
                 unsigned long long t;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                if (t >= until) break;
+                if (t >= w) break;
             }
         }
         __syncthreads();
@@ -675,21 +765,21 @@ void launch_gate1(const GateArgs &a, cudaStream_t st) {
         attr_set = true;
     }
     note_launch();
-    gate1_kernel<<<dim3(a.nblk, a.V), a.TB, smem, st>>>(a);
+    launch_k(gate1_kernel, dim3(a.nblk, a.V), dim3(a.TB), smem, st, a);
 }
 
 void launch_scan1(const Scan1Args &a, cudaStream_t st) {
     if (a.T == 0) return;
     note_launch();
-    scan1_kernel<<<a.V, 512, 0, st>>>(a);
+    launch_k(scan1_kernel, dim3(a.V), dim3(512), 0, st, a);
 }
 
 void launch_rank2(const Rank2Args &a, cudaStream_t st) {
     if (a.items == 0) return;
     note_launch();
-    rank2_kernel<<<dim3(a.nblk, a.V), kRank2Items, 0, st>>>(a);
+    launch_k(rank2_kernel, dim3(a.nblk, a.V), dim3(kRank2Items), 0, st, a);
     note_launch();
-    scan2_kernel<<<a.V, 512, 0, st>>>(a);
+    launch_k(scan2_kernel, dim3(a.V), dim3(512), 0, st, a);
 }
 
 // Rows per warp batch: SMILE_MOVE_RW = 4 (default) or 8.
@@ -733,19 +823,19 @@ static void launch_move(MoveArgs &m, cudaStream_t st) {
     if (grid > 148 * move_gridmul()) grid = 148 * move_gridmul();
     note_launch();
     const int minb = move_minb();
-    if (rw == 8) row_move_kernel<8><<<(int)grid, kMoveThreads, 0, st>>>(m);
-    else if (minb == 3) row_move_kernel_mb<kMoveRowsPerWarp, 3><<<(int)grid, kMoveThreads, 0, st>>>(m);
-    else row_move_kernel<kMoveRowsPerWarp><<<(int)grid, kMoveThreads, 0, st>>>(m);
+    if (rw == 8) launch_k(row_move_kernel<8>, dim3((unsigned)grid), dim3(kMoveThreads), 0, st, m);
+    else if (minb == 3) launch_k(row_move_kernel_mb<kMoveRowsPerWarp, 3>, dim3((unsigned)grid), dim3(kMoveThreads), 0, st, m);
+    else launch_k(row_move_kernel<kMoveRowsPerWarp>, dim3((unsigned)grid), dim3(kMoveThreads), 0, st, m);
 }
 
 void launch_dispatch1(const Dispatch1Args &a, cudaStream_t st) {
     if (a.T == 0) return;
     MoveArgs m{};
-    m.kind = MOVE_DISPATCH1; m.rows = (int64_t)a.V * a.T; m.rowbytes = a.rowbytes; m.d1 = a;
+    m.kind = MOVE_DISPATCH1; m.rows = (int64_t)a.topk * a.V * a.T; m.rowbytes = a.rowbytes; m.d1 = a;
     launch_move(m, st);
     if (a.meta || a.peer.bases && a.peer.n > 0) {
         note_launch();
-        meta_fill_kernel<<<148 * 4, 256, 0, st>>>(a);
+        launch_k(meta_fill_kernel, dim3(148 * 4), dim3(256), 0, st, a);
     }
 }
 
@@ -753,7 +843,7 @@ void launch_meta_fill(const Dispatch1Args &a, cudaStream_t st) {
     if (a.T == 0) return;
     if (a.meta || a.peer.bases && a.peer.n > 0) {
         note_launch();
-        meta_fill_kernel<<<148 * 4, 256, 0, st>>>(a);
+        launch_k(meta_fill_kernel, dim3(148 * 4), dim3(256), 0, st, a);
     }
 }
 
@@ -780,6 +870,14 @@ void launch_combine2(const Combine2Args &a, cudaStream_t st) {
 
 void launch_combine1(const Combine1Args &a, cudaStream_t st) {
     if (a.T == 0) return;
+    if (a.topk > 1) {
+        const int64_t warps = (int64_t)a.V * a.T;
+        int64_t grid = (warps + 7) / 8;
+        if (grid > 148 * 8) grid = 148 * 8;
+        note_launch();
+        launch_k(combine_topk_kernel, dim3((unsigned)grid), dim3(256), 0, st, a);
+        return;
+    }
     MoveArgs m{};
     m.kind = MOVE_COMBINE1; m.rows = (int64_t)a.V * a.T; m.rowbytes = (int64_t)a.d * (a.bf16 ? 2 : 4); m.c1 = a;
     launch_move(m, st);
@@ -788,7 +886,7 @@ void launch_combine1(const Combine1Args &a, cudaStream_t st) {
 void launch_aux(const smile_stats &s, double alpha, double beta, double *loss, int V, int K1, int K2,
                 int64_t T, int flat, cudaStream_t st) {
     note_launch();
-    aux_kernel<<<(V + 127) / 128, 128, 0, st>>>(s, alpha, beta, loss, V, K1, K2, T, flat);
+    launch_k(aux_kernel, dim3((V + 127) / 128), dim3(128), 0, st, s, alpha, beta, loss, V, K1, K2, T, flat);
 }
 
 void launch_peer_barrier(char *const *bases, int64_t off_flags, int me, const int32_t *peers, int npeers, int level,
@@ -800,14 +898,14 @@ void launch_peer_barrier(char *const *bases, int64_t off_flags, int me, const in
 
 void launch_fabric_copy(const CopyXArgs &a, cudaStream_t st) {
     note_launch();
-    fabric_copy_kernel<<<a.V, 256, 0, st>>>(a);
+    fabric_copy_kernel<<<dim3(kFabricCtas, a.V), 256, 0, st>>>(a);
 }
 
 void launch_exchange_copy(const CopyXArgs &a, cudaStream_t st) {
     const int64_t chunks = (a.Csub + kCopyRows - 1) / kCopyRows;
     dim3 grid((unsigned)(a.V * a.P * a.nsub), (unsigned)(chunks > 0 ? chunks : 1));
     note_launch();
-    exchange_copy_kernel<<<grid, 256, 0, st>>>(a);
+    launch_k(exchange_copy_kernel, grid, dim3(256), 0, st, a);
 }
 
 }  // namespace smile

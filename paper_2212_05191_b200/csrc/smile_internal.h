@@ -18,6 +18,33 @@ constexpr int kWarp = 32;
 // calls it immediately before its <<<>>> / cudaLaunchKernelEx.
 void note_launch();
 
+// Programmatic dependent launch (PDL) for the kernels of the forward chain: a kernel
+// launched with launch_k may be scheduled while the previous kernel on the stream is still
+// finishing; its first statement is pdl_wait() (griddepcontrol.wait: blocks until the
+// previous grid has completed and its memory is visible -- so no global access happens
+// before it), and the big kernels call pdl_trigger() after their main loop so the next
+// grid's launch and prologue overlap their tail.  SMILE_PDL=0 disables the attribute.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // Tokens per block of the level-1 gate (sized so the logits tile stays <= 32 KB of smem).
 inline int gate_tokens_per_block(int KW) {
     if (KW <= 32) return 256;
@@ -70,9 +97,9 @@ struct smile_ctx_s {
     bool l1_pending = false;   // the last expert FFN wrote out rows directly: until the next level-1
                                // dispatch, smile_combine(1) may only target the bound output
     const float *d1_gate = nullptr;   // route->gate of the last smile_dispatch(1)
-    int nblk1 = 0;             // gate tiles per rank (fixed-tile gate kernels, fused look-back)
-    int nch1 = 0;              // 32-token chunks per rank: the level-1 scan / statistics tables
-    int *gate_sync = nullptr;  // [2 + V] ranged tensor-core gate: split-ready, done, per-rank chunk counters
+    int nblk1 = 0;             // gate table blocks per rank (TB1 tokens each)
+    bool gate_swapped = false; // the tensor-core gate is the swapped-role 256-token kernel
+    int *gate_sync = nullptr;  // [2] swapped gate: split-ready and done counters
     int nblk2 = 0;             // level-2 ranking blocks per rank
     int *d_err = nullptr;      // sticky device error flag (smile_status)
     int32_t *blk_hist1 = nullptr, *blk_off1 = nullptr, *blk_hist2a = nullptr;
@@ -112,7 +139,8 @@ struct GateArgs {
     const void *x; const float *w; const float *logits; float *logits_out;
     smile_route route; int32_t *blk_hist1, *blk_hist2a; double *blk_psum;
     int *err; int V; int64_t T; int d; int K1, K2, KW; int TB, nblk; int flat; int bf16;
-    int nch;                 // 32-token chunks per rank: granularity of the scan / stats tables
+    int topk;                // FLAT top-k (tables [V][topk][nblk], route [topk][V][T] for dest1 / slot1 / gate)
+    int swapped;             // tensor-core gate: the swapped-role 256-token kernel (KW <= 40)
     // fused level-1 permute (tensor-core gate only; smile_gate_dispatch_inter): final
     // slots by decoupled look-back over the tiles' destination histograms, then the
     // kept rows moved to their slots (send rows / meta, or the peers' receive buffers)
@@ -126,9 +154,10 @@ void launch_gate1(const GateArgs &a, cudaStream_t st);
 struct Scan1Args {
     const int32_t *blk_hist1, *blk_hist2a; const double *blk_psum; int32_t *blk_off1;
     smile_stats stats; int32_t *counts1; int V, nblk, K1, K2, KW; int64_t C1; int flat; int64_t T;
-    PeerMap peer;            // nblk: 32-token chunks per rank (the tables' granularity)
+    PeerMap peer;            // nblk: table blocks per rank and choice
     int *lb_flag;            // reset for the next fused gate (may be null)
     int nlb;                 // look-back tiles per rank (lb_flag entries)
+    int topk;
 };
 void launch_scan1(const Scan1Args &a, cudaStream_t st);
 
@@ -142,6 +171,7 @@ void launch_rank2(const Rank2Args &a, cudaStream_t st);
 struct Dispatch1Args {
     const void *x; smile_route route; const int32_t *blk_off1; const int32_t *blk_hist1;
     void *send; int32_t *meta; int V; int64_t T; int64_t rowbytes; int K1; int64_t C1; int TB, nblk;
+    int topk;                          // FLAT top-k: topk * V * T items, choice-major (R31)
     PeerMap peer;
     void *out;                         // PEER + output bound, every rank in this process: tokens
                                        // dropped at level 1 get their zero output row here
@@ -174,6 +204,7 @@ struct Combine1Args {
     PeerMap peer;
     int skip_direct;           // PEER: tokens whose intermediate and expert are in this process
                                // were written by the expert's GEMM 2 (smile_set_output)
+    int topk;                  // FLAT top-k (> 1): out[t] = sum over kept choices of gate_j * row_j
 };
 void launch_combine1(const Combine1Args &a, cudaStream_t st);
 
@@ -269,13 +300,11 @@ void launch_pad_rows_zero(void *buf, const int32_t *counts, int nseg, int64_t Cs
 
 // Level-1 gate with the router on tcgen05 (gate_tcgen05.cu); needs TB == 128.
 int gate_tc_np(int KW);
-int gate_tc_tile(int KW);            // token tile of the tensor-core gate (128, or 256 for the swapped kernel)
+bool gate_tc_swapped(int KW);        // the swapped-role kernel (256-token tiles of 2 table blocks) for this KW
 int gate_tc_rows(int KW);            // rows of the split-router buffer
 bool gate_tc_supported(int bf16, int d, int KW);
-// The 256-token ("ranged") kernel also builds the split router and runs the level-1 scan
-// (`scan`, counters in gate_sync [2 + V]) and sets *scanned; the 128-token kernel leaves
-// the scan to launch_scan1.
-cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, const Scan1Args *scan,
-                            int *gate_sync, bool *scanned, cudaStream_t st);
+// a.swapped: the swapped-role kernel, which also builds the split router (counters in
+// gate_sync [2]); else the 128-token kernel (split by router_split_kernel).
+cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, int *gate_sync, cudaStream_t st);
 
 }  // namespace smile

@@ -36,7 +36,7 @@ class Shape(C.Structure):
     _fields_ = [("n", C.c_int32), ("m", C.c_int32), ("e", C.c_int32), ("mode", C.c_int32),
                 ("dtype", C.c_int32), ("d", C.c_int32), ("d_ff", C.c_int32), ("T", C.c_int64),
                 ("cf", C.c_double), ("nprocs", C.c_int32), ("proc", C.c_int32), ("device", C.c_int32),
-                ("ffn_impl", C.c_int32)]
+                ("ffn_impl", C.c_int32), ("topk", C.c_int32)]
 
 
 class Sizes(C.Structure):
@@ -115,11 +115,11 @@ def _check(rc: int, what: str):
         raise SmileError(rc, what)
 
 
-def _shape(n, m, e, d, d_ff, T, cf, dtype, mode, nprocs=1, proc=0, device=0, ffn_impl=FFN_AUTO) -> Shape:
+def _shape(n, m, e, d, d_ff, T, cf, dtype, mode, nprocs=1, proc=0, device=0, ffn_impl=FFN_AUTO, topk=1) -> Shape:
     dt = {"fp32": FP32, "bf16": BF16}[dtype] if isinstance(dtype, str) else dtype
     md = {"bilevel": BILEVEL, "flat": FLAT}[mode] if isinstance(mode, str) else mode
     fi = {"auto": FFN_AUTO, "simt": FFN_SIMT, "tcgen05": FFN_TCGEN05}[ffn_impl] if isinstance(ffn_impl, str) else ffn_impl
-    return Shape(n, m, e, md, dt, d, d_ff, T, cf, nprocs, proc, device, fi)
+    return Shape(n, m, e, md, dt, d, d_ff, T, cf, nprocs, proc, device, fi, topk)
 
 
 def plan(**kw) -> Sizes:
@@ -186,9 +186,10 @@ class SmileLayer:
     the current torch stream."""
 
     def __init__(self, n, m, e, d, d_ff, T, cf=2.0, dtype="bf16", mode="bilevel", nprocs=1, proc=0,
-                 device=None, ffn_impl="auto", nccl_id: bytes | None = None):
+                 device=None, ffn_impl="auto", nccl_id: bytes | None = None, topk: int = 1):
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
-        self.shape = _shape(n, m, e, d, d_ff, T, cf, dtype, mode, nprocs, proc, self.device.index, ffn_impl)
+        self.shape = _shape(n, m, e, d, d_ff, T, cf, dtype, mode, nprocs, proc, self.device.index, ffn_impl, topk)
+        self.topk = max(1, topk)
         self.n, self.m, self.e, self.d, self.d_ff, self.T, self.cf = n, m, e, d, d_ff, T, cf
         self.dtype = torch.bfloat16 if self.shape.dtype == BF16 else torch.float32
         self.flat = self.shape.mode == FLAT
@@ -254,6 +255,9 @@ class SmileLayer:
         i32, f32, f64, dt = torch.int32, torch.float32, torch.float64, self.dtype
         out = {k: self._slice(getattr(w.route, k), (V, T), i32 if k in ("dest1", "dest2", "slot1") else f32)
                for k in ("dest1", "dest2", "slot1", "p", "q", "gate")}
+        if self.topk > 1:                     # choice-major [k, V, T] (smile.h smile_route)
+            for k in ("dest1", "slot1", "gate"):
+                out[k] = self._slice(getattr(w.route, k), (self.topk, V, T), i32 if k != "gate" else f32)
         out["hist1"] = self._slice(w.stats.hist1, (V, self.K1), i32)
         out["hist2"] = self._slice(w.stats.hist2, (V, self.K2), i32)
         out["psum1"] = self._slice(w.stats.psum1, (V, self.K1), f64)

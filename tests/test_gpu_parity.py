@@ -565,3 +565,56 @@ def test_out_direct_step_api():
     layer.combine(1, C_ptr(w.back1), outs[0][0], route=w.route)     # the bound output is still fine
     layer.set_output(None)
     layer.close()
+
+
+@pytest.mark.parametrize("mode,fused", [("bilevel", True), ("flat", True), ("bilevel", False)])
+def test_cuda_graph_replay_new_inputs(mode, fused):
+    """smile_forward captured once as a CUDA graph (programmatic dependent launches become
+    graph edges; the swapped gate's split counters and the peer barriers' epochs live on the
+    device) and replayed on new inputs copied into the captured buffers: every replay
+    matches the oracle on its own inputs."""
+    from paper_2212_05191_b200 import SmileLayer
+    n, m, e, T, d, d_ff, cf = 2, 4, 1, 700, 128, 256, 1.25
+    base = Case(n, m, e, T, d, d_ff, cf, dtype="bf16", mode=mode, dist="skewed", seed=81, fused=fused)
+    layer = SmileLayer(n, m, e, d, d_ff, T, cf, "bf16", mode)
+    layer.enable_peer_exchange()
+    g = base.gpu_tensors()
+    out = torch.empty_like(g["x"])
+    loss = torch.empty(layer.V, dtype=torch.float64, device="cuda")
+    fwd = lambda: layer.forward(g["x"], g["W1t"], g["b1"], g["W2t"], g["b2"], out, loss, logits=g["logits"],
+                                w_router=g["w_router"], alpha=base.alpha, beta=base.beta)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fwd()
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        fwd()
+    for k in (1, 2, 3):
+        ck = Case(n, m, e, T, d, d_ff, cf, dtype="bf16", mode=mode, dist="skewed", seed=81 + k, fused=fused)
+        ck.W1, ck.b1, ck.W2, ck.b2, ck.w_router = base.W1, base.b1, base.W2, base.b2, base.w_router
+        gk = ck.gpu_tensors()
+        g["x"].copy_(gk["x"])
+        if g["logits"] is not None:
+            g["logits"].copy_(gk["logits"])
+        out.fill_(float("nan"))
+        graph.replay()
+        torch.cuda.synchronize()
+        assert layer.get_error() == 0
+        lg = None
+        if fused:                                   # route on the GPU's own logits (R3): same gate kernel
+            aux = SmileLayer(n, m, e, d, d_ff, T, cf, "bf16", mode)
+            aux.alloc_workspace()
+            lgt = torch.empty(ck.G, T, ck.cfg.logit_width, dtype=torch.float32, device="cuda")
+            w = aux._view
+            aux.gate_inter(g["x"], w.route, w.stats, C_ptr(w.counts1), w_router=g["w_router"], logits_out=lgt)
+            torch.cuda.synchronize()
+            lg = lgt.cpu().numpy()
+            aux.close()
+        r = ck.oracle_route(logits=lg)
+        np.testing.assert_array_equal(layer.view()["dest1"].cpu().numpy(), r.dest1)
+        assert_close_scaled(out.float().cpu().numpy().reshape(-1, d), ck.oracle_out(r), 2e-2, f"graph replay {k}")
+        np.testing.assert_allclose(loss.cpu().numpy(), r.loss, rtol=1e-6)
+    del graph
+    layer.close()
