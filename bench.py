@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--fabric", default=None,
                     help="GBPS,LATENCY_US: emulated inter-node fabric (smile_set_fabric; SURVEY 8(f) row 1, an in-box "
                          "emulation) on the COPY exchange, N = 1 only")
+    ap.add_argument("--topk", type=int, default=1,
+                    help="experts per token of the FLAT layer (Eq. 2; SURVEY 8(f) row 4); the bi-level layer is top-1")
     ap.add_argument("--exchange", default="peer", choices=["peer", "copy"],
                     help="peer: fused permute -> peer-store exchange (CUDA IPC over NVLink); copy: device copies / NCCL")
     return ap.parse_args()
@@ -275,10 +277,11 @@ class Addr:
         return self.a
 
 
-def make_layer(cfgd, mode, nprocs, proc, dev, ffn, nccl_id):
+def make_layer(cfgd, mode, nprocs, proc, dev, ffn, nccl_id, topk=1):
     from paper_2212_05191_b200 import SmileLayer
     L = SmileLayer(cfgd["n"], cfgd["m"], cfgd["e"], cfgd["d"], cfgd["d_ff"], cfgd["T"], cfgd["cf"], cfgd["dtype"],
-                   mode, nprocs=nprocs, proc=proc, device=dev, ffn_impl=ffn, nccl_id=nccl_id)
+                   mode, nprocs=nprocs, proc=proc, device=dev, ffn_impl=ffn, nccl_id=nccl_id,
+                   topk=topk if mode == "flat" else 1)
     L.alloc_workspace()
     return L
 
@@ -585,7 +588,7 @@ def run_ours(args):
                 buf.copy_(torch.frombuffer(bytearray(smb.unique_id()), dtype=torch.uint8))
             dist.broadcast(buf, 0)
             nccl_id = bytes(buf.cpu().numpy().tobytes())
-        L = make_layer(cfgd, mode, world, rank, local, args.ffn, nccl_id)
+        L = make_layer(cfgd, mode, world, rank, local, args.ffn, nccl_id, topk=args.topk)
         if fabric:
             L.set_fabric(fabric["inter_gbps_per_rank"], fabric["inter_latency_us_per_message"])
         if args.exchange == "peer":
@@ -744,7 +747,7 @@ def run_ours(args):
             nvl = {"world": sum(int(c1[v, E]) for v in range(V) for E in range(c1.shape[1]) if (E // e) // V != rank) * rb}
         ffn_ms = phase_ms["ffn"] if not train else None
         ffn_tc = cfgd["dtype"] == "bf16" and args.ffn != "simt" and smb.TCGEN05_DEFAULT
-        if (mode == "flat" and args.exchange == "peer" and ffn_tc and not train
+        if (mode == "flat" and args.exchange == "peer" and ffn_tc and not train and args.topk == 1
                 and os.environ.get("SMILE_OUT_DIRECT", "1") != "0" and not inp.get("fused_gate")):
             # FLAT gets the same GEMM 2 -> out fusion: out[t] for tokens whose expert is in this
             # process; combine1 moves the other kept tokens and zeroes drops
@@ -907,7 +910,7 @@ def run_ours(args):
                                f"{G} ranks as {cfgd['n']}x{cfgd['m']} (n x m), "
                                f"e={e}/rank, T={T}/rank, d={d}, d_ff={d_ff}, cf={cfgd['cf']}, fused router; "
                                f"{V} ranks per GPU; exchange={args.exchange}", "ranks_per_gpu": V, "mode": modes[0],
-                   "exchange": args.exchange,
+                   "exchange": args.exchange, "flat_topk": args.topk,
                    "fabric": fabric and dict(fabric, note="IN-BOX EMULATION (smile_set_fabric): cross-node transfers "
                                              "of the COPY exchange go through per-rank emulated NICs -- "
                                              "latency per message + bytes / bandwidth of wall time each; not a "

@@ -60,6 +60,11 @@ def main():
         fwd = lambda: layer.forward(xin, sl(g["W1t"], e), sl(g["b1"], e), sl(g["W2t"], e), sl(g["b2"], e), out, loss,
                                     logits=lin, w_router=g["w_router"], alpha=case.alpha, beta=case.beta, train=bwd)
         fwd()
+        torch.cuda.synchronize()
+        # routing state of every resident rank for the bit-exact route check (snapshot before
+        # any graph replay overwrites it with the replayed inputs' routes)
+        vw = {k: t.clone() for k, t in layer.view().items()}
+        out_base, loss_base = out.clone(), loss.clone()
         graph_checks = []
         if c.get("_graph"):
             # smile_forward captured once as a CUDA graph and replayed on new inputs copied into
@@ -112,10 +117,8 @@ def main():
         err = layer.get_error()
         outs = [torch.empty_like(out) for _ in range(world)]
         losses = [torch.empty_like(loss) for _ in range(world)]
-        dist.all_gather(outs, out)
-        dist.all_gather(losses, loss)
-        # routing state of every resident rank, for the bit-exact route check
-        vw = layer.view()
+        dist.all_gather(outs, out_base)
+        dist.all_gather(losses, loss_base)
         rkeys = ["dest1", "dest2", "slot1", "counts1", "hist1"] + ([] if case.flat else ["rmeta1", "slot2", "counts2"])
         routes = {}
         for k in rkeys:

@@ -54,7 +54,9 @@ def _run(n, cases, port):
            json.dumps(cases)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     tail = (r.stdout + r.stderr)[-4000:]
-    assert r.returncode == 0, tail
+    res = [ln for ln in r.stdout.splitlines() if ln.startswith("MGPU_RESULT")]
+    fails = json.loads(res[-1][len("MGPU_RESULT"):])["failures"] if res else None
+    assert r.returncode == 0, f"failures: {fails}\n{tail}"
     assert "MGPU_RESULT" in r.stdout, tail
 
 
