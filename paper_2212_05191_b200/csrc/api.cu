@@ -275,6 +275,9 @@ static smile_status build_level(smile_ctx c, int level, int P, int nsub, int64_t
     CUDA_TRY(cudaMalloc(&L.d_mypos, sizeof(int32_t) * V));
     CUDA_TRY(cudaMemcpy(L.d_member_local, mloc.data(), sizeof(int32_t) * V * P, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(L.d_mypos, pos.data(), sizeof(int32_t) * V, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&L.d_rcnt, sizeof(int32_t) * V * P * nsub));
+    CUDA_TRY(cudaMallocHost(&L.h_scnt, sizeof(int32_t) * V * P * nsub));
+    CUDA_TRY(cudaMallocHost(&L.h_rcnt, sizeof(int32_t) * V * P * nsub));
     return SMILE_OK;
 }
 
@@ -398,7 +401,8 @@ extern "C" smile_status smile_destroy(smile_ctx c) {
     cudaFree(c->d_bases);
     for (int l = 0; l < 3; ++l) cudaFree(c->d_peers[l]);
     for (auto &L : c->lv) {
-        cudaFree(L.d_member_local); cudaFree(L.d_mypos);
+        cudaFree(L.d_member_local); cudaFree(L.d_mypos); cudaFree(L.d_rcnt);
+        cudaFreeHost(L.h_scnt); cudaFreeHost(L.h_rcnt);
         free(L.h_member); free(L.h_mypos);
     }
     delete c;
@@ -683,6 +687,80 @@ extern "C" smile_status smile_gate_intra(smile_ctx c, const int32_t *recv_meta, 
     return post_launch();
 }
 
+// SMILE_XCHG_EXACT=1: the NCCL part of an exchange moves only the valid rows of every
+// (peer, sub-chunk) -- the counts travel first (a small NCCL exchange), the host reads them
+// (one stream sync per forward exchange; the reverse trip reuses them), then grouped
+// ncclSend / ncclRecv of exact sizes land the rows at the padded layout's offsets.  Not
+// graph-capturable (host sync); the default keeps the equal-split padded chunks (R25).
+static bool exact_exchange() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SMILE_XCHG_EXACT");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v != 0;
+}
+
+static smile_status all2all_exact(smile_ctx c, int level, int reverse, const void *send_rows, void *recv_rows,
+                                  const int32_t *send_ints, int32_t *recv_ints, const int32_t *fwd_counts,
+                                  bool split_comm, cudaStream_t st) {
+    Level &L = c->lv[level];
+    const int V = c->sz.V, P = L.P, ns = L.nsub;
+    const int64_t rb = (int64_t)c->shape.d * (c->shape.dtype == SMILE_BF16 ? 2 : 4);
+    // the remote transfers of this process: (send?, peer, comm, chunk)
+    struct Op { int send; int peer; int chunk; };
+    std::vector<Op> ops;
+    ncclComm_t comm = split_comm ? L.comm : c->world;
+    if (split_comm) {                                  // V == 1: comm rank = position in the group
+        for (int p = 0; p < P; ++p)
+            if (p != L.h_mypos[0]) ops.push_back({0, p, p});
+        for (int p = 0; p < P; ++p)
+            if (p != L.h_mypos[0]) ops.push_back({1, p, p});
+    } else {
+        std::vector<smile_xop> xo;
+        exchange_ops(&c->shape, level, xo);
+        for (const smile_xop &o : xo) ops.push_back({o.kind == 0 ? 1 : 0, o.peer_proc, o.chunk});   // kind 0 = send
+    }
+    const size_t ncnt = (size_t)V * P * ns;
+    if (!reverse) {
+        // 1. counts: ours to the peers, theirs into d_rcnt (at our chunk of the transfer)
+        NCCL_TRY(ncclGroupStart());
+        for (const Op &o : ops) {
+            if (o.send) NCCL_TRY(ncclSend(fwd_counts + (size_t)o.chunk * ns, ns, ncclInt32, o.peer, comm, st));
+            else NCCL_TRY(ncclRecv(L.d_rcnt + (size_t)o.chunk * ns, ns, ncclInt32, o.peer, comm, st));
+        }
+        NCCL_TRY(ncclGroupEnd());
+        CUDA_TRY(cudaMemcpyAsync(L.h_scnt, fwd_counts, ncnt * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(L.h_rcnt, L.d_rcnt, ncnt * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (send_ints) {                               // side ints (meta / counts): whole, small
+            const int ipp = L.ints_per_peer;
+            NCCL_TRY(ncclGroupStart());
+            for (const Op &o : ops) {
+                if (o.send) NCCL_TRY(ncclSend(send_ints + (size_t)o.chunk * ipp, ipp, ncclInt32, o.peer, comm, st));
+                else NCCL_TRY(ncclRecv(recv_ints + (size_t)o.chunk * ipp, ipp, ncclInt32, o.peer, comm, st));
+            }
+            NCCL_TRY(ncclGroupEnd());
+        }
+    }
+    // 2. rows: exact sizes per (peer, sub-chunk); the reverse trip sends back what came in
+    const size_t sub = (size_t)L.Csub * rb;
+    NCCL_TRY(ncclGroupStart());
+    for (const Op &o : ops) {
+        for (int k = 0; k < ns; ++k) {
+            const size_t ci = (size_t)o.chunk * ns + k;
+            int32_t rows = o.send ? (reverse ? L.h_rcnt[ci] : L.h_scnt[ci]) : (reverse ? L.h_scnt[ci] : L.h_rcnt[ci]);
+            if (rows > L.Csub) rows = (int32_t)L.Csub;
+            if (rows <= 0) continue;
+            const size_t off = ci * sub, bytes = (size_t)rows * rb;
+            if (o.send) NCCL_TRY(ncclSend((const char *)send_rows + off, bytes, ncclUint8, o.peer, comm, st));
+            else NCCL_TRY(ncclRecv((char *)recv_rows + off, bytes, ncclUint8, o.peer, comm, st));
+        }
+    }
+    NCCL_TRY(ncclGroupEnd());
+    return SMILE_OK;
+}
+
 // One level's equal-split All2All.  Pairs of ranks resident on this
 // device are a device copy; V == 1 uses ncclAlltoAll on the level's split communicator;
 // several resident ranks per process plus remote peers use grouped ncclSend/ncclRecv
@@ -728,6 +806,9 @@ extern "C" smile_status smile_all2all(smile_ctx c, int32_t level, int32_t revers
         if (cudaGetLastError() != cudaSuccess) return SMILE_ECUDA;
     }
     if (c->shape.nprocs == 1) return SMILE_OK;
+    if (exact_exchange() && fwd_counts && (nccl_alltoall || L.any_remote))
+        return all2all_exact(c, level, reverse, send_rows, recv_rows, with_ints ? send_ints : nullptr,
+                             with_ints ? recv_ints : nullptr, fwd_counts, nccl_alltoall, st);
     if (nccl_alltoall) {
         if (with_ints) NCCL_TRY(ncclAlltoAll(send_ints, recv_ints, L.ints_per_peer, ncclInt32, L.comm, st));
         NCCL_TRY(ncclAlltoAll(send_rows, recv_rows, chunk, ncclUint8, L.comm, st));

@@ -66,6 +66,9 @@ struct Level {
     int32_t *h_mypos = nullptr;         // [V]
     int any_remote = 0;
     ncclComm_t comm = nullptr;          // split comm when V == 1 (inter/intra) or world
+    // exact-size NCCL exchange (SMILE_XCHG_EXACT=1): per-chunk valid-row counts [V, P, nsub]
+    int32_t *d_rcnt = nullptr;          // device: counts received from the peers (forward)
+    int32_t *h_scnt = nullptr, *h_rcnt = nullptr;   // host copies of the last forward's counts
 };
 
 // Fused permute -> peer-store exchange (SMILE_XCHG_PEER): every process's workspace

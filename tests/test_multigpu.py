@@ -61,6 +61,24 @@ def _run(n, cases, port):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_multigpu_exact_exchange_2():
+    """SMILE_XCHG_EXACT=1: the NCCL exchanges move valid rows only (counts first); same
+    oracle bar as the padded exchange, forward and training."""
+    base = dict(T=600, d=64, d_ff=128, dist="skewed", seed=11)
+    bw = dict(T=400, d=128, d_ff=256, dist="skewed", seed=12)
+    cases = [dict(n=2, m=1, e=1, cf=1.0, dtype="fp32", mode="bilevel", **base),
+             dict(n=2, m=4, e=1, cf=1.0, dtype="bf16", mode="bilevel", **base),
+             dict(n=2, m=1, e=2, cf=1.25, dtype="bf16", mode="flat", **base),
+             dict(n=2, m=4, e=2, cf=1.0, dtype="bf16", mode="flat", **base),
+             dict(n=2, m=4, e=1, cf=1.25, dtype="bf16", mode="bilevel", _bwd=True, **bw)]
+    os.environ["SMILE_XCHG_EXACT"] = "1"
+    try:
+        _run(2, cases, 29613)
+    finally:
+        del os.environ["SMILE_XCHG_EXACT"]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_multigpu_parity_2():
     _run(2, _cases(2), 29611)
 
