@@ -711,11 +711,11 @@ static smile_status all2all_exact(smile_ctx c, int level, int reverse, const voi
     struct Op { int send; int peer; int chunk; };
     std::vector<Op> ops;
     ncclComm_t comm = split_comm ? L.comm : c->world;
-    if (split_comm) {                                  // V == 1: comm rank = position in the group
-        for (int p = 0; p < P; ++p)
-            if (p != L.h_mypos[0]) ops.push_back({0, p, p});
-        for (int p = 0; p < P; ++p)
-            if (p != L.h_mypos[0]) ops.push_back({1, p, p});
+    if (split_comm) {
+        // V == 1: comm rank = position in the group; every chunk, our own included (the
+        // padded path's ncclAlltoAll covers the self chunk too -- no device copy runs here)
+        for (int p = 0; p < P; ++p) ops.push_back({1, p, p});
+        for (int p = 0; p < P; ++p) ops.push_back({0, p, p});
     } else {
         std::vector<smile_xop> xo;
         exchange_ops(&c->shape, level, xo);

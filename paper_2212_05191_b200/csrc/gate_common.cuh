@@ -159,9 +159,37 @@ __device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j
         if (tid < nt) a.route.slot1[c * VT + tok0 + tid] = lrc;
         for (int k = tid; k < K1; k += nthr) a.blk_hist1[(bo0 + (int64_t)c * a.nblk) * K1 + k] = s_bh[k];
     }
-    // LB statistics partials of the tile (fp64 for the probability sums): one warp per
-    // statistic, lanes stride over tokens, fixed butterfly order => deterministic.
-    {
+    // LB statistics partials of the tile (fp64 for the probability sums), deterministic
+    // (fixed summation order).  Wide routers (KW >= 32): a warp per block of 32
+    // statistics, lane = statistic, tokens in ascending order over 4 interleaved fp64
+    // accumulators (conflict-free row reads; the per-statistic shuffle trees of the narrow
+    // case cost C5's 66-wide gate most of its epilogue).  Narrow routers: one warp per
+    // statistic, lanes stride over tokens, fixed butterfly.
+    if (KW >= 32) {
+        const int lane = tid & 31, w = tid >> 5, NW = nthr >> 5;
+        for (int cb = w; cb < (KW + 31) / 32; cb += NW) {
+            const int k = cb * 32 + lane;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if (k < KW) {
+                int tt = 0;
+                for (; tt + 3 < nt; tt += 4) {
+                    a0 += (double)s_lg[tt * lds + k];
+                    a1 += (double)s_lg[(tt + 1) * lds + k];
+                    a2 += (double)s_lg[(tt + 2) * lds + k];
+                    a3 += (double)s_lg[(tt + 3) * lds + k];
+                }
+                for (; tt < nt; ++tt) a0 += (double)s_lg[tt * lds + k];
+                a.blk_psum[bo0 * (K1 + K2) + k] = (a0 + a1) + (a2 + a3);
+            }
+        }
+        for (int cb = w; cb < (K2 + 31) / 32; cb += NW) {
+            const int k = cb * 32 + lane;
+            int c = 0;
+            for (int tt = 0; tt < nt; ++tt) c += (s_j[tt] == k);
+            if (k < K2) a.blk_hist2a[bo0 * K2 + k] = c;
+        }
+        if (a.flat && tid == 0) a.blk_psum[bo0 * (K1 + K2) + K1] = (double)nt;
+    } else {
         const int lane = tid & 31, w = tid >> 5, NW = nthr >> 5;
         for (int k = w; k < KW; k += NW) {
             double acc = 0.0;

@@ -45,9 +45,9 @@ def main():
             v = float(r[idx[k]].replace(",", ""))
             u = unit[k]
             if k == "dur_us":
-                v = v / 1000.0 if u == "nsecond" else (v * 1000.0 if u == "msecond" else v)
+                v = v / 1000.0 if u in ("nsecond", "ns") else (v * 1000.0 if u in ("msecond", "ms") else v)
             if k in ("rd_MB", "wr_MB"):
-                v = v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
+                v = v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}.get(u, 1.0)
             if k == "sm_ghz":
                 v = v * {"hz": 1e-9, "Khz": 1e-6, "Mhz": 1e-3, "Ghz": 1.0}.get(u.lower().capitalize() if u else "", 1.0)
             return v
