@@ -541,8 +541,14 @@ __global__ void __launch_bounds__(256) combine_topk_kernel(Combine1Args a) {
             float acc[8];
 #pragma unroll
             for (int z = 0; z < 8; ++z) acc[z] = 0.f;
-            for (int k = 0; k < nsrc; ++k) {
-                const int4 u = __ldg(reinterpret_cast<const int4 *>(src[k]) + c);
+            int4 uu[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)                      // every choice's 16 B in flight together
+                if (k < nsrc) uu[k] = __ldg(reinterpret_cast<const int4 *>(src[k]) + c);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (k >= nsrc) break;
+                const int4 u = uu[k];
                 if (a.bf16) {
                     const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
 #pragma unroll
