@@ -321,8 +321,8 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
     const size_t nb2 = (size_t)V * (c->nblk2 > 0 ? c->nblk2 : 1);
     CUDA_TRY(cudaMalloc(&c->d_err, sizeof(int)));
     CUDA_TRY(cudaMemset(c->d_err, 0, sizeof(int)));
-    CUDA_TRY(cudaMalloc(&c->gate_sync, sizeof(int) * 2));
-    CUDA_TRY(cudaMemset(c->gate_sync, 0, sizeof(int) * 2));
+    CUDA_TRY(cudaMalloc(&c->gate_sync, sizeof(int) * 3));
+    CUDA_TRY(cudaMemset(c->gate_sync, 0, sizeof(int) * 3));
     CUDA_TRY(cudaMalloc(&c->blk_hist1, nb1 * z.K1 * 4));
     CUDA_TRY(cudaMalloc(&c->blk_off1, nb1 * z.K1 * 4));
     CUDA_TRY(cudaMalloc(&c->blk_hist2a, nb1 * z.K2 * 4));
@@ -569,17 +569,20 @@ extern "C" smile_status smile_gate_inter(smile_ctx c, const void *x, const float
     a.K1 = c->sz.K1; a.K2 = c->sz.K2; a.KW = c->sz.KW; a.TB = c->TB1; a.nblk = c->nblk1;
     a.flat = c->shape.mode == SMILE_FLAT; a.bf16 = c->shape.dtype == SMILE_BF16;
     a.topk = c->shape.topk > 1 ? c->shape.topk : 1; a.swapped = c->gate_swapped;
-    if (!logits && c->wsplit) {
-        const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, c->gate_sync, S(stream));
-        if (e != cudaSuccess) return SMILE_ECUDA;
-    } else {
-        launch_gate1(a, S(stream));
-    }
     Scan1Args s{};
     s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;
     s.stats = *stats; s.counts1 = counts1; s.V = c->sz.V; s.nblk = c->nblk1; s.K1 = c->sz.K1; s.K2 = c->sz.K2;
     s.KW = c->sz.KW; s.C1 = c->sz.C1; s.flat = a.flat; s.T = c->shape.T; s.peer = peer_of(c); s.topk = a.topk;
-    launch_scan1(s, S(stream));
+    bool scanned = false;                    // the swapped tensor-core gate scans by look-back itself
+    if (!logits && c->wsplit) {
+        Scan1Args sl = s;
+        sl.lb_flag = c->lb_flag; sl.lb_inc = c->lb_inc;
+        const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, c->gate_sync, &sl, &scanned, S(stream));
+        if (e != cudaSuccess) return SMILE_ECUDA;
+    } else {
+        launch_gate1(a, S(stream));
+    }
+    if (!scanned) launch_scan1(s, S(stream));
     return post_launch();
 }
 
@@ -608,7 +611,7 @@ extern "C" smile_status smile_gate_dispatch_inter(smile_ctx c, const void *x, co
     a.flat = !bi; a.bf16 = c->shape.dtype == SMILE_BF16;
     a.fuse_dispatch = 1; a.send = send_rows; a.meta = bi ? send_meta : nullptr; a.rowbytes = rb; a.C1 = c->sz.C1;
     a.peer = peer_of(c); a.lb_flag = c->lb_flag; a.lb_agg = c->lb_agg; a.lb_inc = c->lb_inc;
-    const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, nullptr, S(stream));
+    const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, nullptr, nullptr, nullptr, S(stream));
     if (e != cudaSuccess) return SMILE_ECUDA;
     Scan1Args s{};
     s.blk_hist1 = c->blk_hist1; s.blk_hist2a = c->blk_hist2a; s.blk_psum = c->blk_psum; s.blk_off1 = c->blk_off1;

@@ -464,7 +464,115 @@ struct GateTArgs {
     int nbuilders;   // CTAs that build the split router (0: built by router_split_kernel)
     int *split_ready, *done;
     __nv_bfloat16 *wsplit;   // [NPT, d] the split router
+    // level-1 scan by decoupled look-back inside the kernel (lookback != 0): per-tile flags
+    // carry the call's epoch (2 e + 1: aggregate published, 2 e + 2: inclusive prefix), so
+    // nothing is reset between calls; the last CTA advances *epoch_ctr
+    int lookback;
+    Scan1Args s;
+    int *epoch_ctr;
 };
+
+// Level-1 scan of one tile by decoupled look-back (a3; R5, R8): the tile's destination
+// histogram s_bh (gate_finish's block_rank) is already in blk_hist1; publish it, look back
+// over the rank's earlier tiles (warp 0: lane = predecessor, aggregates summed up to the
+// nearest inclusive prefix), write the tile's exclusive offsets to blk_off1 (what the
+// permute adds to the tile-local ranks) and its inclusive prefix.  The rank's LAST tile
+// then holds the totals: hist1, counts1 = min(total, C1) (and FLAT peer counts), and -- once
+// every tile of the rank has published -- reduces the rank's LB statistics over its tiles in
+// tile order (deterministic).  Tiles run in increasing order on every CTA and every CTA is
+// resident, so every wait terminates.
+template <class Sync>
+__device__ void lookback_scan(const GateTArgs &ta, const int *s_bh, int *s_off, int tile, int epoch) {
+    const GateArgs &a = ta.g;
+    const Scan1Args &sc = ta.s;
+    const int tid = Sync::tid(), lane = tid & 31, w = tid >> 5;
+    const int K1 = a.K1, v = tile / a.nblk, blk = tile - v * a.nblk;
+    int *flag = sc.lb_flag + tile;
+    const int f_agg = 2 * epoch + 1, f_inc = 2 * epoch + 2;
+    // 1. publish (the first tile of a rank: directly its inclusive prefix)
+    for (int k = tid; k < K1; k += Sync::nthr()) {
+        if (blk == 0) sc.lb_inc[(int64_t)tile * K1 + k] = s_bh[k];
+        s_off[k] = 0;
+    }
+    // the threads that wrote this tile's table entries (blk_hist1, lb_inc: tid < K1; psum /
+    // hist2a: lane 0 of the narrow loops, every lane of the wide ones) make them visible
+    if (lane == 0 || tid < K1 || a.KW >= 32) __threadfence();
+    Sync::sync();
+    if (tid == 0) st_release_gpu(flag, blk == 0 ? f_inc : f_agg);
+    // 2. look back (warp 0)
+    if (blk > 0 && w == 0) {
+        const int base = v * a.nblk;
+        for (int p = blk - 1;; p -= 32) {
+            const int pb = p - lane;
+            int fl = f_inc;                             // before the rank's first tile: zero, inclusive
+            if (pb >= 0) {
+                uint64_t spin = 0;
+                while ((fl = ld_acquire_gpu(sc.lb_flag + base + pb)) < f_agg)
+                    if (++spin > (1ull << 28)) __trap();   // a tile that never publishes: abort, never hang
+            }
+            const unsigned incm = __ballot_sync(kFull, fl == f_inc);
+            const int stop = incm ? __ffs(incm) - 1 : 32;
+            for (int k = 0; k < K1; ++k) {
+                int val = 0;
+                if (pb >= 0 && lane < stop) val = __ldcg(sc.blk_hist1 + ((int64_t)base + pb) * K1 + k);
+                else if (pb >= 0 && lane == stop) val = __ldcg(sc.lb_inc + ((int64_t)base + pb) * K1 + k);
+                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(kFull, val, o);
+                if (lane == 0) s_off[k] += val;
+            }
+            if (incm) break;
+        }
+    }
+    Sync::sync();
+    // 3. offsets for the permute, the inclusive prefix for the successors
+    for (int k = tid; k < K1; k += Sync::nthr()) {
+        sc.blk_off1[(int64_t)tile * K1 + k] = s_off[k];
+        if (blk > 0) sc.lb_inc[(int64_t)tile * K1 + k] = s_off[k] + s_bh[k];
+    }
+    if (blk > 0) {
+        __threadfence();
+        Sync::sync();
+        if (tid == 0) st_release_gpu(flag, f_inc);
+    }
+    // 4. the rank's last tile: totals and the LB statistics
+    if (blk == a.nblk - 1) {
+        for (int k = tid; k < K1; k += Sync::nthr()) {
+            const int tot = s_off[k] + s_bh[k];
+            const int32_t cnt = (int32_t)(tot < sc.C1 ? tot : sc.C1);
+            sc.stats.hist1[v * K1 + k] = tot;
+            sc.counts1[v * K1 + k] = cnt;
+            if (sc.peer.bases && sc.flat) {             // counts travel with the rows: rcounts[q][src][k % e]
+                const PeerMap &P = sc.peer;
+                const int rk = P.rank0 + v, q = k / P.e;
+                reinterpret_cast<int32_t *>(P.bases[q / P.V] + P.off_rcounts)[((int64_t)(q % P.V) * P.G + rk) * P.e + k % P.e] = cnt;
+            }
+        }
+        // every tile of the rank has published its partials (flag >= aggregate)
+        if (w == 0) {
+            for (int p = lane; p < a.nblk; p += 32) {
+                uint64_t spin = 0;
+                while (ld_acquire_gpu(sc.lb_flag + v * a.nblk + p) < f_agg)
+                    if (++spin > (1ull << 28)) __trap();
+            }
+        }
+        __threadfence();
+        Sync::sync();
+        const int KS = K1 + a.K2;
+        const int64_t rb = (int64_t)v * a.nblk;
+        for (int jb = w; jb < KS + a.K2; jb += Sync::nthr() >> 5) {
+            if (jb < KS) {
+                const double sum = warp_sum_f64(sc.blk_psum + rb * KS + jb, a.nblk, KS);
+                if (lane == 0) {
+                    if (jb < K1) sc.stats.psum1[v * K1 + jb] = sum;
+                    else sc.stats.psum2[v * a.K2 + (jb - K1)] = sum;
+                }
+            } else {
+                const int k = jb - KS;
+                const int c = warp_sum_i32(sc.blk_hist2a + rb * a.K2 + k, a.nblk, a.K2);
+                if (lane == 0) sc.stats.hist2[v * a.K2 + k] = c;
+            }
+        }
+    }
+}
 
 __global__ void __launch_bounds__(GS_THREADS, 1)
 gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, GateTArgs ta) {
@@ -480,11 +588,14 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
     int *s_j = reinterpret_cast<int *>(s_lg + GS_TOK * lds);          // [256]
     int *s_wh = s_j + GS_TOK;                                         // [8][K1]
     int *s_bh = s_wh + 8 * a.K1;                                      // [K1]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(s_bh + a.K1) + 7) & ~(uintptr_t)7);
+    int *s_off = s_bh + a.K1;                                         // [K1] look-back offsets
+    uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(s_off + a.K1) + 7) & ~(uintptr_t)7);
     uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // the call's look-back epoch: read before any CTA can advance it (the last CTA to finish)
+    const int epoch = ta.lookback ? *reinterpret_cast<volatile int *>(ta.epoch_ctr) : 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
@@ -630,6 +741,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                 EpiSync256<0>::sync();
             }
             gate_finish<EpiSync256<0>>(a, s_lg, lds, s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
+            if (ta.lookback) lookback_scan<EpiSync256<0>>(ta, s_bh, s_off, tile, epoch);
             EpiSync256<0>::sync();
         }
     }
@@ -639,19 +751,21 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
     }
-    if (threadIdx.x == 0 && ta.nbuilders > 0) {
-        // every CTA is past its split wait: the last one resets the counters for the next call
+    if (threadIdx.x == 0 && (ta.nbuilders > 0 || ta.lookback)) {
+        // every CTA is past its split wait and has read the epoch: the last one resets the
+        // split counter and advances the look-back epoch for the next call
         __threadfence();
         if (atomicAdd(ta.done, 1) == (int)gridDim.x - 1) {
             *ta.split_ready = 0;
             *ta.done = 0;
+            if (ta.lookback) *ta.epoch_ctr = epoch + 1;
             __threadfence();
         }
     }
 }
 
 size_t gate_tcT_smem(int KW, int K1, int stages) {
-    return 1024 + (size_t)stages * (GS_W_BYTES + GS_X_BYTES) + ((size_t)GS_TOK * gate_lds(KW) + GS_TOK + 9 * K1) * 4 +
+    return 1024 + (size_t)stages * (GS_W_BYTES + GS_X_BYTES) + ((size_t)GS_TOK * gate_lds(KW) + GS_TOK + 10 * K1) * 4 +
            8 + (2 * stages + 4) * 8 + 16;
 }
 
@@ -682,7 +796,9 @@ bool gate_tc_supported(int bf16, int d, int KW) {
     return bf16 && d % GT_BK == 0 && d >= GT_BK && gate_tc_np(KW) <= GT_MAX_NP && encode_fn() != nullptr;
 }
 
-cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, int *gate_sync, cudaStream_t st) {
+cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, int *gate_sync, const Scan1Args *scan,
+                            bool *scanned, cudaStream_t st) {
+    if (scanned) *scanned = false;
     if (a.T == 0) return cudaSuccess;
     if (a.logits || !gate_tc_supported(a.bf16, a.d, a.KW)) return cudaErrorNotSupported;
     if (a.swapped) {
@@ -709,6 +825,14 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
         ta.nbuilders = NPT < grid ? NPT : grid;
         ta.split_ready = gate_sync; ta.done = gate_sync + 1;
         ta.wsplit = wsplit;
+        // the level-1 scan by look-back inside the kernel (SMILE_GATE_LOOKBACK=0: scan1_kernel)
+        const char *lbe = getenv("SMILE_GATE_LOOKBACK");        // read per call (tests switch it)
+        const int lb_env = (lbe && lbe[0] == '0') ? 0 : 1;
+        if (lb_env && scan && scan->lb_flag && scan->lb_inc && a.topk <= 1) {
+            ta.lookback = 1;
+            ta.s = *scan;
+            ta.epoch_ctr = gate_sync + 2;
+        }
         const char *e2 = getenv("SMILE_GATE_SPLIT_KERNEL");      // 1: the separate split kernel (A/B)
         if (e2 && e2[0] == '1') {
             note_launch();
@@ -718,6 +842,7 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
         }
         note_launch();
         launch_k(gate1_tcT_kernel, dim3(grid), dim3(GS_THREADS), smem, st, mX, mW, ta);
+        if (scanned) *scanned = ta.lookback != 0;
         return cudaGetLastError();
     }
     if (a.TB != GT_BM) return cudaErrorNotSupported;

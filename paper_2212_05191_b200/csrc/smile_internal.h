@@ -102,7 +102,7 @@ struct smile_ctx_s {
     const float *d1_gate = nullptr;   // route->gate of the last smile_dispatch(1)
     int nblk1 = 0;             // gate table blocks per rank (TB1 tokens each)
     bool gate_swapped = false; // the tensor-core gate is the swapped-role 256-token kernel
-    int *gate_sync = nullptr;  // [2] swapped gate: split-ready and done counters
+    int *gate_sync = nullptr;  // [3] swapped gate: split-ready, done, look-back epoch
     int nblk2 = 0;             // level-2 ranking blocks per rank
     int *d_err = nullptr;      // sticky device error flag (smile_status)
     int32_t *blk_hist1 = nullptr, *blk_off1 = nullptr, *blk_hist2a = nullptr;
@@ -160,6 +160,7 @@ struct Scan1Args {
     PeerMap peer;            // nblk: table blocks per rank and choice
     int *lb_flag;            // reset for the next fused gate (may be null)
     int nlb;                 // look-back tiles per rank (lb_flag entries)
+    int32_t *lb_inc;         // look-back inclusive prefixes (the swapped gate's in-kernel scan)
     int topk;
 };
 void launch_scan1(const Scan1Args &a, cudaStream_t st);
@@ -308,6 +309,9 @@ int gate_tc_rows(int KW);            // rows of the split-router buffer
 bool gate_tc_supported(int bf16, int d, int KW);
 // a.swapped: the swapped-role kernel, which also builds the split router (counters in
 // gate_sync [2]); else the 128-token kernel (split by router_split_kernel).
-cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, int *gate_sync, cudaStream_t st);
+// With `scan` (lb_flag, lb_inc set) the swapped kernel also runs the level-1 scan by
+// look-back and sets *scanned (then no scan1_kernel is needed).
+cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sms, int *gate_sync, const Scan1Args *scan,
+                            bool *scanned, cudaStream_t st);
 
 }  // namespace smile
