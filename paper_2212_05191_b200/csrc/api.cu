@@ -305,6 +305,8 @@ extern "C" smile_status smile_create(smile_ctx *out, const smile_shape *shape, c
             // look-back state of the fused gate + permute (flags zero between calls)
             const int64_t nt = (int64_t)z.V * ((shape->T + 127) / 128);   // (the fused path's 128-token tiles)
             if (cudaMalloc(&c->lb_flag, (nt > 0 ? nt : 1) * 4) != cudaSuccess ||
+                cudaMalloc(&c->lb_scan_flag, (nt > 0 ? nt : 1) * 4) != cudaSuccess ||
+                cudaMemset(c->lb_scan_flag, 0, (nt > 0 ? nt : 1) * 4) != cudaSuccess ||
                 cudaMalloc(&c->lb_agg, (nt > 0 ? nt : 1) * z.K1 * 4) != cudaSuccess ||
                 cudaMalloc(&c->lb_inc, (nt > 0 ? nt : 1) * z.K1 * 4) != cudaSuccess ||
                 cudaMemset(c->lb_flag, 0, (nt > 0 ? nt : 1) * 4) != cudaSuccess) {
@@ -384,7 +386,7 @@ extern "C" smile_status smile_destroy(smile_ctx c) {
     cudaFree(c->gate_sync);
     cudaFree(c->wsplit);
     cudaFree(c->colsum_ws);
-    cudaFree(c->lb_flag); cudaFree(c->lb_agg); cudaFree(c->lb_inc);
+    cudaFree(c->lb_flag); cudaFree(c->lb_agg); cudaFree(c->lb_inc); cudaFree(c->lb_scan_flag);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     if (c->ev_chunk_front) cudaEventDestroy(c->ev_chunk_front);
@@ -576,7 +578,7 @@ extern "C" smile_status smile_gate_inter(smile_ctx c, const void *x, const float
     bool scanned = false;                    // the swapped tensor-core gate scans by look-back itself
     if (!logits && c->wsplit) {
         Scan1Args sl = s;
-        sl.lb_flag = c->lb_flag; sl.lb_inc = c->lb_inc;
+        sl.lb_flag = c->lb_scan_flag; sl.lb_inc = c->lb_inc;   // epoch-tagged flags of the in-kernel scan
         const cudaError_t e = launch_gate1_tc(a, c->wsplit, c->num_sms, c->gate_sync, &sl, &scanned, S(stream));
         if (e != cudaSuccess) return SMILE_ECUDA;
     } else {

@@ -68,6 +68,16 @@ __global__ void router_split_kernel(const float *__restrict__ w, __nv_bfloat16 *
     }
 }
 
+// In-kernel level-1 scan of the tensor-core gates (a3): flags [V * nblk] tagged with the
+// call's epoch (2 e + 1: the tile's aggregate published, 2 e + 2: its inclusive prefix), so
+// nothing is reset between calls; the last CTA of a call advances *epoch_ctr.
+struct Lookback {
+    int on;
+    Scan1Args s;     // tables (blk_hist1 = aggregates, blk_off1, psum, hist2a), stats, counts1, lb_inc
+    int *flags;
+    int *epoch_ctr;
+};
+
 struct GateTcArgs {
     GateArgs g;
     int NP;          // accumulator columns (3 * KW rounded up to 32)
@@ -79,6 +89,8 @@ struct GateTcArgs {
     int resident_b;  // 1: every CTA builds the split router (NP x d bf16, SWIZZLE_128B K-major)
                      // in its own smem at start from the fp32 W -- no split kernel, and the
                      // pipeline stages carry x only
+    Lookback lb;     // in-kernel level-1 scan (non-fused gates)
+    int *done;       // CTA arrival counter (the last CTA advances the look-back epoch)
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int *p) {
@@ -88,6 +100,111 @@ __device__ __forceinline__ int ld_acquire_gpu(const int *p) {
 }
 __device__ __forceinline__ void st_release_gpu(int *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Level-1 scan of one tile by decoupled look-back (a3; R5, R8): the tile's destination
+// histogram s_bh (gate_finish's block_rank) is already in blk_hist1; publish it, look back
+// over the rank's earlier tiles (warp 0: lane = predecessor, aggregates summed up to the
+// nearest inclusive prefix), write the tile's exclusive offsets to blk_off1 (what the
+// permute adds to the tile-local ranks) and its inclusive prefix.  The rank's LAST tile
+// then holds the totals: hist1, counts1 = min(total, C1) (and FLAT peer counts), and -- once
+// every tile of the rank has published -- reduces the rank's LB statistics over its tiles in
+// tile order (lane = statistic: deterministic).  Tiles run in increasing order on every CTA
+// and every CTA is resident, so every wait terminates.
+template <class Sync>
+__device__ void lookback_scan(const GateArgs &a, const Lookback &lb, const int *s_bh, int *s_off, int tile,
+                              int epoch) {
+    const Scan1Args &sc = lb.s;
+    const int tid = Sync::tid(), lane = tid & 31, w = tid >> 5, NW = Sync::nthr() >> 5;
+    const int K1 = a.K1, v = tile / a.nblk, blk = tile - v * a.nblk;
+    int *flag = lb.flags + tile;
+    const int f_agg = 2 * epoch + 1, f_inc = 2 * epoch + 2;
+    // 1. publish (the first tile of a rank: directly its inclusive prefix)
+    for (int k = tid; k < K1; k += Sync::nthr()) {
+        if (blk == 0) sc.lb_inc[(int64_t)tile * K1 + k] = s_bh[k];
+        s_off[k] = 0;
+    }
+    // the threads that wrote this tile's table entries (blk_hist1, lb_inc: tid < K1; psum /
+    // hist2a: lane 0 of the narrow loops, every lane of the wide ones) make them visible
+    if (lane == 0 || tid < K1 || a.KW >= 32) __threadfence();
+    Sync::sync();
+    if (tid == 0) st_release_gpu(flag, blk == 0 ? f_inc : f_agg);
+    // 2. look back (warp 0)
+    if (blk > 0 && w == 0) {
+        const int base = v * a.nblk;
+        for (int p = blk - 1;; p -= 32) {
+            const int pb = p - lane;
+            int fl = f_inc;                             // before the rank's first tile: zero, inclusive
+            if (pb >= 0) {
+                uint64_t spin = 0;
+                while ((fl = ld_acquire_gpu(lb.flags + base + pb)) < f_agg)
+                    if (++spin > (1ull << 28)) __trap();   // a tile that never publishes: abort, never hang
+            }
+            const unsigned incm = __ballot_sync(kFull, fl == f_inc);
+            const int stop = incm ? __ffs(incm) - 1 : 32;
+            for (int k = 0; k < K1; ++k) {
+                int val = 0;
+                if (pb >= 0 && lane < stop) val = __ldcg(sc.blk_hist1 + ((int64_t)base + pb) * K1 + k);
+                else if (pb >= 0 && lane == stop) val = __ldcg(sc.lb_inc + ((int64_t)base + pb) * K1 + k);
+                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(kFull, val, o);
+                if (lane == 0) s_off[k] += val;
+            }
+            if (incm) break;
+        }
+    }
+    Sync::sync();
+    // 3. offsets for the permute, the inclusive prefix for the successors
+    for (int k = tid; k < K1; k += Sync::nthr()) {
+        sc.blk_off1[(int64_t)tile * K1 + k] = s_off[k];
+        if (blk > 0) sc.lb_inc[(int64_t)tile * K1 + k] = s_off[k] + s_bh[k];
+    }
+    if (blk > 0) {
+        __threadfence();
+        Sync::sync();
+        if (tid == 0) st_release_gpu(flag, f_inc);
+    }
+    // 4. the rank's last tile: totals and the LB statistics
+    if (blk == a.nblk - 1) {
+        for (int k = tid; k < K1; k += Sync::nthr()) {
+            const int tot = s_off[k] + s_bh[k];
+            const int32_t cnt = (int32_t)(tot < sc.C1 ? tot : sc.C1);
+            sc.stats.hist1[v * K1 + k] = tot;
+            sc.counts1[v * K1 + k] = cnt;
+            if (sc.peer.bases && sc.flat) {             // counts travel with the rows: rcounts[q][src][k % e]
+                const PeerMap &P = sc.peer;
+                const int rk = P.rank0 + v, q = k / P.e;
+                reinterpret_cast<int32_t *>(P.bases[q / P.V] + P.off_rcounts)[((int64_t)(q % P.V) * P.G + rk) * P.e + k % P.e] = cnt;
+            }
+        }
+        if (w == 0) {                                   // every tile of the rank has published its partials
+            for (int p = lane; p < a.nblk; p += 32) {
+                uint64_t spin = 0;
+                while (ld_acquire_gpu(lb.flags + v * a.nblk + p) < f_agg)
+                    if (++spin > (1ull << 28)) __trap();
+            }
+        }
+        __threadfence();
+        Sync::sync();
+        const int KS = K1 + a.K2;
+        const int64_t rb = (int64_t)v * a.nblk;
+        for (int cb = w; cb < (KS + 31) / 32; cb += NW) {
+            const int k = cb * 32 + lane;
+            if (k < KS) {
+                double acc = 0.0;
+                for (int p = 0; p < a.nblk; ++p) acc += __ldcg(sc.blk_psum + (rb + p) * KS + k);
+                if (k < K1) sc.stats.psum1[v * K1 + k] = acc;
+                else sc.stats.psum2[v * a.K2 + (k - K1)] = acc;
+            }
+        }
+        for (int cb = w; cb < (a.K2 + 31) / 32; cb += NW) {
+            const int k = cb * 32 + lane;
+            if (k < a.K2) {
+                int c = 0;
+                for (int p = 0; p < a.nblk; ++p) c += __ldcg(sc.blk_hist2a + (rb + p) * a.K2 + k);
+                sc.stats.hist2[v * a.K2 + k] = c;
+            }
+        }
+    }
 }
 
 // Fused level-1 permute (a4) in the gate's epilogue.  The tile's destination histogram
@@ -250,6 +367,7 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 5);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int epoch = ta.lb.on ? *reinterpret_cast<volatile int *>(ta.lb.epoch_ctr) : 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
@@ -413,8 +531,13 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
-            if (grp == 0) finish_tile<EpiSync<0>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
-            else finish_tile<EpiSync<1>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
+            if (grp == 0) {
+                finish_tile<EpiSync<0>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
+                if (ta.lb.on) lookback_scan<EpiSync<0>>(a, ta.lb, s_bh, s_off, tile, epoch);
+            } else {
+                finish_tile<EpiSync<1>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
+                if (ta.lb.on) lookback_scan<EpiSync<1>>(a, ta.lb, s_bh, s_off, tile, epoch);
+            }
         }
     }
     pdl_trigger();
@@ -422,6 +545,15 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    }
+    if (threadIdx.x == 0 && ta.lb.on) {
+        // every CTA has read the epoch: the last one advances it for the next call
+        __threadfence();
+        if (atomicAdd(ta.done, 1) == (int)gridDim.x - 1) {
+            *ta.done = 0;
+            *ta.lb.epoch_ctr = epoch + 1;
+            __threadfence();
+        }
     }
 }
 
@@ -467,112 +599,8 @@ struct GateTArgs {
     // level-1 scan by decoupled look-back inside the kernel (lookback != 0): per-tile flags
     // carry the call's epoch (2 e + 1: aggregate published, 2 e + 2: inclusive prefix), so
     // nothing is reset between calls; the last CTA advances *epoch_ctr
-    int lookback;
-    Scan1Args s;
-    int *epoch_ctr;
+    Lookback lb;     // in-kernel level-1 scan
 };
-
-// Level-1 scan of one tile by decoupled look-back (a3; R5, R8): the tile's destination
-// histogram s_bh (gate_finish's block_rank) is already in blk_hist1; publish it, look back
-// over the rank's earlier tiles (warp 0: lane = predecessor, aggregates summed up to the
-// nearest inclusive prefix), write the tile's exclusive offsets to blk_off1 (what the
-// permute adds to the tile-local ranks) and its inclusive prefix.  The rank's LAST tile
-// then holds the totals: hist1, counts1 = min(total, C1) (and FLAT peer counts), and -- once
-// every tile of the rank has published -- reduces the rank's LB statistics over its tiles in
-// tile order (deterministic).  Tiles run in increasing order on every CTA and every CTA is
-// resident, so every wait terminates.
-template <class Sync>
-__device__ void lookback_scan(const GateTArgs &ta, const int *s_bh, int *s_off, int tile, int epoch) {
-    const GateArgs &a = ta.g;
-    const Scan1Args &sc = ta.s;
-    const int tid = Sync::tid(), lane = tid & 31, w = tid >> 5;
-    const int K1 = a.K1, v = tile / a.nblk, blk = tile - v * a.nblk;
-    int *flag = sc.lb_flag + tile;
-    const int f_agg = 2 * epoch + 1, f_inc = 2 * epoch + 2;
-    // 1. publish (the first tile of a rank: directly its inclusive prefix)
-    for (int k = tid; k < K1; k += Sync::nthr()) {
-        if (blk == 0) sc.lb_inc[(int64_t)tile * K1 + k] = s_bh[k];
-        s_off[k] = 0;
-    }
-    // the threads that wrote this tile's table entries (blk_hist1, lb_inc: tid < K1; psum /
-    // hist2a: lane 0 of the narrow loops, every lane of the wide ones) make them visible
-    if (lane == 0 || tid < K1 || a.KW >= 32) __threadfence();
-    Sync::sync();
-    if (tid == 0) st_release_gpu(flag, blk == 0 ? f_inc : f_agg);
-    // 2. look back (warp 0)
-    if (blk > 0 && w == 0) {
-        const int base = v * a.nblk;
-        for (int p = blk - 1;; p -= 32) {
-            const int pb = p - lane;
-            int fl = f_inc;                             // before the rank's first tile: zero, inclusive
-            if (pb >= 0) {
-                uint64_t spin = 0;
-                while ((fl = ld_acquire_gpu(sc.lb_flag + base + pb)) < f_agg)
-                    if (++spin > (1ull << 28)) __trap();   // a tile that never publishes: abort, never hang
-            }
-            const unsigned incm = __ballot_sync(kFull, fl == f_inc);
-            const int stop = incm ? __ffs(incm) - 1 : 32;
-            for (int k = 0; k < K1; ++k) {
-                int val = 0;
-                if (pb >= 0 && lane < stop) val = __ldcg(sc.blk_hist1 + ((int64_t)base + pb) * K1 + k);
-                else if (pb >= 0 && lane == stop) val = __ldcg(sc.lb_inc + ((int64_t)base + pb) * K1 + k);
-                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(kFull, val, o);
-                if (lane == 0) s_off[k] += val;
-            }
-            if (incm) break;
-        }
-    }
-    Sync::sync();
-    // 3. offsets for the permute, the inclusive prefix for the successors
-    for (int k = tid; k < K1; k += Sync::nthr()) {
-        sc.blk_off1[(int64_t)tile * K1 + k] = s_off[k];
-        if (blk > 0) sc.lb_inc[(int64_t)tile * K1 + k] = s_off[k] + s_bh[k];
-    }
-    if (blk > 0) {
-        __threadfence();
-        Sync::sync();
-        if (tid == 0) st_release_gpu(flag, f_inc);
-    }
-    // 4. the rank's last tile: totals and the LB statistics
-    if (blk == a.nblk - 1) {
-        for (int k = tid; k < K1; k += Sync::nthr()) {
-            const int tot = s_off[k] + s_bh[k];
-            const int32_t cnt = (int32_t)(tot < sc.C1 ? tot : sc.C1);
-            sc.stats.hist1[v * K1 + k] = tot;
-            sc.counts1[v * K1 + k] = cnt;
-            if (sc.peer.bases && sc.flat) {             // counts travel with the rows: rcounts[q][src][k % e]
-                const PeerMap &P = sc.peer;
-                const int rk = P.rank0 + v, q = k / P.e;
-                reinterpret_cast<int32_t *>(P.bases[q / P.V] + P.off_rcounts)[((int64_t)(q % P.V) * P.G + rk) * P.e + k % P.e] = cnt;
-            }
-        }
-        // every tile of the rank has published its partials (flag >= aggregate)
-        if (w == 0) {
-            for (int p = lane; p < a.nblk; p += 32) {
-                uint64_t spin = 0;
-                while (ld_acquire_gpu(sc.lb_flag + v * a.nblk + p) < f_agg)
-                    if (++spin > (1ull << 28)) __trap();
-            }
-        }
-        __threadfence();
-        Sync::sync();
-        const int KS = K1 + a.K2;
-        const int64_t rb = (int64_t)v * a.nblk;
-        for (int jb = w; jb < KS + a.K2; jb += Sync::nthr() >> 5) {
-            if (jb < KS) {
-                const double sum = warp_sum_f64(sc.blk_psum + rb * KS + jb, a.nblk, KS);
-                if (lane == 0) {
-                    if (jb < K1) sc.stats.psum1[v * K1 + jb] = sum;
-                    else sc.stats.psum2[v * a.K2 + (jb - K1)] = sum;
-                }
-            } else {
-                const int k = jb - KS;
-                const int c = warp_sum_i32(sc.blk_hist2a + rb * a.K2 + k, a.nblk, a.K2);
-                if (lane == 0) sc.stats.hist2[v * a.K2 + k] = c;
-            }
-        }
-    }
-}
 
 __global__ void __launch_bounds__(GS_THREADS, 1)
 gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, GateTArgs ta) {
@@ -595,7 +623,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // the call's look-back epoch: read before any CTA can advance it (the last CTA to finish)
-    const int epoch = ta.lookback ? *reinterpret_cast<volatile int *>(ta.epoch_ctr) : 0;
+    const int epoch = ta.lb.on ? *reinterpret_cast<volatile int *>(ta.lb.epoch_ctr) : 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
@@ -741,7 +769,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                 EpiSync256<0>::sync();
             }
             gate_finish<EpiSync256<0>>(a, s_lg, lds, s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
-            if (ta.lookback) lookback_scan<EpiSync256<0>>(ta, s_bh, s_off, tile, epoch);
+            if (ta.lb.on) lookback_scan<EpiSync256<0>>(a, ta.lb, s_bh, s_off, tile, epoch);
             EpiSync256<0>::sync();
         }
     }
@@ -751,14 +779,14 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
     }
-    if (threadIdx.x == 0 && (ta.nbuilders > 0 || ta.lookback)) {
+    if (threadIdx.x == 0 && (ta.nbuilders > 0 || ta.lb.on)) {
         // every CTA is past its split wait and has read the epoch: the last one resets the
         // split counter and advances the look-back epoch for the next call
         __threadfence();
         if (atomicAdd(ta.done, 1) == (int)gridDim.x - 1) {
             *ta.split_ready = 0;
             *ta.done = 0;
-            if (ta.lookback) *ta.epoch_ctr = epoch + 1;
+            if (ta.lb.on) *ta.lb.epoch_ctr = epoch + 1;
             __threadfence();
         }
     }
@@ -829,9 +857,10 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
         const char *lbe = getenv("SMILE_GATE_LOOKBACK");        // read per call (tests switch it)
         const int lb_env = (lbe && lbe[0] == '0') ? 0 : 1;
         if (lb_env && scan && scan->lb_flag && scan->lb_inc && a.topk <= 1) {
-            ta.lookback = 1;
-            ta.s = *scan;
-            ta.epoch_ctr = gate_sync + 2;
+            ta.lb.on = 1;
+            ta.lb.s = *scan;
+            ta.lb.flags = scan->lb_flag;
+            ta.lb.epoch_ctr = gate_sync + 2;
         }
         const char *e2 = getenv("SMILE_GATE_SPLIT_KERNEL");      // 1: the separate split kernel (A/B)
         if (e2 && e2[0] == '1') {
@@ -842,7 +871,7 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
         }
         note_launch();
         launch_k(gate1_tcT_kernel, dim3(grid), dim3(GS_THREADS), smem, st, mX, mW, ta);
-        if (scanned) *scanned = ta.lookback != 0;
+        if (scanned) *scanned = ta.lb.on != 0;
         return cudaGetLastError();
     }
     if (a.TB != GT_BM) return cudaErrorNotSupported;
@@ -891,8 +920,22 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
         attr = true;
     }
     const int grid = ta.ntiles < num_sms ? ta.ntiles : num_sms;
+    // the level-1 scan by look-back inside the kernel (not with the fused permute, which has
+    // its own look-back; SMILE_GATE_LOOKBACK=0: scan1_kernel)
+    {
+        const char *lbe = getenv("SMILE_GATE_LOOKBACK");
+        const int lb_env = (lbe && lbe[0] == '0') ? 0 : 1;
+        if (lb_env && !a.fuse_dispatch && scan && scan->lb_flag && scan->lb_inc && gate_sync && a.topk <= 1) {
+            ta.lb.on = 1;
+            ta.lb.s = *scan;
+            ta.lb.flags = scan->lb_flag;
+            ta.lb.epoch_ctr = gate_sync + 2;
+            ta.done = gate_sync + 1;
+        }
+    }
     note_launch();
     launch_k(gate1_tc_kernel, dim3(grid), dim3(GT_THREADS), smem, st, mX, mW, ta);
+    if (scanned) *scanned = ta.lb.on != 0;
     return cudaGetLastError();
 }
 

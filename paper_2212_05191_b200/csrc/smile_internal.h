@@ -129,6 +129,7 @@ struct smile_ctx_s {
     float *colsum_ws = nullptr;              // bias-gradient partials of smile_expert_ffn_bwd
     int *lb_flag = nullptr;                  // fused gate + permute: look-back flags [V * nblk1]
     int32_t *lb_agg = nullptr, *lb_inc = nullptr;   // tile aggregates / inclusive prefixes [V * nblk1 * K1]
+    int *lb_scan_flag = nullptr;             // the gates' in-kernel level-1 scan: epoch-tagged flags [V * nblk1]
     // smile_forward_host_stream: copy streams and ping-pong events (created with the ctx)
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
