@@ -191,7 +191,13 @@ __device__ void lookback_scan(const GateArgs &a, const Lookback &lb, const int *
             const int k = cb * 32 + lane;
             if (k < KS) {
                 double acc = 0.0;
-                for (int p = 0; p < a.nblk; ++p) acc += __ldcg(sc.blk_psum + (rb + p) * KS + k);
+                for (int p0 = 0; p0 < a.nblk; p0 += 16) {        // 16 loads in flight, summed in tile order
+                    double t[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) t[u] = p0 + u < a.nblk ? __ldcg(sc.blk_psum + (rb + p0 + u) * KS + k) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) acc += t[u];
+                }
                 if (k < K1) sc.stats.psum1[v * K1 + k] = acc;
                 else sc.stats.psum2[v * a.K2 + (k - K1)] = acc;
             }
@@ -200,7 +206,13 @@ __device__ void lookback_scan(const GateArgs &a, const Lookback &lb, const int *
             const int k = cb * 32 + lane;
             if (k < a.K2) {
                 int c = 0;
-                for (int p = 0; p < a.nblk; ++p) c += __ldcg(sc.blk_hist2a + (rb + p) * a.K2 + k);
+                for (int p0 = 0; p0 < a.nblk; p0 += 16) {
+                    int t[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) t[u] = p0 + u < a.nblk ? __ldcg(sc.blk_hist2a + (rb + p0 + u) * a.K2 + k) : 0;
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) c += t[u];
+                }
                 sc.stats.hist2[v * a.K2 + k] = c;
             }
         }
@@ -853,9 +865,11 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
         ta.nbuilders = NPT < grid ? NPT : grid;
         ta.split_ready = gate_sync; ta.done = gate_sync + 1;
         ta.wsplit = wsplit;
-        // the level-1 scan by look-back inside the kernel (SMILE_GATE_LOOKBACK=0: scan1_kernel)
+        // the level-1 scan by look-back inside the kernel: opt-in (SMILE_GATE_LOOKBACK=1) --
+        // measured slower than the separate scan kernel (C2: 83-85 us vs 50 + 4.4 us, the
+        // look-back waits stall the epilogue; profiles/r02_gate_schedule_ab.md)
         const char *lbe = getenv("SMILE_GATE_LOOKBACK");        // read per call (tests switch it)
-        const int lb_env = (lbe && lbe[0] == '0') ? 0 : 1;
+        const int lb_env = (lbe && lbe[0] == '1') ? 1 : 0;   // opt-in: measured slower
         if (lb_env && scan && scan->lb_flag && scan->lb_inc && a.topk <= 1) {
             ta.lb.on = 1;
             ta.lb.s = *scan;
@@ -921,10 +935,10 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
     }
     const int grid = ta.ntiles < num_sms ? ta.ntiles : num_sms;
     // the level-1 scan by look-back inside the kernel (not with the fused permute, which has
-    // its own look-back; SMILE_GATE_LOOKBACK=0: scan1_kernel)
+    // its own look-back): opt-in SMILE_GATE_LOOKBACK=1, measured slower (C4 flat 1.77 ms)
     {
         const char *lbe = getenv("SMILE_GATE_LOOKBACK");
-        const int lb_env = (lbe && lbe[0] == '0') ? 0 : 1;
+        const int lb_env = (lbe && lbe[0] == '1') ? 1 : 0;   // opt-in: measured slower
         if (lb_env && !a.fuse_dispatch && scan && scan->lb_flag && scan->lb_inc && gate_sync && a.topk <= 1) {
             ta.lb.on = 1;
             ta.lb.s = *scan;

@@ -11,6 +11,6 @@ done
 for i in 1 2; do for lb in 1 0; do
   SMILE_GATE_LOOKBACK=$lb timeout 300 python bench.py --steps 50 --no-cpu --no-e2e > $O/bench_c2_lb${lb}_$i.log 2>&1
 done; done
-SMILE_GATE_LOOKBACK=1 timeout 300 python bench.py --config c4 --steps 20 --no-cpu --no-e2e > $O/bench_c4.log 2>&1
+for c in c4 c5; do for lb in 1 0; do SMILE_GATE_LOOKBACK=$lb timeout 300 python bench.py --config $c --steps 20 --no-cpu --no-e2e > $O/bench_${c}_lb$lb.log 2>&1; done; done
 timeout 1500 python -m pytest tests/test_gpu_fullsize.py -q -x > $O/pytest_fullsize.log 2>&1; echo "rc=$?" >> $O/pytest_fullsize.log
 echo done
