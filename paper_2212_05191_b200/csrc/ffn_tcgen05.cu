@@ -721,13 +721,9 @@ int pick_cg(int num_sms, int BN, int64_t rows_per_expert) {
 
 // Sub-tiles per CTA-pair tile: SMILE_FFN_NSUB=2 (two M = 256 sub-tiles sharing each B
 // stage; TMEM holds both accumulators) or 1 (one sub-tile, double-buffered accumulator).
-int pick_nsub() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SMILE_FFN_NSUB");
-        v = (e && e[0] == '2') ? 2 : 1;
-    }
-    return v;
+int pick_nsub() {                                          // read per launch (tests switch it)
+    const char *e = getenv("SMILE_FFN_NSUB");
+    return (e && e[0] == '2') ? 2 : 1;
 }
 
 template <int CG, int NSUB, int EK>
@@ -772,7 +768,9 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
                         cudaStream_t st, float *colsum = nullptr) {
     const int BN = pick_bn(N);
     const int CG = pick_cg(f.num_sms, BN, (int64_t)f.S * f.Cseg);
-    const int NSUB = CG == 2 ? pick_nsub() : 1;
+    // sub-tiles: SMILE_FFN_NSUB=2 (both tile shapes; single CTAs with two 128-row sub-tiles
+    // sharing each B stage halve the B operand bytes of C5's small experts)
+    const int NSUB = pick_nsub();
     CUtensorMap mA, mA128, mB, mD, mD2;
     if (!make_map(&mA, A, rows_total, K, 32)) return cudaErrorNotSupported;        // 32-row strip boxes
     if (!make_map(&mA128, A, rows_total, K, BM)) return cudaErrorNotSupported;     // 128-row tile box
@@ -828,6 +826,7 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
                    : (ek == 1 ? launch_tc<cg, ns, 1>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st) \
                               : launch_tc<cg, ns, 0>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st))
     if (CG == 2 && NSUB == 2) SMILE_LAUNCH_TC(2, 2);
+    if (CG == 1 && NSUB == 2) SMILE_LAUNCH_TC(1, 2);
     if (CG == 2) SMILE_LAUNCH_TC(2, 1);
     SMILE_LAUNCH_TC(1, 1);
 #undef SMILE_LAUNCH_TC

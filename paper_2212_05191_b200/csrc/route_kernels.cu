@@ -663,6 +663,7 @@ __global__ void exchange_copy_kernel(CopyXArgs a) {
 constexpr int kFabricCtas = 16;
 __global__ void fabric_copy_kernel(CopyXArgs a) {
     __shared__ unsigned long long s_w;
+    pdl_wait();
     const int v = blockIdx.y, b = blockIdx.x, NB = gridDim.x;
     const int pos = a.mypos[v];
     const int nvec = (int)(a.rowbytes / 16);
@@ -724,6 +725,7 @@ __global__ void fabric_copy_kernel(CopyXArgs a) {
 // longer than timeout_ns (0 = forever) sets the sticky SMILE_ETIMEOUT flag and returns.
 __global__ void peer_barrier_kernel(char *const *bases, int64_t off_flags, int me, const int32_t *peers, int npeers,
                                     int level, long long *epoch_ctr, unsigned long long timeout_ns, int *err) {
+    pdl_wait();
     if (threadIdx.x != 0) return;
     const long long epoch = *epoch_ctr + 1;
     *epoch_ctr = epoch;
@@ -899,12 +901,13 @@ void launch_peer_barrier(char *const *bases, int64_t off_flags, int me, const in
                          long long *epoch, unsigned long long timeout_ns, int *err, cudaStream_t st) {
     if (npeers <= 0) return;
     note_launch();
-    peer_barrier_kernel<<<1, 32, 0, st>>>(bases, off_flags, me, peers, npeers, level, epoch, timeout_ns, err);
+    launch_k(peer_barrier_kernel, dim3(1), dim3(32), 0, st, bases, off_flags, me, peers, npeers, level, epoch, timeout_ns,
+             err);
 }
 
 void launch_fabric_copy(const CopyXArgs &a, cudaStream_t st) {
     note_launch();
-    fabric_copy_kernel<<<dim3(kFabricCtas, a.V), 256, 0, st>>>(a);
+    launch_k(fabric_copy_kernel, dim3(kFabricCtas, a.V), dim3(256), 0, st, a);
 }
 
 void launch_exchange_copy(const CopyXArgs &a, cudaStream_t st) {
