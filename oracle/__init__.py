@@ -73,6 +73,11 @@ def lib():
         _lib.oracle_route_topk.argtypes = [C.POINTER(_Cfg), C.c_int32, _P] + [_P] * 8
         _lib.oracle_out_rows_topk.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P,
                                               _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]
+        _lib.oracle_backward_topk.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32, C.c_int32] + [_P] * 11 + \
+            [C.c_double] + [_P] * 7
+        _lib.oracle_objective_topk.restype = C.c_double
+        _lib.oracle_objective_topk.argtypes = [C.POINTER(_Cfg), C.c_int32, C.c_int32, C.c_int32] + [_P] * 11 + \
+            [C.c_double]
         _lib.oracle_logits_mt.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]
         _lib.oracle_out_rows_mt.argtypes = _lib.oracle_out_rows.argtypes
         _lib.oracle_threads.restype = C.c_int32
@@ -311,3 +316,32 @@ def out_rows_topk(cfg: Config, r: RouteTopk, x, W1=None, b1=None, W2=None, b2=No
                                _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2), int(identity), rows.shape[0], _ptr(rows),
                                _ptr(out))
     return out
+
+
+def backward_topk(cfg: Config, r: RouteTopk, x, W1, b1, W2, b2, gout, lam=1.0, W=None, logits=None):
+    """oracle_backward_topk: gradients of the top-k objective (fp64).  Returns a dict like
+    backward(): dlogits [G,T,K], dx [G,T,d], dW [K,d] or None, dW1, db1, dW2, db2."""
+    f = lambda a: None if a is None else np.ascontiguousarray(a, np.float32)
+    x, W1, b1, W2, b2, gout, W, logits = map(f, (x, W1, b1, W2, b2, gout, W, logits))
+    G, T, d = x.shape
+    d_ff = W1.shape[-1]
+    NE = W1.shape[0]
+    K = r.K
+    out = dict(dlogits=np.zeros((G, T, K)), dx=np.zeros((G, T, d)), dW=None if W is None else np.zeros((K, d)),
+               dW1=np.zeros((NE, d, d_ff)), db1=np.zeros((NE, d_ff)), dW2=np.zeros((NE, d_ff, d)),
+               db2=np.zeros((NE, d)))
+    lib().oracle_backward_topk(C.byref(cfg._c()), r.k, d, d_ff, _ptr(x), _ptr_or_none(W), _ptr_or_none(logits),
+                               _ptr(r.dest), _ptr(r.keep), _ptr(r.A1), _ptr(W1), _ptr(b1), _ptr(W2), _ptr(b2),
+                               _ptr(gout), lam, _ptr(out["dlogits"]), _ptr(out["dx"]), _ptr_or_none(out["dW"]),
+                               _ptr(out["dW1"]), _ptr(out["db1"]), _ptr(out["dW2"]), _ptr(out["db2"]))
+    return out
+
+
+def objective_topk(cfg: Config, r: RouteTopk, x, W1, b1, W2, b2, gout, lam=1.0, W=None, logits=None) -> float:
+    """oracle_objective_topk: J with the routing decisions of r held fixed (fp64 inputs)."""
+    f = lambda a: None if a is None else np.ascontiguousarray(a, np.float64)
+    x, W1, b1, W2, b2, gout, W, logits = map(f, (x, W1, b1, W2, b2, gout, W, logits))
+    d = x.shape[-1]
+    return float(lib().oracle_objective_topk(C.byref(cfg._c()), r.k, d, W1.shape[-1], _ptr(x), _ptr_or_none(W),
+                                             _ptr_or_none(logits), _ptr(r.dest), _ptr(r.keep), _ptr(r.A1), _ptr(W1),
+                                             _ptr(b1), _ptr(W2), _ptr(b2), _ptr(gout), lam))

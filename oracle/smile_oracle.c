@@ -834,3 +834,147 @@ void oracle_out_rows_topk(const oracle_cfg *c, int32_t k, int32_t d, int32_t d_f
     }
     free(y);
 }
+
+/* ===================================================================================
+ * Backward of the FLAT top-k layer (Eq. 2; readings R29-R32), the chain rule of
+ *     J = sum_{r,t} < gout[r][t], OUT[r][t] > + lam * sum_r loss_r
+ * with OUT = sum_j keep_j p_{e_j}(x) E_{e_j}(x) (p: the fp64 softmax of the fp64 logits)
+ * and loss_r the Switch loss on the choice-0 fractions f (held constant).  The
+ * choices, slots and keeps are those of oracle_route_topk (run on the fp32 logits).
+ *   per kept choice j: dy_j = p_{e_j} gout; dgate_j = <gout, y_j>; the expert's FFN backward
+ *   dl_k = sum_j dgate_j p_{e_j} (delta_{k, e_j} - p_k) + lam a K / T p_k (f_k - sum_i f_i p_i)
+ *   dW += dl x^T;  dx = sum_j W1_{e_j} dz_j + W^T dl.
+ * Outputs (fp64, overwritten): dlogits [G*T*K], dx [G*T*d], dW [K*d] (W != NULL), dW1, db1,
+ * dW2, db2 per expert (as oracle_backward).
+ * =================================================================================== */
+void oracle_backward_topk(const oracle_cfg *c, int32_t k, int32_t d, int32_t d_ff, const float *x, const float *W,
+                          const float *logits, const int32_t *dest, const uint8_t *keep, const int64_t *A1,
+                          const float *W1, const float *b1, const float *W2, const float *b2, const float *gout,
+                          double lam, double *dlogits, double *dx, double *dW, double *dW1, double *db1, double *dW2,
+                          double *db2) {
+    const int64_t G = (int64_t)c->n * c->m, T = c->T, K = G * c->e, NE = K;
+    const int64_t nx = G * T * d;
+    double *xd = (double *)malloc(sizeof(double) * (size_t)nx);
+    for (int64_t i = 0; i < nx; ++i) xd[i] = (double)x[i];
+    double *Wd = NULL, *ld = NULL;
+    if (W) {
+        Wd = (double *)malloc(sizeof(double) * (size_t)(K * d));
+        for (int64_t i = 0; i < K * d; ++i) Wd[i] = (double)W[i];
+    } else {
+        ld = (double *)malloc(sizeof(double) * (size_t)(G * T * K));
+        for (int64_t i = 0; i < G * T * K; ++i) ld[i] = (double)logits[i];
+    }
+    double *L = (double *)malloc(sizeof(double) * (size_t)(G * T * K));
+    logits_f64(c, d, K, xd, Wd, ld, L);
+    memset(dlogits, 0, sizeof(double) * (size_t)(G * T * K));
+    memset(dx, 0, sizeof(double) * (size_t)nx);
+    if (dW) memset(dW, 0, sizeof(double) * (size_t)(K * d));
+    memset(dW1, 0, sizeof(double) * (size_t)(NE * d * d_ff));
+    memset(db1, 0, sizeof(double) * (size_t)(NE * d_ff));
+    memset(dW2, 0, sizeof(double) * (size_t)(NE * d_ff * d));
+    memset(db2, 0, sizeof(double) * (size_t)(NE * d));
+    double *pv = (double *)malloc(sizeof(double) * (size_t)K);
+    double *a = (double *)malloc(sizeof(double) * (size_t)d_ff), *h = (double *)malloc(sizeof(double) * (size_t)d_ff);
+    double *y = (double *)malloc(sizeof(double) * (size_t)d), *dy = (double *)malloc(sizeof(double) * (size_t)d);
+    double *dz = (double *)malloc(sizeof(double) * (size_t)d_ff);
+    double *w1 = (double *)malloc(sizeof(double) * (size_t)(d * d_ff)), *w2 = (double *)malloc(sizeof(double) * (size_t)(d * d_ff));
+    double *bb1 = (double *)malloc(sizeof(double) * (size_t)d_ff), *bb2 = (double *)malloc(sizeof(double) * (size_t)d);
+    double *dg = (double *)malloc(sizeof(double) * (size_t)k);
+    for (int64_t r = 0; r < G; ++r) {
+        for (int64_t t = 0; t < T; ++t) {
+            const int64_t g = r * T + t;
+            double *dl = dlogits + g * K;
+            softmax_d(L + g * K, K, pv);
+            for (int32_t j = 0; j < k; ++j) {
+                const int64_t xj = (int64_t)j * G * T + g;
+                dg[j] = 0.0;
+                if (!keep[xj]) continue;
+                const int64_t ex = dest[xj];
+                for (int64_t z = 0; z < (int64_t)d * d_ff; ++z) { w1[z] = W1[ex * d * d_ff + z]; w2[z] = W2[ex * d_ff * d + z]; }
+                for (int32_t f = 0; f < d_ff; ++f) bb1[f] = b1[ex * d_ff + f];
+                for (int32_t cc = 0; cc < d; ++cc) bb2[cc] = b2[ex * d + cc];
+                ffn_fwd_d(d, d_ff, xd + g * d, w1, bb1, w2, bb2, a, h, y);
+                const double wj = pv[ex];
+                for (int32_t cc = 0; cc < d; ++cc) {
+                    dg[j] += (double)gout[g * d + cc] * y[cc];
+                    dy[cc] = wj * (double)gout[g * d + cc];
+                    db2[ex * d + cc] += dy[cc];
+                }
+                for (int32_t f = 0; f < d_ff; ++f) {
+                    double dh = 0.0;
+                    for (int32_t cc = 0; cc < d; ++cc) {
+                        dW2[(ex * d_ff + f) * d + cc] += h[f] * dy[cc];
+                        dh += w2[(int64_t)f * d + cc] * dy[cc];
+                    }
+                    dz[f] = dh * gelu_d(a[f]);
+                    db1[ex * d_ff + f] += dz[f];
+                }
+                for (int32_t kk = 0; kk < d; ++kk) {
+                    double s = 0.0;
+                    for (int32_t f = 0; f < d_ff; ++f) {
+                        dW1[(ex * d + kk) * d_ff + f] += xd[g * d + kk] * dz[f];
+                        s += w1[(int64_t)kk * d_ff + f] * dz[f];
+                    }
+                    dx[g * d + kk] += s;
+                }
+            }
+            double fp = 0.0;
+            for (int64_t q = 0; q < K; ++q) fp += ((double)A1[r * K + q] / (double)T) * pv[q];
+            for (int64_t q = 0; q < K; ++q) {
+                double v = 0.0;
+                for (int32_t j = 0; j < k; ++j) {
+                    const int64_t ej = dest[(int64_t)j * G * T + g];
+                    v += dg[j] * pv[ej] * ((q == ej ? 1.0 : 0.0) - pv[q]);
+                }
+                const double fq = (double)A1[r * K + q] / (double)T;
+                dl[q] = v + lam * c->alpha * (double)K / (double)T * pv[q] * (fq - fp);
+            }
+            if (Wd) {
+                for (int64_t q = 0; q < K; ++q)
+                    for (int32_t cc = 0; cc < d; ++cc) {
+                        if (dW) dW[q * d + cc] += dl[q] * xd[g * d + cc];
+                        dx[g * d + cc] += dl[q] * Wd[q * d + cc];
+                    }
+            }
+        }
+    }
+    free(xd); free(Wd); free(ld); free(L); free(pv); free(a); free(h); free(y); free(dy); free(dz);
+    free(w1); free(w2); free(bb1); free(bb2); free(dg);
+}
+
+/* The objective J of oracle_backward_topk evaluated in fp64 with the routing decisions
+ * (dest, keep) held fixed (to pin the backward by central finite differences; a caller
+ * checks separately that its perturbations do not flip a decision). */
+double oracle_objective_topk(const oracle_cfg *c, int32_t k, int32_t d, int32_t d_ff, const double *x, const double *W,
+                             const double *logits, const int32_t *dest, const uint8_t *keep, const int64_t *A1,
+                             const double *W1, const double *b1, const double *W2, const double *b2,
+                             const double *gout, double lam) {
+    const int64_t G = (int64_t)c->n * c->m, T = c->T, K = G * c->e;
+    double *L = (double *)malloc(sizeof(double) * (size_t)(G * T * K));
+    logits_f64(c, d, K, x, W, logits, L);
+    double *pv = (double *)malloc(sizeof(double) * (size_t)K), *P = (double *)malloc(sizeof(double) * (size_t)K);
+    double *a = (double *)malloc(sizeof(double) * (size_t)d_ff), *h = (double *)malloc(sizeof(double) * (size_t)d_ff);
+    double *y = (double *)malloc(sizeof(double) * (size_t)d);
+    double J = 0.0;
+    for (int64_t r = 0; r < G; ++r) {
+        memset(P, 0, sizeof(double) * (size_t)K);
+        for (int64_t t = 0; t < T; ++t) {
+            const int64_t g = r * T + t;
+            softmax_d(L + g * K, K, pv);
+            for (int64_t q = 0; q < K; ++q) P[q] += pv[q] / (double)T;
+            for (int32_t j = 0; j < k; ++j) {
+                const int64_t xj = (int64_t)j * G * T + g;
+                if (!keep[xj]) continue;
+                const int64_t ex = dest[xj];
+                ffn_fwd_d(d, d_ff, x + g * d, W1 + ex * (int64_t)d * d_ff, b1 + ex * (int64_t)d_ff,
+                          W2 + ex * (int64_t)d_ff * d, b2 + ex * (int64_t)d, a, h, y);
+                for (int32_t cc = 0; cc < d; ++cc) J += gout[g * d + cc] * pv[ex] * y[cc];
+            }
+        }
+        double l1 = 0.0;
+        for (int64_t q = 0; q < K; ++q) l1 += ((double)A1[r * K + q] / (double)T) * P[q];
+        J += lam * c->alpha * (double)K * l1;
+    }
+    free(L); free(pv); free(P); free(a); free(h); free(y);
+    return J;
+}

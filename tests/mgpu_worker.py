@@ -36,9 +36,10 @@ def main():
         if rank == 0:
             buf.copy_(torch.frombuffer(bytearray(smb.unique_id()), dtype=torch.uint8))
         dist.broadcast(buf, 0)
+        topk = int(c.get("_topk", 1))
         layer = SmileLayer(case.n, case.m, case.e, case.d, case.d_ff, case.T, case.cf, case.dtype, case.mode,
                            nprocs=world, proc=rank, device=local, ffn_impl=case.ffn_impl,
-                           nccl_id=bytes(buf.cpu().numpy().tobytes()))
+                           nccl_id=bytes(buf.cpu().numpy().tobytes()), topk=topk)
         if c.get("_peer"):
             layer.alloc_workspace()
 
@@ -124,7 +125,8 @@ def main():
         for k in rkeys:
             parts = [torch.empty_like(vw[k]) for _ in range(world)]
             dist.all_gather(parts, vw[k].contiguous())
-            routes[k] = torch.cat(parts).cpu().numpy()
+            # top-k: dest1 / slot1 are [k, V, T] choice-major -- ranks along dim 1
+            routes[k] = torch.cat(parts, dim=1 if (topk > 1 and k in ("dest1", "slot1")) else 0).cpu().numpy()
         gathered = {}
         if grads is not None:
             for k, t in grads.items():
@@ -144,6 +146,18 @@ def main():
                 lg_or = None
                 if case.fused:
                     lg_or = oracle.logits(case.x.reshape(-1, case.d), case.w_router).reshape(case.G, case.T, -1)
+                if topk > 1:
+                    # the FLAT top-k layer (Eq. 2, R29-R32) across processes
+                    rt = oracle.route_topk(case.cfg, topk, case.logits)
+                    np.testing.assert_array_equal(routes["dest1"], rt.dest)
+                    np.testing.assert_array_equal(routes["slot1"], rt.slot)
+                    np.testing.assert_array_equal(routes["counts1"], rt.counts)
+                    got = torch.cat(outs).float().cpu().numpy().reshape(-1, case.d)
+                    assert_close_scaled(got, oracle.out_rows_topk(case.cfg, rt, case.x, case.W1, case.b1, case.W2,
+                                                                  case.b2), 2e-2 if case.dtype == "bf16" else 1e-5,
+                                        f"mgpu top-{topk} {c}")
+                    np.testing.assert_allclose(torch.cat(losses).cpu().numpy(), rt.loss, rtol=1e-6)
+                    raise StopIteration
                 r = case.oracle_route()
                 # routing indices, capacity slots, drop masks and counts: bit-exact (north star).
                 # Fused router: the GPU's fp32 logits may differ from the oracle's in the last
@@ -182,6 +196,8 @@ def main():
                     tol = 3e-2 if case.dtype == "bf16" else 1e-4
                     for k, t in gathered.items():
                         assert_close_scaled(t.float().cpu().numpy().reshape(ref[k].shape), ref[k], tol, f"mgpu bwd {k}")
+            except StopIteration:
+                pass
             except AssertionError as ex:
                 failures.append(f"{c}: {ex}")
         torch.cuda.synchronize()

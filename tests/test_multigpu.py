@@ -36,6 +36,11 @@ def _cases(ngpu):
                dict(n=2, m=1, e=2, cf=1.25, dtype="bf16", mode="flat", _peer=True, _graph=True, **base)]
     if ngpu >= 4:
         cs += [dict(n=2, m=2, e=1, cf=1.0, dtype="bf16", mode="bilevel", _peer=True, _graph=True, **base)]
+    # the FLAT top-k layer (Eq. 2) across processes, both exchanges
+    if ngpu >= 2:
+        cs += [dict(n=2, m=2, e=2, cf=1.0, dtype="bf16", mode="flat", _topk=2, **base),
+               dict(n=2, m=2, e=2, cf=1.0, dtype="bf16", mode="flat", _topk=2, _peer=True, **base),
+               dict(n=2, m=1, e=2, cf=0.75, dtype="fp32", mode="flat", _topk=3, _peer=True, **base)]
     # training steps (a16-a19) over both exchanges
     bw = dict(T=400, d=128, d_ff=256, dist="skewed", seed=12)
     if ngpu >= 2:

@@ -105,3 +105,53 @@ def test_ffn_output_is_sum_of_weighted_experts():
                 ex = r.dest[j, rr, t]
                 ref += float(r.w[j, rr, t]) * oracle.ffn_row(x[rr, t], W1[ex], b1[ex], W2[ex], b2[ex])
         np.testing.assert_allclose(out[g], ref, rtol=1e-12, atol=1e-14)
+
+
+def test_backward_topk_k1_equals_top1_backward():
+    """k = 1: the top-k backward equals the FD-pinned top-1 flat backward (oracle_backward)."""
+    cfg = _cfg(2, 2, 2, 40, 0.75)
+    G, K, T, d, d_ff = 4, 8, 40, 8, 12
+    x = synth.tokens(G, T, d, seed=7, dtype="bf16")
+    W = synth.router_weights(K, d, seed=7)
+    lg = oracle.logits(x.reshape(-1, d), W).reshape(G, T, K)
+    W1, b1, W2, b2 = synth.expert_weights(K, d, d_ff, seed=7)
+    gout = np.random.default_rng(3).normal(size=(G, T, d)).astype(np.float32)
+    r1 = oracle.route(cfg, lg)
+    rk = oracle.route_topk(cfg, 1, lg)
+    a = oracle.backward(cfg, r1, x, W1, b1, W2, b2, gout, lam=2.0, W=W)
+    b = oracle.backward_topk(cfg, rk, x, W1, b1, W2, b2, gout, lam=2.0, W=W)
+    for key in ("dlogits", "dx", "dW", "dW1", "db1", "dW2", "db2"):
+        np.testing.assert_allclose(b[key], a[key], rtol=1e-12, atol=1e-14, err_msg=key)
+
+
+@pytest.mark.parametrize("k,cf", [(2, 8.0), (3, 0.6)])
+def test_backward_topk_finite_differences(k, cf):
+    """Central finite differences of the top-k objective (routing decisions held fixed) along
+    random directions of every input: x, the router W, W1, b1, W2, b2."""
+    cfg = _cfg(2, 1, 2, 5, cf)
+    G, K, T, d, d_ff = 2, 4, 5, 4, 6
+    rs = np.random.default_rng(11)
+    x = rs.normal(size=(G, T, d)).astype(np.float32)
+    W = (0.5 * rs.normal(size=(K, d))).astype(np.float32)
+    W1 = (0.5 * rs.normal(size=(K, d, d_ff))).astype(np.float32)
+    b1 = (0.1 * rs.normal(size=(K, d_ff))).astype(np.float32)
+    W2 = (0.5 * rs.normal(size=(K, d_ff, d))).astype(np.float32)
+    b2 = (0.1 * rs.normal(size=(K, d))).astype(np.float32)
+    gout = rs.normal(size=(G, T, d)).astype(np.float32)
+    lg = oracle.logits(x.reshape(-1, d), W).reshape(G, T, K)
+    r = oracle.route_topk(cfg, k, lg)
+    if cf < 1:
+        assert (r.keep == 0).any()
+    grad = oracle.backward_topk(cfg, r, x, W1, b1, W2, b2, gout, lam=3.0, W=W)
+    base = dict(x=x, W=W, W1=W1, b1=b1, W2=W2, b2=b2)
+    names = dict(x="dx", W="dW", W1="dW1", b1="db1", W2="dW2", b2="db2")
+    eps = 1e-6
+    for p, gk in names.items():
+        u = rs.normal(size=base[p].shape)
+        def J(sign):
+            q = {kk: vv.astype(np.float64) for kk, vv in base.items()}
+            q[p] = q[p] + sign * eps * u
+            return oracle.objective_topk(cfg, r, q["x"], q["W1"], q["b1"], q["W2"], q["b2"], gout, lam=3.0, W=q["W"])
+        fd = (J(1) - J(-1)) / (2 * eps)
+        an = float((grad[gk] * u).sum())
+        assert abs(fd - an) <= 1e-6 * max(1.0, abs(an)), (p, fd, an)
