@@ -86,7 +86,8 @@ typedef struct {
     int32_t ffn_impl;       /* smile_ffn_impl */
     int32_t topk;           /* experts per token (Eq. 2): 0 or 1 = the
                                top-1 layers of the paper (Eq. 3); 2..4 = the FLAT top-k layer
-                               (GShard-style, R29-R32).  BILEVEL requires top-1 */
+                               (GShard-style, R29-R32; forward and backward).  BILEVEL requires
+                               top-1 */
 } smile_shape;
 
 /* Sizes derived from a shape (R5, R7, R20, R31):

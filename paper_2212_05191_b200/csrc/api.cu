@@ -1016,6 +1016,7 @@ extern "C" smile_status smile_combine_bwd(smile_ctx c, const void *gout, const v
     a.dlogits = dlogits; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d; a.K1 = c->sz.K1; a.K2 = c->sz.K2;
     a.KW = c->sz.KW; a.C1 = c->sz.C1; a.alpha = alpha; a.beta = beta; a.lam = lam;
     a.flat = c->shape.mode == SMILE_FLAT; a.bf16 = c->shape.dtype == SMILE_BF16; a.peer = peer_of(c);
+    a.topk = c->shape.topk > 1 ? c->shape.topk : 1;
     launch_combine_bwd(a, S(stream));
     return post_launch();
 }
@@ -1064,7 +1065,7 @@ extern "C" smile_status smile_combine_grad(smile_ctx c, const void *ret_rows, co
     Combine1Args a{};
     a.back1 = ret_rows; a.route = *route; a.out = dx; a.V = c->sz.V; a.T = c->shape.T; a.d = c->shape.d;
     a.K1 = c->sz.K1; a.C1 = c->sz.C1; a.bf16 = c->shape.dtype == SMILE_BF16; a.nogate = 1; a.peer = peer_of(c);
-    a.topk = 1;
+    a.topk = c->shape.topk > 1 ? c->shape.topk : 1;            // top-k: dx[t] = sum of the choices' rows
     launch_combine1(a, S(stream));
     return post_launch();
 }
@@ -1163,7 +1164,6 @@ extern "C" smile_status smile_forward(smile_ctx c, const smile_layer_io *io, voi
     smile_ws_view w;
     STEP(smile_forward_ws(c, io->ws, &w));
     const bool train = io->train != 0;
-    if (train && c->shape.topk > 1) return SMILE_ENOTSUP;      // the top-k layer is forward-only
     // inference binds io->out for this call (GEMM 2 may write in-process rows there)
     struct OutBinding {
         smile_ctx c; void *prev;
@@ -1270,7 +1270,6 @@ extern "C" smile_status smile_forward_host_stream(smile_ctx c, const smile_layer
 
 extern "C" smile_status smile_backward(smile_ctx c, const smile_layer_io *io, const smile_grad_io *g, void *stream) {
     if (!c || !io || !g) return SMILE_EINVAL;
-    if (c->shape.topk > 1) return SMILE_ENOTSUP;               // the top-k layer is forward-only
     if (c->shape.T == 0) {
         // the weight gradients are sums over no tokens
         if (!g->dW1 || !g->db1 || !g->dW2 || !g->db2) return SMILE_EINVAL;

@@ -41,6 +41,30 @@ __device__ void level_dlogits_thread(const float *L, int K, int top, float dtop,
     }
 }
 
+// FLAT top-k (Eq. 2, R29-R32): dl_k = sum_j dgate_j p_{e_j} (delta_{k, e_j} - p_k)
+//                                  + coef p_k (f_k - sum_i f_i p_i)        (serial over k)
+__device__ void topk_dlogits_thread(const float *L, int K, const int *e, const float *dg, int topk, float coef,
+                                    const int32_t *hist, float invT, float *dl) {
+    const float mx = L[e[0]];                   // choice 0 is the argmax (R29)
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += expf(L[k] - mx);
+    const float inv = __frcp_rn(s);
+    float pe[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pe[j] = j < topk ? expf(L[e[j]] - mx) * inv : 0.f;
+    float fp = 0.f;
+    for (int k = 0; k < K; ++k) fp += (float)hist[k] * invT * (expf(L[k] - mx) * inv);
+    for (int k = 0; k < K; ++k) {
+        const float pk = expf(L[k] - mx) * inv;
+        const float fk = (float)hist[k] * invT;
+        float v = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < topk) v += dg[j] * pe[j] * ((k == e[j] ? 1.f : 0.f) - pk);
+        dl[k] = v + coef * pk * (fk - fp);
+    }
+}
+
 // a16 + a19: one warp per token.  dgate = <gout, back1[i, slot1]> (fp32); the gradient
 // row gate * gout goes to dsend[i, slot1] (the forward route); dlogits from Eq. (3)'s
 // p_i q_j and Eq. (4)'s LB terms.
@@ -52,16 +76,19 @@ __global__ void combine_bwd_kernel(CombineBwdArgs a) {
     // a warp takes 32 consecutive tokens: their rows one after the other (16-byte
     // vectors, warp-wide dot product for dgate), then lane t computes token t's dlogits
     const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int topk = a.topk > 1 ? a.topk : 1;
     for (int64_t g0 = wg * 32; g0 < total; g0 += warps * 32) {
-      float my_dgate = 0.f;
+      float my_dgate[4] = {0.f, 0.f, 0.f, 0.f};
       for (int tt = 0; tt < 32 && g0 + tt < total; ++tt) {
-        const int64_t g = g0 + tt;
-        const int v = (int)(g / a.T);
-        const int i = a.route.dest1[g];
-        const int s1 = a.route.slot1[g];
+      const int64_t g = g0 + tt;
+      const int v = (int)(g / a.T);
+      for (int jc = 0; jc < topk; ++jc) {        // top-k: every choice of the token (choice-major route)
+        const int64_t gi = (int64_t)jc * total + g;
+        const int i = a.route.dest1[gi];
+        const int s1 = a.route.slot1[gi];
         float dgate = 0.f;
         if (s1 < a.C1) {
-            const float gt = a.route.gate[g];
+            const float gt = a.route.gate[gi];
             const void *bsrc = a.back1;
             void *gdst = a.dsend;
             int64_t brow = ((int64_t)v * a.K1 + i) * a.C1 + s1, grow = brow;
@@ -139,7 +166,10 @@ __global__ void combine_bwd_kernel(CombineBwdArgs a) {
             }
             dgate = warp_sum(acc);
         }
-        if (lane == tt) my_dgate = dgate;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j == jc && lane == tt) my_dgate[j] = dgate;
+      }
       }
       const int64_t g = g0 + lane;
       if (g < total) {
@@ -148,10 +178,17 @@ __global__ void combine_bwd_kernel(CombineBwdArgs a) {
         float *dl = a.dlogits + g * a.KW;
         const float p = a.route.p[g], q = a.route.q[g];
         const float c1 = (float)(a.lam * a.alpha * (double)a.K1) * invT;
-        level_dlogits_thread(L, a.K1, a.route.dest1[g], q * my_dgate, c1, a.stats.hist1 + (int64_t)v * a.K1, invT, dl);
+        if (topk > 1) {
+            int e[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) e[j] = j < topk ? a.route.dest1[(int64_t)j * total + g] : 0;
+            topk_dlogits_thread(L, a.K1, e, my_dgate, topk, c1, a.stats.hist1 + (int64_t)v * a.K1, invT, dl);
+            continue;
+        }
+        level_dlogits_thread(L, a.K1, a.route.dest1[g], q * my_dgate[0], c1, a.stats.hist1 + (int64_t)v * a.K1, invT, dl);
         if (!a.flat) {
             const float c2 = (float)(a.lam * a.beta * (double)a.K2) * invT;
-            level_dlogits_thread(L + a.K1, a.K2, a.route.dest2[g], p * my_dgate, c2,
+            level_dlogits_thread(L + a.K1, a.K2, a.route.dest2[g], p * my_dgate[0], c2,
                                  a.stats.hist2 + (int64_t)v * a.K2, invT, dl + a.K1);
         }
       }

@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(256) combine_topk_kernel(Combine1Args a) {
                 p = static_cast<const char *>(a.back1) + (((int64_t)v * a.K1 + i) * a.C1 + s1) * rb;
             }
             src[nsrc] = p;
-            w[nsrc] = a.route.gate[gi];
+            w[nsrc] = a.nogate ? 1.f : a.route.gate[gi];       // a18 (dX return): rows already carry the gate
             ++nsrc;
         }
         int4 *dst = reinterpret_cast<int4 *>(static_cast<char *>(a.out) + g * rb);

@@ -222,6 +222,7 @@ struct CombineBwdArgs {
     void *dsend; float *dlogits; int V; int64_t T; int d; int K1, K2, KW; int64_t C1;
     double alpha, beta, lam; int flat; int bf16;
     PeerMap peer;            // PEER: back1 rows are loaded from, and gradient rows stored to, their owner
+    int topk;                // FLAT top-k: every choice's gradient row and dgate (Eq. 2)
 };
 void launch_combine_bwd(const CombineBwdArgs &a, cudaStream_t st);
 

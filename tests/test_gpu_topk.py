@@ -92,3 +92,57 @@ def test_topk_rejections():
         SmileLayer(2, 2, 1, 64, 128, 100, 1.0, "bf16", "bilevel", topk=2)    # bi-level is top-1 (Eq. 3)
     with pytest.raises(SmileError):
         SmileLayer(1, 2, 1, 64, 128, 100, 1.0, "bf16", "flat", topk=3)       # k > K
+
+
+@pytest.mark.parametrize("k,dtype,peer,fused,ffn", [(2, "bf16", False, True, "tcgen05"), (2, "bf16", True, False, "tcgen05"),
+                                                    (3, "fp32", False, True, "simt"), (2, "fp32", True, True, "simt")])
+def test_topk_backward(k, dtype, peer, fused, ffn):
+    """Training step of the FLAT top-k layer (forward with GELU' saved + smile_backward)
+    against the pinned top-k backward oracle (tests/test_oracle_topk.py): dlogits, dx, the
+    router gradient and every expert weight / bias gradient; tolerances as the top-1
+    backward (bf16 3e-2, fp32 1e-4, atol = rtol * max|ref|)."""
+    from paper_2212_05191_b200 import SmileLayer
+    n, m, e, T, d, d_ff, cf = 2, 2, 2, 400, 128, 256, 0.75
+    G, K = n * m, n * m * e
+    cfg = oracle.Config(n, m, e, T, cf, flat=True, alpha=0.01)
+    x = synth.tokens(G, T, d, seed=77, dtype=dtype)
+    W1, b1, W2, b2 = synth.expert_weights(K, d, d_ff, seed=77, dtype=dtype)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    t = lambda a, dt=tdt: torch.from_numpy(np.ascontiguousarray(a)).cuda().to(dt)
+    layer = SmileLayer(n, m, e, d, d_ff, T, cf, dtype, "flat", topk=k, ffn_impl=ffn)
+    if peer:
+        layer.enable_peer_exchange()
+    W = synth.router_weights(K, d, seed=77) if fused else None
+    lg_in = None if fused else synth.supplied_logits(G, T, K, seed=77, dist="skewed")
+    out = torch.empty_like(t(x))
+    loss = torch.empty(G, dtype=torch.float64, device="cuda")
+    layer.forward(t(x), t(W1.transpose(0, 2, 1)), t(b1, torch.float32), t(W2.transpose(0, 2, 1)), t(b2, torch.float32),
+                  out, loss, logits=None if fused else t(lg_in, torch.float32),
+                  w_router=t(W, torch.float32) if fused else None, alpha=0.01, beta=0.0, train=True)
+    rs = np.random.default_rng(5)
+    gout_np = rs.normal(size=(G, T, d)).astype(np.float32)
+    if dtype == "bf16":
+        gout_np = synth.round_bf16(gout_np)
+    f32 = dict(dtype=torch.float32, device="cuda")
+    dx = torch.empty_like(out)
+    dW1 = torch.empty(K, d, d_ff, **f32); db1 = torch.empty(K, d_ff, **f32)
+    dW2 = torch.empty(K, d_ff, d, **f32); db2 = torch.empty(K, d, **f32)
+    dWr = torch.empty(K, d, **f32) if fused else None
+    layer.backward(t(gout_np), dx, t(W1), t(W2), dW1, db1, dW2, db2, dW_router=dWr, lam=2.0)
+    torch.cuda.synchronize()
+    assert layer.get_error() == 0
+    lg = layer.view()["logits"].cpu().numpy() if fused else lg_in      # route on the GPU's logits (R3)
+    r = oracle.route_topk(cfg, k, lg)
+    np.testing.assert_array_equal(layer.view()["dest1"].cpu().numpy(), r.dest)
+    assert (r.keep == 0).any()
+    ref = oracle.backward_topk(cfg, r, x, W1, b1, W2, b2, gout_np, lam=2.0, W=W, logits=None if fused else lg_in)
+    tol = 3e-2 if dtype == "bf16" else 1e-4
+    got = dict(dlogits=layer.view()["dlogits"].cpu().numpy(), dx=dx.float().cpu().numpy(), dW1=dW1.cpu().numpy(),
+               db1=db1.cpu().numpy(), dW2=dW2.cpu().numpy(), db2=db2.cpu().numpy())
+    if fused:
+        got["dW"] = dWr.cpu().numpy()
+    for key, gv in got.items():
+        assert_close_scaled(gv, ref[key], tol, f"top-{k} backward {key}")
+    assert_close_scaled(out.float().cpu().numpy().reshape(-1, d), oracle.out_rows_topk(cfg, r, x, W1, b1, W2, b2),
+                        2e-2 if dtype == "bf16" else 1e-5, "top-k training forward output")
+    layer.close()
