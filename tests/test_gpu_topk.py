@@ -114,11 +114,14 @@ def test_topk_backward(k, dtype, peer, fused, ffn):
         layer.enable_peer_exchange()
     W = synth.router_weights(K, d, seed=77) if fused else None
     lg_in = None if fused else synth.supplied_logits(G, T, K, seed=77, dist="skewed")
-    out = torch.empty_like(t(x))
+    # every input stays alive until the backward (it reads x, the router and the logits again)
+    keep = dict(x=t(x), W1t=t(W1.transpose(0, 2, 1)), b1=t(b1, torch.float32), W2t=t(W2.transpose(0, 2, 1)),
+                b2=t(b2, torch.float32), lg=None if fused else t(lg_in, torch.float32),
+                W=t(W, torch.float32) if fused else None)
+    out = torch.empty_like(keep["x"])
     loss = torch.empty(G, dtype=torch.float64, device="cuda")
-    layer.forward(t(x), t(W1.transpose(0, 2, 1)), t(b1, torch.float32), t(W2.transpose(0, 2, 1)), t(b2, torch.float32),
-                  out, loss, logits=None if fused else t(lg_in, torch.float32),
-                  w_router=t(W, torch.float32) if fused else None, alpha=0.01, beta=0.0, train=True)
+    layer.forward(keep["x"], keep["W1t"], keep["b1"], keep["W2t"], keep["b2"], out, loss, logits=keep["lg"],
+                  w_router=keep["W"], alpha=0.01, beta=0.0, train=True)
     rs = np.random.default_rng(5)
     gout_np = rs.normal(size=(G, T, d)).astype(np.float32)
     if dtype == "bf16":
