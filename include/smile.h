@@ -327,7 +327,10 @@ smile_status smile_gate_intra(smile_ctx ctx, const int32_t *recv_meta, int32_t *
  * (rows only, send_ints/recv_ints ignored); `fwd_counts` is the forward trip's
  * per-chunk valid-row counts (level 1: counts1 [V, n]; level 2: counts2 [V, K2];
  * world: counts1 [V, K1]) used by the device-copy path to move only valid rows;
- * NCCL moves whole padded chunks (R25). */
+ * NCCL moves whole padded chunks (R25) -- or, with SMILE_XCHG_EXACT=1 in the environment,
+ * only the valid rows of every (peer, sub-chunk): the counts travel first and the host
+ * reads them (one stream synchronisation per forward trip, so not CUDA-graph capturable;
+ * the reverse trip reuses them). */
 smile_status smile_all2all(smile_ctx ctx, int32_t level, int32_t reverse, const void *send_rows,
                            void *recv_rows, const int32_t *send_ints, int32_t *recv_ints,
                            const int32_t *fwd_counts, void *stream);
