@@ -14,7 +14,10 @@ the split inter/intra communicators), so total work is fixed: "scaling": "strong
 
 A step = one pass of the whole hot path over one batch.  value =
 G*T / (max over ranks of the device time of the step), inputs resident in HBM; L2 is
-flushed (a 256 MiB write) before every timed step, outside its events.  e2e = the same
+flushed before every timed step, outside its events: a 256 MiB write, then a 256 MiB read of
+another buffer (``--flush write+read``, the default), so the write-back of the flush's own
+dirty lines is finished before the step starts instead of being charged to the step's
+first kernel (``--flush write`` keeps the plain write).  e2e = the same
 metric through smile_forward_host with pinned host buffers (H2D of x and D2H of the
 output and loss inside the timed region).
 """
@@ -73,6 +76,8 @@ def parse():
                          "emulation) on the COPY exchange, N = 1 only")
     ap.add_argument("--topk", type=int, default=1,
                     help="experts per token of the FLAT layer (Eq. 2; SURVEY 8(f) row 4); the bi-level layer is top-1")
+    ap.add_argument("--flush", default="write+read", choices=["write+read", "write"],
+                    help="L2 flush between timed steps (write+read: drain the flush's dirty lines)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "copy"],
                     help="peer: fused permute -> peer-store exchange (CUDA IPC over NVLink); copy: device copies / NCCL")
     return ap.parse_args()
@@ -277,6 +282,32 @@ class Addr:
         return self.a
 
 
+class L2Flush:
+    """Empties L2 between timed steps.  Writing 256 MiB (2x the 126 MB L2) evicts every line
+    of the step's data but leaves L2 full of DIRTY lines of the flush buffer, whose write-back
+    to DRAM would otherwise overlap (and be charged to) the next step's first kernel; a read
+    of another 256 MiB buffer after the write drains them, so each step starts from an L2
+    that holds neither its data nor pending write-backs."""
+
+    def __init__(self, dev, how):
+        import torch
+        self.how = how
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        self.r = torch.ones(32 << 20, dtype=torch.int64, device=dev) if how == "write+read" else None
+        self.sink = torch.empty(1, dtype=torch.int64, device=dev)
+
+    def __call__(self):
+        import torch
+        self.w.zero_()
+        if self.r is not None:
+            torch.sum(self.r, dim=(0,), out=self.sink[0])
+
+    def describe(self):
+        return ("flushed (256 MiB write + 256 MiB read of another buffer) before every timed step, "
+                "outside its events" if self.how == "write+read" else
+                "flushed (256 MiB write) before every timed step, outside its events")
+
+
 def make_layer(cfgd, mode, nprocs, proc, dev, ffn, nccl_id, topk=1):
     from paper_2212_05191_b200 import SmileLayer
     L = SmileLayer(cfgd["n"], cfgd["m"], cfgd["e"], cfgd["d"], cfgd["d_ff"], cfgd["T"], cfgd["cf"], cfgd["dtype"],
@@ -362,7 +393,7 @@ def run_pipelined(args):
     Tc = T // c
     tdt = torch.bfloat16 if cfgd["dtype"] == "bf16" else torch.float32
     modes = ["bilevel", "flat"] if args.mode == "both" else [args.mode]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev, args.flush)
 
     def new_layer(ck, mode):
         nid = None
@@ -394,7 +425,7 @@ def run_pipelined(args):
             dist.barrier()
         torch.cuda.synchronize()
         for k in range(args.steps):
-            flush.zero_()
+            flush()
             t0[k].record()
             fn()
             t1[k].record()
@@ -445,7 +476,7 @@ def run_pipelined(args):
                 "data": "synthetic", "config": {"workload": f"{args.config}: {m0} layer fwd through smile_forward_chunked, "
                                                             f"{c} pipelined chunks of T={Tc}/rank on 2 streams (SURVEY 8(f) row 2)",
                                                  "chunks": c, "exchange": "peer", "timing": "median over steps",
-                                                 "l2": "flushed (256 MiB write) before every timed step"},
+                                                 "l2": flush.describe()},
                 "chunked_ms": out_modes, "unchunked_ms": base_modes,
                 "chunked_over_unchunked": {k: base_modes[k] / out_modes[k] for k in out_modes}}
         print(json.dumps(line), flush=True)
@@ -576,7 +607,7 @@ def run_ours(args):
     tdt = torch.bfloat16 if cfgd["dtype"] == "bf16" else torch.float32
     gen = torch.Generator(device=dev)
     results = {}
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev, args.flush)
     sampler = ClockSampler(local, args.clock_ms) if rank == 0 and args.clock_ms > 0 else None
     if sampler:
         sampler.start()
@@ -646,7 +677,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         for k in range(args.steps):
-            flush.zero_()                       # L2 flush outside the step's events
+            flush()                       # L2 flush outside the step's events
             step_fn(L, inp, evs[k])
         torch.cuda.synchronize()
         if dist:
@@ -663,7 +694,7 @@ def run_ours(args):
         lc0 = smb.launch_count()
         t_beg = time.time()
         for k in range(args.steps):
-            flush.zero_()                       # L2 flush outside the step's events
+            flush()                       # L2 flush outside the step's events
             e0[k].record()
             step_fn(L, inp)
             e1[k].record()
@@ -695,7 +726,7 @@ def run_ours(args):
             g1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
             torch.cuda.synchronize()
             for k in range(args.steps):
-                flush.zero_()
+                flush()
                 g0[k].record()
                 cg.replay()
                 g1[k].record()
@@ -915,7 +946,7 @@ def run_ours(args):
                                              "of the COPY exchange go through per-rank emulated NICs -- "
                                              "latency per message + bytes / bandwidth of wall time each; not a "
                                              "real network"),
-                   "l2": "flushed (256 MiB write) before every timed step, outside its events",
+                   "l2": flush.describe(),
                    "timing": "CUDA events per phase on the launching stream; value from the median step"},
         "phase_ms": main["phase_ms"], "phase_ms_note": "per phase: max over ranks of the mean over steps (events on the launching stream)",
         "rank_ms_per_step": main["rank_ms"], "kept_tokens": main["kept"],

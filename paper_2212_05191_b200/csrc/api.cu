@@ -548,9 +548,35 @@ bool pdl_enabled() {
     }
     return v != 0;
 }
+static unsigned long long *g_trace = nullptr;
+static int g_trace_ctas = 0;
+unsigned long long *trace_buffer(const char *name) {
+    const char *e = getenv("SMILE_TRACE");
+    if (!e || strcmp(e, name) != 0) return nullptr;
+    if (!g_trace) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g_trace_ctas = sms;
+        if (cudaMalloc(&g_trace, (size_t)sms * kTraceSlots * 8) != cudaSuccess) return g_trace = nullptr;
+        cudaMemset(g_trace, 0, (size_t)sms * kTraceSlots * 8);
+    }
+    return g_trace;
+}
 }  // namespace smile
 
 extern "C" int64_t smile_launch_count(void) { return (int64_t)smile::g_launches.load(); }
+
+// Diagnostic (not in smile.h): copy the SMILE_TRACE buffer ([CTAs][kTraceSlots] u64) of the
+// last traced launch to host memory; returns the number of CTA rows copied (0: no trace).
+extern "C" int64_t smile_debug_trace(void *host, int64_t bytes) {
+    if (!smile::g_trace || !host) return 0;
+    int64_t rows = bytes / (smile::kTraceSlots * 8);
+    if (rows > smile::g_trace_ctas) rows = smile::g_trace_ctas;
+    if (cudaMemcpy(host, smile::g_trace, (size_t)rows * smile::kTraceSlots * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    return rows;
+}
 
 static smile_status post_launch() {
     return cudaGetLastError() == cudaSuccess ? SMILE_OK : SMILE_ECUDA;

@@ -76,6 +76,7 @@ struct TcArgs {
                                // 2 no stores, 4 no TMEM reads / epilogue math (release only),
                                // 8 TMA stores into rows [0, 1024) only (L2-resident)
     int *err;
+    unsigned long long *trace;   // SMILE_TRACE=ffn1 / ffn2 timeline (smile_internal.h), or null
 };
 
 // Epilogue modes of the grouped GEMM.
@@ -290,6 +291,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     expert_tile_prefix<4 * CG * NSUB>(s_cnt, a.nseg / a.S, a.S, a.e, s_pref, s_warp);   // ends with __syncthreads
     if (CS > 1) cluster_sync_all();                          // peer barriers initialised before any remote arrive
     tc_fence_after();
+    trace_begin(a.trace);
     const uint32_t tmem_base = *tmem_holder;
     const int ntn = a.N / a.BN;
     const int total = s_pref[a.nseg / a.S] * ntn;
@@ -357,19 +359,25 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
+            trace_clock(a.trace, 5);
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
-            // ---------------- MMA issuer (single thread of the leader) ----------------
+        if (leader) {
+            // ---------------- MMA issuer (warp 1 of the leader) ----------------
+            // The whole warp runs the loop so descriptors and loop state stay warp-uniform
+            // (uniform registers; a single-lane loop pays a register-to-uniform broadcast loop
+            // per MMA), and one elected lane issues the MMAs and commits.
             const uint32_t idesc = make_idesc(BM * CG, a.BN);
+            const uint64_t adesc0 = sw128_desc(smem_u32(sA)), bdesc0 = sw128_desc(smem_u32(sB));
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
             // the 4 K = 16 MMAs of one K block of sub-tile / buffer `acc` on stage `st`
+            // (elected lane only)
             auto kblock = [&](int st, int u, int acc, bool first) {
                 const uint32_t tmem_d = tmem_base + acc * ACC_COLS;
-                const uint64_t ad = sw128_desc(smem_u32(sA + st * A_STAGE + u * A_BYTES));
-                const uint64_t bd = sw128_desc(smem_u32(sB + st * b_stage_bytes));
+                const uint64_t ad = adesc0 + (uint64_t)((uint32_t)(st * A_STAGE + u * A_BYTES) >> 4);
+                const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)(st * b_stage_bytes) >> 4);
 #pragma unroll
                 for (int k = 0; k < BK / 16; ++k) {   // +32 B along K inside the 128 B swizzle atom
                     const uint32_t accum = (first && k == 0) ? 0u : 1u;
@@ -387,14 +395,20 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     const int acc = it & 1;
                     mbar_wait(smem_u32(&tempty[acc]), ((uint32_t)(it >> 1) & 1) ^ 1);
                     tc_fence_after();
+                    if (lane == 0 && it < 240) trace_clock(a.trace, 8 + 2 * it);
                     for (int kb = 0; kb < nk; ++kb) {
                         mbar_wait(smem_u32(&full[stage]), phase);
                         tc_fence_after();
-                        kblock(stage, 0, acc, kb == 0);
-                        release(&empty[stage]);
+                        if (elect_one()) {
+                            kblock(stage, 0, acc, kb == 0);
+                            release(&empty[stage]);
+                        }
+                        __syncwarp();
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    release(&tfull[acc]);
+                    if (elect_one()) release(&tfull[acc]);
+                    __syncwarp();
+                    if (lane == 0 && it < 240) trace_clock(a.trace, 9 + 2 * it);
                 } else {
                     // sub-tile u accumulates in buffer u; both are drained after every tile.
                     // The first P K blocks go to sub-tile 0 alone (their stages stay held)
@@ -408,7 +422,8 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     for (int kb = 0; kb < P; ++kb) {
                         mbar_wait(smem_u32(&full[stage]), phase);
                         tc_fence_after();
-                        kblock(stage, 0, 0, kb == 0);
+                        if (elect_one()) kblock(stage, 0, 0, kb == 0);
+                        __syncwarp();
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                     mbar_wait(smem_u32(&tempty[1]), par);
@@ -416,19 +431,26 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     stage = st0;
                     phase = ph0;
                     for (int kb = 0; kb < P; ++kb) {
-                        kblock(stage, 1, 1, kb == 0);
-                        release(&empty[stage]);
+                        if (elect_one()) {
+                            kblock(stage, 1, 1, kb == 0);
+                            release(&empty[stage]);
+                        }
+                        __syncwarp();
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                     for (int kb = P; kb < nk; ++kb) {
                         mbar_wait(smem_u32(&full[stage]), phase);
                         tc_fence_after();
-                        kblock(stage, 0, 0, false);
-                        kblock(stage, 1, 1, false);
-                        release(&empty[stage]);
+                        if (elect_one()) {
+                            kblock(stage, 0, 0, false);
+                            kblock(stage, 1, 1, false);
+                            release(&empty[stage]);
+                        }
+                        __syncwarp();
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    release(&tfull[0]);
+                    if (elect_one()) release(&tfull[0]);
+                    __syncwarp();
                 }
             }
         }
@@ -506,6 +528,8 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             if (NSUB == 1) mbar_wait(smem_u32(&tfull[acc]), (uint32_t)(it >> 1) & 1);
             else if (sub == 0) mbar_wait(smem_u32(&tfull[0]), (uint32_t)it & 1);
             tc_fence_after();
+            const bool tr = warp == 4 && lane == 0 && it < 240;
+            if (tr) trace_clock(a.trace, 520 + 2 * it);
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC_COLS;
             for (int c = c_beg; c < c_end && srows > 0 && !(a.diag & 4); ++c) {
                 if (dgelu && c > c_beg)
@@ -654,6 +678,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                 if (CG == 1) mbar_arrive(smem_u32(&tempty[acc]));
                 else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), lead));   // the leader's MMA waits on it
             }
+            if (tr) trace_clock(a.trace, 521 + 2 * it);
             if (++sub == NSUB) {
                 sub = 0;
                 tile += ncl;
@@ -664,6 +689,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     if (warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     pdl_trigger();
     __syncthreads();
+    trace_end(a.trace);
     if (CS > 1) cluster_sync_all();           // no remote arrive / MMA into a CTA that has left
     if (warp == 2) {
         tc_fence_after();
@@ -818,6 +844,7 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
         if (f.flat_out && !f.out) a.rbases = nullptr;       // nothing to fuse without the output
     }
     a.err = nullptr;
+    a.trace = trace_buffer(mode == EPI_BIAS ? (gelu ? "ffn1" : "ffn2") : "ffn_bwd");
     const size_t smem = smem_bytes(CG, NSUB, a.stages, nbox, a.tma_store, a.box64, a.nseg);
     const int ek = mode == EPI_DGELU ? 2 : (mode == EPI_BIAS_SAVE ? 1 : 0);
     if (a.box64) mD = mD64;                   // the output map with 32 x 64 SWIZZLE_128B boxes

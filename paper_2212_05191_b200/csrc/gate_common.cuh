@@ -68,15 +68,64 @@ __host__ __device__ __forceinline__ int gate_lds(int KW) { return KW | 1; }
 // tok0: global index of the tile's first token; bo = v * nblk + blk: the tile's index in
 // the per-tile tables (with top-k, choice j of the tile is table row (v * topk + j) * nblk
 // + blk).  Must be entered by all Sync threads after the logits are visible to them.
+// Thread-per-token row passes of phase B over one token's logits in smem, four entries per
+// step with their loads issued together (the per-entry load -> use chains of a plain loop
+// bound the epilogue of the wide routers).  Same results, bit for bit, as the plain loops:
+// the arg max is the FIRST index of the strict maximum (R2, R28: '>' over ascending k, a
+// running max in a register), the sum is accumulated in ascending k.
+__device__ __forceinline__ void row_argmax(const float *L, int K, int &arg, float &mx, bool &finite) {
+    float m = L[0];
+    int b = 0;
+    finite &= isfinite(m);
+    int k = 1;
+    for (; k + 3 < K; k += 4) {
+        const float x0 = L[k], x1 = L[k + 1], x2 = L[k + 2], x3 = L[k + 3];
+        finite &= isfinite(x0) & isfinite(x1) & isfinite(x2) & isfinite(x3);
+        if (x0 > m) { m = x0; b = k; }
+        if (x1 > m) { m = x1; b = k + 1; }
+        if (x2 > m) { m = x2; b = k + 2; }
+        if (x3 > m) { m = x3; b = k + 3; }
+    }
+    for (; k < K; ++k) {
+        const float x = L[k];
+        finite &= isfinite(x);
+        if (x > m) { m = x; b = k; }
+    }
+    arg = b;
+    mx = m;
+}
+// e_k = expf(L_k - mx) written over L_k; returns sum_k e_k (ascending k)
+__device__ __forceinline__ float row_exp_sum(float *L, int K, float mx) {
+    float s = 0.f;
+    int k = 0;
+    for (; k + 3 < K; k += 4) {
+        const float e0 = expf(L[k] - mx), e1 = expf(L[k + 1] - mx), e2 = expf(L[k + 2] - mx), e3 = expf(L[k + 3] - mx);
+        L[k] = e0; L[k + 1] = e1; L[k + 2] = e2; L[k + 3] = e3;
+        s += e0; s += e1; s += e2; s += e3;
+    }
+    for (; k < K; ++k) {
+        const float e = expf(L[k] - mx);
+        L[k] = e;
+        s += e;
+    }
+    return s;
+}
 struct GateTok {
     int i;       // level-1 destination of this thread's token (-1: no token)
     int lr;      // its rank among the tile's tokens with the same destination
 };
 
+// Scratch of gate_finish's statistics (shared memory, per tile in flight): s_part [ceil(TB / 32)
+// x KW] fp64 chunk partials, s_h2 [K2] int counts, s_sc [2][TB] fp32 per-token p and q.
+__host__ __device__ __forceinline__ size_t gate_scratch_bytes(int TB, int KW, int K2) {
+    return (size_t)((TB + 31) / 32) * KW * 8 + (size_t)((K2 + 1) & ~1) * 4 + (size_t)2 * TB * 4;
+}
+
 template <class Sync>
-__device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j, int *s_wh, int *s_bh, int64_t tok0,
-                               int nt, int64_t bo) {
+__device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j, int *s_wh, int *s_bh, double *s_part,
+                               int64_t tok0, int nt, int64_t bo, unsigned long long *trace = nullptr, int tslot = 0) {
     const int tid = Sync::tid(), nthr = Sync::nthr();
+    const bool tr = trace && tid == 0;           // SMILE_TRACE=gate: stamps of the epilogue's phases
     const int KW = a.KW, K1 = a.K1, K2 = a.K2;
     const int topk = a.topk > 1 ? a.topk : 1;
     const int64_t VT = (int64_t)a.V * a.T;
@@ -84,16 +133,17 @@ __device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j
     // the softmax entries for the LB statistics, written back over the logits.  Top-k
     // (FLAT, R29): the further choices by repeated first-argmax over the logits not chosen
     // yet, taken before the logits are transformed.
+    int *s_h2 = reinterpret_cast<int *>(s_part + (size_t)((nthr + 31) >> 5) * KW);
+    float *s_p = reinterpret_cast<float *>(s_h2 + ((K2 + 1) & ~1)), *s_q = s_p + nthr;
+    for (int k = tid; k < K2; k += nthr) s_h2[k] = 0;      // (block_rank's barriers order it)
     int i = -1, j = 0;
     int ch[4] = {-1, -1, -1, -1};
     if (tid < nt) {
         float *L = s_lg + tid * lds;
         bool finite = true;
-        for (int k = 0; k < KW; ++k) finite &= isfinite(L[k]);
-        if (!finite) set_err(a.err, SMILE_ENONFINITE);
-        i = 0;
-        for (int k = 1; k < K1; ++k)
-            if (L[k] > L[i]) i = k;
+        // level 1: argmax, then (top-k) the further choices before the logits are transformed
+        float mi;
+        row_argmax(L, K1, i, mi, finite);
         ch[0] = i;
         for (int c = 1; c < topk; ++c) {
             int best = -1;
@@ -107,31 +157,19 @@ __device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j
         // one expf per entry: e_k = exp(r_k - r_max) is kept, the softmax entry for the
         // statistics is e_k * (1 / sum) (within 1.5 ulp of e_k / sum; the LB loss
         // tolerance is 1e-6 relative), and the top-1 probability is 1 / sum exactly.
-        const float mi = L[i];
-        float s1 = 0.f;
-        for (int k = 0; k < K1; ++k) {
-            const float ek = expf(L[k] - mi);
-            L[k] = ek;
-            s1 += ek;
-        }
-        const float p = __frcp_rn(s1);
+        // The rows keep e_k; the statistics pass scales them by p (level 1) or q (level 2)
+        // as it reads them (the same fp32 products e_k * p, e_k * q).
+        const float p = __frcp_rn(row_exp_sum(L, K1, mi));
         float q = 1.f;
         if (!a.flat) {
             float *L2 = L + K1;
-            j = 0;
-            for (int k = 1; k < K2; ++k)
-                if (L2[k] > L2[j]) j = k;
-            const float mj = L2[j];
-            float s2 = 0.f;
-            for (int k = 0; k < K2; ++k) {
-                const float ek = expf(L2[k] - mj);
-                L2[k] = ek;
-                s2 += ek;
-            }
-            q = __frcp_rn(s2);
-            for (int k = 0; k < K2; ++k) L2[k] *= q;
+            float mj;
+            row_argmax(L2, K2, j, mj, finite);
+            q = __frcp_rn(row_exp_sum(L2, K2, mj));
         }
-        for (int k = 0; k < K1; ++k) L[k] *= p;
+        if (!finite) set_err(a.err, SMILE_ENONFINITE);
+        s_p[tid] = p;
+        s_q[tid] = q;
         const int64_t g = tok0 + tid;
         a.route.dest1[g] = i;
         a.route.dest2[g] = j;
@@ -140,11 +178,12 @@ __device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j
         a.route.gate[g] = __fmul_rn(p, q);
         for (int c = 1; c < topk; ++c) {              // Eq. (2) weights p_e of the further choices (R30)
             a.route.dest1[c * VT + g] = ch[c];
-            a.route.gate[c * VT + g] = L[ch[c]];
+            a.route.gate[c * VT + g] = L[ch[c]] * p;
         }
         if (i < 0 || i >= K1) set_err(a.err, SMILE_EINDEX);
     }
     s_j[tid] = (tid < nt) ? j : -1;
+    if (tr) trace_clock(trace, tslot);
 
     // Phase C: tile-local capacity rank of dest1 (R5, R8) -- per choice with top-k, whose
     // tables are laid out choice-major per rank so the scan gives choice-major slots (R31).
@@ -153,58 +192,52 @@ __device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j
     const int lr = block_rank<Sync>(i, K1, s_wh, s_bh);
     if (tid < nt) a.route.slot1[tok0 + tid] = lr;
     for (int k = tid; k < K1; k += nthr) a.blk_hist1[bo0 * K1 + k] = s_bh[k];
+    if (tr) trace_clock(trace, tslot + 1);
     for (int c = 1; c < topk; ++c) {
         Sync::sync();                                             // s_bh of the previous choice consumed
         const int lrc = block_rank<Sync>(tid < nt ? ch[c] : -1, K1, s_wh, s_bh);
         if (tid < nt) a.route.slot1[c * VT + tok0 + tid] = lrc;
         for (int k = tid; k < K1; k += nthr) a.blk_hist1[(bo0 + (int64_t)c * a.nblk) * K1 + k] = s_bh[k];
     }
-    // LB statistics partials of the tile (fp64 for the probability sums), deterministic
-    // (fixed summation order).  Wide routers (KW >= 32): a warp per block of 32
-    // statistics, lane = statistic, tokens in ascending order over 4 interleaved fp64
-    // accumulators (conflict-free row reads; the per-statistic shuffle trees of the narrow
-    // case cost C5's 66-wide gate most of its epilogue).  Narrow routers: one warp per
-    // statistic, lanes stride over tokens, fixed butterfly.
-    if (KW >= 32) {
+    // LB statistics partials of the tile: fp64 sums of the probabilities (R13) and the
+    // level-2 top-1 counts.  Sums: per 32-token chunk c and statistic k, four interleaved
+    // accumulators over the chunk's tokens in ascending order, then the chunks in ascending
+    // order -- a fixed order that depends only on the tile's token count (deterministic, the
+    // same in every kernel that calls this), with the (chunk, 32-statistic block) items
+    // spread over all warps of Sync.  Counts: warp-aggregated shared-memory adds (exact).
+    {
         const int lane = tid & 31, w = tid >> 5, NW = nthr >> 5;
-        for (int cb = w; cb < (KW + 31) / 32; cb += NW) {
-            const int k = cb * 32 + lane;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const int jj = (tid < nt) ? j : -1;
+        const unsigned peers = __match_any_sync(kFull, jj);
+        if (jj >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_h2[jj], __popc(peers));
+        const int nch = (nt + 31) >> 5, ncb = (KW + 31) >> 5;
+        for (int item = w; item < nch * ncb; item += NW) {
+            const int c = item / ncb, k = (item - c * ncb) * 32 + lane;
             if (k < KW) {
-                int tt = 0;
-                for (; tt + 3 < nt; tt += 4) {
-                    a0 += (double)s_lg[tt * lds + k];
-                    a1 += (double)s_lg[(tt + 1) * lds + k];
-                    a2 += (double)s_lg[(tt + 2) * lds + k];
-                    a3 += (double)s_lg[(tt + 3) * lds + k];
+                const float *sc = k < K1 ? s_p : s_q;             // softmax entry = e_k * p or e_k * q
+                const int t1 = min(nt, c * 32 + 32);
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                int tt = c * 32;
+                for (; tt + 3 < t1; tt += 4) {
+                    a0 += (double)(s_lg[tt * lds + k] * sc[tt]);
+                    a1 += (double)(s_lg[(tt + 1) * lds + k] * sc[tt + 1]);
+                    a2 += (double)(s_lg[(tt + 2) * lds + k] * sc[tt + 2]);
+                    a3 += (double)(s_lg[(tt + 3) * lds + k] * sc[tt + 3]);
                 }
-                for (; tt < nt; ++tt) a0 += (double)s_lg[tt * lds + k];
-                a.blk_psum[bo0 * (K1 + K2) + k] = (a0 + a1) + (a2 + a3);
+                for (; tt < t1; ++tt) a0 += (double)(s_lg[tt * lds + k] * sc[tt]);
+                s_part[c * KW + k] = (a0 + a1) + (a2 + a3);
             }
         }
-        for (int cb = w; cb < (K2 + 31) / 32; cb += NW) {
-            const int k = cb * 32 + lane;
-            int c = 0;
-            for (int tt = 0; tt < nt; ++tt) c += (s_j[tt] == k);
-            if (k < K2) a.blk_hist2a[bo0 * K2 + k] = c;
-        }
-        if (a.flat && tid == 0) a.blk_psum[bo0 * (K1 + K2) + K1] = (double)nt;
-    } else {
-        const int lane = tid & 31, w = tid >> 5, NW = nthr >> 5;
-        for (int k = w; k < KW; k += NW) {
+        Sync::sync();
+        for (int k = tid; k < KW; k += nthr) {
             double acc = 0.0;
-            for (int tt = lane; tt < nt; tt += 32) acc += (double)s_lg[tt * lds + k];
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-            if (lane == 0) a.blk_psum[bo0 * (K1 + K2) + k] = acc;
+            for (int c = 0; c < nch; ++c) acc += s_part[c * KW + k];
+            a.blk_psum[bo0 * (K1 + K2) + k] = acc;
         }
-        for (int k = w; k < K2; k += NW) {
-            int c = 0;
-            for (int tt = lane; tt < nt; tt += 32) c += (s_j[tt] == k);
-            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-            if (lane == 0) a.blk_hist2a[bo0 * K2 + k] = c;
-        }
+        for (int k = tid; k < K2; k += nthr) a.blk_hist2a[bo0 * K2 + k] = s_h2[k];
         if (a.flat && tid == 0) a.blk_psum[bo0 * (K1 + K2) + K1] = (double)nt;
     }
+    if (tr) trace_clock(trace, tslot + 2);
     return GateTok{i, topk > 1 ? -1 : lr};
 }
 

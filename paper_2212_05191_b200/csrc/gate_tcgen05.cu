@@ -91,6 +91,7 @@ struct GateTcArgs {
                      // pipeline stages carry x only
     Lookback lb;     // in-kernel level-1 scan (non-fused gates)
     int *done;       // CTA arrival counter (the last CTA advances the look-back epoch)
+    unsigned long long *trace;   // SMILE_TRACE=gate timeline (smile_internal.h), or null
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int *p) {
@@ -342,7 +343,8 @@ __device__ void fused_dispatch(const GateArgs &a, const GateTok tk, const int *s
 // gate's phases B and C, and (fused) the level-1 permute of the tile.
 template <class Sync>
 __device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int *s_j, int *s_wh, int *s_bh,
-                                            int *s_off, int64_t tok0, int nt, int tile) {
+                                            double *s_part, int *s_off, int64_t tok0, int nt, int tile,
+                                            unsigned long long *trace = nullptr, int tslot = 0) {
     Sync::sync();
     if (a.logits_out) {
         const int lds = gate_lds(a.KW);
@@ -350,7 +352,8 @@ __device__ __forceinline__ void finish_tile(const GateArgs &a, float *s_lg, int 
             a.logits_out[tok0 * a.KW + i] = s_lg[(i / a.KW) * lds + i % a.KW];
         Sync::sync();
     }
-    const GateTok tk = gate_finish<Sync>(a, s_lg, gate_lds(a.KW), s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
+    const GateTok tk = gate_finish<Sync>(a, s_lg, gate_lds(a.KW), s_j, s_wh, s_bh, s_part, tok0, nt, (int64_t)tile, trace,
+                                         tslot);
     if (a.fuse_dispatch) fused_dispatch<Sync>(a, tk, s_bh, s_off, tok0, nt, tile);
     Sync::sync();
 }
@@ -369,9 +372,12 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     unsigned char *sA = base;
     unsigned char *sB = sA + ST * a_bytes;                   // resident: [d / 64][NP rows][128 B]
     const int b_region = resb ? NP * a.d * 2 : ST * b_bytes;
-    // per epilogue group g: logits [128][lds] | s_j [128] | s_wh [4][K1] | s_bh [K1]
+    // per epilogue group g: gate_finish scratch (fp64 first) | logits [128][lds] | s_j [128] |
+    // s_wh [4][K1] | s_bh [K1] | s_off [K1] (fused permute); an even int count per group keeps
+    // every group's scratch 8-byte aligned
     const int lds = gate_lds(KW);
-    const int grp_ints = GT_BM * lds + GT_BM + 6 * a.K1;     // + s_off [K1] (fused permute)
+    const int scr_ints = (int)(gate_scratch_bytes(GT_BM, KW, a.K2) / 4);
+    const int grp_ints = (scr_ints + GT_BM * lds + GT_BM + 6 * a.K1 + 1) & ~1;
     int *grp0 = reinterpret_cast<int *>(sB + b_region);
     uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(grp0 + ta.nbuf * grp_ints) + 7) & ~(uintptr_t)7);
     uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
@@ -404,6 +410,7 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    trace_begin(ta.trace);
     const uint32_t tmem_base = *tmem_holder;
     const int nk = a.d / (GT_BK * nsub);
     const int nbuf = ta.nbuf;
@@ -465,48 +472,59 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
             }
+            trace_clock(ta.trace, 5);
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer ----------------
-            if (resb) mbar_wait(smem_u32(b_ready), 0);
-            const uint32_t idesc = make_idesc(GT_BM, NPc);
-            int stage = 0;
-            uint32_t phase = 0;
-            int it = 0;
-            for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
-                const int buf = it % nbuf;
-                const uint32_t use = (uint32_t)(it / nbuf) & 1;
-                mbar_wait(smem_u32(&tempty[buf]), use ^ 1);
+        // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform descriptors,
+        // advanced by adding 16-byte units to the start-address field), one elected lane issues
+        if (resb) mbar_wait(smem_u32(b_ready), 0);
+        const uint32_t idesc = make_idesc(GT_BM, NPc);
+        const uint64_t adesc0 = sw128_desc(smem_u32(sA)), bdesc0 = sw128_desc(smem_u32(sB));
+        const uint32_t a_st = (uint32_t)a_bytes >> 4, b_st = (uint32_t)b_bytes >> 4;
+        const uint32_t b_sub = (uint32_t)(NP * 128) >> 4, b_half = (uint32_t)(NPc * 128) >> 4;
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
+            const int buf = it % nbuf;
+            const uint32_t use = (uint32_t)(it / nbuf) & 1;
+            mbar_wait(smem_u32(&tempty[buf]), use ^ 1);
+            tc_fence_after();
+            if (lane == 0 && it < 120) trace_clock(ta.trace, 8 + 2 * it);
+            const uint32_t tmem_d = tmem_base + buf * NP;
+            for (int kb = 0; kb < nk; ++kb) {
+                mbar_wait(smem_u32(&full[stage]), phase);
                 tc_fence_after();
-                const uint32_t tmem_d = tmem_base + buf * NP;
-                for (int kb = 0; kb < nk; ++kb) {
-                    mbar_wait(smem_u32(&full[stage]), phase);
-                    tc_fence_after();
+                if (elect_one()) {
                     for (int u = 0; u < nsub; ++u) {
-                        const uint64_t ad = sw128_desc(smem_u32(sA + stage * a_bytes + u * GT_A_BYTES));
+                        const uint64_t ad = adesc0 + (uint64_t)(stage * a_st + u * (GT_A_BYTES >> 4));
+                        const uint64_t bd = bdesc0 + (uint64_t)(resb ? (uint32_t)(kb * nsub + u) * b_sub
+                                                                      : stage * b_st + u * b_sub);
 #pragma unroll
-                        for (int k = 0; k < GT_BK / 16; ++k)
-                            for (int h = 0; h < nchunk_n; ++h) {
-                                const uint64_t bd = sw128_desc(smem_u32(
-                                    resb ? sB + ((size_t)(kb * nsub + u) * NP + h * NPc) * 128
-                                         : sB + stage * b_bytes + u * NP * 128 + h * NPc * 128));
-                                mma_bf16(tmem_d + h * NPc, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc,
-                                         (kb | u | k) ? 1u : 0u);
-                            }
+                        for (int k = 0; k < GT_BK / 16; ++k) {
+                            const uint32_t acc = (kb | u | k) ? 1u : 0u;
+                            mma_bf16(tmem_d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, acc);
+                            if (nchunk_n == 2)
+                                mma_bf16(tmem_d + NPc, ad + (uint64_t)(2 * k), bd + (uint64_t)(b_half + 2 * k), idesc,
+                                         acc);
+                        }
                     }
                     mma_commit(smem_u32(&empty[stage]));
-                    if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(smem_u32(&tfull[buf]));
+                __syncwarp();
+                if (++stage == ST) { stage = 0; phase ^= 1; }
             }
+            if (elect_one()) mma_commit(smem_u32(&tfull[buf]));
+            __syncwarp();
+            if (lane == 0 && it < 120) trace_clock(ta.trace, 9 + 2 * it);
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: thread = token (TMEM lane) ----------------
         const int grp = (warp - 4) >> 2;
         const int q = warp & 3;
         const int row = q * 32 + lane;
-        float *s_lg = reinterpret_cast<float *>(grp0 + grp * grp_ints);
+        double *s_part = reinterpret_cast<double *>(grp0 + grp * grp_ints);
+        float *s_lg = reinterpret_cast<float *>(grp0 + grp * grp_ints + scr_ints);
         int *s_j = reinterpret_cast<int *>(s_lg + GT_BM * lds);
         int *s_wh = s_j + GT_BM;
         int *s_bh = s_wh + 4 * a.K1;
@@ -524,36 +542,67 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
             const int buf = it % nbuf;
             mbar_wait(smem_u32(&tfull[buf]), (uint32_t)(it / nbuf) & 1);
             tc_fence_after();
+            const bool tr = q == 0 && lane == 0 && it < 120;
+            if (tr) trace_clock(ta.trace, 256 + 4 * it);
             const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + buf * NP;
-            // logit k = (piece0 + piece1) + piece2 from columns 3k, 3k+1, 3k+2
-            float accv = 0.f;
-            for (int c = 0; c < NP / 32; ++c) {
-                float vv[32];
-                tmem_ld32(tb + c * 32, vv);
-                int k = (c * 32) / 3, pc = (c * 32) - 3 * k;
+            // logit k = (piece0 + piece1) + piece2 from columns 3k, 3k+1, 3k+2: 32 logits per
+            // group of three 32-column loads in flight (one wait), unrolled so every column's
+            // register is fixed at compile time.  The last group may read past this buffer's
+            // NP columns (into the other buffer or unused columns: discarded, k >= KW); when it
+            // would pass the 512 allocated columns, the column-at-a-time loop instead.
+            const int ng = (KW + 31) / 32;
+            if (buf * NP + ng * 96 <= 512) {
+                for (int g3 = 0; g3 < ng; ++g3) {
+                    float v0[32], v1[32], v2[32];
+                    tmem_ld32_nowait(tb + g3 * 96, v0);
+                    tmem_ld32_nowait(tb + g3 * 96 + 32, v1);
+                    tmem_ld32_nowait(tb + g3 * 96 + 64, v2);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    if (k < KW) {
-                        accv = pc == 0 ? vv[i] : accv + vv[i];
-                        if (pc == 2) s_lg[row * lds + k] = accv;
+                    for (int i = 0; i < 32; ++i) {
+                        const int f = 3 * i;
+                        const float x0 = f < 32 ? v0[f] : f < 64 ? v1[f - 32] : v2[f - 64];
+                        const float x1 = f + 1 < 32 ? v0[f + 1] : f + 1 < 64 ? v1[f - 31] : v2[f - 63];
+                        const float x2 = f + 2 < 32 ? v0[f + 2] : f + 2 < 64 ? v1[f - 30] : v2[f - 62];
+                        const int k = g3 * 32 + i;
+                        if (k < KW) s_lg[row * lds + k] = (x0 + x1) + x2;
                     }
-                    if (++pc == 3) { pc = 0; ++k; }
+                }
+            } else {
+                float accv = 0.f;
+                for (int c = 0; c < NP / 32; ++c) {
+                    float vv[32];
+                    tmem_ld32(tb + c * 32, vv);
+                    int k = (c * 32) / 3, pc = (c * 32) - 3 * k;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        if (k < KW) {
+                            accv = pc == 0 ? vv[i] : accv + vv[i];
+                            if (pc == 2) s_lg[row * lds + k] = accv;
+                        }
+                        if (++pc == 3) { pc = 0; ++k; }
+                    }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+            if (tr) trace_clock(ta.trace, 257 + 4 * it);
             if (grp == 0) {
-                finish_tile<EpiSync<0>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
+                finish_tile<EpiSync<0>>(a, s_lg, s_j, s_wh, s_bh, s_part, s_off, tok0, nt, tile, it < 100 ? ta.trace : nullptr,
+                                        600 + 4 * it);
                 if (ta.lb.on) lookback_scan<EpiSync<0>>(a, ta.lb, s_bh, s_off, tile, epoch);
             } else {
-                finish_tile<EpiSync<1>>(a, s_lg, s_j, s_wh, s_bh, s_off, tok0, nt, tile);
+                finish_tile<EpiSync<1>>(a, s_lg, s_j, s_wh, s_bh, s_part, s_off, tok0, nt, tile, it < 100 ? ta.trace : nullptr,
+                                        600 + 4 * it);
                 if (ta.lb.on) lookback_scan<EpiSync<1>>(a, ta.lb, s_bh, s_off, tile, epoch);
             }
+            if (tr) trace_clock(ta.trace, 258 + 4 * it);
         }
     }
     pdl_trigger();
     __syncthreads();
+    trace_end(ta.trace);
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
@@ -608,10 +657,14 @@ struct GateTArgs {
     int nbuilders;   // CTAs that build the split router (0: built by router_split_kernel)
     int *split_ready, *done;
     __nv_bfloat16 *wsplit;   // [NPT, d] the split router
+    int resw;        // 1: every CTA builds the split router into its own smem (NPT x d bf16,
+                     // resident; small routers) and the stages carry x only -- no global split,
+                     // no publish / poll before the first MMA
     // level-1 scan by decoupled look-back inside the kernel (lookback != 0): per-tile flags
     // carry the call's epoch (2 e + 1: aggregate published, 2 e + 2: inclusive prefix), so
     // nothing is reset between calls; the last CTA advances *epoch_ctr
     Lookback lb;     // in-kernel level-1 scan
+    unsigned long long *trace;   // SMILE_TRACE=gate timeline (smile_internal.h), or null
 };
 
 __global__ void __launch_bounds__(GS_THREADS, 1)
@@ -622,16 +675,23 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
     const int ST = ta.stages, KW = a.KW, NQ = ta.NPT / 32;
     unsigned char *base = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sW = base;
-    unsigned char *sX = sW + ST * GS_W_BYTES;
+    const bool resw = ta.resw != 0;
+    // resident: [d / 64][NPT rows][128 B] (4 KB-aligned k blocks).  The M = 128 MMA also reads
+    // rows NPT..127 past each block -- the next blocks', or the x stages' bytes after the last
+    // one: they only feed TMEM lanes >= NPT, which the epilogue never reads
+    unsigned char *sX = sW + (resw ? (size_t)ta.NPT * a.d * 2 : (size_t)ST * GS_W_BYTES);
     const int lds = gate_lds(KW);
     float *s_lg = reinterpret_cast<float *>(sX + ST * GS_X_BYTES);    // [256][lds]
     int *s_j = reinterpret_cast<int *>(s_lg + GS_TOK * lds);          // [256]
     int *s_wh = s_j + GS_TOK;                                         // [8][K1]
     int *s_bh = s_wh + 8 * a.K1;                                      // [K1]
     int *s_off = s_bh + a.K1;                                         // [K1] look-back offsets
-    uint64_t *bars = reinterpret_cast<uint64_t *>(((uintptr_t)(s_off + a.K1) + 7) & ~(uintptr_t)7);
+    double *s_part = reinterpret_cast<double *>(((uintptr_t)(s_off + a.K1) + 7) & ~(uintptr_t)7);   // gate_finish scratch
+    uint64_t *bars = reinterpret_cast<uint64_t *>(
+        ((uintptr_t)s_part + gate_scratch_bytes(GS_TOK, KW, a.K2) + 7) & ~(uintptr_t)7);
     uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 4);
+    uint64_t *w_ready = bars + 2 * ST + 4;                      // resident split built (8 warps)
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 5);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // the call's look-back epoch: read before any CTA can advance it (the last CTA to finish)
@@ -645,6 +705,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
             mbar_init(smem_u32(&tfull[s]), 1);
             mbar_init(smem_u32(&tempty[s]), 8);
         }
+        mbar_init(smem_u32(w_ready), 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0 && lane == 0) {
@@ -659,6 +720,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    trace_begin(ta.trace);
     const uint32_t tmem_base = *tmem_holder;
     const int nk = a.d / GT_BK;
 
@@ -676,9 +738,10 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full[stage]);
-                    mbar_arrive_tx(fb, GS_W_BYTES + GS_X_BYTES);
+                    mbar_arrive_tx(fb, resw ? GS_X_BYTES : GS_W_BYTES + GS_X_BYTES);
                     tma_load_2d(smem_u32(sX + stage * GS_X_BYTES), &mapX, kb * GT_BK, row0, fb);
-                    if (wready) {
+                    if (resw) {
+                    } else if (wready) {
                         tma_load_2d(smem_u32(sW + stage * GS_W_BYTES), &mapW, kb * GT_BK, 0, fb);
                     } else if (++npend == ST) {
                         // stages 0..ST-1 hold k blocks 0..ST-1 of this CTA's first tile(s)
@@ -687,6 +750,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                         for (int i = 0; i < ST; ++i)
                             tma_load_2d(smem_u32(sW + i * GS_W_BYTES), &mapW, (i % nk) * GT_BK, 0, smem_u32(&full[i]));
                         wready = true;
+                        trace_clock(ta.trace, 4);
                     }
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
@@ -697,22 +761,28 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                 for (int i = 0; i < npend; ++i)
                     tma_load_2d(smem_u32(sW + i * GS_W_BYTES), &mapW, (i % nk) * GT_BK, 0, smem_u32(&full[i]));
             }
+            trace_clock(ta.trace, 5);
         }
     } else if (warp == 1) {
+        // MMA issuer (one lane: this kernel's MMAs are few and wide -- one per 256 tokens x 16
+        // columns -- and the whole-warp issuer of gate1_tc_kernel measured slower here,
+        // 68 vs 64 us gate phase at C2)
         if (lane == 0) {
             const uint32_t idesc = make_idesc(128, GS_TOK);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
+            if (resw) mbar_wait(smem_u32(w_ready), 0);
             for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
                 const int buf = it & 1;
                 mbar_wait(smem_u32(&tempty[buf]), ((uint32_t)(it >> 1) & 1) ^ 1);
                 tc_fence_after();
+                if (it < 120) trace_clock(ta.trace, 8 + 2 * it);
                 const uint32_t tmem_d = tmem_base + buf * GS_TOK;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&full[stage]), phase);
                     tc_fence_after();
-                    const uint64_t ad = sw128_desc(smem_u32(sW + stage * GS_W_BYTES));
+                    const uint64_t ad = sw128_desc(smem_u32(resw ? sW + (size_t)kb * ta.NPT * 128 : sW + stage * GS_W_BYTES));
                     const uint64_t bd = sw128_desc(smem_u32(sX + stage * GS_X_BYTES));
 #pragma unroll
                     for (int k = 0; k < GT_BK / 16; ++k)
@@ -721,12 +791,42 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
                 mma_commit(smem_u32(&tfull[buf]));
+                if (it < 120) trace_clock(ta.trace, 9 + 2 * it);
             }
         }
     } else if (warp >= 4) {
         // the exact three-piece split of W into wsplit ("quad10" rows: row 32 Q + w holds
         // piece w % 3 of logit 10 Q + w / 3 for w < 30, rows 30, 31 of each group zero)
-        if ((int)blockIdx.x < ta.nbuilders) {
+        if (resw) {
+            // ... or into this CTA's resident copy, in the SWIZZLE_128B K-major layout the MMA
+            // reads (16-byte unit u of row r of a 64-column block at u ^ (r & 7))
+            __nv_bfloat16 *bs = reinterpret_cast<__nv_bfloat16 *>(sW);
+            const int etid = threadIdx.x - 128, NPT = ta.NPT, total = NPT * a.d;
+            for (int i0 = etid; i0 < total; i0 += 256 * 4) {
+                float wv[4];
+#pragma unroll
+                for (int z = 0; z < 4; ++z) {
+                    const int idx = i0 + z * 256;
+                    const int r = idx / a.d, c = idx - r * a.d, ww = r & 31;
+                    const int k = ww < 30 ? 10 * (r >> 5) + ww / 3 : KW;
+                    wv[z] = (idx < total && k < KW) ? __ldg(a.w + (int64_t)k * a.d + c) : 0.f;
+                }
+#pragma unroll
+                for (int z = 0; z < 4; ++z) {
+                    const int idx = i0 + z * 256;
+                    if (idx >= total) break;
+                    const int r = idx / a.d, c = idx - r * a.d, p = (r & 31) % 3;
+                    float rem = wv[z];
+                    for (int q = 0; q < p; ++q) rem -= __bfloat162float(__float2bfloat16_rn(rem));
+                    const int kb = c >> 6, u = (c & 63) >> 3;
+                    bs[((size_t)kb * NPT + r) * 64 + ((u ^ (r & 7)) << 3) + (c & 7)] = __float2bfloat16_rn(rem);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(w_ready));
+            if (threadIdx.x == 128) trace_clock(ta.trace, 6);
+        } else if ((int)blockIdx.x < ta.nbuilders) {
             const int etid = threadIdx.x - 128;
             for (int r = blockIdx.x; r < ta.NPT; r += gridDim.x) {
                 const int q = r >> 5, ww = r & 31;
@@ -745,6 +845,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
             __threadfence();
             EpiSync256<0>::sync();
             if (etid == 0) atomicAdd(ta.split_ready, 1);
+            if (etid == 0) trace_clock(ta.trace, 6);
         }
         const int q = warp & 3, hc = (warp - 4) >> 2;    // TMEM lane quadrant, token-column half
         int it = 0;
@@ -756,6 +857,8 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
             const int buf = it & 1;
             mbar_wait(smem_u32(&tfull[buf]), (uint32_t)(it >> 1) & 1);
             tc_fence_after();
+            const bool tr = threadIdx.x == 128 && it < 120;
+            if (tr) trace_clock(ta.trace, 256 + 4 * it);
             if (q < NQ) {
                 const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + buf * GS_TOK + hc * 128;
                 const int k = 10 * q + lane / 3;
@@ -774,19 +877,24 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+            if (tr) trace_clock(ta.trace, 257 + 4 * it);
             EpiSync256<0>::sync();
             if (a.logits_out) {
                 for (int i = EpiSync256<0>::tid(); i < nt * KW; i += 256)
                     a.logits_out[tok0 * KW + i] = s_lg[(i / KW) * lds + i % KW];
                 EpiSync256<0>::sync();
             }
-            gate_finish<EpiSync256<0>>(a, s_lg, lds, s_j, s_wh, s_bh, tok0, nt, (int64_t)tile);
+            gate_finish<EpiSync256<0>>(a, s_lg, lds, s_j, s_wh, s_bh, s_part, tok0, nt, (int64_t)tile,
+                                       it < 100 ? ta.trace : nullptr, 600 + 4 * it);
+            if (tr) trace_clock(ta.trace, 258 + 4 * it);
             if (ta.lb.on) lookback_scan<EpiSync256<0>>(a, ta.lb, s_bh, s_off, tile, epoch);
             EpiSync256<0>::sync();
+            if (tr) trace_clock(ta.trace, 259 + 4 * it);
         }
     }
     pdl_trigger();
     __syncthreads();
+    trace_end(ta.trace);
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
@@ -804,16 +912,18 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
     }
 }
 
-size_t gate_tcT_smem(int KW, int K1, int stages) {
-    return 1024 + (size_t)stages * (GS_W_BYTES + GS_X_BYTES) + ((size_t)GS_TOK * gate_lds(KW) + GS_TOK + 10 * K1) * 4 +
-           8 + (2 * stages + 4) * 8 + 16;
+size_t gate_tcT_smem(int KW, int K1, int K2, int stages, size_t resw_bytes = 0) {
+    return 1024 + (resw_bytes ? resw_bytes + (size_t)stages * GS_X_BYTES : (size_t)stages * (GS_W_BYTES + GS_X_BYTES)) +
+           ((size_t)GS_TOK * gate_lds(KW) + GS_TOK + 10 * K1) * 4 + 8 + gate_scratch_bytes(GS_TOK, KW, K2) + 8 +
+           (2 * stages + 5) * 8 + 16;
 }
 
-size_t gate_tc_smem(int NP, int KW, int K1, int stages, int nsub, int resident_b = 0, int d = 0) {
+size_t gate_tc_smem(int NP, int KW, int K1, int K2, int stages, int nsub, int resident_b = 0, int d = 0) {
     const int groups = 2 * NP <= 512 ? 2 : 1;          // = nbuf
+    const size_t grp_ints = ((gate_scratch_bytes(GT_BM, KW, K2) / 4 + (size_t)GT_BM * gate_lds(KW) + GT_BM + 6 * K1 + 1) &
+                             ~(size_t)1);
     return 1024 + (size_t)stages * nsub * (GT_A_BYTES + (resident_b ? 0 : NP * GT_BK * 2)) +
-           (resident_b ? (size_t)NP * d * 2 : 0) + 8 + groups * ((size_t)GT_BM * gate_lds(KW) + GT_BM + 6 * K1) * 4 + 8 +
-           (2 * stages + 4) * 8 + 16;
+           (resident_b ? (size_t)NP * d * 2 : 0) + 8 + groups * grp_ints * 4 + 8 + (2 * stages + 5) * 8 + 16;
 }
 
 }  // namespace
@@ -852,17 +962,24 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
         ta.g = a;
         ta.NPT = NPT;
         ta.ntiles = a.V * a.nblk;
+        // resident split router when it is small (C2 / C3: 32 rows x 768 = 48 KB) and 4+ x
+        // stages still fit; SMILE_GATE_RESW=0 streams it with x instead
+        const char *rwe = getenv("SMILE_GATE_RESW");             // read per call (A/B, tests)
+        const size_t rbytes = (size_t)NPT * a.d * 2;
+        ta.resw = (!(rwe && rwe[0] == '0') && rbytes <= 64 * 1024 &&
+                   gate_tcT_smem(a.KW, a.K1, a.K2, 4, rbytes) <= 227 * 1024) ? 1 : 0;
         int stages = 8;
-        while (stages > 2 && gate_tcT_smem(a.KW, a.K1, stages) > 227 * 1024) --stages;
+        while (stages > 2 && gate_tcT_smem(a.KW, a.K1, a.K2, stages, ta.resw ? rbytes : 0) > 227 * 1024) --stages;
         ta.stages = stages;
-        const size_t smem = gate_tcT_smem(a.KW, a.K1, stages);
+        const size_t smem = gate_tcT_smem(a.KW, a.K1, a.K2, stages, ta.resw ? rbytes : 0);
         static bool attrT = false;
         if (!attrT) {
             cudaFuncSetAttribute(gate1_tcT_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             attrT = true;
         }
         const int grid = ta.ntiles < num_sms ? ta.ntiles : num_sms;
-        ta.nbuilders = NPT < grid ? NPT : grid;
+        ta.nbuilders = ta.resw ? 0 : (NPT < grid ? NPT : grid);
+        ta.trace = trace_buffer("gate");
         ta.split_ready = gate_sync; ta.done = gate_sync + 1;
         ta.wsplit = wsplit;
         // the level-1 scan by look-back inside the kernel: opt-in (SMILE_GATE_LOOKBACK=1) --
@@ -877,7 +994,7 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
             ta.lb.epoch_ctr = gate_sync + 2;
         }
         const char *e2 = getenv("SMILE_GATE_SPLIT_KERNEL");      // 1: the separate split kernel (A/B)
-        if (e2 && e2[0] == '1') {
+        if (e2 && e2[0] == '1' && !ta.resw) {
             note_launch();
             launch_k(router_split_kernel, dim3((NPT * a.d + 255) / 256 < 1024 ? (NPT * a.d + 255) / 256 : 1024),
                      dim3(256), 0, st, a.w, wsplit, a.KW, a.d, NPT, 1);
@@ -915,6 +1032,7 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
     ta.nbuf = 2 * NP <= 512 ? 2 : 1;
     ta.ntiles = a.V * a.nblk;
     ta.resident_b = resb;
+    ta.trace = trace_buffer("gate");
     // two 64-column sub-blocks per stage when d allows and 3+ such stages fit (same box,
     // C2: 53-55 us vs 58-59 us with one; SMILE_GATE_NSUB=1 forces one)
     static int env_nsub = -1;
@@ -923,11 +1041,11 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
         env_nsub = (e && e[0] == '1') ? 1 : 2;
     }
     ta.nsub = (env_nsub == 2 && a.d % (2 * GT_BK) == 0 &&
-               gate_tc_smem(NP, a.KW, a.K1, 3, 2, resb, a.d) <= 227 * 1024) ? 2 : 1;
+               gate_tc_smem(NP, a.KW, a.K1, a.K2, 3, 2, resb, a.d) <= 227 * 1024) ? 2 : 1;
     int stages = 8;
-    while (stages > 2 && gate_tc_smem(NP, a.KW, a.K1, stages, ta.nsub, resb, a.d) > 227 * 1024) --stages;
+    while (stages > 2 && gate_tc_smem(NP, a.KW, a.K1, a.K2, stages, ta.nsub, resb, a.d) > 227 * 1024) --stages;
     ta.stages = stages;
-    const size_t smem = gate_tc_smem(NP, a.KW, a.K1, stages, ta.nsub, resb, a.d);
+    const size_t smem = gate_tc_smem(NP, a.KW, a.K1, a.K2, stages, ta.nsub, resb, a.d);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(gate1_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

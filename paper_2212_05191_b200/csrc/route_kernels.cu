@@ -133,8 +133,10 @@ __global__ void __launch_bounds__(256, 2) gate1_kernel(GateArgs a) {
     const int lds = gate_lds(a.KW);
     int *s_j = reinterpret_cast<int *>(s_lg + (size_t)a.TB * lds);
     int *s_wh = s_j + a.TB;
-    int *s_bh = s_wh + (((a.TB / 32) * a.K1 + 3) & ~3);               // 16-byte aligned s_w below
-    float *s_w = reinterpret_cast<float *>(s_bh + ((a.K1 + 3) & ~3));   // [KW, d] when it fits
+    int *s_bh = s_wh + (((a.TB / 32) * a.K1 + 3) & ~3);               // 16-byte aligned below
+    double *s_part = reinterpret_cast<double *>(s_bh + ((a.K1 + 3) & ~3));   // gate_finish scratch
+    float *s_w = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(s_part) +
+                                           ((gate_scratch_bytes(a.TB, a.KW, a.K2) + 15) & ~(size_t)15));   // [KW, d] when it fits
 
     const int v = blockIdx.y, blk = blockIdx.x, tid = threadIdx.x;
     const int64_t t0 = (int64_t)blk * a.TB;
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(256, 2) gate1_kernel(GateArgs a) {
         for (int i = tid; i < nt * KW; i += blockDim.x) a.logits_out[tok0 * KW + i] = s_lg[(i / KW) * lds + i % KW];
     if (a.logits_out && !a.logits) __syncthreads();
 
-    gate_finish<BlockSync>(a, s_lg, lds, s_j, s_wh, s_bh, tok0, nt, (int64_t)v * a.nblk + blk);
+    gate_finish<BlockSync>(a, s_lg, lds, s_j, s_wh, s_bh, s_part, tok0, nt, (int64_t)v * a.nblk + blk);
 }
 
 // Level-1 scan over the per-chunk tables (gate_common.cuh scan1_rank), grid = V.
@@ -765,7 +767,7 @@ inline int grid_for(int64_t warps_needed, int per_block_warps, int cap) {
 void launch_gate1(const GateArgs &a, cudaStream_t st) {
     if (a.T == 0) return;
     size_t smem = (size_t)a.TB * gate_lds(a.KW) * 4 + (size_t)a.TB * 4 + (size_t)(((a.TB / 32) * a.K1 + 3) & ~3) * 4 +
-                  (size_t)((a.K1 + 3) & ~3) * 4;
+                  (size_t)((a.K1 + 3) & ~3) * 4 + ((gate_scratch_bytes(a.TB, a.KW, a.K2) + 15) & ~(size_t)15);
     if (!a.logits && (size_t)a.KW * a.d * 4 <= (size_t)kRouterSmem) smem += (size_t)a.KW * a.d * 4;
     static bool attr_set = false;
     if (!attr_set) {

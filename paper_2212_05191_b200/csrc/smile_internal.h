@@ -29,6 +29,38 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 #endif
 bool pdl_enabled();
+
+// Diagnostic per-CTA timelines (measurement only; tools/gpu/trace_kernels.py): with
+// SMILE_TRACE=<name> ("gate", "ffn1", "ffn2") the named kernel gets a device buffer of
+// kTraceSlots clock64 stamps per CTA (slot 0 / 1: %globaltimer at start / end, slots 2 / 3:
+// clock64 at start / end, the rest kernel-specific), read back by smile_debug_trace (not part
+// of smile.h).  Null otherwise: every stamp is one predicated branch.
+constexpr int kTraceSlots = 1024;
+unsigned long long *trace_buffer(const char *name);   // nullptr unless SMILE_TRACE == name
+#ifdef __CUDACC__
+__device__ __forceinline__ void trace_clock(unsigned long long *tr, int slot) {
+    if (tr) {
+        long long t = clock64();
+        tr[(size_t)blockIdx.x * kTraceSlots + slot] = (unsigned long long)t;
+    }
+}
+__device__ __forceinline__ void trace_begin(unsigned long long *tr) {
+    if (tr && threadIdx.x == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        tr[(size_t)blockIdx.x * kTraceSlots + 0] = g;
+        trace_clock(tr, 2);
+    }
+}
+__device__ __forceinline__ void trace_end(unsigned long long *tr) {
+    if (tr && threadIdx.x == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        tr[(size_t)blockIdx.x * kTraceSlots + 1] = g;
+        trace_clock(tr, 3);
+    }
+}
+#endif
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                             Args... args) {

@@ -102,6 +102,15 @@ static __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc,
         : "memory");
 }
 
+// One lane of a converged warp (elect.sync): the MMA issuers run their loops on the whole
+// warp, so descriptors and loop state stay warp-uniform (uniform registers, no per-MMA
+// register-to-uniform broadcast loops), and only the elected lane issues tcgen05.mma/commit.
+static __device__ __forceinline__ bool elect_one() {
+    uint32_t p = 0;
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));
+    return p != 0;
+}
+
 static __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }

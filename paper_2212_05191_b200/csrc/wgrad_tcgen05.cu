@@ -155,9 +155,12 @@ wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
+        if (leader) {
             // ---------------- MMA issuer: A and B both MN-major ----------------
+            // (whole warp, warp-uniform descriptors; one elected lane issues: tc_util.cuh)
             const uint32_t idesc = make_idesc(WG_BM * CG, a.BN) | (1u << 15) | (1u << 16);
+            const uint64_t adesc0 = sw128_mn_desc(smem_u32(sA), WG_BOX_BYTES);
+            const uint64_t bdesc0 = sw128_mn_desc(smem_u32(sB), WG_BOX_BYTES);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -171,23 +174,29 @@ wgrad_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(smem_u32(&full[stage]), phase);
                     tc_fence_after();
-                    const uint64_t ad = sw128_mn_desc(smem_u32(sA + stage * WG_A_BYTES), WG_BOX_BYTES);
-                    const uint64_t bd = sw128_mn_desc(smem_u32(sB + stage * b_bytes), WG_BOX_BYTES);
+                    if (elect_one()) {
+                        const uint64_t ad = adesc0 + (uint64_t)((uint32_t)(stage * WG_A_BYTES) >> 4);
+                        const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)(stage * b_bytes) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < WG_BK / 16; ++kk) {  // 16 K-rows = two 1024 B swizzle atoms
-                        if (CG == 1)
-                            mma_bf16(tmem_d, ad + (uint64_t)(kk * 128), bd + (uint64_t)(kk * 128), idesc,
-                                     (kb | kk) ? 1u : 0u);
-                        else
-                            mma_bf16_pair(tmem_d, ad + (uint64_t)(kk * 128), bd + (uint64_t)(kk * 128), idesc,
-                                          (kb | kk) ? 1u : 0u);
+                        for (int kk = 0; kk < WG_BK / 16; ++kk) {  // 16 K-rows = two 1024 B swizzle atoms
+                            if (CG == 1)
+                                mma_bf16(tmem_d, ad + (uint64_t)(kk * 128), bd + (uint64_t)(kk * 128), idesc,
+                                         (kb | kk) ? 1u : 0u);
+                            else
+                                mma_bf16_pair(tmem_d, ad + (uint64_t)(kk * 128), bd + (uint64_t)(kk * 128), idesc,
+                                              (kb | kk) ? 1u : 0u);
+                        }
+                        if (CG == 1) mma_commit(smem_u32(&empty[stage]));
+                        else mma_commit_pair(smem_u32(&empty[stage]));
                     }
-                    if (CG == 1) mma_commit(smem_u32(&empty[stage]));
-                    else mma_commit_pair(smem_u32(&empty[stage]));
+                    __syncwarp();
                     if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
                 }
-                if (CG == 1) mma_commit(smem_u32(&tfull[acc]));
-                else mma_commit_pair(smem_u32(&tfull[acc]));
+                if (elect_one()) {
+                    if (CG == 1) mma_commit(smem_u32(&tfull[acc]));
+                    else mma_commit_pair(smem_u32(&tfull[acc]));
+                }
+                __syncwarp();
             }
         }
     } else if (warp >= 4) {

@@ -13,7 +13,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsmile.so")
+# SMILE_LIB_PATH: load another build of the library (same-box A/B measurements only)
+LIB_PATH = os.environ.get("SMILE_LIB_PATH") or os.path.join(_HERE, "libsmile.so")
 _lib = None
 
 BILEVEL, FLAT = 0, 1
