@@ -200,39 +200,53 @@ __device__ GateTok gate_finish(const GateArgs &a, float *s_lg, int lds, int *s_j
         for (int k = tid; k < K1; k += nthr) a.blk_hist1[(bo0 + (int64_t)c * a.nblk) * K1 + k] = s_bh[k];
     }
     // LB statistics partials of the tile: fp64 sums of the probabilities (R13) and the
-    // level-2 top-1 counts.  Sums: per 32-token chunk c and statistic k, four interleaved
-    // accumulators over the chunk's tokens in ascending order, then the chunks in ascending
-    // order -- a fixed order that depends only on the tile's token count (deterministic, the
-    // same in every kernel that calls this), with the (chunk, 32-statistic block) items
-    // spread over all warps of Sync.  Counts: warp-aggregated shared-memory adds (exact).
+    // level-2 top-1 counts, in a fixed order that depends only on the tile's token count and
+    // KW (deterministic, the same in every kernel that calls this).  Counts: warp-aggregated
+    // shared-memory adds (exact).  Narrow routers (KW < 32): a warp per statistic, lanes
+    // stride over the tokens, fixed butterfly.  Wide routers: per 32-token chunk c and
+    // statistic k, four interleaved accumulators over the chunk's tokens in ascending order,
+    // then the chunks in ascending order, the (chunk, 32-statistic block) items spread over
+    // all warps (one warp per 32 statistics walking every token left most warps idle and
+    // bounded the epilogue of C4 / C5).
     {
         const int lane = tid & 31, w = tid >> 5, NW = nthr >> 5;
         const int jj = (tid < nt) ? j : -1;
         const unsigned peers = __match_any_sync(kFull, jj);
         if (jj >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_h2[jj], __popc(peers));
-        const int nch = (nt + 31) >> 5, ncb = (KW + 31) >> 5;
-        for (int item = w; item < nch * ncb; item += NW) {
-            const int c = item / ncb, k = (item - c * ncb) * 32 + lane;
-            if (k < KW) {
-                const float *sc = k < K1 ? s_p : s_q;             // softmax entry = e_k * p or e_k * q
-                const int t1 = min(nt, c * 32 + 32);
-                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                int tt = c * 32;
-                for (; tt + 3 < t1; tt += 4) {
-                    a0 += (double)(s_lg[tt * lds + k] * sc[tt]);
-                    a1 += (double)(s_lg[(tt + 1) * lds + k] * sc[tt + 1]);
-                    a2 += (double)(s_lg[(tt + 2) * lds + k] * sc[tt + 2]);
-                    a3 += (double)(s_lg[(tt + 3) * lds + k] * sc[tt + 3]);
-                }
-                for (; tt < t1; ++tt) a0 += (double)(s_lg[tt * lds + k] * sc[tt]);
-                s_part[c * KW + k] = (a0 + a1) + (a2 + a3);
+        if (KW < 32) {
+            for (int k = w; k < KW; k += NW) {
+                const float *sc = k < K1 ? s_p : s_q;         // softmax entry = e_k * p or e_k * q
+                double acc = 0.0;
+                for (int tt = lane; tt < nt; tt += 32) acc += (double)(s_lg[tt * lds + k] * sc[tt]);
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+                if (lane == 0) a.blk_psum[bo0 * (K1 + K2) + k] = acc;
             }
-        }
-        Sync::sync();
-        for (int k = tid; k < KW; k += nthr) {
-            double acc = 0.0;
-            for (int c = 0; c < nch; ++c) acc += s_part[c * KW + k];
-            a.blk_psum[bo0 * (K1 + K2) + k] = acc;
+            Sync::sync();
+        } else {
+            const int nch = (nt + 31) >> 5, ncb = (KW + 31) >> 5;
+            for (int item = w; item < nch * ncb; item += NW) {
+                const int c = item / ncb, k = (item - c * ncb) * 32 + lane;
+                if (k < KW) {
+                    const float *sc = k < K1 ? s_p : s_q;
+                    const int t1 = min(nt, c * 32 + 32);
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                    int tt = c * 32;
+                    for (; tt + 3 < t1; tt += 4) {
+                        a0 += (double)(s_lg[tt * lds + k] * sc[tt]);
+                        a1 += (double)(s_lg[(tt + 1) * lds + k] * sc[tt + 1]);
+                        a2 += (double)(s_lg[(tt + 2) * lds + k] * sc[tt + 2]);
+                        a3 += (double)(s_lg[(tt + 3) * lds + k] * sc[tt + 3]);
+                    }
+                    for (; tt < t1; ++tt) a0 += (double)(s_lg[tt * lds + k] * sc[tt]);
+                    s_part[c * KW + k] = (a0 + a1) + (a2 + a3);
+                }
+            }
+            Sync::sync();
+            for (int k = tid; k < KW; k += nthr) {
+                double acc = 0.0;
+                for (int c = 0; c < nch; ++c) acc += s_part[c * KW + k];
+                a.blk_psum[bo0 * (K1 + K2) + k] = acc;
+            }
         }
         for (int k = tid; k < K2; k += nthr) a.blk_hist2a[bo0 * K2 + k] = s_h2[k];
         if (a.flat && tid == 0) a.blk_psum[bo0 * (K1 + K2) + K1] = (double)nt;

@@ -639,6 +639,8 @@ gate1_tc_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant_
 // 45 us; profiles/r02_gate_schedule_ab.md.)
 // ---------------------------------------------------------------------------------
 constexpr int GS_TOK = 256, GS_THREADS = 128 + 256;
+constexpr int kResWMaxKW = 20;                     // resident split router: KW <= 20 (NPT <= 64),
+constexpr int kResWCols = 4;                       // d <= 1024
 constexpr int GS_X_BYTES = GS_TOK * GT_BK * 2;    // 32 KB per stage
 constexpr int GS_W_BYTES = 128 * GT_BK * 2;       // 16 KB per stage
 
@@ -800,26 +802,32 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
         if (resw) {
             // ... or into this CTA's resident copy, in the SWIZZLE_128B K-major layout the MMA
             // reads (16-byte unit u of row r of a 64-column block at u ^ (r & 7))
+            // Thread = column (up to kResWCols of them, d <= 256 kResWCols): all its router
+            // entries are loaded first (one memory latency for the CTA's whole build), then its
+            // NPT <= 64 rows are produced from registers (loops unrolled: static indices).
             __nv_bfloat16 *bs = reinterpret_cast<__nv_bfloat16 *>(sW);
-            const int etid = threadIdx.x - 128, NPT = ta.NPT, total = NPT * a.d;
-            for (int i0 = etid; i0 < total; i0 += 256 * 4) {
-                float wv[4];
+            const int etid = threadIdx.x - 128, NPT = ta.NPT;
+            float wv[kResWCols][kResWMaxKW];
 #pragma unroll
-                for (int z = 0; z < 4; ++z) {
-                    const int idx = i0 + z * 256;
-                    const int r = idx / a.d, c = idx - r * a.d, ww = r & 31;
-                    const int k = ww < 30 ? 10 * (r >> 5) + ww / 3 : KW;
-                    wv[z] = (idx < total && k < KW) ? __ldg(a.w + (int64_t)k * a.d + c) : 0.f;
-                }
+            for (int ci = 0; ci < kResWCols; ++ci) {
+                const int c = etid + 256 * ci;
 #pragma unroll
-                for (int z = 0; z < 4; ++z) {
-                    const int idx = i0 + z * 256;
-                    if (idx >= total) break;
-                    const int r = idx / a.d, c = idx - r * a.d, p = (r & 31) % 3;
-                    float rem = wv[z];
+                for (int k = 0; k < kResWMaxKW; ++k)
+                    wv[ci][k] = (c < a.d && k < KW) ? __ldg(a.w + (int64_t)k * a.d + c) : 0.f;
+            }
+#pragma unroll
+            for (int ci = 0; ci < kResWCols; ++ci) {
+                const int c = etid + 256 * ci;
+                if (c >= a.d) break;
+                const int kb = c >> 6, u = (c & 63) >> 3;
+                __nv_bfloat16 *col = bs + (size_t)kb * NPT * 64 + (c & 7);
+#pragma unroll
+                for (int r = 0; r < 2 * 32; ++r) {
+                    if (r >= NPT) break;
+                    const int ww = r & 31, k = 10 * (r >> 5) + ww / 3, p = ww % 3;
+                    float rem = (ww < 30 && k < KW) ? wv[ci][k] : 0.f;
                     for (int q = 0; q < p; ++q) rem -= __bfloat162float(__float2bfloat16_rn(rem));
-                    const int kb = c >> 6, u = (c & 63) >> 3;
-                    bs[((size_t)kb * NPT + r) * 64 + ((u ^ (r & 7)) << 3) + (c & 7)] = __float2bfloat16_rn(rem);
+                    col[(size_t)r * 64 + ((u ^ (r & 7)) << 3)] = __float2bfloat16_rn(rem);
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
@@ -966,7 +974,7 @@ cudaError_t launch_gate1_tc(const GateArgs &a, __nv_bfloat16 *wsplit, int num_sm
         // stages still fit; SMILE_GATE_RESW=0 streams it with x instead
         const char *rwe = getenv("SMILE_GATE_RESW");             // read per call (A/B, tests)
         const size_t rbytes = (size_t)NPT * a.d * 2;
-        ta.resw = (!(rwe && rwe[0] == '0') && rbytes <= 64 * 1024 &&
+        ta.resw = (!(rwe && rwe[0] == '0') && a.KW <= kResWMaxKW && a.d <= 256 * kResWCols && rbytes <= 64 * 1024 &&
                    gate_tcT_smem(a.KW, a.K1, a.K2, 4, rbytes) <= 227 * 1024) ? 1 : 0;
         int stages = 8;
         while (stages > 2 && gate_tcT_smem(a.KW, a.K1, a.K2, stages, ta.resw ? rbytes : 0) > 227 * 1024) --stages;

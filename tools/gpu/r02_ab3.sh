@@ -1,7 +1,7 @@
 # Gate epilogue rework (chunked statistics, scaled-on-read softmax, resident split router in the
 # swapped kernel): parity, timelines, same-box A/B against HEAD.
 set -x
-O=gpurun_out/r02ab3
+O=gpurun_out/r02ab4
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 timeout 1500 python -m pytest tests -q -x -m gpu -k "not multigpu" > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
