@@ -692,8 +692,8 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
     uint64_t *bars = reinterpret_cast<uint64_t *>(
         ((uintptr_t)s_part + gate_scratch_bytes(GS_TOK, KW, a.K2) + 7) & ~(uintptr_t)7);
     uint64_t *full = bars, *empty = bars + ST, *tfull = bars + 2 * ST, *tempty = bars + 2 * ST + 2;
-    uint64_t *w_ready = bars + 2 * ST + 4;                      // resident split built (8 warps)
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 5);
+    uint64_t *w_ready = bars + 2 * ST + 4;     // [kResWCols] resident split: columns 256 r.. built
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * ST + 4 + kResWCols);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // the call's look-back epoch: read before any CTA can advance it (the last CTA to finish)
@@ -707,7 +707,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
             mbar_init(smem_u32(&tfull[s]), 1);
             mbar_init(smem_u32(&tempty[s]), 8);
         }
-        mbar_init(smem_u32(w_ready), 8);
+        for (int r = 0; r < kResWCols; ++r) mbar_init(smem_u32(&w_ready[r]), 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0 && lane == 0) {
@@ -774,7 +774,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            if (resw) mbar_wait(smem_u32(w_ready), 0);
+
             for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x, ++it) {
                 const int buf = it & 1;
                 mbar_wait(smem_u32(&tempty[buf]), ((uint32_t)(it >> 1) & 1) ^ 1);
@@ -782,6 +782,9 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
                 if (it < 120) trace_clock(ta.trace, 8 + 2 * it);
                 const uint32_t tmem_d = tmem_base + buf * GS_TOK;
                 for (int kb = 0; kb < nk; ++kb) {
+                    // the resident split is built in rounds of 256 columns (4 k blocks): the
+                    // first tile's MMAs follow the build round by round
+                    if (resw && it == 0 && (kb & 3) == 0) mbar_wait(smem_u32(&w_ready[kb >> 2]), 0);
                     mbar_wait(smem_u32(&full[stage]), phase);
                     tc_fence_after();
                     const uint64_t ad = sw128_desc(smem_u32(resw ? sW + (size_t)kb * ta.NPT * 128 : sW + stage * GS_W_BYTES));
@@ -818,21 +821,22 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
 #pragma unroll
             for (int ci = 0; ci < kResWCols; ++ci) {
                 const int c = etid + 256 * ci;
-                if (c >= a.d) break;
+                if (256 * ci >= a.d) break;
                 const int kb = c >> 6, u = (c & 63) >> 3;
                 __nv_bfloat16 *col = bs + (size_t)kb * NPT * 64 + (c & 7);
 #pragma unroll
                 for (int r = 0; r < 2 * 32; ++r) {
-                    if (r >= NPT) break;
+                    if (r >= NPT || c >= a.d) break;     // (every warp still arrives below)
                     const int ww = r & 31, k = 10 * (r >> 5) + ww / 3, p = ww % 3;
                     float rem = (ww < 30 && k < KW) ? wv[ci][k] : 0.f;
                     for (int q = 0; q < p; ++q) rem -= __bfloat162float(__float2bfloat16_rn(rem));
                     col[(size_t)r * 64 + ((u ^ (r & 7)) << 3)] = __float2bfloat16_rn(rem);
                 }
+                // round ci (columns 256 ci .. 256 ci + 255 = k blocks 4 ci .. 4 ci + 3) is built
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&w_ready[ci]));
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(w_ready));
             if (threadIdx.x == 128) trace_clock(ta.trace, 6);
         } else if ((int)blockIdx.x < ta.nbuilders) {
             const int etid = threadIdx.x - 128;
@@ -923,7 +927,7 @@ gate1_tcT_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant
 size_t gate_tcT_smem(int KW, int K1, int K2, int stages, size_t resw_bytes = 0) {
     return 1024 + (resw_bytes ? resw_bytes + (size_t)stages * GS_X_BYTES : (size_t)stages * (GS_W_BYTES + GS_X_BYTES)) +
            ((size_t)GS_TOK * gate_lds(KW) + GS_TOK + 10 * K1) * 4 + 8 + gate_scratch_bytes(GS_TOK, KW, K2) + 8 +
-           (2 * stages + 5) * 8 + 16;
+           (2 * stages + 4 + kResWCols) * 8 + 16;
 }
 
 size_t gate_tc_smem(int NP, int KW, int K1, int K2, int stages, int nsub, int resident_b = 0, int d = 0) {

@@ -1,9 +1,9 @@
 # Resident split router build (column-parallel loads): gate parity + C2 timeline + A/B.
 set -x
-O=gpurun_out/r02ab5
+O=gpurun_out/r02ab6
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_topk.py tests/test_gpu_fullsize.py -q -x > $O/pytest_gate.log 2>&1; echo "rc=$?" >> $O/pytest_gate.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_topk.py tests/test_gpu_backward.py -q -x > $O/pytest_gate.log 2>&1; echo "rc=$?" >> $O/pytest_gate.log
 SMILE_TRACE=gate timeout 300 python tools/gpu/trace_kernels.py --config c2 --mode bilevel > $O/trace_c2_gate.log 2>&1
 for round in 1 2; do
 for v in new resw0; do
