@@ -200,10 +200,22 @@ struct TileInfo {
 // and its BN/2-row half of B.  Strip u0 + j of the expert goes to TMEM lanes 32j..32j+31;
 // a missing strip (the expert's last tile) has 0 rows and points at row 0 (loaded,
 // computed, never stored).
-template <int CG, int NSUB>
+template <int CG, int NSUB, int MC = 0>
 __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref, int tile, int ntn, int rank,
                                               int sub) {
     TileInfo t;
+    if (MC) {
+        // A-multicast cluster (CG = 1): work item `tile` = (M-tile, pair of N-tiles); cluster
+        // rank r takes N-tile 2 p + r (>= ntn: a dummy that only shares its half of A)
+        const int ntp = (ntn + 1) >> 1;
+        t.nt = 2 * (tile % ntp) + rank;
+        const int mtg = tile / ntp;
+        const int NE = a.nseg / a.S;
+        t.E = tile_segment(s_pref, NE, mtg);
+        t.u0 = (mtg - s_pref[t.E]) * 4;
+        t.b_row = (int64_t)t.E * a.N + (int64_t)t.nt * a.BN;
+        return t;
+    }
     t.nt = tile % ntn;
     const int mtg = tile / ntn;
     const int NE = a.nseg / a.S;
@@ -225,7 +237,12 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref
 // loop is at the tensor peak already; profiles/r01_ffn_epilogue_diagnostics.md), so opt-in.
 // EK: epilogue kind, one instantiation each so the forward kernel carries no backward
 // registers: 0 = EPI_BIAS / EPI_PLAIN, 1 = EPI_BIAS_SAVE, 2 = EPI_DGELU.
-template <int CG, int NSUB, int EK>
+// MC = 1 (CG = 1, NSUB = 1, forward): clusters of 2 CTAs computing two N-tiles of the same
+// 128-row M-tile; each CTA TMA-loads 2 of the tile's 4 A strips multicast into both CTAs,
+// so A crosses L2 -> SM once per pair of N-tiles (C5: the operand traffic from L2 bounds
+// the 128-row tiles; r02_ffn_c5.md).  A stage is refilled only after both CTAs' MMAs have
+// released it (each commit multicasts to both CTAs' empty barrier, count 2).
+template <int CG, int NSUB, int EK, int MC = 0>
 __global__ void __launch_bounds__(NTHREADS, 1)
 ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA128,
                  const __grid_constant__ CUtensorMap mapB,
@@ -250,15 +267,16 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     int *s_cnt = s_pref + a.nseg + 1;                                 // [nseg] segment row counts
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int CS = CG;                                      // cluster size
+    static_assert(!MC || (CG == 1 && NSUB == 1), "A multicast: single-CTA tiles only");
+    constexpr int CS = MC ? 2 : CG;                             // cluster size
     const int rank = CS > 1 ? (int)cluster_ctarank() : 0;
-    const bool leader = rank == 0;
+    const bool leader = MC ? true : rank == 0;                  // this CTA issues its own MMAs
     const uint32_t lead = 0;                                    // cluster rank of the pair's leader
     const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
-            mbar_init(smem_u32(&empty[s]), 1);
+            mbar_init(smem_u32(&empty[s]), MC ? 2 : 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&tfull[s]), 1);
@@ -294,7 +312,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     trace_begin(a.trace);
     const uint32_t tmem_base = *tmem_holder;
     const int ntn = a.N / a.BN;
-    const int total = s_pref[a.nseg / a.S] * ntn;
+    const int total = s_pref[a.nseg / a.S] * (MC ? (ntn + 1) >> 1 : ntn);
     const int nk = a.K / BK;
     const uint32_t b_bytes = (uint32_t)(a.BN / CG) * BK * 2;
 
@@ -313,7 +331,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                 int64_t b_row = 0;
 #pragma unroll
                 for (int u = 0; u < NSUB; ++u) {
-                    const TileInfo t = tile_info<CG, NSUB>(a, s_pref, tile, ntn, rank, u);
+                    const TileInfo t = tile_info<CG, NSUB, MC>(a, s_pref, tile, ntn, rank, u);
                     b_row = t.b_row;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
@@ -329,7 +347,15 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full[stage]);
                     unsigned char *sAs = sA + stage * A_STAGE;
-                    if (CG == 1) {
+                    if (MC) {
+                        // strips 2 rank, 2 rank + 1 of the tile into both CTAs (the peer sends the
+                        // other two); this CTA's own B
+                        mbar_arrive_tx(fb, A_STAGE + b_bytes);
+#pragma unroll
+                        for (int j = 2 * rank; j < 2 * rank + 2; ++j)
+                            tma_load_2d_mc(smem_u32(sAs + j * (A_BYTES / 4)), &mapA, kb * BK, srow[0][j], fb, (uint16_t)3);
+                        tma_load_2d(smem_u32(sB + stage * b_stage_bytes), &mapB, kb * BK, (int)b_row, fb);
+                    } else if (CG == 1) {
                         mbar_arrive_tx(fb, A_STAGE + b_bytes);
 #pragma unroll
                         for (int u = 0; u < NSUB; ++u) {
@@ -389,6 +415,10 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                 if (CG == 1) mma_commit(smem_u32(bar));
                 else mma_commit_pair(smem_u32(bar), (uint16_t)3);
             };
+            auto release_stage = [&](uint64_t *bar) {    // a smem stage: both CTAs' with A multicast
+                if (MC) mma_commit_mc(smem_u32(bar), (uint16_t)3);
+                else release(bar);
+            };
             for (int tile = cid; tile < total; tile += ncl, ++it) {
                 if (NSUB == 1) {
                     // double-buffered accumulator: tile `it` uses buffer it & 1
@@ -401,7 +431,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                         tc_fence_after();
                         if (elect_one()) {
                             kblock(stage, 0, acc, kb == 0);
-                            release(&empty[stage]);
+                            release_stage(&empty[stage]);
                         }
                         __syncwarp();
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -468,16 +498,18 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         int it = 0;
         unsigned char *box = sOut + (warp - 4) * nbox * OUT_BOX_BYTES * (a.box64 ? 2 : 1);
         for (int tile = cid, sub = 0; tile < total;) {
-            const TileInfo t = tile_info<CG, NSUB>(a, s_pref, tile, ntn, rank, sub);
+            const TileInfo t = tile_info<CG, NSUB, MC>(a, s_pref, tile, ntn, rank, sub);
+            const bool nt_ok = !MC || t.nt < ntn;                 // MC: a dummy N-tile stores nothing
             const int acc = NSUB == 2 ? sub : it & 1;
             const bool has_bias = a.mode == EPI_BIAS || a.mode == EPI_BIAS_SAVE;
             const bool act = ((a.mode == EPI_BIAS && a.gelu) || a.mode == EPI_BIAS_SAVE) && !(a.diag & 1);
             constexpr bool dgelu = EK == 2;                 // EPI_DGELU / EPI_BIAS_SAVE: own instantiations
-            const float4 *bias4 = reinterpret_cast<const float4 *>(a.bias + (int64_t)t.E * a.N + (int64_t)t.nt * a.BN);
+            const float4 *bias4 = reinterpret_cast<const float4 *>(a.bias + (int64_t)t.E * a.N + (int64_t)(nt_ok ? t.nt : 0) * a.BN);
             const int64_t dcol0 = (int64_t)t.nt * a.BN;
             int64_t d_row;                                  // this warp's strip
             int srows;
             expert_strip(s_cnt, t.E, a.S, a.e, a.Cseg, t.u0 + q, d_row, srows);
+            if (!nt_ok) srows = 0;
             const int st_row = (a.diag & 8) ? (int)(d_row & 1023) : (int)d_row;   // diag 8: L2-resident store window
             // ret mode: rows whose intermediate (i, l) lives in this process go straight to
             // its ret1 (this lane's row: rdst); a strip is one segment, so one l and one
@@ -752,13 +784,13 @@ int pick_nsub() {                                          // read per launch (t
     return (e && e[0] == '2') ? 2 : 1;
 }
 
-template <int CG, int NSUB, int EK>
+template <int CG, int NSUB, int EK, int MC = 0>
 cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUtensorMap &mB, const CUtensorMap &mD,
                       const CUtensorMap &mD2, const TcArgs &a, size_t smem, int num_sms, cudaStream_t st) {
-    constexpr int CS = CG;
+    constexpr int CS = MC ? 2 : CG;
     static int grid = 0;
     if (!grid) {
-        cudaFuncSetAttribute(ffn_gemm_tcgen05<CG, NSUB, EK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
+        cudaFuncSetAttribute(ffn_gemm_tcgen05<CG, NSUB, EK, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
         grid = num_sms / CS * CS;
         // SMILE_FFN_MAX_CTAS caps the persistent grid (leaves SMs to kernels of other
         // streams, e.g. the permutes of the next chunk in the pipelined layer)
@@ -769,7 +801,7 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
     }
     note_launch();
     if (CS == 1)
-        return launch_k(ffn_gemm_tcgen05<CG, NSUB, EK>, dim3(grid), dim3(NTHREADS), smem, st, mA, mA128, mB, mD, mD2, a);
+        return launch_k(ffn_gemm_tcgen05<CG, NSUB, EK, MC>, dim3(grid), dim3(NTHREADS), smem, st, mA, mA128, mB, mD, mD2, a);
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)grid);
@@ -785,7 +817,7 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
     attrs[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<CG, NSUB, EK>, mA, mA128, mB, mD, mD2, a);
+    return cudaLaunchKernelEx(&cfg, ffn_gemm_tcgen05<CG, NSUB, EK, MC>, mA, mA128, mB, mD, mD2, a);
 }
 
 // One grouped GEMM launch: D[rows, N] = epi(A[rows, K] . B[expert][N, K]^T).
@@ -852,6 +884,13 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     return ek == 2 ? launch_tc<cg, ns, 2>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)          \
                    : (ek == 1 ? launch_tc<cg, ns, 1>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st) \
                               : launch_tc<cg, ns, 0>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st))
+    // A multicast across clusters of 2 single-CTA tiles (forward GEMMs of 128-row tiles):
+    // SMILE_FFN_MCAST=1 (read per launch)
+    {
+        const char *mc = getenv("SMILE_FFN_MCAST");
+        if (CG == 1 && NSUB == 1 && ek == 0 && mc && mc[0] == '1' && f.num_sms >= 2)
+            return launch_tc<1, 1, 0, 1>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
+    }
     if (CG == 2 && NSUB == 2) SMILE_LAUNCH_TC(2, 2);
     if (CG == 1 && NSUB == 2) SMILE_LAUNCH_TC(1, 2);
     if (CG == 2) SMILE_LAUNCH_TC(2, 1);

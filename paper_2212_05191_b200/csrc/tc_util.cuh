@@ -168,6 +168,25 @@ static __device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const C
         : "memory");
 }
 
+// One-CTA TMA load multicast to the CTAs in `mask` of the cluster (same smem offset in each,
+// complete_tx on the barrier at `bar`'s offset in each destination).
+static __device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t bar,
+                                                     uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+        : "memory");
+}
+
+// Commit of this CTA's MMAs arriving on the barrier at `bar`'s offset in every CTA of `mask`.
+static __device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     bar),
+                 "h"(mask)
+                 : "memory");
+}
+
 static __device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                               uint32_t accumulate) {
     asm volatile(
