@@ -884,11 +884,15 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     return ek == 2 ? launch_tc<cg, ns, 2>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)          \
                    : (ek == 1 ? launch_tc<cg, ns, 1>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st) \
                               : launch_tc<cg, ns, 0>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st))
-    // A multicast across clusters of 2 single-CTA tiles (forward GEMMs of 128-row tiles):
-    // SMILE_FFN_MCAST=1 (read per launch)
+    // A multicast across clusters of 2 single-CTA tiles (forward GEMMs of 128-row tiles)
+    // when the N-tiles pair up evenly: C5 GEMM 2 1.94 -> 1.82 ms, while GEMM 1 (25 N-tiles:
+    // a dummy every 13th pair) measured 1.57 -> 1.63 ms (r02_ffn_c5.md).  SMILE_FFN_MCAST=0
+    // turns it off, =1 forces it for odd N-tile counts too (read per launch).
     {
         const char *mc = getenv("SMILE_FFN_MCAST");
-        if (CG == 1 && NSUB == 1 && ek == 0 && mc && mc[0] == '1' && f.num_sms >= 2)
+        const int env = mc ? (mc[0] == '1' ? 1 : 0) : -1;
+        const bool even = (N / BN) % 2 == 0;
+        if (CG == 1 && NSUB == 1 && ek == 0 && f.num_sms >= 2 && (env == 1 || (env < 0 && even)))
             return launch_tc<1, 1, 0, 1>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st);
     }
     if (CG == 2 && NSUB == 2) SMILE_LAUNCH_TC(2, 2);
