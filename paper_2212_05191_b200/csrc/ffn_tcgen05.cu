@@ -33,7 +33,10 @@ namespace {
 using namespace tc;
 
 constexpr int BM = 128, BK = 64, MAXSEG = 1024;
-constexpr int EPI_WARPS = 16;                 // 4 warps per TMEM lane quadrant, split by columns
+#ifndef SMILE_FFN_EPI_WARPS
+#define SMILE_FFN_EPI_WARPS 16
+#endif
+constexpr int EPI_WARPS = SMILE_FFN_EPI_WARPS;  // 4 warps per TMEM lane quadrant, split by columns
 constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
 constexpr int B_BYTES_MAX = 256 * BK * 2;     // 32 KB
@@ -493,8 +496,9 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         // TMEM / global / fixed-latency dependencies of the epilogue behind the MMAs.
         const int q = warp & 3;
         const int h = (warp - 4) >> 2;
+        constexpr int ngc = EPI_WARPS / 4;                  // column groups per quadrant
         const int nch = a.BN / 32;
-        const int c_beg = (h * nch) / 4, c_end = ((h + 1) * nch) / 4;
+        const int c_beg = (h * nch) / ngc, c_end = ((h + 1) * nch) / ngc;
         int it = 0;
         unsigned char *box = sOut + (warp - 4) * nbox * OUT_BOX_BYTES * (a.box64 ? 2 : 1);
         for (int tile = cid, sub = 0; tile < total;) {
