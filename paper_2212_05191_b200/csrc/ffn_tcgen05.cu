@@ -33,10 +33,14 @@ namespace {
 using namespace tc;
 
 constexpr int BM = 128, BK = 64, MAXSEG = 1024;
+// Epilogue warps: EPI_WARPS / 4 per TMEM lane quadrant, splitting the tile's columns.  8
+// measured faster than round 1's 16 (same box: C5 FFN 3.12-3.13 vs 3.37-3.46 ms, C2 GEMM 1
+// 547 vs 559 us; 12 in between; profiles/r02_ffn_c5.md) -- fewer warps competing with the
+// producer / MMA warps for issue slots and with the MMAs for TMEM / shared-memory bandwidth.
 #ifndef SMILE_FFN_EPI_WARPS
-#define SMILE_FFN_EPI_WARPS 16
+#define SMILE_FFN_EPI_WARPS 8
 #endif
-constexpr int EPI_WARPS = SMILE_FFN_EPI_WARPS;  // 4 warps per TMEM lane quadrant, split by columns
+constexpr int EPI_WARPS = SMILE_FFN_EPI_WARPS;
 constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
 constexpr int B_BYTES_MAX = 256 * BK * 2;     // 32 KB
@@ -488,12 +492,11 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             }
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue: 16 warps ----------------
+        // ---------------- epilogue: EPI_WARPS warps ----------------
         // Warp w reads TMEM lane quadrant q = w & 3 (the tile's strip q) and column group
-        // h = (w - 4) >> 2 of 4, in 32-column chunks: tcgen05.ld -> bias / GELU in packed
-        // fp32x2 -> bf16 -> a 32 x 32 SWIZZLE_64B box in smem -> one TMA tensor store.
-        // Four warps per quadrant keep enough independent work in flight to hide the
-        // TMEM / global / fixed-latency dependencies of the epilogue behind the MMAs.
+        // h = (w - 4) >> 2 of EPI_WARPS / 4, in 32-column chunks: tcgen05.ld -> bias / GELU
+        // in packed fp32x2 -> bf16 -> a 32 x 32 SWIZZLE_64B box in smem -> one TMA tensor
+        // store.
         const int q = warp & 3;
         const int h = (warp - 4) >> 2;
         constexpr int ngc = EPI_WARPS / 4;                  // column groups per quadrant
