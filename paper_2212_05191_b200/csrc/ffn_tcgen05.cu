@@ -37,11 +37,13 @@ constexpr int BM = 128, BK = 64, MAXSEG = 1024;
 // measured faster than round 1's 16 (same box: C5 FFN 3.12-3.13 vs 3.37-3.46 ms, C2 GEMM 1
 // 547 vs 559 us; 12 in between; profiles/r02_ffn_c5.md) -- fewer warps competing with the
 // producer / MMA warps for issue slots and with the MMAs for TMEM / shared-memory bandwidth.
+// The dZ epilogue (EPI_DGELU: saved GELU' loads, the product, the db1 column sums) keeps 16:
+// with 8 the C3 backward measured 1-3 % slower.
 #ifndef SMILE_FFN_EPI_WARPS
 #define SMILE_FFN_EPI_WARPS 8
 #endif
-constexpr int EPI_WARPS = SMILE_FFN_EPI_WARPS;
-constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
+constexpr int epi_warps(int ek) { return ek == 2 ? 16 : SMILE_FFN_EPI_WARPS; }
+constexpr int nthreads(int ek) { return 128 + 32 * epi_warps(ek); }
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
 constexpr int B_BYTES_MAX = 256 * BK * 2;     // 32 KB
 constexpr int ACC_COLS = 256;                 // TMEM columns per accumulator buffer
@@ -250,7 +252,7 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, const int *s_pref
 // the 128-row tiles; r02_ffn_c5.md).  A stage is refilled only after both CTAs' MMAs have
 // released it (each commit multicasts to both CTAs' empty barrier, count 2).
 template <int CG, int NSUB, int EK, int MC = 0>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(nthreads(EK), 1)
 ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA128,
                  const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ CUtensorMap mapD, const __grid_constant__ CUtensorMap mapD2, TcArgs a) {
@@ -264,6 +266,7 @@ ffn_gemm_tcgen05(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     const int b_stage_bytes = B_BYTES_MAX / CG;
     constexpr int A_STAGE = NSUB * A_BYTES;                           // NSUB A tiles per stage
     unsigned char *sB = sA + STAGES * A_STAGE;
+    constexpr int EPI_WARPS = epi_warps(EK);
     unsigned char *sOut = sB + STAGES * b_stage_bytes;                // EPI_WARPS x nbox x 2 KB
     uint64_t *bars = reinterpret_cast<uint64_t *>(
         sOut + (a.tma_store ? nbox * EPI_WARPS * OUT_BOX_BYTES * (a.box64 ? 2 : 1) : 0));
@@ -746,9 +749,9 @@ int pick_bn(int N) {
     return 0;
 }
 
-size_t smem_bytes(int CG, int nsub, int stages, int nbox, int tma_store, int box64, int nseg) {
+size_t smem_bytes(int CG, int nsub, int stages, int nbox, int tma_store, int box64, int nseg, int ek) {
     return 1024 + stages * (nsub * A_BYTES + B_BYTES_MAX / CG) +
-           (tma_store ? nbox * EPI_WARPS * OUT_BOX_BYTES * (box64 ? 2 : 1) : 0) +
+           (tma_store ? nbox * epi_warps(ek) * OUT_BOX_BYTES * (box64 ? 2 : 1) : 0) +
            (2 * stages + 4) * 8 +
            16 + 32 * 4 + (nseg + 1) * 4 + nseg * 4;
 }
@@ -768,9 +771,9 @@ int pick_tma_store() {
     return v;
 }
 
-int pick_stages(int CG, int nsub, int nbox, int tma_store, int box64, int nseg) {
+int pick_stages(int CG, int nsub, int nbox, int tma_store, int box64, int nseg, int ek) {
     int st = 8;
-    while (st > 2 && smem_bytes(CG, nsub, st, nbox, tma_store, box64, nseg) > kSmemLimit) --st;
+    while (st > 2 && smem_bytes(CG, nsub, st, nbox, tma_store, box64, nseg, ek) > kSmemLimit) --st;
     return st;
 }
 
@@ -808,11 +811,11 @@ cudaError_t launch_tc(const CUtensorMap &mA, const CUtensorMap &mA128, const CUt
     }
     note_launch();
     if (CS == 1)
-        return launch_k(ffn_gemm_tcgen05<CG, NSUB, EK, MC>, dim3(grid), dim3(NTHREADS), smem, st, mA, mA128, mB, mD, mD2, a);
+        return launch_k(ffn_gemm_tcgen05<CG, NSUB, EK, MC>, dim3(grid), dim3(nthreads(EK)), smem, st, mA, mA128, mB, mD, mD2, a);
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(NTHREADS);
+    cfg.blockDim = dim3(nthreads(EK));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attrs[2];
@@ -864,7 +867,8 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
         const bool want = e ? (e[0] == '1' && gelu) || e[0] == '2' : false;     // 2: both GEMMs
         a.box64 = (want && a.tma_store && nbox == 1 && mode != EPI_DGELU && (BN / 32) % 8 == 0) ? 1 : 0;
     }
-    a.stages = pick_stages(CG, NSUB, nbox, a.tma_store, a.box64, a.nseg);
+    const int ek = mode == EPI_DGELU ? 2 : (mode == EPI_BIAS_SAVE ? 1 : 0);
+    a.stages = pick_stages(CG, NSUB, nbox, a.tma_store, a.box64, a.nseg, ek);
     if (const char *e = getenv("SMILE_FFN_STAGES")) {
         const int s = atoi(e);
         if (s >= 2 && s < a.stages) a.stages = s;
@@ -884,8 +888,7 @@ cudaError_t launch_gemm(const void *A, int64_t rows_total, const void *B, int NE
     }
     a.err = nullptr;
     a.trace = trace_buffer(mode == EPI_BIAS ? (gelu ? "ffn1" : "ffn2") : "ffn_bwd");
-    const size_t smem = smem_bytes(CG, NSUB, a.stages, nbox, a.tma_store, a.box64, a.nseg);
-    const int ek = mode == EPI_DGELU ? 2 : (mode == EPI_BIAS_SAVE ? 1 : 0);
+    const size_t smem = smem_bytes(CG, NSUB, a.stages, nbox, a.tma_store, a.box64, a.nseg, ek);
     if (a.box64) mD = mD64;                   // the output map with 32 x 64 SWIZZLE_128B boxes
 #define SMILE_LAUNCH_TC(cg, ns)                                                                    \
     return ek == 2 ? launch_tc<cg, ns, 2>(mA, mA128, mB, mD, mD2, a, smem, f.num_sms, st)          \
