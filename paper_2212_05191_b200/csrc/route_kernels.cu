@@ -162,12 +162,17 @@ __global__ void __launch_bounds__(256, 2) gate1_kernel(GateArgs a) {
 }
 
 // Level-1 scan over the per-chunk tables (gate_common.cuh scan1_rank), grid = V.
+// grid = V x nb: the rank's independent jobs (one scan / sum per destination or statistic,
+// a warp each) are spread over nb blocks, so a wide router's 100+ jobs run in one round
+// (C5: 132 jobs, 18 -> a few us).
 __global__ void scan1_kernel(Scan1Args a) {
     pdl_wait();
-    const int v = blockIdx.x;
-    if (a.lb_flag)                                   // the fused gate's look-back flags, for the next call
+    const int nb = gridDim.x / a.V;
+    const int v = blockIdx.x / nb, bi = blockIdx.x - v * nb;
+    if (a.lb_flag && bi == 0)                        // the fused gate's look-back flags, for the next call
         for (int b = threadIdx.x; b < a.nlb; b += blockDim.x) a.lb_flag[(int64_t)v * a.nlb + b] = 0;
-    scan1_rank(a, v, threadIdx.x >> 5, blockDim.x >> 5);
+    const int wpb = blockDim.x >> 5;
+    scan1_rank(a, v, bi * wpb + (threadIdx.x >> 5), nb * wpb);
 }
 
 // a6: level-2 gate at the intermediate: rank valid received slots per j, in received
@@ -780,8 +785,11 @@ void launch_gate1(const GateArgs &a, cudaStream_t st) {
 
 void launch_scan1(const Scan1Args &a, cudaStream_t st) {
     if (a.T == 0) return;
+    const int jobs = a.K1 + (a.K1 + a.K2) + a.K2;             // scan1_rank's jobs per rank
+    int nb = (jobs + 15) / 16;                               // 16 warps per block
+    if (nb > 16) nb = 16;
     note_launch();
-    launch_k(scan1_kernel, dim3(a.V), dim3(512), 0, st, a);
+    launch_k(scan1_kernel, dim3(a.V * nb), dim3(512), 0, st, a);
 }
 
 void launch_rank2(const Rank2Args &a, cudaStream_t st) {
