@@ -194,9 +194,12 @@ __global__ void rank2_kernel(Rank2Args a) {
         a.blk_hist2[((int64_t)v * a.nblk + blk) * a.K2 + k] = s_bh[k];
 }
 
+// grid = V x nb: a rank's K2 destination scans (a warp each) spread over nb blocks
 __global__ void scan2_kernel(Rank2Args a) {
     pdl_wait();
-    const int v = blockIdx.x, w = threadIdx.x >> 5, NW = blockDim.x >> 5, lane = threadIdx.x & 31;
+    const int nb = gridDim.x / a.V;
+    const int v = blockIdx.x / nb, bi = blockIdx.x - v * nb;
+    const int w = bi * (blockDim.x >> 5) + (threadIdx.x >> 5), NW = nb * (blockDim.x >> 5), lane = threadIdx.x & 31;
     for (int k = w; k < a.K2; k += NW) {
         const int64_t o = (int64_t)v * a.nblk * a.K2 + k;
         const int tot = warp_exclusive_scan(a.blk_hist2 + o, a.nblk, a.K2, a.blk_off2 + o);
@@ -212,19 +215,16 @@ __global__ void scan2_kernel(Rank2Args a) {
     }
 }
 
-// Row movers (a4, a7, a11, a13) on the TMA bulk-copy engine.  Per batch of R rows the
-// block's threads resolve each row's source / destination (and the slot bookkeeping);
-// one thread then moves the rows with cp.async.bulk (global -> shared, completion on an
-// mbarrier) and cp.async.bulk (shared -> global, bulk groups), double-buffered so the
-// loads of batch b+1 are in flight while batch b is stored.  Rows that must be zero, or
-// scaled by the gate (a13), are rewritten in shared memory by the threads in between.
+// Row movers (a4, a7, a11, a13): plan_row resolves each row's source / destination (and
+// the slot bookkeeping); row_move_body moves the rows warp by warp with 16-byte loads,
+// several rows' loads in flight per lane (see there).  A source of nullptr writes a zero
+// row (a dropped token, a13); a scale != 1 multiplies by the gate (a13).
 enum MoveKind { MOVE_DISPATCH1 = 0, MOVE_DISPATCH2 = 1, MOVE_COMBINE2 = 2, MOVE_COMBINE1 = 3, MOVE_GRAD2 = 4 };
 
 struct MoveArgs {
     int kind;
     int64_t rows;            // total rows (V * items)
     int64_t rowbytes;
-    int R;                   // rows per batch
     Dispatch1Args d1;
     Dispatch2Args d2;
     Combine2Args c2;
@@ -796,8 +796,10 @@ void launch_rank2(const Rank2Args &a, cudaStream_t st) {
     if (a.items == 0) return;
     note_launch();
     launch_k(rank2_kernel, dim3(a.nblk, a.V), dim3(kRank2Items), 0, st, a);
+    int nb = (a.K2 + 15) / 16;                               // 16 warps per block
+    if (nb > 16) nb = 16;
     note_launch();
-    launch_k(scan2_kernel, dim3(a.V), dim3(512), 0, st, a);
+    launch_k(scan2_kernel, dim3(a.V * nb), dim3(512), 0, st, a);
 }
 
 // Rows per warp batch: SMILE_MOVE_RW = 4 (default) or 8.
